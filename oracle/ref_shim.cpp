@@ -1,0 +1,265 @@
+// TEST INFRASTRUCTURE ONLY. Never linked into the product library.
+//
+// extern "C" shim over the UNMODIFIED reference core library (sbopt, compiled
+// from /root/reference/proj/core/src/*.cpp by oracle/Makefile into
+// oracle/_ref/). It exposes exactly the reference entry points the parity
+// tests and the bench's reference arm need, with plain pointers so Python can
+// call them through ctypes. Nothing here re-implements the algorithm: every
+// numeric result comes from the reference's own step()/run()/coupling_matvec()
+// /ising_energy()/batch_best_of()/auto_tune()/time_to_solution().
+//
+// Reference interfaces wrapped (paths relative to /root/reference/proj/core):
+//   step                 src/engine.cpp:55-110   (include/sbopt/engine.hpp:79-80)
+//   init_state           src/engine.cpp:25-39
+//   run                  src/engine.cpp:112-139
+//   coupling_matvec      src/kernels.hpp:33-46
+//   ising_energy         src/model.cpp:112-123
+//   gen_random_dense     src/model.cpp:144-159
+//   auto_tune (wigner)   src/spectral.cpp:294-326
+//   batch_best_of        src/bench.cpp:70-92
+//   success/TTS          src/bench.cpp:15-68
+//   ThreadPool           src/parallel.cpp:59-84
+
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "kernels.hpp"
+#include "sbopt/bench.hpp"
+#include "sbopt/engine.hpp"
+#include "sbopt/model.hpp"
+#include "sbopt/parallel.hpp"
+#include "sbopt/rng.hpp"
+#include "sbopt/spectral.hpp"
+
+using namespace sbopt;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const std::exception& e) {
+  g_err = e.what();
+  return 1;
+}
+
+Variant to_variant(int v) {
+  switch (v) {
+    case 0: return Variant::bsb;
+    case 1: return Variant::dsb;
+    default: return Variant::gbsb;
+  }
+}
+
+IsingInstance make_instance(std::int64_t n, const double* J) {
+  return IsingInstance(static_cast<std::size_t>(n),
+                       std::vector<double>(J, J + static_cast<std::size_t>(n * n)));
+}
+
+SolverConfig make_cfg(int variant, std::uint64_t steps, double dt, double c, double a,
+                      std::uint64_t seed) {
+  SolverConfig cfg;
+  cfg.variant = to_variant(variant);
+  cfg.steps = steps;
+  cfg.dt = dt;
+  cfg.c = c;
+  cfg.a = a;
+  cfg.seed = seed;
+  return cfg;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+std::uint64_t ref_derive_seed(std::uint64_t master, const std::uint64_t* keys, int nkeys) {
+  // derive_seed takes an initializer_list; fold the same way for 0..3 keys.
+  switch (nkeys) {
+    case 0: return derive_seed(master, {});
+    case 1: return derive_seed(master, {keys[0]});
+    case 2: return derive_seed(master, {keys[0], keys[1]});
+    default: return derive_seed(master, {keys[0], keys[1], keys[2]});
+  }
+}
+
+void ref_xoshiro_next(std::uint64_t seed, std::int64_t count, std::uint64_t* out) {
+  Xoshiro256pp rng(seed);
+  for (std::int64_t i = 0; i < count; ++i) out[i] = rng.next();
+}
+
+int ref_gen_random_dense(std::int64_t n, std::uint64_t seed, double* J_out) {
+  try {
+    const auto inst = gen_random_dense(static_cast<std::size_t>(n), seed);
+    for (std::int64_t i = 0; i < n; ++i) {
+      const auto row = inst.row(static_cast<std::size_t>(i));
+      std::memcpy(J_out + i * n, row.data(), sizeof(double) * static_cast<std::size_t>(n));
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int ref_init_state(std::int64_t n, std::uint64_t seed, int chaos_probe, double* x, double* y,
+                   double* p) {
+  try {
+    const auto s = init_state(static_cast<std::size_t>(n), seed,
+                              chaos_probe ? InitMode::chaos_probe : InitMode::uniform_random);
+    std::memcpy(x, s.x.data(), sizeof(double) * s.x.size());
+    std::memcpy(y, s.y.data(), sizeof(double) * s.y.size());
+    std::memcpy(p, s.p.data(), sizeof(double) * s.p.size());
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// Advances an injected state (x, y, p at step index m0) by nsteps calls of the
+// reference step(). BASELINE initial states are not producible by run()
+// (engine.cpp:25-39 always draws x ~ U(-1,1)), so the harness builds the
+// SolverState itself and replicates run()'s loop (engine.cpp:121-126).
+int ref_step_n(int variant, std::int64_t n, const double* J, double* x, double* y, double* p,
+               std::uint64_t m0, std::uint64_t steps, double dt, double c, double a,
+               std::uint64_t nsteps) {
+  try {
+    const auto inst = make_instance(n, J);
+    const auto cfg = make_cfg(variant, steps, dt, c, a, 0);
+    SolverState s;
+    s.x.assign(x, x + n);
+    s.y.assign(y, y + n);
+    s.p.assign(p, p + n);
+    s.m = m0;
+    for (std::uint64_t k = 0; k < nsteps; ++k) step(s, inst, cfg, nullptr);
+    std::memcpy(x, s.x.data(), sizeof(double) * static_cast<std::size_t>(n));
+    std::memcpy(y, s.y.data(), sizeof(double) * static_cast<std::size_t>(n));
+    std::memcpy(p, s.p.data(), sizeof(double) * static_cast<std::size_t>(n));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int ref_coupling_matvec(std::int64_t n, const double* J, const double* v, double* out) {
+  try {
+    const auto inst = make_instance(n, J);
+    detail::coupling_matvec(inst, v, out, nullptr);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int ref_ising_energy(std::int64_t n, const double* J, const std::int8_t* spins, double* energy) {
+  try {
+    const auto inst = make_instance(n, J);
+    *energy = ising_energy(inst, SpinConfig(std::vector<std::int8_t>(spins, spins + n)));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int ref_auto_tune_wigner(std::int64_t n, const double* J, double d_t, double* c, double* dt) {
+  try {
+    const auto t = auto_tune(make_instance(n, J), TuneMode::wigner, d_t);
+    *c = t.c;
+    *dt = t.dt;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// run() with the reference's own init (engine.cpp:112-139).
+int ref_run(int variant, std::int64_t n, const double* J, std::uint64_t steps, double dt,
+            double c, double a, std::uint64_t seed, std::int8_t* spins, double* energy,
+            double* x_final_unused) {
+  (void)x_final_unused;
+  try {
+    const auto inst = make_instance(n, J);
+    TuningResult t;
+    t.c = c;
+    t.dt = dt;
+    const auto r = run(inst, make_cfg(variant, steps, dt, c, a, seed), t, nullptr, nullptr);
+    std::memcpy(spins, r.final_spins.values().data(), static_cast<std::size_t>(n));
+    *energy = r.energy;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int ref_batch_best_of(int variant, std::int64_t n, const double* J, std::uint64_t steps, double dt,
+                      double c, double a, std::int64_t n_batch, std::uint64_t master,
+                      unsigned workers, std::int8_t* spins, double* energy,
+                      std::uint64_t* seed_out) {
+  try {
+    const auto inst = make_instance(n, J);
+    TuningResult t;
+    t.c = c;
+    t.dt = dt;
+    const auto r = batch_best_of(inst, make_cfg(variant, steps, dt, c, a, 0), t,
+                                 static_cast<std::size_t>(n_batch), master, workers, nullptr);
+    std::memcpy(spins, r.final_spins.values().data(), static_cast<std::size_t>(n));
+    *energy = r.energy;
+    *seed_out = r.config_echo.seed;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int ref_success_tts(std::int64_t hits, std::int64_t n_rep, double t_com, double* p_s,
+                    double* delta_p_s, double* tts, double* delta_tts) {
+  try {
+    const auto st = success_from_counts(static_cast<std::size_t>(hits),
+                                        static_cast<std::size_t>(n_rep), 0.0);
+    *p_s = st.p_s;
+    *delta_p_s = st.delta_p_s;
+    const auto tr = time_to_solution(t_com, st);
+    *tts = tr.tts_s;
+    *delta_tts = tr.delta_tts_s;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// The reference arm of the bench: cmd_bench's replica fan-out
+// (tools/sbopt.cpp:265-272) over injected initial states. R replicas are
+// distributed with ThreadPool::for_each_index; each replica runs `steps`
+// reference step() calls (pool = nullptr, as bench.cpp:81 does), then
+// signs_from_positions + ising_energy. x0/y0 are R x n fp32 (BASELINE init),
+// widened to fp64. Returns wall seconds of the whole fan-out.
+int ref_replica_fanout(int variant, std::int64_t n, const double* J, std::int64_t R,
+                       const float* x0, const float* y0, std::uint64_t steps, double dt, double c,
+                       double a, unsigned workers, double* energies, double* wall_s) {
+  try {
+    const auto inst = make_instance(n, J);
+    const auto cfg = make_cfg(variant, steps, dt, c, a, 0);
+    ThreadPool pool(workers);
+    const auto t0 = std::chrono::steady_clock::now();
+    pool.for_each_index(static_cast<std::size_t>(R), [&](std::size_t r) {
+      SolverState s;
+      s.x.assign(x0 + r * n, x0 + (r + 1) * n);
+      s.y.assign(y0 + r * n, y0 + (r + 1) * n);
+      s.p.assign(static_cast<std::size_t>(n), 1.0);
+      s.m = 0;
+      for (std::uint64_t m = 0; m < steps; ++m) step(s, inst, cfg, nullptr);
+      energies[r] = ising_energy(inst, signs_from_positions(s.x));
+    });
+    *wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+unsigned ref_effective_workers(unsigned requested) { return effective_workers(requested); }
+
+}  // extern "C"

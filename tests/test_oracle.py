@@ -1,0 +1,165 @@
+"""Pins the C restatement (oracle/sbg_oracle.c) to the reference.
+
+Against the committed golden vectors (outputs of the unmodified reference core,
+tests/golden/make_golden.py) everywhere, and against the live compiled
+reference (oracle/_ref) when it is present (the build container).
+Reference KATs restated from proj/tests/test_engine.cpp and test_bench.cpp.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+
+BSB, DSB, GBSB, GDSB = 0, 1, 2, 3
+
+
+def test_rng_matches_reference(golden, orc):
+    for s, words in zip(golden["xo_seed"], golden["xo_words"]):
+        assert (orc.xoshiro(int(s), 64) == words).all()
+    for mi, m in enumerate(golden["ds_master"]):
+        for ki, (keys, nk) in enumerate(zip(golden["ds_keys"], golden["ds_nkeys"])):
+            assert orc.derive_seed(int(m), [int(k) for k in keys[:nk]]) == int(golden["ds_out"][mi, ki])
+
+
+@pytest.mark.parametrize("n,seed", [(2, 1), (37, 11), (130, 1)])
+def test_dense_generator_matches_reference(golden, orc, n, seed):
+    assert (orc.gen_dense_i8(n, seed) == golden[f"J_n{n}_s{seed}"]).all()
+
+
+def test_row_sharded_generator(orc):
+    full = orc.gen_dense_i8(97, 3)
+    for row0, rows in [(0, 13), (13, 40), (90, 7)]:
+        assert (orc.gen_dense_i8_rows(97, 3, row0, rows) == full[row0:row0 + rows]).all()
+
+
+def test_matvec_lanes_bitwise(golden, orc):
+    J = golden["J_n37_s11"].astype(np.float64)
+    for v, out in zip(golden["mv_v_sign"], golden["mv_out_sign"]):
+        assert (orc.matvec_lanes_f64(J, v) == out).all()
+    for v, out in zip(golden["mv_v_real"], golden["mv_out_real"]):
+        assert (orc.matvec_lanes_f64(J, v) == out).all()  # same lane order, -ffp-contract=off
+
+
+def test_csr_lane_order_equals_dense(golden, orc):
+    """CSR with lane j%8 (tail -> lane 0) is bitwise the dense row_dot."""
+    for n in (37, 40, 1003):
+        rng = np.random.default_rng(n)
+        (ei, ej, w), (rowptr, col, val) = orc.gen_er_csr(n, 3 * n, 17 + n)
+        dense = np.zeros((n, n))
+        dense[ei, ej] = -w
+        dense[ej, ei] = -w
+        for _ in range(3):
+            v = rng.uniform(-1, 1, n)
+            assert (orc.csr_matvec_lanes_f64(n, rowptr, col, val.astype(np.float64), v)
+                    == orc.matvec_lanes_f64(dense, v)).all()
+
+
+def test_energy_matches_reference(golden, orc):
+    J = golden["J_n37_s11"]
+    x = golden["en_spins"].astype(np.float32)
+    e2 = orc.energy2_i8(J, x)
+    assert (-0.5 * e2 == golden["en_energy"]).all()
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+@pytest.mark.parametrize("variant", [BSB, DSB, GBSB])
+def test_step_f64_bitwise_reference_trajectory(golden, orc, seed, variant):
+    """orc_step_f64 == reference step() bitwise (both -ffp-contract=off) at checkpoints."""
+    J = golden["J_n37_s11"].astype(np.float64)
+    c, dt = float(golden["tune_c"]), float(golden["tune_dt"])
+    x = golden[f"init_ref_s{seed}_x"]
+    y, p = np.zeros_like(x), np.ones_like(x)
+    m = 0
+    for k, cp in enumerate(golden["traj_checkpoints"]):
+        x, y, p = orc.step_f64(variant, J, x, y, p, m, 200, dt, c, 0.2, int(cp) - m)
+        m = int(cp)
+        assert (x == golden[f"traj_ref_v{variant}_s{seed}_x"][k]).all()
+        assert (y == golden[f"traj_ref_v{variant}_s{seed}_y"][k]).all()
+        assert (p == golden[f"traj_ref_v{variant}_s{seed}_p"][k]).all()
+
+
+def test_gdsb_at_a0_is_reference_dsb(golden, orc):
+    """GdSB restatement pin: A=0 GdSB == reference dSB bitwise."""
+    J = golden["J_n37_s11"].astype(np.float64)
+    c, dt = float(golden["tune_c"]), float(golden["tune_dt"])
+    for seed in (1, 2):
+        x = golden[f"init_ref_s{seed}_x"]
+        y, p = np.zeros_like(x), np.ones_like(x)
+        # reference dsb ignores a (engine.cpp:64), GdSB with a = 0 must coincide.
+        gx, gy, gp = orc.step_f64(GDSB, J, x, y, p, 0, 200, dt, c, 0.0, 200)
+        dx, dy, dp = orc.step_f64(DSB, J, x, y, p, 0, 200, dt, c, 0.2, 200)
+        assert (gx == dx).all() and (gy == dy).all() and (gp == dp).all()
+
+
+def test_baseline_init_matches_reference_rng(golden, orc):
+    x, y, p = orc.init_small_uniform(37, 2, master=9, tag=7)
+    for r in (0, 1):
+        assert (x[r].astype(np.float64) == golden[f"init_small_r{r}_x"]).all()
+        assert (y[r].astype(np.float64) == golden[f"init_small_r{r}_y"]).all()
+    assert (p == 1.0).all()
+
+
+@pytest.mark.parametrize("variant", [BSB, DSB, GBSB])
+def test_fp32_mirror_tracks_fp64_reference(golden, orc, variant):
+    """Protocol P3: fp32 (GPU op order) vs fp64 reference, <= 1e-5 relative at 30 steps."""
+    J8 = golden["J_n37_s11"]
+    c, dt = float(golden["tune_c"]), float(golden["tune_dt"])
+    x0 = np.stack([golden[f"init_small_r{r}_x"] for r in (0, 1)]).astype(np.float32)
+    y0 = np.stack([golden[f"init_small_r{r}_y"] for r in (0, 1)]).astype(np.float32)
+    p0 = np.ones_like(x0)
+    x, y, p = orc.step_f32(variant, J8, x0, y0, p0, 0, 200, np.float32(dt), np.float32(c), np.float32(0.2), 30)
+    for r in (0, 1):
+        ref_x = golden[f"traj_small_v{variant}_r{r}_x30"]
+        err = np.abs(x[r] - ref_x).max() / np.abs(ref_x).max()
+        assert err <= 1e-5, err
+
+
+def test_batch_best_of_rule(golden, orc):
+    for v in (0, 1, 2):
+        e = golden[f"bbo_v{v}_replica_energies"]
+        best = orc.argmin((2 * e).astype(np.int64))  # 2E is an exact integer for +-1 J
+        assert e[best] == float(golden[f"bbo_v{v}_energy"])
+        assert best == int(np.flatnonzero(e == e.min())[0])
+
+
+def test_tts_kats(golden, orc):
+    for (h, nr, t), out in zip(golden["tts_in"], golden["tts_out"]):
+        got = orc.success_tts(int(h), int(nr), float(t))
+        assert np.allclose(got, out, rtol=0, atol=0)
+    # test_bench.cpp:89-120 known answers
+    p, dp, tts, dtts = orc.success_tts(500, 1000, 1.0)
+    assert abs(tts - 6.6439) / 6.6439 < 1e-4 and abs(dtts - 0.3031) / 0.3031 < 1e-3
+    assert orc.success_tts(999, 1000, 0.010)[2] == 0.010
+    assert abs(orc.success_tts(9, 10, 1.0)[2] - 2.0) <= 1e-12
+    with pytest.raises(ValueError):
+        orc.success_tts(0, 10, 1.0)
+
+
+def test_phase_kats(orc):
+    """test_engine.cpp:69-122 KATs restated on the fp32 phase."""
+    # single-oscillator step by hand (:80-93): M=1, m=0 -> p=0, y=0, x=0.5
+    x, y, p = orc.step_f32(GBSB, np.zeros((1, 1), np.int8), np.array([[0.5]], np.float32),
+                           np.zeros((1, 1), np.float32), np.ones((1, 1), np.float32), 0, 1,
+                           np.float32(1.0), np.float32(1.0), np.float32(0.0))
+    assert (p[0, 0], y[0, 0], x[0, 0]) == (0.0, 0.0, 0.5)
+    # wall (:95-122)
+    for x0, y0, want in [(0.9, 2.0, 1.0), (-0.9, -2.0, -1.0)]:
+        x, y, p = orc.step_f32(GBSB, np.zeros((1, 1), np.int8), np.array([[x0]], np.float32),
+                               np.array([[y0]], np.float32), np.ones((1, 1), np.float32), 0, 1000,
+                               np.float32(0.1), np.float32(1.0), np.float32(0.0))
+        assert x[0, 0] == want and y[0, 0] == 0.0
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built (no /root/reference)")
+def test_live_reference_agrees_with_restatement(orc):
+    R = oracle.ref()
+    J = R.gen_random_dense(53, 4)
+    x, y, p = R.init_state(53, 5)
+    c, dt = R.auto_tune_wigner(J)
+    assert math.isclose(c, 1 / (2 * math.sqrt(53))) and dt == 1.25
+    for v in (0, 1, 2):
+        a = R.step_n(v, J, x, y, p, 0, 100, dt, c, 0.25, 100)
+        b = orc.step_f64(v, J, x, y, p, 0, 100, dt, c, 0.25, 100)
+        assert all((u == w).all() for u, w in zip(a, b))
