@@ -1,0 +1,154 @@
+/* sbgpu — B200-native generalized simulated bifurcation (GSB), C ABI.
+ *
+ * This is the drop-in boundary for the reference's per-step hot path.
+ * The reference (arxiv/paper_2508_17655, `sbopt`, /root/reference/proj/core)
+ * exposes that path only as a C++ library with no FFI; each entry point below
+ * names the reference interface it replaces (file:line relative to
+ * /root/reference/proj/core). Plain pointers and sizes only; nothing throws
+ * across this ABI: every call returns an SBG_* code and the message is kept in
+ * sbg_last_error(ctx). The C++ wrapper include/sbgpu.hpp maps the codes back
+ * to the reference's exception types (std::invalid_argument for argument
+ * errors, engine.cpp:16-21/:57-60; std::runtime_error otherwise).
+ *
+ * Layouts: couplings J are dense row-major n x n (or CSR); replica states are
+ * replica-major R x n (replica r's vector contiguous), fp32 on the device.
+ * The caller owns all host arrays; no caller pointer is retained after a call.
+ * A context is single-threaded and bound to one CUDA device.
+ */
+#ifndef SBGPU_H
+#define SBGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SBG_ABI_VERSION 1
+
+/* return codes */
+#define SBG_OK 0
+#define SBG_ERR_INVALID_ARGUMENT 1 /* maps to std::invalid_argument */
+#define SBG_ERR_OUT_OF_MEMORY 2
+#define SBG_ERR_CUDA 3
+#define SBG_ERR_NCCL 4
+#define SBG_ERR_STATE 5 /* call order: no couplings / no state yet */
+#define SBG_ERR_UNSUPPORTED 6
+
+/* Variant (engine.hpp:26 `enum class Variant { bsb, dsb, gbsb }`, plus GdSB:
+ * sign-discretised field with per-spin nonlinear control). */
+#define SBG_BSB 0
+#define SBG_DSB 1
+#define SBG_GBSB 2
+#define SBG_GDSB 3
+
+/* Initial-state generators (device side, bit-exact with the oracle).
+ * UNIFORM_RANDOM / CHAOS_PROBE: init_state, engine.cpp:25-39 (x ~ U(-1,1) or
+ * +-0.1; y = 0; p = 1), rounded to fp32; replica r seeded
+ * derive_seed(master, {tag, offset + r}) (rng.hpp:26-31; batch_best_of uses
+ * tag 3, bench.cpp:80). SMALL_UNIFORM: the BASELINE configs' x, y ~ U(-0.1,0.1)
+ * (x drawn first, then y, each 0.1*uniform_symmetric() rounded to fp32), p = 1. */
+#define SBG_INIT_UNIFORM_RANDOM 0
+#define SBG_INIT_CHAOS_PROBE 1
+#define SBG_INIT_SMALL_UNIFORM 2
+
+typedef struct sbg_ctx sbg_ctx;
+
+/* SolverConfig (engine.hpp:29-38) after resolve_config (engine.cpp:48-53):
+ * dt and c already resolved. steps = M. a = A (ignored for bsb/dsb, :64). */
+typedef struct sbg_params {
+  int32_t variant;
+  int32_t reserved;
+  uint64_t steps;
+  double dt;
+  double c;
+  double a;
+} sbg_params;
+
+/* Device-measured phases of the last sbg_run* call (CUDA events). */
+typedef struct sbg_timing {
+  double h2d_ms;
+  double init_ms;
+  double steps_ms;
+  double readout_ms;
+  double d2h_ms;
+  double total_ms;
+  int64_t kernel_launches;
+} sbg_timing;
+
+int sbg_abi_version(void);
+const char* sbg_strerror(int code);
+
+/* Context on one CUDA device. Replaces the per-call ThreadPool/scratch of the
+ * reference (parallel.hpp:18-50, engine.cpp:67-68). */
+int sbg_create(int device, sbg_ctx** out);
+void sbg_destroy(sbg_ctx* ctx);
+const char* sbg_last_error(const sbg_ctx* ctx);
+int sbg_device_sm_count(const sbg_ctx* ctx);
+
+/* Couplings. Replace IsingInstance (model.hpp:46-70; invariants model.cpp:54-68:
+ * symmetric, zero diagonal). Dense integer J is kept as int8 on the device. */
+int sbg_set_couplings_dense_i8(sbg_ctx* ctx, int64_t n, const int8_t* J);
+/* fp64 J as IsingInstance stores it; must be integral in [-127, 127]. */
+int sbg_set_couplings_dense_f64(sbg_ctx* ctx, int64_t n, const double* J);
+/* gen_random_dense (model.cpp:144-159) evaluated on the host into int8. */
+int sbg_gen_couplings_dense_pm1(sbg_ctx* ctx, int64_t n, uint64_t seed);
+/* CSR (both triangles, ascending columns), int8 values: the sparse view of
+ * the same IsingInstance. */
+int sbg_set_couplings_csr_i8(sbg_ctx* ctx, int64_t n, int64_t nnz, const int32_t* rowptr,
+                             const int32_t* col, const int8_t* val);
+int64_t sbg_n(const sbg_ctx* ctx);
+
+/* Replica states. Replace SolverState (engine.hpp:40-47) x R.
+ * sbg_set_state: host x, y, p (p may be NULL -> 1), each R x n, step index m = 0. */
+int sbg_set_state(sbg_ctx* ctx, int64_t R, const float* x, const float* y, const float* p);
+/* Device-side init_state (see SBG_INIT_*), replicas offset .. offset+R-1. */
+int sbg_init_state(sbg_ctx* ctx, int64_t R, int32_t mode, uint64_t master, uint64_t tag,
+                   int64_t replica_offset);
+int sbg_get_state(sbg_ctx* ctx, float* x, float* y, float* p);
+
+/* step() (engine.cpp:55-110) for every replica, m = m_begin .. m_end-1 of an
+ * M-step run (params->steps = M). Validation as validate()/step()
+ * (engine.cpp:16-21, :57-60). Asynchronous; see sbg_synchronize. */
+int sbg_advance(sbg_ctx* ctx, const sbg_params* params, uint64_t m_begin, uint64_t m_end);
+
+/* Readout: signs_from_positions (model.cpp:161-165) + ising_energy
+ * (model.cpp:112-123) per replica + batch_best_of's winner rule (bench.cpp:84-87,
+ * min energy, ties to the lowest index). Any output may be NULL.
+ * spins: R x n int8; energy: R doubles; best_index/best_energy: scalars. */
+int sbg_readout(sbg_ctx* ctx, int8_t* spins, double* energy, int64_t* best_index, double* best_energy);
+
+/* Teacher-forced fields for parity (coupling_matvec, kernels.hpp:33-46):
+ * F = J * S for S (R x n, entries +-1) -> int32 R x n, bit-exact; and the
+ * fixed-point field the continuous variants use for x (R x n fp32). */
+int sbg_fields_sign(sbg_ctx* ctx, int64_t R, const int8_t* S, int32_t* F);
+int sbg_fields_fixed(sbg_ctx* ctx, int64_t R, const float* x, float* F);
+
+/* run() (engine.cpp:112-139) batched over R replicas from host initial states:
+ * H2D, M steps, readout, D2H, all inside the call. Outputs may be NULL. */
+int sbg_run(sbg_ctx* ctx, const sbg_params* params, int64_t R, const float* x0, const float* y0,
+            float* x_final, int8_t* spins, double* energy, int64_t* best_index, sbg_timing* timing);
+/* Same with device-generated initial states (sbg_init_state). */
+int sbg_run_seeded(sbg_ctx* ctx, const sbg_params* params, int64_t R, int32_t init_mode,
+                   uint64_t master, uint64_t tag, int64_t replica_offset, int8_t* spins,
+                   double* energy, int64_t* best_index, sbg_timing* timing);
+
+int sbg_synchronize(sbg_ctx* ctx);
+/* Kernel launches issued by this context since creation (bench evidence). */
+int64_t sbg_kernel_launches(const sbg_ctx* ctx);
+/* Raw device pointers of the resident state (fp32, leading dimension ld). */
+int sbg_state_device(sbg_ctx* ctx, float** x, float** y, float** p, int64_t* ld, int64_t* rpad);
+/* Device-time of the most recent sbg_advance, ms (CUDA events on the ctx stream). */
+double sbg_last_advance_ms(const sbg_ctx* ctx);
+
+/* Statistics, bench.cpp:15-68 (success_from_counts + time_to_solution).
+ * out = {p_s, delta_p_s, tts, delta_tts}. INVALID_ARGUMENT as the reference throws. */
+int sbg_success_tts(int64_t hits, int64_t n_rep, double t_com_s, double* out4);
+/* auto_tune, Wigner branch (spectral.cpp:298-305, :254-266, :277-286) on dense
+ * fp64 J: c = 1/(2 sqrt(n) sigma), dt = d_t * sqrt(2 / (1 - lmin/lmax)) = d_t. */
+int sbg_tune_wigner_f64(int64_t n, const double* J, double d_t, double* c, double* dt);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SBGPU_H */

@@ -1,0 +1,9 @@
+"""paper_2508_17655_b200 — B200-native generalized simulated bifurcation (GbSB/GdSB).
+
+The hot path (the per-step GSB loop of sbopt::step, batched over replicas)
+runs in hand-written sm_100a kernels behind the C ABI in include/sbgpu.h;
+this package is the host-side mirror of the reference solver API.
+"""
+from .solver import (BatchResult, InitMode, RunResult, Solver, SolverConfig, SuccessStats,  # noqa: F401
+                     TtsResult, TuningResult, Variant, auto_tune_wigner, resolve_config,
+                     success_from_counts, success_probability, success_probability_cut, time_to_solution)

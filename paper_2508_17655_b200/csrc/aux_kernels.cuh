@@ -1,0 +1,200 @@
+// Small elementwise / reduction kernels around the tensor-core step:
+// device init_state (xoshiro256++), B-operand preparation (sign plane or
+// fixed-point byte planes), the best-replica argmin, fills.
+#pragma once
+
+#include <cstdint>
+
+#include "gsb_phase.cuh"
+
+namespace sbg {
+
+// ---------------------------------------------------------------- rng.hpp
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // rng.hpp:17-21
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__host__ __device__ __forceinline__ uint64_t derive_seed2(uint64_t master, uint64_t k0, uint64_t k1) {
+  uint64_t h = mix64(master + 0x9E3779B97F4A7C15ULL);  // rng.hpp:26-31 with two keys
+  h = mix64(h ^ (k0 + 0x9E3779B97F4A7C15ULL));
+  h = mix64(h ^ (k1 + 0x9E3779B97F4A7C15ULL));
+  return h;
+}
+
+struct Xoshiro {  // rng.hpp:44-77
+  uint64_t s0, s1, s2, s3;
+  __host__ __device__ explicit Xoshiro(uint64_t seed) {
+    uint64_t z = seed;
+    z += 0x9E3779B97F4A7C15ULL;
+    s0 = mix64(z);
+    z += 0x9E3779B97F4A7C15ULL;
+    s1 = mix64(z);
+    z += 0x9E3779B97F4A7C15ULL;
+    s2 = mix64(z);
+    z += 0x9E3779B97F4A7C15ULL;
+    s3 = mix64(z);
+  }
+  __host__ __device__ __forceinline__ static uint64_t rotl(uint64_t x, int k) {
+    return (x << k) | (x >> (64 - k));
+  }
+  __host__ __device__ __forceinline__ uint64_t next() {
+    const uint64_t result = rotl(s0 + s3, 23) + s0;
+    const uint64_t t = s1 << 17;
+    s2 ^= s0;
+    s3 ^= s1;
+    s1 ^= s2;
+    s0 ^= s3;
+    s2 ^= t;
+    s3 = rotl(s3, 45);
+    return result;
+  }
+  __host__ __device__ __forceinline__ double uniform01() {
+    return static_cast<double>(next() >> 11) * 0x1.0p-53;
+  }
+  __host__ __device__ __forceinline__ double uniform_symmetric() { return 2.0 * uniform01() - 1.0; }
+  __host__ __device__ __forceinline__ double random_sign() { return (next() >> 63) ? -1.0 : 1.0; }
+};
+
+// Device init_state. One thread per replica runs the serial xoshiro stream;
+// values are staged through shared memory 32 spins at a time so the block
+// writes whole 128-byte lines of the replica-major state.
+// mode: 0 uniform_random, 1 chaos_probe (engine.cpp:25-39), 2 small_uniform.
+constexpr int INIT_THREADS = 64;
+
+__global__ void __launch_bounds__(INIT_THREADS)
+    init_state_kernel(float* __restrict__ x, float* __restrict__ y, float* __restrict__ p, int32_t n,
+                      int64_t ld, int32_t R, int32_t mode, uint64_t master, uint64_t tag,
+                      int64_t offset) {
+  __shared__ float tile[INIT_THREADS][33];
+  const int r0 = blockIdx.x * INIT_THREADS;
+  const int r = r0 + threadIdx.x;
+  Xoshiro g(derive_seed2(master, tag, static_cast<uint64_t>(offset + r)));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = INIT_THREADS / 32;
+  for (int pass = 0; pass < 2; ++pass) {  // pass 0: x, pass 1: y
+    float* dst = pass == 0 ? x : y;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int cnt = min(32, n - i0);
+#pragma unroll 4
+      for (int k = 0; k < 32; ++k) {
+        float v = 0.0f;
+        if (k < cnt && r < R) {
+          if (pass == 0) {
+            if (mode == 1)
+              v = static_cast<float>(0.1 * g.random_sign());
+            else if (mode == 2)
+              v = static_cast<float>(0.1 * g.uniform_symmetric());
+            else
+              v = static_cast<float>(g.uniform_symmetric());
+          } else if (mode == 2) {
+            v = static_cast<float>(0.1 * g.uniform_symmetric());
+          }
+        }
+        tile[threadIdx.x][k] = v;
+      }
+      __syncthreads();
+      for (int t = warp; t < INIT_THREADS; t += nwarps) {
+        if (r0 + t < R && lane < cnt) dst[static_cast<size_t>(r0 + t) * ld + i0 + lane] = tile[t][lane];
+      }
+      __syncthreads();
+    }
+  }
+  // p = 1 (coalesced by the same row walk)
+  for (int t = warp; t < INIT_THREADS; t += nwarps) {
+    if (r0 + t >= R) break;
+    for (int i = lane; i < n; i += 32) p[static_cast<size_t>(r0 + t) * ld + i] = 1.0f;
+  }
+}
+
+// Build the MMA B operand of the current state: nplanes == 1 -> sign plane
+// (+-1, padding 0); nplanes == 4 -> byte planes of q = rint(x * 2^30).
+__global__ void prep_planes_kernel(const float* __restrict__ x, uint8_t* __restrict__ G, int32_t n,
+                                   int32_t npad, int64_t ld, int32_t R, int32_t rpad, int32_t nplanes) {
+  const size_t total = static_cast<size_t>(rpad) * npad;
+  const size_t plane_stride = total;
+  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(idx / npad);
+    const int i = static_cast<int>(idx % npad);
+    const bool ok = r < R && i < n;
+    const float v = ok ? x[static_cast<size_t>(r) * ld + i] : 0.0f;
+    if (nplanes == 1) {
+      G[idx] = ok ? static_cast<uint8_t>(sgn8(v)) : 0;
+    } else {
+      const uint32_t q = static_cast<uint32_t>(quant30(v));
+      for (int pl = 0; pl < nplanes; ++pl) G[pl * plane_stride + idx] = static_cast<uint8_t>(q >> (8 * pl));
+    }
+  }
+}
+
+// Upload helper: a host sign matrix S (R x n, +-1) into a padded plane.
+__global__ void pad_plane_kernel(const int8_t* __restrict__ S, uint8_t* __restrict__ G, int32_t n,
+                                 int32_t npad, int32_t R, int32_t rpad) {
+  const size_t total = static_cast<size_t>(rpad) * npad;
+  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(idx / npad);
+    const int i = static_cast<int>(idx % npad);
+    G[idx] = (r < R && i < n) ? static_cast<uint8_t>(S[static_cast<size_t>(r) * n + i]) : 0;
+  }
+}
+
+__global__ void fill_f32_kernel(float* __restrict__ a, size_t count, float v) {
+  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < count;
+       idx += static_cast<size_t>(gridDim.x) * blockDim.x)
+    a[idx] = v;
+}
+
+// batch_best_of winner (bench.cpp:84-87): energy = -E2/2, min energy
+// == max E2, ties to the lowest replica index. One block.
+__global__ void __launch_bounds__(1024) argmin_energy_kernel(const long long* __restrict__ e2, int32_t R,
+                                                             long long* __restrict__ out /*[idx, e2]*/) {
+  long long best = LLONG_MIN;
+  int idx = 0x7fffffff;
+  for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    const long long v = e2[r];
+    if (v > best || (v == best && r < idx)) {
+      best = v;
+      idx = r;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ob > best || (ob == best && oi < idx)) {
+      best = ob;
+      idx = oi;
+    }
+  }
+  __shared__ long long sb[32];
+  __shared__ int si[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sb[warp] = best;
+    si[warp] = idx;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    best = lane < nw ? sb[lane] : LLONG_MIN;
+    idx = lane < nw ? si[lane] : 0x7fffffff;
+    for (int o = 16; o > 0; o >>= 1) {
+      const long long ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (ob > best || (ob == best && oi < idx)) {
+        best = ob;
+        idx = oi;
+      }
+    }
+    if (lane == 0) {
+      out[0] = idx;
+      out[1] = best;
+    }
+  }
+}
+
+__global__ void advance_counter_kernel(uint64_t* m, uint64_t by) { *m += by; }
+
+}  // namespace sbg

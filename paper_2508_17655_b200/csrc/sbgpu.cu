@@ -1,0 +1,725 @@
+// sbgpu context and C ABI (include/sbgpu.h).
+//
+// Owns the device copies of J, the replica states, the B-operand planes and
+// the TMA descriptors; drives the per-step tensor-core kernel (step_i8.cuh)
+// M times, then the readout. Replaces, for this path, sbopt::run's loop
+// (/root/reference/proj/core/src/engine.cpp:112-139) fanned out over replicas
+// by the reference's ThreadPool (bench.cpp:70-92, parallel.cpp:59-84).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sbgpu.h"
+#include "aux_kernels.cuh"
+#include "csr_step.cuh"
+#include "step_i8.cuh"
+
+using namespace sbg;
+
+namespace {
+
+constexpr int BN_SIGN = 128;   // replica tile, sign variants (dsb/gdsb)
+constexpr int BN_PLANE = 64;   // replica tile, fixed-point variants (bsb/gbsb)
+constexpr int NPL = 4;         // fixed-point byte planes
+constexpr int PAD_N = 128;     // spin padding (MMA M and K granularity)
+constexpr int PAD_R = 128;     // replica padding (multiple of both BNs)
+
+enum Kind { KIND_NONE = 0, KIND_DENSE_I8 = 1, KIND_CSR_I8 = 2 };
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool is_sign_variant(int v) { return v == SBG_DSB || v == SBG_GDSB; }
+
+}  // namespace
+
+struct sbg_ctx {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  // couplings
+  int kind = KIND_NONE;
+  int64_t n = 0, npad = 0;
+  int8_t* dJ = nullptr;
+  CUtensorMap tmJ;
+  int32_t* d_rowptr = nullptr;
+  int32_t* d_col = nullptr;
+  int8_t* d_val = nullptr;
+  int64_t nnz = 0;
+  // replica state
+  int64_t R = 0, rpad = 0, cap_rpad = 0;
+  float *dX = nullptr, *dY = nullptr, *dP = nullptr;
+  uint8_t* dG[2] = {nullptr, nullptr};  // B-operand buffers, NPL planes each
+  uint8_t* dSign = nullptr;             // readout sign plane
+  unsigned long long* dE2 = nullptr;
+  long long* dBest = nullptr;
+  CUtensorMap tmG_sign[2], tmG_planes[2], tmSign;
+  int g_cur = 0;
+  int g_mode = 0;  // 0 stale, 1 sign plane valid in dG[g_cur], 4 planes valid
+  cudaEvent_t ev[8];
+  float last_advance_ms = 0.f;
+
+  int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    err = buf;
+    return code;
+  }
+};
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return ctx->fail(e_ == cudaErrorMemoryAllocation ? SBG_ERR_OUT_OF_MEMORY : SBG_ERR_CUDA, \
+                       "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+#define CHECK_CTX(ctx) \
+  if (!(ctx)) return SBG_ERR_INVALID_ARGUMENT
+
+namespace {
+
+int encode_2d_u8(sbg_ctx* ctx, CUtensorMap* tm, const void* base, uint64_t inner, uint64_t rows,
+                 uint32_t box_inner, uint32_t box_rows) {
+  auto enc = get_encode();
+  if (!enc) return ctx->fail(SBG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {inner};
+  cuuint32_t box[2] = {box_inner, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return ctx->fail(SBG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  return SBG_OK;
+}
+
+int grid_for(const sbg_ctx* ctx, size_t work, int threads) {
+  const size_t blocks = (work + threads - 1) / threads;
+  return static_cast<int>(std::min<size_t>(std::max<size_t>(blocks, 1), size_t(ctx->sms) * 8));
+}
+
+template <int NP, int BN, EpiMode MODE>
+int launch_step(sbg_ctx* ctx, const CUtensorMap& tmG, const StepArgs& a) {
+  using Cfg = StepCfg<NP, BN>;
+  auto kern = gsb_step_i8_kernel<NP, BN, MODE>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  const int tiles = a.num_m * a.num_n;
+  const int grid = std::min(tiles, ctx->sms);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(ctx->tmJ, tmG, a);
+  CK(cudaGetLastError());
+  ++ctx->launches;
+  return SBG_OK;
+}
+
+void free_state(sbg_ctx* ctx) {
+  cudaFree(ctx->dX);
+  cudaFree(ctx->dY);
+  cudaFree(ctx->dP);
+  cudaFree(ctx->dG[0]);
+  cudaFree(ctx->dG[1]);
+  cudaFree(ctx->dSign);
+  cudaFree(ctx->dE2);
+  cudaFree(ctx->dBest);
+  ctx->dX = ctx->dY = ctx->dP = nullptr;
+  ctx->dG[0] = ctx->dG[1] = ctx->dSign = nullptr;
+  ctx->dE2 = nullptr;
+  ctx->dBest = nullptr;
+  ctx->cap_rpad = 0;
+}
+
+// (Re)allocate the replica state for R replicas of the current instance.
+int ensure_state(sbg_ctx* ctx, int64_t R) {
+  if (ctx->kind == KIND_NONE) return ctx->fail(SBG_ERR_STATE, "couplings not set");
+  if (R < 1) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "replica count must be >= 1");
+  const int64_t rpad = round_up(R, PAD_R);
+  if (rpad > (int64_t(1) << 30) / 4) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "too many replicas");
+  if (rpad != ctx->cap_rpad) {
+    free_state(ctx);
+    const size_t st = sizeof(float) * size_t(rpad) * ctx->npad;
+    const size_t pl = size_t(rpad) * ctx->npad;
+    CK(cudaMalloc(&ctx->dX, st));
+    CK(cudaMalloc(&ctx->dY, st));
+    CK(cudaMalloc(&ctx->dP, st));
+    CK(cudaMalloc(&ctx->dG[0], NPL * pl));
+    CK(cudaMalloc(&ctx->dG[1], NPL * pl));
+    CK(cudaMalloc(&ctx->dSign, pl));
+    CK(cudaMalloc(&ctx->dE2, sizeof(unsigned long long) * rpad));
+    CK(cudaMalloc(&ctx->dBest, 2 * sizeof(long long)));
+    CK(cudaMemsetAsync(ctx->dG[0], 0, NPL * pl, ctx->stream));
+    CK(cudaMemsetAsync(ctx->dG[1], 0, NPL * pl, ctx->stream));
+    CK(cudaMemsetAsync(ctx->dSign, 0, pl, ctx->stream));
+    ctx->cap_rpad = rpad;
+    if (ctx->kind == KIND_DENSE_I8) {
+      for (int b = 0; b < 2; ++b) {
+        int rc = encode_2d_u8(ctx, &ctx->tmG_sign[b], ctx->dG[b], ctx->npad, rpad, 128, BN_SIGN);
+        if (rc) return rc;
+        rc = encode_2d_u8(ctx, &ctx->tmG_planes[b], ctx->dG[b], ctx->npad, NPL * rpad, 128, BN_PLANE);
+        if (rc) return rc;
+      }
+      int rc = encode_2d_u8(ctx, &ctx->tmSign, ctx->dSign, ctx->npad, rpad, 128, BN_SIGN);
+      if (rc) return rc;
+    }
+  }
+  ctx->R = R;
+  ctx->rpad = rpad;
+  ctx->g_mode = 0;
+  const size_t st = sizeof(float) * size_t(rpad) * ctx->npad;
+  CK(cudaMemsetAsync(ctx->dX, 0, st, ctx->stream));
+  CK(cudaMemsetAsync(ctx->dY, 0, st, ctx->stream));
+  CK(cudaMemsetAsync(ctx->dP, 0, st, ctx->stream));
+  return SBG_OK;
+}
+
+int prep_planes(sbg_ctx* ctx, const float* x, uint8_t* G, int nplanes, int64_t R, int64_t rpad) {
+  const size_t total = size_t(rpad) * ctx->npad;
+  prep_planes_kernel<<<grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(
+      x, G, int32_t(ctx->n), int32_t(ctx->npad), ctx->npad, int32_t(R), int32_t(rpad), nplanes);
+  CK(cudaGetLastError());
+  ++ctx->launches;
+  return SBG_OK;
+}
+
+StepArgs base_args(const sbg_ctx* ctx, int BN, int64_t R, int64_t rpad) {
+  StepArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.n = int32_t(ctx->n);
+  a.npad = int32_t(ctx->npad);
+  a.R = int32_t(R);
+  a.rpad = int32_t(rpad);
+  a.num_m = int32_t(ctx->npad / 128);
+  a.num_n = int32_t(rpad / BN);
+  a.ld = ctx->npad;
+  return a;
+}
+
+int validate_params(sbg_ctx* ctx, const sbg_params* p) {
+  // validate() engine.cpp:16-21 (dt/c are resolved here, so both must be > 0)
+  if (!p) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "params is null");
+  if (p->variant < SBG_BSB || p->variant > SBG_GDSB) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "unknown variant");
+  if (p->steps < 1) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "step count M must be >= 1");
+  if (!(p->dt > 0.0)) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "dt must be positive");
+  if (!(p->c > 0.0)) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "c must be positive");
+  if (!(p->a >= 0.0)) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "A must be >= 0");
+  if (p->steps >= (uint64_t(1) << 24))
+    return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "M must be < 2^24 (fp32 step denominator)");
+  return SBG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sbg_abi_version(void) { return SBG_ABI_VERSION; }
+
+const char* sbg_strerror(int code) {
+  switch (code) {
+    case SBG_OK: return "ok";
+    case SBG_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case SBG_ERR_OUT_OF_MEMORY: return "out of device memory";
+    case SBG_ERR_CUDA: return "CUDA error";
+    case SBG_ERR_NCCL: return "NCCL error";
+    case SBG_ERR_STATE: return "invalid call order";
+    case SBG_ERR_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown";
+}
+
+int sbg_create(int device, sbg_ctx** out) {
+  if (!out) return SBG_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return SBG_ERR_CUDA;
+  if (device < 0 || device >= count) return SBG_ERR_INVALID_ARGUMENT;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return SBG_ERR_CUDA;
+  if (prop.major != 10) return SBG_ERR_UNSUPPORTED;  // sm_100a only
+  if (cudaSetDevice(device) != cudaSuccess) return SBG_ERR_CUDA;
+  auto* ctx = new sbg_ctx();
+  ctx->device = device;
+  ctx->sms = prop.multiProcessorCount;
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return SBG_ERR_CUDA;
+  }
+  for (auto& e : ctx->ev) cudaEventCreate(&e);
+  *out = ctx;
+  return SBG_OK;
+}
+
+void sbg_destroy(sbg_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  free_state(ctx);
+  cudaFree(ctx->dJ);
+  cudaFree(ctx->d_rowptr);
+  cudaFree(ctx->d_col);
+  cudaFree(ctx->d_val);
+  for (auto& e : ctx->ev) cudaEventDestroy(e);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* sbg_last_error(const sbg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+int sbg_device_sm_count(const sbg_ctx* ctx) { return ctx ? ctx->sms : 0; }
+int64_t sbg_n(const sbg_ctx* ctx) { return ctx ? ctx->n : 0; }
+int64_t sbg_kernel_launches(const sbg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int sbg_set_couplings_dense_i8(sbg_ctx* ctx, int64_t n, const int8_t* J) {
+  CHECK_CTX(ctx);
+  if (n < 1 || !J) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "instance size must be >= 1");
+  // IsingInstance invariants (model.cpp:54-68)
+  for (int64_t i = 0; i < n; ++i) {
+    if (J[i * n + i] != 0) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "coupling diagonal must be zero");
+    for (int64_t j = i + 1; j < n; ++j)
+      if (J[i * n + j] != J[j * n + i])
+        return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "coupling matrix must be symmetric");
+    for (int64_t j = 0; j < n; ++j)
+      if (J[i * n + j] == -128)
+        return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "int8 couplings must lie in [-127, 127]");
+  }
+  CK(cudaSetDevice(ctx->device));
+  cudaStreamSynchronize(ctx->stream);
+  free_state(ctx);
+  cudaFree(ctx->dJ);
+  ctx->dJ = nullptr;
+  const int64_t npad = round_up(n, PAD_N);
+  CK(cudaMalloc(&ctx->dJ, size_t(npad) * npad));
+  CK(cudaMemsetAsync(ctx->dJ, 0, size_t(npad) * npad, ctx->stream));
+  CK(cudaMemcpy2DAsync(ctx->dJ, npad, J, n, n, n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->n = n;
+  ctx->npad = npad;
+  ctx->kind = KIND_DENSE_I8;
+  return encode_2d_u8(ctx, &ctx->tmJ, ctx->dJ, npad, npad, 128, 128);
+}
+
+int sbg_set_couplings_dense_f64(sbg_ctx* ctx, int64_t n, const double* J) {
+  CHECK_CTX(ctx);
+  if (n < 1 || !J) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "instance size must be >= 1");
+  std::vector<int8_t> q(size_t(n) * n);
+  for (int64_t k = 0; k < n * n; ++k) {
+    const double v = J[k];
+    if (!(v == std::floor(v)) || v < -127.0 || v > 127.0)
+      return ctx->fail(SBG_ERR_UNSUPPORTED,
+                       "couplings must be integers in [-127, 127] for the int8 tensor-core path");
+    q[size_t(k)] = static_cast<int8_t>(v);
+  }
+  return sbg_set_couplings_dense_i8(ctx, n, q.data());
+}
+
+int sbg_gen_couplings_dense_pm1(sbg_ctx* ctx, int64_t n, uint64_t seed) {
+  CHECK_CTX(ctx);
+  if (n < 2) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "random dense instance needs n >= 2");
+  // gen_random_dense (model.cpp:144-159): upper triangle row-major, top bit of next().
+  std::vector<int8_t> J(size_t(n) * n, 0);
+  Xoshiro g(seed);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = i + 1; j < n; ++j) {
+      const int8_t v = (g.next() >> 63) ? int8_t(-1) : int8_t(1);
+      J[size_t(i) * n + j] = v;
+      J[size_t(j) * n + i] = v;
+    }
+  return sbg_set_couplings_dense_i8(ctx, n, J.data());
+}
+
+int sbg_set_couplings_csr_i8(sbg_ctx* ctx, int64_t n, int64_t nnz, const int32_t* rowptr,
+                             const int32_t* col, const int8_t* val) {
+  CHECK_CTX(ctx);
+  if (n < 1 || nnz < 0 || !rowptr || (nnz > 0 && (!col || !val)))
+    return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "bad CSR arguments");
+  if (rowptr[0] != 0 || rowptr[n] != nnz) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "bad CSR row pointer");
+  for (int64_t i = 0; i < n; ++i) {
+    if (rowptr[i + 1] < rowptr[i]) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "CSR row pointer not monotone");
+    for (int32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+      if (col[k] < 0 || col[k] >= n) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "coupling index out of range");
+      if (col[k] == i) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "coupling diagonal must be zero");
+      if (k > rowptr[i] && col[k] <= col[k - 1])
+        return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "CSR columns must be strictly ascending");
+      if (val[k] == -128) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "int8 couplings must lie in [-127, 127]");
+    }
+  }
+  CK(cudaSetDevice(ctx->device));
+  cudaStreamSynchronize(ctx->stream);
+  free_state(ctx);
+  cudaFree(ctx->dJ);
+  cudaFree(ctx->d_rowptr);
+  cudaFree(ctx->d_col);
+  cudaFree(ctx->d_val);
+  ctx->dJ = nullptr;
+  ctx->d_rowptr = ctx->d_col = nullptr;
+  ctx->d_val = nullptr;
+  CK(cudaMalloc(&ctx->d_rowptr, sizeof(int32_t) * (n + 1)));
+  CK(cudaMalloc(&ctx->d_col, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+  CK(cudaMalloc(&ctx->d_val, std::max<int64_t>(nnz, 1)));
+  CK(cudaMemcpy(ctx->d_rowptr, rowptr, sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice));
+  if (nnz) {
+    CK(cudaMemcpy(ctx->d_col, col, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_val, val, nnz, cudaMemcpyHostToDevice));
+  }
+  ctx->n = n;
+  ctx->npad = round_up(n, 32);
+  ctx->nnz = nnz;
+  ctx->kind = KIND_CSR_I8;
+  return SBG_OK;
+}
+
+int sbg_set_state(sbg_ctx* ctx, int64_t R, const float* x, const float* y, const float* p) {
+  CHECK_CTX(ctx);
+  if (!x || !y) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "x and y are required");
+  CK(cudaSetDevice(ctx->device));
+  int rc = ensure_state(ctx, R);
+  if (rc) return rc;
+  const size_t pitch = sizeof(float) * ctx->npad, w = sizeof(float) * ctx->n;
+  CK(cudaMemcpy2DAsync(ctx->dX, pitch, x, w, w, R, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpy2DAsync(ctx->dY, pitch, y, w, w, R, cudaMemcpyHostToDevice, ctx->stream));
+  if (p) {
+    CK(cudaMemcpy2DAsync(ctx->dP, pitch, p, w, w, R, cudaMemcpyHostToDevice, ctx->stream));
+  } else {
+    const size_t cnt = size_t(ctx->rpad) * ctx->npad;
+    fill_f32_kernel<<<grid_for(ctx, cnt, 256), 256, 0, ctx->stream>>>(ctx->dP, cnt, 1.0f);
+    CK(cudaGetLastError());
+    ++ctx->launches;
+  }
+  return SBG_OK;
+}
+
+int sbg_init_state(sbg_ctx* ctx, int64_t R, int32_t mode, uint64_t master, uint64_t tag, int64_t offset) {
+  CHECK_CTX(ctx);
+  if (mode < 0 || mode > 2) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "unknown init mode");
+  CK(cudaSetDevice(ctx->device));
+  int rc = ensure_state(ctx, R);
+  if (rc) return rc;
+  const int blocks = int((R + INIT_THREADS - 1) / INIT_THREADS);
+  init_state_kernel<<<blocks, INIT_THREADS, 0, ctx->stream>>>(ctx->dX, ctx->dY, ctx->dP, int32_t(ctx->n),
+                                                              ctx->npad, int32_t(R), mode, master, tag, offset);
+  CK(cudaGetLastError());
+  ++ctx->launches;
+  return SBG_OK;
+}
+
+int sbg_get_state(sbg_ctx* ctx, float* x, float* y, float* p) {
+  CHECK_CTX(ctx);
+  if (!ctx->dX) return ctx->fail(SBG_ERR_STATE, "no state");
+  CK(cudaSetDevice(ctx->device));
+  const size_t pitch = sizeof(float) * ctx->npad, w = sizeof(float) * ctx->n;
+  if (x) CK(cudaMemcpy2DAsync(x, w, ctx->dX, pitch, w, ctx->R, cudaMemcpyDeviceToHost, ctx->stream));
+  if (y) CK(cudaMemcpy2DAsync(y, w, ctx->dY, pitch, w, ctx->R, cudaMemcpyDeviceToHost, ctx->stream));
+  if (p) CK(cudaMemcpy2DAsync(p, w, ctx->dP, pitch, w, ctx->R, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SBG_OK;
+}
+
+int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t m_end) {
+  CHECK_CTX(ctx);
+  int rc = validate_params(ctx, prm);
+  if (rc) return rc;
+  if (!ctx->dX || ctx->R < 1) return ctx->fail(SBG_ERR_STATE, "state not initialised");
+  if (m_end > prm->steps || m_begin > m_end)
+    return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "state already at the final step");  // engine.cpp:59
+  CK(cudaSetDevice(ctx->device));
+  const bool sign = is_sign_variant(prm->variant);
+  const bool honours_a = prm->variant == SBG_GBSB || prm->variant == SBG_GDSB;  // engine.cpp:64 (+GdSB)
+  PhaseConsts k;
+  k.a = honours_a ? float(prm->a) : 0.0f;
+  k.c = float(prm->c);
+  k.dt = float(prm->dt);
+  k.denom = 0.0f;
+  CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+  if (ctx->kind == KIND_CSR_I8) {
+    for (uint64_t m = m_begin; m < m_end; ++m) {
+      rc = launch_csr_step(ctx->stream, ctx->sms, int32_t(ctx->n), ctx->d_rowptr, ctx->d_col, ctx->d_val,
+                           ctx->dX, ctx->dY, ctx->dP, ctx->npad, int32_t(ctx->R), sign, k, prm->steps, m);
+      if (rc) return ctx->fail(SBG_ERR_CUDA, "CSR step launch failed: %s", cudaGetErrorString(cudaError_t(rc)));
+      ++ctx->launches;
+    }
+  } else {
+    const int need = sign ? 1 : NPL;
+    if (ctx->g_mode != need) {
+      rc = prep_planes(ctx, ctx->dX, ctx->dG[ctx->g_cur], need, ctx->R, ctx->rpad);
+      if (rc) return rc;
+      ctx->g_mode = need;
+    }
+    for (uint64_t m = m_begin; m < m_end; ++m) {
+      const int cur = ctx->g_cur;
+      StepArgs a = base_args(ctx, sign ? BN_SIGN : BN_PLANE, ctx->R, ctx->rpad);
+      a.x = ctx->dX;
+      a.y = ctx->dY;
+      a.p = ctx->dP;
+      a.planes_next = ctx->dG[cur ^ 1];
+      a.k = k;
+      a.m_dev = nullptr;
+      a.m_off = int64_t(m);
+      a.M = prm->steps;
+      rc = sign ? launch_step<1, BN_SIGN, EpiMode::Step>(ctx, ctx->tmG_sign[cur], a)
+                : launch_step<NPL, BN_PLANE, EpiMode::Step>(ctx, ctx->tmG_planes[cur], a);
+      if (rc) return rc;
+      ctx->g_cur = cur ^ 1;
+    }
+  }
+  CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+  return SBG_OK;
+}
+
+double sbg_last_advance_ms(const sbg_ctx* ctx) {
+  if (!ctx) return -1.0;
+  cudaSetDevice(ctx->device);
+  if (cudaEventSynchronize(ctx->ev[1]) != cudaSuccess) return -1.0;
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]) != cudaSuccess) return -1.0;
+  return ms;
+}
+
+int sbg_readout(sbg_ctx* ctx, int8_t* spins, double* energy, int64_t* best_index, double* best_energy) {
+  CHECK_CTX(ctx);
+  if (!ctx->dX || ctx->R < 1) return ctx->fail(SBG_ERR_STATE, "state not initialised");
+  CK(cudaSetDevice(ctx->device));
+  int rc;
+  CK(cudaMemsetAsync(ctx->dE2, 0, sizeof(unsigned long long) * ctx->rpad, ctx->stream));
+  if (ctx->kind == KIND_CSR_I8) {
+    rc = launch_csr_readout(ctx->stream, ctx->sms, int32_t(ctx->n), ctx->d_rowptr, ctx->d_col, ctx->d_val,
+                            ctx->dX, ctx->npad, int32_t(ctx->R), ctx->dSign, ctx->dE2);
+    if (rc) return ctx->fail(SBG_ERR_CUDA, "CSR readout failed: %s", cudaGetErrorString(cudaError_t(rc)));
+    ctx->launches += 1;
+  } else {
+    rc = prep_planes(ctx, ctx->dX, ctx->dSign, 1, ctx->R, ctx->rpad);
+    if (rc) return rc;
+    StepArgs a = base_args(ctx, BN_SIGN, ctx->R, ctx->rpad);
+    a.sign_in = reinterpret_cast<const int8_t*>(ctx->dSign);
+    a.e2 = ctx->dE2;
+    rc = launch_step<1, BN_SIGN, EpiMode::Readout>(ctx, ctx->tmSign, a);
+    if (rc) return rc;
+  }
+  argmin_energy_kernel<<<1, 1024, 0, ctx->stream>>>(reinterpret_cast<const long long*>(ctx->dE2),
+                                                    int32_t(ctx->R), ctx->dBest);
+  CK(cudaGetLastError());
+  ++ctx->launches;
+  if (spins)
+    CK(cudaMemcpy2DAsync(spins, ctx->n, ctx->dSign, ctx->npad, ctx->n, ctx->R, cudaMemcpyDeviceToHost,
+                         ctx->stream));
+  std::vector<long long> e2;
+  if (energy) {
+    e2.resize(ctx->R);
+    CK(cudaMemcpyAsync(e2.data(), ctx->dE2, sizeof(long long) * ctx->R, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  long long best[2] = {0, 0};
+  CK(cudaMemcpyAsync(best, ctx->dBest, sizeof best, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  // ising_energy = -1/2 sum_i s_i (J s)_i, exact in double for integer J
+  if (energy)
+    for (int64_t r = 0; r < ctx->R; ++r) energy[r] = -0.5 * double(e2[size_t(r)]);
+  if (best_index) *best_index = best[0];
+  if (best_energy) *best_energy = -0.5 * double(best[1]);
+  return SBG_OK;
+}
+
+int sbg_fields_sign(sbg_ctx* ctx, int64_t R, const int8_t* S, int32_t* F) {
+  CHECK_CTX(ctx);
+  if (ctx->kind != KIND_DENSE_I8) return ctx->fail(SBG_ERR_STATE, "dense couplings not set");
+  if (R < 1 || !S || !F) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "bad arguments");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t rpad = round_up(R, PAD_R);
+  const size_t pl = size_t(rpad) * ctx->npad;
+  int8_t* dS = nullptr;
+  uint8_t* dGs = nullptr;
+  int32_t* dF = nullptr;
+  CK(cudaMalloc(&dS, size_t(R) * ctx->n));
+  CK(cudaMalloc(&dGs, pl));
+  CK(cudaMalloc(&dF, sizeof(int32_t) * pl));
+  CK(cudaMemcpyAsync(dS, S, size_t(R) * ctx->n, cudaMemcpyHostToDevice, ctx->stream));
+  pad_plane_kernel<<<grid_for(ctx, pl, 256), 256, 0, ctx->stream>>>(dS, dGs, int32_t(ctx->n),
+                                                                    int32_t(ctx->npad), int32_t(R), int32_t(rpad));
+  CK(cudaGetLastError());
+  CUtensorMap tm;
+  int rc = encode_2d_u8(ctx, &tm, dGs, ctx->npad, rpad, 128, BN_SIGN);
+  if (rc == SBG_OK) {
+    StepArgs a = base_args(ctx, BN_SIGN, R, rpad);
+    a.fields_out = dF;
+    rc = launch_step<1, BN_SIGN, EpiMode::Fields>(ctx, tm, a);
+  }
+  if (rc == SBG_OK) {
+    CK(cudaMemcpy2DAsync(F, sizeof(int32_t) * ctx->n, dF, sizeof(int32_t) * ctx->npad, sizeof(int32_t) * ctx->n,
+                         R, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  cudaFree(dS);
+  cudaFree(dGs);
+  cudaFree(dF);
+  return rc;
+}
+
+int sbg_fields_fixed(sbg_ctx* ctx, int64_t R, const float* x, float* F) {
+  CHECK_CTX(ctx);
+  if (ctx->kind != KIND_DENSE_I8) return ctx->fail(SBG_ERR_STATE, "dense couplings not set");
+  if (R < 1 || !x || !F) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "bad arguments");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t rpad = round_up(R, PAD_R);
+  const size_t pl = size_t(rpad) * ctx->npad;
+  float* dx = nullptr;
+  uint8_t* dGp = nullptr;
+  float* dF = nullptr;
+  CK(cudaMalloc(&dx, sizeof(float) * pl));
+  CK(cudaMalloc(&dGp, NPL * pl));
+  CK(cudaMalloc(&dF, sizeof(float) * pl));
+  CK(cudaMemsetAsync(dx, 0, sizeof(float) * pl, ctx->stream));
+  CK(cudaMemcpy2DAsync(dx, sizeof(float) * ctx->npad, x, sizeof(float) * ctx->n, sizeof(float) * ctx->n, R,
+                       cudaMemcpyHostToDevice, ctx->stream));
+  int rc = prep_planes(ctx, dx, dGp, NPL, R, rpad);
+  CUtensorMap tm;
+  if (rc == SBG_OK) rc = encode_2d_u8(ctx, &tm, dGp, ctx->npad, NPL * rpad, 128, BN_PLANE);
+  if (rc == SBG_OK) {
+    StepArgs a = base_args(ctx, BN_PLANE, R, rpad);
+    a.fields_out = dF;
+    rc = launch_step<NPL, BN_PLANE, EpiMode::Fields>(ctx, tm, a);
+  }
+  if (rc == SBG_OK) {
+    CK(cudaMemcpy2DAsync(F, sizeof(float) * ctx->n, dF, sizeof(float) * ctx->npad, sizeof(float) * ctx->n, R,
+                         cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  cudaFree(dx);
+  cudaFree(dGp);
+  cudaFree(dF);
+  return rc;
+}
+
+static int run_tail(sbg_ctx* ctx, const sbg_params* prm, float* x_final, int8_t* spins, double* energy,
+                    int64_t* best_index, sbg_timing* timing) {
+  CK(cudaEventRecord(ctx->ev[3], ctx->stream));
+  int rc = sbg_advance(ctx, prm, 0, prm->steps);
+  if (rc) return rc;
+  CK(cudaEventRecord(ctx->ev[4], ctx->stream));
+  rc = sbg_readout(ctx, spins, energy, best_index, nullptr);
+  if (rc) return rc;
+  CK(cudaEventRecord(ctx->ev[5], ctx->stream));
+  if (x_final) {
+    const size_t pitch = sizeof(float) * ctx->npad, w = sizeof(float) * ctx->n;
+    CK(cudaMemcpy2DAsync(x_final, w, ctx->dX, pitch, w, ctx->R, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaEventRecord(ctx->ev[6], ctx->stream));
+  CK(cudaEventSynchronize(ctx->ev[6]));
+  if (timing) {
+    float a = 0, b = 0, c = 0, d = 0, e = 0;
+    cudaEventElapsedTime(&a, ctx->ev[2], ctx->ev[7]);
+    cudaEventElapsedTime(&b, ctx->ev[7], ctx->ev[3]);
+    cudaEventElapsedTime(&c, ctx->ev[3], ctx->ev[4]);
+    cudaEventElapsedTime(&d, ctx->ev[4], ctx->ev[5]);
+    cudaEventElapsedTime(&e, ctx->ev[5], ctx->ev[6]);
+    timing->h2d_ms = a;
+    timing->init_ms = b;
+    timing->steps_ms = c;
+    timing->readout_ms = d;
+    timing->d2h_ms = e;
+    timing->total_ms = a + b + c + d + e;
+    timing->kernel_launches = ctx->launches;
+  }
+  return SBG_OK;
+}
+
+int sbg_run(sbg_ctx* ctx, const sbg_params* prm, int64_t R, const float* x0, const float* y0, float* x_final,
+            int8_t* spins, double* energy, int64_t* best_index, sbg_timing* timing) {
+  CHECK_CTX(ctx);
+  int rc = validate_params(ctx, prm);
+  if (rc) return rc;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+  rc = sbg_set_state(ctx, R, x0, y0, nullptr);
+  if (rc) return rc;
+  CK(cudaEventRecord(ctx->ev[7], ctx->stream));
+  return run_tail(ctx, prm, x_final, spins, energy, best_index, timing);
+}
+
+int sbg_run_seeded(sbg_ctx* ctx, const sbg_params* prm, int64_t R, int32_t init_mode, uint64_t master,
+                   uint64_t tag, int64_t offset, int8_t* spins, double* energy, int64_t* best_index,
+                   sbg_timing* timing) {
+  CHECK_CTX(ctx);
+  int rc = validate_params(ctx, prm);
+  if (rc) return rc;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+  CK(cudaEventRecord(ctx->ev[7], ctx->stream));
+  rc = sbg_init_state(ctx, R, init_mode, master, tag, offset);
+  if (rc) return rc;
+  return run_tail(ctx, prm, nullptr, spins, energy, best_index, timing);
+}
+
+int sbg_synchronize(sbg_ctx* ctx) {
+  CHECK_CTX(ctx);
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SBG_OK;
+}
+
+int sbg_state_device(sbg_ctx* ctx, float** x, float** y, float** p, int64_t* ld, int64_t* rpad) {
+  CHECK_CTX(ctx);
+  if (!ctx->dX) return ctx->fail(SBG_ERR_STATE, "no state");
+  if (x) *x = ctx->dX;
+  if (y) *y = ctx->dY;
+  if (p) *p = ctx->dP;
+  if (ld) *ld = ctx->npad;
+  if (rpad) *rpad = ctx->rpad;
+  return SBG_OK;
+}
+
+int sbg_success_tts(int64_t hits, int64_t n_rep, double t_com, double* out) {
+  // success_from_counts + time_to_solution, bench.cpp:15-26, :52-68
+  if (!out) return SBG_ERR_INVALID_ARGUMENT;
+  if (n_rep <= 0 || hits < 0 || hits > n_rep) return SBG_ERR_INVALID_ARGUMENT;
+  const double p = double(hits) / double(n_rep);
+  out[0] = p;
+  out[1] = std::sqrt((p - p * p) / double(n_rep));
+  if (!(t_com > 0.0) || !(p > 0.0)) return SBG_ERR_INVALID_ARGUMENT;
+  if (p > 0.99) {
+    out[2] = t_com;
+    out[3] = 0.0;
+  } else {
+    const double log_miss = std::log1p(-p);
+    out[2] = t_com * std::log(0.01) / log_miss;
+    out[3] = out[2] * out[1] / ((1.0 - p) * std::fabs(log_miss));
+  }
+  return SBG_OK;
+}
+
+int sbg_tune_wigner_f64(int64_t n, const double* J, double d_t, double* c, double* dt) {
+  // auto_tune(wigner): spectral.cpp:298-305 with offdiagonal_sigma (:254-266)
+  if (n < 2 || !J || !c || !dt) return SBG_ERR_INVALID_ARGUMENT;
+  if (!(d_t > 0.0)) return SBG_ERR_INVALID_ARGUMENT;
+  double sum_sq = 0.0;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j)
+      if (j != i) sum_sq += J[i * n + j] * J[i * n + j];
+  const double sigma = std::sqrt(sum_sq / (double(n) * double(n - 1)));
+  if (sigma == 0.0) return SBG_ERR_INVALID_ARGUMENT;  // degenerate instance
+  const double edge = 2.0 * std::sqrt(double(n)) * sigma;
+  *c = 1.0 / edge;
+  *dt = d_t * std::sqrt(2.0 / (1.0 - (-edge) / edge));
+  return SBG_OK;
+}
+
+}  // extern "C"

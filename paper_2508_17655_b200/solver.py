@@ -1,0 +1,351 @@
+"""Host-side mirror of the reference solver API for the GSB hot path.
+
+Names, argument meaning and error behaviour follow sbopt
+(/root/reference/proj/core/include/sbopt/{engine,bench,spectral}.hpp) so that
+parity tests read like the reference's own tests; every call goes through the
+sbgpu C ABI (include/sbgpu.h) to the sm_100a kernels. There is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import enum
+import math
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import ptr, raise_for
+
+
+class Variant(enum.IntEnum):  # engine.hpp:26 (+ gdsb)
+    bsb = _lib.BSB
+    dsb = _lib.DSB
+    gbsb = _lib.GBSB
+    gdsb = _lib.GDSB
+
+
+class InitMode(enum.IntEnum):  # engine.hpp:27 (+ the BASELINE small-uniform init)
+    uniform_random = _lib.INIT_UNIFORM_RANDOM
+    chaos_probe = _lib.INIT_CHAOS_PROBE
+    small_uniform = _lib.INIT_SMALL_UNIFORM
+
+
+SEED_STREAM_BATCH = 3  # rng.hpp:36 seed_stream::batch
+SEED_STREAM_GPU_INIT = 7  # BASELINE "gpu_init" stream
+
+
+@dataclasses.dataclass
+class SolverConfig:  # engine.hpp:29-38
+    variant: Variant = Variant.gbsb
+    steps: int = 1000
+    dt: Optional[float] = None
+    c: Optional[float] = None
+    a: float = 0.0
+    seed: int = 0
+    init_mode: InitMode = InitMode.uniform_random
+
+
+@dataclasses.dataclass
+class TuningResult:  # spectral.hpp:28-33
+    c: float = 0.0
+    dt: float = 0.0
+    d_t_factor: float = 0.0
+    lambda_max: float = float("nan")
+    lambda_min: float = float("nan")
+    method: str = "wigner"
+
+
+@dataclasses.dataclass
+class RunResult:  # engine.hpp:56-64 (batched: one per replica)
+    final_spins: np.ndarray
+    energy: float
+    cut: Optional[int] = None
+    wall_time_s: float = 0.0
+    config_echo: Optional[SolverConfig] = None
+    tuning_echo: Optional[TuningResult] = None
+
+
+def resolve_config(cfg: SolverConfig, tuning: TuningResult) -> SolverConfig:
+    """engine.cpp:48-53 + validate() :16-21 (raises ValueError like std::invalid_argument)."""
+    out = dataclasses.replace(cfg)
+    if out.dt is None:
+        out.dt = tuning.dt
+    if out.c is None:
+        out.c = tuning.c
+    if out.steps < 1:
+        raise ValueError("step count M must be >= 1")
+    if not out.dt > 0.0:
+        raise ValueError("dt must be positive")
+    if not out.c > 0.0:
+        raise ValueError("c must be positive")
+    if not out.a >= 0.0:
+        raise ValueError("A must be >= 0")
+    return out
+
+
+def auto_tune_wigner(J: np.ndarray, d_t_factor: float = 1.25) -> TuningResult:
+    """auto_tune(TuneMode::wigner) (spectral.cpp:294-326) via the C ABI."""
+    J = np.ascontiguousarray(J, np.float64)
+    c, dt = C.c_double(), C.c_double()
+    rc = _lib.lib().sbg_tune_wigner_f64(J.shape[0], ptr(J), d_t_factor, C.byref(c), C.byref(dt))
+    if rc:
+        raise ValueError("degenerate instance: all couplings zero")
+    edge = 1.0 / c.value
+    return TuningResult(c=c.value, dt=dt.value, d_t_factor=d_t_factor, lambda_max=edge, lambda_min=-edge)
+
+
+@dataclasses.dataclass
+class SuccessStats:  # bench.hpp:22-28
+    p_s: float
+    delta_p_s: float
+    n_rep: int
+    target_value: float
+    hit_count: int
+
+
+@dataclasses.dataclass
+class TtsResult:  # bench.hpp:41-46
+    tts_s: float
+    delta_tts_s: float
+    t_com_s: float
+    stats: SuccessStats
+
+
+def success_from_counts(hit_count: int, n_rep: int, target: float) -> SuccessStats:
+    out = (C.c_double * 4)()
+    rc = _lib.lib().sbg_success_tts(hit_count, n_rep, 1.0, out)
+    if rc and not (n_rep > 0 and 0 <= hit_count <= n_rep):
+        raise ValueError("success probability needs n_rep >= 1 and hits <= n_rep")
+    return SuccessStats(out[0], out[1], n_rep, target, hit_count)
+
+
+def success_probability(energies, target: float) -> SuccessStats:
+    """bench.cpp:28-36: hit = energy <= target (exact)."""
+    e = np.asarray(energies, np.float64)
+    if e.size == 0:
+        raise ValueError("no results")
+    return success_from_counts(int((e <= target).sum()), int(e.size), target)
+
+
+def success_probability_cut(cuts, target: float) -> SuccessStats:
+    """bench.cpp:38-50 with HitKind::cut_max: hit = cut >= target."""
+    c = np.asarray(cuts, np.float64)
+    if c.size == 0:
+        raise ValueError("no results")
+    return success_from_counts(int((c >= target).sum()), int(c.size), target)
+
+
+def time_to_solution(t_com_s: float, stats: SuccessStats) -> TtsResult:
+    """bench.cpp:52-68."""
+    if not t_com_s > 0.0:
+        raise ValueError("t_com must be positive")
+    if not stats.p_s > 0.0:
+        raise ValueError("TTS undefined for p_s = 0")
+    out = (C.c_double * 4)()
+    raise_for(_lib.lib().sbg_success_tts(stats.hit_count, stats.n_rep, t_com_s, out), "tts")
+    return TtsResult(out[2], out[3], t_com_s, stats)
+
+
+class Solver:
+    """One sbgpu context on one CUDA device (replaces ThreadPool + per-run state)."""
+
+    def __init__(self, device: int = 0):
+        self._L = _lib.lib()
+        h = C.c_void_p()
+        rc = self._L.sbg_create(device, C.byref(h))
+        if rc:
+            raise _lib.SbgError(rc, f"sbg_create(device={device}) failed: {self._L.sbg_strerror(rc).decode()}")
+        self._h = h
+        self.device = device
+        self.n = 0
+        self.total_weight: Optional[int] = None
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._L.sbg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _check(self, rc: int) -> None:
+        if rc:
+            raise_for(rc, self._L.sbg_last_error(self._h).decode())
+
+    @property
+    def sm_count(self) -> int:
+        return self._L.sbg_device_sm_count(self._h)
+
+    @property
+    def kernel_launches(self) -> int:
+        return self._L.sbg_kernel_launches(self._h)
+
+    # ----------------------------------------------------------- instances
+    def set_instance(self, J: np.ndarray, graph_total_weight: Optional[int] = None) -> None:
+        """IsingInstance (model.hpp:46-70), dense integer J (int8 or integral fp64)."""
+        J = np.ascontiguousarray(J)
+        n = J.shape[0]
+        if J.dtype == np.int8:
+            self._check(self._L.sbg_set_couplings_dense_i8(self._h, n, ptr(J)))
+        else:
+            J = np.ascontiguousarray(J, np.float64)
+            self._check(self._L.sbg_set_couplings_dense_f64(self._h, n, ptr(J)))
+        self.n = n
+        # cut via the bridge (model.hpp:103-104): J = -w  =>  W = -sum_{i<j} J_ij
+        self.total_weight = graph_total_weight if graph_total_weight is not None else int(
+            -np.triu(J.astype(np.int64), 1).sum())
+
+    def gen_random_dense(self, n: int, seed: int) -> None:
+        """gen_random_dense (model.cpp:144-159) straight into the device instance."""
+        self._check(self._L.sbg_gen_couplings_dense_pm1(self._h, n, seed))
+        self.n = n
+        self.total_weight = None
+
+    def set_instance_csr(self, n: int, rowptr, col, val, total_weight: Optional[int] = None) -> None:
+        rowptr = np.ascontiguousarray(rowptr, np.int32)
+        col = np.ascontiguousarray(col, np.int32)
+        val = np.ascontiguousarray(val, np.int8)
+        self._check(self._L.sbg_set_couplings_csr_i8(self._h, n, len(col), ptr(rowptr), ptr(col), ptr(val)))
+        self.n = n
+        self.total_weight = total_weight if total_weight is not None else int(-val.astype(np.int64).sum() // 2)
+
+    # -------------------------------------------------------------- states
+    def set_state(self, x: np.ndarray, y: np.ndarray, p: Optional[np.ndarray] = None) -> None:
+        x = np.ascontiguousarray(x, np.float32)
+        y = np.ascontiguousarray(y, np.float32)
+        if p is not None:
+            p = np.ascontiguousarray(p, np.float32)
+        self._check(self._L.sbg_set_state(self._h, x.shape[0], ptr(x), ptr(y), ptr(p)))
+        self.R = x.shape[0]
+
+    def init_state(self, R: int, mode: InitMode, master: int, tag: int, offset: int = 0) -> None:
+        self._check(self._L.sbg_init_state(self._h, R, int(mode), master, tag, offset))
+        self.R = R
+
+    def get_state(self):
+        x, y, p = (np.empty((self.R, self.n), np.float32) for _ in range(3))
+        self._check(self._L.sbg_get_state(self._h, ptr(x), ptr(y), ptr(p)))
+        return x, y, p
+
+    @staticmethod
+    def params(cfg: SolverConfig) -> _lib.Params:
+        return _lib.Params(int(cfg.variant), 0, int(cfg.steps), float(cfg.dt), float(cfg.c), float(cfg.a))
+
+    def advance(self, cfg: SolverConfig, m_begin: int, m_end: int) -> None:
+        """step() (engine.cpp:55-110) for m = m_begin .. m_end-1 of an M-step run."""
+        prm = self.params(cfg)
+        self._check(self._L.sbg_advance(self._h, C.byref(prm), m_begin, m_end))
+
+    def synchronize(self) -> None:
+        self._check(self._L.sbg_synchronize(self._h))
+
+    def last_advance_ms(self) -> float:
+        return self._L.sbg_last_advance_ms(self._h)
+
+    def readout(self):
+        """(spins R x n int8, energies R, best_index, best_energy)."""
+        spins = np.empty((self.R, self.n), np.int8)
+        energy = np.empty(self.R, np.float64)
+        best = C.c_int64()
+        best_e = C.c_double()
+        self._check(self._L.sbg_readout(self._h, ptr(spins), ptr(energy), C.byref(best), C.byref(best_e)))
+        return spins, energy, int(best.value), float(best_e.value)
+
+    def fields_sign(self, S: np.ndarray) -> np.ndarray:
+        S = np.ascontiguousarray(S, np.int8)
+        F = np.empty(S.shape, np.int32)
+        self._check(self._L.sbg_fields_sign(self._h, S.shape[0], ptr(S), ptr(F)))
+        return F
+
+    def fields_fixed(self, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, np.float32)
+        F = np.empty(x.shape, np.float32)
+        self._check(self._L.sbg_fields_fixed(self._h, x.shape[0], ptr(x), ptr(F)))
+        return F
+
+    # ---------------------------------------------------------------- runs
+    def run_batch(self, cfg: SolverConfig, tuning: TuningResult, R: int, x0: Optional[np.ndarray] = None,
+                  y0: Optional[np.ndarray] = None, master_seed: int = 0, tag: int = SEED_STREAM_BATCH,
+                  replica_offset: int = 0, want_x: bool = False):
+        """run() (engine.cpp:112-139) for R replicas in one device pass.
+
+        Initial states: host x0/y0 (R x n fp32), or generated on the device from
+        derive_seed(master_seed, {tag, replica_offset + r}) with cfg.init_mode.
+        Returns (list-free) arrays: spins, energies, cuts, best index, timing dict, x_final.
+        """
+        rcfg = resolve_config(cfg, tuning)
+        prm = self.params(rcfg)
+        spins = np.empty((R, self.n), np.int8)
+        energy = np.empty(R, np.float64)
+        best = C.c_int64()
+        timing = _lib.Timing()
+        x_final = np.empty((R, self.n), np.float32) if want_x else None
+        if x0 is not None:
+            x0 = np.ascontiguousarray(x0, np.float32)
+            y0 = np.ascontiguousarray(y0 if y0 is not None else np.zeros_like(x0), np.float32)
+            self._check(self._L.sbg_run(self._h, C.byref(prm), R, ptr(x0), ptr(y0), ptr(x_final), ptr(spins),
+                                        ptr(energy), C.byref(best), C.byref(timing)))
+        else:
+            self._check(self._L.sbg_run_seeded(self._h, C.byref(prm), R, int(rcfg.init_mode), master_seed, tag,
+                                               replica_offset, ptr(spins), ptr(energy), C.byref(best),
+                                               C.byref(timing)))
+        self.R = R
+        cuts = None
+        if self.total_weight is not None:
+            # cut = (W - E) / 2 (model.hpp:103-104), exact integers
+            cuts = ((self.total_weight - energy) / 2).astype(np.int64)
+        return BatchResult(spins, energy, cuts, int(best.value), timing.as_dict(), x_final, rcfg, tuning)
+
+    def batch_best_of(self, cfg: SolverConfig, tuning: TuningResult, n_batch: int, master_seed: int) -> RunResult:
+        """bench.cpp:70-92: replicas seeded derive_seed(master, {batch, r}); min energy, ties -> lowest r."""
+        if n_batch < 1:
+            raise ValueError("batch size must be >= 1")
+        b = self.run_batch(cfg, tuning, n_batch, master_seed=master_seed, tag=SEED_STREAM_BATCH)
+        w = b.best_index
+        echo = dataclasses.replace(b.config, seed=_derive_seed(master_seed, [SEED_STREAM_BATCH, w]))
+        return RunResult(final_spins=b.spins[w].copy(), energy=float(b.energies[w]),
+                         cut=None if b.cuts is None else int(b.cuts[w]),
+                         wall_time_s=b.timing["total_ms"] / 1e3, config_echo=echo, tuning_echo=tuning)
+
+
+@dataclasses.dataclass
+class BatchResult:
+    spins: np.ndarray
+    energies: np.ndarray
+    cuts: Optional[np.ndarray]
+    best_index: int
+    timing: dict
+    x_final: Optional[np.ndarray]
+    config: SolverConfig
+    tuning: TuningResult
+
+
+def _mix64(z: int) -> int:
+    M = (1 << 64) - 1
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+    return z ^ (z >> 31)
+
+
+def _derive_seed(master: int, keys) -> int:
+    """rng.hpp:26-31 (host bookkeeping for config echoes only)."""
+    M = (1 << 64) - 1
+    h = _mix64((master + 0x9E3779B97F4A7C15) & M)
+    for k in keys:
+        h = _mix64(h ^ ((k + 0x9E3779B97F4A7C15) & M))
+    return h
+
+
+def cut_from_energy(total_weight: int, energy: float) -> int:
+    return int(math.floor((total_weight - energy) / 2 + 0.5))

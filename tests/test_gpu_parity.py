@@ -1,0 +1,243 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle.
+
+Protocols:
+  P1  teacher-forced fields J*S bit-exact (int32) against the oracle;
+  P2  bitwise trajectories against the fp32 GPU-op-order mirror (all variants:
+      the continuous variants use an exact fixed-point field, so they are
+      bitwise too);
+  P3  fp32 vs the fp64 reference within 1e-5 relative through 30 steps;
+plus readout/argmin, init bit-exactness, CSR == dense, and error behaviour.
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+BSB, DSB, GBSB, GDSB = 0, 1, 2, 3
+
+
+@pytest.fixture(scope="module")
+def solver():
+    from paper_2508_17655_b200 import Solver
+
+    s = Solver(0)
+    yield s
+    s.close()
+
+
+def cfg_for(variant, steps, dt, c, a):
+    from paper_2508_17655_b200 import SolverConfig, Variant
+
+    return SolverConfig(variant=Variant(variant), steps=steps, dt=dt, c=c, a=a)
+
+
+@pytest.mark.parametrize("n,R", [(37, 5), (130, 129), (2000, 300)])
+def test_p1_fields_sign_bit_exact(solver, orc, n, R):
+    J = orc.gen_dense_i8(n, 1)
+    solver.set_instance(J)
+    rng = np.random.default_rng(n + R)
+    S = np.where(rng.random((R, n)) < 0.5, -1, 1).astype(np.int8)
+    F = solver.fields_sign(S)
+    assert (F == orc.fields_i8(J, S)).all()
+
+
+def test_p1_fields_teacher_forced_over_50_steps(solver, orc):
+    """Feed the oracle's own sign matrix of each of 50 steps to the GPU."""
+    n, R = 2000, 64
+    J = orc.gen_dense_i8(n, 1)
+    solver.set_instance(J)
+    x, y, p = orc.init_small_uniform(n, R, master=5)
+    c, dt = 1.0 / (2.0 * np.sqrt(n)), 1.25
+    for m in range(50):
+        S = np.where(x >= 0, 1, -1).astype(np.int8)
+        assert (solver.fields_sign(S) == orc.fields_i8(J, S)).all(), f"step {m}"
+        x, y, p = orc.step_f32(GDSB, J, x, y, p, m, 1000, np.float32(dt), np.float32(c), np.float32(0.2))
+
+
+def test_fields_fixed_point_bit_exact(solver, orc):
+    n, R = 300, 70
+    J = orc.gen_dense_i8(n, 2)
+    solver.set_instance(J)
+    rng = np.random.default_rng(1)
+    x = rng.uniform(-1, 1, (R, n)).astype(np.float32)
+    x[0, :5] = [1.0, -1.0, 0.0, -0.0, 1e-30]
+    F = solver.fields_fixed(x)
+    assert (F.view(np.uint32) == orc.fields_fixed_i8(J, x).view(np.uint32)).all()
+    # and it is fp32-accurate against the exact fp64 dot product
+    exact = x.astype(np.float64) @ J.T.astype(np.float64)
+    assert np.abs(F - exact).max() <= 1e-5 * max(1.0, np.abs(exact).max())
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_device_init_bit_exact(solver, orc, mode):
+    n, R = 203, 77
+    solver.set_instance(orc.gen_dense_i8(n, 3))
+    from paper_2508_17655_b200 import InitMode
+
+    solver.init_state(R, InitMode(mode), master=11, tag=7 if mode == 2 else 3, offset=5)
+    x, y, p = solver.get_state()
+    if mode == 2:
+        ex, ey, ep = orc.init_small_uniform(n, R, master=11, tag=7, r0=5)
+    else:
+        ex, ey, ep = orc.init_reference(n, R, master=11, tag=3, chaos_probe=(mode == 1), r0=5)
+    assert (x == ex).all() and (y == ey).all() and (p == ep).all()
+
+
+@pytest.mark.parametrize("variant", [BSB, DSB, GBSB, GDSB])
+@pytest.mark.parametrize("n,R", [(37, 3), (200, 130)])
+def test_p2_trajectory_bitwise_vs_fp32_mirror(solver, orc, variant, n, R):
+    J = orc.gen_dense_i8(n, 4)
+    solver.set_instance(J)
+    x0, y0, p0 = orc.init_small_uniform(n, R, master=3)
+    c, dt, a, M = np.float32(1 / (2 * np.sqrt(n))), np.float32(1.25), np.float32(0.2), 200
+    solver.set_state(x0, y0, p0)
+    cfg = cfg_for(variant, M, float(dt), float(c), float(a))
+    x, y, p = x0, y0, p0
+    for m0, m1 in [(0, 1), (1, 10), (10, 60)]:
+        solver.advance(cfg, m0, m1)
+        gx, gy, gp = solver.get_state()
+        x, y, p = orc.step_f32(variant, J, x, y, p, m0, M, dt, c, a, m1 - m0)
+        assert (gx.view(np.uint32) == x.view(np.uint32)).all(), (variant, m1)
+        assert (gy.view(np.uint32) == y.view(np.uint32)).all(), (variant, m1)
+        assert (gp.view(np.uint32) == p.view(np.uint32)).all(), (variant, m1)
+
+
+def test_p2_full_run_to_final_step(solver, orc):
+    """M steps to the end (p -> 0 at m = M-1, engine.cpp:89), readout bitwise."""
+    n, R, M = 96, 10, 300
+    J = orc.gen_dense_i8(n, 6)
+    solver.set_instance(J)
+    x0, y0, p0 = orc.init_small_uniform(n, R, master=8)
+    c, dt = np.float32(1 / (2 * np.sqrt(n))), np.float32(1.25)
+    for variant in (GBSB, GDSB):
+        cfg = cfg_for(variant, M, float(dt), float(c), 0.2)
+        from paper_2508_17655_b200 import TuningResult
+
+        b = solver.run_batch(cfg, TuningResult(c=float(c), dt=float(dt)), R, x0=x0, y0=y0, want_x=True)
+        x, y, p = orc.step_f32(variant, J, x0, y0, p0, 0, M, dt, c, np.float32(0.2), M)
+        assert (b.x_final == x).all()
+        e2 = orc.energy2_i8(J, x)
+        assert (b.energies == -0.5 * e2).all()
+        assert b.best_index == orc.argmin(-e2)  # min energy == max E2, ties low
+        assert (b.spins == np.where(x >= 0, 1, -1)).all()
+
+
+@pytest.mark.parametrize("variant", [BSB, DSB, GBSB])
+def test_p3_short_horizon_vs_fp64_reference(solver, golden, variant):
+    """fp32 GPU vs the reference's fp64 step() (golden), <= 1e-5 relative at 30 steps."""
+    J = golden["J_n37_s11"]
+    c, dt = float(golden["tune_c"]), float(golden["tune_dt"])
+    solver.set_instance(J)
+    x0 = np.stack([golden[f"init_small_r{r}_x"] for r in (0, 1)]).astype(np.float32)
+    y0 = np.stack([golden[f"init_small_r{r}_y"] for r in (0, 1)]).astype(np.float32)
+    solver.set_state(x0, y0)
+    solver.advance(cfg_for(variant, 200, dt, c, 0.2), 0, 30)
+    x, _, _ = solver.get_state()
+    for r in (0, 1):
+        ref = golden[f"traj_small_v{variant}_r{r}_x30"]
+        assert np.abs(x[r] - ref).max() / np.abs(ref).max() <= 1e-5
+
+
+def test_readout_matches_reference_energy(solver, golden):
+    J = golden["J_n37_s11"]
+    solver.set_instance(J)
+    S = golden["en_spins"]
+    solver.set_state(S.astype(np.float32) * 0.5, np.zeros(S.shape, np.float32))
+    spins, energy, best, best_e = solver.readout()
+    assert (energy == golden["en_energy"]).all()
+    assert (spins == S).all()
+    e = golden["en_energy"]
+    assert best == int(np.flatnonzero(e == e.min())[0]) and best_e == e.min()
+
+
+def test_argmin_ties_to_lowest_index(solver):
+    """bench.cpp:84-87 / test_bench.cpp:164-175: equal energies -> lowest replica."""
+    J = np.array([[0, 1], [1, 0]], np.int8)
+    solver.set_instance(J)
+    x = np.array([[1, 1], [1, -1], [-1, 1], [0.5, -0.5]], np.float32)
+    solver.set_state(x, np.zeros_like(x))
+    _, energy, best, best_e = solver.readout()
+    assert list(energy) == [-1.0, 1.0, 1.0, 1.0] or list(energy) == [-1.0, 1.0, 1.0, 1.0]
+    assert best == 0 and best_e == -1.0
+    solver.set_state(x[1:], np.zeros_like(x[1:]))
+    _, energy, best, _ = solver.readout()
+    assert best == 0  # three equal energies 1.0 -> index 0
+
+
+def test_small_ground_states_found(solver, orc):
+    """test_engine.cpp:265-281 analogue: N=10, best of 20 replicas reaches the brute-force ground state."""
+    from paper_2508_17655_b200 import InitMode, SolverConfig, Variant, auto_tune_wigner
+
+    for seed in (400, 401, 402):
+        J = orc.gen_dense_i8(10, seed)
+        solver.set_instance(J)
+        bits = ((np.arange(1024)[:, None] >> np.arange(10)) & 1).astype(np.int64) * 2 - 1
+        ground = (-0.5 * np.einsum("ki,ij,kj->k", bits, J.astype(np.int64), bits)).min()
+        t = auto_tune_wigner(J.astype(np.float64))
+        cfg = SolverConfig(variant=Variant.gbsb, steps=2000, a=0.2, init_mode=InitMode.uniform_random)
+        best = solver.batch_best_of(cfg, t, 20, master_seed=seed)
+        assert best.energy == ground
+
+
+def test_csr_equals_dense_and_mirror(solver, orc):
+    n, m, R = 3000, 15000, 33
+    (ei, ej, w), csr = orc.gen_er_csr(n, m, 21)
+    dense = np.zeros((n, n), np.int8)
+    dense[ei, ej] = -w
+    dense[ej, ei] = -w
+    x0, y0, p0 = orc.init_small_uniform(n, R, master=2)
+    c, dt = np.float32(0.158), np.float32(1.25)
+    for variant in (GBSB, GDSB):
+        cfg = cfg_for(variant, 100, float(dt), float(c), 0.2)
+        solver.set_instance_csr(n, *csr)
+        solver.set_state(x0, y0, p0)
+        solver.advance(cfg, 0, 40)
+        cx, cy, cp = solver.get_state()
+        _, ce, cbest, _ = solver.readout()
+        solver.set_instance(dense)
+        solver.set_state(x0, y0, p0)
+        solver.advance(cfg, 0, 40)
+        dx, dy, dp = solver.get_state()
+        _, de, dbest, _ = solver.readout()
+        mx, my, mp = orc.step_f32_csr(variant, n, csr, x0, y0, p0, 0, 100, dt, c, np.float32(0.2), 40)
+        assert (cx == mx).all() and (cy == my).all() and (cp == mp).all()
+        assert (dx == cx).all() and (dy == cy).all() and (dp == cp).all()
+        assert (ce == de).all() and cbest == dbest
+        assert (ce == -0.5 * orc.energy2_csr(n, csr, mx)).all()
+
+
+def test_c2_shape_subset_bitwise(solver, orc):
+    """C2 geometry (N=2000, R=8192, GdSB): GPU replicas r0..r0+7 equal the mirror after 5 steps."""
+    from paper_2508_17655_b200 import InitMode
+
+    n, R = 2000, 8192
+    J = orc.gen_dense_i8(n, 1)
+    solver.set_instance(J)
+    solver.init_state(R, InitMode.small_uniform, master=1, tag=7)
+    c, dt = np.float32(1 / (2 * np.sqrt(n))), np.float32(1.25)
+    solver.advance(cfg_for(GDSB, 1000, float(dt), float(c), 0.2), 0, 5)
+    gx, gy, gp = solver.get_state()
+    for r0 in (0, 4099, 8184):
+        x, y, p = orc.init_small_uniform(n, 8, master=1, tag=7, r0=r0)
+        x, y, p = orc.step_f32(GDSB, J, x, y, p, 0, 1000, dt, c, np.float32(0.2), 5)
+        assert (gx[r0:r0 + 8] == x).all() and (gy[r0:r0 + 8] == y).all() and (gp[r0:r0 + 8] == p).all()
+
+
+def test_invalid_arguments_raise(solver, orc):
+    from paper_2508_17655_b200 import SolverConfig, TuningResult, Variant
+
+    bad = np.array([[0, 1], [2, 0]], np.int8)
+    with pytest.raises(ValueError):
+        solver.set_instance(bad)  # not symmetric (model.cpp:60-63)
+    with pytest.raises(ValueError):
+        solver.set_instance(np.array([[1, 0], [0, 0]], np.int8))  # diagonal
+    solver.set_instance(orc.gen_dense_i8(8, 1))
+    t = TuningResult(c=0.1, dt=0.5)
+    for kw in (dict(steps=0), dict(dt=-1.0), dict(a=-0.5)):
+        with pytest.raises(ValueError):
+            solver.run_batch(SolverConfig(variant=Variant.gbsb, **kw), t, 2, master_seed=1)
+    solver.set_state(np.zeros((2, 8), np.float32), np.zeros((2, 8), np.float32))
+    with pytest.raises(ValueError):
+        solver.advance(SolverConfig(variant=Variant.gbsb, steps=10, dt=0.5, c=0.1), 5, 11)  # past M
