@@ -75,6 +75,7 @@ struct sbg_ctx {
   unsigned long long* dE2 = nullptr;
   long long* dBest = nullptr;
   CUtensorMap tmG_sign[2], tmG_planes[2], tmSign;
+  TmaMaps maps_sign[2], maps_planes[2];  // TMA-staged step kernel, per current B buffer
   int g_cur = 0;
   int g_mode = 0;  // 0 stale, 1 sign plane valid in dG[g_cur], 4 planes valid
   cudaEvent_t ev[8];
@@ -119,6 +120,22 @@ int encode_2d_u8(sbg_ctx* ctx, CUtensorMap* tm, const void* base, uint64_t inner
   return SBG_OK;
 }
 
+int encode_2d(sbg_ctx* ctx, CUtensorMap* tm, CUtensorMapDataType dt, uint32_t esize, const void* base,
+              uint64_t inner, uint64_t rows, uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_rows,
+              CUtensorMapSwizzle swz) {
+  auto enc = get_encode();
+  if (!enc) return ctx->fail(SBG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {row_pitch_bytes};
+  cuuint32_t box[2] = {box_inner, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  (void)esize;
+  CUresult r = enc(tm, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return ctx->fail(SBG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  return SBG_OK;
+}
+
 int grid_for(const sbg_ctx* ctx, size_t work, int threads) {
   const size_t blocks = (work + threads - 1) / threads;
   return static_cast<int>(std::min<size_t>(std::max<size_t>(blocks, 1), size_t(ctx->sms) * 8));
@@ -132,6 +149,19 @@ int launch_step(sbg_ctx* ctx, const CUtensorMap& tmG, const StepArgs& a) {
   const int tiles = a.num_m * a.num_n;
   const int grid = std::min(tiles, ctx->sms);
   kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(ctx->tmJ, tmG, a);
+  CK(cudaGetLastError());
+  ++ctx->launches;
+  return SBG_OK;
+}
+
+template <int NP, int BN>
+int launch_step_tma(sbg_ctx* ctx, const TmaMaps& maps, const StepArgs& a) {
+  using Cfg = TmaStepCfg<NP, BN>;
+  auto kern = gsb_step_tma_kernel<NP, BN>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  const int tiles = a.num_m * a.num_n;
+  const int grid = std::min(tiles, ctx->sms);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(maps, a);
   CK(cudaGetLastError());
   ++ctx->launches;
   return SBG_OK;
@@ -189,6 +219,26 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
   ctx->R = R;
   ctx->rpad = rpad;
   ctx->g_mode = 0;
+  if (ctx->kind == KIND_DENSE_I8) {
+    constexpr int CW = TmaStepCfg<1, BN_SIGN>::CW;
+    for (int b = 0; b < 2; ++b) {
+      for (TmaMaps* mp : {&ctx->maps_sign[b], &ctx->maps_planes[b]}) {
+        const bool planes = mp == &ctx->maps_planes[b];
+        mp->J = ctx->tmJ;
+        mp->Gin = planes ? ctx->tmG_planes[b] : ctx->tmG_sign[b];
+        int rc = encode_2d(ctx, &mp->Gout, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[b ^ 1], ctx->n,
+                           planes ? NPL * rpad : R, ctx->npad, 128, CW, CU_TENSOR_MAP_SWIZZLE_NONE);
+        if (rc) return rc;
+        float* arrs[3] = {ctx->dX, ctx->dY, ctx->dP};
+        CUtensorMap* outs[3] = {&mp->X, &mp->Y, &mp->P};
+        for (int a = 0; a < 3; ++a) {
+          rc = encode_2d(ctx, outs[a], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, arrs[a], ctx->n, R,
+                         sizeof(float) * ctx->npad, 128, CW, CU_TENSOR_MAP_SWIZZLE_NONE);
+          if (rc) return rc;
+        }
+      }
+    }
+  }
   const size_t st = sizeof(float) * size_t(rpad) * ctx->npad;
   CK(cudaMemsetAsync(ctx->dX, 0, st, ctx->stream));
   CK(cudaMemsetAsync(ctx->dY, 0, st, ctx->stream));
@@ -477,8 +527,8 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
       a.m_dev = nullptr;
       a.m_off = int64_t(m);
       a.M = prm->steps;
-      rc = sign ? launch_step<1, BN_SIGN, EpiMode::Step>(ctx, ctx->tmG_sign[cur], a)
-                : launch_step<NPL, BN_PLANE, EpiMode::Step>(ctx, ctx->tmG_planes[cur], a);
+      rc = sign ? launch_step_tma<1, BN_SIGN>(ctx, ctx->maps_sign[cur], a)
+                : launch_step_tma<NPL, BN_PLANE>(ctx, ctx->maps_planes[cur], a);
       if (rc) return rc;
       ctx->g_cur = cur ^ 1;
     }
