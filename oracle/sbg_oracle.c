@@ -292,13 +292,13 @@ void orc_step_f64(int variant, int64_t n, const double* J, double* x, double* y,
 
 /* ------------------------------------------------------- fp32 GPU mirror */
 
-void orc_phase_f32(float F, float* xp, float* yp, float* pp, float a, float c, float dt, float denom) {
+void orc_phase_f32(float F, float* xp, float* yp, float* pp, float a, float c, float dt, float inv) {
   /* engine.cpp:86-103 in the exact fp32 op order of the CUDA epilogue
    * (paper_2508_17655_b200/csrc/gsb_phase.cuh). No contraction. */
   const float x = *xp, y = *yp, p = *pp;
   const float ax2 = (a * x) * x;
   const float gmul = 1.0f - ax2;
-  const float pn = p - (gmul * p) / denom;
+  const float pn = p - (gmul * p) * inv; /* inv = RN(1/(M-m)), see step_f32_impl */
   const float t = pn * x - c * F;
   float yn = y - t * dt;
   float xn = x + yn * dt;
@@ -370,14 +370,14 @@ static void step_f32_impl(int variant, int64_t n, const int8_t* J, const int32_t
                           const int32_t* col, const int8_t* val, int64_t R, int64_t ld, float* x,
                           float* y, float* p, uint64_t m, uint64_t M, float dt, float c, float a_cfg) {
   const float a = honours_a(variant) ? a_cfg : 0.0f;
-  const float denom = (float)(M - m);
+  const float inv = 1.0f / (float)(M - m); /* correctly rounded, == __frcp_rn on the GPU */
   float* F = (float*)malloc(sizeof(float) * (size_t)n);
   int8_t* s = (int8_t*)malloc((size_t)n);
   int32_t* q = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
   for (int64_t r = 0; r < R; ++r) {
     float* xr = x + r * ld;
     fields_for(variant, n, J, rowptr, col, val, xr, F, s, q);
-    for (int64_t i = 0; i < n; ++i) orc_phase_f32(F[i], xr + i, y + r * ld + i, p + r * ld + i, a, c, dt, denom);
+    for (int64_t i = 0; i < n; ++i) orc_phase_f32(F[i], xr + i, y + r * ld + i, p + r * ld + i, a, c, dt, inv);
   }
   free(F);
   free(s);

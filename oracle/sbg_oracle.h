@@ -80,7 +80,7 @@ void orc_step_f32_csr(int variant, int64_t n, const int32_t* rowptr, const int32
                       const int8_t* val, int64_t R, int64_t ld, float* x, float* y, float* p,
                       uint64_t m, uint64_t M, float dt, float c, float a);
 /* The elementwise phase alone (engine.cpp:86-103 in fp32, GPU op order). */
-void orc_phase_f32(float F, float* x, float* y, float* p, float a, float c, float dt, float denom);
+void orc_phase_f32(float F, float* x, float* y, float* p, float a, float c, float dt, float inv);
 
 /* ---- readout ---------------------------------------------------------- */
 /* E2[r] = sum_i s_i (J s)_i with s = sgn(x) (sgn(0)=+1, model.cpp:161-165);

@@ -104,7 +104,7 @@ inline int csr_rpb(int32_t n) { return (2 * sizeof(float) * size_t(n) <= 200 * 1
 inline int launch_csr_step(cudaStream_t st, int sms, int32_t n, const int32_t* rowptr, const int32_t* col,
                            const int8_t* val, float* x, float* y, float* p, int64_t ld, int32_t R, bool sign,
                            PhaseConsts k, uint64_t M, uint64_t m) {
-  k.denom = static_cast<float>(M - m);
+  k.inv = 1.0f / static_cast<float>(M - m);  // host: IEEE division == __frcp_rn
   const int rpb = csr_rpb(n);
   const size_t smem = sizeof(float) * size_t(n) * rpb;
   if (smem > 227 * 1024) return int(cudaErrorInvalidValue);

@@ -2,6 +2,8 @@
 //
 // Semantics: sbopt::step, /root/reference/proj/core/src/engine.cpp:86-103
 //   p <- p - (1 - a x^2) p / (M - m)          (Eq. 7; a = 0 for bsb/dsb, :64)
+//        computed as p - ((1 - a x^2) p) * inv, inv = RN(1 / (M - m)) (one
+//        correctly rounded reciprocal per step instead of a per-spin divide)
 //   y <- y - (p x - c F) dt
 //   x <- x + y dt
 //   |x| > 1  ->  x = sgn(x), y = 0            (strict walls, :93-99)
@@ -19,13 +21,13 @@ struct PhaseConsts {
   float a;      // nonlinear control strength A (0 for bsb/dsb)
   float c;      // coupling scale
   float dt;     // time step
-  float denom;  // (float)(M - m)
+  float inv;    // RN(1 / (float)(M - m))
 };
 
 __device__ __forceinline__ void gsb_phase(float F, float& x, float& y, float& p, const PhaseConsts& k) {
   const float ax2 = __fmul_rn(__fmul_rn(k.a, x), x);
   const float g = __fsub_rn(1.0f, ax2);
-  const float pn = __fsub_rn(p, __fdiv_rn(__fmul_rn(g, p), k.denom));
+  const float pn = __fsub_rn(p, __fmul_rn(__fmul_rn(g, p), k.inv));
   const float t = __fsub_rn(__fmul_rn(pn, x), __fmul_rn(k.c, F));
   float yn = __fsub_rn(y, __fmul_rn(t, k.dt));
   float xn = __fadd_rn(x, __fmul_rn(yn, k.dt));

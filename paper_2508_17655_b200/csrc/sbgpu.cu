@@ -21,6 +21,7 @@
 #include "aux_kernels.cuh"
 #include "csr_step.cuh"
 #include "step_i8.cuh"
+#include "step_tma.cuh"
 
 using namespace sbg;
 
@@ -75,7 +76,8 @@ struct sbg_ctx {
   unsigned long long* dE2 = nullptr;
   long long* dBest = nullptr;
   CUtensorMap tmG_sign[2], tmG_planes[2], tmSign;
-  TmaMaps maps_sign[2], maps_planes[2];  // TMA-staged step kernel, per current B buffer
+  TmaMaps maps_sign[2], maps_planes[2];  // multi-step kernel maps, indexed by the current B buffer
+  uint32_t* d_done = nullptr;            // per replica-block tile counters of the multi-step kernel
   int g_cur = 0;
   int g_mode = 0;  // 0 stale, 1 sign plane valid in dG[g_cur], 4 planes valid
   cudaEvent_t ev[8];
@@ -154,13 +156,26 @@ int launch_step(sbg_ctx* ctx, const CUtensorMap& tmG, const StepArgs& a) {
   return SBG_OK;
 }
 
-template <int NP, int BN>
-int launch_step_tma(sbg_ctx* ctx, const TmaMaps& maps, const StepArgs& a) {
-  using Cfg = TmaStepCfg<NP, BN>;
-  auto kern = gsb_step_tma_kernel<NP, BN>;
+// Multi-step persistent launch (step_tma.cuh). Sign variants: BN 128, 4 operand
+// stages, 3 state buffers; fixed-point planes: BN 64, 3 stages, 2 buffers
+// (best of the measured (stages, buffers) sweeps on B200).
+constexpr int SIGN_STAGES = 4, SIGN_NBUF = 3;
+constexpr int PLANE_STAGES = 3, PLANE_NBUF = 2;
+
+int dev_knob(const char* name) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : 0;
+}
+
+template <int NP, int BN, int ST, int NB>
+int launch_multistep(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& a) {
+  using Cfg = TmaStepCfg<NP, BN, ST, NB>;
+  auto kern = gsb_multistep_kernel<NP, BN, ST, NB>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
-  const int tiles = a.num_m * a.num_n;
-  const int grid = std::min(tiles, ctx->sms);
+  const int64_t tiles = int64_t(a.num_m) * a.num_n * a.nsteps;
+  // persistent: one CTA per SM (all must be co-resident for the dependency walk)
+  const int grid = int(std::min<int64_t>(tiles, ctx->sms));
+  CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * a.num_n, ctx->stream));
   kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(maps, a);
   CK(cudaGetLastError());
   ++ctx->launches;
@@ -176,6 +191,8 @@ void free_state(sbg_ctx* ctx) {
   cudaFree(ctx->dSign);
   cudaFree(ctx->dE2);
   cudaFree(ctx->dBest);
+  cudaFree(ctx->d_done);
+  ctx->d_done = nullptr;
   ctx->dX = ctx->dY = ctx->dP = nullptr;
   ctx->dG[0] = ctx->dG[1] = ctx->dSign = nullptr;
   ctx->dE2 = nullptr;
@@ -201,6 +218,7 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
     CK(cudaMalloc(&ctx->dSign, pl));
     CK(cudaMalloc(&ctx->dE2, sizeof(unsigned long long) * rpad));
     CK(cudaMalloc(&ctx->dBest, 2 * sizeof(long long)));
+    CK(cudaMalloc(&ctx->d_done, sizeof(uint32_t) * (rpad / 16 + 1)));
     CK(cudaMemsetAsync(ctx->dG[0], 0, NPL * pl, ctx->stream));
     CK(cudaMemsetAsync(ctx->dG[1], 0, NPL * pl, ctx->stream));
     CK(cudaMemsetAsync(ctx->dSign, 0, pl, ctx->stream));
@@ -220,22 +238,37 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
   ctx->rpad = rpad;
   ctx->g_mode = 0;
   if (ctx->kind == KIND_DENSE_I8) {
-    constexpr int CW = TmaStepCfg<1, BN_SIGN>::CW;
+    constexpr int CW = TmaStepCfg<1, BN_SIGN, SIGN_STAGES, SIGN_NBUF>::CW;
+    // Per B buffer b: output maps (the next step's B operand lands in the other buffer).
+    CUtensorMap gout_sign[2], gout_planes[2];
     for (int b = 0; b < 2; ++b) {
-      for (TmaMaps* mp : {&ctx->maps_sign[b], &ctx->maps_planes[b]}) {
-        const bool planes = mp == &ctx->maps_planes[b];
-        mp->J = ctx->tmJ;
-        mp->Gin = planes ? ctx->tmG_planes[b] : ctx->tmG_sign[b];
-        int rc = encode_2d(ctx, &mp->Gout, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[b ^ 1], ctx->n,
-                           planes ? NPL * rpad : R, ctx->npad, 128, CW, CU_TENSOR_MAP_SWIZZLE_NONE);
-        if (rc) return rc;
-        float* arrs[3] = {ctx->dX, ctx->dY, ctx->dP};
-        CUtensorMap* outs[3] = {&mp->X, &mp->Y, &mp->P};
-        for (int a = 0; a < 3; ++a) {
-          rc = encode_2d(ctx, outs[a], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, arrs[a], ctx->n, R,
+      int rc = encode_2d(ctx, &gout_sign[b], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[b], ctx->n, R, ctx->npad, 128,
+                         CW, CU_TENSOR_MAP_SWIZZLE_NONE);
+      if (rc) return rc;
+      rc = encode_2d(ctx, &gout_planes[b], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[b], ctx->n, NPL * rpad,
+                     ctx->npad, 128, CW, CU_TENSOR_MAP_SWIZZLE_NONE);
+      if (rc) return rc;
+    }
+    CUtensorMap X, Y, P;
+    float* arrs[3] = {ctx->dX, ctx->dY, ctx->dP};
+    CUtensorMap* outs[3] = {&X, &Y, &P};
+    for (int a = 0; a < 3; ++a) {
+      int rc = encode_2d(ctx, outs[a], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, arrs[a], ctx->n, R,
                          sizeof(float) * ctx->npad, 128, CW, CU_TENSOR_MAP_SWIZZLE_NONE);
-          if (rc) return rc;
-        }
+      if (rc) return rc;
+    }
+    for (int cur = 0; cur < 2; ++cur) {
+      for (int planes = 0; planes < 2; ++planes) {
+        TmaMaps& mp = planes ? ctx->maps_planes[cur] : ctx->maps_sign[cur];
+        mp.J = ctx->tmJ;
+        // step parity 0 reads buffer cur and writes cur^1; parity 1 the reverse
+        mp.Gin[0] = planes ? ctx->tmG_planes[cur] : ctx->tmG_sign[cur];
+        mp.Gin[1] = planes ? ctx->tmG_planes[cur ^ 1] : ctx->tmG_sign[cur ^ 1];
+        mp.Gout[0] = planes ? gout_planes[cur ^ 1] : gout_sign[cur ^ 1];
+        mp.Gout[1] = planes ? gout_planes[cur] : gout_sign[cur];
+        mp.X = X;
+        mp.Y = Y;
+        mp.P = P;
       }
     }
   }
@@ -500,7 +533,7 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
   k.a = honours_a ? float(prm->a) : 0.0f;
   k.c = float(prm->c);
   k.dt = float(prm->dt);
-  k.denom = 0.0f;
+  k.inv = 0.0f;
   CK(cudaEventRecord(ctx->ev[0], ctx->stream));
   if (ctx->kind == KIND_CSR_I8) {
     for (uint64_t m = m_begin; m < m_end; ++m) {
@@ -516,21 +549,41 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
       if (rc) return rc;
       ctx->g_mode = need;
     }
-    for (uint64_t m = m_begin; m < m_end; ++m) {
-      const int cur = ctx->g_cur;
-      StepArgs a = base_args(ctx, sign ? BN_SIGN : BN_PLANE, ctx->R, ctx->rpad);
-      a.x = ctx->dX;
-      a.y = ctx->dY;
-      a.p = ctx->dP;
-      a.planes_next = ctx->dG[cur ^ 1];
+    const int64_t T = (ctx->npad / 128) * (ctx->rpad / (sign ? BN_SIGN : BN_PLANE));
+    const int64_t max_steps = std::max<int64_t>(1, (int64_t(1) << 30) / T);
+    const bool per_step = dev_knob("SBG_PER_STEP_LAUNCH") != 0;
+    for (uint64_t m = m_begin; m < m_end;) {
+      const int64_t ns = per_step ? 1 : std::min<int64_t>(int64_t(m_end - m), max_steps);
+      MultiStepArgs a;
+      std::memset(&a, 0, sizeof a);
+      a.n = int32_t(ctx->n);
+      a.npad = int32_t(ctx->npad);
+      a.R = int32_t(ctx->R);
+      a.rpad = int32_t(ctx->rpad);
+      a.num_m = int32_t(ctx->npad / 128);
+      a.num_n = int32_t(ctx->rpad / (sign ? BN_SIGN : BN_PLANE));
       a.k = k;
-      a.m_dev = nullptr;
-      a.m_off = int64_t(m);
       a.M = prm->steps;
-      rc = sign ? launch_step_tma<1, BN_SIGN>(ctx, ctx->maps_sign[cur], a)
-                : launch_step_tma<NPL, BN_PLANE>(ctx, ctx->maps_planes[cur], a);
+      a.t_begin = m;
+      a.nsteps = int32_t(ns);
+      a.done = ctx->d_done;
+      a.dbg = dev_knob("SBG_STEP_DBG");
+      const int cur = ctx->g_cur;
+      if (sign) {
+        switch (dev_knob("SBG_STEP_CFG")) {  // dev sweep of (operand stages, state buffers)
+          case 1: rc = launch_multistep<1, BN_SIGN, 3, 4>(ctx, ctx->maps_sign[cur], a); break;
+          case 2: rc = launch_multistep<1, BN_SIGN, 2, 5>(ctx, ctx->maps_sign[cur], a); break;
+          default: rc = launch_multistep<1, BN_SIGN, SIGN_STAGES, SIGN_NBUF>(ctx, ctx->maps_sign[cur], a);
+        }
+      } else {
+        switch (dev_knob("SBG_STEP_CFG")) {
+          case 1: rc = launch_multistep<NPL, BN_PLANE, 2, 4>(ctx, ctx->maps_planes[cur], a); break;
+          default: rc = launch_multistep<NPL, BN_PLANE, PLANE_STAGES, PLANE_NBUF>(ctx, ctx->maps_planes[cur], a);
+        }
+      }
       if (rc) return rc;
-      ctx->g_cur = cur ^ 1;
+      ctx->g_cur = cur ^ int(ns & 1);
+      m += uint64_t(ns);
     }
   }
   CK(cudaEventRecord(ctx->ev[1], ctx->stream));
