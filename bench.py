@@ -32,7 +32,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 N_SPINS = 2000
-R_TOTAL = 8192
+R_PER_GPU = 8192
+TTS_POOL = 8
 M_SCHED = 1000
 A_CTRL = 0.2
 DT = 1.25
@@ -159,10 +160,11 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "spin-updates/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(walls),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded gen_random_dense instance, BASELINE U(-0.1,0.1) init)",
-        "config": {"workload": "C2: N=2000 dense +-1, R=8192 (reference timed on a bounded replica sample)",
-                   "n": N_SPINS, "replicas": R_TOTAL, "M": M_SCHED, "A": A_CTRL, "dt": DT},
+        "config": {"workload": "C2 (BASELINE configs[1]): N=2000 dense +-1, GdSB, R=8192 replicas per GPU "
+                               "(reference timed on a bounded replica sample on rank 0's host)",
+                   "n": N_SPINS, "replicas_per_gpu": R_PER_GPU, "M": M_SCHED, "A": A_CTRL, "dt": DT},
         "cpu_baseline": {"value": value, "unit": "spin-updates/s", "cores": threads, "kind": "reference",
                          "sample": sample, "host": oracle.host_description()},
         "e2e": {"value": value, "unit": "spin-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -181,55 +183,45 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2508_17655_b200 import InitMode, Solver, SolverConfig, TuningResult, Variant
 
-    if R_TOTAL % world:
-        raise SystemExit("R must divide evenly over the ranks")
-    R = R_TOTAL // world
+    # Weak scaling over replicas: every rank owns R_PER_GPU whole
+    # replicas with global indices rank*R .. rank*R+R-1 (seeds do not depend on
+    # the rank count); no data-path collective.
+    R = R_PER_GPU
     r0 = rank * R
+    R_all = R * world
     c = 1.0 / (2.0 * math.sqrt(N_SPINS))
     cfg = SolverConfig(variant=Variant.gdsb, steps=M_SCHED, dt=DT, c=c, a=A_CTRL, init_mode=InitMode.small_uniform)
     s = Solver(local)
     s.gen_random_dense(N_SPINS, INSTANCE_SEED)
     s.init_state(R, InitMode.small_uniform, MASTER, INIT_TAG, offset=r0)
     state_bytes = 12 * N_SPINS * R
-    flush = state_bytes < 1.5 * L2_BYTES  # state could largely sit in L2: flush between timed steps
-    flush_buf = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda") if flush else None
+    assert state_bytes > L2_BYTES, "per-GPU state must exceed L2 (timing protocol)"
 
     def barrier():
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
 
-    # warm-up (also builds the B operand once)
-    m = 0
-    s.advance(cfg, m, m + args.warmup)
-    m += args.warmup
+    # warm-up steps (own launch; also builds the B operand once)
+    s.advance(cfg, 0, args.warmup)
     s.synchronize()
     launches0 = s.kernel_launches
     barrier()
     with ClockSampler(local) as clk:
-        if not flush:
-            s.advance(cfg, m, m + args.steps)
-            dev_ms = s.last_advance_ms()
-        else:
-            dev_ms = 0.0
-            for k in range(args.steps):
-                flush_buf.zero_()
-                torch.cuda.synchronize()
-                s.advance(cfg, m + k, m + k + 1)
-                dev_ms += s.last_advance_ms()
+        s.advance(cfg, args.warmup, args.warmup + args.steps)  # K steps, persistent multi-step kernel
+        dev_ms = s.last_advance_ms()
         s.synchronize()
     barrier()
-    m += args.steps
     launches = s.kernel_launches - launches0
     if world > 1:
         t = torch.tensor([dev_ms], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         dev_ms = float(t.item())
-    su_total = N_SPINS * R_TOTAL * args.steps
+    su_total = N_SPINS * R_all * args.steps
     value = su_total / (dev_ms / 1e3)
     ms_per_step = dev_ms / args.steps
 
-    # ---- end to end through the public API: host (pinned) x0,y0 -> run() -> spins/energies on host
+    # ---- end to end through the public API: pinned host x0,y0 -> run() -> spins/energies on host
     x0h, y0h = init_host_states(local, R, r0)
     e2e_steps = args.steps
     cfg_e2e = SolverConfig(variant=Variant.gdsb, steps=e2e_steps, dt=DT, c=c, a=A_CTRL)
@@ -244,9 +236,13 @@ def run_ours(args):
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_val = N_SPINS * R_TOTAL * e2e_steps / e2e_s
+    e2e_val = N_SPINS * R_all * e2e_steps / e2e_s
     h2d = 2 * 4 * N_SPINS * R  # x0, y0 fp32
     d2h = N_SPINS * R + 8 * R + 8  # spins int8 + energies + best index
+
+    tts = None
+    if world == 1 and not args.no_tts:
+        tts = measure_tts(s, local)
 
     if rank != 0:
         s.close()
@@ -254,41 +250,44 @@ def run_ours(args):
             torch.distributed.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (the step kernel; one launch per step)
+    # ---- roofline of the dominant (only) kernel of the timed region
     hbm_peak, peak_src = peaks()
-    bytes_per_launch = 24 * N_SPINS * R + N_SPINS * N_SPINS  # 24 B/SU state + J (int8) once
-    achieved = bytes_per_launch / (ms_per_step / 1e3) / 1e9
+    bytes_per_step = 24 * N_SPINS * R + N_SPINS * N_SPINS  # 24 B/SU state + J (int8) once
+    achieved = bytes_per_step / (ms_per_step / 1e3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "step_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(f"R{R}")
+            traffic = json.load(open(tpath)).get("gdsb_n2000_R8192_bytes_per_step")
         except Exception:
             traffic = None
-    ops_per_launch = 2 * N_SPINS * N_SPINS * R
+    ops_per_step = 2 * N_SPINS * N_SPINS * R
 
     line = {
         "metric": METRIC, "value": value, "unit": "spin-updates/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "i8 field (tcgen05 kind::i8, s32 acc) / f32 state",
         "data": "synthetic (seeded gen_random_dense N=2000 instance; x0,y0~U(-0.1,0.1) from derive_seed(1,{7,r}))",
-        "config": {"workload": "C2 (BASELINE configs[1]): N=2000 dense +-1, GdSB, R=8192 sharded over ranks",
-                   "n": N_SPINS, "replicas": R_TOTAL, "replicas_per_gpu": R, "M": M_SCHED, "A": A_CTRL,
-                   "dt": DT, "c": c, "parallelism": f"replicas/{world}",
-                   "l2": ("flushed (256 MB write) between timed steps" if flush else
-                          f"state {state_bytes / 2**20:.0f} MB per GPU > 126 MB L2 (inputs larger than L2)")},
+        "config": {"workload": "C2 (BASELINE configs[1]): N=2000 dense +-1, GdSB, R=8192 replicas per GPU",
+                   "n": N_SPINS, "replicas_per_gpu": R, "replicas_total": R_all, "M": M_SCHED, "A": A_CTRL,
+                   "dt": DT, "c": c, "parallelism": f"replica-sharded x{world} (no collective)",
+                   "timed": f"{args.steps} steps in one persistent multi-step launch, CUDA events, max over ranks",
+                   "l2": f"inputs larger than L2: state {state_bytes / 2**20:.0f} MiB per GPU > 126 MB L2"},
         "e2e": {"value": e2e_val, "unit": "spin-updates/s", "h2d_bytes_per_step": h2d / e2e_steps,
                 "d2h_bytes_per_step": d2h / e2e_steps,
-                "note": f"one run() of M={e2e_steps} steps per call: H2D x0,y0 from pinned host, M steps, "
+                "note": f"one sbg_run() of M={e2e_steps} steps per rank: H2D x0,y0 from pinned host, M steps, "
                         "readout (energy+argmin), D2H spins/energies; wall clock, max over ranks",
                 "device_breakdown_ms": b.timing},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bytes_per_launch,
-                     "tensor_tops": ops_per_launch / (ms_per_step / 1e3) / 1e12},
+                     "algorithmic_bytes_per_step": bytes_per_step,
+                     "kernel": "gsb_multistep_kernel<1,128,4,3> (all timed steps in one launch)",
+                     "tensor_tops": ops_per_step / (ms_per_step / 1e3) / 1e12},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    if tts is not None:
+        line["tts99"] = tts
     if world == 1 and not args.no_cpu_baseline:
         import oracle
 
@@ -301,6 +300,41 @@ def run_ours(args):
                                 "sample": sample, "host": oracle.host_description()}
     print(json.dumps(line), flush=True)
     s.close()
+
+
+def measure_tts(s, device):
+    """TTS99 on the N=2000 dense +-1 instance, paper K2000 settings:
+    GbSB, M=21500, A=0.2, dt=1.25, c=1/(2 sqrt N), R=1000 replicas per batch (C1 shape),
+    reference init (x~U(-1,1), y=0; batch_best_of seeds). Target = best cut over TTS_POOL
+    batches (the K2000 file is absent). P_S from a fresh batch; TTS via the
+    reference's time_to_solution formula (bench.cpp:52-68)."""
+    from paper_2508_17655_b200 import (InitMode, SolverConfig, TuningResult, Variant, success_probability,
+                                       time_to_solution)
+
+    c = 1.0 / (2.0 * math.sqrt(N_SPINS))
+    cfg = SolverConfig(variant=Variant.gbsb, steps=21500, dt=DT, c=c, a=A_CTRL, init_mode=InitMode.uniform_random)
+    tun = TuningResult(c=c, dt=DT)
+    pool = []
+    for k in range(TTS_POOL):
+        b = s.run_batch(cfg, tun, 1000, master_seed=1000 + k)
+        pool.append(b.energies.min())
+    target_e = float(min(pool))
+    t0 = time.perf_counter()
+    b = s.run_batch(cfg, tun, 1000, master_seed=999)
+    t_batch = time.perf_counter() - t0
+    st = success_probability(b.energies, target_e)
+    out = {"variant": "gbsb", "M": 21500, "A": A_CTRL, "replicas_per_batch": 1000,
+           "target_energy": target_e, "target": f"best energy over {TTS_POOL} GPU batches x 1000 runs",
+           "p_s": st.p_s, "delta_p_s": st.delta_p_s, "t_batch_s": t_batch,
+           "device_ms_batch": b.timing["total_ms"]}
+    if st.p_s > 0:
+        run = time_to_solution(t_batch, st)
+        amort = time_to_solution(t_batch / 1000, st)
+        out.update({"tts99_run_ms": run.tts_s * 1e3, "delta_tts99_run_ms": run.delta_tts_s * 1e3,
+                    "tts99_amortised_ms": amort.tts_s * 1e3})
+    else:
+        out["tts99_run_ms"] = None
+    return out
 
 
 def init_host_states(device: int, R: int, r0: int):
@@ -327,6 +361,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tts", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
