@@ -22,6 +22,7 @@
 #include "csr_step.cuh"
 #include "step_i8.cuh"
 #include "step_tma.cuh"
+#include "step_pair.cuh"
 
 using namespace sbg;
 
@@ -30,8 +31,10 @@ namespace {
 constexpr int BN_SIGN = 128;   // replica tile, sign variants (dsb/gdsb)
 constexpr int BN_PLANE = 64;   // replica tile, fixed-point variants (bsb/gbsb)
 constexpr int NPL = 4;         // fixed-point byte planes
-constexpr int PAD_N = 128;     // spin padding (MMA M and K granularity)
-constexpr int PAD_R = 128;     // replica padding (multiple of both BNs)
+constexpr int PAD_N = 256;     // spin padding (pair MMA M = 256, K granularity 128)
+constexpr int PAD_R = 256;     // replica padding (multiple of every replica tile)
+constexpr int NPAIR_SIGN = 256;   // replicas per pair tile, sign variants
+constexpr int NPAIR_PLANE = 64;   // replicas per pair tile, fixed-point variants
 
 enum Kind { KIND_NONE = 0, KIND_DENSE_I8 = 1, KIND_CSR_I8 = 2 };
 
@@ -77,6 +80,7 @@ struct sbg_ctx {
   long long* dBest = nullptr;
   CUtensorMap tmG_sign[2], tmG_planes[2], tmSign;
   TmaMaps maps_sign[2], maps_planes[2];  // multi-step kernel maps, indexed by the current B buffer
+  TmaMaps pmaps_planes[2];               // pair kernel, fixed-point planes (B half = 32 rows)
   uint32_t* d_done = nullptr;            // per replica-block tile counters of the multi-step kernel
   int g_cur = 0;
   int g_mode = 0;  // 0 stale, 1 sign plane valid in dG[g_cur], 4 planes valid
@@ -182,6 +186,21 @@ int launch_multistep(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& a) 
   return SBG_OK;
 }
 
+template <int NP, int NPAIR, int ST, int NB>
+int launch_multistep_pair(sbg_ctx* ctx, const TmaMaps& maps, MultiStepArgs a) {
+  using Cfg = PairStepCfg<NP, NPAIR, ST, NB>;
+  auto kern = gsb_multistep_pair_kernel<NP, NPAIR, ST, NB>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  a.num_n = int32_t(ctx->rpad / NPAIR);
+  const int64_t pair_tiles = int64_t(a.num_m / 2) * a.num_n * a.nsteps;
+  const int grid = 2 * int(std::min<int64_t>(pair_tiles, ctx->sms / 2));
+  CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * a.num_n, ctx->stream));
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(maps, a);
+  CK(cudaGetLastError());
+  ++ctx->launches;
+  return SBG_OK;
+}
+
 void free_state(sbg_ctx* ctx) {
   cudaFree(ctx->dX);
   cudaFree(ctx->dY);
@@ -269,6 +288,12 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
         mp.X = X;
         mp.Y = Y;
         mp.P = P;
+      }
+      ctx->pmaps_planes[cur] = ctx->maps_planes[cur];
+      for (int par = 0; par < 2; ++par) {
+        int rc = encode_2d_u8(ctx, &ctx->pmaps_planes[cur].Gin[par], ctx->dG[cur ^ par], ctx->npad, NPL * rpad, 128,
+                              NPAIR_PLANE / 2);
+        if (rc) return rc;
       }
     }
   }
@@ -569,15 +594,23 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
       a.done = ctx->d_done;
       a.dbg = dev_knob("SBG_STEP_DBG");
       const int cur = ctx->g_cur;
+      // Defaults (measured on B200, tools/step_driver.py): sign variants on CTA pairs
+      // (3 operand stages, 4 state buffers): 73 us/step at N=2000, R=8192, vs 83 us
+      // single-CTA; fixed-point planes single-CTA (3, 2): 18.5 us/step at R=1024 vs
+      // 20.4 us on pairs. SBG_STEP_CFG selects sweep alternatives (dev only).
+      const int knob = dev_knob("SBG_STEP_CFG");
+      const bool pair_ok = (ctx->npad % 256) == 0;
       if (sign) {
-        switch (dev_knob("SBG_STEP_CFG")) {  // dev sweep of (operand stages, state buffers)
-          case 1: rc = launch_multistep<1, BN_SIGN, 3, 4>(ctx, ctx->maps_sign[cur], a); break;
-          case 2: rc = launch_multistep<1, BN_SIGN, 2, 5>(ctx, ctx->maps_sign[cur], a); break;
-          default: rc = launch_multistep<1, BN_SIGN, SIGN_STAGES, SIGN_NBUF>(ctx, ctx->maps_sign[cur], a);
+        switch (pair_ok ? knob : -1) {
+          case -1: rc = launch_multistep<1, BN_SIGN, SIGN_STAGES, SIGN_NBUF>(ctx, ctx->maps_sign[cur], a); break;
+          case 2: rc = launch_multistep_pair<1, NPAIR_SIGN, 2, 6>(ctx, ctx->maps_sign[cur], a); break;
+          case 3: rc = launch_multistep_pair<1, NPAIR_SIGN, 4, 3>(ctx, ctx->maps_sign[cur], a); break;
+          default: rc = launch_multistep_pair<1, NPAIR_SIGN, 3, 4>(ctx, ctx->maps_sign[cur], a);
         }
       } else {
-        switch (dev_knob("SBG_STEP_CFG")) {
-          case 1: rc = launch_multistep<NPL, BN_PLANE, 2, 4>(ctx, ctx->maps_planes[cur], a); break;
+        switch (pair_ok ? knob : -1) {
+          case 2: rc = launch_multistep_pair<NPL, NPAIR_PLANE, 3, 3>(ctx, ctx->pmaps_planes[cur], a); break;
+          case 3: rc = launch_multistep_pair<NPL, NPAIR_PLANE, 4, 2>(ctx, ctx->pmaps_planes[cur], a); break;
           default: rc = launch_multistep<NPL, BN_PLANE, PLANE_STAGES, PLANE_NBUF>(ctx, ctx->maps_planes[cur], a);
         }
       }

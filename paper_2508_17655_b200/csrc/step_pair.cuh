@@ -1,0 +1,324 @@
+// The hot path on CTA pairs: the multi-step dataflow kernel of step_tma.cuh
+// with the field contraction issued as tcgen05.mma.cta_group::2 (M = 256 spins
+// across the two SMs of a cluster).
+//
+// Why pairs: per step every replica block re-reads J and every spin block
+// re-reads G, so operand bytes per output element are (1/BN + 1/BM). With a
+// pair, each CTA stages only its own 128 rows of J and HALF of the B tile, yet
+// its TMEM receives a full 128 x N accumulator: operand bytes per output halve
+// compared with one CTA, which frees the shared memory the state stream needs
+// (a deeper x/y/p ring), and that stream is what bounds the step (SURVEY 8(d):
+// 24 B of state per spin-update vs one int8 op pair per J entry).
+//
+// Protocol (leader = cluster rank 0):
+//   full[s]   leader only, count 2: each CTA's producer arrive.expect_tx(own bytes)
+//             on the leader's barrier; each CTA's TMA completes tx there (cta_group::2).
+//   empty[s]  both CTAs, count 1: the leader's tcgen05.commit multicasts to both.
+//   tfull[b]  both CTAs, count 1: multicast commit after the last K-stage of a tile.
+//   tempty[b] leader only, count 2*EPI_WARPS: each epilogue warp of both CTAs
+//             arrives (the peer's remotely) when its TMEM reads are done.
+//   state ring barriers and done[] counters: per CTA, exactly as step_tma.cuh.
+// Tile = (step s, replica block n of N_PAIR, spin pair-block mp of 256); CTA rank
+// cr owns spins (2 mp + cr)*128 .. +127 and stages B rows n*N_PAIR + cr*N_PAIR/2.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+
+#include "gsb_phase.cuh"
+#include "ptx.cuh"
+#include "step_tma.cuh"
+
+namespace sbg {
+
+template <int NPLANES, int N_PAIR, int STAGES_, int NBUF_>
+struct PairStepCfg {
+  static constexpr int BM = 128;                        // spins per CTA
+  static constexpr int BK = 128;                        // K bytes per stage
+  static constexpr int B_HALF = N_PAIR / 2;             // B rows staged per CTA (per plane)
+  static constexpr int A_BYTES = BM * BK;
+  static constexpr int B_PLANE_BYTES = B_HALF * BK;
+  static constexpr int STAGE_BYTES = A_BYTES + NPLANES * B_PLANE_BYTES;
+  static constexpr int STAGES = STAGES_;
+  static constexpr int EPI_WARPS = 16;
+  static constexpr int CW = 16;
+  static constexpr int CWQ = CW / (EPI_WARPS / 4);
+  static constexpr int NBUF = NBUF_;
+  static constexpr int ST_ARR = CW * BM * 4;
+  static constexpr int ST_G = CW * BM;
+  static constexpr int BUF_RAW = 3 * ST_ARR + NPLANES * ST_G;
+  static constexpr int BUF_BYTES = (BUF_RAW + 1023) / 1024 * 1024;
+  static constexpr int ACC_COLS = NPLANES * N_PAIR;     // per CTA per accumulator buffer
+  static constexpr int TMEM_COLS = 2 * ACC_COLS;
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
+  static constexpr int NUM_BARS = 2 * STAGES + 4 + 3 * NBUF;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + NBUF * BUF_BYTES + 1024 + 8 * NUM_BARS + 64;
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+  static_assert(N_PAIR % 32 == 0 && N_PAIR <= 256 && N_PAIR >= 32, "UMMA N for M=256");
+  static_assert(N_PAIR % CW == 0, "chunking");
+  static_assert(TMEM_COLS == 256 || TMEM_COLS == 512, "TMEM allocation");
+};
+
+template <int NPLANES, int N_PAIR, int STAGES_, int NBUF_>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES, N_PAIR, STAGES_, NBUF_>::THREADS, 1)
+    gsb_multistep_pair_kernel(const __grid_constant__ TmaMaps maps, const MultiStepArgs args) {
+  using Cfg = PairStepCfg<NPLANES, N_PAIR, STAGES_, NBUF_>;
+  constexpr int STAGES = Cfg::STAGES;
+  constexpr int NBUF = Cfg::NBUF;
+  constexpr int CW = Cfg::CW;
+  constexpr int CWQ = Cfg::CWQ;
+  constexpr int CHUNKS = N_PAIR / CW;
+
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = ptx::smem_u32(smem_raw);
+  const uint32_t base = (raw_addr + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (base - raw_addr);
+  const uint32_t a_base = base;
+  const uint32_t b_base = base + STAGES * Cfg::A_BYTES;
+  const uint32_t s_base = base + STAGES * Cfg::STAGE_BYTES;
+  uint8_t* s_gen = smem + STAGES * Cfg::STAGE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + NBUF * Cfg::BUF_BYTES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
+  auto bar = [&](int i) { return ptx::smem_u32(bars + i); };
+  auto full_bar = [&](int s) { return bar(s); };
+  auto empty_bar = [&](int s) { return bar(STAGES + s); };
+  auto tfull_bar = [&](int b) { return bar(2 * STAGES + b); };
+  auto tempty_bar = [&](int b) { return bar(2 * STAGES + 2 + b); };
+  auto sfull_bar = [&](int b) { return bar(2 * STAGES + 4 + b); };
+  auto sempty_bar = [&](int b) { return bar(2 * STAGES + 4 + NBUF + b); };
+  auto sdone_bar = [&](int b) { return bar(2 * STAGES + 4 + 2 * NBUF + b); };
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t cr = ptx::cluster_ctarank();
+  const bool leader = cr == 0;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(full_bar(s), 2);
+      ptx::mbar_init(empty_bar(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(tfull_bar(b), 1);
+      ptx::mbar_init(tempty_bar(b), 2 * Cfg::EPI_WARPS);
+    }
+    for (int b = 0; b < NBUF; ++b) {
+      ptx::mbar_init(sfull_bar(b), 1);
+      ptx::mbar_init(sempty_bar(b), 1);
+      ptx::mbar_init(sdone_bar(b), Cfg::EPI_WARPS);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) {
+    ptx::tmem_alloc_pair(ptx::smem_u32(tmem_slot), Cfg::TMEM_COLS);
+    ptx::tmem_relinquish_pair();
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_mp = args.num_m / 2;
+  const int T2 = num_mp * args.num_n;  // pair tiles per step
+  const int total = T2 * args.nsteps;
+  const int pair = blockIdx.x >> 1;
+  const int npairs = gridDim.x >> 1;
+  const int KB = args.npad / Cfg::BK;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------- operand producer (both CTAs)
+      ptx::prefetch_tmap(&maps.J);
+      ptx::prefetch_tmap(&maps.Gin[0]);
+      ptx::prefetch_tmap(&maps.Gin[1]);
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int g = pair; g < total; g += npairs) {
+        const int s = g / T2, w = g % T2;
+        const int n_blk = w / num_mp, mp = w % num_mp;
+        const int m_blk = 2 * mp + static_cast<int>(cr);
+        dep::wait_block(args.done, n_blk, static_cast<uint32_t>(s * args.num_m));
+        const CUtensorMap* gin = &maps.Gin[s & 1];
+        for (int kb = 0; kb < KB; ++kb) {
+          ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
+          const uint32_t fb = ptx::mapa(full_bar(stage), 0);  // the leader's full barrier
+          ptx::mbar_arrive_expect_tx_cluster(fb, Cfg::STAGE_BYTES);
+          ptx::tma_load_2d_pair(a_base + stage * Cfg::A_BYTES, &maps.J, fb, kb * Cfg::BK, m_blk * Cfg::BM);
+#pragma unroll
+          for (int pl = 0; pl < NPLANES; ++pl)
+            ptx::tma_load_2d_pair(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES, gin, fb, kb * Cfg::BK,
+                                  pl * args.rpad + n_blk * N_PAIR + static_cast<int>(cr) * Cfg::B_HALF);
+          if (++stage == STAGES) {
+            stage = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // ---------------------------------- MMA issuer (leader only)
+      constexpr uint32_t idesc_s = ptx::idesc_i8(256, N_PAIR, true, true);
+      constexpr uint32_t idesc_u = ptx::idesc_i8(256, N_PAIR, true, false);
+      int stage = 0;
+      uint32_t ph = 0;
+      int lt = 0;
+      for (int g = pair; g < total; g += npairs, ++lt) {
+        const int buf = lt & 1;
+        ptx::mbar_wait(tempty_bar(buf), ((lt >> 1) & 1) ^ 1u);
+        ptx::tc_fence_after();
+        const uint32_t d_base = tmem_base + buf * Cfg::ACC_COLS;
+        for (int kb = 0; kb < KB; ++kb) {
+          ptx::mbar_wait(full_bar(stage), ph);
+          ptx::tc_fence_after();
+          const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + stage * Cfg::A_BYTES);
+#pragma unroll
+          for (int pl = 0; pl < NPLANES; ++pl) {
+            const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES);
+            const uint32_t idesc = (NPLANES == 1 || pl == NPLANES - 1) ? idesc_s : idesc_u;
+#pragma unroll
+            for (int k = 0; k < Cfg::BK / 32; ++k)
+              ptx::mma_i8_pair(d_base + pl * N_PAIR, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          }
+          ptx::mma_commit_pair_mc(empty_bar(stage), 0x3);
+          if (++stage == STAGES) {
+            stage = 0;
+            ph ^= 1u;
+          }
+        }
+        ptx::mma_commit_pair_mc(tfull_bar(buf), 0x3);
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0) {  // ------------------------------------------------ state loader
+      ptx::prefetch_tmap(&maps.X);
+      ptx::prefetch_tmap(&maps.Y);
+      ptx::prefetch_tmap(&maps.P);
+      int ck = 0;
+      for (int g = pair; g < total; g += npairs) {
+        const int s = g / T2, w = g % T2;
+        const int n_blk = w / num_mp, mp = w % num_mp;
+        dep::wait_block(args.done, n_blk, static_cast<uint32_t>(s * args.num_m));
+        const int i0 = (2 * mp + static_cast<int>(cr)) * Cfg::BM, rb = n_blk * N_PAIR;
+        for (int c = 0; c < CHUNKS; ++c, ++ck) {
+          const int b = ck % NBUF;
+          ptx::mbar_wait(sempty_bar(b), ((ck / NBUF) & 1) ^ 1u);
+          ptx::mbar_arrive_expect_tx(sfull_bar(b), 3 * Cfg::ST_ARR);
+          const uint32_t sb = s_base + b * Cfg::BUF_BYTES;
+          ptx::tma_load_2d(sb, &maps.X, sfull_bar(b), i0, rb + c * CW);
+          ptx::tma_load_2d(sb + Cfg::ST_ARR, &maps.Y, sfull_bar(b), i0, rb + c * CW);
+          ptx::tma_load_2d(sb + 2 * Cfg::ST_ARR, &maps.P, sfull_bar(b), i0, rb + c * CW);
+        }
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {  // ------------------------------------------------ state storer
+      ptx::prefetch_tmap(&maps.Gout[0]);
+      ptx::prefetch_tmap(&maps.Gout[1]);
+      int ck = 0;
+      for (int g = pair; g < total; g += npairs) {
+        const int s = g / T2, w = g % T2;
+        const int n_blk = w / num_mp, mp = w % num_mp;
+        const int i0 = (2 * mp + static_cast<int>(cr)) * Cfg::BM, rb = n_blk * N_PAIR;
+        const CUtensorMap* gout = &maps.Gout[s & 1];
+        for (int c = 0; c < CHUNKS; ++c, ++ck) {
+          const int b = ck % NBUF;
+          ptx::mbar_wait(sdone_bar(b), (ck / NBUF) & 1);
+          const uint32_t sb = s_base + b * Cfg::BUF_BYTES;
+          const int r0 = rb + c * CW;
+          ptx::tma_store_2d(&maps.X, sb, i0, r0);
+          ptx::tma_store_2d(&maps.Y, sb + Cfg::ST_ARR, i0, r0);
+          ptx::tma_store_2d(&maps.P, sb + 2 * Cfg::ST_ARR, i0, r0);
+#pragma unroll
+          for (int pl = 0; pl < NPLANES; ++pl)
+            ptx::tma_store_2d(gout, sb + 3 * Cfg::ST_ARR + pl * Cfg::ST_G, i0, (NPLANES == 1 ? 0 : pl * args.rpad) + r0);
+          ptx::bulk_commit();
+          ptx::bulk_wait_read0();
+          ptx::mbar_arrive(sempty_bar(b));
+        }
+        ptx::bulk_wait0();
+        dep::fence_proxy_async_global();
+        __threadfence();
+        dep::release_add(args.done + n_blk, 1u);
+      }
+    }
+  } else {
+    // --------------------------------------------------------------------- epilogue
+    const int q = warp & 3;
+    const int h = (warp - 4) >> 2;
+    const int srow = q * 32 + lane;
+    const uint32_t tempty_leader0 = ptx::mapa(tempty_bar(0), 0);
+    const uint32_t tempty_leader1 = ptx::mapa(tempty_bar(1), 0);
+    PhaseConsts k = args.k;
+    int ck = 0;
+    int lt = 0;
+    for (int g = pair; g < total; g += npairs, ++lt) {
+      const int s = g / T2;
+      k.inv = __frcp_rn(static_cast<float>(args.M - (args.t_begin + static_cast<uint64_t>(s))));
+      const int buf = lt & 1;
+      ptx::mbar_wait(tfull_bar(buf), (lt >> 1) & 1);
+      __syncwarp();
+      ptx::tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * Cfg::ACC_COLS;
+      for (int c = 0; c < CHUNKS; ++c, ++ck) {
+        const int b = ck % NBUF;
+        const int col0 = c * CW + h * CWQ;
+        float F[CWQ];
+        if (NPLANES == 1) {
+          uint32_t v[CWQ];
+          ptx::tmem_ld<CWQ>(t_row + col0, v);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < CWQ; ++j) F[j] = static_cast<float>(static_cast<int32_t>(v[j]));
+        } else {
+          long long tot[CWQ];
+#pragma unroll
+          for (int j = 0; j < CWQ; ++j) tot[j] = 0;
+#pragma unroll
+          for (int pl = 0; pl < NPLANES; ++pl) {
+            uint32_t v[CWQ];
+            ptx::tmem_ld<CWQ>(t_row + pl * N_PAIR + col0, v);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < CWQ; ++j) tot[j] += static_cast<long long>(static_cast<int32_t>(v[j])) << (8 * pl);
+          }
+#pragma unroll
+          for (int j = 0; j < CWQ; ++j) F[j] = __fmul_rn(__ll2float_rn(tot[j]), 0x1p-30f);
+        }
+        ptx::mbar_wait(sfull_bar(b), (ck / NBUF) & 1);
+        float* xs = reinterpret_cast<float*>(s_gen + b * Cfg::BUF_BYTES);
+        float* ys = xs + CW * Cfg::BM;
+        float* ps = ys + CW * Cfg::BM;
+        uint8_t* gs = reinterpret_cast<uint8_t*>(ps + CW * Cfg::BM);
+#pragma unroll
+        for (int j = 0; j < CWQ; ++j) {
+          const int idx = (h * CWQ + j) * Cfg::BM + srow;
+          float xv = xs[idx], yv = ys[idx], pv = ps[idx];
+          gsb_phase(F[j], xv, yv, pv, k);
+          xs[idx] = xv;
+          ys[idx] = yv;
+          ps[idx] = pv;
+          if (NPLANES == 1) {
+            gs[idx] = static_cast<uint8_t>(sgn8(xv));
+          } else {
+            const uint32_t qv = static_cast<uint32_t>(quant30(xv));
+#pragma unroll
+            for (int pl = 0; pl < NPLANES; ++pl) gs[pl * Cfg::ST_G + idx] = static_cast<uint8_t>(qv >> (8 * pl));
+          }
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(sdone_bar(b));
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(buf ? tempty_leader1 : tempty_leader0);
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync_all();  // no remote arrive may target a CTA that has exited
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
+}
+
+}  // namespace sbg
