@@ -118,6 +118,12 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* params, uint64_t m_begin, uint64
  * spins: R x n int8; energy: R doubles; best_index/best_energy: scalars. */
 int sbg_readout(sbg_ctx* ctx, int8_t* spins, double* energy, int64_t* best_index, double* best_energy);
 
+/* batch_best_of's result only (bench.cpp:70-92): the winner's spins (n int8),
+ * its energy and index, plus (optional) all R energies. Copies n + 8R bytes
+ * instead of the R x n spin matrix. */
+int sbg_readout_best(sbg_ctx* ctx, int8_t* best_spins, double* best_energy, int64_t* best_index,
+                     double* energies);
+
 /* Teacher-forced fields for parity (coupling_matvec, kernels.hpp:33-46):
  * F = J * S for S (R x n, entries +-1) -> int32 R x n, bit-exact; and the
  * fixed-point field the continuous variants use for x (R x n fp32). */

@@ -23,7 +23,7 @@ EXPORTS = [
     "sbg_abi_version", "sbg_strerror", "sbg_create", "sbg_destroy", "sbg_last_error", "sbg_device_sm_count",
     "sbg_set_couplings_dense_i8", "sbg_set_couplings_dense_f64", "sbg_gen_couplings_dense_pm1",
     "sbg_set_couplings_csr_i8", "sbg_n", "sbg_set_state", "sbg_init_state", "sbg_get_state", "sbg_advance",
-    "sbg_readout", "sbg_fields_sign", "sbg_fields_fixed", "sbg_run", "sbg_run_seeded", "sbg_synchronize",
+    "sbg_readout", "sbg_readout_best", "sbg_fields_sign", "sbg_fields_fixed", "sbg_run", "sbg_run_seeded", "sbg_synchronize",
     "sbg_kernel_launches", "sbg_state_device", "sbg_last_advance_ms", "sbg_success_tts", "sbg_tune_wigner_f64",
 ]
 
@@ -81,6 +81,7 @@ def lib() -> C.CDLL:
     L.sbg_get_state.argtypes = [P, P, P, P]
     L.sbg_advance.argtypes = [P, C.POINTER(Params), u64, u64]
     L.sbg_readout.argtypes = [P, P, P, P, P]
+    L.sbg_readout_best.argtypes = [P, P, P, P, P]
     L.sbg_fields_sign.argtypes = [P, i64, P, P]
     L.sbg_fields_fixed.argtypes = [P, i64, P, P]
     L.sbg_run.argtypes = [P, C.POINTER(Params), i64, P, P, P, P, P, P, C.POINTER(Timing)]

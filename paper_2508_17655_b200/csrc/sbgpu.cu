@@ -632,9 +632,9 @@ double sbg_last_advance_ms(const sbg_ctx* ctx) {
   return ms;
 }
 
-int sbg_readout(sbg_ctx* ctx, int8_t* spins, double* energy, int64_t* best_index, double* best_energy) {
-  CHECK_CTX(ctx);
-  if (!ctx->dX || ctx->R < 1) return ctx->fail(SBG_ERR_STATE, "state not initialised");
+namespace {
+// Energies of every replica (device) + argmin; leaves dE2/dBest/dSign populated.
+int readout_device(sbg_ctx* ctx) {
   CK(cudaSetDevice(ctx->device));
   int rc;
   CK(cudaMemsetAsync(ctx->dE2, 0, sizeof(unsigned long long) * ctx->rpad, ctx->stream));
@@ -656,6 +656,15 @@ int sbg_readout(sbg_ctx* ctx, int8_t* spins, double* energy, int64_t* best_index
                                                     int32_t(ctx->R), ctx->dBest);
   CK(cudaGetLastError());
   ++ctx->launches;
+  return SBG_OK;
+}
+}  // namespace
+
+int sbg_readout(sbg_ctx* ctx, int8_t* spins, double* energy, int64_t* best_index, double* best_energy) {
+  CHECK_CTX(ctx);
+  if (!ctx->dX || ctx->R < 1) return ctx->fail(SBG_ERR_STATE, "state not initialised");
+  int rc = readout_device(ctx);
+  if (rc) return rc;
   if (spins)
     CK(cudaMemcpy2DAsync(spins, ctx->n, ctx->dSign, ctx->npad, ctx->n, ctx->R, cudaMemcpyDeviceToHost,
                          ctx->stream));
@@ -670,6 +679,28 @@ int sbg_readout(sbg_ctx* ctx, int8_t* spins, double* energy, int64_t* best_index
   // ising_energy = -1/2 sum_i s_i (J s)_i, exact in double for integer J
   if (energy)
     for (int64_t r = 0; r < ctx->R; ++r) energy[r] = -0.5 * double(e2[size_t(r)]);
+  if (best_index) *best_index = best[0];
+  if (best_energy) *best_energy = -0.5 * double(best[1]);
+  return SBG_OK;
+}
+
+int sbg_readout_best(sbg_ctx* ctx, int8_t* best_spins, double* best_energy, int64_t* best_index, double* energies) {
+  CHECK_CTX(ctx);
+  if (!ctx->dX || ctx->R < 1) return ctx->fail(SBG_ERR_STATE, "state not initialised");
+  int rc = readout_device(ctx);
+  if (rc) return rc;
+  long long best[2] = {0, 0};
+  CK(cudaMemcpyAsync(best, ctx->dBest, sizeof best, cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<long long> e2;
+  if (energies) {
+    e2.resize(ctx->R);
+    CK(cudaMemcpyAsync(e2.data(), ctx->dE2, sizeof(long long) * ctx->R, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (best_spins)
+    CK(cudaMemcpy(best_spins, ctx->dSign + size_t(best[0]) * ctx->npad, ctx->n, cudaMemcpyDeviceToHost));
+  if (energies)
+    for (int64_t r = 0; r < ctx->R; ++r) energies[r] = -0.5 * double(e2[size_t(r)]);
   if (best_index) *best_index = best[0];
   if (best_energy) *best_energy = -0.5 * double(best[1]);
   return SBG_OK;
@@ -751,7 +782,8 @@ static int run_tail(sbg_ctx* ctx, const sbg_params* prm, float* x_final, int8_t*
   int rc = sbg_advance(ctx, prm, 0, prm->steps);
   if (rc) return rc;
   CK(cudaEventRecord(ctx->ev[4], ctx->stream));
-  rc = sbg_readout(ctx, spins, energy, best_index, nullptr);
+  rc = spins ? sbg_readout(ctx, spins, energy, best_index, nullptr)
+             : sbg_readout_best(ctx, nullptr, nullptr, best_index, energy);
   if (rc) return rc;
   CK(cudaEventRecord(ctx->ev[5], ctx->stream));
   if (x_final) {

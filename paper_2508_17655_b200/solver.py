@@ -262,6 +262,15 @@ class Solver:
         self._check(self._L.sbg_readout(self._h, ptr(spins), ptr(energy), C.byref(best), C.byref(best_e)))
         return spins, energy, int(best.value), float(best_e.value)
 
+    def readout_best(self):
+        """(best_spins n int8, best_energy, best_index, energies R)."""
+        spins = np.empty(self.n, np.int8)
+        energy = np.empty(self.R, np.float64)
+        best = C.c_int64()
+        best_e = C.c_double()
+        self._check(self._L.sbg_readout_best(self._h, ptr(spins), C.byref(best_e), C.byref(best), ptr(energy)))
+        return spins, float(best_e.value), int(best.value), energy
+
     def fields_sign(self, S: np.ndarray) -> np.ndarray:
         S = np.ascontiguousarray(S, np.int8)
         F = np.empty(S.shape, np.int32)
@@ -277,7 +286,7 @@ class Solver:
     # ---------------------------------------------------------------- runs
     def run_batch(self, cfg: SolverConfig, tuning: TuningResult, R: int, x0: Optional[np.ndarray] = None,
                   y0: Optional[np.ndarray] = None, master_seed: int = 0, tag: int = SEED_STREAM_BATCH,
-                  replica_offset: int = 0, want_x: bool = False):
+                  replica_offset: int = 0, want_x: bool = False, want_spins: bool = True):
         """run() (engine.cpp:112-139) for R replicas in one device pass.
 
         Initial states: host x0/y0 (R x n fp32), or generated on the device from
@@ -286,7 +295,7 @@ class Solver:
         """
         rcfg = resolve_config(cfg, tuning)
         prm = self.params(rcfg)
-        spins = np.empty((R, self.n), np.int8)
+        spins = np.empty((R, self.n), np.int8) if want_spins else None
         energy = np.empty(R, np.float64)
         best = C.c_int64()
         timing = _lib.Timing()

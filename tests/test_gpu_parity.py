@@ -241,3 +241,15 @@ def test_invalid_arguments_raise(solver, orc):
     solver.set_state(np.zeros((2, 8), np.float32), np.zeros((2, 8), np.float32))
     with pytest.raises(ValueError):
         solver.advance(SolverConfig(variant=Variant.gbsb, steps=10, dt=0.5, c=0.1), 5, 11)  # past M
+
+
+def test_readout_best_matches_full_readout(solver, orc):
+    n, R = 300, 77
+    J = orc.gen_dense_i8(n, 12)
+    solver.set_instance(J)
+    x, y, _ = orc.init_reference(n, R, master=4)
+    solver.set_state(x, y)
+    spins, energy, best, best_e = solver.readout()
+    bs, be, bi, energies = solver.readout_best()
+    assert bi == best and be == best_e and (energies == energy).all() and (bs == spins[best]).all()
+    assert (energy == -0.5 * orc.energy2_i8(J, x)).all()
