@@ -1,0 +1,59 @@
+// Exercises the C++ mirror (include/sbgpu.hpp) the way reference code would call
+// sbopt: build an instance, resolve a config from a tuning result, batch_best_of,
+// success probability / TTS, and the reference's exception behaviour.
+// Prints one JSON object; tests/test_cpp_api.py checks it against the oracle.
+#include <cstdio>
+#include <stdexcept>
+#include <vector>
+
+#include "sbgpu.hpp"
+
+int main(int argc, char** argv) {
+  const std::size_t n = 64, R = 8;
+  std::vector<double> J(n * n, 0.0);
+  std::uint64_t z = 12345;
+  for (std::size_t i = 0; i < n; ++i)
+    for (std::size_t j = i + 1; j < n; ++j) {
+      z = sbgpu::detail::mix64(z + 1);
+      J[i * n + j] = J[j * n + i] = (z >> 63) ? -1.0 : 1.0;
+    }
+  int invalid_caught = 0;
+  try {
+    sbgpu::SolverConfig bad;
+    bad.steps = 0;
+    sbgpu::resolve_config(bad, sbgpu::TuningResult{0.1, 0.5});
+  } catch (const std::invalid_argument&) {
+    ++invalid_caught;
+  }
+  try {
+    std::vector<double> asym(4, 0.0);
+    asym[1] = 1.0;
+    sbgpu::Solver s0(0);
+    s0.set_instance(2, asym);
+  } catch (const std::invalid_argument&) {
+    ++invalid_caught;
+  }
+  sbgpu::Solver s(0);
+  s.set_instance(n, J);
+  const auto tuning = sbgpu::auto_tune_wigner(n, J);
+  sbgpu::SolverConfig cfg;
+  cfg.variant = sbgpu::Variant::gdsb;
+  cfg.steps = 100;
+  cfg.a = 0.2;
+  cfg.init_mode = sbgpu::InitMode::small_uniform;
+  auto batch = s.run_batch(cfg, tuning, R, 7, sbgpu::seed_stream::gpu_init);
+  auto best = s.batch_best_of(cfg, tuning, R, 7);
+  std::vector<double> energies;
+  for (auto& r : batch) energies.push_back(r.energy);
+  const auto st = sbgpu::success_probability(energies, best.energy);
+  const auto tts = sbgpu::time_to_solution(1.0, sbgpu::success_from_counts(500, 1000, 0.0));
+  std::printf("{\"n\": %zu, \"R\": %zu, \"c\": %.17g, \"dt\": %.17g, \"energies\": [", n, R, tuning.c, tuning.dt);
+  for (std::size_t r = 0; r < R; ++r) std::printf("%s%.1f", r ? ", " : "", batch[r].energy);
+  std::printf("], \"cuts\": [");
+  for (std::size_t r = 0; r < R; ++r) std::printf("%s%lld", r ? ", " : "", *batch[r].cut);
+  std::printf("], \"best_energy\": %.1f, \"best_seed\": %llu, \"p_s\": %.17g, \"tts_mid\": %.17g, \"invalid_caught\": %d}\n",
+              best.energy, static_cast<unsigned long long>(best.config_echo.seed), st.p_s, tts.tts_s, invalid_caught);
+  (void)argc;
+  (void)argv;
+  return 0;
+}
