@@ -89,8 +89,17 @@ int sbg_device_sm_count(const sbg_ctx* ctx);
 /* Couplings. Replace IsingInstance (model.hpp:46-70; invariants model.cpp:54-68:
  * symmetric, zero diagonal). Dense integer J is kept as int8 on the device. */
 int sbg_set_couplings_dense_i8(sbg_ctx* ctx, int64_t n, const int8_t* J);
-/* fp64 J as IsingInstance stores it; must be integral in [-127, 127]. */
+/* fp64 J as IsingInstance stores it: integral entries in [-127, 127] take the int8
+ * path, anything else the fixed-point real-J path below. */
 int sbg_set_couplings_dense_f64(sbg_ctx* ctx, int64_t n, const double* J);
+/* Real-valued couplings (e.g. Sherrington-Kirkpatrick, BASELINE configs[3]): J is
+ * held as a 24-bit fixed-point image J_int = rint(J * 2^s) (s maximal with
+ * |J_int| < 2^23) in three byte planes; fields are exact integer sums scaled once
+ * (fp32-accurate), energies exact for J_int then scaled by 2^-s. n <= 11000.
+ * sbg_set_couplings_dense_f64 routes non-integral J here. */
+int sbg_set_couplings_dense_f32(sbg_ctx* ctx, int64_t n, const float* J);
+/* The scale exponent s of the fixed-point coupling image (0 for integer J). */
+int sbg_coupling_scale_exp(const sbg_ctx* ctx);
 /* gen_random_dense (model.cpp:144-159) evaluated on the host into int8. */
 int sbg_gen_couplings_dense_pm1(sbg_ctx* ctx, int64_t n, uint64_t seed);
 /* CSR (both triangles, ascending columns), int8 values: the sparse view of

@@ -207,6 +207,11 @@ class _Orc:
         L.orc_argmin_i64.restype = _i64
         L.orc_argmin_i64.argtypes = [_i64, _P]
         L.orc_success_tts.argtypes = [_i64, _i64, _f64, _P, _P, _P, _P]
+        L.orc_fx_quantize.restype = C.c_int
+        L.orc_fx_quantize.argtypes = [_i64, _P, _P]
+        L.orc_step_f32_fx.argtypes = [C.c_int, _i64, _P, C.c_int, _i64, _i64, _P, _P, _P, _u64, _u64, _f32, _f32,
+                                      _f32]
+        L.orc_energy2_fx.argtypes = [_i64, _P, _i64, _i64, _P, _P]
 
     def derive_seed(self, master: int, keys) -> int:
         k = np.asarray(list(keys), dtype=np.uint64)
@@ -325,6 +330,29 @@ class _Orc:
     def argmin(self, v):
         v = np.ascontiguousarray(v, np.int64)
         return int(self.lib.orc_argmin_i64(len(v), _ptr(v)))
+
+    def fx_quantize(self, J):
+        J = np.ascontiguousarray(J, np.float32)
+        n = J.shape[0]
+        planes = np.empty((3, n, n), np.uint8)
+        shift = self.lib.orc_fx_quantize(n, _ptr(J), _ptr(planes))
+        return planes, int(shift)
+
+    def step_f32_fx(self, variant, planes, shift, x, y, p, m, M, dt, c, a, nsteps: int = 1):
+        planes = np.ascontiguousarray(planes, np.uint8)
+        n = planes.shape[1]
+        x, y, p = (np.array(v, np.float32, copy=True) for v in (x, y, p))
+        for k in range(nsteps):
+            self.lib.orc_step_f32_fx(variant, n, _ptr(planes), shift, x.shape[0], x.shape[1], _ptr(x), _ptr(y),
+                                     _ptr(p), m + k, M, dt, c, a)
+        return x, y, p
+
+    def energy_fx(self, planes, shift, x):
+        planes = np.ascontiguousarray(planes, np.uint8)
+        x = np.ascontiguousarray(x, np.float32)
+        E2 = np.empty(x.shape[0], np.int64)
+        self.lib.orc_energy2_fx(planes.shape[1], _ptr(planes), x.shape[0], x.shape[1], _ptr(x), _ptr(E2))
+        return -0.5 * E2.astype(np.float64) * 2.0 ** -shift
 
     def success_tts(self, hits, n_rep, t_com):
         out = [np.zeros(1) for _ in range(4)]

@@ -455,3 +455,84 @@ int orc_success_tts(int64_t hits, int64_t n_rep, double t_com, double* p_s, doub
   }
   return 0;
 }
+
+/* ------------------------------------------- real-valued J, fixed-point mirror */
+
+int orc_fx_quantize(int64_t n, const float* J, uint8_t* planes /* [3][n][n] */) {
+  /* Host quantisation of sbg_set_couplings_dense_f32 (csrc/sbgpu.cu): the largest
+   * s with max|J| * 2^s <= 2^23 - 1, J_int = rint(J * 2^s), bytes (u8, u8, s8). */
+  float amax = 0.0f;
+  for (int64_t k = 0; k < n * n; ++k) amax = fabsf(J[k]) > amax ? fabsf(J[k]) : amax;
+  int shift = 0;
+  while (ldexp((double)amax, shift + 1) <= 8388607.0 && shift < 60) ++shift;
+  while (ldexp((double)amax, shift) > 8388607.0) --shift;
+  for (int64_t k = 0; k < n * n; ++k) {
+    const int32_t q = (int32_t)nearbyint(ldexp((double)J[k], shift));
+    for (int a = 0; a < 3; ++a) planes[(int64_t)a * n * n + k] = (uint8_t)((uint32_t)q >> (8 * a));
+  }
+  return shift;
+}
+
+static inline int64_t jplane(const uint8_t* planes, int64_t n, int a, int64_t i, int64_t j) {
+  const uint8_t b = planes[(int64_t)a * n * n + i * n + j];
+  return a == 2 ? (int64_t)(int8_t)b : (int64_t)b;
+}
+
+void orc_step_f32_fx(int variant, int64_t n, const uint8_t* planes, int shift, int64_t R, int64_t ld, float* x,
+                     float* y, float* p, uint64_t m, uint64_t M, float dt, float c, float a_cfg) {
+  const float a = honours_a(variant) ? a_cfg : 0.0f;
+  const float inv = 1.0f / (float)(M - m);
+  float* F = (float*)malloc(sizeof(float) * (size_t)n);
+  int64_t* qb = (int64_t*)malloc(sizeof(int64_t) * (size_t)n * 4);
+  for (int64_t r = 0; r < R; ++r) {
+    float* xr = x + r * ld;
+    if (is_sign_variant(variant)) {
+      for (int64_t j = 0; j < n; ++j) qb[j] = xr[j] >= 0.0f ? 1 : -1;
+    } else {
+      for (int64_t j = 0; j < n; ++j) {
+        const uint32_t q = (uint32_t)quant30(xr[j]);
+        for (int b = 0; b < 4; ++b) {
+          const uint8_t byte = (uint8_t)(q >> (8 * b));
+          qb[b * n + j] = b == 3 ? (int64_t)(int8_t)byte : (int64_t)byte;
+        }
+      }
+    }
+    const int nb = is_sign_variant(variant) ? 1 : 4;
+    const int nw = 3 + nb - 1;
+    const int e0 = is_sign_variant(variant) ? -shift : -(shift + 30);
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t acc[6] = {0, 0, 0, 0, 0, 0};
+      for (int pa = 0; pa < 3; ++pa)
+        for (int b = 0; b < nb; ++b) {
+          int64_t t = 0;
+          for (int64_t j = 0; j < n; ++j) t += jplane(planes, n, pa, i, j) * qb[b * n + j];
+          acc[pa + b] += t;
+        }
+      double f = 0.0;
+      for (int w = 0; w < nw; ++w) f = f + (double)acc[w] * ldexp(1.0, 8 * w + e0);
+      F[i] = (float)f;
+    }
+    for (int64_t i = 0; i < n; ++i) orc_phase_f32(F[i], xr + i, y + r * ld + i, p + r * ld + i, a, c, dt, inv);
+  }
+  free(F);
+  free(qb);
+}
+
+void orc_energy2_fx(int64_t n, const uint8_t* planes, int64_t R, int64_t ld, const float* x, int64_t* E2) {
+  /* exact sum_i s_i (J_int s)_i; energy = -E2/2 * 2^-shift */
+  int8_t* s = (int8_t*)malloc((size_t)n);
+  for (int64_t r = 0; r < R; ++r) {
+    for (int64_t j = 0; j < n; ++j) s[j] = x[r * ld + j] >= 0.0f ? 1 : -1;
+    int64_t total = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t field = 0;
+      for (int64_t j = 0; j < n; ++j) {
+        const int64_t q = jplane(planes, n, 0, i, j) + (jplane(planes, n, 1, i, j) << 8) + (jplane(planes, n, 2, i, j) << 16);
+        field += q * s[j];
+      }
+      total += field * s[i];
+    }
+    E2[r] = total;
+  }
+  free(s);
+}

@@ -91,6 +91,13 @@ void orc_energy2_csr(int64_t n, const int32_t* rowptr, const int32_t* col, const
 /* batch_best_of winner rule (bench.cpp:84-87): min, ties to lowest index. */
 int64_t orc_argmin_i64(int64_t R, const int64_t* v);
 
+/* ---- real-valued J (fixed-point image, GPU op order) ------------------- */
+/* Quantise J like sbg_set_couplings_dense_f32; returns the scale exponent s. */
+int orc_fx_quantize(int64_t n, const float* J, uint8_t* planes /* [3][n][n] */);
+void orc_step_f32_fx(int variant, int64_t n, const uint8_t* planes, int shift, int64_t R, int64_t ld, float* x,
+                     float* y, float* p, uint64_t m, uint64_t M, float dt, float c, float a);
+void orc_energy2_fx(int64_t n, const uint8_t* planes, int64_t R, int64_t ld, const float* x, int64_t* E2);
+
 /* ---- statistics (bench.cpp:15-68) ------------------------------------- */
 int orc_success_tts(int64_t hits, int64_t n_rep, double t_com, double* p_s, double* dp_s,
                     double* tts, double* dtts);

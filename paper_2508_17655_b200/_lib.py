@@ -21,7 +21,8 @@ INIT_UNIFORM_RANDOM, INIT_CHAOS_PROBE, INIT_SMALL_UNIFORM = 0, 1, 2
 
 EXPORTS = [
     "sbg_abi_version", "sbg_strerror", "sbg_create", "sbg_destroy", "sbg_last_error", "sbg_device_sm_count",
-    "sbg_set_couplings_dense_i8", "sbg_set_couplings_dense_f64", "sbg_gen_couplings_dense_pm1",
+    "sbg_set_couplings_dense_i8", "sbg_set_couplings_dense_f64", "sbg_set_couplings_dense_f32",
+    "sbg_coupling_scale_exp", "sbg_gen_couplings_dense_pm1",
     "sbg_set_couplings_csr_i8", "sbg_n", "sbg_set_state", "sbg_init_state", "sbg_get_state", "sbg_advance",
     "sbg_readout", "sbg_readout_best", "sbg_fields_sign", "sbg_fields_fixed", "sbg_run", "sbg_run_seeded", "sbg_synchronize",
     "sbg_kernel_launches", "sbg_state_device", "sbg_last_advance_ms", "sbg_success_tts", "sbg_tune_wigner_f64",
@@ -73,6 +74,8 @@ def lib() -> C.CDLL:
     L.sbg_set_couplings_dense_i8.argtypes = [P, i64, P]
     L.sbg_set_couplings_dense_f64.argtypes = [P, i64, P]
     L.sbg_gen_couplings_dense_pm1.argtypes = [P, i64, u64]
+    L.sbg_set_couplings_dense_f32.argtypes = [P, i64, P]
+    L.sbg_coupling_scale_exp.argtypes = [P]
     L.sbg_set_couplings_csr_i8.argtypes = [P, i64, i64, P, P, P]
     L.sbg_n.restype = i64
     L.sbg_n.argtypes = [P]

@@ -197,4 +197,14 @@ __global__ void __launch_bounds__(1024) argmin_energy_kernel(const long long* __
 
 __global__ void advance_counter_kernel(uint64_t* m, uint64_t by) { *m += by; }
 
+// Real-valued J readout: E2 = sum_a 2^(8a) E2_a over the J byte planes.
+__global__ void combine_planes_e2_kernel(const long long* __restrict__ parts, int64_t stride, int32_t nplanes,
+                                         int32_t R, long long* __restrict__ e2) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
+    long long t = 0;
+    for (int a = 0; a < nplanes; ++a) t += parts[a * stride + r] * (1ll << (8 * a));
+    e2[r] = t;
+  }
+}
+
 }  // namespace sbg

@@ -36,7 +36,10 @@ constexpr int PAD_R = 256;     // replica padding (multiple of every replica til
 constexpr int NPAIR_SIGN = 256;   // replicas per pair tile, sign variants
 constexpr int NPAIR_PLANE = 64;   // replicas per pair tile, fixed-point variants
 
-enum Kind { KIND_NONE = 0, KIND_DENSE_I8 = 1, KIND_CSR_I8 = 2 };
+enum Kind { KIND_NONE = 0, KIND_DENSE_I8 = 1, KIND_CSR_I8 = 2, KIND_DENSE_FX = 3 };
+constexpr int FX_NA = 3;          // real J: 24-bit fixed point as 3 byte planes (u8, u8, s8)
+constexpr int BN_FX_SIGN = 64;    // replica tile, real J x sign plane (3 accumulators)
+constexpr int BN_FX_PLANE = 32;   // replica tile, real J x 4 x-planes (6 accumulators)
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
@@ -67,6 +70,9 @@ struct sbg_ctx {
   int64_t n = 0, npad = 0;
   int8_t* dJ = nullptr;
   CUtensorMap tmJ;
+  CUtensorMap tmJplane[FX_NA];  // KIND_DENSE_FX: one map per J byte plane (readout)
+  int fx_shift = 0;             // KIND_DENSE_FX: J_int = rint(J * 2^fx_shift)
+  double energy_scale = 1.0;    // energy = -E2/2 * energy_scale (2^-fx_shift for real J)
   int32_t* d_rowptr = nullptr;
   int32_t* d_col = nullptr;
   int8_t* d_val = nullptr;
@@ -81,6 +87,8 @@ struct sbg_ctx {
   CUtensorMap tmG_sign[2], tmG_planes[2], tmSign;
   TmaMaps maps_sign[2], maps_planes[2];  // multi-step kernel maps, indexed by the current B buffer
   TmaMaps pmaps_planes[2];               // pair kernel, fixed-point planes (B half = 32 rows)
+  TmaMaps fxmaps_sign[2], fxmaps_planes[2];  // real-J kernels (B tiles of 64 / 32 rows)
+  unsigned long long* dE2p = nullptr;    // real-J readout: per-J-plane partial E2 [FX_NA][rpad]
   uint32_t* d_done = nullptr;            // per replica-block tile counters of the multi-step kernel
   int g_cur = 0;
   int g_mode = 0;  // 0 stale, 1 sign plane valid in dG[g_cur], 4 planes valid
@@ -148,13 +156,13 @@ int grid_for(const sbg_ctx* ctx, size_t work, int threads) {
 }
 
 template <int NP, int BN, EpiMode MODE>
-int launch_step(sbg_ctx* ctx, const CUtensorMap& tmG, const StepArgs& a) {
+int launch_step(sbg_ctx* ctx, const CUtensorMap& tmG, const StepArgs& a, const CUtensorMap* tmA = nullptr) {
   using Cfg = StepCfg<NP, BN>;
   auto kern = gsb_step_i8_kernel<NP, BN, MODE>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
   const int tiles = a.num_m * a.num_n;
   const int grid = std::min(tiles, ctx->sms);
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(ctx->tmJ, tmG, a);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(tmA ? *tmA : ctx->tmJ, tmG, a);
   CK(cudaGetLastError());
   ++ctx->launches;
   return SBG_OK;
@@ -171,10 +179,10 @@ int dev_knob(const char* name) {
   return e ? atoi(e) : 0;
 }
 
-template <int NP, int BN, int ST, int NB>
+template <int NP, int BN, int ST, int NB, int NA = 1>
 int launch_multistep(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& a) {
-  using Cfg = TmaStepCfg<NP, BN, ST, NB>;
-  auto kern = gsb_multistep_kernel<NP, BN, ST, NB>;
+  using Cfg = TmaStepCfg<NP, BN, ST, NB, NA>;
+  auto kern = gsb_multistep_kernel<NP, BN, ST, NB, NA>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
   const int64_t tiles = int64_t(a.num_m) * a.num_n * a.nsteps;
   // persistent: one CTA per SM (all must be co-resident for the dependency walk)
@@ -209,6 +217,8 @@ void free_state(sbg_ctx* ctx) {
   cudaFree(ctx->dG[1]);
   cudaFree(ctx->dSign);
   cudaFree(ctx->dE2);
+  cudaFree(ctx->dE2p);
+  ctx->dE2p = nullptr;
   cudaFree(ctx->dBest);
   cudaFree(ctx->d_done);
   ctx->d_done = nullptr;
@@ -236,13 +246,14 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
     CK(cudaMalloc(&ctx->dG[1], NPL * pl));
     CK(cudaMalloc(&ctx->dSign, pl));
     CK(cudaMalloc(&ctx->dE2, sizeof(unsigned long long) * rpad));
+    CK(cudaMalloc(&ctx->dE2p, sizeof(unsigned long long) * rpad * FX_NA));
     CK(cudaMalloc(&ctx->dBest, 2 * sizeof(long long)));
     CK(cudaMalloc(&ctx->d_done, sizeof(uint32_t) * (rpad / 16 + 1)));
     CK(cudaMemsetAsync(ctx->dG[0], 0, NPL * pl, ctx->stream));
     CK(cudaMemsetAsync(ctx->dG[1], 0, NPL * pl, ctx->stream));
     CK(cudaMemsetAsync(ctx->dSign, 0, pl, ctx->stream));
     ctx->cap_rpad = rpad;
-    if (ctx->kind == KIND_DENSE_I8) {
+    if (ctx->kind == KIND_DENSE_I8 || ctx->kind == KIND_DENSE_FX) {
       for (int b = 0; b < 2; ++b) {
         int rc = encode_2d_u8(ctx, &ctx->tmG_sign[b], ctx->dG[b], ctx->npad, rpad, 128, BN_SIGN);
         if (rc) return rc;
@@ -256,7 +267,7 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
   ctx->R = R;
   ctx->rpad = rpad;
   ctx->g_mode = 0;
-  if (ctx->kind == KIND_DENSE_I8) {
+  if (ctx->kind == KIND_DENSE_I8 || ctx->kind == KIND_DENSE_FX) {
     constexpr int CW = TmaStepCfg<1, BN_SIGN, SIGN_STAGES, SIGN_NBUF>::CW;
     // Per B buffer b: output maps (the next step's B operand lands in the other buffer).
     CUtensorMap gout_sign[2], gout_planes[2];
@@ -290,9 +301,16 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
         mp.P = P;
       }
       ctx->pmaps_planes[cur] = ctx->maps_planes[cur];
+      ctx->fxmaps_sign[cur] = ctx->maps_sign[cur];
+      ctx->fxmaps_planes[cur] = ctx->maps_planes[cur];
       for (int par = 0; par < 2; ++par) {
         int rc = encode_2d_u8(ctx, &ctx->pmaps_planes[cur].Gin[par], ctx->dG[cur ^ par], ctx->npad, NPL * rpad, 128,
                               NPAIR_PLANE / 2);
+        if (rc) return rc;
+        rc = encode_2d_u8(ctx, &ctx->fxmaps_sign[cur].Gin[par], ctx->dG[cur ^ par], ctx->npad, rpad, 128, BN_FX_SIGN);
+        if (rc) return rc;
+        rc = encode_2d_u8(ctx, &ctx->fxmaps_planes[cur].Gin[par], ctx->dG[cur ^ par], ctx->npad, NPL * rpad, 128,
+                          BN_FX_PLANE);
         if (rc) return rc;
       }
     }
@@ -425,6 +443,7 @@ int sbg_set_couplings_dense_i8(sbg_ctx* ctx, int64_t n, const int8_t* J) {
   ctx->n = n;
   ctx->npad = npad;
   ctx->kind = KIND_DENSE_I8;
+  ctx->energy_scale = 1.0;
   return encode_2d_u8(ctx, &ctx->tmJ, ctx->dJ, npad, npad, 128, 128);
 }
 
@@ -432,15 +451,68 @@ int sbg_set_couplings_dense_f64(sbg_ctx* ctx, int64_t n, const double* J) {
   CHECK_CTX(ctx);
   if (n < 1 || !J) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "instance size must be >= 1");
   std::vector<int8_t> q(size_t(n) * n);
-  for (int64_t k = 0; k < n * n; ++k) {
+  bool integral = true;
+  for (int64_t k = 0; k < n * n && integral; ++k) {
     const double v = J[k];
-    if (!(v == std::floor(v)) || v < -127.0 || v > 127.0)
-      return ctx->fail(SBG_ERR_UNSUPPORTED,
-                       "couplings must be integers in [-127, 127] for the int8 tensor-core path");
-    q[size_t(k)] = static_cast<int8_t>(v);
+    integral = (v == std::floor(v)) && v >= -127.0 && v <= 127.0;
+    q[size_t(k)] = integral ? static_cast<int8_t>(v) : 0;
   }
-  return sbg_set_couplings_dense_i8(ctx, n, q.data());
+  if (integral) return sbg_set_couplings_dense_i8(ctx, n, q.data());
+  // real-valued couplings: the fixed-point path (rounded to fp32 first, as the state is fp32)
+  std::vector<float> f(size_t(n) * n);
+  for (int64_t k = 0; k < n * n; ++k) f[size_t(k)] = static_cast<float>(J[k]);
+  return sbg_set_couplings_dense_f32(ctx, n, f.data());
 }
+
+int sbg_set_couplings_dense_f32(sbg_ctx* ctx, int64_t n, const float* J) {
+  CHECK_CTX(ctx);
+  if (n < 1 || !J) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "instance size must be >= 1");
+  // IsingInstance invariants (model.cpp:54-68)
+  float amax = 0.0f;
+  for (int64_t i = 0; i < n; ++i) {
+    if (J[i * n + i] != 0.0f) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "coupling diagonal must be zero");
+    for (int64_t j = i + 1; j < n; ++j)
+      if (J[i * n + j] != J[j * n + i]) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "coupling matrix must be symmetric");
+    for (int64_t j = 0; j < n; ++j) {
+      if (!std::isfinite(J[i * n + j])) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "couplings must be finite");
+      amax = std::max(amax, std::fabs(J[i * n + j]));
+    }
+  }
+  if (amax == 0.0f) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "degenerate instance: all couplings zero");
+  // J_int = rint(J * 2^s) with |J_int| <= 2^23 - 1 (24-bit two's complement in 3 byte planes),
+  // and the per-weight s32 accumulators must not overflow: 3 * 255 * 255 * n < 2^31.
+  if (3.0 * 255.0 * 255.0 * double(n) >= 2147483648.0)
+    return ctx->fail(SBG_ERR_UNSUPPORTED, "real-valued couplings supported up to n = 11000");
+  int shift = 0;
+  while (std::ldexp(double(amax), shift + 1) <= 8388607.0 && shift < 60) ++shift;
+  while (std::ldexp(double(amax), shift) > 8388607.0) --shift;
+  const int64_t npad = round_up(n, PAD_N);
+  std::vector<uint8_t> planes(size_t(FX_NA) * npad * npad, 0);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      const int32_t qv = static_cast<int32_t>(std::nearbyint(std::ldexp(double(J[i * n + j]), shift)));
+      for (int a = 0; a < FX_NA; ++a)
+        planes[size_t(a) * npad * npad + size_t(i) * npad + j] = static_cast<uint8_t>(uint32_t(qv) >> (8 * a));
+    }
+  CK(cudaSetDevice(ctx->device));
+  cudaStreamSynchronize(ctx->stream);
+  free_state(ctx);
+  cudaFree(ctx->dJ);
+  ctx->dJ = nullptr;
+  CK(cudaMalloc(&ctx->dJ, planes.size()));
+  CK(cudaMemcpy(ctx->dJ, planes.data(), planes.size(), cudaMemcpyHostToDevice));
+  ctx->n = n;
+  ctx->npad = npad;
+  ctx->kind = KIND_DENSE_FX;
+  ctx->fx_shift = shift;
+  ctx->energy_scale = std::ldexp(1.0, -shift);
+  int rc = encode_2d_u8(ctx, &ctx->tmJ, ctx->dJ, npad, FX_NA * npad, 128, 128);
+  for (int a = 0; a < FX_NA && rc == SBG_OK; ++a)
+    rc = encode_2d_u8(ctx, &ctx->tmJplane[a], ctx->dJ + size_t(a) * npad * npad, npad, npad, 128, 128);
+  return rc;
+}
+
+int sbg_coupling_scale_exp(const sbg_ctx* ctx) { return ctx && ctx->kind == KIND_DENSE_FX ? ctx->fx_shift : 0; }
 
 int sbg_gen_couplings_dense_pm1(sbg_ctx* ctx, int64_t n, uint64_t seed) {
   CHECK_CTX(ctx);
@@ -495,6 +567,7 @@ int sbg_set_couplings_csr_i8(sbg_ctx* ctx, int64_t n, int64_t nnz, const int32_t
   ctx->npad = round_up(n, 32);
   ctx->nnz = nnz;
   ctx->kind = KIND_CSR_I8;
+  ctx->energy_scale = 1.0;
   return SBG_OK;
 }
 
@@ -574,7 +647,9 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
       if (rc) return rc;
       ctx->g_mode = need;
     }
-    const int64_t T = (ctx->npad / 128) * (ctx->rpad / (sign ? BN_SIGN : BN_PLANE));
+    const bool fx = ctx->kind == KIND_DENSE_FX;
+    const int bn = fx ? (sign ? BN_FX_SIGN : BN_FX_PLANE) : (sign ? BN_SIGN : BN_PLANE);
+    const int64_t T = (ctx->npad / 128) * (ctx->rpad / bn);
     const int64_t max_steps = std::max<int64_t>(1, (int64_t(1) << 30) / T);
     const bool per_step = dev_knob("SBG_PER_STEP_LAUNCH") != 0;
     for (uint64_t m = m_begin; m < m_end;) {
@@ -586,7 +661,8 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
       a.R = int32_t(ctx->R);
       a.rpad = int32_t(ctx->rpad);
       a.num_m = int32_t(ctx->npad / 128);
-      a.num_n = int32_t(ctx->rpad / (sign ? BN_SIGN : BN_PLANE));
+      a.num_n = int32_t(ctx->rpad / bn);
+      a.fx_exp = sign ? -ctx->fx_shift : -(ctx->fx_shift + 30);
       a.k = k;
       a.M = prm->steps;
       a.t_begin = m;
@@ -600,7 +676,11 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
       // 20.4 us on pairs. SBG_STEP_CFG selects sweep alternatives (dev only).
       const int knob = dev_knob("SBG_STEP_CFG");
       const bool pair_ok = (ctx->npad % 256) == 0;
-      if (sign) {
+      if (fx) {
+        // real-valued J: 3 J planes x (sign | 4 x-planes), single-CTA
+        rc = sign ? launch_multistep<1, BN_FX_SIGN, 2, 4, FX_NA>(ctx, ctx->fxmaps_sign[cur], a)
+                  : launch_multistep<NPL, BN_FX_PLANE, 2, 3, FX_NA>(ctx, ctx->fxmaps_planes[cur], a);
+      } else if (sign) {
         switch (pair_ok ? knob : -1) {
           case -1: rc = launch_multistep<1, BN_SIGN, SIGN_STAGES, SIGN_NBUF>(ctx, ctx->maps_sign[cur], a); break;
           case 2: rc = launch_multistep_pair<1, NPAIR_SIGN, 2, 6>(ctx, ctx->maps_sign[cur], a); break;
@@ -648,9 +728,25 @@ int readout_device(sbg_ctx* ctx) {
     if (rc) return rc;
     StepArgs a = base_args(ctx, BN_SIGN, ctx->R, ctx->rpad);
     a.sign_in = reinterpret_cast<const int8_t*>(ctx->dSign);
-    a.e2 = ctx->dE2;
-    rc = launch_step<1, BN_SIGN, EpiMode::Readout>(ctx, ctx->tmSign, a);
-    if (rc) return rc;
+    if (ctx->kind == KIND_DENSE_FX) {
+      // E2 = sum_a 2^(8a) E2_a over the J byte planes (u8, u8, s8), exact in int64
+      CK(cudaMemsetAsync(ctx->dE2p, 0, sizeof(unsigned long long) * ctx->rpad * FX_NA, ctx->stream));
+      for (int pa = 0; pa < FX_NA; ++pa) {
+        a.e2 = ctx->dE2p + size_t(pa) * ctx->rpad;
+        a.a_unsigned = pa < FX_NA - 1;
+        rc = launch_step<1, BN_SIGN, EpiMode::Readout>(ctx, ctx->tmSign, a, &ctx->tmJplane[pa]);
+        if (rc) return rc;
+      }
+      combine_planes_e2_kernel<<<grid_for(ctx, size_t(ctx->R), 256), 256, 0, ctx->stream>>>(
+          reinterpret_cast<const long long*>(ctx->dE2p), ctx->rpad, FX_NA, int32_t(ctx->R),
+          reinterpret_cast<long long*>(ctx->dE2));
+      CK(cudaGetLastError());
+      ++ctx->launches;
+    } else {
+      a.e2 = ctx->dE2;
+      rc = launch_step<1, BN_SIGN, EpiMode::Readout>(ctx, ctx->tmSign, a);
+      if (rc) return rc;
+    }
   }
   argmin_energy_kernel<<<1, 1024, 0, ctx->stream>>>(reinterpret_cast<const long long*>(ctx->dE2),
                                                     int32_t(ctx->R), ctx->dBest);
@@ -678,9 +774,9 @@ int sbg_readout(sbg_ctx* ctx, int8_t* spins, double* energy, int64_t* best_index
   CK(cudaStreamSynchronize(ctx->stream));
   // ising_energy = -1/2 sum_i s_i (J s)_i, exact in double for integer J
   if (energy)
-    for (int64_t r = 0; r < ctx->R; ++r) energy[r] = -0.5 * double(e2[size_t(r)]);
+    for (int64_t r = 0; r < ctx->R; ++r) energy[r] = -0.5 * double(e2[size_t(r)]) * ctx->energy_scale;
   if (best_index) *best_index = best[0];
-  if (best_energy) *best_energy = -0.5 * double(best[1]);
+  if (best_energy) *best_energy = -0.5 * double(best[1]) * ctx->energy_scale;
   return SBG_OK;
 }
 
@@ -700,9 +796,9 @@ int sbg_readout_best(sbg_ctx* ctx, int8_t* best_spins, double* best_energy, int6
   if (best_spins)
     CK(cudaMemcpy(best_spins, ctx->dSign + size_t(best[0]) * ctx->npad, ctx->n, cudaMemcpyDeviceToHost));
   if (energies)
-    for (int64_t r = 0; r < ctx->R; ++r) energies[r] = -0.5 * double(e2[size_t(r)]);
+    for (int64_t r = 0; r < ctx->R; ++r) energies[r] = -0.5 * double(e2[size_t(r)]) * ctx->energy_scale;
   if (best_index) *best_index = best[0];
-  if (best_energy) *best_energy = -0.5 * double(best[1]);
+  if (best_energy) *best_energy = -0.5 * double(best[1]) * ctx->energy_scale;
   return SBG_OK;
 }
 

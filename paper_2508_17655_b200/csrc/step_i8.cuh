@@ -52,6 +52,7 @@ struct StepArgs {
   int64_t m_off;              // m = (m_dev ? *m_dev : 0) + m_off
   uint64_t M;                 // total steps
   int32_t dbg;                // dev experiments: 1 = no state traffic, 2 = no MMA (F = 0)
+  int32_t a_unsigned;         // A operand bytes are u8 (low planes of a fixed-point J)
 };
 
 template <int NPLANES, int BN>
@@ -171,8 +172,8 @@ __global__ void __launch_bounds__(384, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc_s = ptx::idesc_i8(128, BN, true, true);
-      constexpr uint32_t idesc_u = ptx::idesc_i8(128, BN, true, false);
+      const uint32_t idesc_s = ptx::idesc_i8(128, BN, !args.a_unsigned, true);
+      const uint32_t idesc_u = ptx::idesc_i8(128, BN, !args.a_unsigned, false);
       int stage = 0;
       uint32_t ph = 0;
       int lt = 0;

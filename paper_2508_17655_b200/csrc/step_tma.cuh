@@ -43,13 +43,15 @@
 
 namespace sbg {
 
-template <int NPLANES, int BN, int STAGES_, int NBUF_>
+template <int NPLANES, int BN, int STAGES_, int NBUF_, int NA_ = 1>
 struct TmaStepCfg {
   static constexpr int BM = 128;
   static constexpr int BK = 128;
-  static constexpr int A_BYTES = BM * BK;
+  static constexpr int NA = NA_;                        // J byte planes (1: int8 J; 3: fixed-point real J)
+  static constexpr int NW = NA + NPLANES - 1;           // distinct plane weights 2^(8(a+b))
+  static constexpr int A_BYTES = BM * BK;               // one J plane tile
   static constexpr int B_PLANE_BYTES = BN * BK;
-  static constexpr int STAGE_BYTES = A_BYTES + NPLANES * B_PLANE_BYTES;
+  static constexpr int STAGE_BYTES = NA * A_BYTES + NPLANES * B_PLANE_BYTES;
   static constexpr int STAGES = STAGES_;                // operand ring depth
   static constexpr int EPI_WARPS = 16;                  // 4 per TMEM lane quadrant
   static constexpr int CW = 16;                         // replicas per state chunk
@@ -59,14 +61,14 @@ struct TmaStepCfg {
   static constexpr int ST_G = CW * BM;                  // one byte plane chunk: 2 KB
   static constexpr int BUF_RAW = 3 * ST_ARR + NPLANES * ST_G;
   static constexpr int BUF_BYTES = (BUF_RAW + 1023) / 1024 * 1024;
-  static constexpr int ACC_COLS = NPLANES * BN;
-  static constexpr int TMEM_COLS = 2 * ACC_COLS;
+  static constexpr int ACC_COLS = NW * BN;              // one accumulator per plane weight
+  static constexpr int TMEM_COLS = 2 * ACC_COLS <= 256 ? 256 : 512;
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static constexpr int NUM_BARS = 2 * STAGES + 4 + 3 * NBUF;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + NBUF * BUF_BYTES + 1024 + 8 * NUM_BARS + 64;
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static_assert(BN % CW == 0, "chunking");
-  static_assert(TMEM_COLS == 256 || TMEM_COLS == 512, "TMEM allocation");
+  static_assert(2 * ACC_COLS <= 512, "TMEM allocation");
 };
 
 struct TmaMaps {
@@ -85,6 +87,7 @@ struct MultiStepArgs {
   int32_t nsteps;    // steps in this launch
   uint32_t* done;    // [num_n] tiles completed per replica block, zero at launch
   int32_t dbg;       // dev experiments: 1 = no state traffic, 2 = no MMA, 3 = no MMA and no compute
+  int32_t fx_exp;    // NA > 1: F = sum_w acc_w 2^(8w + fx_exp) (fixed-point J scale + x scale)
 };
 
 namespace dep {
@@ -108,10 +111,11 @@ __device__ __forceinline__ void wait_block(const uint32_t* done, int n, uint32_t
 }
 }  // namespace dep
 
-template <int NPLANES, int BN, int STAGES_, int NBUF_>
-__global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_>::THREADS, 1)
+template <int NPLANES, int BN, int STAGES_, int NBUF_, int NA_ = 1>
+__global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::THREADS, 1)
     gsb_multistep_kernel(const __grid_constant__ TmaMaps maps, const MultiStepArgs args) {
-  using Cfg = TmaStepCfg<NPLANES, BN, STAGES_, NBUF_>;
+  using Cfg = TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>;
+  constexpr int NA = Cfg::NA;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int NBUF = Cfg::NBUF;
   constexpr int CW = Cfg::CW;
@@ -122,8 +126,8 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_>::THREA
   const uint32_t raw_addr = ptx::smem_u32(smem_raw);
   const uint32_t base = (raw_addr + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base - raw_addr);
-  const uint32_t a_base = base;
-  const uint32_t b_base = base + STAGES * Cfg::A_BYTES;
+  const uint32_t a_base = base;                                // J plane tiles [STAGES][NA]
+  const uint32_t b_base = base + STAGES * NA * Cfg::A_BYTES;   // B plane tiles [STAGES][NPLANES]
   const uint32_t s_base = base + STAGES * Cfg::STAGE_BYTES;  // state ring
   uint8_t* s_gen = smem + STAGES * Cfg::STAGE_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + NBUF * Cfg::BUF_BYTES);
@@ -184,7 +188,10 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_>::THREA
         for (int kb = 0; kb < KB; ++kb) {
           ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
           ptx::mbar_arrive_expect_tx(full_bar(stage), Cfg::STAGE_BYTES);
-          ptx::tma_load_2d(a_base + stage * Cfg::A_BYTES, &maps.J, full_bar(stage), kb * Cfg::BK, m_blk * Cfg::BM);
+#pragma unroll
+          for (int ap = 0; ap < NA; ++ap)
+            ptx::tma_load_2d(a_base + (stage * NA + ap) * Cfg::A_BYTES, &maps.J, full_bar(stage), kb * Cfg::BK,
+                             ap * args.npad + m_blk * Cfg::BM);
 #pragma unroll
           for (int pl = 0; pl < NPLANES; ++pl)
             ptx::tma_load_2d(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES, gin, full_bar(stage),
@@ -198,8 +205,6 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_>::THREA
     }
   } else if (warp == 1) {
     if (lane == 0 && args.dbg < 2) {  // ---------------------------------- MMA issuer
-      constexpr uint32_t idesc_s = ptx::idesc_i8(128, BN, true, true);
-      constexpr uint32_t idesc_u = ptx::idesc_i8(128, BN, true, false);
       int stage = 0;
       uint32_t ph = 0;
       int lt = 0;
@@ -211,14 +216,22 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_>::THREA
         for (int kb = 0; kb < KB; ++kb) {
           ptx::mbar_wait(full_bar(stage), ph);
           ptx::tc_fence_after();
-          const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + stage * Cfg::A_BYTES);
 #pragma unroll
-          for (int pl = 0; pl < NPLANES; ++pl) {
-            const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES);
-            const uint32_t idesc = (NPLANES == 1 || pl == NPLANES - 1) ? idesc_s : idesc_u;
+          for (int ap = 0; ap < NA; ++ap) {
+            const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + (stage * NA + ap) * Cfg::A_BYTES);
 #pragma unroll
-            for (int k = 0; k < Cfg::BK / 32; ++k)
-              ptx::mma_i8(d_base + pl * BN, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            for (int pl = 0; pl < NPLANES; ++pl) {
+              const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES);
+              // plane signedness: only the top plane of a multi-plane operand is signed
+              const uint32_t idesc = ptx::idesc_i8(128, BN, NA == 1 || ap == NA - 1, NPLANES == 1 || pl == NPLANES - 1);
+              // products of equal weight 2^(8(ap+pl)) share one accumulator; the first
+              // pair of each weight (in this loop order) starts it at kb == 0
+              const int w = ap + pl;
+              const bool first_pair = ap == (w - (NPLANES - 1) > 0 ? w - (NPLANES - 1) : 0);
+#pragma unroll
+              for (int k = 0; k < Cfg::BK / 32; ++k)
+                ptx::mma_i8(d_base + w * BN, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0 || !first_pair);
+            }
           }
           ptx::mma_commit(empty_bar(stage));
           if (++stage == STAGES) {
@@ -308,7 +321,24 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_>::THREA
         const int b = ck % NBUF;
         const int col0 = c * CW + h * CWQ;
         float F[CWQ];
-        if (NPLANES == 1) {
+        if (NA > 1) {
+          // fixed-point real J: F = fl32(sum_w fl64(acc_w * 2^(8w + fx_exp))), fixed order
+          double f[CWQ];
+#pragma unroll
+          for (int j = 0; j < CWQ; ++j) f[j] = 0.0;
+#pragma unroll
+          for (int w = 0; w < Cfg::NW; ++w) {
+            uint32_t v[CWQ];
+            ptx::tmem_ld<CWQ>(t_row + w * BN + col0, v);
+            ptx::tmem_ld_wait();
+            const double sc = ldexp(1.0, 8 * w + args.fx_exp);
+#pragma unroll
+            for (int j = 0; j < CWQ; ++j)
+              f[j] = __dadd_rn(f[j], __dmul_rn(static_cast<double>(static_cast<int32_t>(v[j])), sc));
+          }
+#pragma unroll
+          for (int j = 0; j < CWQ; ++j) F[j] = __double2float_rn(f[j]);
+        } else if (NPLANES == 1) {
           uint32_t v[CWQ];
           ptx::tmem_ld<CWQ>(t_row + col0, v);
           ptx::tmem_ld_wait();

@@ -198,10 +198,15 @@ class Solver:
         n = J.shape[0]
         if J.dtype == np.int8:
             self._check(self._L.sbg_set_couplings_dense_i8(self._h, n, ptr(J)))
+        elif J.dtype == np.float32:
+            self._check(self._L.sbg_set_couplings_dense_f32(self._h, n, ptr(J)))
         else:
             J = np.ascontiguousarray(J, np.float64)
             self._check(self._L.sbg_set_couplings_dense_f64(self._h, n, ptr(J)))
         self.n = n
+        if not np.all(np.equal(np.mod(J, 1), 0)):
+            self.total_weight = graph_total_weight  # real couplings: no implied MAX-CUT graph
+            return
         # cut via the bridge (model.hpp:103-104): J = -w  =>  W = -sum_{i<j} J_ij
         self.total_weight = graph_total_weight if graph_total_weight is not None else int(
             -np.triu(J.astype(np.int64), 1).sum())
