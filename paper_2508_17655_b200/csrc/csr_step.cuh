@@ -1,17 +1,21 @@
 // GSB step for sparse integer couplings (CSR, both triangles, int8 values).
 //
-// Same semantics as the dense step (engine.cpp:55-110 on the dense view of
-// the instance); the field is the exact integer sum
+// Same semantics as the dense step (engine.cpp:55-110 on the dense view of the
+// instance); the field is the exact integer sum
 //   sign variants:  F_i = sum_k val_k * sgn(x_{col_k})
-//   fixed-point:    F_i = fl32(sum_k val_k * rint(x_{col_k} 2^30)) * 2^-30
+//   fixed-point:    F_i = fl32(sum_k val_k * q_{col_k}) * 2^-30,  q = rint(x 2^30)
 // which equals the dense tensor-core field bit for bit (zeros contribute 0).
 //
-// Layout/strategy: one CTA owns RPB whole replicas; their fp32 x vectors are
-// staged once into shared memory (so the gather x[col] is an on-chip random
-// read and x_i for the update never re-reads HBM), the CSR arrays stream from
-// L2 once per RPB replicas, and each thread updates spins i, i+blockDim, ...
-// with coalesced replica-major state accesses. Because a CTA owns its
-// replicas entirely, the in-place update has no cross-CTA hazard.
+// Layout: while stepping, the state lives SPIN-MAJOR ([npad][rp], replicas
+// contiguous) so that the SpMM gather of row j for a block of replicas is one
+// contiguous, vectorised read: a warp owns (row i, 128 replicas), lane l holds
+// replicas 4l..4l+3 (int4 / char4 / float4 accesses, 512 B per warp per nonzero).
+// The row's (col, val) pairs are loaded once, one per lane, and broadcast with
+// shuffles, so all gathers of a row are independent (memory-level parallelism).
+// The gathered operand (q or sgn x) is ping-ponged between two buffers because
+// other warps still read step t's values while row i writes step t+1's;
+// x, y, p are owned by row i and updated in place. The sbgpu API keeps the
+// replica-major layout; sbg_advance transposes in and out once per call.
 #pragma once
 
 #include <cstdint>
@@ -20,108 +24,144 @@
 
 namespace sbg {
 
-constexpr int CSR_THREADS = 512;
+constexpr int CSR_THREADS = 256;
+constexpr int CSR_RCHUNK = 128;  // replicas per warp task (32 lanes x 4)
 
-template <int RPB, bool SIGN>
+template <bool SIGN>
 __global__ void __launch_bounds__(CSR_THREADS)
-    csr_step_kernel(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-                    const int8_t* __restrict__ val, float* __restrict__ x, float* __restrict__ y,
-                    float* __restrict__ p, int64_t ld, int32_t R, PhaseConsts k) {
-  extern __shared__ float xs[];  // [RPB][n]
-  for (int rb = blockIdx.x * RPB; rb < R; rb += gridDim.x * RPB) {
-    const int nr = min(RPB, R - rb);
-    for (int t = 0; t < nr; ++t)
-      for (int i = threadIdx.x; i < n; i += blockDim.x) xs[t * n + i] = x[static_cast<size_t>(rb + t) * ld + i];
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      long long acc[RPB];
-#pragma unroll
-      for (int t = 0; t < RPB; ++t) acc[t] = 0;
-      const int kb = rowptr[i], ke = rowptr[i + 1];
-      for (int kk = kb; kk < ke; ++kk) {
-        const int j = col[kk];
-        const int v = val[kk];
-#pragma unroll
-        for (int t = 0; t < RPB; ++t) {
-          const float xj = xs[t * n + j];
-          if (SIGN)
-            acc[t] += (xj >= 0.0f) ? v : -v;
-          else
-            acc[t] += static_cast<long long>(v) * quant30(xj);
-        }
+    csr_step_sm_kernel(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                       const int8_t* __restrict__ val, const void* __restrict__ g_cur, void* __restrict__ g_next,
+                       float* __restrict__ xs, float* __restrict__ ys, float* __restrict__ ps, int64_t rp,
+                       int32_t R, PhaseConsts k) {
+  const int lane = threadIdx.x & 31;
+  const int chunks = static_cast<int>((R + CSR_RCHUNK - 1) / CSR_RCHUNK);
+  const int64_t tasks = static_cast<int64_t>(n) * chunks;
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t t = wid; t < tasks; t += nw) {
+    const int i = static_cast<int>(t / chunks);
+    const int r = static_cast<int>(t % chunks) * CSR_RCHUNK + 4 * lane;  // first of this lane's 4 replicas
+    const int kb = rowptr[i], ke = rowptr[i + 1];
+    long long acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+    for (int k0 = kb; k0 < ke; k0 += 32) {
+      const int cnt = min(32, ke - k0);
+      int jl = 0, vl = 0;
+      if (lane < cnt) {
+        jl = col[k0 + lane];
+        vl = val[k0 + lane];
       }
-#pragma unroll
-      for (int t = 0; t < RPB; ++t) {
-        if (t < nr) {
-          const size_t off = static_cast<size_t>(rb + t) * ld + i;
-          const float F = SIGN ? static_cast<float>(acc[t]) : __fmul_rn(__ll2float_rn(acc[t]), 0x1p-30f);
-          float xi = xs[t * n + i], yi = y[off], pi = p[off];
-          gsb_phase(F, xi, yi, pi, k);
-          x[off] = xi;
-          y[off] = yi;
-          p[off] = pi;
+#pragma unroll 4
+      for (int kk = 0; kk < cnt; ++kk) {
+        const int j = __shfl_sync(0xffffffffu, jl, kk);
+        const int v = __shfl_sync(0xffffffffu, vl, kk);
+        if (r < R) {
+          if (SIGN) {
+            const char4 s = *reinterpret_cast<const char4*>(static_cast<const int8_t*>(g_cur) + static_cast<size_t>(j) * rp + r);
+            acc0 += v * s.x;
+            acc1 += v * s.y;
+            acc2 += v * s.z;
+            acc3 += v * s.w;
+          } else {
+            const int4 q = *reinterpret_cast<const int4*>(static_cast<const int32_t*>(g_cur) + static_cast<size_t>(j) * rp + r);
+            acc0 += static_cast<long long>(v) * q.x;
+            acc1 += static_cast<long long>(v) * q.y;
+            acc2 += static_cast<long long>(v) * q.z;
+            acc3 += static_cast<long long>(v) * q.w;
+          }
         }
       }
     }
-    __syncthreads();
+    if (r >= R) continue;
+    const size_t off = static_cast<size_t>(i) * rp + r;
+    float4 x4 = *reinterpret_cast<const float4*>(xs + off);
+    float4 y4 = *reinterpret_cast<const float4*>(ys + off);
+    float4 p4 = *reinterpret_cast<const float4*>(ps + off);
+    float F[4];
+    const long long acc[4] = {acc0, acc1, acc2, acc3};
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      F[u] = SIGN ? static_cast<float>(acc[u]) : __fmul_rn(__ll2float_rn(acc[u]), 0x1p-30f);
+    gsb_phase(F[0], x4.x, y4.x, p4.x, k);
+    gsb_phase(F[1], x4.y, y4.y, p4.y, k);
+    gsb_phase(F[2], x4.z, y4.z, p4.z, k);
+    gsb_phase(F[3], x4.w, y4.w, p4.w, k);
+    // replicas >= R inside the last chunk are padding: their slots exist (rp) and stay inert
+    *reinterpret_cast<float4*>(xs + off) = x4;
+    *reinterpret_cast<float4*>(ys + off) = y4;
+    *reinterpret_cast<float4*>(ps + off) = p4;
+    if (SIGN) {
+      char4 s;
+      s.x = sgn8(x4.x);
+      s.y = sgn8(x4.y);
+      s.z = sgn8(x4.z);
+      s.w = sgn8(x4.w);
+      *reinterpret_cast<char4*>(static_cast<int8_t*>(g_next) + off) = s;
+    } else {
+      *reinterpret_cast<int4*>(static_cast<int32_t*>(g_next) + off) =
+          make_int4(quant30(x4.x), quant30(x4.y), quant30(x4.z), quant30(x4.w));
+    }
   }
 }
 
-// Readout on CSR: sign plane + E2[r] = sum_i s_i sum_k val_k s_{col_k}.
-__global__ void __launch_bounds__(CSR_THREADS)
+// B operand of the current (spin-major) state: sign bytes or q = rint(x 2^30).
+template <bool SIGN>
+__global__ void csr_prep_kernel(const float* __restrict__ xs, void* __restrict__ g, size_t count) {
+  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < count;
+       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    if (SIGN)
+      static_cast<int8_t*>(g)[idx] = sgn8(xs[idx]);
+    else
+      static_cast<int32_t*>(g)[idx] = quant30(xs[idx]);
+  }
+}
+
+// Replica-major [R][ld] <-> spin-major [n][rp] through 32x32 shared tiles.
+__global__ void transpose_f32_kernel(const float* __restrict__ src, float* __restrict__ dst, int32_t rows,
+                                     int32_t cols, int64_t ld_src, int64_t ld_dst) {
+  __shared__ float tile[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int r = r0 + k, c = c0 + threadIdx.x;
+    tile[k][threadIdx.x] = (r < rows && c < cols) ? src[static_cast<size_t>(r) * ld_src + c] : 0.0f;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int c = c0 + k, r = r0 + threadIdx.x;
+    if (c < cols && r < rows) dst[static_cast<size_t>(c) * ld_dst + r] = tile[threadIdx.x][k];
+  }
+}
+
+// Readout on CSR from the replica-major state: sign plane + E2[r] = sum_i s_i sum_k val_k s_{col_k}.
+constexpr int CSR_RO_THREADS = 512;
+__global__ void __launch_bounds__(CSR_RO_THREADS)
     csr_readout_kernel(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                        const int8_t* __restrict__ val, const float* __restrict__ x, int64_t ld, int32_t R,
                        uint8_t* __restrict__ sign_out, unsigned long long* __restrict__ e2) {
-  extern __shared__ float xs[];
-  __shared__ long long red[CSR_THREADS / 32];
+  extern __shared__ float xsm[];
+  __shared__ long long red[CSR_RO_THREADS / 32];
   for (int r = blockIdx.x; r < R; r += gridDim.x) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const float v = x[static_cast<size_t>(r) * ld + i];
-      xs[i] = v;
+      xsm[i] = v;
       sign_out[static_cast<size_t>(r) * ld + i] = static_cast<uint8_t>(sgn8(v));
     }
     __syncthreads();
     long long part = 0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       long long f = 0;
-      for (int kk = rowptr[i]; kk < rowptr[i + 1]; ++kk) f += (xs[col[kk]] >= 0.0f) ? val[kk] : -val[kk];
-      part += (xs[i] >= 0.0f) ? f : -f;
+      for (int kk = rowptr[i]; kk < rowptr[i + 1]; ++kk) f += (xsm[col[kk]] >= 0.0f) ? val[kk] : -val[kk];
+      part += (xsm[i] >= 0.0f) ? f : -f;
     }
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
     __syncthreads();
     if (threadIdx.x < 32) {
-      long long s = threadIdx.x < CSR_THREADS / 32 ? red[threadIdx.x] : 0;
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (threadIdx.x == 0) e2[r] = static_cast<unsigned long long>(s);
+      long long sacc = threadIdx.x < CSR_RO_THREADS / 32 ? red[threadIdx.x] : 0;
+      for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+      if (threadIdx.x == 0) e2[r] = static_cast<unsigned long long>(sacc);
     }
     __syncthreads();
   }
-}
-
-inline int csr_rpb(int32_t n) { return (2 * sizeof(float) * size_t(n) <= 200 * 1024) ? 2 : 1; }
-
-inline int launch_csr_step(cudaStream_t st, int sms, int32_t n, const int32_t* rowptr, const int32_t* col,
-                           const int8_t* val, float* x, float* y, float* p, int64_t ld, int32_t R, bool sign,
-                           PhaseConsts k, uint64_t M, uint64_t m) {
-  k.inv = 1.0f / static_cast<float>(M - m);  // host: IEEE division == __frcp_rn
-  const int rpb = csr_rpb(n);
-  const size_t smem = sizeof(float) * size_t(n) * rpb;
-  if (smem > 227 * 1024) return int(cudaErrorInvalidValue);
-  const int blocks = std::min<int>((R + rpb - 1) / rpb, sms * 4);
-#define SBG_CSR_LAUNCH(RPB_, SIGN_)                                                                     \
-  do {                                                                                                  \
-    auto kern = csr_step_kernel<RPB_, SIGN_>;                                                           \
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));                 \
-    kern<<<blocks, CSR_THREADS, smem, st>>>(n, rowptr, col, val, x, y, p, ld, R, k);                    \
-  } while (0)
-  if (rpb == 2) {
-    if (sign) SBG_CSR_LAUNCH(2, true); else SBG_CSR_LAUNCH(2, false);
-  } else {
-    if (sign) SBG_CSR_LAUNCH(1, true); else SBG_CSR_LAUNCH(1, false);
-  }
-#undef SBG_CSR_LAUNCH
-  return int(cudaGetLastError());
 }
 
 inline int launch_csr_readout(cudaStream_t st, int sms, int32_t n, const int32_t* rowptr, const int32_t* col,
@@ -130,8 +170,8 @@ inline int launch_csr_readout(cudaStream_t st, int sms, int32_t n, const int32_t
   const size_t smem = sizeof(float) * size_t(n);
   if (smem > 200 * 1024) return int(cudaErrorInvalidValue);
   cudaFuncSetAttribute(csr_readout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  csr_readout_kernel<<<std::min<int>(R, sms * 4), CSR_THREADS, smem, st>>>(n, rowptr, col, val, x, ld, R,
-                                                                           sign_out, e2);
+  csr_readout_kernel<<<std::min<int>(R, sms * 4), CSR_RO_THREADS, smem, st>>>(n, rowptr, col, val, x, ld, R,
+                                                                              sign_out, e2);
   return int(cudaGetLastError());
 }
 

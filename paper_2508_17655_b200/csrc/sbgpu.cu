@@ -89,6 +89,10 @@ struct sbg_ctx {
   TmaMaps pmaps_planes[2];               // pair kernel, fixed-point planes (B half = 32 rows)
   TmaMaps fxmaps_sign[2], fxmaps_planes[2];  // real-J kernels (B tiles of 64 / 32 rows)
   unsigned long long* dE2p = nullptr;    // real-J readout: per-J-plane partial E2 [FX_NA][rpad]
+  // CSR: spin-major working copies [npad][rp] and the ping-pong gathered operand (q int32 / sign int8)
+  float *dXs = nullptr, *dYs = nullptr, *dPs = nullptr;
+  int32_t* dQ[2] = {nullptr, nullptr};
+  int64_t rp = 0;
   uint32_t* d_done = nullptr;            // per replica-block tile counters of the multi-step kernel
   int g_cur = 0;
   int g_mode = 0;  // 0 stale, 1 sign plane valid in dG[g_cur], 4 planes valid
@@ -219,6 +223,13 @@ void free_state(sbg_ctx* ctx) {
   cudaFree(ctx->dE2);
   cudaFree(ctx->dE2p);
   ctx->dE2p = nullptr;
+  cudaFree(ctx->dXs);
+  cudaFree(ctx->dYs);
+  cudaFree(ctx->dPs);
+  cudaFree(ctx->dQ[0]);
+  cudaFree(ctx->dQ[1]);
+  ctx->dXs = ctx->dYs = ctx->dPs = nullptr;
+  ctx->dQ[0] = ctx->dQ[1] = nullptr;
   cudaFree(ctx->dBest);
   cudaFree(ctx->d_done);
   ctx->d_done = nullptr;
@@ -252,6 +263,18 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
     CK(cudaMemsetAsync(ctx->dG[0], 0, NPL * pl, ctx->stream));
     CK(cudaMemsetAsync(ctx->dG[1], 0, NPL * pl, ctx->stream));
     CK(cudaMemsetAsync(ctx->dSign, 0, pl, ctx->stream));
+    if (ctx->kind == KIND_CSR_I8) {
+      ctx->rp = round_up(R, CSR_RCHUNK);
+      const size_t sm = size_t(ctx->npad) * ctx->rp;
+      for (float** a : {&ctx->dXs, &ctx->dYs, &ctx->dPs}) {
+        CK(cudaMalloc(a, sizeof(float) * sm));
+        CK(cudaMemsetAsync(*a, 0, sizeof(float) * sm, ctx->stream));
+      }
+      for (int b = 0; b < 2; ++b) {
+        CK(cudaMalloc(&ctx->dQ[b], sizeof(int32_t) * sm));
+        CK(cudaMemsetAsync(ctx->dQ[b], 0, sizeof(int32_t) * sm, ctx->stream));
+      }
+    }
     ctx->cap_rpad = rpad;
     if (ctx->kind == KIND_DENSE_I8 || ctx->kind == KIND_DENSE_FX) {
       for (int b = 0; b < 2; ++b) {
@@ -634,10 +657,46 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
   k.inv = 0.0f;
   CK(cudaEventRecord(ctx->ev[0], ctx->stream));
   if (ctx->kind == KIND_CSR_I8) {
+    // replica-major -> spin-major, B operand, M steps (ping-pong), spin-major -> replica-major
+    const int32_t n32 = int32_t(ctx->n), R32 = int32_t(ctx->R);
+    const dim3 tb(32, 8);
+    const dim3 tg_in(unsigned((ctx->n + 31) / 32), unsigned((ctx->R + 31) / 32));
+    float* rm[3] = {ctx->dX, ctx->dY, ctx->dP};
+    float* sm[3] = {ctx->dXs, ctx->dYs, ctx->dPs};
+    for (int a = 0; a < 3; ++a) {
+      transpose_f32_kernel<<<tg_in, tb, 0, ctx->stream>>>(rm[a], sm[a], R32, n32, ctx->npad, ctx->rp);
+      CK(cudaGetLastError());
+      ++ctx->launches;
+    }
+    const size_t cnt = size_t(ctx->npad) * ctx->rp;
+    if (sign)
+      csr_prep_kernel<true><<<grid_for(ctx, cnt, 256), 256, 0, ctx->stream>>>(ctx->dXs, ctx->dQ[0], cnt);
+    else
+      csr_prep_kernel<false><<<grid_for(ctx, cnt, 256), 256, 0, ctx->stream>>>(ctx->dXs, ctx->dQ[0], cnt);
+    CK(cudaGetLastError());
+    ++ctx->launches;
+    const int64_t tasks = ctx->n * ((ctx->R + CSR_RCHUNK - 1) / CSR_RCHUNK);
+    const int blocks = int(std::min<int64_t>((tasks + CSR_THREADS / 32 - 1) / (CSR_THREADS / 32), int64_t(ctx->sms) * 8));
+    int cur = 0;
     for (uint64_t m = m_begin; m < m_end; ++m) {
-      rc = launch_csr_step(ctx->stream, ctx->sms, int32_t(ctx->n), ctx->d_rowptr, ctx->d_col, ctx->d_val,
-                           ctx->dX, ctx->dY, ctx->dP, ctx->npad, int32_t(ctx->R), sign, k, prm->steps, m);
-      if (rc) return ctx->fail(SBG_ERR_CUDA, "CSR step launch failed: %s", cudaGetErrorString(cudaError_t(rc)));
+      PhaseConsts km = k;
+      km.inv = 1.0f / static_cast<float>(prm->steps - m);  // == __frcp_rn(M - m)
+      if (sign)
+        csr_step_sm_kernel<true><<<blocks, CSR_THREADS, 0, ctx->stream>>>(
+            n32, ctx->d_rowptr, ctx->d_col, ctx->d_val, ctx->dQ[cur], ctx->dQ[cur ^ 1], ctx->dXs, ctx->dYs, ctx->dPs,
+            ctx->rp, R32, km);
+      else
+        csr_step_sm_kernel<false><<<blocks, CSR_THREADS, 0, ctx->stream>>>(
+            n32, ctx->d_rowptr, ctx->d_col, ctx->d_val, ctx->dQ[cur], ctx->dQ[cur ^ 1], ctx->dXs, ctx->dYs, ctx->dPs,
+            ctx->rp, R32, km);
+      CK(cudaGetLastError());
+      ++ctx->launches;
+      cur ^= 1;
+    }
+    const dim3 tg_out(unsigned((ctx->R + 31) / 32), unsigned((ctx->n + 31) / 32));
+    for (int a = 0; a < 3; ++a) {
+      transpose_f32_kernel<<<tg_out, tb, 0, ctx->stream>>>(sm[a], rm[a], n32, R32, ctx->rp, ctx->npad);
+      CK(cudaGetLastError());
       ++ctx->launches;
     }
   } else {
