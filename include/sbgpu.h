@@ -148,6 +148,28 @@ int sbg_run_seeded(sbg_ctx* ctx, const sbg_params* params, int64_t R, int32_t in
                    uint64_t master, uint64_t tag, int64_t replica_offset, int8_t* spins,
                    double* energy, int64_t* best_index, sbg_timing* timing);
 
+/* ---- Row sharding (C5: N too large for one GPU) ----------------------------
+ * Rank `rank` of `world` owns spins [row0, row0 + rows) with rows = kpad/world,
+ * kpad = n_global rounded up to 128*world; Jrows is its rows of J (valid x n_global,
+ * row-major). Its x, y, p cover its spins for every replica; the B operand G (signs
+ * of ALL spins) is replicated: each step's epilogue writes this rank's slab into
+ * its own G and, over NVLink, into every peer's G, then releases per-replica-block
+ * completion counters on every rank (the row-chunked coupling_matvec of
+ * kernels.hpp:33-46 spread over GPUs). Sign variants only (dsb/gdsb).
+ * Order: set_couplings_rows -> set_state/init_state -> (exchange buffers) ->
+ * shard_set_peers -> shard_prepare -> shard_push_slab on all ranks -> barrier -> advance. */
+int sbg_set_couplings_rows_i8(sbg_ctx* ctx, int64_t n_global, int32_t world, int32_t rank, const int8_t* Jrows);
+int sbg_shard_info(const sbg_ctx* ctx, int64_t* row0, int64_t* rows_valid, int64_t* rows_padded, int64_t* kpad);
+int sbg_shard_buffers(sbg_ctx* ctx, void** g0, void** g1, void** done);
+int sbg_shard_set_peers(sbg_ctx* ctx, int32_t npeers, void* const* g0, void* const* g1, void* const* done);
+int sbg_shard_prepare(sbg_ctx* ctx, int32_t variant);
+int sbg_shard_push_slab(sbg_ctx* ctx);
+/* CUDA IPC export/open of (G0, G1, done) for peers in other processes (192 bytes). */
+int sbg_shard_ipc_export(sbg_ctx* ctx, void* out192);
+int sbg_shard_ipc_open(sbg_ctx* ctx, const void* in192, void** g0, void** g1, void** done);
+/* This rank's share of E2 = sum_i s_i (J s)_i over its spins; sum over ranks, energy = -E2/2. */
+int sbg_readout_partial(sbg_ctx* ctx, int64_t* e2);
+
 int sbg_synchronize(sbg_ctx* ctx);
 /* Kernel launches issued by this context since creation (bench evidence). */
 int64_t sbg_kernel_launches(const sbg_ctx* ctx);

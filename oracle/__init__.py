@@ -212,6 +212,7 @@ class _Orc:
         L.orc_step_f32_fx.argtypes = [C.c_int, _i64, _P, C.c_int, _i64, _i64, _P, _P, _P, _u64, _u64, _f32, _f32,
                                       _f32]
         L.orc_energy2_fx.argtypes = [_i64, _P, _i64, _i64, _P, _P]
+        L.orc_phase_batch_f32.argtypes = [_i64, _P, _P, _P, _P, _f32, _f32, _f32, _u64, _u64]
 
     def derive_seed(self, master: int, keys) -> int:
         k = np.asarray(list(keys), dtype=np.uint64)
@@ -330,6 +331,13 @@ class _Orc:
     def argmin(self, v):
         v = np.ascontiguousarray(v, np.int64)
         return int(self.lib.orc_argmin_i64(len(v), _ptr(v)))
+
+    def phase_batch(self, F, x, y, p, a, c, dt, m, M):
+        """In-place fp32 phase update (GPU op order) of contiguous float32 arrays."""
+        F = np.ascontiguousarray(F, np.float32)
+        for v in (x, y, p):
+            assert v.dtype == np.float32 and v.flags["C_CONTIGUOUS"]
+        self.lib.orc_phase_batch_f32(F.size, _ptr(F), _ptr(x), _ptr(y), _ptr(p), a, c, dt, m, M)
 
     def fx_quantize(self, J):
         J = np.ascontiguousarray(J, np.float32)

@@ -536,3 +536,11 @@ void orc_energy2_fx(int64_t n, const uint8_t* planes, int64_t R, int64_t ld, con
   }
   free(s);
 }
+
+/* Phase update over arrays with given fields (fields computed elsewhere, e.g. by a
+ * row-sharded model); same op order as orc_phase_f32. */
+void orc_phase_batch_f32(int64_t count, const float* F, float* x, float* y, float* p, float a, float c, float dt,
+                         uint64_t m, uint64_t M) {
+  const float inv = 1.0f / (float)(M - m);
+  for (int64_t k = 0; k < count; ++k) orc_phase_f32(F[k], x + k, y + k, p + k, a, c, dt, inv);
+}

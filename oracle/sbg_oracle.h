@@ -82,6 +82,9 @@ void orc_step_f32_csr(int variant, int64_t n, const int32_t* rowptr, const int32
 /* The elementwise phase alone (engine.cpp:86-103 in fp32, GPU op order). */
 void orc_phase_f32(float F, float* x, float* y, float* p, float a, float c, float dt, float inv);
 
+void orc_phase_batch_f32(int64_t count, const float* F, float* x, float* y, float* p, float a, float c, float dt,
+                         uint64_t m, uint64_t M);
+
 /* ---- readout ---------------------------------------------------------- */
 /* E2[r] = sum_i s_i (J s)_i with s = sgn(x) (sgn(0)=+1, model.cpp:161-165);
  * energy = -E2/2 (model.cpp:112-123), exact for integer J. */

@@ -26,6 +26,8 @@ EXPORTS = [
     "sbg_set_couplings_csr_i8", "sbg_n", "sbg_set_state", "sbg_init_state", "sbg_get_state", "sbg_advance",
     "sbg_readout", "sbg_readout_best", "sbg_fields_sign", "sbg_fields_fixed", "sbg_run", "sbg_run_seeded", "sbg_synchronize",
     "sbg_kernel_launches", "sbg_state_device", "sbg_last_advance_ms", "sbg_success_tts", "sbg_tune_wigner_f64",
+    "sbg_set_couplings_rows_i8", "sbg_shard_info", "sbg_shard_buffers", "sbg_shard_set_peers", "sbg_shard_prepare",
+    "sbg_shard_push_slab", "sbg_shard_ipc_export", "sbg_shard_ipc_open", "sbg_readout_partial",
 ]
 
 
@@ -97,6 +99,15 @@ def lib() -> C.CDLL:
     L.sbg_last_advance_ms.argtypes = [P]
     L.sbg_success_tts.argtypes = [i64, i64, f64, P]
     L.sbg_tune_wigner_f64.argtypes = [i64, P, f64, P, P]
+    L.sbg_set_couplings_rows_i8.argtypes = [P, i64, i32, i32, P]
+    L.sbg_shard_info.argtypes = [P, P, P, P, P]
+    L.sbg_shard_buffers.argtypes = [P, P, P, P]
+    L.sbg_shard_set_peers.argtypes = [P, i32, P, P, P]
+    L.sbg_shard_prepare.argtypes = [P, i32]
+    L.sbg_shard_push_slab.argtypes = [P]
+    L.sbg_shard_ipc_export.argtypes = [P, P]
+    L.sbg_shard_ipc_open.argtypes = [P, P, P, P, P]
+    L.sbg_readout_partial.argtypes = [P, P]
     _lib = L
     return L
 

@@ -63,18 +63,26 @@ struct Xoshiro {  // rng.hpp:44-77
 // mode: 0 uniform_random, 1 chaos_probe (engine.cpp:25-39), 2 small_uniform.
 constexpr int INIT_THREADS = 64;
 
+// Row-sharded instances (spins row0 .. row0+n-1 of n_global): the replica's
+// stream is walked past the draws of the other ranks' spins (x_i is draw i,
+// y_i is draw n_global + i), so every rank reproduces its slice of the
+// unsharded initial state exactly.
 __global__ void __launch_bounds__(INIT_THREADS)
     init_state_kernel(float* __restrict__ x, float* __restrict__ y, float* __restrict__ p, int32_t n,
                       int64_t ld, int32_t R, int32_t mode, uint64_t master, uint64_t tag,
-                      int64_t offset) {
+                      int64_t offset, int64_t n_global = -1, int64_t row0 = 0) {
   __shared__ float tile[INIT_THREADS][33];
   const int r0 = blockIdx.x * INIT_THREADS;
   const int r = r0 + threadIdx.x;
   Xoshiro g(derive_seed2(master, tag, static_cast<uint64_t>(offset + r)));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = INIT_THREADS / 32;
+  if (n_global < 0) n_global = n;
   for (int pass = 0; pass < 2; ++pass) {  // pass 0: x, pass 1: y
     float* dst = pass == 0 ? x : y;
+    if (r < R && (pass == 0 || mode == 2)) {  // skip the draws of spins before this shard
+      for (int64_t s = 0; s < row0; ++s) g.next();
+    }
     for (int i0 = 0; i0 < n; i0 += 32) {
       const int cnt = min(32, n - i0);
 #pragma unroll 4
@@ -100,6 +108,9 @@ __global__ void __launch_bounds__(INIT_THREADS)
       }
       __syncthreads();
     }
+    if (r < R && (pass == 0 || mode == 2)) {  // ... and after it
+      for (int64_t s = row0 + n; s < n_global; ++s) g.next();
+    }
   }
   // p = 1 (coalesced by the same row walk)
   for (int t = warp; t < INIT_THREADS; t += nwarps) {
@@ -110,21 +121,26 @@ __global__ void __launch_bounds__(INIT_THREADS)
 
 // Build the MMA B operand of the current state: nplanes == 1 -> sign plane
 // (+-1, padding 0); nplanes == 4 -> byte planes of q = rint(x * 2^30).
+// G is [nplanes][rpad][g_ld]; this writes columns col0 .. col0+npad-1 (a row
+// shard's slab; the whole width when unsharded: g_ld = npad, col0 = 0).
 __global__ void prep_planes_kernel(const float* __restrict__ x, uint8_t* __restrict__ G, int32_t n,
-                                   int32_t npad, int64_t ld, int32_t R, int32_t rpad, int32_t nplanes) {
+                                   int32_t npad, int64_t ld, int32_t R, int32_t rpad, int32_t nplanes,
+                                   int64_t g_ld = -1, int64_t col0 = 0) {
+  if (g_ld < 0) g_ld = npad;
   const size_t total = static_cast<size_t>(rpad) * npad;
-  const size_t plane_stride = total;
+  const size_t plane_stride = static_cast<size_t>(rpad) * g_ld;
   for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const int r = static_cast<int>(idx / npad);
     const int i = static_cast<int>(idx % npad);
     const bool ok = r < R && i < n;
     const float v = ok ? x[static_cast<size_t>(r) * ld + i] : 0.0f;
+    const size_t gi = static_cast<size_t>(r) * g_ld + col0 + i;
     if (nplanes == 1) {
-      G[idx] = ok ? static_cast<uint8_t>(sgn8(v)) : 0;
+      G[gi] = ok ? static_cast<uint8_t>(sgn8(v)) : 0;
     } else {
       const uint32_t q = static_cast<uint32_t>(quant30(v));
-      for (int pl = 0; pl < nplanes; ++pl) G[pl * plane_stride + idx] = static_cast<uint8_t>(q >> (8 * pl));
+      for (int pl = 0; pl < nplanes; ++pl) G[pl * plane_stride + gi] = static_cast<uint8_t>(q >> (8 * pl));
     }
   }
 }

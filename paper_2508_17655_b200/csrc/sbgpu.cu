@@ -93,6 +93,13 @@ struct sbg_ctx {
   float *dXs = nullptr, *dYs = nullptr, *dPs = nullptr;
   int32_t* dQ[2] = {nullptr, nullptr};
   int64_t rp = 0;
+  // Row sharding (C5): this context owns spins [row0, row0 + npad) of an n_global problem;
+  // the contraction runs over kpad = padded n_global columns. Unsharded: n_global = n, row0 = 0.
+  bool sharded = false;
+  int64_t n_global = 0, kpad = 0, row0 = 0, num_m_total = 0;
+  uint32_t done_base = 0;  // done[] counters run on across launches (peers increment them)
+  std::vector<uint8_t*> peer_g0, peer_g1;
+  std::vector<uint32_t*> peer_done;
   uint32_t* d_done = nullptr;            // per replica-block tile counters of the multi-step kernel
   int g_cur = 0;
   int g_mode = 0;  // 0 stale, 1 sign plane valid in dG[g_cur], 4 planes valid
@@ -109,6 +116,9 @@ struct sbg_ctx {
     return code;
   }
 };
+
+// Width (bytes per replica row) of the B-operand buffers: all spins of the problem.
+int64_t gdim(const sbg_ctx* ctx) { return ctx->sharded ? ctx->kpad : ctx->npad; }
 
 #define CK(call)                                                                          \
   do {                                                                                    \
@@ -191,10 +201,11 @@ int launch_multistep(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& a) 
   const int64_t tiles = int64_t(a.num_m) * a.num_n * a.nsteps;
   // persistent: one CTA per SM (all must be co-resident for the dependency walk)
   const int grid = int(std::min<int64_t>(tiles, ctx->sms));
-  CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * a.num_n, ctx->stream));
+  if (!ctx->sharded) CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * a.num_n, ctx->stream));
   kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(maps, a);
   CK(cudaGetLastError());
   ++ctx->launches;
+  if (ctx->sharded) ctx->done_base += uint32_t(a.nsteps * a.num_m_total);
   return SBG_OK;
 }
 
@@ -250,18 +261,19 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
     free_state(ctx);
     const size_t st = sizeof(float) * size_t(rpad) * ctx->npad;
     const size_t pl = size_t(rpad) * ctx->npad;
+    const size_t gpl = size_t(rpad) * gdim(ctx);  // B operand spans all spins (global when sharded)
     CK(cudaMalloc(&ctx->dX, st));
     CK(cudaMalloc(&ctx->dY, st));
     CK(cudaMalloc(&ctx->dP, st));
-    CK(cudaMalloc(&ctx->dG[0], NPL * pl));
-    CK(cudaMalloc(&ctx->dG[1], NPL * pl));
+    CK(cudaMalloc(&ctx->dG[0], NPL * gpl));
+    CK(cudaMalloc(&ctx->dG[1], NPL * gpl));
     CK(cudaMalloc(&ctx->dSign, pl));
     CK(cudaMalloc(&ctx->dE2, sizeof(unsigned long long) * rpad));
     CK(cudaMalloc(&ctx->dE2p, sizeof(unsigned long long) * rpad * FX_NA));
     CK(cudaMalloc(&ctx->dBest, 2 * sizeof(long long)));
     CK(cudaMalloc(&ctx->d_done, sizeof(uint32_t) * (rpad / 16 + 1)));
-    CK(cudaMemsetAsync(ctx->dG[0], 0, NPL * pl, ctx->stream));
-    CK(cudaMemsetAsync(ctx->dG[1], 0, NPL * pl, ctx->stream));
+    CK(cudaMemsetAsync(ctx->dG[0], 0, NPL * gpl, ctx->stream));
+    CK(cudaMemsetAsync(ctx->dG[1], 0, NPL * gpl, ctx->stream));
     CK(cudaMemsetAsync(ctx->dSign, 0, pl, ctx->stream));
     if (ctx->kind == KIND_CSR_I8) {
       ctx->rp = round_up(R, CSR_RCHUNK);
@@ -278,9 +290,9 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
     ctx->cap_rpad = rpad;
     if (ctx->kind == KIND_DENSE_I8 || ctx->kind == KIND_DENSE_FX) {
       for (int b = 0; b < 2; ++b) {
-        int rc = encode_2d_u8(ctx, &ctx->tmG_sign[b], ctx->dG[b], ctx->npad, rpad, 128, BN_SIGN);
+        int rc = encode_2d_u8(ctx, &ctx->tmG_sign[b], ctx->dG[b], gdim(ctx), rpad, 128, BN_SIGN);
         if (rc) return rc;
-        rc = encode_2d_u8(ctx, &ctx->tmG_planes[b], ctx->dG[b], ctx->npad, NPL * rpad, 128, BN_PLANE);
+        rc = encode_2d_u8(ctx, &ctx->tmG_planes[b], ctx->dG[b], gdim(ctx), NPL * rpad, 128, BN_PLANE);
         if (rc) return rc;
       }
       int rc = encode_2d_u8(ctx, &ctx->tmSign, ctx->dSign, ctx->npad, rpad, 128, BN_SIGN);
@@ -295,11 +307,13 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
     // Per B buffer b: output maps (the next step's B operand lands in the other buffer).
     CUtensorMap gout_sign[2], gout_planes[2];
     for (int b = 0; b < 2; ++b) {
-      int rc = encode_2d(ctx, &gout_sign[b], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[b], ctx->n, R, ctx->npad, 128,
+      // stores of this shard's slab land at columns row0 + i; clip at the valid global width
+      const uint64_t gvalid = uint64_t(ctx->sharded ? ctx->n_global : ctx->n);
+      int rc = encode_2d(ctx, &gout_sign[b], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[b], gvalid, R, gdim(ctx), 128,
                          CW, CU_TENSOR_MAP_SWIZZLE_NONE);
       if (rc) return rc;
-      rc = encode_2d(ctx, &gout_planes[b], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[b], ctx->n, NPL * rpad,
-                     ctx->npad, 128, CW, CU_TENSOR_MAP_SWIZZLE_NONE);
+      rc = encode_2d(ctx, &gout_planes[b], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[b], gvalid, NPL * rpad,
+                     gdim(ctx), 128, CW, CU_TENSOR_MAP_SWIZZLE_NONE);
       if (rc) return rc;
     }
     CUtensorMap X, Y, P;
@@ -345,10 +359,13 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
   return SBG_OK;
 }
 
-int prep_planes(sbg_ctx* ctx, const float* x, uint8_t* G, int nplanes, int64_t R, int64_t rpad) {
+int prep_planes(sbg_ctx* ctx, const float* x, uint8_t* G, int nplanes, int64_t R, int64_t rpad,
+                bool into_global = false) {
   const size_t total = size_t(rpad) * ctx->npad;
+  const int64_t g_ld = into_global ? gdim(ctx) : ctx->npad;
+  const int64_t col0 = into_global && ctx->sharded ? ctx->row0 : 0;
   prep_planes_kernel<<<grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(
-      x, G, int32_t(ctx->n), int32_t(ctx->npad), ctx->npad, int32_t(R), int32_t(rpad), nplanes);
+      x, G, int32_t(ctx->n), int32_t(ctx->npad), ctx->npad, int32_t(R), int32_t(rpad), nplanes, g_ld, col0);
   CK(cudaGetLastError());
   ++ctx->launches;
   return SBG_OK;
@@ -363,6 +380,7 @@ StepArgs base_args(const sbg_ctx* ctx, int BN, int64_t R, int64_t rpad) {
   a.rpad = int32_t(rpad);
   a.num_m = int32_t(ctx->npad / 128);
   a.num_n = int32_t(rpad / BN);
+  a.kpad = int32_t(ctx->sharded ? ctx->kpad : ctx->npad);
   a.ld = ctx->npad;
   return a;
 }
@@ -621,8 +639,9 @@ int sbg_init_state(sbg_ctx* ctx, int64_t R, int32_t mode, uint64_t master, uint6
   int rc = ensure_state(ctx, R);
   if (rc) return rc;
   const int blocks = int((R + INIT_THREADS - 1) / INIT_THREADS);
-  init_state_kernel<<<blocks, INIT_THREADS, 0, ctx->stream>>>(ctx->dX, ctx->dY, ctx->dP, int32_t(ctx->n),
-                                                              ctx->npad, int32_t(R), mode, master, tag, offset);
+  init_state_kernel<<<blocks, INIT_THREADS, 0, ctx->stream>>>(
+      ctx->dX, ctx->dY, ctx->dP, int32_t(ctx->n), ctx->npad, int32_t(R), mode, master, tag, offset,
+      ctx->sharded ? ctx->n_global : ctx->n, ctx->sharded ? ctx->row0 : 0);
   CK(cudaGetLastError());
   ++ctx->launches;
   return SBG_OK;
@@ -702,7 +721,7 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
   } else {
     const int need = sign ? 1 : NPL;
     if (ctx->g_mode != need) {
-      rc = prep_planes(ctx, ctx->dX, ctx->dG[ctx->g_cur], need, ctx->R, ctx->rpad);
+      rc = prep_planes(ctx, ctx->dX, ctx->dG[ctx->g_cur], need, ctx->R, ctx->rpad, /*into_global=*/true);
       if (rc) return rc;
       ctx->g_mode = need;
     }
@@ -727,14 +746,26 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
       a.t_begin = m;
       a.nsteps = int32_t(ns);
       a.done = ctx->d_done;
-      a.dbg = dev_knob("SBG_STEP_DBG");
       const int cur = ctx->g_cur;
+      a.kpad = int32_t(ctx->sharded ? ctx->kpad : ctx->npad);
+      a.num_m_total = int32_t(ctx->sharded ? ctx->num_m_total : ctx->npad / 128);
+      a.col0 = int32_t(ctx->sharded ? ctx->row0 : 0);
+      a.done_base = ctx->sharded ? ctx->done_base : 0;
+      a.g_ld = ctx->sharded ? ctx->kpad : ctx->npad;
+      a.npeers = ctx->sharded ? int32_t(ctx->peer_done.size()) : 0;
+      for (int pr = 0; pr < a.npeers; ++pr) {
+        // step parity 0 writes buffer cur^1, parity 1 buffer cur (as the local Gout maps)
+        a.peer_g[0][pr] = cur == 0 ? ctx->peer_g1[size_t(pr)] : ctx->peer_g0[size_t(pr)];
+        a.peer_g[1][pr] = cur == 0 ? ctx->peer_g0[size_t(pr)] : ctx->peer_g1[size_t(pr)];
+        a.peer_done[pr] = ctx->peer_done[size_t(pr)];
+      }
+      a.dbg = dev_knob("SBG_STEP_DBG");
       // Defaults (measured on B200, tools/step_driver.py): sign variants on CTA pairs
       // (3 operand stages, 4 state buffers): 73 us/step at N=2000, R=8192, vs 83 us
       // single-CTA; fixed-point planes single-CTA (3, 2): 18.5 us/step at R=1024 vs
       // 20.4 us on pairs. SBG_STEP_CFG selects sweep alternatives (dev only).
       const int knob = dev_knob("SBG_STEP_CFG");
-      const bool pair_ok = (ctx->npad % 256) == 0;
+      const bool pair_ok = (ctx->npad % 256) == 0 && !ctx->sharded;
       if (fx) {
         // real-valued J: 3 J planes x (sign | 4 x-planes), single-CTA
         rc = sign ? launch_multistep<1, BN_FX_SIGN, 2, 4, FX_NA>(ctx, ctx->fxmaps_sign[cur], a)
@@ -990,6 +1021,158 @@ int sbg_run_seeded(sbg_ctx* ctx, const sbg_params* prm, int64_t R, int32_t init_
   rc = sbg_init_state(ctx, R, init_mode, master, tag, offset);
   if (rc) return rc;
   return run_tail(ctx, prm, nullptr, spins, energy, best_index, timing);
+}
+
+// ------------------------------------------------------------------ row sharding (C5)
+
+int sbg_set_couplings_rows_i8(sbg_ctx* ctx, int64_t n_global, int32_t world, int32_t rank, const int8_t* Jrows) {
+  CHECK_CTX(ctx);
+  if (n_global < 1 || world < 1 || world > 8 || rank < 0 || rank >= world || !Jrows)
+    return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "bad row-shard arguments");
+  const int64_t kpad = round_up(n_global, int64_t(128) * world);
+  const int64_t rows = kpad / world;  // multiple of 128
+  const int64_t row0 = int64_t(rank) * rows;
+  const int64_t valid = std::max<int64_t>(0, std::min<int64_t>(rows, n_global - row0));
+  for (int64_t i = 0; i < valid; ++i) {
+    if (Jrows[i * n_global + row0 + i] != 0) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "coupling diagonal must be zero");
+    for (int64_t j = 0; j < n_global; ++j)
+      if (Jrows[i * n_global + j] == -128)
+        return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "int8 couplings must lie in [-127, 127]");
+  }
+  CK(cudaSetDevice(ctx->device));
+  cudaStreamSynchronize(ctx->stream);
+  free_state(ctx);
+  cudaFree(ctx->dJ);
+  ctx->dJ = nullptr;
+  CK(cudaMalloc(&ctx->dJ, size_t(rows) * kpad));
+  CK(cudaMemsetAsync(ctx->dJ, 0, size_t(rows) * kpad, ctx->stream));
+  if (valid > 0)
+    CK(cudaMemcpy2DAsync(ctx->dJ, kpad, Jrows, n_global, n_global, valid, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->kind = KIND_DENSE_I8;
+  ctx->energy_scale = 1.0;
+  ctx->sharded = true;
+  ctx->n = valid;
+  ctx->npad = rows;
+  ctx->n_global = n_global;
+  ctx->kpad = kpad;
+  ctx->row0 = row0;
+  ctx->num_m_total = kpad / 128;
+  ctx->done_base = 0;
+  ctx->peer_g0.clear();
+  ctx->peer_g1.clear();
+  ctx->peer_done.clear();
+  if (valid == 0) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "rank owns no spins (too many ranks for n)");
+  return encode_2d_u8(ctx, &ctx->tmJ, ctx->dJ, kpad, rows, 128, 128);
+}
+
+int sbg_shard_info(const sbg_ctx* ctx, int64_t* row0, int64_t* rows_valid, int64_t* rows_padded, int64_t* kpad) {
+  if (!ctx || !ctx->sharded) return SBG_ERR_STATE;
+  if (row0) *row0 = ctx->row0;
+  if (rows_valid) *rows_valid = ctx->n;
+  if (rows_padded) *rows_padded = ctx->npad;
+  if (kpad) *kpad = ctx->kpad;
+  return SBG_OK;
+}
+
+int sbg_shard_buffers(sbg_ctx* ctx, void** g0, void** g1, void** done) {
+  CHECK_CTX(ctx);
+  if (!ctx->sharded || !ctx->dG[0]) return ctx->fail(SBG_ERR_STATE, "row shard with state required");
+  if (g0) *g0 = ctx->dG[0];
+  if (g1) *g1 = ctx->dG[1];
+  if (done) *done = ctx->d_done;
+  return SBG_OK;
+}
+
+int sbg_shard_set_peers(sbg_ctx* ctx, int32_t npeers, void* const* g0, void* const* g1, void* const* done) {
+  CHECK_CTX(ctx);
+  if (!ctx->sharded) return ctx->fail(SBG_ERR_STATE, "not a row shard");
+  if (npeers < 0 || npeers > MAX_PEERS) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "at most 7 peers");
+  ctx->peer_g0.assign(size_t(npeers), nullptr);
+  ctx->peer_g1.assign(size_t(npeers), nullptr);
+  ctx->peer_done.assign(size_t(npeers), nullptr);
+  for (int i = 0; i < npeers; ++i) {
+    ctx->peer_g0[size_t(i)] = static_cast<uint8_t*>(g0[i]);
+    ctx->peer_g1[size_t(i)] = static_cast<uint8_t*>(g1[i]);
+    ctx->peer_done[size_t(i)] = static_cast<uint32_t*>(done[i]);
+  }
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * (ctx->rpad / 16 + 1), ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->done_base = 0;
+  return SBG_OK;
+}
+
+// Build this shard's slab of the step-0 B operand (sign variants) in the local G buffer.
+int sbg_shard_prepare(sbg_ctx* ctx, int32_t variant) {
+  CHECK_CTX(ctx);
+  if (!ctx->sharded || !ctx->dX) return ctx->fail(SBG_ERR_STATE, "row shard with state required");
+  if (!is_sign_variant(variant)) return ctx->fail(SBG_ERR_UNSUPPORTED, "row sharding supports dsb/gdsb");
+  CK(cudaSetDevice(ctx->device));
+  int rc = prep_planes(ctx, ctx->dX, ctx->dG[ctx->g_cur], 1, ctx->R, ctx->rpad, /*into_global=*/true);
+  if (rc) return rc;
+  ctx->g_mode = 1;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SBG_OK;
+}
+
+// Copy this shard's slab of the current B operand into every peer's buffer.
+int sbg_shard_push_slab(sbg_ctx* ctx) {
+  CHECK_CTX(ctx);
+  if (!ctx->sharded) return ctx->fail(SBG_ERR_STATE, "not a row shard");
+  CK(cudaSetDevice(ctx->device));
+  for (size_t i = 0; i < ctx->peer_g0.size(); ++i) {
+    uint8_t* dst = (ctx->g_cur == 0 ? ctx->peer_g0[i] : ctx->peer_g1[i]) + ctx->row0;
+    const uint8_t* src = ctx->dG[ctx->g_cur] + ctx->row0;
+    CK(cudaMemcpy2DAsync(dst, ctx->kpad, src, ctx->kpad, ctx->npad, ctx->R, cudaMemcpyDefault, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SBG_OK;
+}
+
+// Export this shard's buffers for cross-process peers (3 CUDA IPC handles, 64 B each).
+int sbg_shard_ipc_export(sbg_ctx* ctx, void* out192) {
+  CHECK_CTX(ctx);
+  if (!ctx->sharded || !ctx->dG[0] || !out192) return ctx->fail(SBG_ERR_STATE, "row shard with state required");
+  CK(cudaSetDevice(ctx->device));
+  cudaIpcMemHandle_t h[3];
+  CK(cudaIpcGetMemHandle(&h[0], ctx->dG[0]));
+  CK(cudaIpcGetMemHandle(&h[1], ctx->dG[1]));
+  CK(cudaIpcGetMemHandle(&h[2], ctx->d_done));
+  std::memcpy(out192, h, sizeof h);
+  return SBG_OK;
+}
+
+int sbg_shard_ipc_open(sbg_ctx* ctx, const void* in192, void** g0, void** g1, void** done) {
+  CHECK_CTX(ctx);
+  if (!in192) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "null handles");
+  CK(cudaSetDevice(ctx->device));
+  cudaIpcMemHandle_t h[3];
+  std::memcpy(h, in192, sizeof h);
+  void* p[3] = {nullptr, nullptr, nullptr};
+  for (int i = 0; i < 3; ++i) CK(cudaIpcOpenMemHandle(&p[i], h[i], cudaIpcMemLazyEnablePeerAccess));
+  *g0 = p[0];
+  *g1 = p[1];
+  *done = p[2];
+  return SBG_OK;
+}
+
+// This shard's share of E2 (sum over its spins i of s_i (J s)_i), from the full sign
+// plane G[cur] (all spins, sign variants after a step or sbg_shard_prepare + push).
+int sbg_readout_partial(sbg_ctx* ctx, int64_t* e2) {
+  CHECK_CTX(ctx);
+  if (!ctx->sharded || !ctx->dX || ctx->g_mode != 1) return ctx->fail(SBG_ERR_STATE, "sign-variant row shard required");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemsetAsync(ctx->dE2, 0, sizeof(unsigned long long) * ctx->rpad, ctx->stream));
+  StepArgs a = base_args(ctx, BN_SIGN, ctx->R, ctx->rpad);
+  a.sign_in = reinterpret_cast<const int8_t*>(ctx->dG[ctx->g_cur]) + ctx->row0;
+  a.sign_ld = ctx->kpad;
+  a.e2 = ctx->dE2;
+  int rc = launch_step<1, BN_SIGN, EpiMode::Readout>(ctx, ctx->tmG_sign[ctx->g_cur], a);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(e2, ctx->dE2, sizeof(long long) * ctx->R, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return SBG_OK;
 }
 
 int sbg_synchronize(sbg_ctx* ctx) {

@@ -53,6 +53,8 @@ struct StepArgs {
   uint64_t M;                 // total steps
   int32_t dbg;                // dev experiments: 1 = no state traffic, 2 = no MMA (F = 0)
   int32_t a_unsigned;         // A operand bytes are u8 (low planes of a fixed-point J)
+  int32_t kpad;               // K extent (global padded n; == npad unless row-sharded)
+  int64_t sign_ld;            // Readout: row pitch of sign_in (sign_in may point into a wider G)
 };
 
 template <int NPLANES, int BN>
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(384, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int num_tiles = args.num_m * args.num_n;
-  const int KB = args.npad / Cfg::BK;
+  const int KB = (args.kpad ? args.kpad : args.npad) / Cfg::BK;
 
   if (warp == 0) {
     // ---------------------------------------------------------- TMA producer
@@ -300,7 +302,7 @@ __global__ void __launch_bounds__(384, 1)
           for (int j = 0; j < CW; ++j) {
             long long part = 0;
             if (row_ok && r0 + j < args.R) {
-              const int s = args.sign_in[static_cast<size_t>(r0 + j) * args.npad + row];
+              const int s = args.sign_in[static_cast<size_t>(r0 + j) * (args.sign_ld ? args.sign_ld : args.npad) + row];
               part = static_cast<long long>(s) * Fi[j];
             }
 #pragma unroll

@@ -123,7 +123,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
   const int total = T2 * args.nsteps;
   const int pair = blockIdx.x >> 1;
   const int npairs = gridDim.x >> 1;
-  const int KB = args.npad / Cfg::BK;
+  const int KB = args.kpad / Cfg::BK;
 
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------- operand producer (both CTAs)
@@ -136,7 +136,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
         const int s = g / T2, w = g % T2;
         const int n_blk = w / num_mp, mp = w % num_mp;
         const int m_blk = 2 * mp + static_cast<int>(cr);
-        dep::wait_block(args.done, n_blk, static_cast<uint32_t>(s * args.num_m));
+        dep::wait_block(args.done, n_blk, args.done_base, static_cast<uint32_t>(s * args.num_m));
         const CUtensorMap* gin = &maps.Gin[s & 1];
         for (int kb = 0; kb < KB; ++kb) {
           ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
@@ -196,7 +196,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
       for (int g = pair; g < total; g += npairs) {
         const int s = g / T2, w = g % T2;
         const int n_blk = w / num_mp, mp = w % num_mp;
-        dep::wait_block(args.done, n_blk, static_cast<uint32_t>(s * args.num_m));
+        dep::wait_block(args.done, n_blk, args.done_base, static_cast<uint32_t>(s * args.num_m));
         const int i0 = (2 * mp + static_cast<int>(cr)) * Cfg::BM, rb = n_blk * N_PAIR;
         for (int c = 0; c < CHUNKS; ++c, ++ck) {
           const int b = ck % NBUF;

@@ -88,7 +88,18 @@ struct MultiStepArgs {
   uint32_t* done;    // [num_n] tiles completed per replica block, zero at launch
   int32_t dbg;       // dev experiments: 1 = no state traffic, 2 = no MMA, 3 = no MMA and no compute
   int32_t fx_exp;    // NA > 1: F = sum_w acc_w 2^(8w + fx_exp) (fixed-point J scale + x scale)
+  // --- row sharding. Unsharded: kpad = npad, num_m_total = num_m,
+  // col0 = 0, done_base = 0, npeers = 0.
+  int32_t kpad;          // K extent of the contraction (global padded n)
+  int32_t num_m_total;   // 128-spin row tiles over all ranks (dependency count per step)
+  int32_t col0;          // this rank's first spin (column offset of its slab of G)
+  uint32_t done_base;    // done[] value at launch (counters run on across launches)
+  int32_t npeers;        // other ranks that receive this rank's G slab
+  int64_t g_ld;          // row pitch (bytes) of the G buffers
+  uint8_t* peer_g[2][7]; // peers' G buffers for step parity 0/1 (NVLink peer / IPC pointers)
+  uint32_t* peer_done[7];
 };
+constexpr int MAX_PEERS = 7;
 
 namespace dep {
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
@@ -104,9 +115,23 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 }
 // Block until `need` tiles of replica block n are complete, then order the
 // caller's subsequent async-proxy (TMA) reads after that observation.
-__device__ __forceinline__ void wait_block(const uint32_t* done, int n, uint32_t need) {
+__device__ __forceinline__ void wait_block(const uint32_t* done, int n, uint32_t base, uint32_t need) {
   if (need == 0) return;
-  while (ld_acquire(done + n) < need) __nanosleep(32);
+  while (ld_acquire(done + n) - base < need) __nanosleep(32);
+  fence_proxy_async_global();
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void release_add_sys(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Sharded variant: counters are incremented by peer GPUs over NVLink (sys scope).
+__device__ __forceinline__ void wait_block_sys(const uint32_t* done, int n, uint32_t base, uint32_t need) {
+  if (need == 0) return;
+  while (ld_acquire_sys(done + n) - base < need) __nanosleep(64);
   fence_proxy_async_global();
 }
 }  // namespace dep
@@ -171,7 +196,15 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
 
   const int T = args.num_m * args.num_n;
   const int total = T * args.nsteps;
-  const int KB = args.npad / Cfg::BK;
+  const int KB = args.kpad / Cfg::BK;
+  const bool sharded = args.npeers > 0;
+  auto wait_dep = [&](int n_blk, int s) {
+    const uint32_t need = static_cast<uint32_t>(s * args.num_m_total);
+    if (sharded)
+      dep::wait_block_sys(args.done, n_blk, args.done_base, need);
+    else
+      dep::wait_block(args.done, n_blk, args.done_base, need);
+  };
 
   if (warp == 0) {
     if (lane == 0 && args.dbg < 2) {  // ---------------------------- operand producer
@@ -183,7 +216,7 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
       for (int g = blockIdx.x; g < total; g += gridDim.x) {
         const int s = g / T, w = g % T;
         const int n_blk = w / args.num_m, m_blk = w % args.num_m;
-        dep::wait_block(args.done, n_blk, static_cast<uint32_t>(s * args.num_m));
+        wait_dep(n_blk, s);
         const CUtensorMap* gin = &maps.Gin[s & 1];
         for (int kb = 0; kb < KB; ++kb) {
           ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
@@ -191,7 +224,7 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
 #pragma unroll
           for (int ap = 0; ap < NA; ++ap)
             ptx::tma_load_2d(a_base + (stage * NA + ap) * Cfg::A_BYTES, &maps.J, full_bar(stage), kb * Cfg::BK,
-                             ap * args.npad + m_blk * Cfg::BM);
+                             ap * args.num_m * Cfg::BM + m_blk * Cfg::BM);
 #pragma unroll
           for (int pl = 0; pl < NPLANES; ++pl)
             ptx::tma_load_2d(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES, gin, full_bar(stage),
@@ -251,7 +284,7 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
       for (int g = blockIdx.x; g < total; g += gridDim.x) {
         const int s = g / T, w = g % T;
         const int n_blk = w / args.num_m, m_blk = w % args.num_m;
-        dep::wait_block(args.done, n_blk, static_cast<uint32_t>(s * args.num_m));
+        wait_dep(n_blk, s);
         const int i0 = m_blk * Cfg::BM, rb = n_blk * BN;
         for (int c = 0; c < CHUNKS; ++c, ++ck) {
           const int b = ck % NBUF;
@@ -265,41 +298,79 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
       }
     }
   } else if (warp == 3) {
-    if (lane == 0) {  // ------------------------------------------------ state storer
+    // ------------------------------------------------------------------ state storer
+    // lane 0 drives the TMA stores; in sharded runs the whole warp also pushes the
+    // freshly computed slab of G_{t+1} into every peer's buffer (NVLink stores) so
+    // the next step's contraction on every rank sees all spins.
+    if (lane == 0) {
       ptx::prefetch_tmap(&maps.Gout[0]);
       ptx::prefetch_tmap(&maps.Gout[1]);
-      int ck = 0;
-      for (int g = blockIdx.x; g < total; g += gridDim.x) {
-        const int s = g / T, w = g % T;
-        const int n_blk = w / args.num_m, m_blk = w % args.num_m;
-        const int i0 = m_blk * Cfg::BM, rb = n_blk * BN;
-        const CUtensorMap* gout = &maps.Gout[s & 1];
-        for (int c = 0; c < CHUNKS; ++c, ++ck) {
-          const int b = ck % NBUF;
-          ptx::mbar_wait(sdone_bar(b), (ck / NBUF) & 1);
+    }
+    int ck = 0;
+    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+      const int s = g / T, w = g % T;
+      const int n_blk = w / args.num_m, m_blk = w % args.num_m;
+      const int i0 = m_blk * Cfg::BM, rb = n_blk * BN;
+      const CUtensorMap* gout = &maps.Gout[s & 1];
+      for (int c = 0; c < CHUNKS; ++c, ++ck) {
+        const int b = ck % NBUF;
+        ptx::mbar_wait(sdone_bar(b), (ck / NBUF) & 1);
+        const uint32_t sb = s_base + b * Cfg::BUF_BYTES;
+        const int r0 = rb + c * CW;
+        if (lane == 0) {
           if (args.dbg != 1) {
-            const uint32_t sb = s_base + b * Cfg::BUF_BYTES;
-            const int r0 = rb + c * CW;
             ptx::tma_store_2d(&maps.X, sb, i0, r0);
             ptx::tma_store_2d(&maps.Y, sb + Cfg::ST_ARR, i0, r0);
             ptx::tma_store_2d(&maps.P, sb + 2 * Cfg::ST_ARR, i0, r0);
 #pragma unroll
             for (int pl = 0; pl < NPLANES; ++pl)
-              ptx::tma_store_2d(gout, sb + 3 * Cfg::ST_ARR + pl * Cfg::ST_G, i0,
+              ptx::tma_store_2d(gout, sb + 3 * Cfg::ST_ARR + pl * Cfg::ST_G, args.col0 + i0,
                                 (NPLANES == 1 ? 0 : pl * args.rpad) + r0);
           }
           ptx::bulk_commit();
+        }
+        if (sharded) {
+          // chunk of G: CW replica rows x 128 spins (128 contiguous bytes each), per plane
+          const uint8_t* gs = s_gen + b * Cfg::BUF_BYTES + 3 * Cfg::ST_ARR;
+          for (int pr = 0; pr < args.npeers; ++pr) {
+            uint8_t* dst0 = args.peer_g[s & 1][pr];
+#pragma unroll
+            for (int pl = 0; pl < NPLANES; ++pl) {
+              for (int e = lane; e < CW * Cfg::BM / 16; e += 32) {  // 16-byte pieces
+                const int row = e / (Cfg::BM / 16), piece = e % (Cfg::BM / 16);
+                const int rr = r0 + row;
+                if (rr >= args.R) continue;
+                const int spin = args.col0 + i0 + piece * 16;
+                const uint4 v = *reinterpret_cast<const uint4*>(gs + pl * Cfg::ST_G + row * Cfg::BM + piece * 16);
+                *reinterpret_cast<uint4*>(dst0 + (static_cast<size_t>(NPLANES == 1 ? 0 : pl * args.rpad) + rr) *
+                                                     args.g_ld + spin) = v;
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
           ptx::bulk_wait_read0();  // smem slot reusable as soon as the engine has read it
           ptx::mbar_arrive(sempty_bar(b));
         }
-        // Tile complete: its global writes must land before block n is released.
-        // (Deferring this past the next tile's stores deadlocks: the next tile
-        // may itself wait on this release.)
+        __syncwarp();
+      }
+      // Tile complete: its global writes must land before block n is released.
+      // (Deferring this past the next tile's stores deadlocks: the next tile
+      // may itself wait on this release.)
+      if (lane == 0) {
         ptx::bulk_wait0();
         dep::fence_proxy_async_global();
-        __threadfence();
-        dep::release_add(args.done + n_blk, 1u);
+        if (sharded) {
+          __threadfence_system();
+          dep::release_add_sys(args.done + n_blk, 1u);
+          for (int pr = 0; pr < args.npeers; ++pr) dep::release_add_sys(args.peer_done[pr] + n_blk, 1u);
+        } else {
+          __threadfence();
+          dep::release_add(args.done + n_blk, 1u);
+        }
       }
+      __syncwarp();
     }
   } else {
     // --------------------------------------------------------------------- epilogue

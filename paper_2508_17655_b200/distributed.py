@@ -90,3 +90,41 @@ def distributed_batch_best_of(solver, cfg, tuning, n_batch: int, master_seed: in
     echo = dataclasses.replace(b.config, seed=_derive_seed(master_seed, [SEED_STREAM_BATCH, gi]))
     return RunResult(final_spins=wspins, energy=ge, cut=None, wall_time_s=b.timing["total_ms"] / 1e3,
                      config_echo=echo, tuning_echo=tuning)
+
+
+# ----------------------------------------------------------------- row sharding (C5)
+
+def row_shard(n_global: int, world: int, rank: int) -> tuple[int, int, int]:
+    """(row0, rows_valid, rows_padded): the split sbg_set_couplings_rows_i8 applies
+    (kpad = n rounded up to 128*world, equal 128-multiple slabs)."""
+    kpad = -(-n_global // (128 * world)) * 128 * world
+    rows = kpad // world
+    row0 = rank * rows
+    return row0, max(0, min(rows, n_global - row0)), rows
+
+
+def connect_row_shards_local(solvers) -> None:
+    """Peer wiring for shards that live in ONE process (device pointers of each other,
+    e.g. several GPUs driven by one host thread, or the single-GPU lockstep emulation
+    used by the tests, where every launch runs one step so no kernel waits on another)."""
+    bufs = [s.shard_buffers() for s in solvers]
+    for k, s in enumerate(solvers):
+        s.shard_set_peers([b for j, b in enumerate(bufs) if j != k])
+
+
+def connect_row_shards_ipc(solver, group=None) -> None:
+    """Peer wiring across processes (one rank per GPU): CUDA IPC handles of every rank's
+    (G0, G1, done) are all-gathered over torch.distributed and opened locally."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    mine = solver.shard_ipc_export()
+    handles = [None] * world
+    dist.all_gather_object(handles, mine, group=group)
+    solver.shard_set_peers([solver.shard_ipc_open(h) for k, h in enumerate(handles) if k != rank])
+
+
+def row_sharded_energies(partials_by_rank) -> np.ndarray:
+    """ising_energy per replica from the ranks' E2 shares (model.cpp:112-123)."""
+    return -0.5 * np.sum(np.stack(partials_by_rank), axis=0).astype(np.float64)

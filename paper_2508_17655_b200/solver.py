@@ -211,6 +211,53 @@ class Solver:
         self.total_weight = graph_total_weight if graph_total_weight is not None else int(
             -np.triu(J.astype(np.int64), 1).sum())
 
+    # ------------------------------------------------------- row sharding (C5)
+    def set_instance_rows(self, J_rows: np.ndarray, n_global: int, world: int, rank: int) -> None:
+        """This rank's rows of J (rows x n_global int8; rows as sbg_set_couplings_rows_i8 assigns)."""
+        J_rows = np.ascontiguousarray(J_rows, np.int8)
+        self._check(self._L.sbg_set_couplings_rows_i8(self._h, n_global, world, rank, ptr(J_rows)))
+        info = self.shard_info()
+        self.n = info["rows_valid"]
+        self.n_global = n_global
+        self.total_weight = None
+
+    def shard_info(self) -> dict:
+        vals = [C.c_int64() for _ in range(4)]
+        self._check(self._L.sbg_shard_info(self._h, *(C.byref(v) for v in vals)))
+        return dict(zip(["row0", "rows_valid", "rows_padded", "kpad"], (v.value for v in vals)))
+
+    def shard_buffers(self):
+        g0, g1, d = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        self._check(self._L.sbg_shard_buffers(self._h, C.byref(g0), C.byref(g1), C.byref(d)))
+        return g0.value, g1.value, d.value
+
+    def shard_set_peers(self, peers) -> None:
+        """peers: list of (g0, g1, done) device pointers of the OTHER ranks."""
+        n = len(peers)
+        arr = [(C.c_void_p * max(n, 1))(*[p[k] for p in peers]) for k in range(3)]
+        self._check(self._L.sbg_shard_set_peers(self._h, n, arr[0], arr[1], arr[2]))
+
+    def shard_prepare(self, variant) -> None:
+        self._check(self._L.sbg_shard_prepare(self._h, int(variant)))
+
+    def shard_push_slab(self) -> None:
+        self._check(self._L.sbg_shard_push_slab(self._h))
+
+    def shard_ipc_export(self) -> bytes:
+        buf = (C.c_char * 192)()
+        self._check(self._L.sbg_shard_ipc_export(self._h, buf))
+        return bytes(buf)
+
+    def shard_ipc_open(self, handles: bytes):
+        g0, g1, d = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        self._check(self._L.sbg_shard_ipc_open(self._h, handles, C.byref(g0), C.byref(g1), C.byref(d)))
+        return g0.value, g1.value, d.value
+
+    def readout_partial(self) -> np.ndarray:
+        e2 = np.empty(self.R, np.int64)
+        self._check(self._L.sbg_readout_partial(self._h, ptr(e2)))
+        return e2
+
     def gen_random_dense(self, n: int, seed: int) -> None:
         """gen_random_dense (model.cpp:144-159) straight into the device instance."""
         self._check(self._L.sbg_gen_couplings_dense_pm1(self._h, n, seed))
