@@ -164,6 +164,11 @@ int sbg_shard_buffers(sbg_ctx* ctx, void** g0, void** g1, void** done);
 int sbg_shard_set_peers(sbg_ctx* ctx, int32_t npeers, void* const* g0, void* const* g1, void* const* done);
 int sbg_shard_prepare(sbg_ctx* ctx, int32_t variant);
 int sbg_shard_push_slab(sbg_ctx* ctx);
+/* Device-generated +-1 couplings for large-N throughput runs: J_ij = J_ji = sign from
+ * splitmix64(seed ^ (min(i,j) * n + max(i,j))), zero diagonal (i.i.d. uniform +-1 like
+ * gen_random_dense, NOT its draw order; parity tests use the exact order at small n).
+ * world == 1: the whole matrix; world > 1: rank's rows as sbg_set_couplings_rows_i8. */
+int sbg_gen_couplings_hash_pm1(sbg_ctx* ctx, int64_t n_global, int32_t world, int32_t rank, uint64_t seed);
 /* CUDA IPC export/open of (G0, G1, done) for peers in other processes (192 bytes). */
 int sbg_shard_ipc_export(sbg_ctx* ctx, void* out192);
 int sbg_shard_ipc_open(sbg_ctx* ctx, const void* in192, void** g0, void** g1, void** done);

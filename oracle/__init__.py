@@ -188,6 +188,7 @@ class _Orc:
         L.orc_xoshiro_next_n.argtypes = [_u64, _i64, _P]
         L.orc_gen_dense_i8.argtypes = [_i64, _u64, _P]
         L.orc_gen_dense_i8_rows.argtypes = [_i64, _u64, _i64, _i64, _P]
+        L.orc_gen_hash_pm1_rows.argtypes = [_i64, _u64, _i64, _i64, _P]
         L.orc_gen_er_edges.restype = _i64
         L.orc_gen_er_edges.argtypes = [_i64, _i64, _u64, _P, _P, _P]
         L.orc_edges_to_csr.argtypes = [_i64, _i64, _P, _P, _P, _P, _P, _P]
@@ -231,6 +232,11 @@ class _Orc:
     def gen_dense_i8_rows(self, n: int, seed: int, row0: int, rows: int) -> np.ndarray:
         J = np.empty((rows, n), np.int8)
         self.lib.orc_gen_dense_i8_rows(n, seed, row0, rows, _ptr(J))
+        return J
+
+    def gen_hash_pm1_rows(self, n: int, seed: int, row0: int, rows: int) -> np.ndarray:
+        J = np.empty((rows, n), np.int8)
+        self.lib.orc_gen_hash_pm1_rows(n, seed, row0, rows, _ptr(J))
         return J
 
     def gen_er_csr(self, n: int, m: int, seed: int):

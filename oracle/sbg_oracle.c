@@ -544,3 +544,17 @@ void orc_phase_batch_f32(int64_t count, const float* F, float* x, float* y, floa
   const float inv = 1.0f / (float)(M - m);
   for (int64_t k = 0; k < count; ++k) orc_phase_f32(F[k], x + k, y + k, p + k, a, c, dt, inv);
 }
+
+/* Counter-based +-1 instance of sbg_gen_couplings_hash_pm1 (rows row0..row0+rows-1). */
+void orc_gen_hash_pm1_rows(int64_t n, uint64_t seed, int64_t row0, int64_t rows, int8_t* Jr) {
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t j = 0; j < n; ++j) {
+      const int64_t i = row0 + r;
+      int8_t v = 0;
+      if (i != j) {
+        const uint64_t lo = (uint64_t)(i < j ? i : j), hi = (uint64_t)(i < j ? j : i);
+        v = (orc_mix64(seed ^ (lo * (uint64_t)n + hi)) >> 63) ? -1 : 1;
+      }
+      Jr[r * n + j] = v;
+    }
+}

@@ -32,6 +32,8 @@ void orc_gen_dense_i8(int64_t n, uint64_t seed, int8_t* J);
 /* Rows [row0, row0+rows) of the same matrix, for instances too big to hold
  * whole (C5). Cost is O(row0*n) skipped draws. */
 void orc_gen_dense_i8_rows(int64_t n, uint64_t seed, int64_t row0, int64_t rows, int8_t* Jrows);
+/* Counter-based +-1 rows of sbg_gen_couplings_hash_pm1 (large-N throughput instance). */
+void orc_gen_hash_pm1_rows(int64_t n, uint64_t seed, int64_t row0, int64_t rows, int8_t* Jrows);
 /* Erdos-Renyi G(n, m) MAX-CUT graph (new; the reference has none): one
  * Xoshiro256pp(seed) stream, (i, j) = (next() % n, next() % n), self-loops and
  * duplicates rejected, then one random_sign() weight per accepted edge. */

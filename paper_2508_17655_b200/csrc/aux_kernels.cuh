@@ -213,6 +213,40 @@ __global__ void __launch_bounds__(1024) argmin_energy_kernel(const long long* __
 
 __global__ void advance_counter_kernel(uint64_t* m, uint64_t by) { *m += by; }
 
+// Counter-based +-1 couplings for large-N throughput runs (C5, N = 1e5: the
+// reference's serial gen_random_dense stream would take minutes on the host):
+// J_ij = J_ji = (mix64(seed ^ (min(i,j) * n + max(i,j))) top bit) ? -1 : +1, zero
+// diagonal -- i.i.d. uniform +-1 like gen_random_dense, but NOT its draw order.
+// Writes rows [row0, row0 + rows) of the n_global x n_global matrix into a
+// [rows][ld] buffer (zero padding beyond n_global). One coalesced pass.
+__global__ void gen_hash_pm1_kernel(int8_t* __restrict__ J, int64_t n_global, int64_t row0, int64_t rows, int64_t ld,
+                                    uint64_t seed) {
+  const uint64_t total = static_cast<uint64_t>(rows) * static_cast<uint64_t>(ld);
+  for (uint64_t idx = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) * 16; idx < total;
+       idx += static_cast<uint64_t>(gridDim.x) * blockDim.x * 16) {
+    const int64_t r = static_cast<int64_t>(idx / ld);
+    const int64_t c0 = static_cast<int64_t>(idx % ld);
+    const int64_t i = row0 + r;
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int64_t j = c0 + q * 4 + b;
+        int8_t v = 0;
+        if (i < n_global && j < n_global && i != j) {
+          const uint64_t lo = static_cast<uint64_t>(i < j ? i : j), hi = static_cast<uint64_t>(i < j ? j : i);
+          v = (mix64(seed ^ (lo * static_cast<uint64_t>(n_global) + hi)) >> 63) ? int8_t(-1) : int8_t(1);
+        }
+        word |= static_cast<uint32_t>(static_cast<uint8_t>(v)) << (8 * b);
+      }
+      w[q] = word;
+    }
+    *reinterpret_cast<uint4*>(J + idx) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
 // Real-valued J readout: E2 = sum_a 2^(8a) E2_a over the J byte planes.
 __global__ void combine_planes_e2_kernel(const long long* __restrict__ parts, int64_t stride, int32_t nplanes,
                                          int32_t R, long long* __restrict__ e2) {

@@ -1025,6 +1025,44 @@ int sbg_run_seeded(sbg_ctx* ctx, const sbg_params* prm, int64_t R, int32_t init_
 
 // ------------------------------------------------------------------ row sharding (C5)
 
+int sbg_gen_couplings_hash_pm1(sbg_ctx* ctx, int64_t n_global, int32_t world, int32_t rank, uint64_t seed) {
+  CHECK_CTX(ctx);
+  if (n_global < 2 || world < 1 || world > 8 || rank < 0 || rank >= world)
+    return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "bad arguments");
+  CK(cudaSetDevice(ctx->device));
+  cudaStreamSynchronize(ctx->stream);
+  free_state(ctx);
+  cudaFree(ctx->dJ);
+  ctx->dJ = nullptr;
+  const bool shard = world > 1;
+  const int64_t kpad = shard ? round_up(n_global, int64_t(128) * world) : round_up(n_global, PAD_N);
+  const int64_t rows = shard ? kpad / world : kpad;
+  const int64_t row0 = shard ? int64_t(rank) * rows : 0;
+  const int64_t valid = std::max<int64_t>(0, std::min<int64_t>(rows, n_global - row0));
+  if (valid == 0) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "rank owns no spins");
+  CK(cudaMalloc(&ctx->dJ, size_t(rows) * kpad));
+  const uint64_t work = uint64_t(rows) * kpad / 16;
+  gen_hash_pm1_kernel<<<int(std::min<uint64_t>((work + 255) / 256, uint64_t(ctx->sms) * 32)), 256, 0,
+                        ctx->stream>>>(ctx->dJ, n_global, row0, rows, kpad, seed);
+  CK(cudaGetLastError());
+  ++ctx->launches;
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->kind = KIND_DENSE_I8;
+  ctx->energy_scale = 1.0;
+  ctx->sharded = shard;
+  ctx->n = shard ? valid : n_global;
+  ctx->npad = rows;
+  ctx->n_global = n_global;
+  ctx->kpad = kpad;
+  ctx->row0 = row0;
+  ctx->num_m_total = kpad / 128;
+  ctx->done_base = 0;
+  ctx->peer_g0.clear();
+  ctx->peer_g1.clear();
+  ctx->peer_done.clear();
+  return encode_2d_u8(ctx, &ctx->tmJ, ctx->dJ, kpad, rows, 128, 128);
+}
+
 int sbg_set_couplings_rows_i8(sbg_ctx* ctx, int64_t n_global, int32_t world, int32_t rank, const int8_t* Jrows) {
   CHECK_CTX(ctx);
   if (n_global < 1 || world < 1 || world > 8 || rank < 0 || rank >= world || !Jrows)

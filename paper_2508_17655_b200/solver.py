@@ -221,6 +221,13 @@ class Solver:
         self.n_global = n_global
         self.total_weight = None
 
+    def gen_hash_pm1(self, n_global: int, seed: int, world: int = 1, rank: int = 0) -> None:
+        """Device-generated +-1 couplings (large-N throughput runs; not gen_random_dense's order)."""
+        self._check(self._L.sbg_gen_couplings_hash_pm1(self._h, n_global, world, rank, seed))
+        self.n = self.shard_info()["rows_valid"] if world > 1 else n_global
+        self.n_global = n_global
+        self.total_weight = None
+
     def shard_info(self) -> dict:
         vals = [C.c_int64() for _ in range(4)]
         self._check(self._L.sbg_shard_info(self._h, *(C.byref(v) for v in vals)))

@@ -52,3 +52,45 @@ def test_two_shards_lockstep_equal_unsharded(orc):
     finally:
         for s in shards:
             s.close()
+
+
+def test_hash_couplings_match_oracle_and_shards(orc):
+    """Device +-1 generator (large-N instances) == its oracle restatement; row shards of it
+    reproduce the unsharded GdSB run bitwise (lockstep emulation)."""
+    from paper_2508_17655_b200 import InitMode, Solver, SolverConfig, Variant
+    from paper_2508_17655_b200.distributed import connect_row_shards_local, row_shard
+
+    n, R, seed, world, steps = 900, 64, 77, 2, 12
+    J = orc.gen_hash_pm1_rows(n, seed, 0, n)
+    assert (J == J.T).all() and (np.diag(J) == 0).all()
+    rng = np.random.default_rng(0)
+    S = np.where(rng.random((R, n)) < 0.5, -1, 1).astype(np.int8)
+    cfg = SolverConfig(variant=Variant.dsb, steps=100, dt=1.25, c=1 / (2 * np.sqrt(n)), a=0.0)
+    with Solver(0) as full:
+        full.gen_hash_pm1(n, seed)
+        assert (full.fields_sign(S) == orc.fields_i8(J, S)).all()
+        full.init_state(R, InitMode.small_uniform, 9, 7)
+        full.advance(cfg, 0, steps)
+        fx, _, _ = full.get_state()
+    shards = [Solver(0) for _ in range(world)]
+    try:
+        for k, s in enumerate(shards):
+            s.gen_hash_pm1(n, seed, world, k)
+            s.init_state(R, InitMode.small_uniform, 9, 7)
+        connect_row_shards_local(shards)
+        for s in shards:
+            s.shard_prepare(Variant.dsb)
+        for s in shards:
+            s.shard_push_slab()
+        for m in range(steps):
+            for s in shards:
+                s.advance(cfg, m, m + 1)
+            for s in shards:
+                s.synchronize()
+        for k, s in enumerate(shards):
+            row0, valid, _ = row_shard(n, world, k)
+            x, _, _ = s.get_state()
+            assert (x == fx[:, row0:row0 + valid]).all()
+    finally:
+        for s in shards:
+            s.close()
