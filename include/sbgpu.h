@@ -114,6 +114,9 @@ int sbg_set_state(sbg_ctx* ctx, int64_t R, const float* x, const float* y, const
 /* Device-side init_state (see SBG_INIT_*), replicas offset .. offset+R-1. */
 int sbg_init_state(sbg_ctx* ctx, int64_t R, int32_t mode, uint64_t master, uint64_t tag,
                    int64_t replica_offset);
+/* Same with an explicit seed per replica (e.g. the sweep's derive_seed(seed,
+ * {sweep, mi, ai, r}), bench.cpp:159). */
+int sbg_init_state_seeds(sbg_ctx* ctx, int64_t R, int32_t mode, const uint64_t* seeds);
 int sbg_get_state(sbg_ctx* ctx, float* x, float* y, float* p);
 
 /* step() (engine.cpp:55-110) for every replica, m = m_begin .. m_end-1 of an
@@ -174,6 +177,11 @@ int sbg_shard_ipc_export(sbg_ctx* ctx, void* out192);
 int sbg_shard_ipc_open(sbg_ctx* ctx, const void* in192, void** g0, void** g1, void** done);
 /* This rank's share of E2 = sum_i s_i (J s)_i over its spins; sum over ranks, energy = -E2/2. */
 int sbg_readout_partial(sbg_ctx* ctx, int64_t* e2);
+
+/* Per-replica control strength A for gbsb/gdsb (R values, each >= 0; NULL clears):
+ * a whole A sweep (bench.cpp:143-197, run_sweep_cell over the A axis) in one launch.
+ * Applies while the state has exactly R replicas. */
+int sbg_set_replica_a(sbg_ctx* ctx, int64_t R, const float* a);
 
 int sbg_synchronize(sbg_ctx* ctx);
 /* Kernel launches issued by this context since creation (bench evidence). */

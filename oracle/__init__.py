@@ -213,6 +213,7 @@ class _Orc:
         L.orc_step_f32_fx.argtypes = [C.c_int, _i64, _P, C.c_int, _i64, _i64, _P, _P, _P, _u64, _u64, _f32, _f32,
                                       _f32]
         L.orc_energy2_fx.argtypes = [_i64, _P, _i64, _i64, _P, _P]
+        L.orc_init_reference_seeds.argtypes = [_i64, _i64, _i64, _P, C.c_int, _P, _P, _P]
         L.orc_phase_batch_f32.argtypes = [_i64, _P, _P, _P, _P, _f32, _f32, _f32, _u64, _u64]
 
     def derive_seed(self, master: int, keys) -> int:
@@ -266,6 +267,13 @@ class _Orc:
         ld = n if ld is None else ld
         x, y, p = (np.empty((R, ld), np.float32) for _ in range(3))
         self.lib.orc_init_reference(n, ld, r0, R, master, tag, int(chaos_probe), _ptr(x), _ptr(y), _ptr(p))
+        return x, y, p
+
+    def init_reference_seeds(self, n: int, seeds, chaos_probe: bool = False):
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        R = len(seeds)
+        x, y, p = (np.empty((R, n), np.float32) for _ in range(3))
+        self.lib.orc_init_reference_seeds(n, n, R, _ptr(seeds), int(chaos_probe), _ptr(x), _ptr(y), _ptr(p))
         return x, y, p
 
     def matvec_lanes_f64(self, J, v):

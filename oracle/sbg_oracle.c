@@ -558,3 +558,17 @@ void orc_gen_hash_pm1_rows(int64_t n, uint64_t seed, int64_t row0, int64_t rows,
       Jr[r * n + j] = v;
     }
 }
+
+void orc_init_reference_seeds(int64_t n, int64_t ld, int64_t R, const uint64_t* seeds, int chaos_probe, float* x,
+                              float* y, float* p) {
+  for (int64_t r = 0; r < R; ++r) { /* engine.cpp:25-39 with an explicit seed */
+    xo_t g;
+    xo_seed(&g, seeds[r]);
+    for (int64_t i = 0; i < n; ++i)
+      x[r * ld + i] = chaos_probe ? (float)(0.1 * xo_random_sign(&g)) : (float)xo_uniform_symmetric(&g);
+    for (int64_t i = 0; i < n; ++i) {
+      y[r * ld + i] = 0.0f;
+      p[r * ld + i] = 1.0f;
+    }
+  }
+}

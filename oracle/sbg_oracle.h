@@ -57,6 +57,9 @@ void orc_init_small_uniform(int64_t n, int64_t ld, int64_t r0, int64_t R, uint64
 void orc_init_reference(int64_t n, int64_t ld, int64_t r0, int64_t R, uint64_t master, uint64_t tag,
                         int chaos_probe, float* x, float* y, float* p);
 
+void orc_init_reference_seeds(int64_t n, int64_t ld, int64_t R, const uint64_t* seeds, int chaos_probe, float* x,
+                              float* y, float* p);
+
 /* ---- fp64 restatement of the reference step --------------------------- */
 /* row_dot / coupling_matvec (kernels.hpp:14-46): 8 lanes, tail in lane 0. */
 void orc_matvec_lanes_f64(int64_t n, const double* J, const double* v, double* out);

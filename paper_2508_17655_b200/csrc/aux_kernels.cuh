@@ -70,11 +70,13 @@ constexpr int INIT_THREADS = 64;
 __global__ void __launch_bounds__(INIT_THREADS)
     init_state_kernel(float* __restrict__ x, float* __restrict__ y, float* __restrict__ p, int32_t n,
                       int64_t ld, int32_t R, int32_t mode, uint64_t master, uint64_t tag,
-                      int64_t offset, int64_t n_global = -1, int64_t row0 = 0) {
+                      int64_t offset, int64_t n_global = -1, int64_t row0 = 0,
+                      const uint64_t* __restrict__ seeds = nullptr) {
   __shared__ float tile[INIT_THREADS][33];
   const int r0 = blockIdx.x * INIT_THREADS;
   const int r = r0 + threadIdx.x;
-  Xoshiro g(derive_seed2(master, tag, static_cast<uint64_t>(offset + r)));
+  // replica seed: derive_seed(master, {tag, offset + r}), or an explicit per-replica list
+  Xoshiro g(seeds ? seeds[r < R ? r : 0] : derive_seed2(master, tag, static_cast<uint64_t>(offset + r)));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = INIT_THREADS / 32;
   if (n_global < 0) n_global = n;

@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(CSR_THREADS)
     csr_step_sm_kernel(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                        const int8_t* __restrict__ val, const void* __restrict__ g_cur, void* __restrict__ g_next,
                        float* __restrict__ xs, float* __restrict__ ys, float* __restrict__ ps, int64_t rp,
-                       int32_t R, PhaseConsts k) {
+                       int32_t R, PhaseConsts k, const float* __restrict__ a_rep = nullptr) {
   const int lane = threadIdx.x & 31;
   const int chunks = static_cast<int>((R + CSR_RCHUNK - 1) / CSR_RCHUNK);
   const int64_t tasks = static_cast<int64_t>(n) * chunks;
@@ -81,10 +81,15 @@ __global__ void __launch_bounds__(CSR_THREADS)
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       F[u] = SIGN ? static_cast<float>(acc[u]) : __fmul_rn(__ll2float_rn(acc[u]), 0x1p-30f);
-    gsb_phase(F[0], x4.x, y4.x, p4.x, k);
-    gsb_phase(F[1], x4.y, y4.y, p4.y, k);
-    gsb_phase(F[2], x4.z, y4.z, p4.z, k);
-    gsb_phase(F[3], x4.w, y4.w, p4.w, k);
+    PhaseConsts kk[4] = {k, k, k, k};
+    if (a_rep) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) kk[u].a = a_rep[min(r + u, R - 1)];
+    }
+    gsb_phase(F[0], x4.x, y4.x, p4.x, kk[0]);
+    gsb_phase(F[1], x4.y, y4.y, p4.y, kk[1]);
+    gsb_phase(F[2], x4.z, y4.z, p4.z, kk[2]);
+    gsb_phase(F[3], x4.w, y4.w, p4.w, kk[3]);
     // replicas >= R inside the last chunk are padding: their slots exist (rp) and stay inert
     *reinterpret_cast<float4*>(xs + off) = x4;
     *reinterpret_cast<float4*>(ys + off) = y4;

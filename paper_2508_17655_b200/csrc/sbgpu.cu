@@ -100,6 +100,8 @@ struct sbg_ctx {
   uint32_t done_base = 0;  // done[] counters run on across launches (peers increment them)
   std::vector<uint8_t*> peer_g0, peer_g1;
   std::vector<uint32_t*> peer_done;
+  float* d_arep = nullptr;  // optional per-replica A (sbg_set_replica_a), honoured by gbsb/gdsb
+  int64_t arep_n = 0;
   uint32_t* d_done = nullptr;            // per replica-block tile counters of the multi-step kernel
   int g_cur = 0;
   int g_mode = 0;  // 0 stale, 1 sign plane valid in dG[g_cur], 4 planes valid
@@ -444,6 +446,7 @@ void sbg_destroy(sbg_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   free_state(ctx);
+  cudaFree(ctx->d_arep);
   cudaFree(ctx->dJ);
   cudaFree(ctx->d_rowptr);
   cudaFree(ctx->d_col);
@@ -647,6 +650,26 @@ int sbg_init_state(sbg_ctx* ctx, int64_t R, int32_t mode, uint64_t master, uint6
   return SBG_OK;
 }
 
+int sbg_init_state_seeds(sbg_ctx* ctx, int64_t R, int32_t mode, const uint64_t* seeds) {
+  CHECK_CTX(ctx);
+  if (mode < 0 || mode > 2 || !seeds) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "bad init arguments");
+  CK(cudaSetDevice(ctx->device));
+  int rc = ensure_state(ctx, R);
+  if (rc) return rc;
+  uint64_t* dseeds = nullptr;
+  CK(cudaMalloc(&dseeds, sizeof(uint64_t) * size_t(R)));
+  CK(cudaMemcpyAsync(dseeds, seeds, sizeof(uint64_t) * size_t(R), cudaMemcpyHostToDevice, ctx->stream));
+  const int blocks = int((R + INIT_THREADS - 1) / INIT_THREADS);
+  init_state_kernel<<<blocks, INIT_THREADS, 0, ctx->stream>>>(
+      ctx->dX, ctx->dY, ctx->dP, int32_t(ctx->n), ctx->npad, int32_t(R), mode, 0, 0, 0,
+      ctx->sharded ? ctx->n_global : ctx->n, ctx->sharded ? ctx->row0 : 0, dseeds);
+  CK(cudaGetLastError());
+  ++ctx->launches;
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(dseeds);
+  return SBG_OK;
+}
+
 int sbg_get_state(sbg_ctx* ctx, float* x, float* y, float* p) {
   CHECK_CTX(ctx);
   if (!ctx->dX) return ctx->fail(SBG_ERR_STATE, "no state");
@@ -697,17 +720,18 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
     const int64_t tasks = ctx->n * ((ctx->R + CSR_RCHUNK - 1) / CSR_RCHUNK);
     const int blocks = int(std::min<int64_t>((tasks + CSR_THREADS / 32 - 1) / (CSR_THREADS / 32), int64_t(ctx->sms) * 8));
     int cur = 0;
+    const float* arep = (honours_a && ctx->d_arep && ctx->arep_n == ctx->R) ? ctx->d_arep : nullptr;
     for (uint64_t m = m_begin; m < m_end; ++m) {
       PhaseConsts km = k;
       km.inv = 1.0f / static_cast<float>(prm->steps - m);  // == __frcp_rn(M - m)
       if (sign)
         csr_step_sm_kernel<true><<<blocks, CSR_THREADS, 0, ctx->stream>>>(
             n32, ctx->d_rowptr, ctx->d_col, ctx->d_val, ctx->dQ[cur], ctx->dQ[cur ^ 1], ctx->dXs, ctx->dYs, ctx->dPs,
-            ctx->rp, R32, km);
+            ctx->rp, R32, km, arep);
       else
         csr_step_sm_kernel<false><<<blocks, CSR_THREADS, 0, ctx->stream>>>(
             n32, ctx->d_rowptr, ctx->d_col, ctx->d_val, ctx->dQ[cur], ctx->dQ[cur ^ 1], ctx->dXs, ctx->dYs, ctx->dPs,
-            ctx->rp, R32, km);
+            ctx->rp, R32, km, arep);
       CK(cudaGetLastError());
       ++ctx->launches;
       cur ^= 1;
@@ -746,6 +770,7 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
       a.t_begin = m;
       a.nsteps = int32_t(ns);
       a.done = ctx->d_done;
+      a.a_rep = (honours_a && ctx->d_arep && ctx->arep_n == ctx->R) ? ctx->d_arep : nullptr;
       const int cur = ctx->g_cur;
       a.kpad = int32_t(ctx->sharded ? ctx->kpad : ctx->npad);
       a.num_m_total = int32_t(ctx->sharded ? ctx->num_m_total : ctx->npad / 128);
@@ -1210,6 +1235,27 @@ int sbg_readout_partial(sbg_ctx* ctx, int64_t* e2) {
   if (rc) return rc;
   CK(cudaMemcpyAsync(e2, ctx->dE2, sizeof(long long) * ctx->R, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  return SBG_OK;
+}
+
+// Per-replica control strength A (a_rep[r] for replica r of the current state,
+// R values): one launch then covers a whole A-sweep column (bench.cpp:143-197's
+// run_sweep_cell fan-out over A). NULL clears it. Ignored by bsb/dsb (engine.cpp:64).
+int sbg_set_replica_a(sbg_ctx* ctx, int64_t R, const float* a) {
+  CHECK_CTX(ctx);
+  CK(cudaSetDevice(ctx->device));
+  if (!a) {
+    ctx->arep_n = 0;
+    return SBG_OK;
+  }
+  if (R < 1) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "replica count must be >= 1");
+  for (int64_t r = 0; r < R; ++r)
+    if (!(a[r] >= 0.0f)) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "A must be >= 0");
+  cudaFree(ctx->d_arep);
+  ctx->d_arep = nullptr;
+  CK(cudaMalloc(&ctx->d_arep, sizeof(float) * size_t(R)));
+  CK(cudaMemcpy(ctx->d_arep, a, sizeof(float) * size_t(R), cudaMemcpyHostToDevice));
+  ctx->arep_n = R;
   return SBG_OK;
 }
 

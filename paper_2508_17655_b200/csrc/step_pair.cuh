@@ -252,6 +252,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
     int lt = 0;
     for (int g = pair; g < total; g += npairs, ++lt) {
       const int s = g / T2;
+      const int rbase = ((g % T2) / num_mp) * N_PAIR;  // first replica of this pair tile
       k.inv = __frcp_rn(static_cast<float>(args.M - (args.t_begin + static_cast<uint64_t>(s))));
       const int buf = lt & 1;
       ptx::mbar_wait(tfull_bar(buf), (lt >> 1) & 1);
@@ -292,7 +293,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
         for (int j = 0; j < CWQ; ++j) {
           const int idx = (h * CWQ + j) * Cfg::BM + srow;
           float xv = xs[idx], yv = ys[idx], pv = ps[idx];
-          gsb_phase(F[j], xv, yv, pv, k);
+          PhaseConsts kj = k;
+          if (args.a_rep) kj.a = args.a_rep[min(rbase + col0 + j, args.R - 1)];
+          gsb_phase(F[j], xv, yv, pv, kj);
           xs[idx] = xv;
           ys[idx] = yv;
           ps[idx] = pv;

@@ -98,6 +98,7 @@ struct MultiStepArgs {
   int64_t g_ld;          // row pitch (bytes) of the G buffers
   uint8_t* peer_g[2][7]; // peers' G buffers for step parity 0/1 (NVLink peer / IPC pointers)
   uint32_t* peer_done[7];
+  const float* a_rep;    // optional per-replica control strength A (sweeps over A in one launch)
 };
 constexpr int MAX_PEERS = 7;
 
@@ -382,6 +383,7 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
     int lt = 0;
     for (int g = blockIdx.x; g < total; g += gridDim.x, ++lt) {
       const int s = g / T;
+      const int rbase = ((g % T) / args.num_m) * BN;  // first replica of this tile
       k.inv = __frcp_rn(static_cast<float>(args.M - (args.t_begin + static_cast<uint64_t>(s))));
       const int buf = lt & 1;
       if (args.dbg < 2) ptx::mbar_wait(tfull_bar(buf), (lt >> 1) & 1);
@@ -441,7 +443,9 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
             for (int j = 0; j < CWQ; ++j) {
               const int idx = (h * CWQ + j) * Cfg::BM + srow;
               float xv = xs[idx], yv = ys[idx], pv = ps[idx];
-              gsb_phase(F[j], xv, yv, pv, k);
+              PhaseConsts kj = k;
+              if (args.a_rep) kj.a = args.a_rep[min(rbase + col0 + j, args.R - 1)];
+              gsb_phase(F[j], xv, yv, pv, kj);
               xs[idx] = xv;
               ys[idx] = yv;
               ps[idx] = pv;

@@ -292,6 +292,19 @@ class Solver:
         self._check(self._L.sbg_init_state(self._h, R, int(mode), master, tag, offset))
         self.R = R
 
+    def init_state_seeds(self, seeds, mode: InitMode) -> None:
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        self._check(self._L.sbg_init_state_seeds(self._h, len(seeds), int(mode), ptr(seeds)))
+        self.R = len(seeds)
+
+    def set_replica_a(self, a) -> None:
+        """Per-replica A (gbsb/gdsb); None clears."""
+        if a is None:
+            self._check(self._L.sbg_set_replica_a(self._h, 0, None))
+            return
+        a = np.ascontiguousarray(a, np.float32)
+        self._check(self._L.sbg_set_replica_a(self._h, len(a), ptr(a)))
+
     def get_state(self):
         x, y, p = (np.empty((self.R, self.n), np.float32) for _ in range(3))
         self._check(self._L.sbg_get_state(self._h, ptr(x), ptr(y), ptr(p)))
@@ -417,3 +430,46 @@ def _derive_seed(master: int, keys) -> int:
 
 def cut_from_energy(total_weight: int, energy: float) -> int:
     return int(math.floor((total_weight - energy) / 2 + 0.5))
+
+
+SEED_STREAM_SWEEP = 1  # rng.hpp:34 seed_stream::sweep
+
+
+@dataclasses.dataclass
+class SweepCell:  # bench.hpp:72-80
+    mi: int
+    ai: int
+    m_steps: int
+    a: float
+    stats: SuccessStats
+    mean_energy: float
+    best_energy: float
+    energies: np.ndarray
+
+
+def sweep(solver: "Solver", m_values, a_values, reps: int, cfg_base: SolverConfig, tuning: TuningResult,
+          target: float):
+    """sbopt::sweep (bench.cpp:171-197) on the GPU: one launch per M value covering every
+    A cell x reps replicas (per-replica A); replica r of cell (mi, ai) is seeded
+    derive_seed(cfg_base.seed, {sweep, mi, ai, r}) with cfg_base.init_mode, as
+    run_sweep_cell does (bench.cpp:159). Cells row-major, M outer, A inner."""
+    if len(m_values) == 0 or len(a_values) == 0:
+        raise ValueError("empty sweep axes")
+    if reps < 1:
+        raise ValueError("sweep needs reps >= 1")
+    cells = []
+    na = len(a_values)
+    for mi, m_steps in enumerate(m_values):
+        cfg = resolve_config(dataclasses.replace(cfg_base, steps=int(m_steps)), tuning)
+        seeds = np.array([_derive_seed(cfg_base.seed, [SEED_STREAM_SWEEP, mi, ai, r])
+                          for ai in range(na) for r in range(reps)], np.uint64)
+        solver.init_state_seeds(seeds, cfg.init_mode)
+        solver.set_replica_a(np.repeat(np.asarray(a_values, np.float32), reps))
+        solver.advance(cfg, 0, int(m_steps))
+        _, energies, _, _ = solver.readout()
+        solver.set_replica_a(None)
+        for ai, a in enumerate(a_values):
+            e = energies[ai * reps:(ai + 1) * reps]
+            cells.append(SweepCell(mi, ai, int(m_steps), float(a), success_probability(e, target),
+                                   float(e.mean()), float(e.min()), e.copy()))
+    return cells

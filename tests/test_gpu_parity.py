@@ -253,3 +253,27 @@ def test_readout_best_matches_full_readout(solver, orc):
     bs, be, bi, energies = solver.readout_best()
     assert bi == best and be == best_e and (energies == energy).all() and (bs == spins[best]).all()
     assert (energy == -0.5 * orc.energy2_i8(J, x)).all()
+
+
+def test_sweep_grid_matches_mirror_per_cell(solver, orc):
+    """sweep (bench.cpp:171-197) on the GPU: per-replica A in one launch per M, seeds
+    derive_seed(seed, {sweep, mi, ai, r}); every cell's energies bitwise vs the mirror."""
+    from paper_2508_17655_b200 import SolverConfig, TuningResult, Variant
+    from paper_2508_17655_b200.solver import _derive_seed, sweep
+
+    n, reps = 64, 5
+    J = orc.gen_dense_i8(n, 17)
+    solver.set_instance(J)
+    c, dt = 1 / (2 * np.sqrt(n)), 1.25
+    base = SolverConfig(variant=Variant.gbsb, seed=99)
+    t = TuningResult(c=c, dt=dt)
+    m_values, a_values = [30, 80], [0.0, 0.2, 0.5]
+    cells = sweep(solver, m_values, a_values, reps, base, t, target=-1e9)
+    assert [(cl.mi, cl.ai) for cl in cells] == [(mi, ai) for mi in range(2) for ai in range(3)]
+    for cl in cells:
+        seeds = [_derive_seed(99, [1, cl.mi, cl.ai, r]) for r in range(reps)]
+        x, y, p = orc.init_reference_seeds(n, seeds)
+        x, y, p = orc.step_f32(2, J, x, y, p, 0, cl.m_steps, np.float32(dt), np.float32(c), np.float32(cl.a),
+                               cl.m_steps)
+        assert (cl.energies == -0.5 * orc.energy2_i8(J, x)).all(), (cl.mi, cl.ai)
+        assert cl.best_energy == cl.energies.min()
