@@ -85,6 +85,7 @@ class _Ref:
                                          C.c_uint, _P, _P]
         L.ref_effective_workers.restype = C.c_uint
         L.ref_effective_workers.argtypes = [C.c_uint]
+        L.ref_chaos_scan.argtypes = [_i64, _P, _P, _i64, _i64, _u64, _f64, _f64, _u64, C.c_uint, _P]
 
     def _check(self, rc: int) -> None:
         if rc != 0:
@@ -173,6 +174,14 @@ class _Ref:
         self._check(self.lib.ref_replica_fanout(variant, J.shape[0], _ptr(J), R, _ptr(x0), _ptr(y0), steps,
                                                 dt, c, a, workers, _ptr(e), _ptr(wall)))
         return e, float(wall[0])
+
+    def chaos_scan(self, J, a_values, reps, steps, dt, c, seed, workers=0):
+        J = np.ascontiguousarray(J, np.float64)
+        a = np.ascontiguousarray(a_values, np.float64)
+        out = np.empty((len(a), reps))
+        self._check(self.lib.ref_chaos_scan(J.shape[0], _ptr(J), _ptr(a), len(a), reps, steps, dt, c, seed,
+                                            workers, _ptr(out)))
+        return out
 
     def effective_workers(self, requested: int = 0) -> int:
         return int(self.lib.ref_effective_workers(requested))

@@ -29,6 +29,7 @@
 
 #include "kernels.hpp"
 #include "sbopt/bench.hpp"
+#include "sbopt/chaos.hpp"
 #include "sbopt/engine.hpp"
 #include "sbopt/model.hpp"
 #include "sbopt/parallel.hpp"
@@ -261,5 +262,26 @@ int ref_replica_fanout(int variant, std::int64_t n, const double* J, std::int64_
 }
 
 unsigned ref_effective_workers(unsigned requested) { return effective_workers(requested); }
+
+// chaos_scan (chaos.cpp:65-102): final deltas, row-major [a][rep].
+int ref_chaos_scan(std::int64_t n, const double* J, const double* a_values, std::int64_t na, std::int64_t reps,
+                   std::uint64_t steps, double dt, double c, std::uint64_t seed, unsigned workers,
+                   double* final_deltas) {
+  try {
+    const auto inst = make_instance(n, J);
+    TuningResult t;
+    t.c = c;
+    t.dt = dt;
+    SolverConfig cfg = make_cfg(2, steps, dt, c, 0.0, seed);
+    const auto rows = chaos_scan(inst, std::span<const double>(a_values, static_cast<std::size_t>(na)),
+                                 static_cast<std::size_t>(reps), cfg, t, workers);
+    for (std::size_t ai = 0; ai < rows.size(); ++ai)
+      for (std::size_t r = 0; r < rows[ai].final_deltas.size(); ++r)
+        final_deltas[ai * static_cast<std::size_t>(reps) + r] = rows[ai].final_deltas[r];
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
 
 }  // extern "C"

@@ -45,6 +45,7 @@ class SolverConfig:  # engine.hpp:29-38
     a: float = 0.0
     seed: int = 0
     init_mode: InitMode = InitMode.uniform_random
+    sample_stride: int = 0  # 0 = record the final state only (engine.hpp:37)
 
 
 @dataclasses.dataclass
@@ -366,6 +367,8 @@ class Solver:
         Returns (list-free) arrays: spins, energies, cuts, best index, timing dict, x_final.
         """
         rcfg = resolve_config(cfg, tuning)
+        if rcfg.sample_stride > 0:
+            return self._run_batch_sampled(rcfg, tuning, R, x0, y0, master_seed, tag, replica_offset, want_spins)
         prm = self.params(rcfg)
         spins = np.empty((R, self.n), np.int8) if want_spins else None
         energy = np.empty(R, np.float64)
@@ -387,6 +390,33 @@ class Solver:
             # cut = (W - E) / 2 (model.hpp:103-104), exact integers
             cuts = ((self.total_weight - energy) / 2).astype(np.int64)
         return BatchResult(spins, energy, cuts, int(best.value), timing.as_dict(), x_final, rcfg, tuning)
+
+    def _run_batch_sampled(self, rcfg, tuning, R, x0, y0, master_seed, tag, replica_offset, want_spins):
+        """run() with sample_stride (engine.cpp:117-133): x recorded at m = 0, every
+        stride steps and at the final step; trajectory[k] = (m, x of all replicas)."""
+        import time
+
+        t0 = time.perf_counter()
+        if x0 is not None:
+            self.set_state(x0, y0 if y0 is not None else np.zeros_like(x0))
+        else:
+            self.init_state(R, rcfg.init_mode, master_seed, tag, replica_offset)
+        traj = [(0, self.get_state()[0])]
+        m = 0
+        while m < rcfg.steps:
+            nxt = min(m + rcfg.sample_stride, rcfg.steps)
+            self.advance(rcfg, m, nxt)
+            m = nxt
+            if m % rcfg.sample_stride == 0 or m == rcfg.steps:
+                traj.append((m, self.get_state()[0]))
+        spins, energies, best, _ = self.readout()
+        cuts = None
+        if self.total_weight is not None:
+            cuts = ((self.total_weight - energies) / 2).astype(np.int64)
+        timing = {"total_ms": (time.perf_counter() - t0) * 1e3}
+        b = BatchResult(spins if want_spins else None, energies, cuts, best, timing, traj[-1][1], rcfg, tuning)
+        b.trajectory = traj
+        return b
 
     def batch_best_of(self, cfg: SolverConfig, tuning: TuningResult, n_batch: int, master_seed: int) -> RunResult:
         """bench.cpp:70-92: replicas seeded derive_seed(master, {batch, r}); min energy, ties -> lowest r."""
@@ -410,6 +440,7 @@ class BatchResult:
     x_final: Optional[np.ndarray]
     config: SolverConfig
     tuning: TuningResult
+    trajectory: Optional[list] = None  # [(m, x[R][n])] when config.sample_stride > 0
 
 
 def _mix64(z: int) -> int:
@@ -473,3 +504,92 @@ def sweep(solver: "Solver", m_values, a_values, reps: int, cfg_base: SolverConfi
             cells.append(SweepCell(mi, ai, int(m_steps), float(a), success_probability(e, target),
                                    float(e.mean()), float(e.min()), e.copy()))
     return cells
+
+
+SEED_STREAM_CHAOS = 4  # rng.hpp:37
+SEED_STREAM_CHAOS_PERTURB = 5  # rng.hpp:38
+
+
+class _HostXoshiro:
+    """rng.hpp:44-77 on the host, for building explicit initial states (chaos pairs)."""
+
+    M64 = (1 << 64) - 1
+
+    def __init__(self, seed: int):
+        z = seed
+        self.s = []
+        for _ in range(4):
+            z = (z + 0x9E3779B97F4A7C15) & self.M64
+            self.s.append(_mix64(z))
+
+    def next(self) -> int:
+        s0, s1, s2, s3 = self.s
+        M = self.M64
+        result = ((((s0 + s3) & M) << 23 | ((s0 + s3) & M) >> 41) & M) + s0 & M
+        t = (s1 << 17) & M
+        s2 ^= s0
+        s3 ^= s1
+        s1 ^= s2
+        s0 ^= s3
+        s2 ^= t
+        s3 = ((s3 << 45) | (s3 >> 19)) & M
+        self.s = [s0, s1, s2, s3]
+        return result
+
+    def random_sign(self) -> float:
+        return -1.0 if (self.next() >> 63) else 1.0
+
+
+def paired_initial_conditions(n: int, seed: int):
+    """chaos.cpp:11-18 rounded to fp32: x1 = +-0.1 (init_state chaos_probe), x2 = x1 +
+    2e-6 * random_sign from Xoshiro(derive_seed(seed, {chaos_perturb})); y = 0, p = 1."""
+    g = _HostXoshiro(seed)
+    x1 = np.array([0.1 * g.random_sign() for _ in range(n)])
+    h = _HostXoshiro(_derive_seed(seed, [SEED_STREAM_CHAOS_PERTURB]))
+    x2 = x1 + np.array([2e-6 * h.random_sign() for _ in range(n)])
+    return x1.astype(np.float32), x2.astype(np.float32)
+
+
+def normalized_distance(x1, x2) -> float:
+    """chaos.cpp:20-29: sqrt(sum (x1 - x2)^2 / (4 N))."""
+    d = np.asarray(x1, np.float64) - np.asarray(x2, np.float64)
+    return float(np.sqrt((d * d).sum() / (4.0 * d.size)))
+
+
+@dataclasses.dataclass
+class ChaosScanRow:  # chaos.hpp:44-51
+    a: float
+    mean_final_delta: float
+    std_error: float
+    reps: int
+    seed: int
+    final_deltas: np.ndarray
+
+
+def chaos_scan(solver: "Solver", a_values, reps: int, cfg_base: SolverConfig, tuning: TuningResult):
+    """sbopt::chaos_scan (chaos.cpp:65-102) on the GPU: all len(a_values) x reps
+    trajectory PAIRS run as 2 x that many replicas of one launch (per-replica A),
+    pair (ai, r) seeded derive_seed(cfg_base.seed, {chaos, ai, r})."""
+    if reps < 1:
+        raise ValueError("chaos scan needs reps >= 1")
+    cfg = resolve_config(dataclasses.replace(cfg_base, variant=Variant.gbsb), tuning)
+    n = solver.n
+    xs, a_rep = [], []
+    for ai, a in enumerate(a_values):
+        for r in range(reps):
+            x1, x2 = paired_initial_conditions(n, _derive_seed(cfg_base.seed, [SEED_STREAM_CHAOS, ai, r]))
+            xs += [x1, x2]
+            a_rep += [a, a]
+    x0 = np.stack(xs)
+    solver.set_state(x0, np.zeros_like(x0))
+    solver.set_replica_a(np.asarray(a_rep, np.float32))
+    solver.advance(cfg, 0, int(cfg.steps))
+    x, _, _ = solver.get_state()
+    solver.set_replica_a(None)
+    rows = []
+    for ai, a in enumerate(a_values):
+        d = np.array([normalized_distance(x[2 * (ai * reps + r)], x[2 * (ai * reps + r) + 1]) for r in range(reps)])
+        mean = float(d.mean())
+        se = float(np.sqrt(((d - mean) ** 2).sum() / (reps - 1) / reps)) if reps > 1 else 0.0
+        rows.append(ChaosScanRow(float(a), mean, se, reps, cfg_base.seed, d))
+    return rows

@@ -277,3 +277,24 @@ def test_sweep_grid_matches_mirror_per_cell(solver, orc):
                                cl.m_steps)
         assert (cl.energies == -0.5 * orc.energy2_i8(J, x)).all(), (cl.mi, cl.ai)
         assert cl.best_energy == cl.energies.min()
+
+
+def test_trajectory_sampling_records_start_strides_final(solver, orc):
+    """test_engine.cpp:232-249 analogue: stride 50 over M=120 -> m = 0, 50, 100, 120, bitwise states."""
+    from paper_2508_17655_b200 import SolverConfig, TuningResult, Variant
+
+    n, R = 40, 3
+    J = orc.gen_dense_i8(n, 1)
+    solver.set_instance(J)
+    x0, y0, p0 = orc.init_small_uniform(n, R, master=6)
+    cfg = SolverConfig(variant=Variant.gbsb, steps=120, dt=1.0, c=0.2, a=0.0, sample_stride=50)
+    b = solver.run_batch(cfg, TuningResult(c=0.2, dt=1.0), R, x0=x0, y0=y0)
+    assert [m for m, _ in b.trajectory] == [0, 50, 100, 120]
+    x, y, p = x0, y0, p0
+    prev = 0
+    for m, xs in b.trajectory[1:]:
+        x, y, p = orc.step_f32(2, J, x, y, p, prev, 120, np.float32(1.0), np.float32(0.2), np.float32(0.0), m - prev)
+        prev = m
+        assert (xs == x).all()
+    cfg.sample_stride = 0
+    assert solver.run_batch(cfg, TuningResult(c=0.2, dt=1.0), R, x0=x0, y0=y0).trajectory is None
