@@ -132,6 +132,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
       ptx::prefetch_tmap(&maps.Gin[1]);
       int stage = 0;
       uint32_t ph = 0;
+      const uint64_t keep = ptx::policy_evict_last();  // J and G are re-read every step: keep them in L2
       for (int g = pair; g < total; g += npairs) {
         const int s = g / T2, w = g % T2;
         const int n_blk = w / num_mp, mp = w % num_mp;
@@ -142,11 +143,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
           ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
           const uint32_t fb = ptx::mapa(full_bar(stage), 0);  // the leader's full barrier
           ptx::mbar_arrive_expect_tx_cluster(fb, Cfg::STAGE_BYTES);
-          ptx::tma_load_2d_pair(a_base + stage * Cfg::A_BYTES, &maps.J, fb, kb * Cfg::BK, m_blk * Cfg::BM);
+          ptx::tma_load_2d_pair_hint(a_base + stage * Cfg::A_BYTES, &maps.J, fb, kb * Cfg::BK, m_blk * Cfg::BM, keep);
 #pragma unroll
           for (int pl = 0; pl < NPLANES; ++pl)
-            ptx::tma_load_2d_pair(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES, gin, fb, kb * Cfg::BK,
-                                  pl * args.rpad + n_blk * N_PAIR + static_cast<int>(cr) * Cfg::B_HALF);
+            ptx::tma_load_2d_pair_hint(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES, gin, fb, kb * Cfg::BK,
+                                       pl * args.rpad + n_blk * N_PAIR + static_cast<int>(cr) * Cfg::B_HALF, keep);
           if (++stage == STAGES) {
             stage = 0;
             ph ^= 1u;
@@ -193,6 +194,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
       ptx::prefetch_tmap(&maps.Y);
       ptx::prefetch_tmap(&maps.P);
       int ck = 0;
+      const uint64_t stream = ptx::policy_evict_first();  // x, y, p are touched once per step
       for (int g = pair; g < total; g += npairs) {
         const int s = g / T2, w = g % T2;
         const int n_blk = w / num_mp, mp = w % num_mp;
@@ -203,9 +205,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
           ptx::mbar_wait(sempty_bar(b), ((ck / NBUF) & 1) ^ 1u);
           ptx::mbar_arrive_expect_tx(sfull_bar(b), 3 * Cfg::ST_ARR);
           const uint32_t sb = s_base + b * Cfg::BUF_BYTES;
-          ptx::tma_load_2d(sb, &maps.X, sfull_bar(b), i0, rb + c * CW);
-          ptx::tma_load_2d(sb + Cfg::ST_ARR, &maps.Y, sfull_bar(b), i0, rb + c * CW);
-          ptx::tma_load_2d(sb + 2 * Cfg::ST_ARR, &maps.P, sfull_bar(b), i0, rb + c * CW);
+          ptx::tma_load_2d_hint(sb, &maps.X, sfull_bar(b), i0, rb + c * CW, stream);
+          ptx::tma_load_2d_hint(sb + Cfg::ST_ARR, &maps.Y, sfull_bar(b), i0, rb + c * CW, stream);
+          ptx::tma_load_2d_hint(sb + 2 * Cfg::ST_ARR, &maps.P, sfull_bar(b), i0, rb + c * CW, stream);
         }
       }
     }
@@ -214,6 +216,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
       ptx::prefetch_tmap(&maps.Gout[0]);
       ptx::prefetch_tmap(&maps.Gout[1]);
       int ck = 0;
+      const uint64_t stream = ptx::policy_evict_first();
+      const uint64_t keep = ptx::policy_evict_last();
       for (int g = pair; g < total; g += npairs) {
         const int s = g / T2, w = g % T2;
         const int n_blk = w / num_mp, mp = w % num_mp;
@@ -224,12 +228,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
           ptx::mbar_wait(sdone_bar(b), (ck / NBUF) & 1);
           const uint32_t sb = s_base + b * Cfg::BUF_BYTES;
           const int r0 = rb + c * CW;
-          ptx::tma_store_2d(&maps.X, sb, i0, r0);
-          ptx::tma_store_2d(&maps.Y, sb + Cfg::ST_ARR, i0, r0);
-          ptx::tma_store_2d(&maps.P, sb + 2 * Cfg::ST_ARR, i0, r0);
+          ptx::tma_store_2d_hint(&maps.X, sb, i0, r0, stream);
+          ptx::tma_store_2d_hint(&maps.Y, sb + Cfg::ST_ARR, i0, r0, stream);
+          ptx::tma_store_2d_hint(&maps.P, sb + 2 * Cfg::ST_ARR, i0, r0, stream);
 #pragma unroll
           for (int pl = 0; pl < NPLANES; ++pl)
-            ptx::tma_store_2d(gout, sb + 3 * Cfg::ST_ARR + pl * Cfg::ST_G, i0, (NPLANES == 1 ? 0 : pl * args.rpad) + r0);
+            ptx::tma_store_2d_hint(gout, sb + 3 * Cfg::ST_ARR + pl * Cfg::ST_G, i0,
+                                   (NPLANES == 1 ? 0 : pl * args.rpad) + r0, keep);
           ptx::bulk_commit();
           ptx::bulk_wait_read0();
           ptx::mbar_arrive(sempty_bar(b));
