@@ -27,6 +27,53 @@ namespace sbg {
 constexpr int CSR_THREADS = 256;
 constexpr int CSR_RCHUNK = 128;  // replicas per warp task (32 lanes x 4)
 
+// L2 eviction priorities: the x/y/p stream is touched once per step (evict_first);
+// the gathered operand (q or signs, re-read ~degree times per step) should stay.
+namespace l2 {
+__device__ __forceinline__ uint64_t evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 ld_f4(const float* a, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_f4(float* a, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ int4 ld_i4(const int32_t* a, uint64_t pol) {
+  int4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_i4(int32_t* a, int4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.s32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(a), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t ld_u32(const void* a, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_u32(void* a, uint32_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol) : "memory");
+}
+}  // namespace l2
+
 template <bool SIGN>
 __global__ void __launch_bounds__(CSR_THREADS)
     csr_step_sm_kernel(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
@@ -38,6 +85,7 @@ __global__ void __launch_bounds__(CSR_THREADS)
   const int64_t tasks = static_cast<int64_t>(n) * chunks;
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t stream = l2::evict_first(), keep = l2::evict_last();
   for (int64_t t = wid; t < tasks; t += nw) {
     const int i = static_cast<int>(t / chunks);
     const int r = static_cast<int>(t % chunks) * CSR_RCHUNK + 4 * lane;  // first of this lane's 4 replicas
@@ -56,13 +104,14 @@ __global__ void __launch_bounds__(CSR_THREADS)
         const int v = __shfl_sync(0xffffffffu, vl, kk);
         if (r < R) {
           if (SIGN) {
-            const char4 s = *reinterpret_cast<const char4*>(static_cast<const int8_t*>(g_cur) + static_cast<size_t>(j) * rp + r);
+            const uint32_t w = l2::ld_u32(static_cast<const int8_t*>(g_cur) + static_cast<size_t>(j) * rp + r, keep);
+            const char4 s = *reinterpret_cast<const char4*>(&w);
             acc0 += v * s.x;
             acc1 += v * s.y;
             acc2 += v * s.z;
             acc3 += v * s.w;
           } else {
-            const int4 q = *reinterpret_cast<const int4*>(static_cast<const int32_t*>(g_cur) + static_cast<size_t>(j) * rp + r);
+            const int4 q = l2::ld_i4(static_cast<const int32_t*>(g_cur) + static_cast<size_t>(j) * rp + r, keep);
             acc0 += static_cast<long long>(v) * q.x;
             acc1 += static_cast<long long>(v) * q.y;
             acc2 += static_cast<long long>(v) * q.z;
@@ -73,9 +122,9 @@ __global__ void __launch_bounds__(CSR_THREADS)
     }
     if (r >= R) continue;
     const size_t off = static_cast<size_t>(i) * rp + r;
-    float4 x4 = *reinterpret_cast<const float4*>(xs + off);
-    float4 y4 = *reinterpret_cast<const float4*>(ys + off);
-    float4 p4 = *reinterpret_cast<const float4*>(ps + off);
+    float4 x4 = l2::ld_f4(xs + off, stream);
+    float4 y4 = l2::ld_f4(ys + off, stream);
+    float4 p4 = l2::ld_f4(ps + off, stream);
     float F[4];
     const long long acc[4] = {acc0, acc1, acc2, acc3};
 #pragma unroll
@@ -91,19 +140,19 @@ __global__ void __launch_bounds__(CSR_THREADS)
     gsb_phase(F[2], x4.z, y4.z, p4.z, kk[2]);
     gsb_phase(F[3], x4.w, y4.w, p4.w, kk[3]);
     // replicas >= R inside the last chunk are padding: their slots exist (rp) and stay inert
-    *reinterpret_cast<float4*>(xs + off) = x4;
-    *reinterpret_cast<float4*>(ys + off) = y4;
-    *reinterpret_cast<float4*>(ps + off) = p4;
+    l2::st_f4(xs + off, x4, stream);
+    l2::st_f4(ys + off, y4, stream);
+    l2::st_f4(ps + off, p4, stream);
     if (SIGN) {
       char4 s;
       s.x = sgn8(x4.x);
       s.y = sgn8(x4.y);
       s.z = sgn8(x4.z);
       s.w = sgn8(x4.w);
-      *reinterpret_cast<char4*>(static_cast<int8_t*>(g_next) + off) = s;
+      l2::st_u32(static_cast<int8_t*>(g_next) + off, *reinterpret_cast<uint32_t*>(&s), keep);
     } else {
-      *reinterpret_cast<int4*>(static_cast<int32_t*>(g_next) + off) =
-          make_int4(quant30(x4.x), quant30(x4.y), quant30(x4.z), quant30(x4.w));
+      l2::st_i4(static_cast<int32_t*>(g_next) + off,
+                make_int4(quant30(x4.x), quant30(x4.y), quant30(x4.z), quant30(x4.w)), keep);
     }
   }
 }

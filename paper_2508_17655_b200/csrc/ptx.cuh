@@ -306,3 +306,20 @@ __device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* m, uint32_t
 
 }  // namespace ptx
 }  // namespace sbg
+
+namespace sbg {
+namespace ptx {
+// One elected lane of a converged warp. Issuing tcgen05/TMA from an elected lane
+// (rather than `if (lane == 0)`) lets the compiler keep descriptors in uniform
+// registers instead of wrapping every instruction in a waterfall loop.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+}  // namespace ptx
+}  // namespace sbg

@@ -800,13 +800,28 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
           case -1: rc = launch_multistep<1, BN_SIGN, SIGN_STAGES, SIGN_NBUF>(ctx, ctx->maps_sign[cur], a); break;
           case 2: rc = launch_multistep_pair<1, NPAIR_SIGN, 2, 6>(ctx, ctx->maps_sign[cur], a); break;
           case 3: rc = launch_multistep_pair<1, NPAIR_SIGN, 4, 3>(ctx, ctx->maps_sign[cur], a); break;
+          case 4: rc = launch_multistep_pair<1, NPAIR_SIGN, 2, 5>(ctx, ctx->maps_sign[cur], a); break;
           default: rc = launch_multistep_pair<1, NPAIR_SIGN, 3, 4>(ctx, ctx->maps_sign[cur], a);
         }
       } else {
         switch (pair_ok ? knob : -1) {
           case 2: rc = launch_multistep_pair<NPL, NPAIR_PLANE, 3, 3>(ctx, ctx->pmaps_planes[cur], a); break;
           case 3: rc = launch_multistep_pair<NPL, NPAIR_PLANE, 4, 2>(ctx, ctx->pmaps_planes[cur], a); break;
-          default: rc = launch_multistep<NPL, BN_PLANE, PLANE_STAGES, PLANE_NBUF>(ctx, ctx->maps_planes[cur], a);
+          case 6: rc = launch_multistep_pair<NPL, NPAIR_PLANE, 5, 2>(ctx, ctx->pmaps_planes[cur], a); break;
+          case 7: rc = launch_multistep<NPL, BN_PLANE, PLANE_STAGES, PLANE_NBUF>(ctx, ctx->maps_planes[cur], a); break;
+          case 4: {  // smaller replica tiles: more tiles per step for small R
+            MultiStepArgs a32 = a;
+            a32.num_n = int32_t(ctx->rpad / 32);
+            rc = launch_multistep<NPL, 32, 4, 3>(ctx, ctx->fxmaps_planes[cur], a32);
+            break;
+          }
+          case 5: {
+            MultiStepArgs a32 = a;
+            a32.num_n = int32_t(ctx->rpad / 32);
+            rc = launch_multistep<NPL, 32, 3, 4>(ctx, ctx->fxmaps_planes[cur], a32);
+            break;
+          }
+          default: rc = launch_multistep_pair<NPL, NPAIR_PLANE, 4, 2>(ctx, ctx->pmaps_planes[cur], a);
         }
       }
       if (rc) return rc;

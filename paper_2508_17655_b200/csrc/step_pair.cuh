@@ -126,10 +126,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
   const int KB = args.kpad / Cfg::BK;
 
   if (warp == 0) {
-    if (lane == 0) {  // ------------------------------------------- operand producer (both CTAs)
-      ptx::prefetch_tmap(&maps.J);
-      ptx::prefetch_tmap(&maps.Gin[0]);
-      ptx::prefetch_tmap(&maps.Gin[1]);
+    {  // -------------------------------------------------------------- operand producer (both CTAs)
+      // whole warp walks the schedule (uniform values), one elected lane issues TMA
+      if (ptx::elect_one()) {
+        ptx::prefetch_tmap(&maps.J);
+        ptx::prefetch_tmap(&maps.Gin[0]);
+        ptx::prefetch_tmap(&maps.Gin[1]);
+      }
       int stage = 0;
       uint32_t ph = 0;
       const uint64_t keep = ptx::policy_evict_last();  // J and G are re-read every step: keep them in L2
@@ -141,13 +144,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
         const CUtensorMap* gin = &maps.Gin[s & 1];
         for (int kb = 0; kb < KB; ++kb) {
           ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
-          const uint32_t fb = ptx::mapa(full_bar(stage), 0);  // the leader's full barrier
-          ptx::mbar_arrive_expect_tx_cluster(fb, Cfg::STAGE_BYTES);
-          ptx::tma_load_2d_pair_hint(a_base + stage * Cfg::A_BYTES, &maps.J, fb, kb * Cfg::BK, m_blk * Cfg::BM, keep);
+          if (ptx::elect_one()) {
+            const uint32_t fb = ptx::mapa(full_bar(stage), 0);  // the leader's full barrier
+            ptx::mbar_arrive_expect_tx_cluster(fb, Cfg::STAGE_BYTES);
+            ptx::tma_load_2d_pair_hint(a_base + stage * Cfg::A_BYTES, &maps.J, fb, kb * Cfg::BK, m_blk * Cfg::BM, keep);
 #pragma unroll
-          for (int pl = 0; pl < NPLANES; ++pl)
-            ptx::tma_load_2d_pair_hint(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES, gin, fb, kb * Cfg::BK,
-                                       pl * args.rpad + n_blk * N_PAIR + static_cast<int>(cr) * Cfg::B_HALF, keep);
+            for (int pl = 0; pl < NPLANES; ++pl)
+              ptx::tma_load_2d_pair_hint(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES, gin, fb, kb * Cfg::BK,
+                                         pl * args.rpad + n_blk * N_PAIR + static_cast<int>(cr) * Cfg::B_HALF, keep);
+          }
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             ph ^= 1u;
@@ -156,7 +162,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {  // ---------------------------------- MMA issuer (leader only)
+    if (leader) {  // ------------------------------------------ MMA issuer (leader CTA only)
+      // whole warp walks the schedule; one elected lane issues (uniform descriptors)
       constexpr uint32_t idesc_s = ptx::idesc_i8(256, N_PAIR, true, true);
       constexpr uint32_t idesc_u = ptx::idesc_i8(256, N_PAIR, true, false);
       int stage = 0;
@@ -170,22 +177,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
         for (int kb = 0; kb < KB; ++kb) {
           ptx::mbar_wait(full_bar(stage), ph);
           ptx::tc_fence_after();
-          const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + stage * Cfg::A_BYTES);
+          if (ptx::elect_one()) {
+            const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + stage * Cfg::A_BYTES);
 #pragma unroll
-          for (int pl = 0; pl < NPLANES; ++pl) {
-            const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES);
-            const uint32_t idesc = (NPLANES == 1 || pl == NPLANES - 1) ? idesc_s : idesc_u;
+            for (int pl = 0; pl < NPLANES; ++pl) {
+              const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES);
+              const uint32_t idesc = (NPLANES == 1 || pl == NPLANES - 1) ? idesc_s : idesc_u;
 #pragma unroll
-            for (int k = 0; k < Cfg::BK / 32; ++k)
-              ptx::mma_i8_pair(d_base + pl * N_PAIR, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+              for (int k = 0; k < Cfg::BK / 32; ++k)
+                ptx::mma_i8_pair(d_base + pl * N_PAIR, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            }
+            ptx::mma_commit_pair_mc(empty_bar(stage), 0x3);
           }
-          ptx::mma_commit_pair_mc(empty_bar(stage), 0x3);
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             ph ^= 1u;
           }
         }
-        ptx::mma_commit_pair_mc(tfull_bar(buf), 0x3);
+        if (ptx::elect_one()) ptx::mma_commit_pair_mc(tfull_bar(buf), 0x3);
+        __syncwarp();
       }
     }
   } else if (warp == 2) {

@@ -208,10 +208,13 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
   };
 
   if (warp == 0) {
-    if (lane == 0 && args.dbg < 2) {  // ---------------------------- operand producer
-      ptx::prefetch_tmap(&maps.J);
-      ptx::prefetch_tmap(&maps.Gin[0]);
-      ptx::prefetch_tmap(&maps.Gin[1]);
+    if (args.dbg < 2) {  // ------------------------------------------ operand producer
+      // whole warp walks the schedule (uniform values), one elected lane issues TMA
+      if (ptx::elect_one()) {
+        ptx::prefetch_tmap(&maps.J);
+        ptx::prefetch_tmap(&maps.Gin[0]);
+        ptx::prefetch_tmap(&maps.Gin[1]);
+      }
       int stage = 0;
       uint32_t ph = 0;
       for (int g = blockIdx.x; g < total; g += gridDim.x) {
@@ -221,15 +224,18 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
         const CUtensorMap* gin = &maps.Gin[s & 1];
         for (int kb = 0; kb < KB; ++kb) {
           ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
-          ptx::mbar_arrive_expect_tx(full_bar(stage), Cfg::STAGE_BYTES);
+          if (ptx::elect_one()) {
+            ptx::mbar_arrive_expect_tx(full_bar(stage), Cfg::STAGE_BYTES);
 #pragma unroll
-          for (int ap = 0; ap < NA; ++ap)
-            ptx::tma_load_2d(a_base + (stage * NA + ap) * Cfg::A_BYTES, &maps.J, full_bar(stage), kb * Cfg::BK,
-                             ap * args.num_m * Cfg::BM + m_blk * Cfg::BM);
+            for (int ap = 0; ap < NA; ++ap)
+              ptx::tma_load_2d(a_base + (stage * NA + ap) * Cfg::A_BYTES, &maps.J, full_bar(stage), kb * Cfg::BK,
+                               ap * args.num_m * Cfg::BM + m_blk * Cfg::BM);
 #pragma unroll
-          for (int pl = 0; pl < NPLANES; ++pl)
-            ptx::tma_load_2d(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES, gin, full_bar(stage),
-                             kb * Cfg::BK, pl * args.rpad + n_blk * BN);
+            for (int pl = 0; pl < NPLANES; ++pl)
+              ptx::tma_load_2d(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES, gin, full_bar(stage),
+                               kb * Cfg::BK, pl * args.rpad + n_blk * BN);
+          }
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             ph ^= 1u;
@@ -238,7 +244,8 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && args.dbg < 2) {  // ---------------------------------- MMA issuer
+    if (args.dbg < 2) {  // ------------------------------------------------ MMA issuer
+      // the whole warp walks the (warp-uniform) schedule; one elected lane issues
       int stage = 0;
       uint32_t ph = 0;
       int lt = 0;
@@ -250,30 +257,35 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
         for (int kb = 0; kb < KB; ++kb) {
           ptx::mbar_wait(full_bar(stage), ph);
           ptx::tc_fence_after();
+          if (ptx::elect_one()) {
 #pragma unroll
-          for (int ap = 0; ap < NA; ++ap) {
-            const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + (stage * NA + ap) * Cfg::A_BYTES);
+            for (int ap = 0; ap < NA; ++ap) {
+              const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + (stage * NA + ap) * Cfg::A_BYTES);
 #pragma unroll
-            for (int pl = 0; pl < NPLANES; ++pl) {
-              const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES);
-              // plane signedness: only the top plane of a multi-plane operand is signed
-              const uint32_t idesc = ptx::idesc_i8(128, BN, NA == 1 || ap == NA - 1, NPLANES == 1 || pl == NPLANES - 1);
-              // products of equal weight 2^(8(ap+pl)) share one accumulator; the first
-              // pair of each weight (in this loop order) starts it at kb == 0
-              const int w = ap + pl;
-              const bool first_pair = ap == (w - (NPLANES - 1) > 0 ? w - (NPLANES - 1) : 0);
+              for (int pl = 0; pl < NPLANES; ++pl) {
+                const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES);
+                // plane signedness: only the top plane of a multi-plane operand is signed
+                const uint32_t idesc =
+                    ptx::idesc_i8(128, BN, NA == 1 || ap == NA - 1, NPLANES == 1 || pl == NPLANES - 1);
+                // products of equal weight 2^(8(ap+pl)) share one accumulator; the first
+                // pair of each weight (in this loop order) starts it at kb == 0
+                const int w = ap + pl;
+                const bool first_pair = ap == (w - (NPLANES - 1) > 0 ? w - (NPLANES - 1) : 0);
 #pragma unroll
-              for (int k = 0; k < Cfg::BK / 32; ++k)
-                ptx::mma_i8(d_base + w * BN, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0 || !first_pair);
+                for (int k = 0; k < Cfg::BK / 32; ++k)
+                  ptx::mma_i8(d_base + w * BN, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0 || !first_pair);
+              }
             }
+            ptx::mma_commit(empty_bar(stage));
           }
-          ptx::mma_commit(empty_bar(stage));
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             ph ^= 1u;
           }
         }
-        ptx::mma_commit(tfull_bar(buf));
+        if (ptx::elect_one()) ptx::mma_commit(tfull_bar(buf));
+        __syncwarp();
       }
     }
   } else if (warp == 2) {
