@@ -323,3 +323,12 @@ __device__ __forceinline__ bool elect_one() {
 }
 }  // namespace ptx
 }  // namespace sbg
+
+namespace sbg {
+namespace ptx {
+template <>
+__device__ __forceinline__ void tmem_ld<2>(uint32_t taddr, uint32_t (&v)[2]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(taddr));
+}
+}  // namespace ptx
+}  // namespace sbg

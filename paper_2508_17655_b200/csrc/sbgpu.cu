@@ -88,6 +88,7 @@ struct sbg_ctx {
   TmaMaps maps_sign[2], maps_planes[2];  // multi-step kernel maps, indexed by the current B buffer
   TmaMaps pmaps_planes[2];               // pair kernel, fixed-point planes (B half = 32 rows)
   TmaMaps fxmaps_sign[2], fxmaps_planes[2];  // real-J kernels (B tiles of 64 / 32 rows)
+  TmaMaps maps_sign_cw8[2];                  // sign pair kernel with 8-replica state chunks
   unsigned long long* dE2p = nullptr;    // real-J readout: per-J-plane partial E2 [FX_NA][rpad]
   // CSR: spin-major working copies [npad][rp] and the ping-pong gathered operand (q int32 / sign int8)
   float *dXs = nullptr, *dYs = nullptr, *dPs = nullptr;
@@ -211,10 +212,10 @@ int launch_multistep(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& a) 
   return SBG_OK;
 }
 
-template <int NP, int NPAIR, int ST, int NB>
+template <int NP, int NPAIR, int ST, int NB, int CW = 16>
 int launch_multistep_pair(sbg_ctx* ctx, const TmaMaps& maps, MultiStepArgs a) {
-  using Cfg = PairStepCfg<NP, NPAIR, ST, NB>;
-  auto kern = gsb_multistep_pair_kernel<NP, NPAIR, ST, NB>;
+  using Cfg = PairStepCfg<NP, NPAIR, ST, NB, CW>;
+  auto kern = gsb_multistep_pair_kernel<NP, NPAIR, ST, NB, CW>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
   a.num_n = int32_t(ctx->rpad / NPAIR);
   const int64_t pair_tiles = int64_t(a.num_m / 2) * a.num_n * a.nsteps;
@@ -340,6 +341,22 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
         mp.P = P;
       }
       ctx->pmaps_planes[cur] = ctx->maps_planes[cur];
+      ctx->maps_sign_cw8[cur] = ctx->maps_sign[cur];
+      {
+        const uint64_t gvalid = uint64_t(ctx->sharded ? ctx->n_global : ctx->n);
+        TmaMaps& m8 = ctx->maps_sign_cw8[cur];
+        int rc8 = encode_2d(ctx, &m8.Gout[0], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ 1], gvalid, R, gdim(ctx),
+                            128, 8, CU_TENSOR_MAP_SWIZZLE_NONE);
+        if (!rc8)
+          rc8 = encode_2d(ctx, &m8.Gout[1], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur], gvalid, R, gdim(ctx), 128, 8,
+                          CU_TENSOR_MAP_SWIZZLE_NONE);
+        float* arrs8[3] = {ctx->dX, ctx->dY, ctx->dP};
+        CUtensorMap* outs8[3] = {&m8.X, &m8.Y, &m8.P};
+        for (int a8 = 0; a8 < 3 && !rc8; ++a8)
+          rc8 = encode_2d(ctx, outs8[a8], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, arrs8[a8], ctx->n, R,
+                          sizeof(float) * ctx->npad, 128, 8, CU_TENSOR_MAP_SWIZZLE_NONE);
+        if (rc8) return rc8;
+      }
       ctx->fxmaps_sign[cur] = ctx->maps_sign[cur];
       ctx->fxmaps_planes[cur] = ctx->maps_planes[cur];
       for (int par = 0; par < 2; ++par) {
@@ -801,6 +818,8 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
           case 2: rc = launch_multistep_pair<1, NPAIR_SIGN, 2, 6>(ctx, ctx->maps_sign[cur], a); break;
           case 3: rc = launch_multistep_pair<1, NPAIR_SIGN, 4, 3>(ctx, ctx->maps_sign[cur], a); break;
           case 4: rc = launch_multistep_pair<1, NPAIR_SIGN, 2, 5>(ctx, ctx->maps_sign[cur], a); break;
+          case 5: rc = launch_multistep_pair<1, NPAIR_SIGN, 3, 8, 8>(ctx, ctx->maps_sign_cw8[cur], a); break;
+          case 6: rc = launch_multistep_pair<1, NPAIR_SIGN, 2, 10, 8>(ctx, ctx->maps_sign_cw8[cur], a); break;
           default: rc = launch_multistep_pair<1, NPAIR_SIGN, 3, 4>(ctx, ctx->maps_sign[cur], a);
         }
       } else {

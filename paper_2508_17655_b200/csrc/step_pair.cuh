@@ -31,7 +31,7 @@
 
 namespace sbg {
 
-template <int NPLANES, int N_PAIR, int STAGES_, int NBUF_>
+template <int NPLANES, int N_PAIR, int STAGES_, int NBUF_, int CW_ = 16>
 struct PairStepCfg {
   static constexpr int BM = 128;                        // spins per CTA
   static constexpr int BK = 128;                        // K bytes per stage
@@ -41,7 +41,7 @@ struct PairStepCfg {
   static constexpr int STAGE_BYTES = A_BYTES + NPLANES * B_PLANE_BYTES;
   static constexpr int STAGES = STAGES_;
   static constexpr int EPI_WARPS = 16;
-  static constexpr int CW = 16;
+  static constexpr int CW = CW_;                        // replicas per state chunk (TMA box rows)
   static constexpr int CWQ = CW / (EPI_WARPS / 4);
   static constexpr int NBUF = NBUF_;
   static constexpr int ST_ARR = CW * BM * 4;
@@ -59,10 +59,10 @@ struct PairStepCfg {
   static_assert(TMEM_COLS == 256 || TMEM_COLS == 512, "TMEM allocation");
 };
 
-template <int NPLANES, int N_PAIR, int STAGES_, int NBUF_>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES, N_PAIR, STAGES_, NBUF_>::THREADS, 1)
+template <int NPLANES, int N_PAIR, int STAGES_, int NBUF_, int CW_ = 16>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES, N_PAIR, STAGES_, NBUF_, CW_>::THREADS, 1)
     gsb_multistep_pair_kernel(const __grid_constant__ TmaMaps maps, const MultiStepArgs args) {
-  using Cfg = PairStepCfg<NPLANES, N_PAIR, STAGES_, NBUF_>;
+  using Cfg = PairStepCfg<NPLANES, N_PAIR, STAGES_, NBUF_, CW_>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int NBUF = Cfg::NBUF;
   constexpr int CW = Cfg::CW;
