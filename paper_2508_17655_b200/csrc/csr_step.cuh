@@ -8,8 +8,9 @@
 //
 // Layout: while stepping, the state lives SPIN-MAJOR ([npad][rp], replicas
 // contiguous) so that the SpMM gather of row j for a block of replicas is one
-// contiguous, vectorised read: a warp owns (row i, 128 replicas), lane l holds
-// replicas 4l..4l+3 (int4 / char4 / float4 accesses, 512 B per warp per nonzero).
+// contiguous, vectorised read: a warp owns (row i, 256 replicas), lane l holds
+// replicas 4l..4l+3 and 128+4l..+3 (int4 / char4 / float4 accesses, two 512 B
+// gathers per warp per nonzero: twice the loads in flight of one group).
 // The row's (col, val) pairs are loaded once, one per lane, and broadcast with
 // shuffles, so all gathers of a row are independent (memory-level parallelism).
 // The gathered operand (q or sgn x) is ping-ponged between two buffers because
@@ -25,7 +26,8 @@
 namespace sbg {
 
 constexpr int CSR_THREADS = 256;
-constexpr int CSR_RCHUNK = 128;  // replicas per warp task (32 lanes x 4)
+constexpr int CSR_VEC = 2;                     // 4-replica groups per lane (more gathers in flight)
+constexpr int CSR_RCHUNK = 128 * CSR_VEC;      // replicas per warp task
 
 // L2 eviction priorities: the x/y/p stream is touched once per step (evict_first);
 // the gathered operand (q or signs, re-read ~degree times per step) should stay.
@@ -88,9 +90,11 @@ __global__ void __launch_bounds__(CSR_THREADS)
   const uint64_t stream = l2::evict_first(), keep = l2::evict_last();
   for (int64_t t = wid; t < tasks; t += nw) {
     const int i = static_cast<int>(t / chunks);
-    const int r = static_cast<int>(t % chunks) * CSR_RCHUNK + 4 * lane;  // first of this lane's 4 replicas
+    const int rc = static_cast<int>(t % chunks) * CSR_RCHUNK + 4 * lane;  // group u covers rc + 128 u .. +3
     const int kb = rowptr[i], ke = rowptr[i + 1];
-    long long acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+    long long acc[CSR_VEC][4];
+#pragma unroll
+    for (int u = 0; u < CSR_VEC; ++u) acc[u][0] = acc[u][1] = acc[u][2] = acc[u][3] = 0;
     for (int k0 = kb; k0 < ke; k0 += 32) {
       const int cnt = min(32, ke - k0);
       int jl = 0, vl = 0;
@@ -98,61 +102,68 @@ __global__ void __launch_bounds__(CSR_THREADS)
         jl = col[k0 + lane];
         vl = val[k0 + lane];
       }
-#pragma unroll 4
+#pragma unroll 2
       for (int kk = 0; kk < cnt; ++kk) {
         const int j = __shfl_sync(0xffffffffu, jl, kk);
-        const int v = __shfl_sync(0xffffffffu, vl, kk);
-        if (r < R) {
-          if (SIGN) {
-            const uint32_t w = l2::ld_u32(static_cast<const int8_t*>(g_cur) + static_cast<size_t>(j) * rp + r, keep);
-            const char4 s = *reinterpret_cast<const char4*>(&w);
-            acc0 += v * s.x;
-            acc1 += v * s.y;
-            acc2 += v * s.z;
-            acc3 += v * s.w;
-          } else {
-            const int4 q = l2::ld_i4(static_cast<const int32_t*>(g_cur) + static_cast<size_t>(j) * rp + r, keep);
-            acc0 += static_cast<long long>(v) * q.x;
-            acc1 += static_cast<long long>(v) * q.y;
-            acc2 += static_cast<long long>(v) * q.z;
-            acc3 += static_cast<long long>(v) * q.w;
+        const long long v = __shfl_sync(0xffffffffu, vl, kk);
+#pragma unroll
+        for (int u = 0; u < CSR_VEC; ++u) {
+          const int r = rc + 128 * u;
+          if (r < R) {
+            if (SIGN) {
+              const uint32_t w = l2::ld_u32(static_cast<const int8_t*>(g_cur) + static_cast<size_t>(j) * rp + r, keep);
+              const char4 s = *reinterpret_cast<const char4*>(&w);
+              acc[u][0] += v * s.x;
+              acc[u][1] += v * s.y;
+              acc[u][2] += v * s.z;
+              acc[u][3] += v * s.w;
+            } else {
+              const int4 q = l2::ld_i4(static_cast<const int32_t*>(g_cur) + static_cast<size_t>(j) * rp + r, keep);
+              acc[u][0] += v * q.x;
+              acc[u][1] += v * q.y;
+              acc[u][2] += v * q.z;
+              acc[u][3] += v * q.w;
+            }
           }
         }
       }
     }
-    if (r >= R) continue;
-    const size_t off = static_cast<size_t>(i) * rp + r;
-    float4 x4 = l2::ld_f4(xs + off, stream);
-    float4 y4 = l2::ld_f4(ys + off, stream);
-    float4 p4 = l2::ld_f4(ps + off, stream);
-    float F[4];
-    const long long acc[4] = {acc0, acc1, acc2, acc3};
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      F[u] = SIGN ? static_cast<float>(acc[u]) : __fmul_rn(__ll2float_rn(acc[u]), 0x1p-30f);
-    PhaseConsts kk[4] = {k, k, k, k};
-    if (a_rep) {
+    for (int u = 0; u < CSR_VEC; ++u) {
+      const int r = rc + 128 * u;
+      if (r >= R) continue;
+      const size_t off = static_cast<size_t>(i) * rp + r;
+      float4 x4 = l2::ld_f4(xs + off, stream);
+      float4 y4 = l2::ld_f4(ys + off, stream);
+      float4 p4 = l2::ld_f4(ps + off, stream);
+      float F[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) kk[u].a = a_rep[min(r + u, R - 1)];
-    }
-    gsb_phase(F[0], x4.x, y4.x, p4.x, kk[0]);
-    gsb_phase(F[1], x4.y, y4.y, p4.y, kk[1]);
-    gsb_phase(F[2], x4.z, y4.z, p4.z, kk[2]);
-    gsb_phase(F[3], x4.w, y4.w, p4.w, kk[3]);
-    // replicas >= R inside the last chunk are padding: their slots exist (rp) and stay inert
-    l2::st_f4(xs + off, x4, stream);
-    l2::st_f4(ys + off, y4, stream);
-    l2::st_f4(ps + off, p4, stream);
-    if (SIGN) {
-      char4 s;
-      s.x = sgn8(x4.x);
-      s.y = sgn8(x4.y);
-      s.z = sgn8(x4.z);
-      s.w = sgn8(x4.w);
-      l2::st_u32(static_cast<int8_t*>(g_next) + off, *reinterpret_cast<uint32_t*>(&s), keep);
-    } else {
-      l2::st_i4(static_cast<int32_t*>(g_next) + off,
-                make_int4(quant30(x4.x), quant30(x4.y), quant30(x4.z), quant30(x4.w)), keep);
+      for (int e = 0; e < 4; ++e)
+        F[e] = SIGN ? static_cast<float>(acc[u][e]) : __fmul_rn(__ll2float_rn(acc[u][e]), 0x1p-30f);
+      PhaseConsts kk[4] = {k, k, k, k};
+      if (a_rep) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) kk[e].a = a_rep[min(r + e, R - 1)];
+      }
+      gsb_phase(F[0], x4.x, y4.x, p4.x, kk[0]);
+      gsb_phase(F[1], x4.y, y4.y, p4.y, kk[1]);
+      gsb_phase(F[2], x4.z, y4.z, p4.z, kk[2]);
+      gsb_phase(F[3], x4.w, y4.w, p4.w, kk[3]);
+      // replicas >= R inside the last group are padding: their slots exist (rp) and stay inert
+      l2::st_f4(xs + off, x4, stream);
+      l2::st_f4(ys + off, y4, stream);
+      l2::st_f4(ps + off, p4, stream);
+      if (SIGN) {
+        char4 s;
+        s.x = sgn8(x4.x);
+        s.y = sgn8(x4.y);
+        s.z = sgn8(x4.z);
+        s.w = sgn8(x4.w);
+        l2::st_u32(static_cast<int8_t*>(g_next) + off, *reinterpret_cast<uint32_t*>(&s), keep);
+      } else {
+        l2::st_i4(static_cast<int32_t*>(g_next) + off,
+                  make_int4(quant30(x4.x), quant30(x4.y), quant30(x4.z), quant30(x4.w)), keep);
+      }
     }
   }
 }
