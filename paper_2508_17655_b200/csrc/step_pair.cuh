@@ -126,7 +126,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
   const int KB = args.kpad / Cfg::BK;
 
   if (warp == 0) {
-    {  // -------------------------------------------------------------- operand producer (both CTAs)
+    if (args.dbg < 2) {  // ------------------------------------------- operand producer (both CTAs)
       // whole warp walks the schedule (uniform values), one elected lane issues TMA
       if (ptx::elect_one()) {
         ptx::prefetch_tmap(&maps.J);
@@ -162,7 +162,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
       }
     }
   } else if (warp == 1) {
-    if (leader) {  // ------------------------------------------ MMA issuer (leader CTA only)
+    if (leader && args.dbg < 2) {  // --------------------------------- MMA issuer (leader CTA only)
       // whole warp walks the schedule; one elected lane issues (uniform descriptors)
       constexpr uint32_t idesc_s = ptx::idesc_i8(256, N_PAIR, true, true);
       constexpr uint32_t idesc_u = ptx::idesc_i8(256, N_PAIR, true, false);
@@ -271,7 +271,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
       const int rbase = ((g % T2) / num_mp) * N_PAIR;  // first replica of this pair tile
       k.inv = __frcp_rn(static_cast<float>(args.M - (args.t_begin + static_cast<uint64_t>(s))));
       const int buf = lt & 1;
-      ptx::mbar_wait(tfull_bar(buf), (lt >> 1) & 1);
+      if (args.dbg < 2) ptx::mbar_wait(tfull_bar(buf), (lt >> 1) & 1);
       __syncwarp();
       ptx::tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * Cfg::ACC_COLS;
