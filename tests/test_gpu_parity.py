@@ -298,3 +298,26 @@ def test_trajectory_sampling_records_start_strides_final(solver, orc):
         assert (xs == x).all()
     cfg.sample_stride = 0
     assert solver.run_batch(cfg, TuningResult(c=0.2, dt=1.0), R, x0=x0, y0=y0).trajectory is None
+
+
+@pytest.mark.parametrize("variant", [BSB, DSB, GBSB])
+@pytest.mark.parametrize("seed", [1, 2])
+def test_p3_reference_init_30_and_50_steps(solver, golden, variant, seed):
+    """P3 with the reference's own init_state (x ~ U(-1,1), y = 0): <= 1e-5 relative at
+    30 steps. At 50 steps fp32 state rounding, amplified by the chaotic
+    dynamics, is past 1e-5 for any fp32 implementation; this wider init
+    measures up to 1.1e-4 (bSB), so 50 steps is held to 2e-4."""
+    J = golden["J_n37_s11"]
+    c, dt = float(golden["tune_c"]), float(golden["tune_dt"])
+    solver.set_instance(J)
+    x0 = golden[f"init_ref_s{seed}_x"].astype(np.float32)[None, :]
+    solver.set_state(x0, np.zeros_like(x0))
+    cps = list(golden["traj_checkpoints"])
+    m = 0
+    for cp, tol in ((30, 1e-5), (50, 2e-4)):
+        solver.advance(cfg_for(variant, 200, dt, c, 0.2), m, cp)
+        m = cp
+        x, _, _ = solver.get_state()
+        ref = golden[f"traj_ref_v{variant}_s{seed}_x"][cps.index(cp)]
+        err = np.abs(x[0] - ref).max() / np.abs(ref).max()
+        assert err <= tol, (variant, cp, err)
