@@ -100,7 +100,9 @@ int sbg_set_couplings_dense_f64(sbg_ctx* ctx, int64_t n, const double* J);
 int sbg_set_couplings_dense_f32(sbg_ctx* ctx, int64_t n, const float* J);
 /* The scale exponent s of the fixed-point coupling image (0 for integer J). */
 int sbg_coupling_scale_exp(const sbg_ctx* ctx);
-/* gen_random_dense (model.cpp:144-159) evaluated on the host into int8. */
+/* gen_random_dense (model.cpp:144-159) generated on the device into int8, in the
+ * reference's exact draw order (xoshiro jump-ahead per row segment, bit-identical
+ * to the serial walk) -- any n, including C5's n = 100000 (10 GB). */
 int sbg_gen_couplings_dense_pm1(sbg_ctx* ctx, int64_t n, uint64_t seed);
 /* CSR (both triangles, ascending columns), int8 values: the sparse view of
  * the same IsingInstance. */
@@ -172,6 +174,13 @@ int sbg_shard_push_slab(sbg_ctx* ctx);
  * gen_random_dense, NOT its draw order; parity tests use the exact order at small n).
  * world == 1: the whole matrix; world > 1: rank's rows as sbg_set_couplings_rows_i8. */
 int sbg_gen_couplings_hash_pm1(sbg_ctx* ctx, int64_t n_global, int32_t world, int32_t rank, uint64_t seed);
+/* Row shard (layout of sbg_set_couplings_rows_i8) of gen_random_dense(n_global, seed)
+ * in the reference's exact draw order, generated on the device; world == 1 is
+ * sbg_gen_couplings_dense_pm1. */
+int sbg_gen_couplings_dense_pm1_rows(sbg_ctx* ctx, int64_t n_global, int32_t world, int32_t rank, uint64_t seed);
+/* Copies rows [row_begin, row_begin + rows) of the context's int8 couplings back
+ * (row-major, n columns; for a shard, local rows of its rows_valid x n_global). */
+int sbg_get_couplings_i8(sbg_ctx* ctx, int64_t row_begin, int64_t rows, int8_t* J);
 /* CUDA IPC export/open of (G0, G1, done) for peers in other processes (192 bytes). */
 int sbg_shard_ipc_export(sbg_ctx* ctx, void* out192);
 int sbg_shard_ipc_open(sbg_ctx* ctx, const void* in192, void** g0, void** g1, void** done);

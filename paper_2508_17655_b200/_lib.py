@@ -29,6 +29,7 @@ EXPORTS = [
     "sbg_set_couplings_rows_i8", "sbg_shard_info", "sbg_shard_buffers", "sbg_shard_set_peers", "sbg_shard_prepare",
     "sbg_shard_push_slab", "sbg_shard_ipc_export", "sbg_shard_ipc_open", "sbg_readout_partial",
     "sbg_gen_couplings_hash_pm1", "sbg_set_replica_a", "sbg_init_state_seeds",
+    "sbg_gen_couplings_dense_pm1_rows", "sbg_get_couplings_i8",
 ]
 
 
@@ -110,6 +111,8 @@ def lib() -> C.CDLL:
     L.sbg_shard_ipc_open.argtypes = [P, P, P, P, P]
     L.sbg_readout_partial.argtypes = [P, P]
     L.sbg_gen_couplings_hash_pm1.argtypes = [P, i64, i32, i32, u64]
+    L.sbg_gen_couplings_dense_pm1_rows.argtypes = [P, i64, i32, i32, u64]
+    L.sbg_get_couplings_i8.argtypes = [P, i64, i64, P]
     L.sbg_set_replica_a.argtypes = [P, i64, P]
     L.sbg_init_state_seeds.argtypes = [P, i64, i32, P]
     _lib = L

@@ -20,6 +20,7 @@
 #include "../../include/sbgpu.h"
 #include "aux_kernels.cuh"
 #include "csr_step.cuh"
+#include "gen_dense.cuh"
 #include "step_i8.cuh"
 #include "step_tma.cuh"
 #include "step_pair.cuh"
@@ -417,6 +418,90 @@ int validate_params(sbg_ctx* ctx, const sbg_params* p) {
   return SBG_OK;
 }
 
+
+// ------------------------------------------------------------- device generators
+
+enum { GEN_HASH = 0, GEN_EXACT = 1 };
+
+// xoshiro jump matrices T^(2^k) (gen_dense.cuh), computed once per process.
+const std::vector<uint64_t>& jump_matrices() {
+  static const std::vector<uint64_t> m = gen_jump_matrices(GEN_MAXK);
+  return m;
+}
+
+// Allocates this context's dense int8 rows (all rows when world == 1, else the
+// row-shard layout of sbg_set_couplings_rows_i8) and fills them on the device:
+// GEN_EXACT = gen_random_dense's draw order (gen_dense.cuh), GEN_HASH = the
+// counter-based i.i.d. +-1 instance.
+int gen_rows_common(sbg_ctx* ctx, int64_t n_global, int32_t world, int32_t rank, uint64_t seed, int which) {
+  if (n_global < 2 || world < 1 || world > 8 || rank < 0 || rank >= world)
+    return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "bad arguments");
+  const int64_t total = n_global * (n_global - 1) / 2;
+  if (which == GEN_EXACT && (total >> GEN_MAXK) != 0) return ctx->fail(SBG_ERR_UNSUPPORTED, "n too large");
+  CK(cudaSetDevice(ctx->device));
+  cudaStreamSynchronize(ctx->stream);
+  free_state(ctx);
+  cudaFree(ctx->dJ);
+  ctx->dJ = nullptr;
+  const bool shard = world > 1;
+  const int64_t kpad = shard ? round_up(n_global, int64_t(128) * world) : round_up(n_global, PAD_N);
+  const int64_t rows = shard ? kpad / world : kpad;
+  const int64_t row0 = shard ? int64_t(rank) * rows : 0;
+  const int64_t valid = std::max<int64_t>(0, std::min<int64_t>(rows, n_global - row0));
+  if (valid == 0) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "rank owns no spins");
+  CK(cudaMalloc(&ctx->dJ, size_t(rows) * kpad));
+  if (which == GEN_HASH) {
+    const uint64_t work = uint64_t(rows) * kpad / 16;
+    gen_hash_pm1_kernel<<<int(std::min<uint64_t>((work + 255) / 256, uint64_t(ctx->sms) * 32)), 256, 0,
+                          ctx->stream>>>(ctx->dJ, n_global, row0, rows, kpad, seed);
+    CK(cudaGetLastError());
+    ++ctx->launches;
+  } else {
+    int seg = GEN_SEG;
+    if (const char* e = getenv("SBG_GEN_SEG")) seg = std::max(8, atoi(e) / 8 * 8);  // dev knob (tests)
+    int kmax = 1;
+    while (kmax < GEN_MAXK && (uint64_t(total) >> kmax) != 0) ++kmax;
+    const auto& mats = jump_matrices();
+    ulonglong4* dmat = nullptr;
+    CK(cudaMalloc(&dmat, sizeof(uint64_t) * 1024 * kmax));
+    CK(cudaMemcpyAsync(dmat, mats.data(), sizeof(uint64_t) * 1024 * kmax, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemsetAsync(ctx->dJ, 0, size_t(rows) * kpad, ctx->stream));
+    const int64_t r1 = row0 + valid;
+    const int64_t up_threads = valid * ((n_global + seg - 1) / seg);
+    gen_dense_upper_kernel<<<unsigned((up_threads + 127) / 128), 128, 0, ctx->stream>>>(
+        ctx->dJ, kpad, n_global, row0, r1, dmat, kmax, seed, seg);
+    CK(cudaGetLastError());
+    ++ctx->launches;
+    if (!shard) {
+      mirror_lower_kernel<<<dim3(unsigned(kpad / 64), unsigned(kpad / 64)), 256, 0, ctx->stream>>>(ctx->dJ, kpad,
+                                                                                                  n_global);
+    } else {
+      const int64_t st_threads = r1 * ((valid + seg - 1) / seg);
+      gen_dense_strip_kernel<<<unsigned((st_threads + 127) / 128), 128, 0, ctx->stream>>>(
+          ctx->dJ, kpad, n_global, row0, r1, dmat, kmax, seed, seg);
+    }
+    CK(cudaGetLastError());
+    ++ctx->launches;
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(dmat);
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->kind = KIND_DENSE_I8;
+  ctx->energy_scale = 1.0;
+  ctx->sharded = shard;
+  ctx->n = shard ? valid : n_global;
+  ctx->npad = rows;
+  ctx->n_global = n_global;
+  ctx->kpad = kpad;
+  ctx->row0 = row0;
+  ctx->num_m_total = kpad / 128;
+  ctx->done_base = 0;
+  ctx->peer_g0.clear();
+  ctx->peer_g1.clear();
+  ctx->peer_done.clear();
+  return encode_2d_u8(ctx, &ctx->tmJ, ctx->dJ, kpad, rows, 128, 128);
+}
+
 }  // namespace
 
 extern "C" {
@@ -578,16 +663,7 @@ int sbg_coupling_scale_exp(const sbg_ctx* ctx) { return ctx && ctx->kind == KIND
 int sbg_gen_couplings_dense_pm1(sbg_ctx* ctx, int64_t n, uint64_t seed) {
   CHECK_CTX(ctx);
   if (n < 2) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "random dense instance needs n >= 2");
-  // gen_random_dense (model.cpp:144-159): upper triangle row-major, top bit of next().
-  std::vector<int8_t> J(size_t(n) * n, 0);
-  Xoshiro g(seed);
-  for (int64_t i = 0; i < n; ++i)
-    for (int64_t j = i + 1; j < n; ++j) {
-      const int8_t v = (g.next() >> 63) ? int8_t(-1) : int8_t(1);
-      J[size_t(i) * n + j] = v;
-      J[size_t(j) * n + i] = v;
-    }
-  return sbg_set_couplings_dense_i8(ctx, n, J.data());
+  return gen_rows_common(ctx, n, 1, 0, seed, GEN_EXACT);
 }
 
 int sbg_set_couplings_csr_i8(sbg_ctx* ctx, int64_t n, int64_t nnz, const int32_t* rowptr,
@@ -1086,40 +1162,26 @@ int sbg_run_seeded(sbg_ctx* ctx, const sbg_params* prm, int64_t R, int32_t init_
 
 int sbg_gen_couplings_hash_pm1(sbg_ctx* ctx, int64_t n_global, int32_t world, int32_t rank, uint64_t seed) {
   CHECK_CTX(ctx);
-  if (n_global < 2 || world < 1 || world > 8 || rank < 0 || rank >= world)
-    return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "bad arguments");
+  return gen_rows_common(ctx, n_global, world, rank, seed, GEN_HASH);
+}
+
+int sbg_gen_couplings_dense_pm1_rows(sbg_ctx* ctx, int64_t n_global, int32_t world, int32_t rank, uint64_t seed) {
+  CHECK_CTX(ctx);
+  return gen_rows_common(ctx, n_global, world, rank, seed, GEN_EXACT);
+}
+
+int sbg_get_couplings_i8(sbg_ctx* ctx, int64_t row_begin, int64_t rows, int8_t* J) {
+  CHECK_CTX(ctx);
+  if (ctx->kind != KIND_DENSE_I8) return ctx->fail(SBG_ERR_STATE, "int8 dense couplings not set");
+  if (!J || row_begin < 0 || rows < 0 || row_begin + rows > ctx->n)
+    return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "bad row range");
+  if (rows == 0) return SBG_OK;
   CK(cudaSetDevice(ctx->device));
-  cudaStreamSynchronize(ctx->stream);
-  free_state(ctx);
-  cudaFree(ctx->dJ);
-  ctx->dJ = nullptr;
-  const bool shard = world > 1;
-  const int64_t kpad = shard ? round_up(n_global, int64_t(128) * world) : round_up(n_global, PAD_N);
-  const int64_t rows = shard ? kpad / world : kpad;
-  const int64_t row0 = shard ? int64_t(rank) * rows : 0;
-  const int64_t valid = std::max<int64_t>(0, std::min<int64_t>(rows, n_global - row0));
-  if (valid == 0) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "rank owns no spins");
-  CK(cudaMalloc(&ctx->dJ, size_t(rows) * kpad));
-  const uint64_t work = uint64_t(rows) * kpad / 16;
-  gen_hash_pm1_kernel<<<int(std::min<uint64_t>((work + 255) / 256, uint64_t(ctx->sms) * 32)), 256, 0,
-                        ctx->stream>>>(ctx->dJ, n_global, row0, rows, kpad, seed);
-  CK(cudaGetLastError());
-  ++ctx->launches;
+  const int64_t cols = ctx->sharded ? ctx->n_global : ctx->n;
+  const int64_t ld = ctx->sharded ? ctx->kpad : ctx->npad;
+  CK(cudaMemcpy2DAsync(J, cols, ctx->dJ + row_begin * ld, ld, cols, rows, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  ctx->kind = KIND_DENSE_I8;
-  ctx->energy_scale = 1.0;
-  ctx->sharded = shard;
-  ctx->n = shard ? valid : n_global;
-  ctx->npad = rows;
-  ctx->n_global = n_global;
-  ctx->kpad = kpad;
-  ctx->row0 = row0;
-  ctx->num_m_total = kpad / 128;
-  ctx->done_base = 0;
-  ctx->peer_g0.clear();
-  ctx->peer_g1.clear();
-  ctx->peer_done.clear();
-  return encode_2d_u8(ctx, &ctx->tmJ, ctx->dJ, kpad, rows, 128, 128);
+  return SBG_OK;
 }
 
 int sbg_set_couplings_rows_i8(sbg_ctx* ctx, int64_t n_global, int32_t world, int32_t rank, const int8_t* Jrows) {

@@ -160,7 +160,7 @@ class Solver:
             raise _lib.SbgError(rc, f"sbg_create(device={device}) failed: {self._L.sbg_strerror(rc).decode()}")
         self._h = h
         self.device = device
-        self.n = 0
+        self.n = self.n_global = 0
         self.total_weight: Optional[int] = None
 
     def close(self) -> None:
@@ -204,7 +204,7 @@ class Solver:
         else:
             J = np.ascontiguousarray(J, np.float64)
             self._check(self._L.sbg_set_couplings_dense_f64(self._h, n, ptr(J)))
-        self.n = n
+        self.n = self.n_global = n
         if not np.all(np.equal(np.mod(J, 1), 0)):
             self.total_weight = graph_total_weight  # real couplings: no implied MAX-CUT graph
             return
@@ -266,18 +266,31 @@ class Solver:
         self._check(self._L.sbg_readout_partial(self._h, ptr(e2)))
         return e2
 
-    def gen_random_dense(self, n: int, seed: int) -> None:
-        """gen_random_dense (model.cpp:144-159) straight into the device instance."""
-        self._check(self._L.sbg_gen_couplings_dense_pm1(self._h, n, seed))
-        self.n = n
+    def gen_random_dense(self, n: int, seed: int, world: int = 1, rank: int = 0) -> None:
+        """gen_random_dense (model.cpp:144-159) generated on the device in the reference's
+        exact draw order; world > 1 keeps only this rank's rows (row sharding)."""
+        if world == 1:
+            self._check(self._L.sbg_gen_couplings_dense_pm1(self._h, n, seed))
+            self.n = n
+        else:
+            self._check(self._L.sbg_gen_couplings_dense_pm1_rows(self._h, n, world, rank, seed))
+            self.n = self.shard_info()["rows_valid"]
+        self.n_global = n
         self.total_weight = None
+
+    def get_couplings(self, row_begin: int = 0, rows: Optional[int] = None) -> np.ndarray:
+        """Rows of the device int8 couplings (all n columns; local rows for a shard)."""
+        rows = self.n - row_begin if rows is None else rows
+        out = np.empty((rows, self.n_global), np.int8)
+        self._check(self._L.sbg_get_couplings_i8(self._h, row_begin, rows, ptr(out)))
+        return out
 
     def set_instance_csr(self, n: int, rowptr, col, val, total_weight: Optional[int] = None) -> None:
         rowptr = np.ascontiguousarray(rowptr, np.int32)
         col = np.ascontiguousarray(col, np.int32)
         val = np.ascontiguousarray(val, np.int8)
         self._check(self._L.sbg_set_couplings_csr_i8(self._h, n, len(col), ptr(rowptr), ptr(col), ptr(val)))
-        self.n = n
+        self.n = self.n_global = n
         self.total_weight = total_weight if total_weight is not None else int(-val.astype(np.int64).sum() // 2)
 
     # -------------------------------------------------------------- states

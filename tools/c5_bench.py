@@ -1,5 +1,5 @@
-"""C5 on ONE GPU (world = 1): N = 100000 dense +-1 (device-generated counter-based +-1
-instance, 10 GB int8), GdSB, R = 256, M = 5000 schedule; K timed steps in one
+"""C5 on ONE GPU (world = 1): N = 100000 dense +-1 (gen_random_dense(100000, 1) in the
+reference's exact draw order, generated on the device, 10 GB int8), GdSB, R = 256, M = 5000 schedule; K timed steps in one
 persistent launch. Bound: streaming J (N^2 bytes/step) from HBM."""
 import argparse
 import json
@@ -17,7 +17,7 @@ ap.add_argument("--steps", type=int, default=20)
 args = ap.parse_args()
 n, R = args.n, args.R
 with Solver(0) as s:
-    s.gen_hash_pm1(n, 1)
+    s.gen_random_dense(n, 1)
     s.init_state(R, InitMode.small_uniform, 1, 7)
     cfg = SolverConfig(variant=Variant.gdsb, steps=5000, dt=1.25, c=1 / (2 * math.sqrt(n)), a=0.2)
     s.advance(cfg, 0, 2)
