@@ -34,6 +34,7 @@ extern "C" {
 #define SBG_ERR_NCCL 4
 #define SBG_ERR_STATE 5 /* call order: no couplings / no state yet */
 #define SBG_ERR_UNSUPPORTED 6
+#define SBG_ERR_CONVERGENCE 7 /* maps to sbopt::ConvergenceError (spectral.hpp:38-47) */
 
 /* Variant (engine.hpp:26 `enum class Variant { bsb, dsb, gbsb }`, plus GdSB:
  * sign-discretised field with per-spin nonlinear control). */
@@ -206,6 +207,39 @@ int sbg_success_tts(int64_t hits, int64_t n_rep, double t_com_s, double* out4);
 /* auto_tune, Wigner branch (spectral.cpp:298-305, :254-266, :277-286) on dense
  * fp64 J: c = 1/(2 sqrt(n) sigma), dt = d_t * sqrt(2 / (1 - lmin/lmax)) = d_t. */
 int sbg_tune_wigner_f64(int64_t n, const double* J, double d_t, double* c, double* dt);
+
+/* SpectralEstimate + TuningResult (spectral.hpp:17-34). */
+#define SBG_SPECTRAL_POWER_ITERATION 0
+#define SBG_SPECTRAL_WIGNER 1
+#define SBG_SPECTRAL_EXACT_SMALL 2
+#define SBG_TUNE_WIGNER 0
+#define SBG_TUNE_NUMERICAL 1
+typedef struct sbg_spectral {
+  double lambda_max;
+  double lambda_min; /* NaN when lambda_max did not converge */
+  double c;          /* sbg_auto_tune only: 1 / lambda_max */
+  double dt;         /* sbg_auto_tune only: d_t * sqrt(2 / (1 - lambda_min / lambda_max)) */
+  double d_t_factor;
+  double tolerance;  /* power iteration: tol; 0 for wigner / exact_small */
+  uint64_t iterations;
+  int32_t method;    /* SBG_SPECTRAL_* */
+  int32_t converged; /* 0: auto_tune fell back to the carried estimate (the reference's warning) */
+} sbg_spectral;
+
+/* extreme_eigenvalues (spectral.cpp:207-246) of the context's couplings on the
+ * device (dense int8, CSR int8, or the fixed-point real-J image): n == 2 closed
+ * form, n <= 32 cyclic Jacobi, else Gershgorin-shifted power iteration on each
+ * end -- bitwise the reference's estimates for integer couplings. max_iters == 0
+ * means 10 n. Non-convergence returns SBG_ERR_CONVERGENCE with the carried
+ * estimate in *out (lambda_min NaN if lambda_max failed). v_max / v_min: optional
+ * n doubles each (the unit eigenvector estimates). */
+int sbg_extreme_eigenvalues(sbg_ctx* ctx, double tol, uint64_t max_iters, sbg_spectral* out, double* v_max,
+                            double* v_min);
+/* auto_tune (spectral.cpp:294-326) on the context's couplings: mode
+ * SBG_TUNE_WIGNER (sigma from the device couplings) or SBG_TUNE_NUMERICAL
+ * (sbg_extreme_eigenvalues, keeping a finite carried estimate on non-convergence
+ * with converged = 0, as the reference does after its warning). */
+int sbg_auto_tune(sbg_ctx* ctx, int32_t mode, double d_t_factor, double tol, uint64_t max_iters, sbg_spectral* out);
 
 #ifdef __cplusplus
 }

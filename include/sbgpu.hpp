@@ -45,12 +45,41 @@ struct SolverConfig {  // engine.hpp:29-38
   InitMode init_mode = InitMode::uniform_random;
 };
 
-struct TuningResult {  // spectral.hpp:28-33 (source estimate reduced to the two edges)
+enum class SpectralMethod {  // spectral.hpp:17
+  power_iteration = SBG_SPECTRAL_POWER_ITERATION,
+  wigner = SBG_SPECTRAL_WIGNER,
+  exact_small = SBG_SPECTRAL_EXACT_SMALL
+};
+enum class TuneMode { wigner = SBG_TUNE_WIGNER, numerical = SBG_TUNE_NUMERICAL };  // spectral.hpp:64
+
+struct SpectralEstimate {  // spectral.hpp:19-27
+  double lambda_max = 0.0;
+  double lambda_min = 0.0;
+  SpectralMethod method = SpectralMethod::power_iteration;
+  double tolerance = 0.0;
+  std::vector<double> v_max;  // empty for wigner
+  std::vector<double> v_min;
+  std::size_t iterations = 0;
+};
+
+// spectral.hpp:38-47: estimation missed the residual target; best estimate attached.
+class ConvergenceError : public std::runtime_error {
+ public:
+  ConvergenceError(const std::string& message, SpectralEstimate last)
+      : std::runtime_error(message), last_(std::move(last)) {}
+  const SpectralEstimate& last_estimate() const noexcept { return last_; }
+
+ private:
+  SpectralEstimate last_;
+};
+
+struct TuningResult {  // spectral.hpp:28-33 (lambda_max/lambda_min mirror source's edges)
   double c = 0.0;
   double dt = 0.0;
   double d_t_factor = 0.0;
   double lambda_max = 0.0;
   double lambda_min = 0.0;
+  SpectralEstimate source;
 };
 
 struct RunResult {  // engine.hpp:56-64
@@ -186,6 +215,34 @@ class Solver {
     total_weight_.reset();
   }
 
+  // extreme_eigenvalues (spectral.cpp:207-246) of the device couplings.
+  SpectralEstimate extreme_eigenvalues(double tol = 1e-6, std::size_t max_iters = 0) {
+    sbg_spectral st{};
+    SpectralEstimate e;
+    e.v_max.resize(n_);
+    e.v_min.resize(n_);
+    const int rc = sbg_extreme_eigenvalues(ctx_, tol, max_iters, &st, e.v_max.data(), e.v_min.data());
+    fill(st, e);
+    if (rc == SBG_ERR_CONVERGENCE) throw ConvergenceError(sbg_last_error(ctx_), e);
+    check(rc);
+    return e;
+  }
+  // auto_tune (spectral.cpp:294-326) of the device couplings.
+  TuningResult auto_tune(TuneMode mode, double d_t_factor = 1.25, double tol = 1e-6, std::size_t max_iters = 0) {
+    sbg_spectral st{};
+    const int rc = sbg_auto_tune(ctx_, static_cast<std::int32_t>(mode), d_t_factor, tol, max_iters, &st);
+    TuningResult t;
+    fill(st, t.source);
+    if (rc == SBG_ERR_CONVERGENCE) throw ConvergenceError(sbg_last_error(ctx_), t.source);
+    check(rc);
+    t.c = st.c;
+    t.dt = st.dt;
+    t.d_t_factor = st.d_t_factor;
+    t.lambda_max = st.lambda_max;
+    t.lambda_min = st.lambda_min;
+    return t;
+  }
+
   // R runs of run() (engine.cpp:112-139) in one device pass; replica r is seeded
   // derive_seed(master_seed, {tag, r}) with cfg.init_mode. Returns one RunResult per
   // replica (final spins, energy, cut when a total weight is known).
@@ -239,6 +296,17 @@ class Solver {
     return p;
   }
   void check(int rc) const { detail::check(rc, sbg_last_error(ctx_)); }
+  static void fill(const sbg_spectral& st, SpectralEstimate& e) {
+    e.lambda_max = st.lambda_max;
+    e.lambda_min = st.lambda_min;
+    e.method = static_cast<SpectralMethod>(st.method);
+    e.tolerance = st.tolerance;
+    e.iterations = static_cast<std::size_t>(st.iterations);
+    if (e.method == SpectralMethod::wigner) {
+      e.v_max.clear();
+      e.v_min.clear();
+    }
+  }
 
   sbg_ctx* ctx_ = nullptr;
   std::size_t n_ = 0;

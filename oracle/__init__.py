@@ -77,6 +77,8 @@ class _Ref:
         L.ref_coupling_matvec.argtypes = [_i64, _P, _P, _P]
         L.ref_ising_energy.argtypes = [_i64, _P, _P, _P]
         L.ref_auto_tune_wigner.argtypes = [_i64, _P, _f64, _P, _P]
+        L.ref_extreme_eigenvalues.argtypes = [_i64, _P, _f64, _u64, _P, _P, _P]
+        L.ref_auto_tune.argtypes = [_i64, _P, C.c_int, _f64, _f64, _u64, _P]
         L.ref_run.argtypes = [C.c_int, _i64, _P, _u64, _f64, _f64, _f64, _u64, _P, _P, _P]
         L.ref_batch_best_of.argtypes = [C.c_int, _i64, _P, _u64, _f64, _f64, _f64, _i64, _u64,
                                         C.c_uint, _P, _P, _P]
@@ -182,6 +184,33 @@ class _Ref:
         self._check(self.lib.ref_chaos_scan(J.shape[0], _ptr(J), _ptr(a), len(a), reps, steps, dt, c, seed,
                                             workers, _ptr(out)))
         return out
+
+    def extreme_eigenvalues(self, J, tol: float = 1e-6, max_iters: int = 0):
+        """-> (rc, dict(lambda_max, lambda_min, iterations, method, tolerance, converged), v_max, v_min);
+        rc 0 ok, 7 ConvergenceError (carried estimate), 1 invalid argument (ValueError raised)."""
+        J = np.ascontiguousarray(J, np.float64)
+        n = J.shape[0]
+        out = np.zeros(6)
+        vmax, vmin = np.full(n, np.nan), np.full(n, np.nan)
+        rc = self.lib.ref_extreme_eigenvalues(n, _ptr(J), tol, max_iters, _ptr(out), _ptr(vmax), _ptr(vmin))
+        if rc == 1:
+            raise ValueError(self.lib.ref_last_error().decode())
+        keys = ["lambda_max", "lambda_min", "iterations", "method", "tolerance", "converged"]
+        d = dict(zip(keys, out.tolist()))
+        d["iterations"], d["method"] = int(d["iterations"]), int(d["method"])
+        return rc, d, vmax, vmin
+
+    def auto_tune(self, J, numerical: bool, d_t: float = 1.25, tol: float = 1e-6, max_iters: int = 0):
+        """-> (rc, (c, dt, lambda_max, lambda_min)); rc 7 = ConvergenceError propagated."""
+        J = np.ascontiguousarray(J, np.float64)
+        out = np.zeros(4)
+        rc = self.lib.ref_auto_tune(J.shape[0], _ptr(J), int(numerical), d_t, tol, max_iters, _ptr(out))
+        if rc == 1:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return rc, tuple(out.tolist())
+
+    def last_error(self) -> str:
+        return self.lib.ref_last_error().decode()
 
     def effective_workers(self, requested: int = 0) -> int:
         return int(self.lib.ref_effective_workers(requested))

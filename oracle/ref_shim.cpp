@@ -263,6 +263,52 @@ int ref_replica_fanout(int variant, std::int64_t n, const double* J, std::int64_
 
 unsigned ref_effective_workers(unsigned requested) { return effective_workers(requested); }
 
+// extreme_eigenvalues (spectral.cpp:207-246). out6 = {lambda_max, lambda_min,
+// iterations, method, tolerance, converged}; v_max / v_min n doubles (or null).
+// Returns 0, 1 (invalid argument) or 7 (ConvergenceError, carried estimate in out6).
+int ref_extreme_eigenvalues(std::int64_t n, const double* J, double tol, std::uint64_t max_iters, double* out6,
+                            double* v_max, double* v_min) {
+  auto fill = [&](const SpectralEstimate& e, bool conv) {
+    out6[0] = e.lambda_max;
+    out6[1] = e.lambda_min;
+    out6[2] = static_cast<double>(e.iterations);
+    out6[3] = static_cast<double>(static_cast<int>(e.method));
+    out6[4] = e.tolerance;
+    out6[5] = conv ? 1.0 : 0.0;
+    if (v_max && e.v_max.size() == static_cast<std::size_t>(n)) std::memcpy(v_max, e.v_max.data(), sizeof(double) * n);
+    if (v_min && e.v_min.size() == static_cast<std::size_t>(n)) std::memcpy(v_min, e.v_min.data(), sizeof(double) * n);
+  };
+  try {
+    fill(extreme_eigenvalues(make_instance(n, J), tol, static_cast<std::size_t>(max_iters)), true);
+    return 0;
+  } catch (const ConvergenceError& e) {
+    g_err = e.what();
+    fill(e.last_estimate(), false);
+    return 7;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// auto_tune (spectral.cpp:294-326): out4 = {c, dt, lambda_max, lambda_min}.
+int ref_auto_tune(std::int64_t n, const double* J, int numerical, double d_t, double tol, std::uint64_t max_iters,
+                  double* out4) {
+  try {
+    const auto t = auto_tune(make_instance(n, J), numerical ? TuneMode::numerical : TuneMode::wigner, d_t, tol,
+                             static_cast<std::size_t>(max_iters));
+    out4[0] = t.c;
+    out4[1] = t.dt;
+    out4[2] = t.source.lambda_max;
+    out4[3] = t.source.lambda_min;
+    return 0;
+  } catch (const ConvergenceError& e) {
+    g_err = e.what();
+    return 7;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // chaos_scan (chaos.cpp:65-102): final deltas, row-major [a][rep].
 int ref_chaos_scan(std::int64_t n, const double* J, const double* a_values, std::int64_t na, std::int64_t reps,
                    std::uint64_t steps, double dt, double c, std::uint64_t seed, unsigned workers,

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libsbgpu.so")
 
 SBG_OK, SBG_ERR_INVALID_ARGUMENT, SBG_ERR_OUT_OF_MEMORY, SBG_ERR_CUDA, SBG_ERR_NCCL, SBG_ERR_STATE, \
-    SBG_ERR_UNSUPPORTED = range(7)
+    SBG_ERR_UNSUPPORTED, SBG_ERR_CONVERGENCE = range(8)
 BSB, DSB, GBSB, GDSB = 0, 1, 2, 3
 INIT_UNIFORM_RANDOM, INIT_CHAOS_PROBE, INIT_SMALL_UNIFORM = 0, 1, 2
 
@@ -29,7 +29,7 @@ EXPORTS = [
     "sbg_set_couplings_rows_i8", "sbg_shard_info", "sbg_shard_buffers", "sbg_shard_set_peers", "sbg_shard_prepare",
     "sbg_shard_push_slab", "sbg_shard_ipc_export", "sbg_shard_ipc_open", "sbg_readout_partial",
     "sbg_gen_couplings_hash_pm1", "sbg_set_replica_a", "sbg_init_state_seeds",
-    "sbg_gen_couplings_dense_pm1_rows", "sbg_get_couplings_i8",
+    "sbg_gen_couplings_dense_pm1_rows", "sbg_get_couplings_i8", "sbg_extreme_eigenvalues", "sbg_auto_tune",
 ]
 
 
@@ -46,6 +46,12 @@ class SbgInvalidArgument(SbgError, ValueError):
 class Params(C.Structure):
     _fields_ = [("variant", C.c_int32), ("reserved", C.c_int32), ("steps", C.c_uint64), ("dt", C.c_double),
                 ("c", C.c_double), ("a", C.c_double)]
+
+
+class Spectral(C.Structure):  # sbg_spectral
+    _fields_ = [("lambda_max", C.c_double), ("lambda_min", C.c_double), ("c", C.c_double), ("dt", C.c_double),
+                ("d_t_factor", C.c_double), ("tolerance", C.c_double), ("iterations", C.c_uint64),
+                ("method", C.c_int32), ("converged", C.c_int32)]
 
 
 class Timing(C.Structure):
@@ -113,6 +119,8 @@ def lib() -> C.CDLL:
     L.sbg_gen_couplings_hash_pm1.argtypes = [P, i64, i32, i32, u64]
     L.sbg_gen_couplings_dense_pm1_rows.argtypes = [P, i64, i32, i32, u64]
     L.sbg_get_couplings_i8.argtypes = [P, i64, i64, P]
+    L.sbg_extreme_eigenvalues.argtypes = [P, C.c_double, u64, C.POINTER(Spectral), P, P]
+    L.sbg_auto_tune.argtypes = [P, i32, C.c_double, C.c_double, u64, C.POINTER(Spectral)]
     L.sbg_set_replica_a.argtypes = [P, i64, P]
     L.sbg_init_state_seeds.argtypes = [P, i64, i32, P]
     _lib = L

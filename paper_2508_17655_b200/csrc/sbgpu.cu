@@ -21,6 +21,7 @@
 #include "aux_kernels.cuh"
 #include "csr_step.cuh"
 #include "gen_dense.cuh"
+#include "spectral.cuh"
 #include "step_i8.cuh"
 #include "step_tma.cuh"
 #include "step_pair.cuh"
@@ -502,6 +503,104 @@ int gen_rows_common(sbg_ctx* ctx, int64_t n_global, int32_t world, int32_t rank,
   return encode_2d_u8(ctx, &ctx->tmJ, ctx->dJ, kpad, rows, 128, 128);
 }
 
+
+// ------------------------------------------------------------------ spectral (auto_tune)
+
+int make_jview(sbg_ctx* ctx, JView* v) {
+  if (ctx->kind == KIND_NONE) return ctx->fail(SBG_ERR_STATE, "couplings not set");
+  if (ctx->sharded) return ctx->fail(SBG_ERR_UNSUPPORTED, "spectral estimation of a row shard");
+  *v = JView{};
+  v->n = ctx->n;
+  if (ctx->kind == KIND_CSR_I8) {
+    v->kind = JV_CSR_I8;
+    v->rowptr = ctx->d_rowptr;
+    v->col = ctx->d_col;
+    v->val = ctx->d_val;
+  } else {
+    v->kind = ctx->kind == KIND_DENSE_I8 ? JV_DENSE_I8 : JV_DENSE_FX;
+    v->J = ctx->dJ;
+    v->ld = ctx->npad;
+    v->plane = ctx->npad * ctx->npad;
+    v->scale = std::ldexp(1.0, -ctx->fx_shift);
+  }
+  return SBG_OK;
+}
+
+// Row sums of J^2 (off-diagonal) and |J| on the device; sum_sq summed on the host in
+// row order, beta = max row sum (exact for integer J in any order).
+int row_stats(sbg_ctx* ctx, const JView& jv, double* sum_sq, double* beta) {
+  double* d = nullptr;
+  CK(cudaMalloc(&d, sizeof(double) * 2 * jv.n));
+  row_stats_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>(jv, d, d + jv.n);
+  ++ctx->launches;
+  std::vector<double> h(size_t(2 * jv.n));
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), d, sizeof(double) * 2 * jv.n, cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return ctx->fail(SBG_ERR_CUDA, "row statistics: %s", cudaGetErrorString(e));
+  double sq = 0.0, b = 0.0;
+  for (int64_t i = 0; i < jv.n; ++i) {
+    sq += h[size_t(i)];
+    b = std::max(b, h[size_t(jv.n + i)]);
+  }
+  *sum_sq = sq;
+  *beta = b;
+  return SBG_OK;
+}
+
+struct PowerOutcome {
+  double lambda = 0.0, residual = 0.0;
+  uint64_t iterations = 0;
+  bool converged = false;
+};
+
+// One end of the spectrum (spectral.cpp:50-118) as one cooperative launch.
+int power_end(sbg_ctx* ctx, const JView& jv, double beta, double sign, double tol, uint64_t max_iters,
+              PowerOutcome* out, double* v_out) {
+  const int64_t n = jv.n;
+  double* buf = nullptr;
+  const size_t nb = size_t(3 * n + 8);
+  CK(cudaMalloc(&buf, sizeof(double) * nb + 64));
+  CK(cudaMemsetAsync(buf, 0, sizeof(double) * nb + 64, ctx->stream));
+  PowerArgs a{};
+  a.J = jv;
+  a.beta = beta;
+  a.sign = sign;
+  a.tol = tol;
+  a.v_init = 1.0 / std::sqrt(static_cast<double>(n));
+  a.max_iters = max_iters;
+  a.v[0] = buf;
+  a.v[1] = buf + n;
+  a.jv = buf + 2 * n;
+  a.result = buf + 3 * n;             // 5 doubles
+  a.bar = reinterpret_cast<unsigned long long*>(buf + 3 * n + 6);
+  a.ctrl = reinterpret_cast<int*>(buf + 3 * n + 7);
+  CK(cudaFuncSetAttribute(power_iteration_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PI_SMEM_BYTES));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, power_iteration_kernel, PI_THREADS, PI_SMEM_BYTES));
+  if (per_sm < 1) {
+    cudaFree(buf);
+    return ctx->fail(SBG_ERR_CUDA, "power iteration kernel cannot be resident");
+  }
+  void* params[] = {&a};
+  cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(power_iteration_kernel), dim3(ctx->sms),
+                                              dim3(PI_THREADS), params, PI_SMEM_BYTES, ctx->stream);
+  ++ctx->launches;
+  double res[5] = {0, 0, 0, 0, 0};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(res, a.result, sizeof res, cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e == cudaSuccess && v_out)
+    e = cudaMemcpy(v_out, a.v[int(res[4])], sizeof(double) * n, cudaMemcpyDeviceToHost);
+  cudaFree(buf);
+  if (e != cudaSuccess) return ctx->fail(SBG_ERR_CUDA, "power iteration: %s", cudaGetErrorString(e));
+  out->lambda = res[0];
+  out->residual = res[1];
+  out->iterations = uint64_t(res[2]);
+  out->converged = res[3] != 0.0;
+  return SBG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -517,6 +616,7 @@ const char* sbg_strerror(int code) {
     case SBG_ERR_NCCL: return "NCCL error";
     case SBG_ERR_STATE: return "invalid call order";
     case SBG_ERR_UNSUPPORTED: return "unsupported";
+    case SBG_ERR_CONVERGENCE: return "eigenvalue estimation did not converge";
   }
   return "unknown";
 }
@@ -1405,6 +1505,105 @@ int sbg_tune_wigner_f64(int64_t n, const double* J, double d_t, double* c, doubl
   const double edge = 2.0 * std::sqrt(double(n)) * sigma;
   *c = 1.0 / edge;
   *dt = d_t * std::sqrt(2.0 / (1.0 - (-edge) / edge));
+  return SBG_OK;
+}
+
+int sbg_extreme_eigenvalues(sbg_ctx* ctx, double tol, uint64_t max_iters, sbg_spectral* out, double* v_max,
+                            double* v_min) {
+  CHECK_CTX(ctx);
+  if (!out) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "null output");
+  *out = sbg_spectral{};
+  JView jv;
+  int rc = make_jview(ctx, &jv);
+  if (rc) return rc;
+  const int64_t n = jv.n;
+  // extreme_eigenvalues argument checks, in order (spectral.cpp:209-213)
+  if (n < 2) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "extreme_eigenvalues needs n >= 2");
+  if (!(tol > 0.0)) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "tolerance must be positive");
+  CK(cudaSetDevice(ctx->device));
+  double sum_sq = 0.0, beta = 0.0;
+  if ((rc = row_stats(ctx, jv, &sum_sq, &beta))) return rc;
+  if (beta == 0.0) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "degenerate instance: all couplings zero");
+  if (max_iters == 0) max_iters = 10 * uint64_t(n);
+  if (n <= 32) {  // closed form / Jacobi (spectral.cpp:215-216)
+    double* d = nullptr;
+    CK(cudaMalloc(&d, sizeof(double) * (2 + 2 * n)));
+    spectral_small_kernel<<<1, 32, 0, ctx->stream>>>(jv, d);
+    ++ctx->launches;
+    std::vector<double> h(size_t(2 + 2 * n));
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), d, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(d);
+    if (e != cudaSuccess) return ctx->fail(SBG_ERR_CUDA, "small spectrum: %s", cudaGetErrorString(e));
+    out->lambda_max = h[0];
+    out->lambda_min = h[1];
+    out->method = SBG_SPECTRAL_EXACT_SMALL;
+    out->converged = 1;
+    if (v_max) std::memcpy(v_max, &h[2], sizeof(double) * n);
+    if (v_min) std::memcpy(v_min, &h[2 + n], sizeof(double) * n);
+    return SBG_OK;
+  }
+  out->method = SBG_SPECTRAL_POWER_ITERATION;
+  out->tolerance = tol;
+  PowerOutcome hi, lo;
+  if ((rc = power_end(ctx, jv, beta, +1.0, tol, max_iters, &hi, v_max))) return rc;
+  out->lambda_max = hi.lambda;
+  out->iterations = hi.iterations;
+  if (!hi.converged) {
+    out->lambda_min = std::nan("");
+    return ctx->fail(SBG_ERR_CONVERGENCE, "lambda_max estimation did not converge in %s iterations (residual %s)",
+                     std::to_string(max_iters).c_str(), std::to_string(hi.residual).c_str());
+  }
+  if ((rc = power_end(ctx, jv, beta, -1.0, tol, max_iters, &lo, v_min))) return rc;
+  out->lambda_min = lo.lambda;
+  out->iterations += lo.iterations;
+  if (!lo.converged)
+    return ctx->fail(SBG_ERR_CONVERGENCE, "lambda_min estimation did not converge in %s iterations (residual %s)",
+                     std::to_string(max_iters).c_str(), std::to_string(lo.residual).c_str());
+  out->converged = 1;
+  return SBG_OK;
+}
+
+int sbg_auto_tune(sbg_ctx* ctx, int32_t mode, double d_t_factor, double tol, uint64_t max_iters, sbg_spectral* out) {
+  CHECK_CTX(ctx);
+  if (!out) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "null output");
+  int rc;
+  if (mode == SBG_TUNE_WIGNER) {  // spectral.cpp:298-305
+    *out = sbg_spectral{};
+    JView jv;
+    if ((rc = make_jview(ctx, &jv))) return rc;
+    CK(cudaSetDevice(ctx->device));
+    const int64_t n = jv.n;
+    double sum_sq = 0.0, beta = 0.0;
+    if ((rc = row_stats(ctx, jv, &sum_sq, &beta))) return rc;
+    const double sigma = n < 2 ? 0.0 : std::sqrt(sum_sq / (static_cast<double>(n) * static_cast<double>(n - 1)));
+    if (sigma == 0.0) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "degenerate instance: all couplings zero");
+    const double edge = 2.0 * std::sqrt(static_cast<double>(n)) * sigma;
+    out->method = SBG_SPECTRAL_WIGNER;
+    out->lambda_max = edge;
+    out->lambda_min = -edge;
+    out->converged = 1;
+  } else if (mode == SBG_TUNE_NUMERICAL) {  // :306-320
+    rc = sbg_extreme_eigenvalues(ctx, tol, max_iters, out, nullptr, nullptr);
+    if (rc == SBG_ERR_CONVERGENCE) {
+      if (!std::isfinite(out->lambda_max) || !std::isfinite(out->lambda_min) || !(out->lambda_max > 0.0) ||
+          !(out->lambda_min < 0.0))
+        return rc;
+      out->converged = 0;  // tuned from the carried estimate (the reference warns on stderr)
+    } else if (rc) {
+      return rc;
+    }
+  } else {
+    return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "unknown tune mode");
+  }
+  // tune_dt (spectral.cpp:277-286)
+  if (!(out->lambda_max > 0.0)) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "lambda_max must be positive");
+  if (!(out->lambda_min < 0.0)) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "lambda_min must be negative");
+  if (!(d_t_factor > 0.0)) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "d_t_factor must be positive");
+  out->d_t_factor = d_t_factor;
+  out->c = 1.0 / out->lambda_max;
+  out->dt = d_t_factor * std::sqrt(2.0 / (1.0 - out->lambda_min / out->lambda_max));
   return SBG_OK;
 }
 

@@ -49,6 +49,29 @@ class SolverConfig:  # engine.hpp:29-38
 
 
 @dataclasses.dataclass
+class SpectralEstimate:  # spectral.hpp:19-27
+    lambda_max: float = 0.0
+    lambda_min: float = 0.0
+    method: str = "power_iteration"  # power_iteration | wigner | exact_small (SpectralMethod)
+    tolerance: float = 0.0
+    v_max: Optional[np.ndarray] = None
+    v_min: Optional[np.ndarray] = None
+    iterations: int = 0
+
+
+class ConvergenceError(RuntimeError):
+    """spectral.hpp:38-47: iterative estimation missed the residual target; the
+    carried estimate is attached."""
+
+    def __init__(self, message: str, last_estimate: SpectralEstimate):
+        super().__init__(message)
+        self.last_estimate = last_estimate
+
+
+_SPECTRAL_METHODS = {0: "power_iteration", 1: "wigner", 2: "exact_small"}
+
+
+@dataclasses.dataclass
 class TuningResult:  # spectral.hpp:28-33
     c: float = 0.0
     dt: float = 0.0
@@ -56,6 +79,8 @@ class TuningResult:  # spectral.hpp:28-33
     lambda_max: float = float("nan")
     lambda_min: float = float("nan")
     method: str = "wigner"
+    source: Optional[SpectralEstimate] = None
+    converged: bool = True  # False: tuned from a carried estimate (the reference's stderr warning)
 
 
 @dataclasses.dataclass
@@ -211,6 +236,37 @@ class Solver:
         # cut via the bridge (model.hpp:103-104): J = -w  =>  W = -sum_{i<j} J_ij
         self.total_weight = graph_total_weight if graph_total_weight is not None else int(
             -np.triu(J.astype(np.int64), 1).sum())
+
+    # ------------------------------------------------------- spectrum / tuning
+
+    def extreme_eigenvalues(self, tol: float = 1e-6, max_iters: int = 0, want_vectors: bool = False):
+        """extreme_eigenvalues (spectral.cpp:207-246) on the device couplings. Raises
+        ConvergenceError (estimate attached) like the reference."""
+        st = _lib.Spectral()
+        vmax = np.full(self.n, np.nan) if want_vectors else None
+        vmin = np.full(self.n, np.nan) if want_vectors else None
+        rc = self._L.sbg_extreme_eigenvalues(self._h, tol, max_iters, C.byref(st),
+                                             ptr(vmax) if want_vectors else None, ptr(vmin) if want_vectors else None)
+        est = SpectralEstimate(st.lambda_max, st.lambda_min, _SPECTRAL_METHODS[st.method], st.tolerance,
+                               vmax, vmin, int(st.iterations))
+        if rc == _lib.SBG_ERR_CONVERGENCE:
+            raise ConvergenceError(self._L.sbg_last_error(self._h).decode(), est)
+        self._check(rc)
+        return est
+
+    def auto_tune(self, mode: str = "numerical", d_t_factor: float = 1.25, tol: float = 1e-6,
+                  max_iters: int = 0) -> TuningResult:
+        """auto_tune (spectral.cpp:294-326) on the device couplings; mode "wigner" | "numerical"."""
+        st = _lib.Spectral()
+        m = {"wigner": 0, "numerical": 1}[mode]
+        rc = self._L.sbg_auto_tune(self._h, m, d_t_factor, tol, max_iters, C.byref(st))
+        est = SpectralEstimate(st.lambda_max, st.lambda_min, _SPECTRAL_METHODS[st.method], st.tolerance,
+                               None, None, int(st.iterations))
+        if rc == _lib.SBG_ERR_CONVERGENCE:
+            raise ConvergenceError(self._L.sbg_last_error(self._h).decode(), est)
+        self._check(rc)
+        return TuningResult(c=st.c, dt=st.dt, d_t_factor=st.d_t_factor, lambda_max=st.lambda_max,
+                            lambda_min=st.lambda_min, method=est.method, source=est, converged=bool(st.converged))
 
     # ------------------------------------------------------- row sharding (C5)
     def set_instance_rows(self, J_rows: np.ndarray, n_global: int, world: int, rank: int) -> None:
