@@ -109,6 +109,17 @@ int sbg_gen_couplings_dense_pm1(sbg_ctx* ctx, int64_t n, uint64_t seed);
  * the same IsingInstance. */
 int sbg_set_couplings_csr_i8(sbg_ctx* ctx, int64_t n, int64_t nnz, const int32_t* rowptr,
                              const int32_t* col, const int8_t* val);
+/* MAX-CUT graph ingestion straight to CSR (no dense fp64): CutGraph edges
+ * (model.hpp:72-95; 0-based endpoints, checks of model.cpp:91-103 in input order)
+ * mapped by maxcut_to_ising (model.cpp:134-142, J_ij = J_ji = -w). Weights must lie
+ * in [-127, 127]. *total_weight (optional) receives W, so cut = (W - E) / 2. */
+int sbg_set_couplings_graph(sbg_ctx* ctx, int64_t n, int64_t m, const int64_t* i, const int64_t* j,
+                            const int64_t* w, int64_t* total_weight);
+/* IsingInstance::from_entries (model.cpp:70-86; the JSON instance document's
+ * [i, j, J_ij] triples): integer entries in [-127, 127] go to CSR when sparse
+ * (2m < n^2/16), anything else to the dense paths. */
+int sbg_set_couplings_entries_f64(sbg_ctx* ctx, int64_t n, int64_t m, const int64_t* i, const int64_t* j,
+                                  const double* value);
 int64_t sbg_n(const sbg_ctx* ctx);
 
 /* Replica states. Replace SolverState (engine.hpp:40-47) x R.

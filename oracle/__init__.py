@@ -79,6 +79,11 @@ class _Ref:
         L.ref_auto_tune_wigner.argtypes = [_i64, _P, _f64, _P, _P]
         L.ref_extreme_eigenvalues.argtypes = [_i64, _P, _f64, _u64, _P, _P, _P]
         L.ref_auto_tune.argtypes = [_i64, _P, C.c_int, _f64, _f64, _u64, _P]
+        L.ref_parse_gset.argtypes = [C.c_char_p, _P, _P, _i64, _P, _P, _P]
+        L.ref_cut_value.argtypes = [_i64, _i64, _P, _P, _P, _P, _P]
+        L.ref_instance_from_json.argtypes = [C.c_char_p, _i64, _P, _P]
+        L.ref_instance_to_json.restype = _i64
+        L.ref_instance_to_json.argtypes = [_i64, _P, C.c_char_p, _i64]
         L.ref_run.argtypes = [C.c_int, _i64, _P, _u64, _f64, _f64, _f64, _u64, _P, _P, _P]
         L.ref_batch_best_of.argtypes = [C.c_int, _i64, _P, _u64, _f64, _f64, _f64, _i64, _u64,
                                         C.c_uint, _P, _P, _P]
@@ -208,6 +213,39 @@ class _Ref:
         if rc == 1:
             raise ValueError(self.lib.ref_last_error().decode())
         return rc, tuple(out.tolist())
+
+    def parse_gset(self, text: str):
+        """-> (n, i, j, w) 0-based, or raises ValueError(message) like the reference's ParseError."""
+        n, m = np.zeros(1, np.int64), np.zeros(1, np.int64)
+        cap = max(1, text.count("\n") + 1)
+        ei, ej, w = (np.zeros(cap, np.int64) for _ in range(3))
+        if self.lib.ref_parse_gset(text.encode(), _ptr(n), _ptr(m), cap, _ptr(ei), _ptr(ej), _ptr(w)):
+            raise ValueError(self.lib.ref_last_error().decode())
+        k = int(m[0])
+        return int(n[0]), ei[:k], ej[:k], w[:k]
+
+    def cut_value(self, n, ei, ej, w, spins) -> int:
+        ei, ej, w = (np.ascontiguousarray(a, np.int64) for a in (ei, ej, w))
+        spins = np.ascontiguousarray(spins, np.int8)
+        out = C.c_longlong()
+        self._check(self.lib.ref_cut_value(n, len(ei), _ptr(ei), _ptr(ej), _ptr(w), _ptr(spins), C.byref(out)))
+        return int(out.value)
+
+    def instance_from_json(self, text: str, cap: int = 1 << 22):
+        n = np.zeros(1, np.int64)
+        J = np.zeros(cap)
+        if self.lib.ref_instance_from_json(text.encode(), cap, _ptr(n), _ptr(J)):
+            raise ValueError(self.lib.ref_last_error().decode())
+        k = int(n[0])
+        return J[:k * k].reshape(k, k)
+
+    def instance_to_json(self, J) -> str:
+        J = np.ascontiguousarray(J, np.float64)
+        cap = 64 + 48 * J.size
+        buf = C.create_string_buffer(cap)
+        if self.lib.ref_instance_to_json(J.shape[0], _ptr(J), buf, cap) < 0:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return buf.value.decode()
 
     def last_error(self) -> str:
         return self.lib.ref_last_error().decode()

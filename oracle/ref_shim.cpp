@@ -263,6 +263,77 @@ int ref_replica_fanout(int variant, std::int64_t n, const double* J, std::int64_
 
 unsigned ref_effective_workers(unsigned requested) { return effective_workers(requested); }
 
+// parse_gset (model.cpp:225-282). Returns 0 and fills n, m (and up to cap edges as
+// 0-based i, j, w); 2 on ParseError / invalid_argument with the message in ref_last_error.
+int ref_parse_gset(const char* text, std::int64_t* n, std::int64_t* m, std::int64_t cap, std::int64_t* ei,
+                   std::int64_t* ej, std::int64_t* w) {
+  try {
+    const auto g = parse_gset(std::string_view(text));
+    *n = static_cast<std::int64_t>(g.n());
+    *m = static_cast<std::int64_t>(g.edges().size());
+    std::int64_t k = 0;
+    for (const auto& e : g.edges()) {
+      if (k >= cap) break;
+      ei[k] = static_cast<std::int64_t>(e.i);
+      ej[k] = static_cast<std::int64_t>(e.j);
+      w[k] = e.w;
+      ++k;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+// cut_value (model.cpp:125-132) of a CutGraph for given spins.
+int ref_cut_value(std::int64_t n, std::int64_t m, const std::int64_t* ei, const std::int64_t* ej,
+                  const std::int64_t* w, const std::int8_t* spins, long long* cut) {
+  try {
+    std::vector<CutEdge> edges;
+    edges.reserve(static_cast<std::size_t>(m));
+    for (std::int64_t k = 0; k < m; ++k)
+      edges.push_back({static_cast<std::size_t>(ei[k]), static_cast<std::size_t>(ej[k]), w[k]});
+    const CutGraph g(static_cast<std::size_t>(n), std::move(edges));
+    *cut = cut_value(g, SpinConfig(std::vector<std::int8_t>(spins, spins + n)));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// instance_from_json (model.cpp:318-348) -> dense fp64 (n*n must fit J_out's cap).
+int ref_instance_from_json(const char* text, std::int64_t cap, std::int64_t* n, double* J_out) {
+  try {
+    const auto inst = instance_from_json(std::string_view(text));
+    *n = static_cast<std::int64_t>(inst.n());
+    if (*n * *n <= cap)
+      for (std::int64_t i = 0; i < *n; ++i) {
+        const auto row = inst.row(static_cast<std::size_t>(i));
+        std::memcpy(J_out + i * *n, row.data(), sizeof(double) * static_cast<std::size_t>(*n));
+      }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+// instance_to_json (model.cpp:296-316) of a dense fp64 instance; returns the length
+// written (truncated at cap - 1) or -1.
+std::int64_t ref_instance_to_json(std::int64_t n, const double* J, char* out, std::int64_t cap) {
+  try {
+    const auto s = instance_to_json(make_instance(n, J));
+    const auto len = std::min<std::int64_t>(static_cast<std::int64_t>(s.size()), cap - 1);
+    std::memcpy(out, s.data(), static_cast<std::size_t>(len));
+    out[len] = 0;
+    return static_cast<std::int64_t>(s.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // extreme_eigenvalues (spectral.cpp:207-246). out6 = {lambda_max, lambda_min,
 // iterations, method, tolerance, converged}; v_max / v_min n doubles (or null).
 // Returns 0, 1 (invalid argument) or 7 (ConvergenceError, carried estimate in out6).

@@ -30,6 +30,7 @@ EXPORTS = [
     "sbg_shard_push_slab", "sbg_shard_ipc_export", "sbg_shard_ipc_open", "sbg_readout_partial",
     "sbg_gen_couplings_hash_pm1", "sbg_set_replica_a", "sbg_init_state_seeds",
     "sbg_gen_couplings_dense_pm1_rows", "sbg_get_couplings_i8", "sbg_extreme_eigenvalues", "sbg_auto_tune",
+    "sbg_set_couplings_graph", "sbg_set_couplings_entries_f64",
 ]
 
 
@@ -121,6 +122,8 @@ def lib() -> C.CDLL:
     L.sbg_get_couplings_i8.argtypes = [P, i64, i64, P]
     L.sbg_extreme_eigenvalues.argtypes = [P, C.c_double, u64, C.POINTER(Spectral), P, P]
     L.sbg_auto_tune.argtypes = [P, i32, C.c_double, C.c_double, u64, C.POINTER(Spectral)]
+    L.sbg_set_couplings_graph.argtypes = [P, i64, i64, P, P, P, P]
+    L.sbg_set_couplings_entries_f64.argtypes = [P, i64, i64, P, P, P]
     L.sbg_set_replica_a.argtypes = [P, i64, P]
     L.sbg_init_state_seeds.argtypes = [P, i64, i32, P]
     _lib = L

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/sbgpu.h"
@@ -806,6 +807,116 @@ int sbg_set_couplings_csr_i8(sbg_ctx* ctx, int64_t n, int64_t nnz, const int32_t
   ctx->kind = KIND_CSR_I8;
   ctx->energy_scale = 1.0;
   return SBG_OK;
+}
+
+namespace {
+// Both-triangle CSR with ascending columns from an upper-or-lower edge list (val = J_ij).
+int csr_from_pairs(sbg_ctx* ctx, int64_t n, const std::vector<int64_t>& a, const std::vector<int64_t>& b,
+                   const std::vector<int8_t>& v) {
+  std::vector<int32_t> rowptr(size_t(n) + 1, 0);
+  for (size_t k = 0; k < a.size(); ++k) {
+    ++rowptr[size_t(a[k]) + 1];
+    ++rowptr[size_t(b[k]) + 1];
+  }
+  for (int64_t r = 0; r < n; ++r) rowptr[size_t(r) + 1] += rowptr[size_t(r)];
+  const int64_t nnz = rowptr[size_t(n)];
+  std::vector<int32_t> fill(rowptr.begin(), rowptr.end() - 1), col(static_cast<size_t>(std::max<int64_t>(nnz, 1)));
+  std::vector<int8_t> val(static_cast<size_t>(std::max<int64_t>(nnz, 1)));
+  for (size_t k = 0; k < a.size(); ++k) {
+    int32_t& fa = fill[size_t(a[k])];
+    col[size_t(fa)] = int32_t(b[k]);
+    val[size_t(fa++)] = v[k];
+    int32_t& fb = fill[size_t(b[k])];
+    col[size_t(fb)] = int32_t(a[k]);
+    val[size_t(fb++)] = v[k];
+  }
+  std::vector<std::pair<int32_t, int8_t>> row;
+  for (int64_t r = 0; r < n; ++r) {
+    const int32_t lo = rowptr[size_t(r)], hi = rowptr[size_t(r) + 1];
+    row.clear();
+    for (int32_t k = lo; k < hi; ++k) row.emplace_back(col[size_t(k)], val[size_t(k)]);
+    std::sort(row.begin(), row.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+    for (int32_t k = lo; k < hi; ++k) {
+      col[size_t(k)] = row[size_t(k - lo)].first;
+      val[size_t(k)] = row[size_t(k - lo)].second;
+    }
+  }
+  return sbg_set_couplings_csr_i8(ctx, n, nnz, rowptr.data(), col.data(), val.data());
+}
+
+uint64_t pair_key(int64_t i, int64_t j) {  // model.cpp pair_key: unordered pair
+  const uint64_t a = uint64_t(std::min(i, j)), b = uint64_t(std::max(i, j));
+  return (a << 32) ^ b;
+}
+}  // namespace
+
+int sbg_set_couplings_graph(sbg_ctx* ctx, int64_t n, int64_t m, const int64_t* ei, const int64_t* ej,
+                            const int64_t* w, int64_t* total_weight) {
+  CHECK_CTX(ctx);
+  if (n < 1) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "instance size must be >= 1");
+  if (m < 0 || (m > 0 && (!ei || !ej || !w))) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "bad edge arrays");
+  if (n > INT32_MAX) return ctx->fail(SBG_ERR_UNSUPPORTED, "n beyond int32 CSR indices");
+  // CutGraph invariants (model.cpp:91-103), in input order
+  std::unordered_set<uint64_t> seen;
+  seen.reserve(size_t(m));
+  std::vector<int64_t> a(static_cast<size_t>(m)), b(static_cast<size_t>(m));
+  std::vector<int8_t> v(static_cast<size_t>(m));
+  long long W = 0;
+  for (int64_t k = 0; k < m; ++k) {
+    if (ei[k] < 0 || ej[k] < 0 || ei[k] >= n || ej[k] >= n)
+      return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "edge endpoint out of range");
+    if (ei[k] == ej[k]) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "self-loops are not allowed");
+    if (!seen.insert(pair_key(ei[k], ej[k])).second)
+      return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "duplicate edge (%lld, %lld)", (long long)ei[k], (long long)ej[k]);
+    if (w[k] < -127 || w[k] > 127)
+      return ctx->fail(SBG_ERR_UNSUPPORTED, "edge weight %lld outside the int8 coupling range", (long long)w[k]);
+    a[size_t(k)] = ei[k];
+    b[size_t(k)] = ej[k];
+    v[size_t(k)] = int8_t(-w[k]);  // maxcut_to_ising (model.cpp:134-142): J = -w
+    W += w[k];
+  }
+  const int rc = csr_from_pairs(ctx, n, a, b, v);
+  if (rc == SBG_OK && total_weight) *total_weight = W;
+  return rc;
+}
+
+int sbg_set_couplings_entries_f64(sbg_ctx* ctx, int64_t n, int64_t m, const int64_t* ei, const int64_t* ej,
+                                  const double* value) {
+  CHECK_CTX(ctx);
+  if (n < 1) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "instance size must be >= 1");
+  if (m < 0 || (m > 0 && (!ei || !ej || !value))) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "bad entry arrays");
+  // IsingInstance::from_entries (model.cpp:70-86), in input order
+  std::unordered_set<uint64_t> seen;
+  seen.reserve(size_t(m));
+  bool integral = true;
+  for (int64_t k = 0; k < m; ++k) {
+    if (ei[k] < 0 || ej[k] < 0 || ei[k] >= n || ej[k] >= n)
+      return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "coupling index out of range");
+    if (ei[k] == ej[k]) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "diagonal couplings are not allowed");
+    if (!seen.insert(pair_key(ei[k], ej[k])).second)
+      return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "duplicate coupling entry (%lld, %lld)", (long long)ei[k],
+                       (long long)ej[k]);
+    const double x = value[k];
+    integral = integral && x == std::floor(x) && x >= -127.0 && x <= 127.0;
+  }
+  if (integral && n <= INT32_MAX && double(2 * m) < double(n) * double(n) / 16.0) {
+    std::vector<int64_t> a, b;
+    std::vector<int8_t> v;
+    for (int64_t k = 0; k < m; ++k)
+      if (value[k] != 0.0) {
+        a.push_back(ei[k]);
+        b.push_back(ej[k]);
+        v.push_back(int8_t(value[k]));
+      }
+    return csr_from_pairs(ctx, n, a, b, v);
+  }
+  if (double(n) * double(n) > 4e10) return ctx->fail(SBG_ERR_UNSUPPORTED, "dense real-valued instance too large");
+  std::vector<double> J(size_t(n) * size_t(n), 0.0);
+  for (int64_t k = 0; k < m; ++k) {
+    J[size_t(ei[k]) * size_t(n) + size_t(ej[k])] = value[k];
+    J[size_t(ej[k]) * size_t(n) + size_t(ei[k])] = value[k];
+  }
+  return sbg_set_couplings_dense_f64(ctx, n, J.data());
 }
 
 int sbg_set_state(sbg_ctx* ctx, int64_t R, const float* x, const float* y, const float* p) {

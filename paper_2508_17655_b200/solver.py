@@ -237,6 +237,26 @@ class Solver:
         self.total_weight = graph_total_weight if graph_total_weight is not None else int(
             -np.triu(J.astype(np.int64), 1).sum())
 
+    def set_graph(self, graph) -> None:
+        """MAX-CUT graph (instances.CutGraph) straight to device CSR: maxcut_to_ising
+        (model.cpp:134-142) without the dense fp64 matrix; cut = (W - E) / 2."""
+        W = C.c_int64()
+        self._check(self._L.sbg_set_couplings_graph(self._h, graph.n, graph.m, ptr(graph.i), ptr(graph.j),
+                                                    ptr(graph.w), C.byref(W)))
+        self.n = self.n_global = graph.n
+        self.total_weight = int(W.value)
+
+    def set_instance_entries(self, entries, graph_total_weight: Optional[int] = None) -> None:
+        """IsingInstance::from_entries (model.cpp:70-86) from instances.CouplingEntries."""
+        i = np.ascontiguousarray(entries.i, np.int64)
+        j = np.ascontiguousarray(entries.j, np.int64)
+        v = np.ascontiguousarray(entries.value, np.float64)
+        self._check(self._L.sbg_set_couplings_entries_f64(self._h, entries.n, len(i), ptr(i), ptr(j), ptr(v)))
+        self.n = self.n_global = entries.n
+        integral = bool(np.all(np.mod(v, 1) == 0))
+        self.total_weight = graph_total_weight if graph_total_weight is not None else (
+            int(-v.astype(np.int64).sum()) if integral else None)
+
     # ------------------------------------------------------- spectrum / tuning
 
     def extreme_eigenvalues(self, tol: float = 1e-6, max_iters: int = 0, want_vectors: bool = False):
