@@ -86,6 +86,7 @@ int sbg_create(int device, sbg_ctx** out);
 void sbg_destroy(sbg_ctx* ctx);
 const char* sbg_last_error(const sbg_ctx* ctx);
 int sbg_device_sm_count(const sbg_ctx* ctx);
+const char* sbg_device_name(const sbg_ctx* ctx);
 
 /* Couplings. Replace IsingInstance (model.hpp:46-70; invariants model.cpp:54-68:
  * symmetric, zero diagonal). Dense integer J is kept as int8 on the device. */

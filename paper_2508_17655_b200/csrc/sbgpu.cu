@@ -65,6 +65,7 @@ bool is_sign_variant(int v) { return v == SBG_DSB || v == SBG_GDSB; }
 struct sbg_ctx {
   int device = 0;
   int sms = 148;
+  std::string device_name;
   cudaStream_t stream = nullptr;
   std::string err;
   int64_t launches = 0;
@@ -635,6 +636,7 @@ int sbg_create(int device, sbg_ctx** out) {
   auto* ctx = new sbg_ctx();
   ctx->device = device;
   ctx->sms = prop.multiProcessorCount;
+  ctx->device_name = prop.name;
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete ctx;
     return SBG_ERR_CUDA;
@@ -661,6 +663,7 @@ void sbg_destroy(sbg_ctx* ctx) {
 
 const char* sbg_last_error(const sbg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 int sbg_device_sm_count(const sbg_ctx* ctx) { return ctx ? ctx->sms : 0; }
+const char* sbg_device_name(const sbg_ctx* ctx) { return ctx ? ctx->device_name.c_str() : ""; }
 int64_t sbg_n(const sbg_ctx* ctx) { return ctx ? ctx->n : 0; }
 int64_t sbg_kernel_launches(const sbg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 

@@ -210,6 +210,10 @@ class Solver:
             raise_for(rc, self._L.sbg_last_error(self._h).decode())
 
     @property
+    def device_name(self) -> str:
+        return self._L.sbg_device_name(self._h).decode()
+
+    @property
     def sm_count(self) -> int:
         return self._L.sbg_device_sm_count(self._h)
 
@@ -507,6 +511,21 @@ class Solver:
         b.trajectory = traj
         return b
 
+    def run(self, cfg: SolverConfig, tuning: TuningResult) -> RunResult:
+        """run() (engine.cpp:112-139) for one replica: init_state(n, cfg.seed, cfg.init_mode),
+        M steps, readout; wall time covers init + steps + readout."""
+        import time
+
+        rcfg = resolve_config(cfg, tuning)
+        t0 = time.perf_counter()
+        self.init_state_seeds(np.array([rcfg.seed], np.uint64), rcfg.init_mode)
+        self.advance(rcfg, 0, int(rcfg.steps))
+        spins, energy, _, _ = self.readout()
+        wall = time.perf_counter() - t0
+        cut = None if self.total_weight is None else cut_from_energy(self.total_weight, float(energy[0]))
+        return RunResult(final_spins=spins[0].copy(), energy=float(energy[0]), cut=cut, wall_time_s=wall,
+                         config_echo=rcfg, tuning_echo=tuning)
+
     def batch_best_of(self, cfg: SolverConfig, tuning: TuningResult, n_batch: int, master_seed: int) -> RunResult:
         """bench.cpp:70-92: replicas seeded derive_seed(master, {batch, r}); min energy, ties -> lowest r."""
         if n_batch < 1:
@@ -592,6 +611,76 @@ def sweep(solver: "Solver", m_values, a_values, reps: int, cfg_base: SolverConfi
             e = energies[ai * reps:(ai + 1) * reps]
             cells.append(SweepCell(mi, ai, int(m_steps), float(a), success_probability(e, target),
                                    float(e.mean()), float(e.min()), e.copy()))
+    return cells
+
+
+SEED_STREAM_DT_SWEEP = 2  # rng.hpp:35 seed_stream::dt_sweep
+SEED_STREAM_BENCH = 6  # rng.hpp:39 seed_stream::bench
+
+
+def tune_dt(lambda_min: float, lambda_max: float, d_t_factor: float) -> float:
+    """spectral.cpp:277-286: dt = D_t sqrt(2 / (1 - lambda_min / lambda_max))."""
+    if not lambda_max > 0.0:
+        raise ValueError("lambda_max must be positive")
+    if not lambda_min < 0.0:
+        raise ValueError("lambda_min must be negative")
+    if not d_t_factor > 0.0:
+        raise ValueError("d_t_factor must be positive")
+    return d_t_factor * math.sqrt(2.0 / (1.0 - lambda_min / lambda_max))
+
+
+def stability_limit(lambda_min: float, lambda_max: float) -> float:
+    """spectral.cpp:288-292."""
+    if not lambda_max > 0.0:
+        raise ValueError("lambda_max must be positive")
+    if not lambda_min < 0.0:
+        raise ValueError("lambda_min must be negative")
+    return 2.0 / math.sqrt(1.0 - lambda_min / lambda_max)
+
+
+@dataclasses.dataclass
+class DtSweepCell:  # bench.hpp:114-124
+    di: int
+    ti: int
+    d_t_factor: float
+    t_final: float
+    dt: float
+    m_steps: int
+    stats: SuccessStats
+    mean_energy: float
+    best_energy: float
+    energies: np.ndarray
+
+
+def dt_sweep(solver: "Solver", d_t_values, t_final_values, a: float, reps: int, cfg_base: SolverConfig,
+             tuning: TuningResult, target: float):
+    """sbopt::dt_sweep (bench.cpp:208-269) on the GPU: cell (di, ti) runs reps replicas at
+    dt = tune_dt(lambda_min, lambda_max, D_t) and M = llround(t_M / dt), replica r seeded
+    derive_seed(cfg_base.seed, {dt_sweep, di, ti, r}); one device launch per cell."""
+    if len(d_t_values) == 0 or len(t_final_values) == 0:
+        raise ValueError("empty sweep axes")
+    if reps < 1:
+        raise ValueError("sweep needs reps >= 1")
+    if any(not v > 0.0 for v in d_t_values):
+        raise ValueError("D_t values must be positive")
+    if any(not v > 0.0 for v in t_final_values):
+        raise ValueError("t_M values must be positive")
+    cells = []
+    for di, d_t in enumerate(d_t_values):
+        dt = tune_dt(tuning.lambda_min, tuning.lambda_max, d_t)
+        for ti, t_final in enumerate(t_final_values):
+            q = t_final / dt  # std::llround: half away from zero
+            m_steps = int(math.floor(q + 0.5)) if q >= 0 else -int(math.floor(-q + 0.5))
+            if m_steps == 0:
+                raise ValueError(f"t_M = {t_final:f} rounds to zero steps at dt = {dt:f}")
+            cfg = resolve_config(dataclasses.replace(cfg_base, steps=m_steps, dt=dt, a=a), tuning)
+            seeds = np.array([_derive_seed(cfg_base.seed, [SEED_STREAM_DT_SWEEP, di, ti, r]) for r in range(reps)],
+                             np.uint64)
+            solver.init_state_seeds(seeds, cfg.init_mode)
+            solver.advance(cfg, 0, m_steps)
+            _, e, _, _ = solver.readout()
+            cells.append(DtSweepCell(di, ti, float(d_t), float(t_final), dt, m_steps, success_probability(e, target),
+                                     float(e.mean()), float(e.min()), e.copy()))
     return cells
 
 
