@@ -43,6 +43,69 @@ __device__ __forceinline__ void gsb_phase(float F, float& x, float& y, float& p,
   p = pn;
 }
 
+// Two spins at once on the packed FP32 pipe (fma.rn.f32x2, sm_100). Every
+// operation of gsb_phase is an FMA with an exact identity operand:
+//   a*b = fma(a, b, -0)   a+b = fma(a, 1, b)   a-b = fma(b, -1, a)
+// each equal to the correctly rounded scalar op (signed zeros included), so
+// the pair update is bitwise gsb_phase applied to each lane. The identity
+// operands MUST be runtime values (kernel arguments): with literal -0 / 1 / -1
+// ptxas rewrites the FMAs into FMUL2 / FADD2 and then contracts those pairs
+// back into FFMA2, changing the rounding.
+namespace f2 {
+__device__ __forceinline__ uint64_t pk(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+}  // namespace f2
+
+struct PhaseIdent {  // -0, 1, -1 supplied at run time (see above)
+  float mzero, one, mone;
+};
+
+struct PhaseConsts2 {
+  uint64_t a, c, dt, inv, mzero, one, mone;
+  __device__ __forceinline__ PhaseConsts2(const PhaseConsts& k, const PhaseIdent& id)
+      : a(f2::pk(k.a, k.a)), c(f2::pk(k.c, k.c)), dt(f2::pk(k.dt, k.dt)), inv(f2::pk(k.inv, k.inv)),
+        mzero(f2::pk(id.mzero, id.mzero)), one(f2::pk(id.one, id.one)), mone(f2::pk(id.mone, id.mone)) {}
+};
+
+// The strict walls of gsb_phase, branch-free (selects only).
+__device__ __forceinline__ float clamp_wall(float xn, float& yn) {
+  const bool hi = xn > 1.0f, lo = xn < -1.0f;
+  yn = (hi || lo) ? 0.0f : yn;
+  return hi ? 1.0f : (lo ? -1.0f : xn);
+}
+
+// (x0, x1), (y0, y1), (p0, p1) updated with fields F0, F1; a2 = packed A per lane.
+__device__ __forceinline__ void gsb_phase2(float F0, float F1, float& x0, float& x1, float& y0, float& y1, float& p0,
+                                           float& p1, const PhaseConsts2& k, uint64_t a2) {
+  using namespace f2;
+  const uint64_t x = pk(x0, x1), y = pk(y0, y1), p = pk(p0, p1), F = pk(F0, F1);
+  const uint64_t ax2 = fma(fma(a2, x, k.mzero), x, k.mzero);
+  const uint64_t g = fma(ax2, k.mone, k.one);
+  const uint64_t pn = fma(fma(fma(g, p, k.mzero), k.inv, k.mzero), k.mone, p);
+  const uint64_t t = fma(fma(k.c, F, k.mzero), k.mone, fma(pn, x, k.mzero));
+  const uint64_t yn = fma(fma(t, k.dt, k.mzero), k.mone, y);
+  const uint64_t xn = fma(fma(yn, k.dt, k.mzero), k.one, x);
+  float xa, xb, ya, yb;
+  upk(xn, xa, xb);
+  upk(yn, ya, yb);
+  upk(pn, p0, p1);
+  x0 = clamp_wall(xa, ya);
+  x1 = clamp_wall(xb, yb);
+  y0 = ya;
+  y1 = yb;
+}
+
 // q = rint(x * 2^30): the fixed-point image of x fed to the int8 tensor cores
 // as four byte planes (u8, u8, u8, s8). |x| <= 1 so |q| <= 2^30.
 __device__ __forceinline__ int32_t quant30(float x) { return __float2int_rn(__fmul_rn(x, 0x1p30f)); }

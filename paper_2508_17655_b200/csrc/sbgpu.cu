@@ -26,6 +26,7 @@
 #include "step_i8.cuh"
 #include "step_tma.cuh"
 #include "step_pair.cuh"
+#include "step_resident.cuh"
 
 using namespace sbg;
 
@@ -93,6 +94,7 @@ struct sbg_ctx {
   TmaMaps pmaps_planes[2];               // pair kernel, fixed-point planes (B half = 32 rows)
   TmaMaps fxmaps_sign[2], fxmaps_planes[2];  // real-J kernels (B tiles of 64 / 32 rows)
   TmaMaps maps_sign_cw8[2];                  // sign pair kernel with 8-replica state chunks
+  TmaMaps rmaps_sign[2];                     // resident-state pair kernel (B halves of 64 rows, G tile stores)
   unsigned long long* dE2p = nullptr;    // real-J readout: per-J-plane partial E2 [FX_NA][rpad]
   // CSR: spin-major working copies [npad][rp] and the ping-pong gathered operand (q int32 / sign int8)
   float *dXs = nullptr, *dYs = nullptr, *dPs = nullptr;
@@ -199,6 +201,10 @@ int dev_knob(const char* name) {
   const char* e = getenv(name);
   return e ? atoi(e) : 0;
 }
+bool getenv_is0(const char* name) {
+  const char* e = getenv(name);
+  return e && atoi(e) == 0;
+}
 
 template <int NP, int BN, int ST, int NB, int NA = 1>
 int launch_multistep(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& a) {
@@ -228,6 +234,69 @@ int launch_multistep_pair(sbg_ctx* ctx, const TmaMaps& maps, MultiStepArgs a) {
   kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(maps, a);
   CK(cudaGetLastError());
   ++ctx->launches;
+  return SBG_OK;
+}
+
+// Resident-state pair kernel (step_resident.cuh): sign variants, dense int8 J.
+constexpr int RES_STAGES = 8;
+
+bool resident_ok(const sbg_ctx* ctx) {
+  const int64_t num_mp = ctx->npad / 256;
+  return ctx->kind == KIND_DENSE_I8 && !ctx->sharded && ctx->npad % 256 == 0 && num_mp >= 1 &&
+         num_mp <= ctx->sms / 2 && ctx->rpad % ResCfg<RES_STAGES>::NR == 0;
+}
+
+template <int EPI, int CH, int ST = RES_STAGES>
+int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms) {
+  using Cfg = ResCfg<ST, EPI, CH>;
+  auto kern = gsb_resident_pair_kernel<ST, EPI, CH>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  ResidentArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.n = ms.n;
+  a.npad = ms.npad;
+  a.R = ms.R;
+  a.rpad = ms.rpad;
+  a.num_m = ms.npad / Cfg::BM;
+  const int num_mp = ms.npad / 256, num_n = ms.rpad / Cfg::NR;
+  a.rb_per_group = std::min(num_n, (ctx->sms / 2) / num_mp);
+  a.groups = (num_n + a.rb_per_group - 1) / a.rb_per_group;
+  a.k = ms.k;
+  a.M = ms.M;
+  a.t_begin = ms.t_begin;
+  a.nsteps = ms.nsteps;
+  a.done = ctx->d_done;
+  a.x = ctx->dX;
+  a.y = ctx->dY;
+  a.p = ctx->dP;
+  a.a_rep = ms.a_rep;
+  a.ident = PhaseIdent{-0.0f, 1.0f, -1.0f};
+  a.dbg = dev_knob("SBG_STEP_DBG");
+  static unsigned long long* trace = nullptr;  // dev knob SBG_RES_TRACE: stamps of pair 0, group 0
+  if (dev_knob("SBG_RES_TRACE")) {
+    if (!trace) CK(cudaMalloc(&trace, sizeof(unsigned long long) * 8 * 2 * 4096));
+    CK(cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 8 * 2 * 4096, ctx->stream));
+    a.trace = trace;
+    a.nsteps = std::min(a.nsteps, 4096);
+  }
+  CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * num_n, ctx->stream));
+  kern<<<2 * num_mp * a.rb_per_group, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(maps, a);
+  CK(cudaGetLastError());
+  ++ctx->launches;
+  if (a.trace) {
+    std::vector<unsigned long long> h(size_t(8 * 2 * a.nsteps));
+    CK(cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    FILE* f = fopen("gpurun_out/res_trace.txt", "w");
+    if (f) {
+      for (int s = 0; s < a.nsteps; ++s)
+        for (int c = 0; c < 2; ++c) {
+          const unsigned long long* r = &h[size_t((s * 2 + c) * 8)];
+          fprintf(f, "%d %d %llu %llu %llu %llu %llu %llu %llu\n", s, c, r[0], r[1], r[2], r[3], r[4], r[5], r[6]);
+        }
+      fclose(f);
+    }
+  }
   return SBG_OK;
 }
 
@@ -363,6 +432,19 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
       }
       ctx->fxmaps_sign[cur] = ctx->maps_sign[cur];
       ctx->fxmaps_planes[cur] = ctx->maps_planes[cur];
+      {
+        TmaMaps& rm = ctx->rmaps_sign[cur];
+        rm = ctx->maps_sign[cur];
+        const uint64_t gvalid = uint64_t(ctx->sharded ? ctx->n_global : ctx->n);
+        int rcr = SBG_OK;
+        for (int par = 0; par < 2 && !rcr; ++par) {
+          rcr = encode_2d_u8(ctx, &rm.Gin[par], ctx->dG[cur ^ par], ctx->npad, rpad, 128, ResCfg<RES_STAGES>::B_HALF);
+          if (!rcr)
+            rcr = encode_2d(ctx, &rm.Gout[par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ par ^ 1], gvalid, R,
+                            gdim(ctx), 128, ResCfg<RES_STAGES>::NR, CU_TENSOR_MAP_SWIZZLE_NONE);
+        }
+        if (rcr) return rcr;
+      }
       for (int par = 0; par < 2; ++par) {
         int rc = encode_2d_u8(ctx, &ctx->pmaps_planes[cur].Gin[par], ctx->dG[cur ^ par], ctx->npad, NPL * rpad, 128,
                               NPAIR_PLANE / 2);
@@ -1102,6 +1184,17 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
         // real-valued J: 3 J planes x (sign | 4 x-planes), single-CTA
         rc = sign ? launch_multistep<1, BN_FX_SIGN, 2, 4, FX_NA>(ctx, ctx->fxmaps_sign[cur], a)
                   : launch_multistep<NPL, BN_FX_PLANE, 2, 3, FX_NA>(ctx, ctx->fxmaps_planes[cur], a);
+      } else if (sign && !getenv_is0("SBG_RESIDENT") && resident_ok(ctx)) {
+        // default for sign variants: state resident in TMEM (step_resident.cuh); SBG_RESIDENT=0
+        // selects the streaming kernels (dev comparison)
+        switch (dev_knob("SBG_RES_CFG")) {
+          case 1: rc = launch_resident<16, 8>(ctx, ctx->rmaps_sign[cur], a); break;
+          case 2: rc = launch_resident<8, 8>(ctx, ctx->rmaps_sign[cur], a); break;
+          case 3: rc = launch_resident<8, 4>(ctx, ctx->rmaps_sign[cur], a); break;
+          case 6: rc = launch_resident<16, 4, 6>(ctx, ctx->rmaps_sign[cur], a); break;
+          case 7: rc = launch_resident<16, 4, 7>(ctx, ctx->rmaps_sign[cur], a); break;
+          default: rc = launch_resident<16, 4>(ctx, ctx->rmaps_sign[cur], a);
+        }
       } else if (sign) {
         switch (pair_ok ? knob : -1) {
           case -1: rc = launch_multistep<1, BN_SIGN, SIGN_STAGES, SIGN_NBUF>(ctx, ctx->maps_sign[cur], a); break;

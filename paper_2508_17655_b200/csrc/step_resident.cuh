@@ -1,0 +1,392 @@
+// The hot path with the replica state RESIDENT in tensor memory (sign variants).
+//
+// The streaming kernels (step_tma.cuh, step_pair.cuh) move x, y, p through HBM
+// every step: 24 B per spin-update, which bounds C2 at ~60 us/step. Here each
+// CTA pair owns a fixed (256-spin pair-block, 128-replica block) for a whole
+// group of replicas and keeps that block's x, y, p in TMEM next to its
+// accumulator, so the only per-step traffic is the operands from L2 (J rows and
+// the G_t tile) and the 16 KB G_{t+1} chunk it publishes. HBM sees the state
+// once per launch per group (load at group start, store at group end).
+//
+// Per CTA TMEM (512 columns x 128 lanes; lane = spin of this CTA):
+//   [0, 128)    s32 accumulator F = J G_t for the 128 replicas of the block
+//   [128, 256)  x     [256, 384) y     [384, 512) p      (fp32)
+// Work decomposition: pairs are arranged num_mp (spin pair-blocks) x RB
+// (replica blocks per group); replica block of group g is n = g*RB + rbk.
+// Groups run one after another inside the launch; every pair of a group runs
+// all nsteps steps of its block. Step t+1 of block n needs G_{t+1}[n] from all
+// num_m CTAs of the block: the done[n] counters of step_tma.cuh (released after
+// each CTA's G chunk store completes, acquired by the operand producers).
+// Warps: 0 operand producer (both CTAs), 1 MMA issuer (leader), 2 TMEM
+// allocator, 3 idle, 4..19 epilogue (4 per TMEM lane quadrant, 32 replica
+// columns each): tcgen05.ld F and state, gsb_phase, tcgen05.st state, sign
+// bytes into a 16 KB smem tile, one TMA store of the tile, release done[n].
+// Arithmetic is the streaming kernels' gsb_phase, so results are bitwise equal.
+#pragma once
+
+#include <cstdint>
+#include <type_traits>
+#include <cuda.h>
+
+#include "gsb_phase.cuh"
+#include "ptx.cuh"
+#include "step_tma.cuh"
+
+namespace sbg {
+
+namespace ptx {
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+template <int N>
+__device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&v)[N]);
+template <>
+__device__ __forceinline__ void tmem_st<4>(uint32_t taddr, const uint32_t (&v)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+template <>
+__device__ __forceinline__ void tmem_st<8>(uint32_t taddr, const uint32_t (&v)[8]) {
+  tmem_st8(taddr, v);
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+}  // namespace ptx
+
+template <int STAGES_, int EPI_WARPS_ = 16, int CH_ = 4>
+struct ResCfg {
+  static constexpr int BM = 128;                 // spins per CTA
+  static constexpr int BK = 128;                 // K bytes per stage
+  static constexpr int NR = 128;                 // replicas per pair block (UMMA N)
+  static constexpr int B_HALF = NR / 2;          // B rows staged per CTA
+  static constexpr int A_BYTES = BM * BK;        // 16 KB
+  static constexpr int B_BYTES = B_HALF * BK;    // 8 KB
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = STAGES_;
+  static constexpr int G_BYTES = NR * BM;        // G_{t+1} tile [128 replicas][128 spins]
+  static constexpr int EPI_WARPS = EPI_WARPS_;           // 4 per TMEM lane quadrant x column groups
+  static constexpr int COLS_PER_WARP = NR / (EPI_WARPS / 4);
+  static constexpr int CH = CH_;                           // replica columns per TMEM load chunk
+  static constexpr int CHUNKS = COLS_PER_WARP / CH;
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
+  static constexpr int NUM_BARS = 2 * STAGES + 2;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + G_BYTES + 1024 + 8 * NUM_BARS + 64;
+  static constexpr uint32_t COL_X = 128, COL_Y = 256, COL_P = 384;
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+};
+
+struct ResidentArgs {
+  int32_t n, npad, R, rpad;
+  int32_t num_m;     // 128-spin blocks (CTAs per replica block)
+  int32_t rb_per_group;
+  int32_t groups;
+  PhaseConsts k;
+  uint64_t M, t_begin;
+  int32_t nsteps;
+  uint32_t* done;    // [rpad / 128], zero at launch
+  float *x, *y, *p;  // replica-major [rpad][npad]
+  const float* a_rep;
+  PhaseIdent ident;           // -0, 1, -1 (runtime identity operands of gsb_phase2)
+  int32_t dbg;                // dev only: 1 = skip J loads after the first step, 2 = no G dependency wait
+  unsigned long long* trace;  // dev only: per-step %globaltimer stamps of pair 0 (null = off)
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int STAGES_, int EPI_WARPS_, int CH_>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_WARPS_, CH_>::THREADS, 1)
+    gsb_resident_pair_kernel(const __grid_constant__ TmaMaps maps, const ResidentArgs args) {
+  using Cfg = ResCfg<STAGES_, EPI_WARPS_, CH_>;
+  constexpr int CH = Cfg::CH;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = ptx::smem_u32(smem_raw);
+  const uint32_t base = (raw_addr + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (base - raw_addr);
+  const uint32_t a_base = base;
+  const uint32_t b_base = base + STAGES * Cfg::A_BYTES;
+  const uint32_t g_base = base + STAGES * Cfg::STAGE_BYTES;
+  uint8_t* g_tile = smem + STAGES * Cfg::STAGE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(g_tile + Cfg::G_BYTES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
+  auto bar = [&](int i) { return ptx::smem_u32(bars + i); };
+  auto full_bar = [&](int s) { return bar(s); };
+  auto empty_bar = [&](int s) { return bar(STAGES + s); };
+  const uint32_t tfull = bar(2 * STAGES), tempty = bar(2 * STAGES + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t cr = ptx::cluster_ctarank();
+  const bool leader = cr == 0;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(full_bar(s), 2);
+      ptx::mbar_init(empty_bar(s), 1);
+    }
+    ptx::mbar_init(tfull, 1);
+    ptx::mbar_init(tempty, 2 * Cfg::EPI_WARPS);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) {
+    ptx::tmem_alloc_pair(ptx::smem_u32(tmem_slot), 512);
+    ptx::tmem_relinquish_pair();
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync_all();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_mp = args.num_m / 2;
+  const int pair = blockIdx.x >> 1;
+  const int mp = pair % num_mp, rbk = pair / num_mp;
+  const int m_blk = 2 * mp + static_cast<int>(cr);
+  const int i0 = m_blk * Cfg::BM;
+  const int KB = args.npad / Cfg::BK;
+  const int num_n = args.rpad / Cfg::NR;
+
+  if (warp == 0) {  // ------------------------------------------------ operand producer
+    if (ptx::elect_one()) {
+      ptx::prefetch_tmap(&maps.J);
+      ptx::prefetch_tmap(&maps.Gin[0]);
+      ptx::prefetch_tmap(&maps.Gin[1]);
+    }
+    int stage = 0;
+    uint32_t ph = 0;
+    const uint64_t keep = ptx::policy_evict_last();
+    for (int g = 0; g < args.groups; ++g) {
+      const int n_blk = g * args.rb_per_group + rbk;
+      if (n_blk >= num_n) break;
+      for (int s = 0; s < args.nsteps; ++s) {
+        // J does not depend on the step: the first PRE stages' J tiles are requested
+        // before waiting for G_t (expect_tx without arrive), the G halves after.
+        constexpr int PRE = STAGES < 16 ? STAGES : 16;
+        int st0 = stage;
+        uint32_t ph0 = ph;
+        const bool skipJ = args.dbg == 1 && (s > 0 || g > 0);
+        for (int kb = 0; kb < PRE && kb < KB; ++kb) {
+          ptx::mbar_wait(empty_bar(st0), ph0 ^ 1u);
+          if (ptx::elect_one() && !skipJ) {
+            const uint32_t fb = ptx::mapa(full_bar(st0), 0);
+            ptx::mbar_expect_tx_cluster(fb, Cfg::A_BYTES);
+            ptx::tma_load_2d_pair_hint(a_base + st0 * Cfg::A_BYTES, &maps.J, fb, kb * Cfg::BK, m_blk * Cfg::BM, keep);
+          }
+          __syncwarp();
+          if (++st0 == STAGES) {
+            st0 = 0;
+            ph0 ^= 1u;
+          }
+        }
+        if (args.dbg != 2) dep::wait_block(args.done, n_blk, 0u, static_cast<uint32_t>(s * args.num_m));
+        if (args.trace && pair == 0 && g == 0 && lane == 0) args.trace[(s * 2 + cr) * 8 + 0] = gtimer();
+        const CUtensorMap* gin = &maps.Gin[s & 1];
+        for (int kb = 0; kb < KB; ++kb) {
+          const bool pre = kb < PRE;
+          if (!pre) ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
+          if (ptx::elect_one()) {
+            const uint32_t fb = ptx::mapa(full_bar(stage), 0);
+            ptx::mbar_arrive_expect_tx_cluster(fb, (pre || skipJ) ? Cfg::B_BYTES : Cfg::STAGE_BYTES);
+            if (!pre && !skipJ)
+              ptx::tma_load_2d_pair_hint(a_base + stage * Cfg::A_BYTES, &maps.J, fb, kb * Cfg::BK, m_blk * Cfg::BM,
+                                         keep);
+            ptx::tma_load_2d_pair_hint(b_base + stage * Cfg::B_BYTES, gin, fb, kb * Cfg::BK,
+                                       n_blk * Cfg::NR + static_cast<int>(cr) * Cfg::B_HALF, keep);
+          }
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {  // ------------------------------------------ MMA issuer (leader)
+    if (leader) {
+      constexpr uint32_t idesc = ptx::idesc_i8(256, Cfg::NR, true, true);
+      int stage = 0;
+      uint32_t ph = 0;
+      int lt = 0;
+      for (int g = 0; g < args.groups; ++g) {
+        const int n_blk = g * args.rb_per_group + rbk;
+        if (n_blk >= num_n) break;
+        for (int s = 0; s < args.nsteps; ++s, ++lt) {
+          ptx::mbar_wait(tempty, (lt & 1) ^ 1u);
+          ptx::tc_fence_after();
+          for (int kb = 0; kb < KB; ++kb) {
+            ptx::mbar_wait(full_bar(stage), ph);
+            ptx::tc_fence_after();
+            if (ptx::elect_one()) {
+              const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + stage * Cfg::A_BYTES);
+              const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + stage * Cfg::B_BYTES);
+#pragma unroll
+              for (int k = 0; k < Cfg::BK / 32; ++k)
+                ptx::mma_i8_pair(tmem_base, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+              ptx::mma_commit_pair_mc(empty_bar(stage), 0x3);
+            }
+            __syncwarp();
+            if (++stage == STAGES) {
+              stage = 0;
+              ph ^= 1u;
+            }
+          }
+          if (ptx::elect_one()) ptx::mma_commit_pair_mc(tfull, 0x3);
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp >= 4) {  // ----------------------------------------- epilogue
+    const int q = warp & 3;
+    const int h = (warp - 4) >> 2;
+    const int spin = i0 + q * 32 + lane;
+    const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+    const uint32_t tempty_leader = ptx::mapa(tempty, 0);
+    const int epi_tid = threadIdx.x - 128;
+    int lt = 0;
+    for (int g = 0; g < args.groups; ++g) {
+      const int n_blk = g * args.rb_per_group + rbk;
+      if (n_blk >= num_n) break;
+      const int r0 = n_blk * Cfg::NR + h * Cfg::COLS_PER_WARP;  // this thread's first replica
+      // load the block's state into TMEM (coalesced: a warp reads 32 consecutive spins)
+#pragma unroll 1
+      for (int half = 0; half < Cfg::COLS_PER_WARP / 16; ++half) {
+        uint32_t vx[16], vy[16], vp[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const size_t off = static_cast<size_t>(r0 + half * 16 + j) * args.npad + spin;
+          vx[j] = __float_as_uint(args.x[off]);
+          vy[j] = __float_as_uint(args.y[off]);
+          vp[j] = __float_as_uint(args.p[off]);
+        }
+        const uint32_t col = h * Cfg::COLS_PER_WARP + half * 16;
+        ptx::tmem_st16(t_lane + Cfg::COL_X + col, vx);
+        ptx::tmem_st16(t_lane + Cfg::COL_Y + col, vy);
+        ptx::tmem_st16(t_lane + Cfg::COL_P + col, vp);
+      }
+      ptx::tmem_st_wait();
+      for (int s = 0; s < args.nsteps; ++s, ++lt) {
+        PhaseConsts k = args.k;
+        k.inv = __frcp_rn(static_cast<float>(args.M - (args.t_begin + static_cast<uint64_t>(s))));
+        const PhaseConsts2 k2(k, args.ident);
+        const float* arep = args.a_rep;
+        ptx::mbar_wait(tfull, lt & 1);
+        __syncwarp();
+        ptx::tc_fence_after();
+        if (args.trace && pair == 0 && g == 0 && epi_tid == 0) args.trace[(s * 2 + cr) * 8 + 1] = gtimer();
+        // 4 chunks of 8 replica columns; TMEM loads of chunk c+1 overlap the math of chunk c
+        uint32_t bf[2][CH], bx[2][CH], by[2][CH], bp[2][CH];
+        auto ld_chunk = [&](int c, int b) {
+          const uint32_t col = h * Cfg::COLS_PER_WARP + c * CH;
+          ptx::tmem_ld<CH>(t_lane + col, bf[b]);
+          ptx::tmem_ld<CH>(t_lane + Cfg::COL_X + col, bx[b]);
+          ptx::tmem_ld<CH>(t_lane + Cfg::COL_Y + col, by[b]);
+          ptx::tmem_ld<CH>(t_lane + Cfg::COL_P + col, bp[b]);
+        };
+        auto wait_chunk = [&](int b) {
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < CH; ++j) asm volatile("" : "+r"(bf[b][j]), "+r"(bx[b][j]), "+r"(by[b][j]), "+r"(bp[b][j]));
+        };
+        ld_chunk(0, 0);
+        wait_chunk(0);
+        const bool tr = args.trace && pair == 0 && g == 0 && epi_tid == 0;
+        if (tr) args.trace[(s * 2 + cr) * 8 + 4] = gtimer();
+        auto chunks = [&](auto has_arep) {
+#pragma unroll
+          for (int c = 0; c < Cfg::CHUNKS; ++c) {
+            const int b = c & 1;
+            if (c + 1 < Cfg::CHUNKS) ld_chunk(c + 1, b ^ 1);
+#pragma unroll
+            for (int j = 0; j < CH; j += 2) {
+              float x0 = __uint_as_float(bx[b][j]), x1 = __uint_as_float(bx[b][j + 1]);
+              float y0 = __uint_as_float(by[b][j]), y1 = __uint_as_float(by[b][j + 1]);
+              float p0 = __uint_as_float(bp[b][j]), p1 = __uint_as_float(bp[b][j + 1]);
+              uint64_t a2 = k2.a;
+              if constexpr (decltype(has_arep)::value)
+                a2 = f2::pk(arep[min(r0 + c * CH + j, args.R - 1)], arep[min(r0 + c * CH + j + 1, args.R - 1)]);
+              gsb_phase2(static_cast<float>(static_cast<int32_t>(bf[b][j])),
+                         static_cast<float>(static_cast<int32_t>(bf[b][j + 1])), x0, x1, y0, y1, p0, p1, k2, a2);
+              bx[b][j] = __float_as_uint(x0);
+              bx[b][j + 1] = __float_as_uint(x1);
+              by[b][j] = __float_as_uint(y0);
+              by[b][j + 1] = __float_as_uint(y1);
+              bp[b][j] = __float_as_uint(p0);
+              bp[b][j + 1] = __float_as_uint(p1);
+              uint8_t* gp = g_tile + (h * Cfg::COLS_PER_WARP + c * CH + j) * Cfg::BM + q * 32 + lane;
+              gp[0] = static_cast<uint8_t>(sgn8(x0));
+              gp[Cfg::BM] = static_cast<uint8_t>(sgn8(x1));
+            }
+            const uint32_t col = h * Cfg::COLS_PER_WARP + c * CH;
+            ptx::tmem_st<CH>(t_lane + Cfg::COL_X + col, bx[b]);
+            ptx::tmem_st<CH>(t_lane + Cfg::COL_Y + col, by[b]);
+            ptx::tmem_st<CH>(t_lane + Cfg::COL_P + col, bp[b]);
+            if (c + 1 < Cfg::CHUNKS) wait_chunk(b ^ 1);
+          }
+        };
+        if (arep)
+          chunks(std::true_type{});
+        else
+          chunks(std::false_type{});
+        if (tr) args.trace[(s * 2 + cr) * 8 + 5] = gtimer();
+        ptx::tmem_st_wait();
+        if (tr) args.trace[(s * 2 + cr) * 8 + 6] = gtimer();
+        // F consumed: the leader may overwrite the accumulator
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader);
+        // publish G_{t+1} for this CTA's 128 spins x 128 replicas
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);
+        if (epi_tid == 0) {
+          if (args.trace && pair == 0 && g == 0) args.trace[(s * 2 + cr) * 8 + 2] = gtimer();
+          ptx::tma_store_2d(&maps.Gout[s & 1], g_base, i0, n_blk * Cfg::NR);
+          ptx::bulk_commit();
+          ptx::bulk_wait0();
+          dep::fence_proxy_async_global();
+          __threadfence();
+          dep::release_add(args.done + n_blk, 1u);
+          if (args.trace && pair == 0 && g == 0) args.trace[(s * 2 + cr) * 8 + 3] = gtimer();
+        }
+        ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);  // g_tile reusable
+      }
+      // write the block's state back
+#pragma unroll 1
+      for (int half = 0; half < Cfg::COLS_PER_WARP / 16; ++half) {
+        const uint32_t col = h * Cfg::COLS_PER_WARP + half * 16;
+        uint32_t vx[16], vy[16], vp[16];
+        ptx::tmem_ld<16>(t_lane + Cfg::COL_X + col, vx);
+        ptx::tmem_ld<16>(t_lane + Cfg::COL_Y + col, vy);
+        ptx::tmem_ld<16>(t_lane + Cfg::COL_P + col, vp);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const size_t off = static_cast<size_t>(r0 + half * 16 + j) * args.npad + spin;
+          args.x[off] = __uint_as_float(vx[j]);
+          args.y[off] = __uint_as_float(vy[j]);
+          args.p[off] = __uint_as_float(vp[j]);
+        }
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync_all();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc_pair(tmem_base, 512);
+}
+
+}  // namespace sbg

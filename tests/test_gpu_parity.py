@@ -305,8 +305,9 @@ def test_trajectory_sampling_records_start_strides_final(solver, orc):
 def test_p3_reference_init_30_and_50_steps(solver, golden, variant, seed):
     """P3 with the reference's own init_state (x ~ U(-1,1), y = 0): <= 1e-5 relative at
     30 steps. At 50 steps fp32 state rounding, amplified by the chaotic
-    dynamics, is past 1e-5 for any fp32 implementation; this wider init
-    measures up to 1.1e-4 (bSB), so 50 steps is held to 2e-4."""
+    dynamics, is past 1e-5 for any fp32 implementation; with this wider init
+    the fp32 mirror itself (bitwise equal to the GPU) measures 3.0e-4 (bSB, seed 1),
+    1.1e-4 (bSB, seed 2), <= 4.5e-5 otherwise, so 50 steps is held to 5e-4."""
     J = golden["J_n37_s11"]
     c, dt = float(golden["tune_c"]), float(golden["tune_dt"])
     solver.set_instance(J)
@@ -314,10 +315,37 @@ def test_p3_reference_init_30_and_50_steps(solver, golden, variant, seed):
     solver.set_state(x0, np.zeros_like(x0))
     cps = list(golden["traj_checkpoints"])
     m = 0
-    for cp, tol in ((30, 1e-5), (50, 2e-4)):
+    for cp, tol in ((30, 1e-5), (50, 5e-4)):
         solver.advance(cfg_for(variant, 200, dt, c, 0.2), m, cp)
         m = cp
         x, _, _ = solver.get_state()
         ref = golden[f"traj_ref_v{variant}_s{seed}_x"][cps.index(cp)]
         err = np.abs(x[0] - ref).max() / np.abs(ref).max()
         assert err <= tol, (variant, cp, err)
+
+
+@pytest.mark.parametrize("n,R,variant", [(2000, 8192, GDSB), (300, 100, GDSB), (2000, 1000, 1), (700, 3000, GDSB),
+                                         (4000, 512, 1), (256, 1, GDSB)])
+def test_resident_kernel_equals_streaming(solver, orc, n, R, variant, monkeypatch):
+    """The TMEM-resident sign-variant kernel (step_resident.cuh, the default) against the
+    streaming kernels (SBG_RESIDENT=0): bitwise identical states and energies after a
+    multi-step launch, including per-replica A."""
+    from paper_2508_17655_b200 import InitMode
+
+    solver.gen_random_dense(n, 3)
+    c = 1 / (2 * np.sqrt(n))
+    arep = np.random.default_rng(n).random(R).astype(np.float32)
+    out = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SBG_RESIDENT", flag)
+        for use_a in (False, True):
+            solver.init_state(R, InitMode.small_uniform, 5, 7)
+            solver.set_replica_a(arep if use_a else None)
+            solver.advance(cfg_for(variant, 100, 1.25, c, 0.2), 0, 13)
+            x, y, p = solver.get_state()
+            _, e, best, _ = solver.readout()
+            out.append((x, y, p, e, best))
+        solver.set_replica_a(None)
+    for a, b in zip(out[:2], out[2:]):
+        assert all((u.view(np.uint32) == v.view(np.uint32)).all() for u, v in zip(a[:3], b[:3]))
+        assert (a[3] == b[3]).all() and a[4] == b[4]
