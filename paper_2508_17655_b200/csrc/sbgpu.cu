@@ -27,6 +27,7 @@
 #include "step_tma.cuh"
 #include "step_pair.cuh"
 #include "step_resident.cuh"
+#include "step_resident2.cuh"
 
 using namespace sbg;
 
@@ -95,6 +96,7 @@ struct sbg_ctx {
   TmaMaps fxmaps_sign[2], fxmaps_planes[2];  // real-J kernels (B tiles of 64 / 32 rows)
   TmaMaps maps_sign_cw8[2];                  // sign pair kernel with 8-replica state chunks
   TmaMaps rmaps_sign[2];                     // resident-state pair kernel (B halves of 64 rows, G tile stores)
+  TmaMaps rmaps2_sign[2];                    // ping-pong resident kernel (B halves of 32 rows, 64-row G tiles)
   unsigned long long* dE2p = nullptr;    // real-J readout: per-J-plane partial E2 [FX_NA][rpad]
   // CSR: spin-major working copies [npad][rp] and the ping-pong gathered operand (q int32 / sign int8)
   float *dXs = nullptr, *dYs = nullptr, *dPs = nullptr;
@@ -239,6 +241,7 @@ int launch_multistep_pair(sbg_ctx* ctx, const TmaMaps& maps, MultiStepArgs a) {
 
 // Resident-state pair kernel (step_resident.cuh): sign variants, dense int8 J.
 constexpr int RES_STAGES = 8;
+constexpr int RES2_STAGES = 8;
 
 bool resident_ok(const sbg_ctx* ctx) {
   const int64_t num_mp = ctx->npad / 256;
@@ -293,6 +296,60 @@ int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms) 
         for (int c = 0; c < 2; ++c) {
           const unsigned long long* r = &h[size_t((s * 2 + c) * 8)];
           fprintf(f, "%d %d %llu %llu %llu %llu %llu %llu %llu\n", s, c, r[0], r[1], r[2], r[3], r[4], r[5], r[6]);
+        }
+      fclose(f);
+    }
+  }
+  return SBG_OK;
+}
+
+template <int ST = RES2_STAGES>
+int launch_resident_pp(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms) {
+  using Cfg = Res2Cfg<ST>;
+  auto kern = gsb_resident_pp_kernel<ST>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  ResidentArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.n = ms.n;
+  a.npad = ms.npad;
+  a.R = ms.R;
+  a.rpad = ms.rpad;
+  a.num_m = ms.npad / Cfg::BM;
+  const int num_mp = ms.npad / 256, num_pb = ms.rpad / (2 * Cfg::NR);  // 128-replica pair blocks
+  a.rb_per_group = std::min(num_pb, (ctx->sms / 2) / num_mp);
+  a.groups = (num_pb + a.rb_per_group - 1) / a.rb_per_group;
+  a.k = ms.k;
+  a.M = ms.M;
+  a.t_begin = ms.t_begin;
+  a.nsteps = ms.nsteps;
+  a.done = ctx->d_done;
+  a.x = ctx->dX;
+  a.y = ctx->dY;
+  a.p = ctx->dP;
+  a.a_rep = ms.a_rep;
+  a.dbg = dev_knob("SBG_STEP_DBG");
+  a.ident = PhaseIdent{-0.0f, 1.0f, -1.0f};
+  static unsigned long long* trace = nullptr;  // dev knob SBG_RES_TRACE (pair 0, CTA 0, group 0)
+  if (dev_knob("SBG_RES_TRACE")) {
+    if (!trace) CK(cudaMalloc(&trace, sizeof(unsigned long long) * 8 * 2 * 4096));
+    CK(cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 8 * 2 * 4096, ctx->stream));
+    a.trace = trace;
+    a.nsteps = std::min(a.nsteps, 4096);
+  }
+  CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * (ms.rpad / Cfg::NR), ctx->stream));
+  kern<<<2 * num_mp * a.rb_per_group, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(maps, a);
+  CK(cudaGetLastError());
+  ++ctx->launches;
+  if (a.trace) {
+    std::vector<unsigned long long> h(size_t(8 * 2 * a.nsteps));
+    CK(cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    FILE* f = fopen("gpurun_out/res_trace.txt", "w");
+    if (f) {
+      for (int st = 0; st < a.nsteps; ++st)
+        for (int X = 0; X < 2; ++X) {
+          const unsigned long long* r = &h[size_t((st * 2 + X) * 8)];
+          fprintf(f, "%d %d %llu %llu %llu %llu 0 0 0\n", st, X, r[0], r[1], r[2], r[3]);
         }
       fclose(f);
     }
@@ -442,6 +499,15 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
           if (!rcr)
             rcr = encode_2d(ctx, &rm.Gout[par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ par ^ 1], gvalid, R,
                             gdim(ctx), 128, ResCfg<RES_STAGES>::NR, CU_TENSOR_MAP_SWIZZLE_NONE);
+        }
+        if (rcr) return rcr;
+        TmaMaps& rm2 = ctx->rmaps2_sign[cur];
+        rm2 = ctx->maps_sign[cur];
+        for (int par = 0; par < 2 && !rcr; ++par) {
+          rcr = encode_2d_u8(ctx, &rm2.Gin[par], ctx->dG[cur ^ par], ctx->npad, rpad, 128, Res2Cfg<RES2_STAGES>::B_HALF);
+          if (!rcr)
+            rcr = encode_2d(ctx, &rm2.Gout[par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ par ^ 1], gvalid, R,
+                            gdim(ctx), 128, Res2Cfg<RES2_STAGES>::NR, CU_TENSOR_MAP_SWIZZLE_NONE);
         }
         if (rcr) return rcr;
       }
@@ -1188,6 +1254,7 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
         // default for sign variants: state resident in TMEM (step_resident.cuh); SBG_RESIDENT=0
         // selects the streaming kernels (dev comparison)
         switch (dev_knob("SBG_RES_CFG")) {
+          case 10: rc = launch_resident_pp(ctx, ctx->rmaps2_sign[cur], a); break;
           case 1: rc = launch_resident<16, 8>(ctx, ctx->rmaps_sign[cur], a); break;
           case 2: rc = launch_resident<8, 8>(ctx, ctx->rmaps_sign[cur], a); break;
           case 3: rc = launch_resident<8, 4>(ctx, ctx->rmaps_sign[cur], a); break;

@@ -226,22 +226,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
         for (int s = 0; s < args.nsteps; ++s, ++lt) {
           ptx::mbar_wait(tempty, (lt & 1) ^ 1u);
           ptx::tc_fence_after();
-          for (int kb = 0; kb < KB; ++kb) {
+          // two K-stages per issue round: the per-round handshake (wait, fence, elect,
+          // commit) costs ~260 cycles, more than 4 MMAs of N <= 128 (tools/dev/pipe_probe.cu)
+          for (int kb = 0; kb < KB; kb += 2) {
+            const int st0 = stage;
             ptx::mbar_wait(full_bar(stage), ph);
-            ptx::tc_fence_after();
-            if (ptx::elect_one()) {
-              const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + stage * Cfg::A_BYTES);
-              const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + stage * Cfg::B_BYTES);
-#pragma unroll
-              for (int k = 0; k < Cfg::BK / 32; ++k)
-                ptx::mma_i8_pair(tmem_base, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
-              ptx::mma_commit_pair_mc(empty_bar(stage), 0x3);
-            }
-            __syncwarp();
             if (++stage == STAGES) {
               stage = 0;
               ph ^= 1u;
             }
+            const int st1 = stage;
+            const bool two = kb + 1 < KB;
+            if (two) {
+              ptx::mbar_wait(full_bar(stage), ph);
+              if (++stage == STAGES) {
+                stage = 0;
+                ph ^= 1u;
+              }
+            }
+            ptx::tc_fence_after();
+            if (ptx::elect_one()) {
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                if (u == 1 && !two) break;
+                const int st = u ? st1 : st0;
+                const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + st * Cfg::A_BYTES);
+                const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + st * Cfg::B_BYTES);
+#pragma unroll
+                for (int k = 0; k < Cfg::BK / 32; ++k)
+                  ptx::mma_i8_pair(tmem_base, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | u | k) != 0);
+                ptx::mma_commit_pair_mc(empty_bar(st), 0x3);
+              }
+            }
+            __syncwarp();
           }
           if (ptx::elect_one()) ptx::mma_commit_pair_mc(tfull, 0x3);
           __syncwarp();
