@@ -1270,7 +1270,11 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
           case 4: rc = launch_multistep_pair<1, NPAIR_SIGN, 2, 5>(ctx, ctx->maps_sign[cur], a); break;
           case 5: rc = launch_multistep_pair<1, NPAIR_SIGN, 3, 8, 8>(ctx, ctx->maps_sign_cw8[cur], a); break;
           case 6: rc = launch_multistep_pair<1, NPAIR_SIGN, 2, 10, 8>(ctx, ctx->maps_sign_cw8[cur], a); break;
-          default: rc = launch_multistep_pair<1, NPAIR_SIGN, 3, 4>(ctx, ctx->maps_sign[cur], a);
+          case 7: rc = launch_multistep_pair<1, NPAIR_SIGN, 5, 2>(ctx, ctx->maps_sign[cur], a); break;
+          case 8: rc = launch_multistep_pair<1, NPAIR_SIGN, 3, 4>(ctx, ctx->maps_sign[cur], a); break;
+          // non-resident sign launches are the large-N J-streaming regime (C5: 2.06 ms/step,
+          // 0.79 of HBM with 5 operand stages vs 2.29 ms with 3)
+          default: rc = launch_multistep_pair<1, NPAIR_SIGN, 5, 2>(ctx, ctx->maps_sign[cur], a);
         }
       } else {
         switch (pair_ok ? knob : -1) {
