@@ -16,6 +16,7 @@
 #include <cstring>
 #include <string>
 #include <unordered_set>
+#include <utility>
 #include <vector>
 
 #include "../../include/sbgpu.h"
@@ -208,6 +209,25 @@ bool getenv_is0(const char* name) {
   return e && atoi(e) == 0;
 }
 
+// Persistent multi-step kernels spin on counters released by other CTAs of the
+// same launch, so every CTA must be resident at once: launch them cooperatively
+// (the driver then never co-schedules them partially next to another kernel).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_persistent(void (*kern)(KArgs...), int grid, int block, int smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(block));
+  cfg.dynamicSmemBytes = size_t(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 template <int NP, int BN, int ST, int NB, int NA = 1>
 int launch_multistep(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& a) {
   using Cfg = TmaStepCfg<NP, BN, ST, NB, NA>;
@@ -217,8 +237,7 @@ int launch_multistep(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& a) 
   // persistent: one CTA per SM (all must be co-resident for the dependency walk)
   const int grid = int(std::min<int64_t>(tiles, ctx->sms));
   if (!ctx->sharded) CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * a.num_n, ctx->stream));
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(maps, a);
-  CK(cudaGetLastError());
+  CK(launch_persistent(kern, grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream, maps, a));
   ++ctx->launches;
   if (ctx->sharded) ctx->done_base += uint32_t(a.nsteps * a.num_m_total);
   return SBG_OK;
@@ -233,8 +252,7 @@ int launch_multistep_pair(sbg_ctx* ctx, const TmaMaps& maps, MultiStepArgs a) {
   const int64_t pair_tiles = int64_t(a.num_m / 2) * a.num_n * a.nsteps;
   const int grid = 2 * int(std::min<int64_t>(pair_tiles, ctx->sms / 2));
   CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * a.num_n, ctx->stream));
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(maps, a);
-  CK(cudaGetLastError());
+  CK(launch_persistent(kern, grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream, maps, a));
   ++ctx->launches;
   return SBG_OK;
 }
@@ -283,8 +301,7 @@ int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms) 
     a.nsteps = std::min(a.nsteps, 4096);
   }
   CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * num_n, ctx->stream));
-  kern<<<2 * num_mp * a.rb_per_group, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(maps, a);
-  CK(cudaGetLastError());
+  CK(launch_persistent(kern, 2 * num_mp * a.rb_per_group, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream, maps, a));
   ++ctx->launches;
   if (a.trace) {
     std::vector<unsigned long long> h(size_t(8 * 2 * a.nsteps));
@@ -337,8 +354,7 @@ int launch_resident_pp(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& m
     a.nsteps = std::min(a.nsteps, 4096);
   }
   CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * (ms.rpad / Cfg::NR), ctx->stream));
-  kern<<<2 * num_mp * a.rb_per_group, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(maps, a);
-  CK(cudaGetLastError());
+  CK(launch_persistent(kern, 2 * num_mp * a.rb_per_group, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream, maps, a));
   ++ctx->launches;
   if (a.trace) {
     std::vector<unsigned long long> h(size_t(8 * 2 * a.nsteps));
