@@ -47,12 +47,25 @@ int main(int argc, char** argv) {
   for (auto& r : batch) energies.push_back(r.energy);
   const auto st = sbgpu::success_probability(energies, best.energy);
   const auto tts = sbgpu::time_to_solution(1.0, sbgpu::success_from_counts(500, 1000, 0.0));
+  // device spectra: numerical auto_tune at n = 64 hits the 10 n cap (ConvergenceError, as the
+  // reference at this size); with a larger cap both ends converge
+  int convergence_caught = 0;
+  try {
+    s.auto_tune(sbgpu::TuneMode::numerical);
+  } catch (const sbgpu::ConvergenceError& e) {
+    convergence_caught = e.last_estimate().iterations > 0 ? 1 : 0;
+  }
+  const auto est = s.extreme_eigenvalues(1e-6, 100000);
+  const auto tw = s.auto_tune(sbgpu::TuneMode::wigner, 1.25);
   std::printf("{\"n\": %zu, \"R\": %zu, \"c\": %.17g, \"dt\": %.17g, \"energies\": [", n, R, tuning.c, tuning.dt);
   for (std::size_t r = 0; r < R; ++r) std::printf("%s%.1f", r ? ", " : "", batch[r].energy);
   std::printf("], \"cuts\": [");
   for (std::size_t r = 0; r < R; ++r) std::printf("%s%lld", r ? ", " : "", *batch[r].cut);
-  std::printf("], \"best_energy\": %.1f, \"best_seed\": %llu, \"p_s\": %.17g, \"tts_mid\": %.17g, \"invalid_caught\": %d}\n",
-              best.energy, static_cast<unsigned long long>(best.config_echo.seed), st.p_s, tts.tts_s, invalid_caught);
+  std::printf("], \"best_energy\": %.1f, \"best_seed\": %llu, \"p_s\": %.17g, \"tts_mid\": %.17g, \"invalid_caught\": %d,"
+              " \"convergence_caught\": %d, \"lambda_max\": %.17g, \"lambda_min\": %.17g, \"iterations\": %zu,"
+              " \"wigner_c\": %.17g}\n",
+              best.energy, static_cast<unsigned long long>(best.config_echo.seed), st.p_s, tts.tts_s, invalid_caught,
+              convergence_caught, est.lambda_max, est.lambda_min, est.iterations, tw.c);
   (void)argc;
   (void)argv;
   return 0;

@@ -4,6 +4,8 @@ import os
 import subprocess
 
 import numpy as np
+
+import oracle
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -30,6 +32,7 @@ def test_cpp_api_matches_oracle(tmp_path, orc):
     build(exe)
     out = json.loads(subprocess.run([exe], check=True, capture_output=True, text=True).stdout)
     assert out["invalid_caught"] == 2
+    assert out["convergence_caught"] == 1
     n, R = out["n"], out["R"]
     # rebuild the demo's instance and run the fp32 mirror from the same seeded states
     J = np.zeros((n, n), np.int8)
@@ -49,3 +52,8 @@ def test_cpp_api_matches_oracle(tmp_path, orc):
     W = -int(np.triu(J.astype(np.int64), 1).sum())
     assert out["cuts"] == [int((W - v) // 2) for v in e]
     assert abs(out["tts_mid"] - 6.6439) < 1e-3
+    assert out["wigner_c"] == out["c"]
+    if oracle.ref_available():  # device power iteration == the reference's, bitwise
+        rc, want, _, _ = oracle.ref().extreme_eigenvalues(J.astype(np.float64), 1e-6, 100000)
+        assert rc == 0 and (out["lambda_max"], out["lambda_min"], out["iterations"]) == (
+            want["lambda_max"], want["lambda_min"], want["iterations"])
