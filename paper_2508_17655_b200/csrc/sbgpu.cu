@@ -28,7 +28,6 @@
 #include "step_tma.cuh"
 #include "step_pair.cuh"
 #include "step_resident.cuh"
-#include "step_resident2.cuh"
 
 using namespace sbg;
 
@@ -62,6 +61,19 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 bool is_sign_variant(int v) { return v == SBG_DSB || v == SBG_GDSB; }
+
+using PFN_writeValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_writeValue32 get_write_value32() {
+  static PFN_writeValue32 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_writeValue32>(p);
+  }
+  return fn;
+}
 
 }  // namespace
 
@@ -97,7 +109,6 @@ struct sbg_ctx {
   TmaMaps fxmaps_sign[2], fxmaps_planes[2];  // real-J kernels (B tiles of 64 / 32 rows)
   TmaMaps maps_sign_cw8[2];                  // sign pair kernel with 8-replica state chunks
   TmaMaps rmaps_sign[2];                     // resident-state pair kernel (B halves of 64 rows, G tile stores)
-  TmaMaps rmaps2_sign[2];                    // ping-pong resident kernel (B halves of 32 rows, 64-row G tiles)
   unsigned long long* dE2p = nullptr;    // real-J readout: per-J-plane partial E2 [FX_NA][rpad]
   // CSR: spin-major working copies [npad][rp] and the ping-pong gathered operand (q int32 / sign int8)
   float *dXs = nullptr, *dYs = nullptr, *dPs = nullptr;
@@ -113,9 +124,13 @@ struct sbg_ctx {
   float* d_arep = nullptr;  // optional per-replica A (sbg_set_replica_a), honoured by gbsb/gdsb
   int64_t arep_n = 0;
   uint32_t* d_done = nullptr;            // per replica-block tile counters of the multi-step kernel
+  uint32_t* d_ready = nullptr;           // per replica-group "state copied" flags (sbg_run pipelining)
+  int64_t ready_cap = 0;
   int g_cur = 0;
   int g_mode = 0;  // 0 stale, 1 sign plane valid in dG[g_cur], 4 planes valid
   cudaEvent_t ev[8];
+  cudaStream_t cstream = nullptr;  // host->device copies overlapped with the resident kernel (sbg_run)
+  cudaEvent_t evc[3];
   float last_advance_ms = 0.f;
 
   int fail(int code, const char* fmt, ...) {
@@ -259,7 +274,12 @@ int launch_multistep_pair(sbg_ctx* ctx, const TmaMaps& maps, MultiStepArgs a) {
 
 // Resident-state pair kernel (step_resident.cuh): sign variants, dense int8 J.
 constexpr int RES_STAGES = 8;
-constexpr int RES2_STAGES = 8;
+
+bool resident_ok(const sbg_ctx* ctx);
+bool use_resident(const sbg_ctx* ctx, int variant) {
+  // default for sign variants on dense int8 J; SBG_RESIDENT=0 selects the streaming kernels (dev)
+  return (variant == SBG_DSB || variant == SBG_GDSB) && !getenv_is0("SBG_RESIDENT") && resident_ok(ctx);
+}
 
 bool resident_ok(const sbg_ctx* ctx) {
   const int64_t num_mp = ctx->npad / 256;
@@ -267,8 +287,17 @@ bool resident_ok(const sbg_ctx* ctx) {
          num_mp <= ctx->sms / 2 && ctx->rpad % ResCfg<RES_STAGES>::NR == 0;
 }
 
+// Replica-group geometry of the resident kernel: 128-replica blocks, num_mp pairs per block,
+// as many blocks per group as CTA pairs fit (one CTA per SM).
+void resident_geometry(const sbg_ctx* ctx, int64_t npad, int64_t rpad, int* rb_per_group, int* groups) {
+  const int num_mp = int(npad / 256), num_n = int(rpad / ResCfg<RES_STAGES>::NR);
+  *rb_per_group = std::min(num_n, (ctx->sms / 2) / num_mp);
+  *groups = (num_n + *rb_per_group - 1) / *rb_per_group;
+}
+
 template <int EPI, int CH, int ST = RES_STAGES>
-int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms) {
+int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms, int group0 = 0, int ngroups = -1,
+                    const uint32_t* ready = nullptr) {
   using Cfg = ResCfg<ST, EPI, CH>;
   auto kern = gsb_resident_pair_kernel<ST, EPI, CH>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
@@ -280,8 +309,10 @@ int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms) 
   a.rpad = ms.rpad;
   a.num_m = ms.npad / Cfg::BM;
   const int num_mp = ms.npad / 256, num_n = ms.rpad / Cfg::NR;
-  a.rb_per_group = std::min(num_n, (ctx->sms / 2) / num_mp);
-  a.groups = (num_n + a.rb_per_group - 1) / a.rb_per_group;
+  int total_groups = 0;
+  resident_geometry(ctx, ms.npad, ms.rpad, &a.rb_per_group, &total_groups);
+  a.group0 = group0;
+  a.groups = ngroups < 0 ? total_groups - group0 : ngroups;
   a.k = ms.k;
   a.M = ms.M;
   a.t_begin = ms.t_begin;
@@ -292,6 +323,7 @@ int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms) 
   a.p = ctx->dP;
   a.a_rep = ms.a_rep;
   a.ident = PhaseIdent{-0.0f, 1.0f, -1.0f};
+  a.ready = ready;
   a.dbg = dev_knob("SBG_STEP_DBG");
   static unsigned long long* trace = nullptr;  // dev knob SBG_RES_TRACE: stamps of pair 0, group 0
   if (dev_knob("SBG_RES_TRACE")) {
@@ -313,59 +345,6 @@ int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms) 
         for (int c = 0; c < 2; ++c) {
           const unsigned long long* r = &h[size_t((s * 2 + c) * 8)];
           fprintf(f, "%d %d %llu %llu %llu %llu %llu %llu %llu\n", s, c, r[0], r[1], r[2], r[3], r[4], r[5], r[6]);
-        }
-      fclose(f);
-    }
-  }
-  return SBG_OK;
-}
-
-template <int ST = RES2_STAGES>
-int launch_resident_pp(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms) {
-  using Cfg = Res2Cfg<ST>;
-  auto kern = gsb_resident_pp_kernel<ST>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
-  ResidentArgs a;
-  std::memset(&a, 0, sizeof a);
-  a.n = ms.n;
-  a.npad = ms.npad;
-  a.R = ms.R;
-  a.rpad = ms.rpad;
-  a.num_m = ms.npad / Cfg::BM;
-  const int num_mp = ms.npad / 256, num_pb = ms.rpad / (2 * Cfg::NR);  // 128-replica pair blocks
-  a.rb_per_group = std::min(num_pb, (ctx->sms / 2) / num_mp);
-  a.groups = (num_pb + a.rb_per_group - 1) / a.rb_per_group;
-  a.k = ms.k;
-  a.M = ms.M;
-  a.t_begin = ms.t_begin;
-  a.nsteps = ms.nsteps;
-  a.done = ctx->d_done;
-  a.x = ctx->dX;
-  a.y = ctx->dY;
-  a.p = ctx->dP;
-  a.a_rep = ms.a_rep;
-  a.dbg = dev_knob("SBG_STEP_DBG");
-  a.ident = PhaseIdent{-0.0f, 1.0f, -1.0f};
-  static unsigned long long* trace = nullptr;  // dev knob SBG_RES_TRACE (pair 0, CTA 0, group 0)
-  if (dev_knob("SBG_RES_TRACE")) {
-    if (!trace) CK(cudaMalloc(&trace, sizeof(unsigned long long) * 8 * 2 * 4096));
-    CK(cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 8 * 2 * 4096, ctx->stream));
-    a.trace = trace;
-    a.nsteps = std::min(a.nsteps, 4096);
-  }
-  CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * (ms.rpad / Cfg::NR), ctx->stream));
-  CK(launch_persistent(kern, 2 * num_mp * a.rb_per_group, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream, maps, a));
-  ++ctx->launches;
-  if (a.trace) {
-    std::vector<unsigned long long> h(size_t(8 * 2 * a.nsteps));
-    CK(cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    FILE* f = fopen("gpurun_out/res_trace.txt", "w");
-    if (f) {
-      for (int st = 0; st < a.nsteps; ++st)
-        for (int X = 0; X < 2; ++X) {
-          const unsigned long long* r = &h[size_t((st * 2 + X) * 8)];
-          fprintf(f, "%d %d %llu %llu %llu %llu 0 0 0\n", st, X, r[0], r[1], r[2], r[3]);
         }
       fclose(f);
     }
@@ -515,15 +494,6 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
           if (!rcr)
             rcr = encode_2d(ctx, &rm.Gout[par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ par ^ 1], gvalid, R,
                             gdim(ctx), 128, ResCfg<RES_STAGES>::NR, CU_TENSOR_MAP_SWIZZLE_NONE);
-        }
-        if (rcr) return rcr;
-        TmaMaps& rm2 = ctx->rmaps2_sign[cur];
-        rm2 = ctx->maps_sign[cur];
-        for (int par = 0; par < 2 && !rcr; ++par) {
-          rcr = encode_2d_u8(ctx, &rm2.Gin[par], ctx->dG[cur ^ par], ctx->npad, rpad, 128, Res2Cfg<RES2_STAGES>::B_HALF);
-          if (!rcr)
-            rcr = encode_2d(ctx, &rm2.Gout[par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ par ^ 1], gvalid, R,
-                            gdim(ctx), 128, Res2Cfg<RES2_STAGES>::NR, CU_TENSOR_MAP_SWIZZLE_NONE);
         }
         if (rcr) return rcr;
       }
@@ -806,6 +776,11 @@ int sbg_create(int device, sbg_ctx** out) {
     return SBG_ERR_CUDA;
   }
   for (auto& e : ctx->ev) cudaEventCreate(&e);
+  for (auto& e : ctx->evc) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  if (cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking) != cudaSuccess) {
+    sbg_destroy(ctx);
+    return SBG_ERR_CUDA;
+  }
   *out = ctx;
   return SBG_OK;
 }
@@ -816,11 +791,17 @@ void sbg_destroy(sbg_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   free_state(ctx);
   cudaFree(ctx->d_arep);
+  cudaFree(ctx->d_ready);
   cudaFree(ctx->dJ);
   cudaFree(ctx->d_rowptr);
   cudaFree(ctx->d_col);
   cudaFree(ctx->d_val);
   for (auto& e : ctx->ev) cudaEventDestroy(e);
+  for (auto& e : ctx->evc) cudaEventDestroy(e);
+  if (ctx->cstream) {
+    cudaStreamSynchronize(ctx->cstream);
+    cudaStreamDestroy(ctx->cstream);
+  }
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -1215,11 +1196,13 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
     }
   } else {
     const int need = sign ? 1 : NPL;
-    if (ctx->g_mode != need) {
+    const bool resident = use_resident(ctx, prm->variant);
+    if (ctx->g_mode != need && !resident) {  // the resident kernel publishes its own G_0
       rc = prep_planes(ctx, ctx->dX, ctx->dG[ctx->g_cur], need, ctx->R, ctx->rpad, /*into_global=*/true);
       if (rc) return rc;
       ctx->g_mode = need;
     }
+    if (resident) ctx->g_mode = 1;
     const bool fx = ctx->kind == KIND_DENSE_FX;
     const int bn = fx ? (sign ? BN_FX_SIGN : BN_FX_PLANE) : (sign ? BN_SIGN : BN_PLANE);
     const int64_t T = (ctx->npad / 128) * (ctx->rpad / bn);
@@ -1266,11 +1249,10 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
         // real-valued J: 3 J planes x (sign | 4 x-planes), single-CTA
         rc = sign ? launch_multistep<1, BN_FX_SIGN, 2, 4, FX_NA>(ctx, ctx->fxmaps_sign[cur], a)
                   : launch_multistep<NPL, BN_FX_PLANE, 2, 3, FX_NA>(ctx, ctx->fxmaps_planes[cur], a);
-      } else if (sign && !getenv_is0("SBG_RESIDENT") && resident_ok(ctx)) {
+      } else if (resident) {
         // default for sign variants: state resident in TMEM (step_resident.cuh); SBG_RESIDENT=0
         // selects the streaming kernels (dev comparison)
         switch (dev_knob("SBG_RES_CFG")) {
-          case 10: rc = launch_resident_pp(ctx, ctx->rmaps2_sign[cur], a); break;
           case 1: rc = launch_resident<16, 8>(ctx, ctx->rmaps_sign[cur], a); break;
           case 2: rc = launch_resident<8, 8>(ctx, ctx->rmaps_sign[cur], a); break;
           case 3: rc = launch_resident<8, 4>(ctx, ctx->rmaps_sign[cur], a); break;
@@ -1492,10 +1474,13 @@ int sbg_fields_fixed(sbg_ctx* ctx, int64_t R, const float* x, float* F) {
 }
 
 static int run_tail(sbg_ctx* ctx, const sbg_params* prm, float* x_final, int8_t* spins, double* energy,
-                    int64_t* best_index, sbg_timing* timing) {
-  CK(cudaEventRecord(ctx->ev[3], ctx->stream));
-  int rc = sbg_advance(ctx, prm, 0, prm->steps);
-  if (rc) return rc;
+                    int64_t* best_index, sbg_timing* timing, bool advanced = false) {
+  int rc;
+  if (!advanced) {
+    CK(cudaEventRecord(ctx->ev[3], ctx->stream));
+    rc = sbg_advance(ctx, prm, 0, prm->steps);
+    if (rc) return rc;
+  }
   CK(cudaEventRecord(ctx->ev[4], ctx->stream));
   rc = spins ? sbg_readout(ctx, spins, energy, best_index, nullptr)
              : sbg_readout_best(ctx, nullptr, nullptr, best_index, energy);
@@ -1525,12 +1510,91 @@ static int run_tail(sbg_ctx* ctx, const sbg_params* prm, float* x_final, int8_t*
   return SBG_OK;
 }
 
+// sbg_run on the resident kernel: the replica groups are independent for the whole
+// run, so group g's M steps start as soon as ITS x0/y0 rows have arrived; the copies of
+// the later groups (copy stream) overlap the earlier groups' steps.
+static int run_pipelined(sbg_ctx* ctx, const sbg_params* prm, int64_t R, const float* x0, const float* y0,
+                         float* x_final, int8_t* spins, double* energy, int64_t* best_index, sbg_timing* timing) {
+  int rc;
+  auto write_value = get_write_value32();
+  int rbg = 0, groups = 0;
+  resident_geometry(ctx, ctx->npad, ctx->rpad, &rbg, &groups);
+  if (!write_value || groups < 2) {  // nothing to overlap: plain path
+    rc = sbg_set_state(ctx, R, x0, y0, nullptr);
+    if (rc) return rc;
+    CK(cudaEventRecord(ctx->ev[7], ctx->stream));
+    return run_tail(ctx, prm, x_final, spins, energy, best_index, timing);
+  }
+  if (ctx->ready_cap < groups) {
+    cudaFree(ctx->d_ready);
+    ctx->d_ready = nullptr;
+    CK(cudaMalloc(&ctx->d_ready, sizeof(uint32_t) * groups));
+    ctx->ready_cap = groups;
+  }
+  CK(cudaMemsetAsync(ctx->d_ready, 0, sizeof(uint32_t) * groups, ctx->stream));
+  const size_t cnt = size_t(ctx->rpad) * ctx->npad;
+  fill_f32_kernel<<<grid_for(ctx, cnt, 256), 256, 0, ctx->stream>>>(ctx->dP, cnt, 1.0f);
+  CK(cudaGetLastError());
+  ++ctx->launches;
+  const int64_t Rg = int64_t(rbg) * ResCfg<RES_STAGES>::NR;
+  const size_t pitch = sizeof(float) * ctx->npad, w = sizeof(float) * ctx->n;
+  CK(cudaEventRecord(ctx->evc[0], ctx->stream));  // state buffers and flags (re)initialised
+  const bool honours_a = prm->variant == SBG_GDSB;
+  MultiStepArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.n = int32_t(ctx->n);
+  a.npad = int32_t(ctx->npad);
+  a.R = int32_t(ctx->R);
+  a.rpad = int32_t(ctx->rpad);
+  a.k.a = honours_a ? float(prm->a) : 0.0f;
+  a.k.c = float(prm->c);
+  a.k.dt = float(prm->dt);
+  a.M = prm->steps;
+  a.t_begin = 0;
+  a.nsteps = int32_t(prm->steps);
+  a.a_rep = (honours_a && ctx->d_arep && ctx->arep_n == ctx->R) ? ctx->d_arep : nullptr;
+  const int cur = ctx->g_cur;
+  // the kernel is enqueued BEFORE the copies: each replica group waits on its flag, so
+  // pageable host buffers (synchronous staging on the host) still overlap the steps
+  CK(cudaEventRecord(ctx->ev[7], ctx->stream));
+  CK(cudaEventRecord(ctx->ev[3], ctx->stream));
+  CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+  rc = launch_resident<16, 4>(ctx, ctx->rmaps_sign[cur], a, 0, groups, ctx->d_ready);
+  if (rc) return rc;
+  CK(cudaStreamWaitEvent(ctx->cstream, ctx->evc[0], 0));
+  for (int g = 0; g < groups; ++g) {
+    const int64_t r0 = g * Rg, rows = std::min<int64_t>(R - r0, Rg);
+    if (rows > 0) {
+      CK(cudaMemcpy2DAsync(ctx->dX + r0 * ctx->npad, pitch, x0 + r0 * ctx->n, w, w, rows, cudaMemcpyHostToDevice,
+                           ctx->cstream));
+      CK(cudaMemcpy2DAsync(ctx->dY + r0 * ctx->npad, pitch, y0 + r0 * ctx->n, w, w, rows, cudaMemcpyHostToDevice,
+                           ctx->cstream));
+    }
+    // stream-ordered flag write (with the default memory barrier: the rows are visible first)
+    if (write_value(reinterpret_cast<CUstream>(ctx->cstream), reinterpret_cast<CUdeviceptr>(ctx->d_ready + g), 1u,
+                    0) != CUDA_SUCCESS)
+      return ctx->fail(SBG_ERR_CUDA, "cuStreamWriteValue32 failed");
+  }
+  CK(cudaEventRecord(ctx->evc[1], ctx->cstream));
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->evc[1], 0));
+  ctx->g_cur = cur ^ int(prm->steps & 1);
+  ctx->g_mode = 1;
+  CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+  return run_tail(ctx, prm, x_final, spins, energy, best_index, timing, /*advanced=*/true);
+}
+
 int sbg_run(sbg_ctx* ctx, const sbg_params* prm, int64_t R, const float* x0, const float* y0, float* x_final,
             int8_t* spins, double* energy, int64_t* best_index, sbg_timing* timing) {
   CHECK_CTX(ctx);
   int rc = validate_params(ctx, prm);
   if (rc) return rc;
   CK(cudaSetDevice(ctx->device));
+  if (x0 && y0 && R >= 1 && use_resident(ctx, prm->variant) && !dev_knob("SBG_RUN_SERIAL")) {
+    CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+    rc = ensure_state(ctx, R);  // resident_ok depends on the padded replica count
+    if (rc) return rc;
+    if (resident_ok(ctx)) return run_pipelined(ctx, prm, R, x0, y0, x_final, spins, energy, best_index, timing);
+  }
   CK(cudaEventRecord(ctx->ev[2], ctx->stream));
   rc = sbg_set_state(ctx, R, x0, y0, nullptr);
   if (rc) return rc;

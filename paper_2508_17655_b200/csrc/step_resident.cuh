@@ -89,7 +89,8 @@ struct ResidentArgs {
   int32_t n, npad, R, rpad;
   int32_t num_m;     // 128-spin blocks (CTAs per replica block)
   int32_t rb_per_group;
-  int32_t groups;
+  int32_t group0;    // first replica group of this launch
+  int32_t groups;    // groups in this launch
   PhaseConsts k;
   uint64_t M, t_begin;
   int32_t nsteps;
@@ -97,6 +98,8 @@ struct ResidentArgs {
   float *x, *y, *p;  // replica-major [rpad][npad]
   const float* a_rep;
   PhaseIdent ident;           // -0, 1, -1 (runtime identity operands of gsb_phase2)
+  const uint32_t* ready;      // optional [groups]: nonzero once group g's x, y rows have landed (sbg_run
+                              // overlaps the host->device copies of later groups with earlier groups)
   int32_t dbg;                // dev only: 1 = skip J loads after the first step, 2 = no G dependency wait
   unsigned long long* trace;  // dev only: per-step %globaltimer stamps of pair 0 (null = off)
 };
@@ -168,7 +171,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
     int stage = 0;
     uint32_t ph = 0;
     const uint64_t keep = ptx::policy_evict_last();
-    for (int g = 0; g < args.groups; ++g) {
+    for (int g = args.group0; g < args.group0 + args.groups; ++g) {
       const int n_blk = g * args.rb_per_group + rbk;
       if (n_blk >= num_n) break;
       for (int s = 0; s < args.nsteps; ++s) {
@@ -191,7 +194,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
             ph0 ^= 1u;
           }
         }
-        if (args.dbg != 2) dep::wait_block(args.done, n_blk, 0u, static_cast<uint32_t>(s * args.num_m));
+        // G_t of block n is complete when all num_m CTAs released it (the launch's
+        // initial G_0 is published by the kernel itself at group start: one release each)
+        if (args.dbg != 2) dep::wait_block(args.done, n_blk, 0u, static_cast<uint32_t>((s + 1) * args.num_m));
         if (args.trace && pair == 0 && g == 0 && lane == 0) args.trace[(s * 2 + cr) * 8 + 0] = gtimer();
         const CUtensorMap* gin = &maps.Gin[s & 1];
         for (int kb = 0; kb < KB; ++kb) {
@@ -220,7 +225,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
       int stage = 0;
       uint32_t ph = 0;
       int lt = 0;
-      for (int g = 0; g < args.groups; ++g) {
+      for (int g = args.group0; g < args.group0 + args.groups; ++g) {
         const int n_blk = g * args.rb_per_group + rbk;
         if (n_blk >= num_n) break;
         for (int s = 0; s < args.nsteps; ++s, ++lt) {
@@ -273,10 +278,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
     const uint32_t tempty_leader = ptx::mapa(tempty, 0);
     const int epi_tid = threadIdx.x - 128;
     int lt = 0;
-    for (int g = 0; g < args.groups; ++g) {
+    for (int g = args.group0; g < args.group0 + args.groups; ++g) {
       const int n_blk = g * args.rb_per_group + rbk;
       if (n_blk >= num_n) break;
       const int r0 = n_blk * Cfg::NR + h * Cfg::COLS_PER_WARP;  // this thread's first replica
+      if (args.ready)
+        while (dep::ld_acquire_sys(args.ready + g) == 0) __nanosleep(256);
       // load the block's state into TMEM (coalesced: a warp reads 32 consecutive spins)
 #pragma unroll 1
       for (int half = 0; half < Cfg::COLS_PER_WARP / 16; ++half) {
@@ -292,8 +299,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
         ptx::tmem_st16(t_lane + Cfg::COL_X + col, vx);
         ptx::tmem_st16(t_lane + Cfg::COL_Y + col, vy);
         ptx::tmem_st16(t_lane + Cfg::COL_P + col, vp);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          g_tile[(col + j) * Cfg::BM + q * 32 + lane] = static_cast<uint8_t>(sgn8(__uint_as_float(vx[j])));
       }
       ptx::tmem_st_wait();
+      // publish G_0 = sgn(x) of this block (the B operand of the launch's first step:
+      // the buffer Gout[1] writes), so a launch needs no host-side preparation
+      ptx::fence_proxy_async_smem();
+      ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);
+      if (epi_tid == 0) {
+        ptx::tma_store_2d(&maps.Gout[1], g_base, i0, n_blk * Cfg::NR);
+        ptx::bulk_commit();
+        ptx::bulk_wait0();
+        dep::fence_proxy_async_global();
+        __threadfence();
+        dep::release_add(args.done + n_blk, 1u);
+      }
+      ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);
       for (int s = 0; s < args.nsteps; ++s, ++lt) {
         PhaseConsts k = args.k;
         k.inv = __frcp_rn(static_cast<float>(args.M - (args.t_begin + static_cast<uint64_t>(s))));

@@ -349,3 +349,24 @@ def test_resident_kernel_equals_streaming(solver, orc, n, R, variant, monkeypatc
     for a, b in zip(out[:2], out[2:]):
         assert all((u.view(np.uint32) == v.view(np.uint32)).all() for u, v in zip(a[:3], b[:3]))
         assert (a[3] == b[3]).all() and a[4] == b[4]
+
+
+@pytest.mark.parametrize("n,R", [(2000, 8192), (500, 2500)])
+def test_run_pipelined_copies_equal_serial(solver, orc, n, R, monkeypatch):
+    """sbg_run on the resident kernel overlaps each replica group's host->device copy with
+    the earlier groups' steps (stream-ordered ready flags): results bitwise equal to the
+    serial copy-then-run path, for pageable host buffers too."""
+    from paper_2508_17655_b200 import SolverConfig, TuningResult, Variant
+
+    solver.gen_random_dense(n, 2)
+    x0, y0, _ = orc.init_small_uniform(n, R, master=3)
+    c = 1 / (2 * np.sqrt(n))
+    cfg = SolverConfig(variant=Variant.gdsb, steps=23, dt=1.25, c=c, a=0.2)
+    out = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SBG_RUN_SERIAL", flag)
+        b = solver.run_batch(cfg, TuningResult(c=c, dt=1.25), R, x0=x0, y0=y0, want_x=True)
+        out.append(b)
+    assert (out[0].x_final.view(np.uint32) == out[1].x_final.view(np.uint32)).all()
+    assert (out[0].energies == out[1].energies).all() and out[0].best_index == out[1].best_index
+    assert (out[0].spins == out[1].spins).all()
