@@ -108,7 +108,8 @@ struct sbg_ctx {
   TmaMaps pmaps_planes[2];               // pair kernel, fixed-point planes (B half = 32 rows)
   TmaMaps fxmaps_sign[2], fxmaps_planes[2];  // real-J kernels (B tiles of 64 / 32 rows)
   TmaMaps maps_sign_cw8[2];                  // sign pair kernel with 8-replica state chunks
-  TmaMaps rmaps_sign[2];                     // resident-state pair kernel (B halves of 64 rows, G tile stores)
+  TmaMaps rmaps_sign[2];                     // resident-state pair kernel, NR 128 (B halves of 64 rows)
+  TmaMaps rmaps160_sign[2];                  // resident-state pair kernel, NR 160 (B halves of 80 rows)
   unsigned long long* dE2p = nullptr;    // real-J readout: per-J-plane partial E2 [FX_NA][rpad]
   // CSR: spin-major working copies [npad][rp] and the ping-pong gathered operand (q int32 / sign int8)
   float *dXs = nullptr, *dYs = nullptr, *dPs = nullptr;
@@ -284,22 +285,35 @@ bool use_resident(const sbg_ctx* ctx, int variant) {
 bool resident_ok(const sbg_ctx* ctx) {
   const int64_t num_mp = ctx->npad / 256;
   return ctx->kind == KIND_DENSE_I8 && !ctx->sharded && ctx->npad % 256 == 0 && num_mp >= 1 &&
-         num_mp <= ctx->sms / 2 && ctx->rpad % ResCfg<RES_STAGES>::NR == 0;
+         num_mp <= ctx->sms / 2;
 }
 
 // Replica-group geometry of the resident kernel: 128-replica blocks, num_mp pairs per block,
 // as many blocks per group as CTA pairs fit (one CTA per SM).
-void resident_geometry(const sbg_ctx* ctx, int64_t npad, int64_t rpad, int* rb_per_group, int* groups) {
-  const int num_mp = int(npad / 256), num_n = int(rpad / ResCfg<RES_STAGES>::NR);
+constexpr int RES_NR = 160;  // replicas per pair block of the default resident kernel (p in smem)
+constexpr int RES_NR_STAGES = 4;
+
+void resident_geometry(const sbg_ctx* ctx, int64_t npad, int64_t rpad, int* rb_per_group, int* groups,
+                       int nr = RES_NR) {
+  const int num_mp = int(npad / 256), num_n = int((rpad + nr - 1) / nr);
   *rb_per_group = std::min(num_n, (ctx->sms / 2) / num_mp);
   *groups = (num_n + *rb_per_group - 1) / *rb_per_group;
 }
 
-template <int EPI, int CH, int ST = RES_STAGES>
+// NR 160 (p in shared memory) only pays when it cuts the number of sequential replica
+// groups (C2: 8 -> 6); otherwise NR 128 is faster per group.
+int resident_nr(const sbg_ctx* ctx) {
+  int rb = 0, g128 = 0, g160 = 0;
+  resident_geometry(ctx, ctx->npad, ctx->rpad, &rb, &g128, 128);
+  resident_geometry(ctx, ctx->npad, ctx->rpad, &rb, &g160, RES_NR);
+  return g160 < g128 ? RES_NR : 128;
+}
+
+template <int EPI, int CH, int ST = RES_STAGES, int NR = 128>
 int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms, int group0 = 0, int ngroups = -1,
                     const uint32_t* ready = nullptr) {
-  using Cfg = ResCfg<ST, EPI, CH>;
-  auto kern = gsb_resident_pair_kernel<ST, EPI, CH>;
+  using Cfg = ResCfg<ST, EPI, CH, NR>;
+  auto kern = gsb_resident_pair_kernel<ST, EPI, CH, NR>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
   ResidentArgs a;
   std::memset(&a, 0, sizeof a);
@@ -308,9 +322,9 @@ int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms, 
   a.R = ms.R;
   a.rpad = ms.rpad;
   a.num_m = ms.npad / Cfg::BM;
-  const int num_mp = ms.npad / 256, num_n = ms.rpad / Cfg::NR;
+  const int num_mp = ms.npad / 256, num_n = (ms.rpad + Cfg::NR - 1) / Cfg::NR;
   int total_groups = 0;
-  resident_geometry(ctx, ms.npad, ms.rpad, &a.rb_per_group, &total_groups);
+  resident_geometry(ctx, ms.npad, ms.rpad, &a.rb_per_group, &total_groups, Cfg::NR);
   a.group0 = group0;
   a.groups = ngroups < 0 ? total_groups - group0 : ngroups;
   a.k = ms.k;
@@ -486,14 +500,21 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
       ctx->fxmaps_planes[cur] = ctx->maps_planes[cur];
       {
         TmaMaps& rm = ctx->rmaps_sign[cur];
+        TmaMaps& rm160 = ctx->rmaps160_sign[cur];
         rm = ctx->maps_sign[cur];
+        rm160 = ctx->maps_sign[cur];
         const uint64_t gvalid = uint64_t(ctx->sharded ? ctx->n_global : ctx->n);
         int rcr = SBG_OK;
         for (int par = 0; par < 2 && !rcr; ++par) {
-          rcr = encode_2d_u8(ctx, &rm.Gin[par], ctx->dG[cur ^ par], ctx->npad, rpad, 128, ResCfg<RES_STAGES>::B_HALF);
+          rcr = encode_2d_u8(ctx, &rm.Gin[par], ctx->dG[cur ^ par], ctx->npad, rpad, 128, 64);
           if (!rcr)
             rcr = encode_2d(ctx, &rm.Gout[par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ par ^ 1], gvalid, R,
-                            gdim(ctx), 128, ResCfg<RES_STAGES>::NR, CU_TENSOR_MAP_SWIZZLE_NONE);
+                            gdim(ctx), 128, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
+          // B boxes of the last block may pass rpad: rows beyond are zero-filled (padding columns)
+          if (!rcr) rcr = encode_2d_u8(ctx, &rm160.Gin[par], ctx->dG[cur ^ par], ctx->npad, rpad, 128, RES_NR / 2);
+          if (!rcr)
+            rcr = encode_2d(ctx, &rm160.Gout[par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ par ^ 1], gvalid, R,
+                            gdim(ctx), 128, RES_NR, CU_TENSOR_MAP_SWIZZLE_NONE);
         }
         if (rcr) return rcr;
       }
@@ -1258,7 +1279,11 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
           case 3: rc = launch_resident<8, 4>(ctx, ctx->rmaps_sign[cur], a); break;
           case 6: rc = launch_resident<16, 4, 6>(ctx, ctx->rmaps_sign[cur], a); break;
           case 7: rc = launch_resident<16, 4, 7>(ctx, ctx->rmaps_sign[cur], a); break;
-          default: rc = launch_resident<16, 4>(ctx, ctx->rmaps_sign[cur], a);
+          case 11: rc = launch_resident<16, 4>(ctx, ctx->rmaps_sign[cur], a); break;  // NR 128, all in TMEM
+          default:
+            rc = resident_nr(ctx) == RES_NR
+                     ? launch_resident<16, 4, RES_NR_STAGES, RES_NR>(ctx, ctx->rmaps160_sign[cur], a)
+                     : launch_resident<16, 4>(ctx, ctx->rmaps_sign[cur], a);
         }
       } else if (sign) {
         switch (pair_ok ? knob : -1) {
@@ -1518,7 +1543,8 @@ static int run_pipelined(sbg_ctx* ctx, const sbg_params* prm, int64_t R, const f
   int rc;
   auto write_value = get_write_value32();
   int rbg = 0, groups = 0;
-  resident_geometry(ctx, ctx->npad, ctx->rpad, &rbg, &groups);
+  const int nr = resident_nr(ctx);
+  resident_geometry(ctx, ctx->npad, ctx->rpad, &rbg, &groups, nr);
   if (!write_value || groups < 2) {  // nothing to overlap: plain path
     rc = sbg_set_state(ctx, R, x0, y0, nullptr);
     if (rc) return rc;
@@ -1536,7 +1562,7 @@ static int run_pipelined(sbg_ctx* ctx, const sbg_params* prm, int64_t R, const f
   fill_f32_kernel<<<grid_for(ctx, cnt, 256), 256, 0, ctx->stream>>>(ctx->dP, cnt, 1.0f);
   CK(cudaGetLastError());
   ++ctx->launches;
-  const int64_t Rg = int64_t(rbg) * ResCfg<RES_STAGES>::NR;
+  const int64_t Rg = int64_t(rbg) * nr;
   const size_t pitch = sizeof(float) * ctx->npad, w = sizeof(float) * ctx->n;
   CK(cudaEventRecord(ctx->evc[0], ctx->stream));  // state buffers and flags (re)initialised
   const bool honours_a = prm->variant == SBG_GDSB;
@@ -1559,7 +1585,9 @@ static int run_pipelined(sbg_ctx* ctx, const sbg_params* prm, int64_t R, const f
   CK(cudaEventRecord(ctx->ev[7], ctx->stream));
   CK(cudaEventRecord(ctx->ev[3], ctx->stream));
   CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-  rc = launch_resident<16, 4>(ctx, ctx->rmaps_sign[cur], a, 0, groups, ctx->d_ready);
+  rc = nr == RES_NR
+           ? launch_resident<16, 4, RES_NR_STAGES, RES_NR>(ctx, ctx->rmaps160_sign[cur], a, 0, groups, ctx->d_ready)
+           : launch_resident<16, 4>(ctx, ctx->rmaps_sign[cur], a, 0, groups, ctx->d_ready);
   if (rc) return rc;
   CK(cudaStreamWaitEvent(ctx->cstream, ctx->evc[0], 0));
   for (int g = 0; g < groups; ++g) {

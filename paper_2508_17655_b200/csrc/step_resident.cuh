@@ -63,26 +63,33 @@ __device__ __forceinline__ void tmem_st<8>(uint32_t taddr, const uint32_t (&v)[8
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 }  // namespace ptx
 
-template <int STAGES_, int EPI_WARPS_ = 16, int CH_ = 4>
+// NR_ = replicas per pair block (UMMA N). 128: F, x, y, p all in TMEM (4 x 128 columns);
+// 160: F, x, y in TMEM (480 columns) and p in shared memory ([160][128] fp32, 80 KB),
+// which takes 25% more replicas per group (fewer sequential groups per step).
+template <int STAGES_, int EPI_WARPS_ = 16, int CH_ = 4, int NR_ = 128>
 struct ResCfg {
   static constexpr int BM = 128;                 // spins per CTA
   static constexpr int BK = 128;                 // K bytes per stage
-  static constexpr int NR = 128;                 // replicas per pair block (UMMA N)
+  static constexpr int NR = NR_;                 // replicas per pair block (UMMA N)
+  static constexpr bool P_SMEM = 4 * NR > 512;   // p leaves TMEM
   static constexpr int B_HALF = NR / 2;          // B rows staged per CTA
   static constexpr int A_BYTES = BM * BK;        // 16 KB
-  static constexpr int B_BYTES = B_HALF * BK;    // 8 KB
+  static constexpr int B_BYTES = B_HALF * BK;    // 8 KB (NR 128)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = STAGES_;
-  static constexpr int G_BYTES = NR * BM;        // G_{t+1} tile [128 replicas][128 spins]
+  static constexpr int G_BYTES = NR * BM;        // G_{t+1} tile [NR replicas][128 spins]
+  static constexpr int P_BYTES = P_SMEM ? NR * BM * 4 : 0;
   static constexpr int EPI_WARPS = EPI_WARPS_;           // 4 per TMEM lane quadrant x column groups
   static constexpr int COLS_PER_WARP = NR / (EPI_WARPS / 4);
   static constexpr int CH = CH_;                           // replica columns per TMEM load chunk
   static constexpr int CHUNKS = COLS_PER_WARP / CH;
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static constexpr int NUM_BARS = 2 * STAGES + 2;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + G_BYTES + 1024 + 8 * NUM_BARS + 64;
-  static constexpr uint32_t COL_X = 128, COL_Y = 256, COL_P = 384;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + G_BYTES + P_BYTES + 1024 + 8 * NUM_BARS + 64;
+  static constexpr uint32_t COL_X = NR, COL_Y = 2 * NR, COL_P = 3 * NR;  // COL_P unused when P_SMEM
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+  static_assert(NR % 16 == 0 && NR <= 256 && COLS_PER_WARP % 8 == 0, "UMMA N / epilogue chunking");
+  static_assert((P_SMEM ? 3 : 4) * NR <= 512, "TMEM columns");
 };
 
 struct ResidentArgs {
@@ -110,10 +117,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-template <int STAGES_, int EPI_WARPS_, int CH_>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_WARPS_, CH_>::THREADS, 1)
+template <int STAGES_, int EPI_WARPS_, int CH_, int NR_>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_WARPS_, CH_, NR_>::THREADS, 1)
     gsb_resident_pair_kernel(const __grid_constant__ TmaMaps maps, const ResidentArgs args) {
-  using Cfg = ResCfg<STAGES_, EPI_WARPS_, CH_>;
+  using Cfg = ResCfg<STAGES_, EPI_WARPS_, CH_, NR_>;
   constexpr int CH = Cfg::CH;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -124,7 +131,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
   const uint32_t b_base = base + STAGES * Cfg::A_BYTES;
   const uint32_t g_base = base + STAGES * Cfg::STAGE_BYTES;
   uint8_t* g_tile = smem + STAGES * Cfg::STAGE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(g_tile + Cfg::G_BYTES);
+  float* p_smem = reinterpret_cast<float*>(g_tile + Cfg::G_BYTES);  // [NR][128] when P_SMEM
+  uint64_t* bars = reinterpret_cast<uint64_t*>(g_tile + Cfg::G_BYTES + Cfg::P_BYTES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
   auto bar = [&](int i) { return ptx::smem_u32(bars + i); };
   auto full_bar = [&](int s) { return bar(s); };
@@ -160,7 +168,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
   const int m_blk = 2 * mp + static_cast<int>(cr);
   const int i0 = m_blk * Cfg::BM;
   const int KB = args.npad / Cfg::BK;
-  const int num_n = args.rpad / Cfg::NR;
+  const int num_n = (args.rpad + Cfg::NR - 1) / Cfg::NR;  // the last block may pass rpad (NR 160)
 
   if (warp == 0) {  // ------------------------------------------------ operand producer
     if (ptx::elect_one()) {
@@ -174,6 +182,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
     for (int g = args.group0; g < args.group0 + args.groups; ++g) {
       const int n_blk = g * args.rb_per_group + rbk;
       if (n_blk >= num_n) break;
+      const int b_row0 = n_blk * Cfg::NR + static_cast<int>(cr) * Cfg::B_HALF;  // this CTA's B rows
       for (int s = 0; s < args.nsteps; ++s) {
         // J does not depend on the step: the first PRE stages' J tiles are requested
         // before waiting for G_t (expect_tx without arrive), the G halves after.
@@ -208,8 +217,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
             if (!pre && !skipJ)
               ptx::tma_load_2d_pair_hint(a_base + stage * Cfg::A_BYTES, &maps.J, fb, kb * Cfg::BK, m_blk * Cfg::BM,
                                          keep);
-            ptx::tma_load_2d_pair_hint(b_base + stage * Cfg::B_BYTES, gin, fb, kb * Cfg::BK,
-                                       n_blk * Cfg::NR + static_cast<int>(cr) * Cfg::B_HALF, keep);
+            ptx::tma_load_2d_pair_hint(b_base + stage * Cfg::B_BYTES, gin, fb, kb * Cfg::BK, b_row0, keep);
           }
           __syncwarp();
           if (++stage == STAGES) {
@@ -286,21 +294,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
         while (dep::ld_acquire_sys(args.ready + g) == 0) __nanosleep(256);
       // load the block's state into TMEM (coalesced: a warp reads 32 consecutive spins)
 #pragma unroll 1
-      for (int half = 0; half < Cfg::COLS_PER_WARP / 16; ++half) {
-        uint32_t vx[16], vy[16], vp[16];
+      for (int c8 = 0; c8 < Cfg::COLS_PER_WARP / 8; ++c8) {
+        uint32_t vx[8], vy[8], vp[8];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const size_t off = static_cast<size_t>(r0 + half * 16 + j) * args.npad + spin;
-          vx[j] = __float_as_uint(args.x[off]);
-          vy[j] = __float_as_uint(args.y[off]);
-          vp[j] = __float_as_uint(args.p[off]);
+        for (int j = 0; j < 8; ++j) {
+          const int r = r0 + c8 * 8 + j;
+          const size_t off = static_cast<size_t>(r) * args.npad + spin;
+          const bool in = r < args.rpad;  // the last block of a non-dividing NR may pass rpad
+          vx[j] = in ? __float_as_uint(args.x[off]) : 0u;
+          vy[j] = in ? __float_as_uint(args.y[off]) : 0u;
+          vp[j] = in ? __float_as_uint(args.p[off]) : 0u;
         }
-        const uint32_t col = h * Cfg::COLS_PER_WARP + half * 16;
-        ptx::tmem_st16(t_lane + Cfg::COL_X + col, vx);
-        ptx::tmem_st16(t_lane + Cfg::COL_Y + col, vy);
-        ptx::tmem_st16(t_lane + Cfg::COL_P + col, vp);
+        const uint32_t col = h * Cfg::COLS_PER_WARP + c8 * 8;
+        ptx::tmem_st<8>(t_lane + Cfg::COL_X + col, vx);
+        ptx::tmem_st<8>(t_lane + Cfg::COL_Y + col, vy);
+        if constexpr (Cfg::P_SMEM) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
+          for (int j = 0; j < 8; ++j) p_smem[(col + j) * Cfg::BM + q * 32 + lane] = __uint_as_float(vp[j]);
+        } else {
+          ptx::tmem_st<8>(t_lane + Cfg::COL_P + col, vp);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
           g_tile[(col + j) * Cfg::BM + q * 32 + lane] = static_cast<uint8_t>(sgn8(__uint_as_float(vx[j])));
       }
       ptx::tmem_st_wait();
@@ -326,14 +341,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
         __syncwarp();
         ptx::tc_fence_after();
         if (args.trace && pair == 0 && g == 0 && epi_tid == 0) args.trace[(s * 2 + cr) * 8 + 1] = gtimer();
-        // 4 chunks of 8 replica columns; TMEM loads of chunk c+1 overlap the math of chunk c
+        // chunks of CH replica columns; TMEM loads of chunk c+1 overlap the math of chunk c
         uint32_t bf[2][CH], bx[2][CH], by[2][CH], bp[2][CH];
         auto ld_chunk = [&](int c, int b) {
           const uint32_t col = h * Cfg::COLS_PER_WARP + c * CH;
           ptx::tmem_ld<CH>(t_lane + col, bf[b]);
           ptx::tmem_ld<CH>(t_lane + Cfg::COL_X + col, bx[b]);
           ptx::tmem_ld<CH>(t_lane + Cfg::COL_Y + col, by[b]);
-          ptx::tmem_ld<CH>(t_lane + Cfg::COL_P + col, bp[b]);
+          if constexpr (Cfg::P_SMEM) {
+#pragma unroll
+            for (int j = 0; j < CH; ++j) bp[b][j] = __float_as_uint(p_smem[(col + j) * Cfg::BM + q * 32 + lane]);
+          } else {
+            ptx::tmem_ld<CH>(t_lane + Cfg::COL_P + col, bp[b]);
+          }
         };
         auto wait_chunk = [&](int b) {
           ptx::tmem_ld_wait();
@@ -372,7 +392,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
             const uint32_t col = h * Cfg::COLS_PER_WARP + c * CH;
             ptx::tmem_st<CH>(t_lane + Cfg::COL_X + col, bx[b]);
             ptx::tmem_st<CH>(t_lane + Cfg::COL_Y + col, by[b]);
-            ptx::tmem_st<CH>(t_lane + Cfg::COL_P + col, bp[b]);
+            if constexpr (Cfg::P_SMEM) {
+#pragma unroll
+              for (int j = 0; j < CH; ++j) p_smem[(col + j) * Cfg::BM + q * 32 + lane] = __uint_as_float(bp[b][j]);
+            } else {
+              ptx::tmem_st<CH>(t_lane + Cfg::COL_P + col, bp[b]);
+            }
             if (c + 1 < Cfg::CHUNKS) wait_chunk(b ^ 1);
           }
         };
@@ -387,7 +412,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader);
-        // publish G_{t+1} for this CTA's 128 spins x 128 replicas
+        // publish G_{t+1} for this CTA's 128 spins x NR replicas
         ptx::fence_proxy_async_smem();
         ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);
         if (epi_tid == 0) {
@@ -404,16 +429,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
       }
       // write the block's state back
 #pragma unroll 1
-      for (int half = 0; half < Cfg::COLS_PER_WARP / 16; ++half) {
-        const uint32_t col = h * Cfg::COLS_PER_WARP + half * 16;
-        uint32_t vx[16], vy[16], vp[16];
-        ptx::tmem_ld<16>(t_lane + Cfg::COL_X + col, vx);
-        ptx::tmem_ld<16>(t_lane + Cfg::COL_Y + col, vy);
-        ptx::tmem_ld<16>(t_lane + Cfg::COL_P + col, vp);
+      for (int c8 = 0; c8 < Cfg::COLS_PER_WARP / 8; ++c8) {
+        const uint32_t col = h * Cfg::COLS_PER_WARP + c8 * 8;
+        uint32_t vx[8], vy[8], vp[8];
+        ptx::tmem_ld<8>(t_lane + Cfg::COL_X + col, vx);
+        ptx::tmem_ld<8>(t_lane + Cfg::COL_Y + col, vy);
+        if constexpr (!Cfg::P_SMEM) ptx::tmem_ld<8>(t_lane + Cfg::COL_P + col, vp);
         ptx::tmem_ld_wait();
+        if constexpr (Cfg::P_SMEM) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const size_t off = static_cast<size_t>(r0 + half * 16 + j) * args.npad + spin;
+          for (int j = 0; j < 8; ++j) vp[j] = __float_as_uint(p_smem[(col + j) * Cfg::BM + q * 32 + lane]);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int r = r0 + c8 * 8 + j;
+          if (r >= args.rpad) continue;
+          const size_t off = static_cast<size_t>(r) * args.npad + spin;
           args.x[off] = __uint_as_float(vx[j]);
           args.y[off] = __uint_as_float(vy[j]);
           args.p[off] = __uint_as_float(vp[j]);
