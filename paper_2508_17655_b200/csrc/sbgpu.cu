@@ -1580,15 +1580,10 @@ static int run_pipelined(sbg_ctx* ctx, const sbg_params* prm, int64_t R, const f
   a.nsteps = int32_t(prm->steps);
   a.a_rep = (honours_a && ctx->d_arep && ctx->arep_n == ctx->R) ? ctx->d_arep : nullptr;
   const int cur = ctx->g_cur;
-  // the kernel is enqueued BEFORE the copies: each replica group waits on its flag, so
-  // pageable host buffers (synchronous staging on the host) still overlap the steps
-  CK(cudaEventRecord(ctx->ev[7], ctx->stream));
-  CK(cudaEventRecord(ctx->ev[3], ctx->stream));
-  CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-  rc = nr == RES_NR
-           ? launch_resident<16, 4, RES_NR_STAGES, RES_NR>(ctx, ctx->rmaps160_sign[cur], a, 0, groups, ctx->d_ready)
-           : launch_resident<16, 4>(ctx, ctx->rmaps_sign[cur], a, 0, groups, ctx->d_ready);
-  if (rc) return rc;
+  // Copies (second stream) are enqueued BEFORE the launch, which waits on nothing but each
+  // group's flag: with pinned buffers the copies of later groups overlap the earlier groups'
+  // steps; with pageable buffers, a serialising profiler or CUDA_LAUNCH_BLOCKING the copies
+  // simply complete first (the kernel can never wait on work queued behind it).
   CK(cudaStreamWaitEvent(ctx->cstream, ctx->evc[0], 0));
   for (int g = 0; g < groups; ++g) {
     const int64_t r0 = g * Rg, rows = std::min<int64_t>(R - r0, Rg);
@@ -1603,6 +1598,13 @@ static int run_pipelined(sbg_ctx* ctx, const sbg_params* prm, int64_t R, const f
                     0) != CUDA_SUCCESS)
       return ctx->fail(SBG_ERR_CUDA, "cuStreamWriteValue32 failed");
   }
+  CK(cudaEventRecord(ctx->ev[7], ctx->stream));
+  CK(cudaEventRecord(ctx->ev[3], ctx->stream));
+  CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+  rc = nr == RES_NR
+           ? launch_resident<16, 4, RES_NR_STAGES, RES_NR>(ctx, ctx->rmaps160_sign[cur], a, 0, groups, ctx->d_ready)
+           : launch_resident<16, 4>(ctx, ctx->rmaps_sign[cur], a, 0, groups, ctx->d_ready);
+  if (rc) return rc;
   CK(cudaEventRecord(ctx->evc[1], ctx->cstream));
   CK(cudaStreamWaitEvent(ctx->stream, ctx->evc[1], 0));
   ctx->g_cur = cur ^ int(prm->steps & 1);
