@@ -295,8 +295,8 @@ def run_ours(args):
         "roofline": {"bound": "tensor", "achieved": tops, "peak": i8_peak, "unit": "TFLOP/s",
                      "frac": tops / i8_peak, "traffic": traffic, "peak_source": i8_src,
                      "op_type": "int8 tensor ops (2 per MAC), 2*N*N*R per step",
-                     "kernel": "gsb_resident_pair_kernel<4,16,4,160> (all timed steps in one launch; x, y in TMEM, "
-                               "p in shared memory)",
+                     "kernel": "gsb_resident_pair_kernel<5,16,4,160> (all timed steps in one launch; x, y in TMEM, "
+                               "p split TMEM / shared memory)",
                      "streaming_equivalent": {"bytes_per_step": stream_bytes,
                                               "gbs": stream_bytes / (ms_per_step / 1e3) / 1e9,
                                               "hbm_peak_gbs": hbm_peak, "hbm_peak_source": hbm_src,

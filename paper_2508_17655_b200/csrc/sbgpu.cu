@@ -291,7 +291,7 @@ bool resident_ok(const sbg_ctx* ctx) {
 // Replica-group geometry of the resident kernel: 128-replica blocks, num_mp pairs per block,
 // as many blocks per group as CTA pairs fit (one CTA per SM).
 constexpr int RES_NR = 160;  // replicas per pair block of the default resident kernel (p in smem)
-constexpr int RES_NR_STAGES = 4;
+constexpr int RES_NR_STAGES = 5;  // 32 of the 160 p columns stay in TMEM: room for a 5th ring stage
 
 void resident_geometry(const sbg_ctx* ctx, int64_t npad, int64_t rpad, int* rb_per_group, int* groups,
                        int nr = RES_NR) {
@@ -338,6 +338,8 @@ int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms, 
   a.a_rep = ms.a_rep;
   a.ident = PhaseIdent{-0.0f, 1.0f, -1.0f};
   a.ready = ready;
+  a.gbuf[0] = ctx->dG[ctx->g_cur ^ 1];  // step parity 0 writes the other buffer (as Gout[0])
+  a.gbuf[1] = ctx->dG[ctx->g_cur];
   a.dbg = dev_knob("SBG_STEP_DBG");
   static unsigned long long* trace = nullptr;  // dev knob SBG_RES_TRACE: stamps of pair 0, group 0
   if (dev_knob("SBG_RES_TRACE")) {

@@ -66,19 +66,23 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 // NR_ = replicas per pair block (UMMA N). 128: F, x, y, p all in TMEM (4 x 128 columns);
 // 160: F, x, y in TMEM (480 columns) and p in shared memory ([160][128] fp32, 80 KB),
 // which takes 25% more replicas per group (fewer sequential groups per step).
-template <int STAGES_, int EPI_WARPS_ = 16, int CH_ = 4, int NR_ = 128>
+template <int STAGES_, int EPI_WARPS_ = 16, int CH_ = 4, int NR_ = 128, bool GD_ = false>
 struct ResCfg {
   static constexpr int BM = 128;                 // spins per CTA
   static constexpr int BK = 128;                 // K bytes per stage
   static constexpr int NR = NR_;                 // replicas per pair block (UMMA N)
-  static constexpr bool P_SMEM = 4 * NR > 512;   // p leaves TMEM
+  static constexpr bool P_SMEM = 4 * NR > 512;   // part of p leaves TMEM
+  static constexpr int P_T = P_SMEM ? 512 - 3 * NR : NR;  // p columns kept in TMEM (the rest in smem)
   static constexpr int B_HALF = NR / 2;          // B rows staged per CTA
   static constexpr int A_BYTES = BM * BK;        // 16 KB
   static constexpr int B_BYTES = B_HALF * BK;    // 8 KB (NR 128)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = STAGES_;
-  static constexpr int G_BYTES = NR * BM;        // G_{t+1} tile [NR replicas][128 spins]
-  static constexpr int P_BYTES = P_SMEM ? NR * BM * 4 : 0;
+  // G_{t+1} staging tile [NR][128] for one TMA store; G_DIRECT: the epilogue stores the sign
+  // bytes straight to global memory instead (frees the tile's shared memory for a ring stage)
+  static constexpr bool G_DIRECT = GD_;
+  static constexpr int G_BYTES = G_DIRECT ? 0 : NR * BM;
+  static constexpr int P_BYTES = (NR - P_T) * BM * 4;
   static constexpr int EPI_WARPS = EPI_WARPS_;           // 4 per TMEM lane quadrant x column groups
   static constexpr int COLS_PER_WARP = NR / (EPI_WARPS / 4);
   static constexpr int CH = CH_;                           // replica columns per TMEM load chunk
@@ -86,10 +90,14 @@ struct ResCfg {
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static constexpr int NUM_BARS = 2 * STAGES + 2;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + G_BYTES + P_BYTES + 1024 + 8 * NUM_BARS + 64;
-  static constexpr uint32_t COL_X = NR, COL_Y = 2 * NR, COL_P = 3 * NR;  // COL_P unused when P_SMEM
+  static constexpr uint32_t COL_X = NR, COL_Y = 2 * NR, COL_P = 3 * NR;  // p: [COL_P, COL_P + P_T)
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static_assert(NR % 16 == 0 && NR <= 256 && COLS_PER_WARP % 8 == 0, "UMMA N / epilogue chunking");
-  static_assert((P_SMEM ? 3 : 4) * NR <= 512, "TMEM columns");
+  static_assert(3 * NR + P_T <= 512 && P_T % 8 == 0, "TMEM columns");
+  // p of a warp's column block: its first PT_W columns in TMEM, the rest in shared memory
+  // (balanced over the column groups so no epilogue warp does more TMEM traffic)
+  static constexpr int PT_W = P_T / (EPI_WARPS / 4);
+  static_assert(PT_W % 8 == 0 || !P_SMEM, "p split granularity");
 };
 
 struct ResidentArgs {
@@ -105,6 +113,7 @@ struct ResidentArgs {
   float *x, *y, *p;  // replica-major [rpad][npad]
   const float* a_rep;
   PhaseIdent ident;           // -0, 1, -1 (runtime identity operands of gsb_phase2)
+  uint8_t* gbuf[2];           // G_DIRECT: output G buffer of step parity 0/1 ([rpad][npad] bytes)
   const uint32_t* ready;      // optional [groups]: nonzero once group g's x, y rows have landed (sbg_run
                               // overlaps the host->device copies of later groups with earlier groups)
   int32_t dbg;                // dev only: 1 = skip J loads after the first step, 2 = no G dependency wait
@@ -131,7 +140,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
   const uint32_t b_base = base + STAGES * Cfg::A_BYTES;
   const uint32_t g_base = base + STAGES * Cfg::STAGE_BYTES;
   uint8_t* g_tile = smem + STAGES * Cfg::STAGE_BYTES;
-  float* p_smem = reinterpret_cast<float*>(g_tile + Cfg::G_BYTES);  // [NR][128] when P_SMEM
+  float* p_smem = reinterpret_cast<float*>(g_tile + Cfg::G_BYTES);  // p columns >= P_T: [NR - P_T][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(g_tile + Cfg::G_BYTES + Cfg::P_BYTES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
   auto bar = [&](int i) { return ptx::smem_u32(bars + i); };
@@ -285,6 +294,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
     const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
     const uint32_t tempty_leader = ptx::mapa(tempty, 0);
     const int epi_tid = threadIdx.x - 128;
+    // G_{t+1} byte of (replica column col of the block, this thread's spin): smem tile, or
+    // straight to the global buffer of step parity par (bounded like the TMA store: R x n)
+    auto put_g = [&](int n_blk, int col, int par, float xv) {
+      if constexpr (Cfg::G_DIRECT) {
+        const int r = n_blk * Cfg::NR + col;
+        if (r < args.R && spin < args.n)
+          args.gbuf[par][static_cast<size_t>(r) * args.npad + spin] = static_cast<uint8_t>(sgn8(xv));
+      } else {
+        g_tile[col * Cfg::BM + (spin - i0)] = static_cast<uint8_t>(sgn8(xv));
+      }
+    };
+    // publish this CTA's G chunk of block n_blk for the consumers of step parity par
+    auto publish = [&](int n_blk, int par) {
+      if constexpr (Cfg::G_DIRECT) {
+        __threadfence();
+        ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);
+        if (epi_tid == 0) {
+          dep::fence_proxy_async_global();
+          dep::release_add(args.done + n_blk, 1u);
+        }
+      } else {
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);
+        if (epi_tid == 0) {
+          ptx::tma_store_2d(&maps.Gout[par], g_base, i0, n_blk * Cfg::NR);
+          ptx::bulk_commit();
+          ptx::bulk_wait0();
+          dep::fence_proxy_async_global();
+          __threadfence();
+          dep::release_add(args.done + n_blk, 1u);
+        }
+        ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);  // g_tile reusable
+      }
+    };
     int lt = 0;
     for (int g = args.group0; g < args.group0 + args.groups; ++g) {
       const int n_blk = g * args.rb_per_group + rbk;
@@ -308,30 +351,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
         const uint32_t col = h * Cfg::COLS_PER_WARP + c8 * 8;
         ptx::tmem_st<8>(t_lane + Cfg::COL_X + col, vx);
         ptx::tmem_st<8>(t_lane + Cfg::COL_Y + col, vy);
-        if constexpr (Cfg::P_SMEM) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) p_smem[(col + j) * Cfg::BM + q * 32 + lane] = __uint_as_float(vp[j]);
+        if (c8 * 8 < Cfg::PT_W) {
+          ptx::tmem_st<8>(t_lane + Cfg::COL_P + h * Cfg::PT_W + c8 * 8, vp);
         } else {
-          ptx::tmem_st<8>(t_lane + Cfg::COL_P + col, vp);
+          const int ps = h * (Cfg::COLS_PER_WARP - Cfg::PT_W) + c8 * 8 - Cfg::PT_W;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) p_smem[(ps + j) * Cfg::BM + q * 32 + lane] = __uint_as_float(vp[j]);
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          g_tile[(col + j) * Cfg::BM + q * 32 + lane] = static_cast<uint8_t>(sgn8(__uint_as_float(vx[j])));
+        for (int j = 0; j < 8; ++j) put_g(n_blk, col + j, 1, __uint_as_float(vx[j]));
       }
       ptx::tmem_st_wait();
       // publish G_0 = sgn(x) of this block (the B operand of the launch's first step:
       // the buffer Gout[1] writes), so a launch needs no host-side preparation
-      ptx::fence_proxy_async_smem();
-      ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);
-      if (epi_tid == 0) {
-        ptx::tma_store_2d(&maps.Gout[1], g_base, i0, n_blk * Cfg::NR);
-        ptx::bulk_commit();
-        ptx::bulk_wait0();
-        dep::fence_proxy_async_global();
-        __threadfence();
-        dep::release_add(args.done + n_blk, 1u);
-      }
-      ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);
+      publish(n_blk, 1);
       for (int s = 0; s < args.nsteps; ++s, ++lt) {
         PhaseConsts k = args.k;
         k.inv = __frcp_rn(static_cast<float>(args.M - (args.t_begin + static_cast<uint64_t>(s))));
@@ -348,11 +381,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
           ptx::tmem_ld<CH>(t_lane + col, bf[b]);
           ptx::tmem_ld<CH>(t_lane + Cfg::COL_X + col, bx[b]);
           ptx::tmem_ld<CH>(t_lane + Cfg::COL_Y + col, by[b]);
-          if constexpr (Cfg::P_SMEM) {
-#pragma unroll
-            for (int j = 0; j < CH; ++j) bp[b][j] = __float_as_uint(p_smem[(col + j) * Cfg::BM + q * 32 + lane]);
+          if (c * CH < Cfg::PT_W) {
+            ptx::tmem_ld<CH>(t_lane + Cfg::COL_P + h * Cfg::PT_W + c * CH, bp[b]);
           } else {
-            ptx::tmem_ld<CH>(t_lane + Cfg::COL_P + col, bp[b]);
+            const int ps = h * (Cfg::COLS_PER_WARP - Cfg::PT_W) + c * CH - Cfg::PT_W;
+#pragma unroll
+            for (int j = 0; j < CH; ++j) bp[b][j] = __float_as_uint(p_smem[(ps + j) * Cfg::BM + q * 32 + lane]);
           }
         };
         auto wait_chunk = [&](int b) {
@@ -385,18 +419,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
               by[b][j + 1] = __float_as_uint(y1);
               bp[b][j] = __float_as_uint(p0);
               bp[b][j + 1] = __float_as_uint(p1);
-              uint8_t* gp = g_tile + (h * Cfg::COLS_PER_WARP + c * CH + j) * Cfg::BM + q * 32 + lane;
-              gp[0] = static_cast<uint8_t>(sgn8(x0));
-              gp[Cfg::BM] = static_cast<uint8_t>(sgn8(x1));
+              put_g(n_blk, h * Cfg::COLS_PER_WARP + c * CH + j, s & 1, x0);
+              put_g(n_blk, h * Cfg::COLS_PER_WARP + c * CH + j + 1, s & 1, x1);
             }
             const uint32_t col = h * Cfg::COLS_PER_WARP + c * CH;
             ptx::tmem_st<CH>(t_lane + Cfg::COL_X + col, bx[b]);
             ptx::tmem_st<CH>(t_lane + Cfg::COL_Y + col, by[b]);
-            if constexpr (Cfg::P_SMEM) {
-#pragma unroll
-              for (int j = 0; j < CH; ++j) p_smem[(col + j) * Cfg::BM + q * 32 + lane] = __uint_as_float(bp[b][j]);
+            if (c * CH < Cfg::PT_W) {
+              ptx::tmem_st<CH>(t_lane + Cfg::COL_P + h * Cfg::PT_W + c * CH, bp[b]);
             } else {
-              ptx::tmem_st<CH>(t_lane + Cfg::COL_P + col, bp[b]);
+              const int ps = h * (Cfg::COLS_PER_WARP - Cfg::PT_W) + c * CH - Cfg::PT_W;
+#pragma unroll
+              for (int j = 0; j < CH; ++j) p_smem[(ps + j) * Cfg::BM + q * 32 + lane] = __uint_as_float(bp[b][j]);
             }
             if (c + 1 < Cfg::CHUNKS) wait_chunk(b ^ 1);
           }
@@ -413,19 +447,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader);
         // publish G_{t+1} for this CTA's 128 spins x NR replicas
-        ptx::fence_proxy_async_smem();
-        ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);
-        if (epi_tid == 0) {
-          if (args.trace && pair == 0 && g == 0) args.trace[(s * 2 + cr) * 8 + 2] = gtimer();
-          ptx::tma_store_2d(&maps.Gout[s & 1], g_base, i0, n_blk * Cfg::NR);
-          ptx::bulk_commit();
-          ptx::bulk_wait0();
-          dep::fence_proxy_async_global();
-          __threadfence();
-          dep::release_add(args.done + n_blk, 1u);
-          if (args.trace && pair == 0 && g == 0) args.trace[(s * 2 + cr) * 8 + 3] = gtimer();
-        }
-        ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);  // g_tile reusable
+        if (tr) args.trace[(s * 2 + cr) * 8 + 2] = gtimer();
+        publish(n_blk, s & 1);
+        if (tr) args.trace[(s * 2 + cr) * 8 + 3] = gtimer();
       }
       // write the block's state back
 #pragma unroll 1
@@ -434,11 +458,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
         uint32_t vx[8], vy[8], vp[8];
         ptx::tmem_ld<8>(t_lane + Cfg::COL_X + col, vx);
         ptx::tmem_ld<8>(t_lane + Cfg::COL_Y + col, vy);
-        if constexpr (!Cfg::P_SMEM) ptx::tmem_ld<8>(t_lane + Cfg::COL_P + col, vp);
+        if (c8 * 8 < Cfg::PT_W) ptx::tmem_ld<8>(t_lane + Cfg::COL_P + h * Cfg::PT_W + c8 * 8, vp);
         ptx::tmem_ld_wait();
-        if constexpr (Cfg::P_SMEM) {
+        if (c8 * 8 >= Cfg::PT_W) {
+          const int ps = h * (Cfg::COLS_PER_WARP - Cfg::PT_W) + c8 * 8 - Cfg::PT_W;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) vp[j] = __float_as_uint(p_smem[(col + j) * Cfg::BM + q * 32 + lane]);
+          for (int j = 0; j < 8; ++j) vp[j] = __float_as_uint(p_smem[(ps + j) * Cfg::BM + q * 32 + lane]);
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
