@@ -78,11 +78,12 @@ struct PhaseConsts2 {
         mzero(f2::pk(id.mzero, id.mzero)), one(f2::pk(id.one, id.one)), mone(f2::pk(id.mone, id.mone)) {}
 };
 
-// The strict walls of gsb_phase, branch-free (selects only).
+// The strict walls of gsb_phase, branch-free: one |xn| > 1 test (false for NaN, like both
+// of gsb_phase's tests), then +-1 = copysign(1, xn) by a bit operation, and y = +0.
 __device__ __forceinline__ float clamp_wall(float xn, float& yn) {
-  const bool hi = xn > 1.0f, lo = xn < -1.0f;
-  yn = (hi || lo) ? 0.0f : yn;
-  return hi ? 1.0f : (lo ? -1.0f : xn);
+  const bool out = fabsf(xn) > 1.0f;
+  yn = out ? 0.0f : yn;
+  return out ? __uint_as_float((__float_as_uint(xn) & 0x80000000u) | 0x3F800000u) : xn;
 }
 
 // (x0, x1), (y0, y1), (p0, p1) updated with fields F0, F1; a2 = packed A per lane.

@@ -21,6 +21,7 @@
 
 #include "../../include/sbgpu.h"
 #include "aux_kernels.cuh"
+#include "e2m1.cuh"
 #include "csr_step.cuh"
 #include "gen_dense.cuh"
 #include "spectral.cuh"
@@ -89,6 +90,10 @@ struct sbg_ctx {
   int64_t n = 0, npad = 0;
   int8_t* dJ = nullptr;
   CUtensorMap tmJ;
+  // packed e2m1 copy of an e2m1-exact dense int8 J ([npad][npad / 2]; e2m1.cuh): the sign
+  // variants' resident kernel then runs kind::mxf4 MMAs (SBG_Q4=0 disables, dev)
+  uint8_t* dJ4 = nullptr;
+  CUtensorMap tmJ4;
   CUtensorMap tmJplane[FX_NA];  // KIND_DENSE_FX: one map per J byte plane (readout)
   int fx_shift = 0;             // KIND_DENSE_FX: J_int = rint(J * 2^fx_shift)
   double energy_scale = 1.0;    // energy = -E2/2 * energy_scale (2^-fx_shift for real J)
@@ -110,6 +115,7 @@ struct sbg_ctx {
   TmaMaps maps_sign_cw8[2];                  // sign pair kernel with 8-replica state chunks
   TmaMaps rmaps_sign[2];                     // resident-state pair kernel, NR 128 (B halves of 64 rows)
   TmaMaps rmaps160_sign[2];                  // resident-state pair kernel, NR 160 (B halves of 80 rows)
+  TmaMaps qmaps_sign[2], qmaps160_sign[2];   // the same on e2m1 operands (J4; G as [rpad][npad / 2])
   unsigned long long* dE2p = nullptr;    // real-J readout: per-J-plane partial E2 [FX_NA][rpad]
   // CSR: spin-major working copies [npad][rp] and the ping-pong gathered operand (q int32 / sign int8)
   float *dXs = nullptr, *dYs = nullptr, *dPs = nullptr;
@@ -309,11 +315,11 @@ int resident_nr(const sbg_ctx* ctx) {
   return g160 < g128 ? RES_NR : 128;
 }
 
-template <int EPI, int CH, int ST = RES_STAGES, int NR = 128>
+template <int EPI, int CH, int ST = RES_STAGES, int NR = 128, bool Q4 = false>
 int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms, int group0 = 0, int ngroups = -1,
                     const uint32_t* ready = nullptr) {
-  using Cfg = ResCfg<ST, EPI, CH, NR>;
-  auto kern = gsb_resident_pair_kernel<ST, EPI, CH, NR>;
+  using Cfg = ResCfg<ST, EPI, CH, NR, false, Q4>;
+  auto kern = gsb_resident_pair_kernel<ST, EPI, CH, NR, Q4>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
   ResidentArgs a;
   std::memset(&a, 0, sizeof a);
@@ -519,6 +525,22 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
                             gdim(ctx), 128, RES_NR, CU_TENSOR_MAP_SWIZZLE_NONE);
         }
         if (rcr) return rcr;
+        if (ctx->dJ4 && !ctx->sharded) {  // e2m1 operands: G as [rpad][npad / 2], two spins per byte
+          const uint64_t gb = uint64_t(ctx->npad / 2), gv4 = (gvalid + 1) / 2;
+          const int nrs[2] = {128, RES_NR};
+          for (int w = 0; w < 2 && !rcr; ++w) {
+            TmaMaps& qm = w ? ctx->qmaps160_sign[cur] : ctx->qmaps_sign[cur];
+            qm = w ? rm160 : rm;
+            qm.J = ctx->tmJ4;
+            for (int par = 0; par < 2 && !rcr; ++par) {
+              rcr = encode_2d_u8(ctx, &qm.Gin[par], ctx->dG[cur ^ par], gb, rpad, 128, nrs[w] / 2);
+              if (!rcr)
+                rcr = encode_2d(ctx, &qm.Gout[par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ par ^ 1], gv4, R,
+                                gb, 64, nrs[w], CU_TENSOR_MAP_SWIZZLE_NONE);
+            }
+          }
+          if (rcr) return rcr;
+        }
       }
       for (int par = 0; par < 2; ++par) {
         int rc = encode_2d_u8(ctx, &ctx->pmaps_planes[cur].Gin[par], ctx->dG[cur ^ par], ctx->npad, NPL * rpad, 128,
@@ -589,6 +611,32 @@ const std::vector<uint64_t>& jump_matrices() {
   return m;
 }
 
+// The e2m1 copy of a dense int8 J (rows x kpad), kept only if every entry is e2m1-exact.
+int build_q4(sbg_ctx* ctx, int64_t rows, int64_t kpad) {
+  cudaFree(ctx->dJ4);
+  ctx->dJ4 = nullptr;
+  if (getenv_is0("SBG_Q4")) return SBG_OK;
+  const size_t bytes = size_t(rows) * size_t(kpad / 2);
+  unsigned* bad = nullptr;
+  CK(cudaMalloc(&ctx->dJ4, bytes));
+  CK(cudaMalloc(&bad, sizeof(unsigned)));
+  CK(cudaMemsetAsync(bad, 0, sizeof(unsigned), ctx->stream));
+  pack_e2m1_kernel<<<grid_for(ctx, bytes / 16, 256), 256, 0, ctx->stream>>>(ctx->dJ, ctx->dJ4, bytes, bad);
+  ++ctx->launches;
+  unsigned h = 1;
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, bad, sizeof h, cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(bad);
+  if (e != cudaSuccess) return ctx->fail(SBG_ERR_CUDA, "e2m1 packing: %s", cudaGetErrorString(e));
+  if (h) {
+    cudaFree(ctx->dJ4);
+    ctx->dJ4 = nullptr;
+    return SBG_OK;
+  }
+  return encode_2d_u8(ctx, &ctx->tmJ4, ctx->dJ4, uint64_t(kpad / 2), uint64_t(rows), 128, 128);
+}
+
 // Allocates this context's dense int8 rows (all rows when world == 1, else the
 // row-shard layout of sbg_set_couplings_rows_i8) and fills them on the device:
 // GEN_EXACT = gen_random_dense's draw order (gen_dense.cuh), GEN_HASH = the
@@ -602,6 +650,8 @@ int gen_rows_common(sbg_ctx* ctx, int64_t n_global, int32_t world, int32_t rank,
   cudaStreamSynchronize(ctx->stream);
   free_state(ctx);
   cudaFree(ctx->dJ);
+  cudaFree(ctx->dJ4);
+  ctx->dJ4 = nullptr;
   ctx->dJ = nullptr;
   const bool shard = world > 1;
   const int64_t kpad = shard ? round_up(n_global, int64_t(128) * world) : round_up(n_global, PAD_N);
@@ -659,7 +709,8 @@ int gen_rows_common(sbg_ctx* ctx, int64_t n_global, int32_t world, int32_t rank,
   ctx->peer_g0.clear();
   ctx->peer_g1.clear();
   ctx->peer_done.clear();
-  return encode_2d_u8(ctx, &ctx->tmJ, ctx->dJ, kpad, rows, 128, 128);
+  const int rc = encode_2d_u8(ctx, &ctx->tmJ, ctx->dJ, kpad, rows, 128, 128);
+  return rc ? rc : build_q4(ctx, rows, kpad);
 }
 
 
@@ -816,6 +867,8 @@ void sbg_destroy(sbg_ctx* ctx) {
   cudaFree(ctx->d_arep);
   cudaFree(ctx->d_ready);
   cudaFree(ctx->dJ);
+  cudaFree(ctx->dJ4);
+  ctx->dJ4 = nullptr;
   cudaFree(ctx->d_rowptr);
   cudaFree(ctx->d_col);
   cudaFree(ctx->d_val);
@@ -852,6 +905,8 @@ int sbg_set_couplings_dense_i8(sbg_ctx* ctx, int64_t n, const int8_t* J) {
   cudaStreamSynchronize(ctx->stream);
   free_state(ctx);
   cudaFree(ctx->dJ);
+  cudaFree(ctx->dJ4);
+  ctx->dJ4 = nullptr;
   ctx->dJ = nullptr;
   const int64_t npad = round_up(n, PAD_N);
   CK(cudaMalloc(&ctx->dJ, size_t(npad) * npad));
@@ -862,7 +917,8 @@ int sbg_set_couplings_dense_i8(sbg_ctx* ctx, int64_t n, const int8_t* J) {
   ctx->npad = npad;
   ctx->kind = KIND_DENSE_I8;
   ctx->energy_scale = 1.0;
-  return encode_2d_u8(ctx, &ctx->tmJ, ctx->dJ, npad, npad, 128, 128);
+  const int rc = encode_2d_u8(ctx, &ctx->tmJ, ctx->dJ, npad, npad, 128, 128);
+  return rc ? rc : build_q4(ctx, npad, npad);
 }
 
 int sbg_set_couplings_dense_f64(sbg_ctx* ctx, int64_t n, const double* J) {
@@ -916,6 +972,8 @@ int sbg_set_couplings_dense_f32(sbg_ctx* ctx, int64_t n, const float* J) {
   cudaStreamSynchronize(ctx->stream);
   free_state(ctx);
   cudaFree(ctx->dJ);
+  cudaFree(ctx->dJ4);
+  ctx->dJ4 = nullptr;
   ctx->dJ = nullptr;
   CK(cudaMalloc(&ctx->dJ, planes.size()));
   CK(cudaMemcpy(ctx->dJ, planes.data(), planes.size(), cudaMemcpyHostToDevice));
@@ -958,6 +1016,8 @@ int sbg_set_couplings_csr_i8(sbg_ctx* ctx, int64_t n, int64_t nnz, const int32_t
   cudaStreamSynchronize(ctx->stream);
   free_state(ctx);
   cudaFree(ctx->dJ);
+  cudaFree(ctx->dJ4);
+  ctx->dJ4 = nullptr;
   cudaFree(ctx->d_rowptr);
   cudaFree(ctx->d_col);
   cudaFree(ctx->d_val);
@@ -1157,6 +1217,9 @@ int sbg_get_state(sbg_ctx* ctx, float* x, float* y, float* p) {
   return SBG_OK;
 }
 
+static int launch_resident_default(sbg_ctx* ctx, int cur, const MultiStepArgs& a, int groups, const uint32_t* ready,
+                                   int* g_mode);
+
 int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t m_end) {
   CHECK_CTX(ctx);
   int rc = validate_params(ctx, prm);
@@ -1282,10 +1345,12 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
           case 6: rc = launch_resident<16, 4, 6>(ctx, ctx->rmaps_sign[cur], a); break;
           case 7: rc = launch_resident<16, 4, 7>(ctx, ctx->rmaps_sign[cur], a); break;
           case 11: rc = launch_resident<16, 4>(ctx, ctx->rmaps_sign[cur], a); break;  // NR 128, all in TMEM
-          default:
-            rc = resident_nr(ctx) == RES_NR
-                     ? launch_resident<16, 4, RES_NR_STAGES, RES_NR>(ctx, ctx->rmaps160_sign[cur], a)
-                     : launch_resident<16, 4>(ctx, ctx->rmaps_sign[cur], a);
+          case 12: rc = launch_resident<16, 4, RES_NR_STAGES, RES_NR>(ctx, ctx->rmaps160_sign[cur], a); break;
+          default: {
+            int gm = 1;
+            rc = launch_resident_default(ctx, cur, a, -1, nullptr, &gm);
+            ctx->g_mode = gm;
+          }
         }
       } else if (sign) {
         switch (pair_ok ? knob : -1) {
@@ -1537,6 +1602,19 @@ static int run_tail(sbg_ctx* ctx, const sbg_params* prm, float* x_final, int8_t*
   return SBG_OK;
 }
 
+// The default resident launch: NR 160 when it cuts the group count, e2m1 operands when J
+// has an e2m1 copy. Returns the G-buffer mode left behind (1 = int8 sign plane, 0 = e2m1).
+static int launch_resident_default(sbg_ctx* ctx, int cur, const MultiStepArgs& a, int groups, const uint32_t* ready,
+                                   int* g_mode) {
+  const bool q4 = ctx->dJ4 != nullptr && !ctx->sharded;
+  *g_mode = q4 ? 0 : 1;
+  if (resident_nr(ctx) == RES_NR)
+    return q4 ? launch_resident<16, 4, RES_NR_STAGES, RES_NR, true>(ctx, ctx->qmaps160_sign[cur], a, 0, groups, ready)
+              : launch_resident<16, 4, RES_NR_STAGES, RES_NR>(ctx, ctx->rmaps160_sign[cur], a, 0, groups, ready);
+  return q4 ? launch_resident<16, 4, RES_STAGES, 128, true>(ctx, ctx->qmaps_sign[cur], a, 0, groups, ready)
+            : launch_resident<16, 4>(ctx, ctx->rmaps_sign[cur], a, 0, groups, ready);
+}
+
 // sbg_run on the resident kernel: the replica groups are independent for the whole
 // run, so group g's M steps start as soon as ITS x0/y0 rows have arrived; the copies of
 // the later groups (copy stream) overlap the earlier groups' steps.
@@ -1603,14 +1681,13 @@ static int run_pipelined(sbg_ctx* ctx, const sbg_params* prm, int64_t R, const f
   CK(cudaEventRecord(ctx->ev[7], ctx->stream));
   CK(cudaEventRecord(ctx->ev[3], ctx->stream));
   CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-  rc = nr == RES_NR
-           ? launch_resident<16, 4, RES_NR_STAGES, RES_NR>(ctx, ctx->rmaps160_sign[cur], a, 0, groups, ctx->d_ready)
-           : launch_resident<16, 4>(ctx, ctx->rmaps_sign[cur], a, 0, groups, ctx->d_ready);
+  int gm = 1;
+  rc = launch_resident_default(ctx, cur, a, groups, ctx->d_ready, &gm);
   if (rc) return rc;
   CK(cudaEventRecord(ctx->evc[1], ctx->cstream));
   CK(cudaStreamWaitEvent(ctx->stream, ctx->evc[1], 0));
   ctx->g_cur = cur ^ int(prm->steps & 1);
-  ctx->g_mode = 1;
+  ctx->g_mode = gm;
   CK(cudaEventRecord(ctx->ev[1], ctx->stream));
   return run_tail(ctx, prm, x_final, spins, energy, best_index, timing, /*advanced=*/true);
 }
@@ -1692,6 +1769,8 @@ int sbg_set_couplings_rows_i8(sbg_ctx* ctx, int64_t n_global, int32_t world, int
   cudaStreamSynchronize(ctx->stream);
   free_state(ctx);
   cudaFree(ctx->dJ);
+  cudaFree(ctx->dJ4);
+  ctx->dJ4 = nullptr;
   ctx->dJ = nullptr;
   CK(cudaMalloc(&ctx->dJ, size_t(rows) * kpad));
   CK(cudaMemsetAsync(ctx->dJ, 0, size_t(rows) * kpad, ctx->stream));

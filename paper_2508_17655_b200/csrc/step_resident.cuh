@@ -66,13 +66,22 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 // NR_ = replicas per pair block (UMMA N). 128: F, x, y, p all in TMEM (4 x 128 columns);
 // 160: F, x, y in TMEM (480 columns) and p in shared memory ([160][128] fp32, 80 KB),
 // which takes 25% more replicas per group (fewer sequential groups per step).
-template <int STAGES_, int EPI_WARPS_ = 16, int CH_ = 4, int NR_ = 128, bool GD_ = false>
+// Q4_: operands as packed e2m1 (two K elements per byte, even element in the low nibble):
+// J entries in {0, +-1, +-2, +-3, +-4, +-6} and G = +-1 are exact in e2m1, so
+// tcgen05.mma.kind::mxf4.block_scale with unit (E8M0 = 127) scales accumulates the
+// same integer field in fp32 (exact: |F| < 2^24), at twice the int8 MMA rate and half
+// the operand bytes (tools/dev/mxf4_probe.cu). The unit scales take SF_COLS TMEM columns.
+template <int STAGES_, int EPI_WARPS_ = 16, int CH_ = 4, int NR_ = 128, bool GD_ = false, bool Q4_ = false>
 struct ResCfg {
+  static constexpr bool Q4 = Q4_;
   static constexpr int BM = 128;                 // spins per CTA
-  static constexpr int BK = 128;                 // K bytes per stage
+  static constexpr int BK = 128;                 // K bytes per stage (128 int8 / 256 e2m1 elements)
+  static constexpr int KPB = Q4 ? 2 : 1;         // K elements per byte
   static constexpr int NR = NR_;                 // replicas per pair block (UMMA N)
-  static constexpr bool P_SMEM = 4 * NR > 512;   // part of p leaves TMEM
-  static constexpr int P_T = P_SMEM ? 512 - 3 * NR : NR;  // p columns kept in TMEM (the rest in smem)
+  static constexpr int SF_COLS = Q4 ? 16 : 0;    // unit scale factors (last TMEM columns)
+  static constexpr uint32_t COL_SF = 512 - SF_COLS;
+  static constexpr bool P_SMEM = 4 * NR + SF_COLS > 512;  // part of p leaves TMEM
+  static constexpr int P_T = P_SMEM ? 512 - SF_COLS - 3 * NR : NR;  // p columns kept in TMEM (the rest in smem)
   static constexpr int B_HALF = NR / 2;          // B rows staged per CTA
   static constexpr int A_BYTES = BM * BK;        // 16 KB
   static constexpr int B_BYTES = B_HALF * BK;    // 8 KB (NR 128)
@@ -81,7 +90,7 @@ struct ResCfg {
   // G_{t+1} staging tile [NR][128] for one TMA store; G_DIRECT: the epilogue stores the sign
   // bytes straight to global memory instead (frees the tile's shared memory for a ring stage)
   static constexpr bool G_DIRECT = GD_;
-  static constexpr int G_BYTES = G_DIRECT ? 0 : NR * BM;
+  static constexpr int G_BYTES = G_DIRECT ? 0 : NR * BM / KPB;
   static constexpr int P_BYTES = (NR - P_T) * BM * 4;
   static constexpr int EPI_WARPS = EPI_WARPS_;           // 4 per TMEM lane quadrant x column groups
   static constexpr int COLS_PER_WARP = NR / (EPI_WARPS / 4);
@@ -93,11 +102,12 @@ struct ResCfg {
   static constexpr uint32_t COL_X = NR, COL_Y = 2 * NR, COL_P = 3 * NR;  // p: [COL_P, COL_P + P_T)
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static_assert(NR % 16 == 0 && NR <= 256 && COLS_PER_WARP % 8 == 0, "UMMA N / epilogue chunking");
-  static_assert(3 * NR + P_T <= 512 && P_T % 8 == 0, "TMEM columns");
+  static_assert(3 * NR + P_T + SF_COLS <= 512 && P_T % 4 == 0, "TMEM columns");
   // p of a warp's column block: its first PT_W columns in TMEM, the rest in shared memory
   // (balanced over the column groups so no epilogue warp does more TMEM traffic)
   static constexpr int PT_W = P_T / (EPI_WARPS / 4);
-  static_assert(PT_W % 8 == 0 || !P_SMEM, "p split granularity");
+  static_assert((PT_W % 4 == 0 && CH_ % 4 == 0) || !P_SMEM, "p split granularity");
+  static_assert(!(Q4 && G_DIRECT), "e2m1 G is published through the smem tile");
 };
 
 struct ResidentArgs {
@@ -126,10 +136,32 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-template <int STAGES_, int EPI_WARPS_, int CH_, int NR_>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_WARPS_, CH_, NR_>::THREADS, 1)
-    gsb_resident_pair_kernel(const __grid_constant__ TmaMaps maps, const ResidentArgs args) {
-  using Cfg = ResCfg<STAGES_, EPI_WARPS_, CH_, NR_>;
+namespace ptx {
+// Instruction descriptor for kind::mxf4 (e2m1 x e2m1, E8M0 block-32 scales, f32 accumulate,
+// K-major, K = 64 per instruction).
+__host__ __device__ constexpr uint32_t idesc_mxf4(uint32_t M, uint32_t N) {
+  return (1u << 7)             // a_format: E2M1
+         | (1u << 10)          // b_format: E2M1
+         | ((N >> 3) << 17)    // n_dim
+         | (1u << 23)          // scale format: UE8M0
+         | ((M >> 4) << 24);   // m_dim; scale-factor ids 0
+}
+__device__ __forceinline__ void mma_mxf4_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t sf_tmem, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sf_tmem)
+      : "memory");
+}
+}  // namespace ptx
+
+template <int STAGES_, int EPI_WARPS_, int CH_, int NR_, bool Q4_ = false>
+__global__ void __cluster_dims__(2, 1, 1)
+    __launch_bounds__(ResCfg<STAGES_, EPI_WARPS_, CH_, NR_, false, Q4_>::THREADS, 1)
+        gsb_resident_pair_kernel(const __grid_constant__ TmaMaps maps, const ResidentArgs args) {
+  using Cfg = ResCfg<STAGES_, EPI_WARPS_, CH_, NR_, false, Q4_>;
   constexpr int CH = Cfg::CH;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -170,13 +202,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
   ptx::cluster_sync_all();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if constexpr (Cfg::Q4) {  // unit E8M0 scale factors (127 = 2^0) in the last SF_COLS columns
+    if (warp >= 4 && warp < 8) {
+      uint32_t v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = 0x7F7F7F7Fu;
+      const uint32_t t = tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16) + Cfg::COL_SF;
+#pragma unroll
+      for (int c = 0; c < Cfg::SF_COLS; c += 8) ptx::tmem_st8(t + c, v);
+      ptx::tmem_st_wait();
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync_all();
+    ptx::tc_fence_after();
+  }
 
   const int num_mp = args.num_m / 2;
   const int pair = blockIdx.x >> 1;
   const int mp = pair % num_mp, rbk = pair / num_mp;
   const int m_blk = 2 * mp + static_cast<int>(cr);
   const int i0 = m_blk * Cfg::BM;
-  const int KB = args.npad / Cfg::BK;
+  const int KB = args.npad / (Cfg::BK * Cfg::KPB);
   const int num_n = (args.rpad + Cfg::NR - 1) / Cfg::NR;  // the last block may pass rpad (NR 160)
 
   if (warp == 0) {  // ------------------------------------------------ operand producer
@@ -238,7 +284,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
     }
   } else if (warp == 1) {  // ------------------------------------------ MMA issuer (leader)
     if (leader) {
-      constexpr uint32_t idesc = ptx::idesc_i8(256, Cfg::NR, true, true);
+      constexpr uint32_t idesc = Cfg::Q4 ? ptx::idesc_mxf4(256, Cfg::NR) : ptx::idesc_i8(256, Cfg::NR, true, true);
+      const uint32_t sf = tmem_base + Cfg::COL_SF;
       int stage = 0;
       uint32_t ph = 0;
       int lt = 0;
@@ -275,8 +322,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
                 const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + st * Cfg::A_BYTES);
                 const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + st * Cfg::B_BYTES);
 #pragma unroll
-                for (int k = 0; k < Cfg::BK / 32; ++k)
-                  ptx::mma_i8_pair(tmem_base, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | u | k) != 0);
+                for (int k = 0; k < Cfg::BK / 32; ++k) {  // 32 bytes per MMA (K = 32 int8 / 64 e2m1)
+                  if constexpr (Cfg::Q4)
+                    ptx::mma_mxf4_pair(tmem_base, adesc + 2 * k, bdesc + 2 * k, idesc, sf, (kb | u | k) != 0);
+                  else
+                    ptx::mma_i8_pair(tmem_base, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | u | k) != 0);
+                }
                 ptx::mma_commit_pair_mc(empty_bar(st), 0x3);
               }
             }
@@ -305,6 +356,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
         g_tile[col * Cfg::BM + (spin - i0)] = static_cast<uint8_t>(sgn8(xv));
       }
     };
+    // G_{t+1} of columns (col, col + 1), col even: int8 bytes, or for Q4 e2m1 codes (+1 = 0x2,
+    // -1 = 0xA) packed two spins per byte; lanes 2i, 2i+1 (spins 2i, 2i+1) swap codes so the
+    // even lane writes column col's byte and the odd lane column col + 1's. Warp-uniform.
+    const uint32_t g_sel = (lane & 1) ? 0x15u : 0x40u;
+    auto put_g2 = [&](int n_blk, int col, int par, float xa, float xb) {
+      if constexpr (Cfg::Q4) {
+        const uint32_t mine = (xa >= 0.0f ? 0x2u : 0xAu) | ((xb >= 0.0f ? 0x2u : 0xAu) << 8);
+        const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, mine, 1);
+        // even lane: (its code, partner's code) of column col; odd: (partner's, its) of col + 1
+        const uint32_t t = __byte_perm(mine, other, g_sel);
+        g_tile[(col + (lane & 1)) * (Cfg::BM / 2) + ((spin - i0) >> 1)] = static_cast<uint8_t>(t | (t >> 4));
+      } else {
+        put_g(n_blk, col, par, xa);
+        put_g(n_blk, col + 1, par, xb);
+      }
+    };
     // publish this CTA's G chunk of block n_blk for the consumers of step parity par
     auto publish = [&](int n_blk, int par) {
       if constexpr (Cfg::G_DIRECT) {
@@ -318,7 +385,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
         ptx::fence_proxy_async_smem();
         ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);
         if (epi_tid == 0) {
-          ptx::tma_store_2d(&maps.Gout[par], g_base, i0, n_blk * Cfg::NR);
+          ptx::tma_store_2d(&maps.Gout[par], g_base, i0 / Cfg::KPB, n_blk * Cfg::NR);
           ptx::bulk_commit();
           ptx::bulk_wait0();
           dep::fence_proxy_async_global();
@@ -351,15 +418,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
         const uint32_t col = h * Cfg::COLS_PER_WARP + c8 * 8;
         ptx::tmem_st<8>(t_lane + Cfg::COL_X + col, vx);
         ptx::tmem_st<8>(t_lane + Cfg::COL_Y + col, vy);
-        if (c8 * 8 < Cfg::PT_W) {
-          ptx::tmem_st<8>(t_lane + Cfg::COL_P + h * Cfg::PT_W + c8 * 8, vp);
-        } else {
-          const int ps = h * (Cfg::COLS_PER_WARP - Cfg::PT_W) + c8 * 8 - Cfg::PT_W;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) p_smem[(ps + j) * Cfg::BM + q * 32 + lane] = __uint_as_float(vp[j]);
+        for (int u = 0; u < 8; u += 4) {  // p in units of 4 columns: TMEM below PT_W, else smem
+          const int c4 = c8 * 8 + u;
+          if (c4 < Cfg::PT_W) {
+            const uint32_t v4[4] = {vp[u], vp[u + 1], vp[u + 2], vp[u + 3]};
+            ptx::tmem_st<4>(t_lane + Cfg::COL_P + h * Cfg::PT_W + c4, v4);
+          } else {
+            const int ps = h * (Cfg::COLS_PER_WARP - Cfg::PT_W) + c4 - Cfg::PT_W;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) p_smem[(ps + j) * Cfg::BM + q * 32 + lane] = __uint_as_float(vp[u + j]);
+          }
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) put_g(n_blk, col + j, 1, __uint_as_float(vx[j]));
+        for (int j = 0; j < 8; j += 2) put_g2(n_blk, col + j, 1, __uint_as_float(vx[j]), __uint_as_float(vx[j + 1]));
       }
       ptx::tmem_st_wait();
       // publish G_0 = sgn(x) of this block (the B operand of the launch's first step:
@@ -411,16 +483,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
               uint64_t a2 = k2.a;
               if constexpr (decltype(has_arep)::value)
                 a2 = f2::pk(arep[min(r0 + c * CH + j, args.R - 1)], arep[min(r0 + c * CH + j + 1, args.R - 1)]);
-              gsb_phase2(static_cast<float>(static_cast<int32_t>(bf[b][j])),
-                         static_cast<float>(static_cast<int32_t>(bf[b][j + 1])), x0, x1, y0, y1, p0, p1, k2, a2);
+              // the field: s32 (int8 MMA) or the same integer in f32 (e2m1 MMA; exact)
+              const float f0 = Cfg::Q4 ? __uint_as_float(bf[b][j]) : static_cast<float>(static_cast<int32_t>(bf[b][j]));
+              const float f1 =
+                  Cfg::Q4 ? __uint_as_float(bf[b][j + 1]) : static_cast<float>(static_cast<int32_t>(bf[b][j + 1]));
+              gsb_phase2(f0, f1, x0, x1, y0, y1, p0, p1, k2, a2);
               bx[b][j] = __float_as_uint(x0);
               bx[b][j + 1] = __float_as_uint(x1);
               by[b][j] = __float_as_uint(y0);
               by[b][j + 1] = __float_as_uint(y1);
               bp[b][j] = __float_as_uint(p0);
               bp[b][j + 1] = __float_as_uint(p1);
-              put_g(n_blk, h * Cfg::COLS_PER_WARP + c * CH + j, s & 1, x0);
-              put_g(n_blk, h * Cfg::COLS_PER_WARP + c * CH + j + 1, s & 1, x1);
+              put_g2(n_blk, h * Cfg::COLS_PER_WARP + c * CH + j, s & 1, x0, x1);
             }
             const uint32_t col = h * Cfg::COLS_PER_WARP + c * CH;
             ptx::tmem_st<CH>(t_lane + Cfg::COL_X + col, bx[b]);
@@ -455,15 +529,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ResCfg<STAGES_, EPI_
 #pragma unroll 1
       for (int c8 = 0; c8 < Cfg::COLS_PER_WARP / 8; ++c8) {
         const uint32_t col = h * Cfg::COLS_PER_WARP + c8 * 8;
-        uint32_t vx[8], vy[8], vp[8];
+        uint32_t vx[8], vy[8], vp[8], vp4[2][4];
         ptx::tmem_ld<8>(t_lane + Cfg::COL_X + col, vx);
         ptx::tmem_ld<8>(t_lane + Cfg::COL_Y + col, vy);
-        if (c8 * 8 < Cfg::PT_W) ptx::tmem_ld<8>(t_lane + Cfg::COL_P + h * Cfg::PT_W + c8 * 8, vp);
-        ptx::tmem_ld_wait();
-        if (c8 * 8 >= Cfg::PT_W) {
-          const int ps = h * (Cfg::COLS_PER_WARP - Cfg::PT_W) + c8 * 8 - Cfg::PT_W;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) vp[j] = __float_as_uint(p_smem[(ps + j) * Cfg::BM + q * 32 + lane]);
+        for (int u = 0; u < 2; ++u)
+          if (c8 * 8 + 4 * u < Cfg::PT_W) ptx::tmem_ld<4>(t_lane + Cfg::COL_P + h * Cfg::PT_W + c8 * 8 + 4 * u, vp4[u]);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int c4 = c8 * 8 + 4 * u;
+          const int ps = h * (Cfg::COLS_PER_WARP - Cfg::PT_W) + c4 - Cfg::PT_W;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            vp[4 * u + j] = c4 < Cfg::PT_W ? vp4[u][j] : __float_as_uint(p_smem[(ps + j) * Cfg::BM + q * 32 + lane]);
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
