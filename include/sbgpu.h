@@ -94,6 +94,11 @@ int sbg_set_couplings_dense_i8(sbg_ctx* ctx, int64_t n, const int8_t* J);
 /* fp64 J as IsingInstance stores it: integral entries in [-127, 127] take the int8
  * path, anything else the fixed-point real-J path below. */
 int sbg_set_couplings_dense_f64(sbg_ctx* ctx, int64_t n, const double* J);
+/* 1 if the dense couplings also hold a packed e2m1 (FP4) copy, made at upload when every
+ * entry lies in {0, +-1, +-2, +-3, +-4, +-6} (all +-1 instances): the sign variants'
+ * resident kernel then multiplies with tcgen05 kind::mxf4 (exact integer fields, twice
+ * the int8 rate); else 0 (int8 operands). */
+int sbg_couplings_e2m1(const sbg_ctx* ctx);
 /* Real-valued couplings (e.g. Sherrington-Kirkpatrick, BASELINE configs[3]): J is
  * held as a 24-bit fixed-point image J_int = rint(J * 2^s) (s maximal with
  * |J_int| < 2^23) in three byte planes; fields are exact integer sums scaled once

@@ -21,7 +21,7 @@ INIT_UNIFORM_RANDOM, INIT_CHAOS_PROBE, INIT_SMALL_UNIFORM = 0, 1, 2
 
 EXPORTS = [
     "sbg_abi_version", "sbg_strerror", "sbg_create", "sbg_destroy", "sbg_last_error", "sbg_device_sm_count",
-    "sbg_device_name",
+    "sbg_device_name", "sbg_couplings_e2m1",
     "sbg_set_couplings_dense_i8", "sbg_set_couplings_dense_f64", "sbg_set_couplings_dense_f32",
     "sbg_coupling_scale_exp", "sbg_gen_couplings_dense_pm1",
     "sbg_set_couplings_csr_i8", "sbg_n", "sbg_set_state", "sbg_init_state", "sbg_get_state", "sbg_advance",
@@ -85,6 +85,7 @@ def lib() -> C.CDLL:
     L.sbg_device_sm_count.argtypes = [P]
     L.sbg_device_name.argtypes = [P]
     L.sbg_device_name.restype = C.c_char_p
+    L.sbg_couplings_e2m1.argtypes = [P]
     L.sbg_set_couplings_dense_i8.argtypes = [P, i64, P]
     L.sbg_set_couplings_dense_f64.argtypes = [P, i64, P]
     L.sbg_gen_couplings_dense_pm1.argtypes = [P, i64, u64]

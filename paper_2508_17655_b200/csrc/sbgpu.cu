@@ -886,6 +886,7 @@ const char* sbg_last_error(const sbg_ctx* ctx) { return ctx ? ctx->err.c_str() :
 int sbg_device_sm_count(const sbg_ctx* ctx) { return ctx ? ctx->sms : 0; }
 const char* sbg_device_name(const sbg_ctx* ctx) { return ctx ? ctx->device_name.c_str() : ""; }
 int64_t sbg_n(const sbg_ctx* ctx) { return ctx ? ctx->n : 0; }
+int sbg_couplings_e2m1(const sbg_ctx* ctx) { return ctx && ctx->dJ4 ? 1 : 0; }
 int64_t sbg_kernel_launches(const sbg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 int sbg_set_couplings_dense_i8(sbg_ctx* ctx, int64_t n, const int8_t* J) {

@@ -214,6 +214,12 @@ class Solver:
         return self._L.sbg_device_name(self._h).decode()
 
     @property
+    def operand_format(self) -> str:
+        """'e2m1' when the dense couplings carry a packed FP4 copy (sign variants then run
+        kind::mxf4 MMAs), else 'int8'."""
+        return "e2m1" if self._L.sbg_couplings_e2m1(self._h) else "int8"
+
+    @property
     def sm_count(self) -> int:
         return self._L.sbg_device_sm_count(self._h)
 

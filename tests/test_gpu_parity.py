@@ -351,6 +351,80 @@ def test_resident_kernel_equals_streaming(solver, orc, n, R, variant, monkeypatc
         assert (a[3] == b[3]).all() and a[4] == b[4]
 
 
+def _run_resident(solver, J, R, variant, steps, monkeypatch, q4, resident="1", arep=None):
+    from paper_2508_17655_b200 import InitMode
+
+    monkeypatch.setenv("SBG_Q4", "1" if q4 else "0")
+    monkeypatch.setenv("SBG_RESIDENT", resident)
+    solver.set_instance(J)
+    n = J.shape[0]
+    solver.init_state(R, InitMode.small_uniform, 5, 7)
+    solver.set_replica_a(arep)
+    solver.advance(cfg_for(variant, 100, 1.25, 1 / (2 * np.sqrt(n)), 0.2), 0, steps)
+    x, y, p = solver.get_state()
+    _, e, best, _ = solver.readout()
+    fmt = solver.operand_format
+    solver.set_replica_a(None)
+    return fmt, (x, y, p, e, best)
+
+
+def _same(a, b):
+    assert all((u.view(np.uint32) == v.view(np.uint32)).all() for u, v in zip(a[:3], b[:3]))
+    assert (a[3] == b[3]).all() and a[4] == b[4]
+
+
+E2M1_INTS = np.array([0, 1, -1, 2, -2, 3, -3, 4, -4, 6, -6], np.int8)
+
+
+def _sym(n, values, seed):
+    rng = np.random.default_rng(seed)
+    J = np.triu(rng.choice(values, size=(n, n)), 1).astype(np.int8)
+    return (J + J.T).astype(np.int8)
+
+
+@pytest.mark.parametrize("n,R,variant,values", [(2000, 3000, GDSB, "pm1"), (777, 1500, DSB, "e2m1"),
+                                                (513, 400, GDSB, "e2m1"), (1500, 2000, GDSB, "pm1")])
+def test_e2m1_resident_equals_int8(solver, n, R, variant, values, monkeypatch):
+    """kind::mxf4 operands (packed e2m1 J and G, unit E8M0 scales, f32 accumulation) give
+    the same integer fields as the int8 MMAs: states, energies and winner bitwise equal to
+    the int8 resident kernel and to the streaming kernels, for +-1 J and for J over every
+    e2m1-exact integer {0, +-1, +-2, +-3, +-4, +-6}; odd n exercises the half-filled
+    last byte of each packed row; per-replica A included."""
+    J = _sym(n, np.array([1, -1], np.int8) if values == "pm1" else E2M1_INTS, n)
+    arep = np.random.default_rng(n).random(R).astype(np.float32)
+    f4, a = _run_resident(solver, J, R, variant, 17, monkeypatch, True, arep=arep)
+    f8, b = _run_resident(solver, J, R, variant, 17, monkeypatch, False, arep=arep)
+    _, c = _run_resident(solver, J, R, variant, 17, monkeypatch, True, resident="0", arep=arep)
+    assert (f4, f8) == ("e2m1", "int8")
+    _same(a, b)
+    _same(a, c)
+
+
+def test_e2m1_large_fields_exact(solver, monkeypatch):
+    """f32 accumulation of e2m1 products is exact while |F| < 2^24: J_ij = 6 everywhere
+    off the diagonal and aligned spins drive |F| to 6 (n - 1) = 55,194 at n = 9200 (past
+    2^15; the probe tools/dev/mxf4_probe.cu also checks 1.3e5), bitwise equal to int8."""
+    n, R = 9200, 320
+    J = np.full((n, n), 6, np.int8)
+    np.fill_diagonal(J, 0)
+    f4, a = _run_resident(solver, J, R, DSB, 5, monkeypatch, True)
+    f8, b = _run_resident(solver, J, R, DSB, 5, monkeypatch, False)
+    assert (f4, f8) == ("e2m1", "int8")
+    _same(a, b)
+
+
+def test_non_e2m1_couplings_stay_int8(solver, monkeypatch):
+    """A coupling outside the e2m1-exact set (5, or |J| > 6) keeps the int8 operands."""
+    for bad in (5, 7, -100):
+        J = _sym(300, E2M1_INTS, 1)
+        J[3, 7] = J[7, 3] = bad
+        monkeypatch.setenv("SBG_Q4", "1")
+        solver.set_instance(J)
+        assert solver.operand_format == "int8"
+    solver.set_instance(_sym(300, E2M1_INTS, 1))
+    assert solver.operand_format == "e2m1"
+
+
 @pytest.mark.parametrize("n,R", [(2000, 8192), (500, 2500)])
 def test_run_pipelined_copies_equal_serial(solver, orc, n, R, monkeypatch):
     """sbg_run on the resident kernel overlaps each replica group's host->device copy with
