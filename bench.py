@@ -57,14 +57,23 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def int8_peak():
-    """Dense int8 tensor peak measured on this pool's B200 (tools/int8_peak.py: cuBLASLt
-    int8 GEMM 8192^3, burst), as SURVEY 8(d) asks; the nominal 4500 TOPS otherwise."""
+DTYPES = {"e2m1": "e2m1 operands (tcgen05 kind::mxf4, unit E8M0 scales, f32 acc: exact integer field) / f32 state",
+          "int8": "i8 operands (tcgen05 kind::i8, s32 acc) / f32 state"}
+KERNELS = {"e2m1": "gsb_resident_pair_kernel<5,16,4,160,true>", "int8": "gsb_resident_pair_kernel<5,16,4,160,false>"}
+
+
+def tensor_peak(fmt):
+    """Dense tensor peak of the pipe the resident kernel multiplies on, measured on this pool's
+    B200 as SURVEY 8(d) asks: e2m1 -> tools/fp4_peak.py (cuBLASLt FP4 GEMM 8192^3, burst),
+    int8 -> tools/int8_peak.py (cuBLASLt int8 GEMM 8192^3, burst); the datasheet dense
+    figure (9000 / 4500 TOPS) if the measurement file is missing."""
+    name, key, nominal = ("fp4_peak.json", "fp4_tops_burst", 9000.0) if fmt == "e2m1" else \
+        ("int8_peak.json", "int8_tops_burst", 4500.0)
     try:
-        with open(os.path.join(ROOT, "profiles", "int8_peak.json")) as f:
-            return float(json.load(f)["int8_tops_burst"]), "measured (profiles/int8_peak.json, cuBLASLt 8192^3 burst)"
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return float(json.load(f)[key]), f"measured (profiles/{name}, cuBLASLt 8192^3 burst)"
     except Exception:
-        return 4500.0, "nominal (datasheet dense int8)"
+        return nominal, f"nominal (datasheet dense {fmt})"
 
 
 class ClockSampler:
@@ -203,6 +212,7 @@ def run_ours(args):
     cfg = SolverConfig(variant=Variant.gdsb, steps=M_SCHED, dt=DT, c=c, a=A_CTRL, init_mode=InitMode.small_uniform)
     s = Solver(local)
     s.gen_random_dense(N_SPINS, INSTANCE_SEED)
+    fmt = s.operand_format  # e2m1 for +-1 J: the resident kernel runs kind::mxf4 MMAs
     s.init_state(R, InitMode.small_uniform, MASTER, INIT_TAG, offset=r0)
     state_bytes = 12 * N_SPINS * R
     assert state_bytes > L2_BYTES, "per-GPU state must exceed L2 (timing protocol)"
@@ -265,7 +275,7 @@ def run_ours(args):
     # streaming formulation never reaches HBM; "if the kernel keeps state on-chip
     # across steps and beats the HBM term, report the tensor-only fraction and say so".
     hbm_peak, hbm_src = peaks()
-    i8_peak, i8_src = int8_peak()
+    t_peak, t_src = tensor_peak(fmt)
     ops_per_step = 2 * N_SPINS * N_SPINS * R  # 2N ops per spin-update
     tops = ops_per_step / (ms_per_step / 1e3) / 1e12
     stream_bytes = 24 * N_SPINS * R + N_SPINS * N_SPINS  # the streaming formulation's HBM bytes per step
@@ -273,14 +283,14 @@ def run_ours(args):
     tpath = os.path.join(ROOT, "profiles", "step_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("resident_gdsb_n2000_R8192_dram_bytes_per_step")
+            traffic = json.load(open(tpath)).get(f"resident_gdsb_n2000_R8192_{fmt}_dram_bytes_per_step")
         except Exception:
             traffic = None
 
     line = {
         "metric": METRIC, "value": value, "unit": "spin-updates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "i8 field (tcgen05 kind::i8, s32 acc) / f32 state",
+        "vs_baseline": None, "dtype": DTYPES[fmt],
         "data": "synthetic (seeded gen_random_dense N=2000 instance; x0,y0~U(-0.1,0.1) from derive_seed(1,{7,r}))",
         "config": {"workload": "C2 (BASELINE configs[1]): N=2000 dense +-1, GdSB, R=8192 replicas per GPU",
                    "n": N_SPINS, "replicas_per_gpu": R, "replicas_total": R_all, "M": M_SCHED, "A": A_CTRL,
@@ -292,10 +302,10 @@ def run_ours(args):
                 "note": f"one sbg_run() of M={e2e_steps} steps per rank: H2D x0,y0 from pinned host, M steps, "
                         "readout (energy+argmin), D2H energies+best index; wall clock, max over ranks",
                 "device_breakdown_ms": b.timing},
-        "roofline": {"bound": "tensor", "achieved": tops, "peak": i8_peak, "unit": "TFLOP/s",
-                     "frac": tops / i8_peak, "traffic": traffic, "peak_source": i8_src,
-                     "op_type": "int8 tensor ops (2 per MAC), 2*N*N*R per step",
-                     "kernel": "gsb_resident_pair_kernel<5,16,4,160> (all timed steps in one launch; x, y in TMEM, "
+        "roofline": {"bound": "tensor", "achieved": tops, "peak": t_peak, "unit": "TFLOP/s",
+                     "frac": tops / t_peak, "traffic": traffic, "peak_source": t_src,
+                     "op_type": f"{fmt} tensor ops (2 per MAC), 2*N*N*R per step",
+                     "kernel": KERNELS[fmt] + " (all timed steps in one launch; x, y in TMEM, "
                                "p split TMEM / shared memory)",
                      "streaming_equivalent": {"bytes_per_step": stream_bytes,
                                               "gbs": stream_bytes / (ms_per_step / 1e3) / 1e9,
