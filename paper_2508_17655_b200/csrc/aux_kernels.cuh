@@ -147,6 +147,24 @@ __global__ void prep_planes_kernel(const float* __restrict__ x, uint8_t* __restr
   }
 }
 
+// The e2m1 sign plane ([rpad][npad / 2] bytes): byte b of row r packs spins 2b (low
+// nibble) and 2b + 1 as e2m1 codes (+1 = 0x2, -1 = 0xA; padding 0x0).
+__global__ void prep_sign4_kernel(const float* __restrict__ x, uint8_t* __restrict__ G, int32_t n, int32_t npad,
+                                  int32_t R, int32_t rpad) {
+  const int32_t hb = npad / 2;
+  const size_t total = static_cast<size_t>(rpad) * hb;
+  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(idx / hb);
+    const int i = 2 * static_cast<int>(idx % hb);
+    uint32_t v = 0;
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      if (r < R && i + e < n) v |= (x[static_cast<size_t>(r) * npad + i + e] >= 0.0f ? 0x2u : 0xAu) << (4 * e);
+    G[idx] = static_cast<uint8_t>(v);
+  }
+}
+
 // Upload helper: a host sign matrix S (R x n, +-1) into a padded plane.
 __global__ void pad_plane_kernel(const int8_t* __restrict__ S, uint8_t* __restrict__ G, int32_t n,
                                  int32_t npad, int32_t R, int32_t rpad) {

@@ -335,5 +335,24 @@ template <>
 __device__ __forceinline__ void tmem_ld<2>(uint32_t taddr, uint32_t (&v)[2]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(taddr));
 }
+
+// Instruction descriptor for kind::mxf4 (e2m1 x e2m1, E8M0 block-32 scales, f32 accumulate,
+// K-major, K = 64 per instruction).
+__host__ __device__ constexpr uint32_t idesc_mxf4(uint32_t M, uint32_t N) {
+  return (1u << 7)             // a_format: E2M1
+         | (1u << 10)          // b_format: E2M1
+         | ((N >> 3) << 17)    // n_dim
+         | (1u << 23)          // scale format: UE8M0
+         | ((M >> 4) << 24);   // m_dim; scale-factor ids 0
+}
+__device__ __forceinline__ void mma_mxf4_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t sf_tmem, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sf_tmem)
+      : "memory");
+}
 }  // namespace ptx
 }  // namespace sbg

@@ -116,6 +116,7 @@ struct sbg_ctx {
   TmaMaps rmaps_sign[2];                     // resident-state pair kernel, NR 128 (B halves of 64 rows)
   TmaMaps rmaps160_sign[2];                  // resident-state pair kernel, NR 160 (B halves of 80 rows)
   TmaMaps qmaps_sign[2], qmaps160_sign[2];   // the same on e2m1 operands (J4; G as [rpad][npad / 2])
+  TmaMaps pqmaps_sign[2];                    // streaming sign pair kernel on e2m1 operands
   unsigned long long* dE2p = nullptr;    // real-J readout: per-J-plane partial E2 [FX_NA][rpad]
   // CSR: spin-major working copies [npad][rp] and the ping-pong gathered operand (q int32 / sign int8)
   float *dXs = nullptr, *dYs = nullptr, *dPs = nullptr;
@@ -134,7 +135,7 @@ struct sbg_ctx {
   uint32_t* d_ready = nullptr;           // per replica-group "state copied" flags (sbg_run pipelining)
   int64_t ready_cap = 0;
   int g_cur = 0;
-  int g_mode = 0;  // 0 stale, 1 sign plane valid in dG[g_cur], 4 planes valid
+  int g_mode = 0;  // 0 stale, 1 sign plane valid in dG[g_cur], 2 e2m1 sign plane, 4 planes valid
   cudaEvent_t ev[8];
   cudaStream_t cstream = nullptr;  // host->device copies overlapped with the resident kernel (sbg_run)
   cudaEvent_t evc[3];
@@ -265,10 +266,10 @@ int launch_multistep(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& a) 
   return SBG_OK;
 }
 
-template <int NP, int NPAIR, int ST, int NB, int CW = 16>
+template <int NP, int NPAIR, int ST, int NB, int CW = 16, bool Q4 = false>
 int launch_multistep_pair(sbg_ctx* ctx, const TmaMaps& maps, MultiStepArgs a) {
-  using Cfg = PairStepCfg<NP, NPAIR, ST, NB, CW>;
-  auto kern = gsb_multistep_pair_kernel<NP, NPAIR, ST, NB, CW>;
+  using Cfg = PairStepCfg<NP, NPAIR, ST, NB, CW, Q4>;
+  auto kern = gsb_multistep_pair_kernel<NP, NPAIR, ST, NB, CW, Q4>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
   a.num_n = int32_t(ctx->rpad / NPAIR);
   const int64_t pair_tiles = int64_t(a.num_m / 2) * a.num_n * a.nsteps;
@@ -538,6 +539,15 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
                 rcr = encode_2d(ctx, &qm.Gout[par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ par ^ 1], gv4, R,
                                 gb, 64, nrs[w], CU_TENSOR_MAP_SWIZZLE_NONE);
             }
+          }
+          TmaMaps& pq = ctx->pqmaps_sign[cur];
+          pq = ctx->maps_sign[cur];
+          pq.J = ctx->tmJ4;
+          for (int par = 0; par < 2 && !rcr; ++par) {
+            rcr = encode_2d_u8(ctx, &pq.Gin[par], ctx->dG[cur ^ par], gb, rpad, 128, NPAIR_SIGN / 2);
+            if (!rcr)
+              rcr = encode_2d(ctx, &pq.Gout[par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ par ^ 1], gv4, R, gb,
+                              64, 16, CU_TENSOR_MAP_SWIZZLE_NONE);
           }
           if (rcr) return rcr;
         }
@@ -1282,11 +1292,23 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
       ++ctx->launches;
     }
   } else {
-    const int need = sign ? 1 : NPL;
     const bool resident = use_resident(ctx, prm->variant);
+    const int knob = dev_knob("SBG_STEP_CFG");
+    const bool pair_ok = (ctx->npad % 256) == 0 && !ctx->sharded;
+    // streaming sign launches on e2m1 operands (the J-streaming regime, e.g. C5: half the bytes)
+    const bool q4s = sign && !resident && ctx->dJ4 && pair_ok && knob == 0 && ctx->kind == KIND_DENSE_I8;
+    const int need = q4s ? 2 : sign ? 1 : NPL;
     if (ctx->g_mode != need && !resident) {  // the resident kernel publishes its own G_0
-      rc = prep_planes(ctx, ctx->dX, ctx->dG[ctx->g_cur], need, ctx->R, ctx->rpad, /*into_global=*/true);
-      if (rc) return rc;
+      if (q4s) {
+        const size_t tot = size_t(ctx->rpad) * (ctx->npad / 2);
+        prep_sign4_kernel<<<grid_for(ctx, tot, 256), 256, 0, ctx->stream>>>(
+            ctx->dX, ctx->dG[ctx->g_cur], int32_t(ctx->n), int32_t(ctx->npad), int32_t(ctx->R), int32_t(ctx->rpad));
+        CK(cudaGetLastError());
+        ++ctx->launches;
+      } else {
+        rc = prep_planes(ctx, ctx->dX, ctx->dG[ctx->g_cur], need, ctx->R, ctx->rpad, /*into_global=*/true);
+        if (rc) return rc;
+      }
       ctx->g_mode = need;
     }
     if (resident) ctx->g_mode = 1;
@@ -1330,8 +1352,6 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
       // (3 operand stages, 4 state buffers): 73 us/step at N=2000, R=8192, vs 83 us
       // single-CTA; fixed-point planes single-CTA (3, 2): 18.5 us/step at R=1024 vs
       // 20.4 us on pairs. SBG_STEP_CFG selects sweep alternatives (dev only).
-      const int knob = dev_knob("SBG_STEP_CFG");
-      const bool pair_ok = (ctx->npad % 256) == 0 && !ctx->sharded;
       if (fx) {
         // real-valued J: 3 J planes x (sign | 4 x-planes), single-CTA
         rc = sign ? launch_multistep<1, BN_FX_SIGN, 2, 4, FX_NA>(ctx, ctx->fxmaps_sign[cur], a)
@@ -1364,8 +1384,10 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
           case 7: rc = launch_multistep_pair<1, NPAIR_SIGN, 5, 2>(ctx, ctx->maps_sign[cur], a); break;
           case 8: rc = launch_multistep_pair<1, NPAIR_SIGN, 3, 4>(ctx, ctx->maps_sign[cur], a); break;
           // non-resident sign launches are the large-N J-streaming regime (C5: 2.06 ms/step,
-          // 0.79 of HBM with 5 operand stages vs 2.29 ms with 3)
-          default: rc = launch_multistep_pair<1, NPAIR_SIGN, 5, 2>(ctx, ctx->maps_sign[cur], a);
+          // 0.79 of HBM with 5 operand stages vs 2.29 ms with 3); e2m1 operands halve J
+          default:
+            rc = q4s ? launch_multistep_pair<1, NPAIR_SIGN, 5, 2, 16, true>(ctx, ctx->pqmaps_sign[cur], a)
+                     : launch_multistep_pair<1, NPAIR_SIGN, 5, 2>(ctx, ctx->maps_sign[cur], a);
         }
       } else {
         switch (pair_ok ? knob : -1) {

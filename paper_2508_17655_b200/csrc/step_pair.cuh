@@ -31,8 +31,14 @@
 
 namespace sbg {
 
-template <int NPLANES, int N_PAIR, int STAGES_, int NBUF_, int CW_ = 16>
+// Q4_ (sign plane only): packed e2m1 J and G with kind::mxf4 MMAs, as in step_resident.cuh
+// -- half the J bytes per step (the bound of the J-streaming regime, C5) at twice the MMA
+// rate. Its unit scale factors take 16 TMEM columns, so the accumulator is single-buffered
+// (N_PAIR = 256 leaves no room for two).
+template <int NPLANES, int N_PAIR, int STAGES_, int NBUF_, int CW_ = 16, bool Q4_ = false>
 struct PairStepCfg {
+  static constexpr bool Q4 = Q4_;
+  static constexpr int KPB = Q4 ? 2 : 1;                // K elements per operand byte
   static constexpr int BM = 128;                        // spins per CTA
   static constexpr int BK = 128;                        // K bytes per stage
   static constexpr int B_HALF = N_PAIR / 2;             // B rows staged per CTA (per plane)
@@ -45,11 +51,13 @@ struct PairStepCfg {
   static constexpr int CWQ = CW / (EPI_WARPS / 4);
   static constexpr int NBUF = NBUF_;
   static constexpr int ST_ARR = CW * BM * 4;
-  static constexpr int ST_G = CW * BM;
+  static constexpr int ST_G = CW * BM / KPB;
   static constexpr int BUF_RAW = 3 * ST_ARR + NPLANES * ST_G;
   static constexpr int BUF_BYTES = (BUF_RAW + 1023) / 1024 * 1024;
   static constexpr int ACC_COLS = NPLANES * N_PAIR;     // per CTA per accumulator buffer
-  static constexpr int TMEM_COLS = 2 * ACC_COLS;
+  static constexpr int NACC = Q4 ? 1 : 2;               // accumulator buffers
+  static constexpr int TMEM_COLS = Q4 ? 512 : 2 * ACC_COLS;
+  static constexpr uint32_t COL_SF = 512 - 16;          // Q4: unit E8M0 scale factors
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static constexpr int NUM_BARS = 2 * STAGES + 4 + 3 * NBUF;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + NBUF * BUF_BYTES + 1024 + 8 * NUM_BARS + 64;
@@ -57,12 +65,15 @@ struct PairStepCfg {
   static_assert(N_PAIR % 32 == 0 && N_PAIR <= 256 && N_PAIR >= 32, "UMMA N for M=256");
   static_assert(N_PAIR % CW == 0, "chunking");
   static_assert(TMEM_COLS == 256 || TMEM_COLS == 512, "TMEM allocation");
+  static_assert(!Q4 || (NPLANES == 1 && ACC_COLS <= 496), "e2m1: sign plane, room for the scale factors");
 };
 
-template <int NPLANES, int N_PAIR, int STAGES_, int NBUF_, int CW_ = 16>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES, N_PAIR, STAGES_, NBUF_, CW_>::THREADS, 1)
-    gsb_multistep_pair_kernel(const __grid_constant__ TmaMaps maps, const MultiStepArgs args) {
-  using Cfg = PairStepCfg<NPLANES, N_PAIR, STAGES_, NBUF_, CW_>;
+template <int NPLANES, int N_PAIR, int STAGES_, int NBUF_, int CW_ = 16, bool Q4_ = false>
+__global__ void __cluster_dims__(2, 1, 1)
+    __launch_bounds__(PairStepCfg<NPLANES, N_PAIR, STAGES_, NBUF_, CW_, Q4_>::THREADS, 1)
+        gsb_multistep_pair_kernel(const __grid_constant__ TmaMaps maps, const MultiStepArgs args) {
+  using Cfg = PairStepCfg<NPLANES, N_PAIR, STAGES_, NBUF_, CW_, Q4_>;
+  constexpr int NACC = Cfg::NACC;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int NBUF = Cfg::NBUF;
   constexpr int CW = Cfg::CW;
@@ -117,13 +128,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
   ptx::cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if constexpr (Cfg::Q4) {  // unit E8M0 scale factors (127 = 2^0) in columns [COL_SF, 512)
+    if (warp >= 4 && warp < 8) {
+      uint32_t v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = 0x7F7F7F7Fu;
+      const uint32_t t = tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16) + Cfg::COL_SF;
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(t), "r"(v[0]),
+                   "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                   : "memory");
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(t + 8), "r"(v[0]),
+                   "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                   : "memory");
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync_all();
+    ptx::tc_fence_after();
+  }
 
   const int num_mp = args.num_m / 2;
   const int T2 = num_mp * args.num_n;  // pair tiles per step
   const int total = T2 * args.nsteps;
   const int pair = blockIdx.x >> 1;
   const int npairs = gridDim.x >> 1;
-  const int KB = args.kpad / Cfg::BK;
+  const int KB = args.kpad / (Cfg::BK * Cfg::KPB);
 
   if (warp == 0) {
     if (args.dbg < 2) {  // ------------------------------------------- operand producer (both CTAs)
@@ -164,14 +193,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
   } else if (warp == 1) {
     if (leader && args.dbg < 2) {  // --------------------------------- MMA issuer (leader CTA only)
       // whole warp walks the schedule; one elected lane issues (uniform descriptors)
-      constexpr uint32_t idesc_s = ptx::idesc_i8(256, N_PAIR, true, true);
+      constexpr uint32_t idesc_s = Cfg::Q4 ? ptx::idesc_mxf4(256, N_PAIR) : ptx::idesc_i8(256, N_PAIR, true, true);
       constexpr uint32_t idesc_u = ptx::idesc_i8(256, N_PAIR, true, false);
+      const uint32_t sf = tmem_base + Cfg::COL_SF;
       int stage = 0;
       uint32_t ph = 0;
       int lt = 0;
       for (int g = pair; g < total; g += npairs, ++lt) {
-        const int buf = lt & 1;
-        ptx::mbar_wait(tempty_bar(buf), ((lt >> 1) & 1) ^ 1u);
+        const int buf = lt % NACC;
+        ptx::mbar_wait(tempty_bar(buf), ((lt / NACC) & 1) ^ 1u);
         ptx::tc_fence_after();
         const uint32_t d_base = tmem_base + buf * Cfg::ACC_COLS;
         for (int kb = 0; kb < KB; ++kb) {
@@ -184,8 +214,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
               const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES);
               const uint32_t idesc = (NPLANES == 1 || pl == NPLANES - 1) ? idesc_s : idesc_u;
 #pragma unroll
-              for (int k = 0; k < Cfg::BK / 32; ++k)
-                ptx::mma_i8_pair(d_base + pl * N_PAIR, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+              for (int k = 0; k < Cfg::BK / 32; ++k) {  // 32 bytes per MMA (K = 32 int8 / 64 e2m1)
+                if constexpr (Cfg::Q4)
+                  ptx::mma_mxf4_pair(d_base, adesc + 2 * k, bdesc + 2 * k, idesc, sf, (kb | k) != 0);
+                else
+                  ptx::mma_i8_pair(d_base + pl * N_PAIR, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+              }
             }
             ptx::mma_commit_pair_mc(empty_bar(stage), 0x3);
           }
@@ -244,7 +278,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
           ptx::tma_store_2d_hint(&maps.P, sb + 2 * Cfg::ST_ARR, i0, r0, stream);
 #pragma unroll
           for (int pl = 0; pl < NPLANES; ++pl)
-            ptx::tma_store_2d_hint(gout, sb + 3 * Cfg::ST_ARR + pl * Cfg::ST_G, i0,
+            ptx::tma_store_2d_hint(gout, sb + 3 * Cfg::ST_ARR + pl * Cfg::ST_G, i0 / Cfg::KPB,
                                    (NPLANES == 1 ? 0 : pl * args.rpad) + r0, keep);
           ptx::bulk_commit();
           ptx::bulk_wait_read0();
@@ -270,8 +304,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
       const int s = g / T2;
       const int rbase = ((g % T2) / num_mp) * N_PAIR;  // first replica of this pair tile
       k.inv = __frcp_rn(static_cast<float>(args.M - (args.t_begin + static_cast<uint64_t>(s))));
-      const int buf = lt & 1;
-      if (args.dbg < 2) ptx::mbar_wait(tfull_bar(buf), (lt >> 1) & 1);
+      const int buf = lt % NACC;
+      if (args.dbg < 2) ptx::mbar_wait(tfull_bar(buf), (lt / NACC) & 1);
       __syncwarp();
       ptx::tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * Cfg::ACC_COLS;
@@ -284,7 +318,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
           ptx::tmem_ld<CWQ>(t_row + col0, v);
           ptx::tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < CWQ; ++j) F[j] = static_cast<float>(static_cast<int32_t>(v[j]));
+          for (int j = 0; j < CWQ; ++j)  // s32 (int8 MMA) or the same integer in f32 (e2m1 MMA; exact)
+            F[j] = Cfg::Q4 ? __uint_as_float(v[j]) : static_cast<float>(static_cast<int32_t>(v[j]));
         } else {
           long long tot[CWQ];
 #pragma unroll
@@ -315,7 +350,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairStepCfg<NPLANES,
           xs[idx] = xv;
           ys[idx] = yv;
           ps[idx] = pv;
-          if (NPLANES == 1) {
+          if constexpr (Cfg::Q4) {
+            // e2m1 codes (+1 = 0x2, -1 = 0xA) two spins per byte: lanes 2i, 2i+1 hold spins
+            // 2i, 2i+1 of column j; the even lane writes the byte (warp-uniform shuffle)
+            const uint32_t code = xv >= 0.0f ? 0x2u : 0xAu;
+            const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, code, 1);
+            if (!(lane & 1)) gs[(h * CWQ + j) * (Cfg::BM / 2) + (srow >> 1)] = static_cast<uint8_t>(code | (other << 4));
+          } else if (NPLANES == 1) {
             gs[idx] = static_cast<uint8_t>(sgn8(xv));
           } else {
             const uint32_t qv = static_cast<uint32_t>(quant30(xv));

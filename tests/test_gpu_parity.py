@@ -400,6 +400,20 @@ def test_e2m1_resident_equals_int8(solver, n, R, variant, values, monkeypatch):
     _same(a, c)
 
 
+def test_e2m1_streaming_large_n(solver, monkeypatch):
+    """Past the resident kernel's size limit the streaming pair kernel runs on e2m1 operands
+    (single-buffered accumulator, nibble-packed G written by the epilogue): bitwise equal to
+    its int8 form at n = 20001 (odd), R = 256 -- the C5 regime."""
+    n, R = 20001, 256
+    rng = np.random.default_rng(4)
+    J = np.triu(rng.choice(np.array([1, -1], np.int8), size=(n, n)), 1)
+    J = (J + J.T).astype(np.int8)
+    f4, a = _run_resident(solver, J, R, GDSB, 4, monkeypatch, True)
+    f8, b = _run_resident(solver, J, R, GDSB, 4, monkeypatch, False)
+    assert (f4, f8) == ("e2m1", "int8")
+    _same(a, b)
+
+
 def test_e2m1_large_fields_exact(solver, monkeypatch):
     """f32 accumulation of e2m1 products is exact while |F| < 2^24: J_ij = 6 everywhere
     off the diagonal and aligned spins drive |F| to 6 (n - 1) = 55,194 at n = 9200 (past
