@@ -29,6 +29,7 @@
 #include "step_tma.cuh"
 #include "step_pair.cuh"
 #include "step_resident.cuh"
+#include "step_resident_split.cuh"
 
 using namespace sbg;
 
@@ -117,6 +118,7 @@ struct sbg_ctx {
   TmaMaps rmaps160_sign[2];                  // resident-state pair kernel, NR 160 (B halves of 80 rows)
   TmaMaps qmaps_sign[2], qmaps160_sign[2];   // the same on e2m1 operands (J4; G as [rpad][npad / 2])
   TmaMaps pqmaps_sign[2];                    // streaming sign pair kernel on e2m1 operands
+  TmaMaps smaps_sign[2];                     // split resident kernel (B halves of 40 rows, G tiles of 80)
   unsigned long long* dE2p = nullptr;    // real-J readout: per-J-plane partial E2 [FX_NA][rpad]
   // CSR: spin-major working copies [npad][rp] and the ping-pong gathered operand (q int32 / sign int8)
   float *dXs = nullptr, *dYs = nullptr, *dPs = nullptr;
@@ -298,7 +300,8 @@ bool resident_ok(const sbg_ctx* ctx) {
 // Replica-group geometry of the resident kernel: 128-replica blocks, num_mp pairs per block,
 // as many blocks per group as CTA pairs fit (one CTA per SM).
 constexpr int RES_NR = 160;  // replicas per pair block of the default resident kernel (p in smem)
-constexpr int RES_NR_STAGES = 5;  // 32 of the 160 p columns stay in TMEM: room for a 5th ring stage
+constexpr int RES_NR_STAGES = 5;
+constexpr int RES_SPLIT_STAGES = 6;  // split kernel: 21 KB stages (J 16 KB + a half's G 5 KB)  // 32 of the 160 p columns stay in TMEM: room for a 5th ring stage
 
 void resident_geometry(const sbg_ctx* ctx, int64_t npad, int64_t rpad, int* rb_per_group, int* groups,
                        int nr = RES_NR) {
@@ -316,11 +319,17 @@ int resident_nr(const sbg_ctx* ctx) {
   return g160 < g128 ? RES_NR : 128;
 }
 
-template <int EPI, int CH, int ST = RES_STAGES, int NR = 128, bool Q4 = false>
+template <int EPI, int CH, int ST = RES_STAGES, int NR = 128, bool Q4 = false, bool SPLIT = false>
 int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms, int group0 = 0, int ngroups = -1,
                     const uint32_t* ready = nullptr) {
-  using Cfg = ResCfg<ST, EPI, CH, NR, false, Q4>;
-  auto kern = gsb_resident_pair_kernel<ST, EPI, CH, NR, Q4>;
+  // SPLIT: step_resident_split.cuh (e2m1, 160-replica blocks as two interleaved halves)
+  using Cfg = std::conditional_t<SPLIT, SplitCfg<ST>, ResCfg<ST, EPI, CH, NR, false, Q4>>;
+  auto kern = [] {
+    if constexpr (SPLIT)
+      return gsb_resident_split_kernel<ST>;
+    else
+      return gsb_resident_pair_kernel<ST, EPI, CH, NR, Q4>;
+  }();
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
   ResidentArgs a;
   std::memset(&a, 0, sizeof a);
@@ -355,7 +364,7 @@ int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms, 
     a.trace = trace;
     a.nsteps = std::min(a.nsteps, 4096);
   }
-  CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * num_n, ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * num_n * (SPLIT ? 2 : 1), ctx->stream));
   CK(launch_persistent(kern, 2 * num_mp * a.rb_per_group, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream, maps, a));
   ++ctx->launches;
   if (a.trace) {
@@ -539,6 +548,14 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
                 rcr = encode_2d(ctx, &qm.Gout[par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ par ^ 1], gv4, R,
                                 gb, 64, nrs[w], CU_TENSOR_MAP_SWIZZLE_NONE);
             }
+          }
+          TmaMaps& sq = ctx->smaps_sign[cur];
+          sq = ctx->qmaps160_sign[cur];
+          for (int par = 0; par < 2 && !rcr; ++par) {
+            rcr = encode_2d_u8(ctx, &sq.Gin[par], ctx->dG[cur ^ par], gb, rpad, 128, RES_NR / 4);
+            if (!rcr)
+              rcr = encode_2d(ctx, &sq.Gout[par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ par ^ 1], gv4, R, gb,
+                              64, RES_NR / 2, CU_TENSOR_MAP_SWIZZLE_NONE);
           }
           TmaMaps& pq = ctx->pqmaps_sign[cur];
           pq = ctx->maps_sign[cur];
@@ -1631,9 +1648,14 @@ static int launch_resident_default(sbg_ctx* ctx, int cur, const MultiStepArgs& a
                                    int* g_mode) {
   const bool q4 = ctx->dJ4 != nullptr && !ctx->sharded;
   *g_mode = q4 ? 0 : 1;
-  if (resident_nr(ctx) == RES_NR)
+  if (resident_nr(ctx) == RES_NR) {
+    // e2m1: the split kernel (two interleaved half-block chains; SBG_RES_SPLIT=0 = one chain, dev)
+    if (q4 && !getenv_is0("SBG_RES_SPLIT"))
+      return launch_resident<16, 4, RES_SPLIT_STAGES, RES_NR, true, true>(ctx, ctx->smaps_sign[cur], a, 0, groups,
+                                                                          ready);
     return q4 ? launch_resident<16, 4, RES_NR_STAGES, RES_NR, true>(ctx, ctx->qmaps160_sign[cur], a, 0, groups, ready)
               : launch_resident<16, 4, RES_NR_STAGES, RES_NR>(ctx, ctx->rmaps160_sign[cur], a, 0, groups, ready);
+  }
   return q4 ? launch_resident<16, 4, RES_STAGES, 128, true>(ctx, ctx->qmaps_sign[cur], a, 0, groups, ready)
             : launch_resident<16, 4>(ctx, ctx->rmaps_sign[cur], a, 0, groups, ready);
 }

@@ -1,0 +1,422 @@
+// The resident sign-variant kernel with each replica block split into two independent
+// HALVES whose step chains interleave (e2m1 operands only).
+//
+// step_resident.cuh runs one chain per replica block and step: G wait -> operand loads
+// -> MMA -> epilogue -> publish G_{t+1} -> the next G wait. Every link is latency (the
+// G exchange goes through L2 between all the CTA pairs of the block), so the tensor pipe
+// and the epilogue warps idle most of the step. The halves h = 0, 1 (replica columns
+// [80h, 80h + 80) of the 160-replica block) have separate accumulators, G tiles, done
+// counters and handshakes: while half 0 publishes and waits for its peers, half 1's MMAs
+// and epilogue run, and vice versa. J is streamed once per half-step (e2m1: 128 KB per
+// CTA), the price of decoupling the halves.
+//
+// Per CTA TMEM (lane = spin of this CTA): [0, 160) f32 accumulators (half h at 80h),
+// [160, 320) x, [320, 480) y, [496, 512) unit E8M0 scale factors; p in shared memory.
+// Warps: 0 operand producer, 1 MMA issuer (leader CTA), 2 TMEM allocator, 3 G publisher
+// (TMA store of a half's G tile, completion wait, release of done[2n + h]: off the
+// epilogue's path), 4..19 epilogue: warp (q = lane quadrant, g = column group) owns
+// columns 80h + 20g + [0, 20) of both halves.
+// Arithmetic is gsb_phase2 on the same integer fields: bitwise equal to step_resident.cuh.
+#pragma once
+
+#include <cstdint>
+#include <type_traits>
+#include <cuda.h>
+
+#include "gsb_phase.cuh"
+#include "ptx.cuh"
+#include "step_resident.cuh"
+#include "step_tma.cuh"
+
+namespace sbg {
+
+template <int STAGES_>
+struct SplitCfg {
+  static constexpr int BM = 128;                  // spins per CTA
+  static constexpr int BK = 128;                  // K bytes per stage (256 e2m1 elements)
+  static constexpr int NR = 160;                  // replicas per pair block
+  static constexpr int NH = 80;                   // replicas per half (UMMA N)
+  static constexpr int HB = NH / 2;               // B rows staged per CTA per half
+  static constexpr int A_BYTES = BM * BK;         // 16 KB
+  static constexpr int B_BYTES = HB * BK;         // 5 KB
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = STAGES_;
+  static constexpr int EPI_WARPS = 16;
+  static constexpr int COLS_H = NH / 4;           // columns per epilogue warp per half (20)
+  static constexpr int CH = 4;                    // columns per TMEM load chunk
+  static constexpr int CHUNKS = COLS_H / CH;      // 5
+  static constexpr int T_BYTES = NH * BM / 2;     // G tile of a half: [80][64] bytes
+  static constexpr int P_BYTES = NR * BM * 4;     // p [160][128] fp32
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
+  static constexpr int NUM_BARS = 2 * STAGES + 8;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 2 * T_BYTES + P_BYTES + 1024 + 8 * NUM_BARS + 64;
+  static constexpr uint32_t COL_X = NR, COL_Y = 2 * NR, COL_SF = 512 - 16;
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+  static_assert(A_BYTES % 1024 == 0 && B_BYTES % 1024 == 0, "SW128 stage alignment");
+};
+
+template <int STAGES_>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_>::THREADS, 1)
+    gsb_resident_split_kernel(const __grid_constant__ TmaMaps maps, const ResidentArgs args) {
+  using Cfg = SplitCfg<STAGES_>;
+  constexpr int CH = Cfg::CH;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = ptx::smem_u32(smem_raw);
+  const uint32_t base = (raw_addr + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (base - raw_addr);
+  const uint32_t a_base = base;
+  const uint32_t b_base = base + STAGES * Cfg::A_BYTES;
+  const uint32_t t_base = base + STAGES * Cfg::STAGE_BYTES;  // G tiles of the two halves
+  uint8_t* g_tile = smem + STAGES * Cfg::STAGE_BYTES;
+  float* p_smem = reinterpret_cast<float*>(g_tile + 2 * Cfg::T_BYTES);  // [160][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(g_tile + 2 * Cfg::T_BYTES + Cfg::P_BYTES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
+  auto bar = [&](int i) { return ptx::smem_u32(bars + i); };
+  auto full_bar = [&](int s) { return bar(s); };
+  auto empty_bar = [&](int s) { return bar(STAGES + s); };
+  auto tfull_bar = [&](int h) { return bar(2 * STAGES + h); };       // accumulator h ready (both CTAs)
+  auto tempty_bar = [&](int h) { return bar(2 * STAGES + 2 + h); };  // accumulator h drained (leader)
+  auto gfull_bar = [&](int h) { return bar(2 * STAGES + 4 + h); };   // G tile h written (local)
+  auto gempty_bar = [&](int h) { return bar(2 * STAGES + 6 + h); };  // G tile h stored (local)
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t cr = ptx::cluster_ctarank();
+  const bool leader = cr == 0;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(full_bar(s), 2);
+      ptx::mbar_init(empty_bar(s), 1);
+    }
+    for (int h = 0; h < 2; ++h) {
+      ptx::mbar_init(tfull_bar(h), 1);
+      ptx::mbar_init(tempty_bar(h), 2 * Cfg::EPI_WARPS);
+      ptx::mbar_init(gfull_bar(h), Cfg::EPI_WARPS);
+      ptx::mbar_init(gempty_bar(h), 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) {
+    ptx::tmem_alloc_pair(ptx::smem_u32(tmem_slot), 512);
+    ptx::tmem_relinquish_pair();
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync_all();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (warp >= 4 && warp < 8) {  // unit E8M0 scale factors (127 = 2^0)
+    uint32_t v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = 0x7F7F7F7Fu;
+    const uint32_t t = tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16) + Cfg::COL_SF;
+    ptx::tmem_st8(t, v);
+    ptx::tmem_st8(t + 8, v);
+    ptx::tmem_st_wait();
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync_all();
+  ptx::tc_fence_after();
+
+  const int num_mp = args.num_m / 2;
+  const int pair = blockIdx.x >> 1;
+  const int mp = pair % num_mp, rbk = pair / num_mp;
+  const int m_blk = 2 * mp + static_cast<int>(cr);
+  const int i0 = m_blk * Cfg::BM;
+  const int KB = args.npad / (2 * Cfg::BK);
+  const int num_n = (args.rpad + Cfg::NR - 1) / Cfg::NR;
+
+  if (warp == 0) {  // ------------------------------------------------ operand producer
+    if (ptx::elect_one()) {
+      ptx::prefetch_tmap(&maps.J);
+      ptx::prefetch_tmap(&maps.Gin[0]);
+      ptx::prefetch_tmap(&maps.Gin[1]);
+    }
+    int stage = 0;
+    uint32_t ph = 0;
+    const uint64_t keep = ptx::policy_evict_last();
+    for (int g = args.group0; g < args.group0 + args.groups; ++g) {
+      const int n_blk = g * args.rb_per_group + rbk;
+      if (n_blk >= num_n) break;
+      for (int s = 0; s < args.nsteps; ++s) {
+        const CUtensorMap* gin = &maps.Gin[s & 1];
+        for (int h = 0; h < 2; ++h) {
+          const int b_row0 = n_blk * Cfg::NR + h * Cfg::NH + static_cast<int>(cr) * Cfg::HB;
+          // J tiles do not depend on the step: requested before the dependency wait
+          int st0 = stage;
+          uint32_t ph0 = ph;
+          for (int kb = 0; kb < STAGES && kb < KB; ++kb) {
+            ptx::mbar_wait(empty_bar(st0), ph0 ^ 1u);
+            if (ptx::elect_one()) {
+              const uint32_t fb = ptx::mapa(full_bar(st0), 0);
+              ptx::mbar_expect_tx_cluster(fb, Cfg::A_BYTES);
+              ptx::tma_load_2d_pair_hint(a_base + st0 * Cfg::A_BYTES, &maps.J, fb, kb * Cfg::BK, m_blk * Cfg::BM,
+                                         keep);
+            }
+            __syncwarp();
+            if (++st0 == STAGES) {
+              st0 = 0;
+              ph0 ^= 1u;
+            }
+          }
+          // G_t half h of block n: released by all num_m CTAs (G_0 by the kernel at group start)
+          dep::wait_block(args.done, 2 * n_blk + h, 0u, static_cast<uint32_t>((s + 1) * args.num_m));
+          if (args.trace && pair == 0 && g == 0 && lane == 0 && h == 0) args.trace[(s * 2 + cr) * 8 + 0] = gtimer();
+          for (int kb = 0; kb < KB; ++kb) {
+            const bool pre = kb < STAGES;
+            if (!pre) ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
+            if (ptx::elect_one()) {
+              const uint32_t fb = ptx::mapa(full_bar(stage), 0);
+              ptx::mbar_arrive_expect_tx_cluster(fb, pre ? Cfg::B_BYTES : Cfg::STAGE_BYTES);
+              if (!pre)
+                ptx::tma_load_2d_pair_hint(a_base + stage * Cfg::A_BYTES, &maps.J, fb, kb * Cfg::BK, m_blk * Cfg::BM,
+                                           keep);
+              ptx::tma_load_2d_pair_hint(b_base + stage * Cfg::B_BYTES, gin, fb, kb * Cfg::BK, b_row0, keep);
+            }
+            __syncwarp();
+            if (++stage == STAGES) {
+              stage = 0;
+              ph ^= 1u;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {  // ------------------------------------------ MMA issuer (leader)
+    if (leader) {
+      constexpr uint32_t idesc = ptx::idesc_mxf4(256, Cfg::NH);
+      const uint32_t sf = tmem_base + Cfg::COL_SF;
+      int stage = 0;
+      uint32_t ph = 0;
+      int lt = 0;
+      for (int g = args.group0; g < args.group0 + args.groups; ++g) {
+        const int n_blk = g * args.rb_per_group + rbk;
+        if (n_blk >= num_n) break;
+        for (int s = 0; s < args.nsteps; ++s, ++lt) {
+          for (int h = 0; h < 2; ++h) {
+            ptx::mbar_wait(tempty_bar(h), (lt & 1) ^ 1u);
+            ptx::tc_fence_after();
+            const uint32_t d = tmem_base + h * Cfg::NH;
+            for (int kb = 0; kb < KB; kb += 2) {  // two K-stages per issue round
+              const int st0 = stage;
+              ptx::mbar_wait(full_bar(stage), ph);
+              if (++stage == STAGES) {
+                stage = 0;
+                ph ^= 1u;
+              }
+              const int st1 = stage;
+              const bool two = kb + 1 < KB;
+              if (two) {
+                ptx::mbar_wait(full_bar(stage), ph);
+                if (++stage == STAGES) {
+                  stage = 0;
+                  ph ^= 1u;
+                }
+              }
+              ptx::tc_fence_after();
+              if (ptx::elect_one()) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                  if (u == 1 && !two) break;
+                  const int st = u ? st1 : st0;
+                  const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + st * Cfg::A_BYTES);
+                  const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + st * Cfg::B_BYTES);
+#pragma unroll
+                  for (int k = 0; k < Cfg::BK / 32; ++k)
+                    ptx::mma_mxf4_pair(d, adesc + 2 * k, bdesc + 2 * k, idesc, sf, (kb | u | k) != 0);
+                  ptx::mma_commit_pair_mc(empty_bar(st), 0x3);
+                }
+              }
+              __syncwarp();
+            }
+            if (ptx::elect_one()) ptx::mma_commit_pair_mc(tfull_bar(h), 0x3);
+            __syncwarp();
+          }
+        }
+      }
+    }
+  } else if (warp == 3) {  // ------------------------------------------ G publisher
+    if (lane == 0) {
+      ptx::prefetch_tmap(&maps.Gout[0]);
+      ptx::prefetch_tmap(&maps.Gout[1]);
+      int pc = 0;  // publishes per half so far
+      for (int g = args.group0; g < args.group0 + args.groups; ++g) {
+        const int n_blk = g * args.rb_per_group + rbk;
+        if (n_blk >= num_n) break;
+        // G_0 (written by the state load into the buffer Gout[1] writes), then G_{s+1}
+        for (int s = -1; s < args.nsteps; ++s, ++pc) {
+          const int par = s < 0 ? 1 : (s & 1);
+          for (int h = 0; h < 2; ++h) {
+            ptx::mbar_wait(gfull_bar(h), pc & 1);
+            ptx::tma_store_2d(&maps.Gout[par], t_base + h * Cfg::T_BYTES, i0 / 2, n_blk * Cfg::NR + h * Cfg::NH);
+            ptx::bulk_commit();
+            ptx::bulk_wait_read0();
+            ptx::mbar_arrive(gempty_bar(h));  // tile reusable
+            ptx::bulk_wait0();
+            dep::fence_proxy_async_global();
+            __threadfence();
+            dep::release_add(args.done + 2 * n_blk + h, 1u);
+          }
+        }
+      }
+    }
+  } else if (warp >= 4) {  // ----------------------------------------- epilogue
+    const int q = warp & 3;
+    const int cg = (warp - 4) >> 2;
+    const int spin = i0 + q * 32 + lane;
+    const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+    const uint32_t tempty_leader0 = ptx::mapa(tempty_bar(0), 0), tempty_leader1 = ptx::mapa(tempty_bar(1), 0);
+    const int prow = q * 32 + lane;
+    const uint32_t g_sel = (lane & 1) ? 0x15u : 0x40u;
+    // e2m1 G codes of columns (col, col + 1) of half h, col even: lanes 2i, 2i+1 swap codes,
+    // the even lane writes column col's byte, the odd lane column col + 1's (warp-uniform)
+    auto put_g2 = [&](int h, int col, float xa, float xb) {
+      const uint32_t mine = (xa >= 0.0f ? 0x2u : 0xAu) | ((xb >= 0.0f ? 0x2u : 0xAu) << 8);
+      const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, mine, 1);
+      const uint32_t t = __byte_perm(mine, other, g_sel);
+      g_tile[h * Cfg::T_BYTES + (col + (lane & 1)) * (Cfg::BM / 2) + ((spin - i0) >> 1)] =
+          static_cast<uint8_t>(t | (t >> 4));
+    };
+    auto tile_written = [&](int h) {
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(gfull_bar(h));
+    };
+    int lt = 0, pc = 0;
+    for (int g = args.group0; g < args.group0 + args.groups; ++g) {
+      const int n_blk = g * args.rb_per_group + rbk;
+      if (n_blk >= num_n) break;
+      if (args.ready)
+        while (dep::ld_acquire_sys(args.ready + g) == 0) __nanosleep(256);
+      // load the block's state (x, y to TMEM, p to smem) and write G_0 = sgn(x_0)
+      for (int h = 0; h < 2; ++h) ptx::mbar_wait(gempty_bar(h), (pc & 1) ^ 1u);
+#pragma unroll 1
+      for (int u = 0; u < 2 * Cfg::COLS_H / 4; ++u) {  // 10 units of 4 columns: 5 per half
+        const int h = u / (Cfg::COLS_H / 4);
+        const int col = h * Cfg::NH + cg * Cfg::COLS_H + (u % (Cfg::COLS_H / 4)) * 4;
+        uint32_t vx[4], vy[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = n_blk * Cfg::NR + col + j;
+          const size_t off = static_cast<size_t>(r) * args.npad + spin;
+          const bool in = r < args.rpad;
+          vx[j] = in ? __float_as_uint(args.x[off]) : 0u;
+          vy[j] = in ? __float_as_uint(args.y[off]) : 0u;
+          p_smem[(col + j) * Cfg::BM + prow] = in ? args.p[off] : 0.0f;
+        }
+        ptx::tmem_st<4>(t_lane + Cfg::COL_X + col, vx);
+        ptx::tmem_st<4>(t_lane + Cfg::COL_Y + col, vy);
+        put_g2(h, col - h * Cfg::NH, __uint_as_float(vx[0]), __uint_as_float(vx[1]));
+        put_g2(h, col - h * Cfg::NH + 2, __uint_as_float(vx[2]), __uint_as_float(vx[3]));
+      }
+      ptx::tmem_st_wait();
+      tile_written(0);
+      tile_written(1);
+      ++pc;
+      for (int s = 0; s < args.nsteps; ++s, ++lt, ++pc) {
+        PhaseConsts k = args.k;
+        k.inv = __frcp_rn(static_cast<float>(args.M - (args.t_begin + static_cast<uint64_t>(s))));
+        const PhaseConsts2 k2(k, args.ident);
+        const float* arep = args.a_rep;
+        for (int h = 0; h < 2; ++h) {
+          ptx::mbar_wait(tfull_bar(h), lt & 1);
+          __syncwarp();
+          ptx::tc_fence_after();
+          const bool tr = args.trace && pair == 0 && g == 0 && warp == 4 && lane == 0 && h == 0;
+          if (tr) args.trace[(s * 2 + cr) * 8 + 1] = gtimer();
+          ptx::mbar_wait(gempty_bar(h), (pc & 1) ^ 1u);  // this half's G tile stored
+          const int c0 = h * Cfg::NH + cg * Cfg::COLS_H;     // this warp's first column of half h
+          uint32_t bf[2][CH], bx[2][CH], by[2][CH];
+          float bp[2][CH];
+          auto ld_chunk = [&](int c, int b) {
+            const uint32_t col = c0 + c * CH;
+            ptx::tmem_ld<CH>(t_lane + col, bf[b]);
+            ptx::tmem_ld<CH>(t_lane + Cfg::COL_X + col, bx[b]);
+            ptx::tmem_ld<CH>(t_lane + Cfg::COL_Y + col, by[b]);
+#pragma unroll
+            for (int j = 0; j < CH; ++j) bp[b][j] = p_smem[(col + j) * Cfg::BM + prow];
+          };
+          auto wait_chunk = [&](int b) {
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < CH; ++j) asm volatile("" : "+r"(bf[b][j]), "+r"(bx[b][j]), "+r"(by[b][j]), "+f"(bp[b][j]));
+          };
+          ld_chunk(0, 0);
+          wait_chunk(0);
+          auto chunks = [&](auto has_arep) {
+#pragma unroll
+            for (int c = 0; c < Cfg::CHUNKS; ++c) {
+              const int b = c & 1;
+              if (c + 1 < Cfg::CHUNKS) ld_chunk(c + 1, b ^ 1);
+              const int col = c0 + c * CH;
+#pragma unroll
+              for (int j = 0; j < CH; j += 2) {
+                float x0 = __uint_as_float(bx[b][j]), x1 = __uint_as_float(bx[b][j + 1]);
+                float y0 = __uint_as_float(by[b][j]), y1 = __uint_as_float(by[b][j + 1]);
+                float p0 = bp[b][j], p1 = bp[b][j + 1];
+                uint64_t a2 = k2.a;
+                if constexpr (decltype(has_arep)::value) {
+                  const int r = n_blk * Cfg::NR + col + j;
+                  a2 = f2::pk(arep[min(r, args.R - 1)], arep[min(r + 1, args.R - 1)]);
+                }
+                // the field: the exact integer in f32 (e2m1 MMA)
+                gsb_phase2(__uint_as_float(bf[b][j]), __uint_as_float(bf[b][j + 1]), x0, x1, y0, y1, p0, p1, k2, a2);
+                bx[b][j] = __float_as_uint(x0);
+                bx[b][j + 1] = __float_as_uint(x1);
+                by[b][j] = __float_as_uint(y0);
+                by[b][j + 1] = __float_as_uint(y1);
+                bp[b][j] = p0;
+                bp[b][j + 1] = p1;
+                put_g2(h, col - h * Cfg::NH + j, x0, x1);
+              }
+              ptx::tmem_st<CH>(t_lane + Cfg::COL_X + col, bx[b]);
+              ptx::tmem_st<CH>(t_lane + Cfg::COL_Y + col, by[b]);
+#pragma unroll
+              for (int j = 0; j < CH; ++j) p_smem[(col + j) * Cfg::BM + prow] = bp[b][j];
+              if (c + 1 < Cfg::CHUNKS) wait_chunk(b ^ 1);
+            }
+          };
+          if (arep)
+            chunks(std::true_type{});
+          else
+            chunks(std::false_type{});
+          ptx::tmem_st_wait();
+          // accumulator h consumed: the leader may issue this half's next MMAs
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_cluster(h ? tempty_leader1 : tempty_leader0);
+          tile_written(h);  // the publisher stores G_{t+1} of half h and releases done[2n + h]
+          if (tr) args.trace[(s * 2 + cr) * 8 + 2] = gtimer();
+        }
+      }
+      // write the block's state back (after the last step's TMEM stores)
+#pragma unroll 1
+      for (int u = 0; u < 2 * Cfg::COLS_H / 4; ++u) {
+        const int h = u / (Cfg::COLS_H / 4);
+        const int col = h * Cfg::NH + cg * Cfg::COLS_H + (u % (Cfg::COLS_H / 4)) * 4;
+        uint32_t vx[4], vy[4];
+        ptx::tmem_ld<4>(t_lane + Cfg::COL_X + col, vx);
+        ptx::tmem_ld<4>(t_lane + Cfg::COL_Y + col, vy);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = n_blk * Cfg::NR + col + j;
+          if (r >= args.rpad) continue;
+          const size_t off = static_cast<size_t>(r) * args.npad + spin;
+          args.x[off] = __uint_as_float(vx[j]);
+          args.y[off] = __uint_as_float(vy[j]);
+          args.p[off] = p_smem[(col + j) * Cfg::BM + prow];
+        }
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync_all();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc_pair(tmem_base, 512);
+}
+
+}  // namespace sbg
