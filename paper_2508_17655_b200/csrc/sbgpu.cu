@@ -301,7 +301,9 @@ bool resident_ok(const sbg_ctx* ctx) {
 // as many blocks per group as CTA pairs fit (one CTA per SM).
 constexpr int RES_NR = 160;  // replicas per pair block of the default resident kernel (p in smem)
 constexpr int RES_NR_STAGES = 5;
-constexpr int RES_SPLIT_STAGES = 6;  // split kernel: 21 KB stages (J 16 KB + a half's G 5 KB)  // 32 of the 160 p columns stay in TMEM: room for a 5th ring stage
+constexpr int RES_SPLIT_STAGES = 6;   // split kernel: 21 KB stages (J 16 KB + a half's G 5 KB)
+constexpr int RES_SPLITR_STAGES = 10;  // split kernel with p in registers: 80 KB more for the ring
+constexpr int RES_SPLITJ_STAGES = 16;  // ... and J resident (128 KB): 5 KB G-only stages  // 32 of the 160 p columns stay in TMEM: room for a 5th ring stage
 
 void resident_geometry(const sbg_ctx* ctx, int64_t npad, int64_t rpad, int* rb_per_group, int* groups,
                        int nr = RES_NR) {
@@ -319,14 +321,15 @@ int resident_nr(const sbg_ctx* ctx) {
   return g160 < g128 ? RES_NR : 128;
 }
 
-template <int EPI, int CH, int ST = RES_STAGES, int NR = 128, bool Q4 = false, bool SPLIT = false>
+template <int EPI, int CH, int ST = RES_STAGES, int NR = 128, bool Q4 = false, int SPLIT = 0>
 int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms, int group0 = 0, int ngroups = -1,
                     const uint32_t* ready = nullptr) {
-  // SPLIT: step_resident_split.cuh (e2m1, 160-replica blocks as two interleaved halves)
-  using Cfg = std::conditional_t<SPLIT, SplitCfg<ST>, ResCfg<ST, EPI, CH, NR, false, Q4>>;
+  // SPLIT: step_resident_split.cuh (e2m1, 160-replica blocks as two interleaved halves;
+  // 1 = p in shared memory, 2 = p in registers, 3 = p in registers and J resident in smem)
+  using Cfg = std::conditional_t<SPLIT != 0, SplitCfg<ST, SPLIT >= 2, SPLIT == 3>, ResCfg<ST, EPI, CH, NR, false, Q4>>;
   auto kern = [] {
-    if constexpr (SPLIT)
-      return gsb_resident_split_kernel<ST>;
+    if constexpr (SPLIT != 0)
+      return gsb_resident_split_kernel<ST, SPLIT >= 2, SPLIT == 3>;
     else
       return gsb_resident_pair_kernel<ST, EPI, CH, NR, Q4>;
   }();
@@ -364,7 +367,7 @@ int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms, 
     a.trace = trace;
     a.nsteps = std::min(a.nsteps, 4096);
   }
-  CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * num_n * (SPLIT ? 2 : 1), ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * num_n * (SPLIT != 0 ? 2 : 1), ctx->stream));
   CK(launch_persistent(kern, 2 * num_mp * a.rb_per_group, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream, maps, a));
   ++ctx->launches;
   if (a.trace) {
@@ -376,7 +379,8 @@ int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms, 
       for (int s = 0; s < a.nsteps; ++s)
         for (int c = 0; c < 2; ++c) {
           const unsigned long long* r = &h[size_t((s * 2 + c) * 8)];
-          fprintf(f, "%d %d %llu %llu %llu %llu %llu %llu %llu\n", s, c, r[0], r[1], r[2], r[3], r[4], r[5], r[6]);
+          fprintf(f, "%d %d %llu %llu %llu %llu %llu %llu %llu %llu\n", s, c, r[0], r[1], r[2], r[3], r[4], r[5], r[6],
+                  r[7]);
         }
       fclose(f);
     }
@@ -1650,9 +1654,15 @@ static int launch_resident_default(sbg_ctx* ctx, int cur, const MultiStepArgs& a
   *g_mode = q4 ? 0 : 1;
   if (resident_nr(ctx) == RES_NR) {
     // e2m1: the split kernel (two interleaved half-block chains; SBG_RES_SPLIT=0 = one chain, dev)
-    if (q4 && !getenv_is0("SBG_RES_SPLIT"))
-      return launch_resident<16, 4, RES_SPLIT_STAGES, RES_NR, true, true>(ctx, ctx->smaps_sign[cur], a, 0, groups,
-                                                                          ready);
+    if (q4 && dev_knob("SBG_RES_SPLIT") == 1)
+      return launch_resident<16, 4, RES_SPLIT_STAGES, RES_NR, true, 1>(ctx, ctx->smaps_sign[cur], a, 0, groups,
+                                                                       ready);
+    if (q4 && (dev_knob("SBG_RES_SPLIT") == 2 || (ctx->npad > 2048 && !getenv_is0("SBG_RES_SPLIT"))))
+      return launch_resident<16, 4, RES_SPLITR_STAGES, RES_NR, true, 2>(ctx, ctx->smaps_sign[cur], a, 0, groups,
+                                                                        ready);
+    if (q4 && !getenv_is0("SBG_RES_SPLIT"))  // npad <= 2048: J resident in shared memory
+      return launch_resident<16, 4, RES_SPLITJ_STAGES, RES_NR, true, 3>(ctx, ctx->smaps_sign[cur], a, 0, groups,
+                                                                        ready);
     return q4 ? launch_resident<16, 4, RES_NR_STAGES, RES_NR, true>(ctx, ctx->qmaps160_sign[cur], a, 0, groups, ready)
               : launch_resident<16, 4, RES_NR_STAGES, RES_NR>(ctx, ctx->rmaps160_sign[cur], a, 0, groups, ready);
   }

@@ -30,8 +30,16 @@
 
 namespace sbg {
 
-template <int STAGES_>
+// PREG_: p lives in the epilogue threads' registers (40 per thread, statically indexed)
+// instead of shared memory, which frees 80 KB for a deeper operand ring.
+// JRES_: J resident in shared memory for the whole launch (npad <= 2048: a CTA's 128 rows
+// are 8 stages of 16 KB, 128 KB e2m1); the ring then carries only G, so no J bytes cross
+// L2 after the first load and a half-step's MMAs wait only for its G.
+template <int STAGES_, bool PREG_ = false, bool JRES_ = false>
 struct SplitCfg {
+  static constexpr bool PREG = PREG_;
+  static constexpr bool JRES = JRES_;
+  static constexpr int J_SLOTS = JRES ? 8 : 0;    // resident J tiles (K <= 2048)
   static constexpr int BM = 128;                  // spins per CTA
   static constexpr int BK = 128;                  // K bytes per stage (256 e2m1 elements)
   static constexpr int NR = 160;                  // replicas per pair block
@@ -39,36 +47,39 @@ struct SplitCfg {
   static constexpr int HB = NH / 2;               // B rows staged per CTA per half
   static constexpr int A_BYTES = BM * BK;         // 16 KB
   static constexpr int B_BYTES = HB * BK;         // 5 KB
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGE_BYTES = (JRES ? 0 : A_BYTES) + B_BYTES;
   static constexpr int STAGES = STAGES_;
+  static constexpr int RND = STAGES_ >= 8 ? 4 : 2;  // K-stages per MMA issue round
   static constexpr int EPI_WARPS = 16;
   static constexpr int COLS_H = NH / 4;           // columns per epilogue warp per half (20)
   static constexpr int CH = 4;                    // columns per TMEM load chunk
   static constexpr int CHUNKS = COLS_H / CH;      // 5
   static constexpr int T_BYTES = NH * BM / 2;     // G tile of a half: [80][64] bytes
-  static constexpr int P_BYTES = NR * BM * 4;     // p [160][128] fp32
+  static constexpr int P_BYTES = PREG ? 0 : NR * BM * 4;  // p [160][128] fp32
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
-  static constexpr int NUM_BARS = 2 * STAGES + 8;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 2 * T_BYTES + P_BYTES + 1024 + 8 * NUM_BARS + 64;
+  static constexpr int NUM_BARS = 2 * STAGES + 9;
+  static constexpr int SMEM_BYTES =
+      J_SLOTS * A_BYTES + STAGES * STAGE_BYTES + 2 * T_BYTES + P_BYTES + 1024 + 8 * NUM_BARS + 64;
   static constexpr uint32_t COL_X = NR, COL_Y = 2 * NR, COL_SF = 512 - 16;
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static_assert(A_BYTES % 1024 == 0 && B_BYTES % 1024 == 0, "SW128 stage alignment");
 };
 
-template <int STAGES_>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_>::THREADS, 1)
+template <int STAGES_, bool PREG_ = false, bool JRES_ = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_, PREG_, JRES_>::THREADS, 1)
     gsb_resident_split_kernel(const __grid_constant__ TmaMaps maps, const ResidentArgs args) {
-  using Cfg = SplitCfg<STAGES_>;
+  using Cfg = SplitCfg<STAGES_, PREG_, JRES_>;
   constexpr int CH = Cfg::CH;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = ptx::smem_u32(smem_raw);
   const uint32_t base = (raw_addr + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base - raw_addr);
+  // JRES: [J_SLOTS] resident J tiles, then the G stages; else [STAGES] J tiles, [STAGES] G tiles
   const uint32_t a_base = base;
-  const uint32_t b_base = base + STAGES * Cfg::A_BYTES;
-  const uint32_t t_base = base + STAGES * Cfg::STAGE_BYTES;  // G tiles of the two halves
-  uint8_t* g_tile = smem + STAGES * Cfg::STAGE_BYTES;
+  const uint32_t b_base = base + (Cfg::JRES ? Cfg::J_SLOTS : STAGES) * Cfg::A_BYTES;
+  const uint32_t t_base = base + Cfg::J_SLOTS * Cfg::A_BYTES + STAGES * Cfg::STAGE_BYTES;  // G tiles of the halves
+  uint8_t* g_tile = smem + (t_base - base);
   float* p_smem = reinterpret_cast<float*>(g_tile + 2 * Cfg::T_BYTES);  // [160][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(g_tile + 2 * Cfg::T_BYTES + Cfg::P_BYTES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
@@ -79,6 +90,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_>::T
   auto tempty_bar = [&](int h) { return bar(2 * STAGES + 2 + h); };  // accumulator h drained (leader)
   auto gfull_bar = [&](int h) { return bar(2 * STAGES + 4 + h); };   // G tile h written (local)
   auto gempty_bar = [&](int h) { return bar(2 * STAGES + 6 + h); };  // G tile h stored (local)
+  const uint32_t jfull_bar = bar(2 * STAGES + 8);                     // JRES: J resident (leader)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -96,6 +108,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_>::T
       ptx::mbar_init(gfull_bar(h), Cfg::EPI_WARPS);
       ptx::mbar_init(gempty_bar(h), 1);
     }
+    ptx::mbar_init(jfull_bar, 2);
     ptx::fence_mbar_init();
   }
   if (warp == 2) {
@@ -136,6 +149,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_>::T
     int stage = 0;
     uint32_t ph = 0;
     const uint64_t keep = ptx::policy_evict_last();
+    if constexpr (Cfg::JRES) {  // this CTA's 128 rows of J, once per launch
+      if (ptx::elect_one()) {
+        const uint32_t fb = ptx::mapa(jfull_bar, 0);
+        ptx::mbar_arrive_expect_tx_cluster(fb, KB * Cfg::A_BYTES);
+        for (int kb = 0; kb < KB; ++kb)
+          ptx::tma_load_2d_pair_hint(a_base + kb * Cfg::A_BYTES, &maps.J, fb, kb * Cfg::BK, m_blk * Cfg::BM, keep);
+      }
+      __syncwarp();
+    }
     for (int g = args.group0; g < args.group0 + args.groups; ++g) {
       const int n_blk = g * args.rb_per_group + rbk;
       if (n_blk >= num_n) break;
@@ -146,7 +168,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_>::T
           // J tiles do not depend on the step: requested before the dependency wait
           int st0 = stage;
           uint32_t ph0 = ph;
-          for (int kb = 0; kb < STAGES && kb < KB; ++kb) {
+          for (int kb = 0; !Cfg::JRES && kb < STAGES && kb < KB; ++kb) {
             ptx::mbar_wait(empty_bar(st0), ph0 ^ 1u);
             if (ptx::elect_one()) {
               const uint32_t fb = ptx::mapa(full_bar(st0), 0);
@@ -164,12 +186,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_>::T
           dep::wait_block(args.done, 2 * n_blk + h, 0u, static_cast<uint32_t>((s + 1) * args.num_m));
           if (args.trace && pair == 0 && g == 0 && lane == 0 && h == 0) args.trace[(s * 2 + cr) * 8 + 0] = gtimer();
           for (int kb = 0; kb < KB; ++kb) {
-            const bool pre = kb < STAGES;
+            const bool pre = kb < STAGES && !Cfg::JRES;
             if (!pre) ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
             if (ptx::elect_one()) {
               const uint32_t fb = ptx::mapa(full_bar(stage), 0);
               ptx::mbar_arrive_expect_tx_cluster(fb, pre ? Cfg::B_BYTES : Cfg::STAGE_BYTES);
-              if (!pre)
+              if (!pre && !Cfg::JRES)
                 ptx::tma_load_2d_pair_hint(a_base + stage * Cfg::A_BYTES, &maps.J, fb, kb * Cfg::BK, m_blk * Cfg::BM,
                                            keep);
               ptx::tma_load_2d_pair_hint(b_base + stage * Cfg::B_BYTES, gin, fb, kb * Cfg::BK, b_row0, keep);
@@ -190,6 +212,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_>::T
       int stage = 0;
       uint32_t ph = 0;
       int lt = 0;
+      if constexpr (Cfg::JRES) ptx::mbar_wait(jfull_bar, 0);
       for (int g = args.group0; g < args.group0 + args.groups; ++g) {
         const int n_blk = g * args.rb_per_group + rbk;
         if (n_blk >= num_n) break;
@@ -198,34 +221,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_>::T
             ptx::mbar_wait(tempty_bar(h), (lt & 1) ^ 1u);
             ptx::tc_fence_after();
             const uint32_t d = tmem_base + h * Cfg::NH;
-            for (int kb = 0; kb < KB; kb += 2) {  // two K-stages per issue round
-              const int st0 = stage;
-              ptx::mbar_wait(full_bar(stage), ph);
-              if (++stage == STAGES) {
-                stage = 0;
-                ph ^= 1u;
-              }
-              const int st1 = stage;
-              const bool two = kb + 1 < KB;
-              if (two) {
-                ptx::mbar_wait(full_bar(stage), ph);
-                if (++stage == STAGES) {
-                  stage = 0;
-                  ph ^= 1u;
+            const bool trm = args.trace && pair == 0 && g == 0 && h == 0;
+            // RND K-stages per issue round: one handshake (wait, fence, elect) per round; a
+            // half-step's G loads are issued together, so its stages land close together
+            constexpr int RND = Cfg::RND;
+            for (int kb = 0; kb < KB; kb += RND) {
+              int sts[RND];
+              const int cnt = KB - kb < RND ? KB - kb : RND;
+#pragma unroll
+              for (int u = 0; u < RND; ++u) {
+                if (u < cnt) {
+                  ptx::mbar_wait(full_bar(stage), ph);
+                  sts[u] = stage;
+                  if (++stage == STAGES) {
+                    stage = 0;
+                    ph ^= 1u;
+                  }
                 }
               }
+              if (trm && kb == 0 && lane == 0) args.trace[(s * 2) * 8 + 6] = gtimer();
               ptx::tc_fence_after();
               if (ptx::elect_one()) {
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                  if (u == 1 && !two) break;
-                  const int st = u ? st1 : st0;
-                  const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + st * Cfg::A_BYTES);
-                  const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + st * Cfg::B_BYTES);
+                for (int u = 0; u < RND; ++u) {
+                  if (u < cnt) {
+                    const uint64_t adesc =
+                        ptx::smem_desc_k_sw128(a_base + (Cfg::JRES ? kb + u : sts[u]) * Cfg::A_BYTES);
+                    const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + sts[u] * Cfg::B_BYTES);
 #pragma unroll
-                  for (int k = 0; k < Cfg::BK / 32; ++k)
-                    ptx::mma_mxf4_pair(d, adesc + 2 * k, bdesc + 2 * k, idesc, sf, (kb | u | k) != 0);
-                  ptx::mma_commit_pair_mc(empty_bar(st), 0x3);
+                    for (int k = 0; k < Cfg::BK / 32; ++k)
+                      ptx::mma_mxf4_pair(d, adesc + 2 * k, bdesc + 2 * k, idesc, sf, (kb | u | k) != 0);
+                    ptx::mma_commit_pair_mc(empty_bar(sts[u]), 0x3);
+                  }
                 }
               }
               __syncwarp();
@@ -249,14 +276,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_>::T
           const int par = s < 0 ? 1 : (s & 1);
           for (int h = 0; h < 2; ++h) {
             ptx::mbar_wait(gfull_bar(h), pc & 1);
+            const bool tr = args.trace && pair == 0 && g == 0 && h == 0 && s >= 0;
+            if (tr) args.trace[(s * 2 + cr) * 8 + 3] = gtimer();
             ptx::tma_store_2d(&maps.Gout[par], t_base + h * Cfg::T_BYTES, i0 / 2, n_blk * Cfg::NR + h * Cfg::NH);
             ptx::bulk_commit();
             ptx::bulk_wait_read0();
             ptx::mbar_arrive(gempty_bar(h));  // tile reusable
             ptx::bulk_wait0();
+            if (tr) args.trace[(s * 2 + cr) * 8 + 4] = gtimer();
             dep::fence_proxy_async_global();
-            __threadfence();
+            if (tr) args.trace[(s * 2 + cr) * 8 + 7] = gtimer();
+            // red.release orders the completed (proxy-fenced) tile writes before the count
             dep::release_add(args.done + 2 * n_blk + h, 1u);
+            if (tr) args.trace[(s * 2 + cr) * 8 + 5] = gtimer();
           }
         }
       }
@@ -269,6 +301,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_>::T
     const uint32_t tempty_leader0 = ptx::mapa(tempty_bar(0), 0), tempty_leader1 = ptx::mapa(tempty_bar(1), 0);
     const int prow = q * 32 + lane;
     const uint32_t g_sel = (lane & 1) ? 0x15u : 0x40u;
+    // p of (half h, chunk c, column j of the chunk): registers (PREG) or shared memory
+    float preg[Cfg::PREG ? 2 : 1][Cfg::PREG ? Cfg::CHUNKS : 1][CH];
+    auto p_ref = [&](int h, int c, int j) -> float& {
+      if constexpr (Cfg::PREG)
+        return preg[h][c][j];
+      else
+        return p_smem[(h * Cfg::NH + cg * Cfg::COLS_H + c * CH + j) * Cfg::BM + prow];
+    };
     // e2m1 G codes of columns (col, col + 1) of half h, col even: lanes 2i, 2i+1 swap codes,
     // the even lane writes column col's byte, the odd lane column col + 1's (warp-uniform)
     auto put_g2 = [&](int h, int col, float xa, float xb) {
@@ -291,10 +331,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_>::T
         while (dep::ld_acquire_sys(args.ready + g) == 0) __nanosleep(256);
       // load the block's state (x, y to TMEM, p to smem) and write G_0 = sgn(x_0)
       for (int h = 0; h < 2; ++h) ptx::mbar_wait(gempty_bar(h), (pc & 1) ^ 1u);
-#pragma unroll 1
-      for (int u = 0; u < 2 * Cfg::COLS_H / 4; ++u) {  // 10 units of 4 columns: 5 per half
-        const int h = u / (Cfg::COLS_H / 4);
-        const int col = h * Cfg::NH + cg * Cfg::COLS_H + (u % (Cfg::COLS_H / 4)) * 4;
+#pragma unroll
+      for (int u = 0; u < 2 * Cfg::CHUNKS; ++u) {  // 10 units of 4 columns: 5 per half
+        const int h = u / Cfg::CHUNKS, c = u % Cfg::CHUNKS;
+        const int col = h * Cfg::NH + cg * Cfg::COLS_H + c * CH;
         uint32_t vx[4], vy[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -303,7 +343,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_>::T
           const bool in = r < args.rpad;
           vx[j] = in ? __float_as_uint(args.x[off]) : 0u;
           vy[j] = in ? __float_as_uint(args.y[off]) : 0u;
-          p_smem[(col + j) * Cfg::BM + prow] = in ? args.p[off] : 0.0f;
+          p_ref(h, c, j) = in ? args.p[off] : 0.0f;
         }
         ptx::tmem_st<4>(t_lane + Cfg::COL_X + col, vx);
         ptx::tmem_st<4>(t_lane + Cfg::COL_Y + col, vy);
@@ -319,6 +359,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_>::T
         k.inv = __frcp_rn(static_cast<float>(args.M - (args.t_begin + static_cast<uint64_t>(s))));
         const PhaseConsts2 k2(k, args.ident);
         const float* arep = args.a_rep;
+#pragma unroll
         for (int h = 0; h < 2; ++h) {
           ptx::mbar_wait(tfull_bar(h), lt & 1);
           __syncwarp();
@@ -335,7 +376,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_>::T
             ptx::tmem_ld<CH>(t_lane + Cfg::COL_X + col, bx[b]);
             ptx::tmem_ld<CH>(t_lane + Cfg::COL_Y + col, by[b]);
 #pragma unroll
-            for (int j = 0; j < CH; ++j) bp[b][j] = p_smem[(col + j) * Cfg::BM + prow];
+            for (int j = 0; j < CH; ++j) bp[b][j] = p_ref(h, c, j);
           };
           auto wait_chunk = [&](int b) {
             ptx::tmem_ld_wait();
@@ -373,7 +414,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_>::T
               ptx::tmem_st<CH>(t_lane + Cfg::COL_X + col, bx[b]);
               ptx::tmem_st<CH>(t_lane + Cfg::COL_Y + col, by[b]);
 #pragma unroll
-              for (int j = 0; j < CH; ++j) p_smem[(col + j) * Cfg::BM + prow] = bp[b][j];
+              for (int j = 0; j < CH; ++j) p_ref(h, c, j) = bp[b][j];
               if (c + 1 < Cfg::CHUNKS) wait_chunk(b ^ 1);
             }
           };
@@ -391,10 +432,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_>::T
         }
       }
       // write the block's state back (after the last step's TMEM stores)
-#pragma unroll 1
-      for (int u = 0; u < 2 * Cfg::COLS_H / 4; ++u) {
-        const int h = u / (Cfg::COLS_H / 4);
-        const int col = h * Cfg::NH + cg * Cfg::COLS_H + (u % (Cfg::COLS_H / 4)) * 4;
+#pragma unroll
+      for (int u = 0; u < 2 * Cfg::CHUNKS; ++u) {
+        const int h = u / Cfg::CHUNKS, c = u % Cfg::CHUNKS;
+        const int col = h * Cfg::NH + cg * Cfg::COLS_H + c * CH;
         uint32_t vx[4], vy[4];
         ptx::tmem_ld<4>(t_lane + Cfg::COL_X + col, vx);
         ptx::tmem_ld<4>(t_lane + Cfg::COL_Y + col, vy);
@@ -406,7 +447,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SplitCfg<STAGES_>::T
           const size_t off = static_cast<size_t>(r) * args.npad + spin;
           args.x[off] = __uint_as_float(vx[j]);
           args.y[off] = __uint_as_float(vy[j]);
-          args.p[off] = p_smem[(col + j) * Cfg::BM + prow];
+          args.p[off] = p_ref(h, c, j);
         }
       }
     }

@@ -190,6 +190,8 @@ void run() {
 }
 
 int main() {
+  run<48>();
+  run<80>();
   run<128>();
   run<160>();
   run<256>();
