@@ -29,7 +29,7 @@
 #include "step_tma.cuh"
 #include "step_pair.cuh"
 #include "step_resident.cuh"
-#include "step_resident_split.cuh"
+#include "step_resident_parts.cuh"
 
 using namespace sbg;
 
@@ -118,7 +118,6 @@ struct sbg_ctx {
   TmaMaps rmaps160_sign[2];                  // resident-state pair kernel, NR 160 (B halves of 80 rows)
   TmaMaps qmaps_sign[2], qmaps160_sign[2];   // the same on e2m1 operands (J4; G as [rpad][npad / 2])
   TmaMaps pqmaps_sign[2];                    // streaming sign pair kernel on e2m1 operands
-  TmaMaps smaps_sign[2];                     // split resident kernel (B halves of 40 rows, G tiles of 80)
   unsigned long long* dE2p = nullptr;    // real-J readout: per-J-plane partial E2 [FX_NA][rpad]
   // CSR: spin-major working copies [npad][rp] and the ping-pong gathered operand (q int32 / sign int8)
   float *dXs = nullptr, *dYs = nullptr, *dPs = nullptr;
@@ -300,10 +299,7 @@ bool resident_ok(const sbg_ctx* ctx) {
 // Replica-group geometry of the resident kernel: 128-replica blocks, num_mp pairs per block,
 // as many blocks per group as CTA pairs fit (one CTA per SM).
 constexpr int RES_NR = 160;  // replicas per pair block of the default resident kernel (p in smem)
-constexpr int RES_NR_STAGES = 5;
-constexpr int RES_SPLIT_STAGES = 6;   // split kernel: 21 KB stages (J 16 KB + a half's G 5 KB)
-constexpr int RES_SPLITR_STAGES = 10;  // split kernel with p in registers: 80 KB more for the ring
-constexpr int RES_SPLITJ_STAGES = 16;  // ... and J resident (128 KB): 5 KB G-only stages  // 32 of the 160 p columns stay in TMEM: room for a 5th ring stage
+constexpr int RES_NR_STAGES = 5;  // 32 of the 160 p columns stay in TMEM: room for a 5th ring stage
 
 void resident_geometry(const sbg_ctx* ctx, int64_t npad, int64_t rpad, int* rb_per_group, int* groups,
                        int nr = RES_NR) {
@@ -321,15 +317,17 @@ int resident_nr(const sbg_ctx* ctx) {
   return g160 < g128 ? RES_NR : 128;
 }
 
-template <int EPI, int CH, int ST = RES_STAGES, int NR = 128, bool Q4 = false, int SPLIT = 0>
-int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms, int group0 = 0, int ngroups = -1,
+template <int EPI, int CH, int ST = RES_STAGES, int NR = 128, bool Q4 = false, int PARTS = 0, bool JRES = false,
+          class Maps = TmaMaps>
+int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int group0 = 0, int ngroups = -1,
                     const uint32_t* ready = nullptr) {
-  // SPLIT: step_resident_split.cuh (e2m1, 160-replica blocks as two interleaved halves;
-  // 1 = p in shared memory, 2 = p in registers, 3 = p in registers and J resident in smem)
-  using Cfg = std::conditional_t<SPLIT != 0, SplitCfg<ST, SPLIT >= 2, SPLIT == 3>, ResCfg<ST, EPI, CH, NR, false, Q4>>;
+  // PARTS > 0: step_resident_parts.cuh (e2m1, 160-replica blocks as PARTS interleaved column
+  // parts; JRES = J resident in shared memory); else step_resident.cuh
+  using Cfg = std::conditional_t<PARTS != 0, PartsCfg<ST, JRES, (PARTS > 0 ? PARTS : 2)>,
+                                 ResCfg<ST, EPI, CH, NR, false, Q4>>;
   auto kern = [] {
-    if constexpr (SPLIT != 0)
-      return gsb_resident_split_kernel<ST, SPLIT >= 2, SPLIT == 3>;
+    if constexpr (PARTS != 0)
+      return gsb_resident_parts_kernel<ST, JRES, PARTS>;
     else
       return gsb_resident_pair_kernel<ST, EPI, CH, NR, Q4>;
   }();
@@ -367,7 +365,9 @@ int launch_resident(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& ms, 
     a.trace = trace;
     a.nsteps = std::min(a.nsteps, 4096);
   }
-  CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * num_n * (SPLIT != 0 ? 2 : 1), ctx->stream));
+  // done counters per replica block (one per part)
+  const int counters = PARTS != 0 ? PARTS : 1;
+  CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * num_n * counters, ctx->stream));
   CK(launch_persistent(kern, 2 * num_mp * a.rb_per_group, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream, maps, a));
   ++ctx->launches;
   if (a.trace) {
@@ -552,14 +552,6 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
                 rcr = encode_2d(ctx, &qm.Gout[par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ par ^ 1], gv4, R,
                                 gb, 64, nrs[w], CU_TENSOR_MAP_SWIZZLE_NONE);
             }
-          }
-          TmaMaps& sq = ctx->smaps_sign[cur];
-          sq = ctx->qmaps160_sign[cur];
-          for (int par = 0; par < 2 && !rcr; ++par) {
-            rcr = encode_2d_u8(ctx, &sq.Gin[par], ctx->dG[cur ^ par], gb, rpad, 128, RES_NR / 4);
-            if (!rcr)
-              rcr = encode_2d(ctx, &sq.Gout[par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ par ^ 1], gv4, R, gb,
-                              64, RES_NR / 2, CU_TENSOR_MAP_SWIZZLE_NONE);
           }
           TmaMaps& pq = ctx->pqmaps_sign[cur];
           pq = ctx->maps_sign[cur];
@@ -1646,6 +1638,33 @@ static int run_tail(sbg_ctx* ctx, const sbg_params* prm, float* x_final, int8_t*
   return SBG_OK;
 }
 
+// Tensor maps of the parts kernel for G-buffer parity cur and part widths w0 (class 0), w1 (class 1).
+static int encode_part_maps(sbg_ctx* ctx, PartMaps* pm, int cur, int w0, int w1) {
+  pm->J = ctx->tmJ4;
+  const uint64_t gb = uint64_t(ctx->npad / 2), gv4 = uint64_t((ctx->n + 1) / 2);
+  const int ws[2] = {w0, w1};
+  for (int c = 0; c < 2; ++c)
+    for (int par = 0; par < 2; ++par) {
+      int rc = encode_2d_u8(ctx, &pm->Gin[c][par], ctx->dG[cur ^ par], gb, uint64_t(ctx->rpad), 128, uint32_t(ws[c] / 2));
+      if (!rc)
+        rc = encode_2d(ctx, &pm->Gout[c][par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ par ^ 1], gv4,
+                       uint64_t(ctx->R), gb, 64, uint32_t(ws[c]), CU_TENSOR_MAP_SWIZZLE_NONE);
+      if (rc) return rc;
+    }
+  return SBG_OK;
+}
+
+extern "C++" {
+template <int PARTS, int ST, bool JRES>
+int launch_parts(sbg_ctx* ctx, int cur, const MultiStepArgs& a, int groups, const uint32_t* ready) {
+  using T = PartTable<PARTS>;
+  PartMaps pm;
+  const int rc = encode_part_maps(ctx, &pm, cur, T::W[0], T::W[PARTS - 1]);
+  if (rc) return rc;
+  return launch_resident<16, 4, ST, RES_NR, true, PARTS, JRES>(ctx, pm, a, 0, groups, ready);
+}
+}
+
 // The default resident launch: NR 160 when it cuts the group count, e2m1 operands when J
 // has an e2m1 copy. Returns the G-buffer mode left behind (1 = int8 sign plane, 0 = e2m1).
 static int launch_resident_default(sbg_ctx* ctx, int cur, const MultiStepArgs& a, int groups, const uint32_t* ready,
@@ -1653,16 +1672,16 @@ static int launch_resident_default(sbg_ctx* ctx, int cur, const MultiStepArgs& a
   const bool q4 = ctx->dJ4 != nullptr && !ctx->sharded;
   *g_mode = q4 ? 0 : 1;
   if (resident_nr(ctx) == RES_NR) {
-    // e2m1: the split kernel (two interleaved half-block chains; SBG_RES_SPLIT=0 = one chain, dev)
-    if (q4 && dev_knob("SBG_RES_SPLIT") == 1)
-      return launch_resident<16, 4, RES_SPLIT_STAGES, RES_NR, true, 1>(ctx, ctx->smaps_sign[cur], a, 0, groups,
-                                                                       ready);
-    if (q4 && (dev_knob("SBG_RES_SPLIT") == 2 || (ctx->npad > 2048 && !getenv_is0("SBG_RES_SPLIT"))))
-      return launch_resident<16, 4, RES_SPLITR_STAGES, RES_NR, true, 2>(ctx, ctx->smaps_sign[cur], a, 0, groups,
-                                                                        ready);
-    if (q4 && !getenv_is0("SBG_RES_SPLIT"))  // npad <= 2048: J resident in shared memory
-      return launch_resident<16, 4, RES_SPLITJ_STAGES, RES_NR, true, 3>(ctx, ctx->smaps_sign[cur], a, 0, groups,
-                                                                        ready);
+    // e2m1: the parts kernel, two interleaved half-block chains (SBG_RES_SPLIT=0 = one chain,
+    // SBG_RES_PARTS=3/4 = more, narrower parts: dev). npad <= 2048: J resident in shared memory.
+    if (q4 && !getenv_is0("SBG_RES_SPLIT")) {
+      if (ctx->npad > 2048) return launch_parts<2, 10, false>(ctx, cur, a, groups, ready);
+      switch (dev_knob("SBG_RES_PARTS")) {
+        case 3: return launch_parts<3, 20, true>(ctx, cur, a, groups, ready);
+        case 4: return launch_parts<4, 24, true>(ctx, cur, a, groups, ready);
+        default: return launch_parts<2, 16, true>(ctx, cur, a, groups, ready);
+      }
+    }
     return q4 ? launch_resident<16, 4, RES_NR_STAGES, RES_NR, true>(ctx, ctx->qmaps160_sign[cur], a, 0, groups, ready)
               : launch_resident<16, 4, RES_NR_STAGES, RES_NR>(ctx, ctx->rmaps160_sign[cur], a, 0, groups, ready);
   }
