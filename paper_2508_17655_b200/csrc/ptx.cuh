@@ -354,5 +354,14 @@ __device__ __forceinline__ void mma_mxf4_pair(uint32_t d_tmem, uint64_t adesc, u
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sf_tmem)
       : "memory");
 }
+// 3D tile load on a CTA pair (completes bytes on the leader's barrier), with an L2 hint.
+__device__ __forceinline__ void tma_load_3d_pair_hint(uint32_t smem_dst, const CUtensorMap* m, uint32_t bar_cluster,
+                                                      int32_t c0, int32_t c1, int32_t c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
+}
 }  // namespace ptx
 }  // namespace sbg

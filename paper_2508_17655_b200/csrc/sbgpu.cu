@@ -360,8 +360,8 @@ int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int
   a.dbg = dev_knob("SBG_STEP_DBG");
   static unsigned long long* trace = nullptr;  // dev knob SBG_RES_TRACE: stamps of pair 0, group 0
   if (dev_knob("SBG_RES_TRACE")) {
-    if (!trace) CK(cudaMalloc(&trace, sizeof(unsigned long long) * 8 * 2 * 4096));
-    CK(cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 8 * 2 * 4096, ctx->stream));
+    if (!trace) CK(cudaMalloc(&trace, sizeof(unsigned long long) * 16 * 2 * 4096));
+    CK(cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 16 * 2 * 4096, ctx->stream));
     a.trace = trace;
     a.nsteps = std::min(a.nsteps, 4096);
   }
@@ -371,16 +371,17 @@ int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int
   CK(launch_persistent(kern, 2 * num_mp * a.rb_per_group, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream, maps, a));
   ++ctx->launches;
   if (a.trace) {
-    std::vector<unsigned long long> h(size_t(8 * 2 * a.nsteps));
+    std::vector<unsigned long long> h(size_t(16 * 2 * a.nsteps));
     CK(cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     FILE* f = fopen("gpurun_out/res_trace.txt", "w");
     if (f) {
       for (int s = 0; s < a.nsteps; ++s)
         for (int c = 0; c < 2; ++c) {
-          const unsigned long long* r = &h[size_t((s * 2 + c) * 8)];
-          fprintf(f, "%d %d %llu %llu %llu %llu %llu %llu %llu %llu\n", s, c, r[0], r[1], r[2], r[3], r[4], r[5], r[6],
-                  r[7]);
+          const unsigned long long* r = &h[size_t((s * 2 + c) * 16)];
+          fprintf(f, "%d %d", s, c);
+          for (int k = 0; k < 16; ++k) fprintf(f, " %llu", r[k]);
+          fprintf(f, "\n");
         }
       fclose(f);
     }
@@ -1643,8 +1644,19 @@ static int encode_part_maps(sbg_ctx* ctx, PartMaps* pm, int cur, int w0, int w1)
   pm->J = ctx->tmJ4;
   const uint64_t gb = uint64_t(ctx->npad / 2), gv4 = uint64_t((ctx->n + 1) / 2);
   const int ws[2] = {w0, w1};
+  auto enc = get_encode();
+  if (!enc) return ctx->fail(SBG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  const uint32_t kbs = uint32_t(std::min<int64_t>(8, ctx->npad / 256));  // K blocks (J resident: <= 8)
   for (int c = 0; c < 2; ++c)
     for (int par = 0; par < 2; ++par) {
+      // [K block][rpad][128 B] view of G (K block kb = bytes [128 kb, 128 kb + 128) of each row)
+      cuuint64_t dims[3] = {128, cuuint64_t(ctx->rpad), cuuint64_t(gb / 128)};
+      cuuint64_t strides[2] = {cuuint64_t(gb), 128};
+      cuuint32_t box[3] = {128, uint32_t(ws[c] / 2), kbs}, es[3] = {1, 1, 1};
+      if (enc(&pm->Gin3[c][par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, ctx->dG[cur ^ par], dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return ctx->fail(SBG_ERR_CUDA, "cuTensorMapEncodeTiled (3D G) failed");
       int rc = encode_2d_u8(ctx, &pm->Gin[c][par], ctx->dG[cur ^ par], gb, uint64_t(ctx->rpad), 128, uint32_t(ws[c] / 2));
       if (!rc)
         rc = encode_2d(ctx, &pm->Gout[c][par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ par ^ 1], gv4,
@@ -1672,14 +1684,15 @@ static int launch_resident_default(sbg_ctx* ctx, int cur, const MultiStepArgs& a
   const bool q4 = ctx->dJ4 != nullptr && !ctx->sharded;
   *g_mode = q4 ? 0 : 1;
   if (resident_nr(ctx) == RES_NR) {
-    // e2m1: the parts kernel, two interleaved half-block chains (SBG_RES_SPLIT=0 = one chain,
-    // SBG_RES_PARTS=3/4 = more, narrower parts: dev). npad <= 2048: J resident in shared memory.
+    // e2m1: the parts kernel, PARTS interleaved column-part chains (SBG_RES_SPLIT=0 = one chain,
+    // SBG_RES_PARTS=2/3: fewer, wider parts, dev). npad <= 2048: J resident in shared memory and
+    // each part-step's G in one 3D TMA load; larger npad: 2 parts, J streamed.
     if (q4 && !getenv_is0("SBG_RES_SPLIT")) {
       if (ctx->npad > 2048) return launch_parts<2, 10, false>(ctx, cur, a, groups, ready);
       switch (dev_knob("SBG_RES_PARTS")) {
-        case 3: return launch_parts<3, 20, true>(ctx, cur, a, groups, ready);
-        case 4: return launch_parts<4, 24, true>(ctx, cur, a, groups, ready);
-        default: return launch_parts<2, 16, true>(ctx, cur, a, groups, ready);
+        case 2: return launch_parts<2, 2, true>(ctx, cur, a, groups, ready);
+        case 3: return launch_parts<3, 2, true>(ctx, cur, a, groups, ready);
+        default: return launch_parts<4, 3, true>(ctx, cur, a, groups, ready);  // C2: 28.3 us (3: 28.3, 2: 28.9)
       }
     }
     return q4 ? launch_resident<16, 4, RES_NR_STAGES, RES_NR, true>(ctx, ctx->qmaps160_sign[cur], a, 0, groups, ready)

@@ -55,6 +55,8 @@ struct PartMaps {
   CUtensorMap J;           // e2m1 J [npad][npad / 2], box 128 x 128 B, 128B swizzle
   CUtensorMap Gin[2][2];   // [class][step parity]: B operand [rpad][npad / 2], box W / 2 rows x 128 B
   CUtensorMap Gout[2][2];  // [class][step parity]: next G, [R][ceil(n / 2)], box W rows x 64 B
+  CUtensorMap Gin3[2][2];  // JRES: the same B operand viewed [K block][rpad][128 B], box {128 B, W / 2, KB}:
+                           // a part-step's whole G operand in one load
 };
 
 template <int I, int N, class F>
@@ -79,7 +81,9 @@ struct PartsCfg {
   static constexpr int J_SLOTS = JRES ? 8 : 0;    // resident J tiles (K <= 2048)
   static constexpr int A_BYTES = BM * BK;         // 16 KB
   static constexpr int B_BYTES = (w(0) / 2) * BK; // G rows of the widest part per CTA
-  static constexpr int STAGE_BYTES = (JRES ? 0 : A_BYTES) + B_BYTES;
+  // JRES: a ring of STAGES super-stages, each holding a part-step's whole G operand (KB <= 8 K
+  // blocks of W / 2 rows, one 3D TMA load and one barrier); else STAGES stages of (J tile, G tile)
+  static constexpr int STAGE_BYTES = JRES ? J_SLOTS * B_BYTES : A_BYTES + B_BYTES;
   static constexpr int STAGES = STAGES_;
   static constexpr int RND = 4;                   // K-stages per MMA issue round
   static constexpr int EPI_WARPS = 16;
@@ -125,6 +129,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
   const int lane = threadIdx.x & 31;
   const uint32_t cr = ptx::cluster_ctarank();
   const bool leader = cr == 0;
+  // dev trace (SBG_RES_TRACE): %globaltimer stamps of pair 0's leader CTA, group 0, parts 0 and 1:
+  // [s][part][k], k = 0 G dependency met, 6 first MMA round's stages landed, 7 all stages landed,
+  // 1 accumulator ready (epilogue), 2 epilogue done, 3 publisher has the tile, 4 store complete,
+  // 5 released, 8 producer issued all G loads, 9 MMAs issued
+  auto stamp = [&](int g, int s, int i, int k) {
+    if (args.trace && g == args.group0 && s >= 0 && i < 2 && cr == 0 && (blockIdx.x >> 1) == 0)
+      args.trace[(s * 2 + i) * 16 + k] = gtimer();
+  };
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -217,14 +229,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
           // (Per-producer-pair flags with the stages issued as their pairs become ready measured
           // slower: 34.0 vs 31.4 us/step at C2.)
           dep::wait_block(args.done, PARTS * n_blk + i, 0u, static_cast<uint32_t>((s + 1) * args.num_m));
-          if (args.trace && pair == 0 && g == 0 && lane == 0 && i == 0) args.trace[(s * 2 + cr) * 8 + 0] = gtimer();
-          for (int kb = 0; kb < KB; ++kb) {
-            const bool pre = kb < STAGES && !Cfg::JRES;
+          if (lane == 0) stamp(g, s, i, 0);
+          if constexpr (Cfg::JRES) {  // the part-step's KB G tiles in one 3D load
+            ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
+            if (ptx::elect_one()) {
+              const uint32_t fb = ptx::mapa(full_bar(stage), 0);
+              ptx::mbar_arrive_expect_tx_cluster(fb, KB * b_bytes);
+              ptx::tma_load_3d_pair_hint(b_base + stage * Cfg::STAGE_BYTES, &maps.Gin3[Cfg::cls(i)][s & 1], fb, 0,
+                                         b_row0, 0, keep);
+            }
+            __syncwarp();
+            if (++stage == STAGES) {
+              stage = 0;
+              ph ^= 1u;
+            }
+          }
+          for (int kb = 0; !Cfg::JRES && kb < KB; ++kb) {
+            const bool pre = kb < STAGES;
             if (!pre) ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
             if (ptx::elect_one()) {
               const uint32_t fb = ptx::mapa(full_bar(stage), 0);
-              ptx::mbar_arrive_expect_tx_cluster(fb, (pre || Cfg::JRES) ? b_bytes : Cfg::A_BYTES + b_bytes);
-              if (!pre && !Cfg::JRES)
+              ptx::mbar_arrive_expect_tx_cluster(fb, pre ? b_bytes : Cfg::A_BYTES + b_bytes);
+              if (!pre)
                 ptx::tma_load_2d_pair_hint(a_base + stage * Cfg::A_BYTES, &maps.J, fb, kb * Cfg::BK, m_blk * Cfg::BM,
                                            keep);
               ptx::tma_load_2d_pair_hint(b_base + stage * Cfg::B_BYTES, gin, fb, kb * Cfg::BK, b_row0, keep);
@@ -235,6 +261,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
               ph ^= 1u;
             }
           }
+          if (lane == 0) stamp(g, s, i, 8);
         });
       }
     }
@@ -255,10 +282,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
             ptx::mbar_wait(tempty_bar(i), (lt & 1) ^ 1u);
             ptx::tc_fence_after();
             const uint32_t d = tmem_base + Cfg::off(i);
-            const bool trm = args.trace && pair == 0 && g == 0 && i == 0;
+            if constexpr (Cfg::JRES) {  // one super-stage: all KB K blocks of this part-step
+              ptx::mbar_wait(full_bar(stage), ph);
+              if (lane == 0) {
+                stamp(g, s, i, 6);
+                stamp(g, s, i, 7);
+              }
+              ptx::tc_fence_after();
+              if (ptx::elect_one()) {
+                const uint32_t bb = b_base + stage * Cfg::STAGE_BYTES;
+                for (int kb = 0; kb < KB; ++kb) {
+                  const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + kb * Cfg::A_BYTES);
+                  const uint64_t bdesc = ptx::smem_desc_k_sw128(bb + kb * (Cfg::w(i) / 2) * Cfg::BK);
+#pragma unroll
+                  for (int k = 0; k < Cfg::BK / 32; ++k)
+                    ptx::mma_mxf4_pair(d, adesc + 2 * k, bdesc + 2 * k, idesc, sf, (kb | k) != 0);
+                }
+                ptx::mma_commit_pair_mc(empty_bar(stage), 0x3);
+              }
+              __syncwarp();
+              if (++stage == STAGES) {
+                stage = 0;
+                ph ^= 1u;
+              }
+            }
             // RND K-stages per issue round: one handshake (wait, fence, elect) per round
             constexpr int RND = Cfg::RND;
-            for (int kb = 0; kb < KB; kb += RND) {
+            for (int kb = 0; !Cfg::JRES && kb < KB; kb += RND) {
               int sts[RND];
               const int cnt = KB - kb < RND ? KB - kb : RND;
 #pragma unroll
@@ -272,14 +322,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
                   }
                 }
               }
-              if (trm && kb == 0 && lane == 0) args.trace[(s * 2) * 8 + 6] = gtimer();
+              if (lane == 0 && kb == 0) stamp(g, s, i, 6);
+              if (lane == 0 && kb + RND >= KB) stamp(g, s, i, 7);
               ptx::tc_fence_after();
               if (ptx::elect_one()) {
 #pragma unroll
                 for (int u = 0; u < RND; ++u) {
                   if (u < cnt) {
-                    const uint64_t adesc =
-                        ptx::smem_desc_k_sw128(a_base + (Cfg::JRES ? kb + u : sts[u]) * Cfg::A_BYTES);
+                    const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + sts[u] * Cfg::A_BYTES);
                     const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + sts[u] * Cfg::B_BYTES);
 #pragma unroll
                     for (int k = 0; k < Cfg::BK / 32; ++k)
@@ -292,6 +342,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
             }
             if (ptx::elect_one()) ptx::mma_commit_pair_mc(tfull_bar(i), 0x3);
             __syncwarp();
+            if (lane == 0) stamp(g, s, i, 9);
           });
         }
       }
@@ -319,19 +370,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
         for (int s = -1; s < args.nsteps; ++s, ++pc) {
           const int par = s < 0 ? 1 : (s & 1);
           ptx::mbar_wait(gfull_bar(lane), pc & 1);
-          const bool tr = args.trace && pair == 0 && g == 0 && lane == 0 && s >= 0;
-          if (tr) args.trace[(s * 2 + cr) * 8 + 3] = gtimer();
+          stamp(g, s, lane, 3);
           ptx::tma_store_2d(&maps.Gout[clsi][par], t_base + offi * (Cfg::BM / 2), i0 / 2, n_blk * Cfg::NR + offi);
           ptx::bulk_commit();
           ptx::bulk_wait_read0();
           ptx::mbar_arrive(gempty_bar(lane));  // tile reusable
           ptx::bulk_wait0();
-          if (tr) args.trace[(s * 2 + cr) * 8 + 4] = gtimer();
+          stamp(g, s, lane, 4);
           dep::fence_proxy_async_global();
-          if (tr) args.trace[(s * 2 + cr) * 8 + 7] = gtimer();
           // red.release orders the completed (proxy-fenced) tile writes before the count
           dep::release_add(args.done + PARTS * n_blk + lane, 1u);
-          if (tr) args.trace[(s * 2 + cr) * 8 + 5] = gtimer();
+          stamp(g, s, lane, 5);
         }
       }
     }
@@ -398,8 +447,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
           ptx::mbar_wait(tfull_bar(i), lt & 1);
           __syncwarp();
           ptx::tc_fence_after();
-          const bool tr = args.trace && pair == 0 && g == 0 && warp == 4 && lane == 0 && i == 0;
-          if (tr) args.trace[(s * 2 + cr) * 8 + 1] = gtimer();
+          const bool tr = warp == 4 && lane == 0;
+          if (tr) stamp(g, s, i, 1);
           ptx::mbar_wait(gempty_bar(i), (pc & 1) ^ 1u);  // this part's G tile stored
           const int c0 = Cfg::off(i) + cg * (Cfg::w(i) / 4);  // this warp's first column of part i
           uint32_t bf[2][CH], bx[2][CH], by[2][CH];
@@ -456,7 +505,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(tempty_bar(i), 0));
           tile_written(i);  // the publisher stores G_{t+1} of part i and releases its counter
-          if (tr) args.trace[(s * 2 + cr) * 8 + 2] = gtimer();
+          if (tr) stamp(g, s, i, 2);
         });
       }
       // write the block's state back (after the last step's TMEM stores)
