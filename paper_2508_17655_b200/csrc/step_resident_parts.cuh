@@ -441,15 +441,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
         k.inv = __frcp_rn(static_cast<float>(args.M - (args.t_begin + static_cast<uint64_t>(s))));
         const PhaseConsts2 k2(k, args.ident);
         const float* arep = args.a_rep;
+        // the previous step's x, y stores must land before this step re-reads those columns;
+        // within a step every column is loaded once, so one wait per step covers all parts
+        ptx::tmem_st_wait();
         static_for<0, PARTS>([&](auto I) {
           constexpr int i = decltype(I)::value;
           constexpr int CHUNKS = Cfg::w(i) / 16;
-          ptx::mbar_wait(tfull_bar(i), lt & 1);
-          __syncwarp();
-          ptx::tc_fence_after();
-          const bool tr = warp == 4 && lane == 0;
-          if (tr) stamp(g, s, i, 1);
-          ptx::mbar_wait(gempty_bar(i), (pc & 1) ^ 1u);  // this part's G tile stored
           const int c0 = Cfg::off(i) + cg * (Cfg::w(i) / 4);  // this warp's first column of part i
           uint32_t bf[2][CH], bx[2][CH], by[2][CH];
           auto ld_chunk = [&](int c, int b) {
@@ -463,8 +460,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
 #pragma unroll
             for (int j = 0; j < CH; ++j) asm volatile("" : "+r"(bf[b][j]), "+r"(bx[b][j]), "+r"(by[b][j]));
           };
-          ld_chunk(0, 0);
+          // x, y of the first chunk do not depend on the MMA: requested before its completion
+          ptx::tmem_ld<CH>(t_lane + Cfg::COL_X + c0, bx[0]);
+          ptx::tmem_ld<CH>(t_lane + Cfg::COL_Y + c0, by[0]);
+          ptx::mbar_wait(tfull_bar(i), lt & 1);
+          __syncwarp();
+          ptx::tc_fence_after();
+          const bool tr = warp == 4 && lane == 0;
+          if (tr) stamp(g, s, i, 1);
+          ptx::mbar_wait(gempty_bar(i), (pc & 1) ^ 1u);  // this part's G tile stored
+          if (tr) stamp(g, s, i, 10);
+          ptx::tmem_ld<CH>(t_lane + c0, bf[0]);
           wait_chunk(0);
+          if (tr) stamp(g, s, i, 11);
           auto chunks = [&](auto has_arep) {
             static_for<0, CHUNKS>([&](auto C) {
               constexpr int c = decltype(C)::value;
@@ -499,16 +507,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
             chunks(std::true_type{});
           else
             chunks(std::false_type{});
-          ptx::tmem_st_wait();
-          // accumulator i consumed: the leader may issue this part's next MMAs
+          if (tr) stamp(g, s, i, 12);
+          tile_written(i);  // first: the publisher stores G_{t+1} of part i and releases its counter
+          // accumulator i consumed (all F loads waited): the leader may issue this part's next MMAs
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(tempty_bar(i), 0));
-          tile_written(i);  // the publisher stores G_{t+1} of part i and releases its counter
           if (tr) stamp(g, s, i, 2);
         });
       }
       // write the block's state back (after the last step's TMEM stores)
+      ptx::tmem_st_wait();
       static_for<0, PARTS>([&](auto I) {
         constexpr int i = decltype(I)::value;
         static_for<0, Cfg::w(i) / 16>([&](auto C) {

@@ -5,8 +5,9 @@ import sys
 import numpy as np
 d = np.loadtxt(sys.argv[1], dtype=np.int64)
 names = {0: "dep met", 8: "loads issued", 6: "1st round landed", 7: "all landed", 9: "MMAs issued",
-         1: "acc ready", 2: "epilogue done", 3: "publisher has tile", 4: "store complete", 5: "released"}
-order = [0, 8, 6, 7, 9, 1, 2, 3, 4, 5]
+         1: "acc ready", 10: "tile free", 11: "1st chunk loaded", 12: "math done", 13: "st waited",
+         2: "epilogue done", 3: "publisher has tile", 4: "store complete", 5: "released"}
+order = [0, 8, 6, 7, 9, 1, 10, 11, 12, 13, 2, 3, 4, 5]
 steps = sorted(set(d[:, 0]))[5:40]
 ref = {s: d[(d[:, 0] == s) & (d[:, 1] == 0)][0, 2] for s in steps}
 for part in (0, 1):
