@@ -59,8 +59,8 @@ def peaks():
 
 DTYPES = {"e2m1": "e2m1 operands (tcgen05 kind::mxf4, unit E8M0 scales, f32 acc: exact integer field) / f32 state",
           "int8": "i8 operands (tcgen05 kind::i8, s32 acc) / f32 state"}
-KERNELS = {"e2m1": "gsb_resident_parts_kernel<16,true,2> (two interleaved 80-replica chains per block, J resident "
-                   "in shared memory, p in registers)",
+KERNELS = {"e2m1": "gsb_resident_parts_kernel<3,true,4> (four interleaved column-part chains per 160-replica block, "
+                   "J resident in shared memory, one 3D TMA load of G per part-step, p in registers)",
            "int8": "gsb_resident_pair_kernel<5,16,4,160,false>"}
 
 
