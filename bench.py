@@ -245,7 +245,7 @@ def run_ours(args):
 
     # ---- end to end through the public API: pinned host x0,y0 -> run() -> spins/energies on host
     x0h, y0h = init_host_states(local, R, r0)
-    e2e_steps = args.steps
+    e2e_steps = M_SCHED  # one whole run of the C2 schedule (M = 1000), as the reference's run() does
     cfg_e2e = SolverConfig(variant=Variant.gdsb, steps=e2e_steps, dt=DT, c=c, a=A_CTRL)
     tun = TuningResult(c=c, dt=DT)
     s.run_batch(cfg_e2e, tun, R, x0=x0h, y0=y0h, want_spins=False)  # warm

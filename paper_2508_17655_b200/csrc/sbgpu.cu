@@ -1702,9 +1702,10 @@ static int launch_resident_default(sbg_ctx* ctx, int cur, const MultiStepArgs& a
             : launch_resident<16, 4>(ctx, ctx->rmaps_sign[cur], a, 0, groups, ready);
 }
 
-// sbg_run on the resident kernel: the replica groups are independent for the whole
-// run, so group g's M steps start as soon as ITS x0/y0 rows have arrived; the copies of
-// the later groups (copy stream) overlap the earlier groups' steps.
+// sbg_run on the resident kernel: the replica blocks are independent for the whole run,
+// so a block's M steps start as soon as ITS x0/y0 rows have arrived; the copies of later
+// groups (copy stream) overlap the earlier groups' steps. The first group's blocks get a
+// flag each (their copies are the only exposed ones), later groups one flag per group.
 static int run_pipelined(sbg_ctx* ctx, const sbg_params* prm, int64_t R, const float* x0, const float* y0,
                          float* x_final, int8_t* spins, double* energy, int64_t* best_index, sbg_timing* timing) {
   int rc;
@@ -1718,18 +1719,18 @@ static int run_pipelined(sbg_ctx* ctx, const sbg_params* prm, int64_t R, const f
     CK(cudaEventRecord(ctx->ev[7], ctx->stream));
     return run_tail(ctx, prm, x_final, spins, energy, best_index, timing);
   }
-  if (ctx->ready_cap < groups) {
+  const int nflags = rbg + groups - 1;  // [0, rbg): group 0's blocks; rbg + g - 1: group g >= 1
+  if (ctx->ready_cap < nflags) {
     cudaFree(ctx->d_ready);
     ctx->d_ready = nullptr;
-    CK(cudaMalloc(&ctx->d_ready, sizeof(uint32_t) * groups));
-    ctx->ready_cap = groups;
+    CK(cudaMalloc(&ctx->d_ready, sizeof(uint32_t) * nflags));
+    ctx->ready_cap = nflags;
   }
-  CK(cudaMemsetAsync(ctx->d_ready, 0, sizeof(uint32_t) * groups, ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_ready, 0, sizeof(uint32_t) * nflags, ctx->stream));
   const size_t cnt = size_t(ctx->rpad) * ctx->npad;
   fill_f32_kernel<<<grid_for(ctx, cnt, 256), 256, 0, ctx->stream>>>(ctx->dP, cnt, 1.0f);
   CK(cudaGetLastError());
   ++ctx->launches;
-  const int64_t Rg = int64_t(rbg) * nr;
   const size_t pitch = sizeof(float) * ctx->npad, w = sizeof(float) * ctx->n;
   CK(cudaEventRecord(ctx->evc[0], ctx->stream));  // state buffers and flags (re)initialised
   const bool honours_a = prm->variant == SBG_GDSB;
@@ -1747,13 +1748,14 @@ static int run_pipelined(sbg_ctx* ctx, const sbg_params* prm, int64_t R, const f
   a.nsteps = int32_t(prm->steps);
   a.a_rep = (honours_a && ctx->d_arep && ctx->arep_n == ctx->R) ? ctx->d_arep : nullptr;
   const int cur = ctx->g_cur;
-  // Copies (second stream) are enqueued BEFORE the launch, which waits on nothing but each
-  // group's flag: with pinned buffers the copies of later groups overlap the earlier groups'
-  // steps; with pageable buffers, a serialising profiler or CUDA_LAUNCH_BLOCKING the copies
-  // simply complete first (the kernel can never wait on work queued behind it).
+  // Copies (second stream) are enqueued BEFORE the launch, which waits on nothing but the
+  // flags: with pinned buffers the copies of later groups overlap the earlier groups' steps;
+  // with pageable buffers, a serialising profiler or CUDA_LAUNCH_BLOCKING the copies simply
+  // complete first (the kernel can never wait on work queued behind it).
   CK(cudaStreamWaitEvent(ctx->cstream, ctx->evc[0], 0));
-  for (int g = 0; g < groups; ++g) {
-    const int64_t r0 = g * Rg, rows = std::min<int64_t>(R - r0, Rg);
+  for (int g = 0; g < nflags; ++g) {  // flag g covers replica rows [r0, r0 + rows)
+    const int64_t r0 = g < rbg ? int64_t(g) * nr : int64_t(rbg) * nr * (g - rbg + 1);
+    const int64_t rows = std::min<int64_t>(R - r0, g < rbg ? int64_t(nr) : int64_t(rbg) * nr);
     if (rows > 0) {
       CK(cudaMemcpy2DAsync(ctx->dX + r0 * ctx->npad, pitch, x0 + r0 * ctx->n, w, w, rows, cudaMemcpyHostToDevice,
                            ctx->cstream));

@@ -124,8 +124,9 @@ struct ResidentArgs {
   const float* a_rep;
   PhaseIdent ident;           // -0, 1, -1 (runtime identity operands of gsb_phase2)
   uint8_t* gbuf[2];           // G_DIRECT: output G buffer of step parity 0/1 ([rpad][npad] bytes)
-  const uint32_t* ready;      // optional [groups]: nonzero once group g's x, y rows have landed (sbg_run
-                              // overlaps the host->device copies of later groups with earlier groups)
+  const uint32_t* ready;      // optional: nonzero once the x, y rows have landed (sbg_run overlaps the
+                              // host->device copies with the steps): [0, rb_per_group) the blocks of
+                              // group 0, then one flag per later group (rb_per_group + g - 1)
   int32_t dbg;                // dev only: 1 = skip J loads after the first step, 2 = no G dependency wait
   unsigned long long* trace;  // dev only: per-step %globaltimer stamps of pair 0 (null = off)
 };
@@ -380,7 +381,8 @@ __global__ void __cluster_dims__(2, 1, 1)
       if (n_blk >= num_n) break;
       const int r0 = n_blk * Cfg::NR + h * Cfg::COLS_PER_WARP;  // this thread's first replica
       if (args.ready)
-        while (dep::ld_acquire_sys(args.ready + g) == 0) __nanosleep(256);
+        while (dep::ld_acquire_sys(args.ready + (g == 0 ? rbk : args.rb_per_group + g - 1)) == 0)
+          __nanosleep(256);
       // load the block's state into TMEM (coalesced: a warp reads 32 consecutive spins)
 #pragma unroll 1
       for (int c8 = 0; c8 < Cfg::COLS_PER_WARP / 8; ++c8) {

@@ -409,7 +409,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
       const int n_blk = g * args.rb_per_group + rbk;
       if (n_blk >= num_n) break;
       if (args.ready)
-        while (dep::ld_acquire_sys(args.ready + g) == 0) __nanosleep(256);
+        while (dep::ld_acquire_sys(args.ready + (g == 0 ? rbk : args.rb_per_group + g - 1)) == 0)
+          __nanosleep(256);
       // load the block's state (x, y to TMEM, p to registers) and write G_0 = sgn(x_0)
       static_for<0, PARTS>([&](auto I) {
         constexpr int i = decltype(I)::value;
