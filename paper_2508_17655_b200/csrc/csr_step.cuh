@@ -8,9 +8,12 @@
 //
 // Layout: while stepping, the state lives SPIN-MAJOR ([npad][rp], replicas
 // contiguous) so that the SpMM gather of row j for a block of replicas is one
-// contiguous, vectorised read: a warp owns (row i, 256 replicas), lane l holds
-// replicas 4l..4l+3 and 128+4l..+3 (int4 / char4 / float4 accesses, two 512 B
-// gathers per warp per nonzero: twice the loads in flight of one group).
+// contiguous, vectorised read: a warp owns (row i, 128 CSR_VEC replicas), lane l holds
+// replicas 4l..4l+3 (+ 128 u for CSR_VEC > 1; int4 / char4 / float4 accesses, one 512 B
+// gather per warp per nonzero and group). CSR_VEC = 1 at 32 registers (8 blocks of 256
+// threads per SM) measured 77.9 us/step at C3 vs 80.2 for CSR_VEC = 2 at 48 registers;
+// a variant that prefetches x, y, p and batches 4-8 gathers before use was slower
+// (85-167 us: the extra registers cost more occupancy than the batching gains).
 // The row's (col, val) pairs are loaded once, one per lane, and broadcast with
 // shuffles, so all gathers of a row are independent (memory-level parallelism).
 // The gathered operand (q or sgn x) is ping-ponged between two buffers because
@@ -26,8 +29,9 @@
 namespace sbg {
 
 constexpr int CSR_THREADS = 256;
-constexpr int CSR_VEC = 2;                     // 4-replica groups per lane (more gathers in flight)
+constexpr int CSR_VEC = 1;                     // 4-replica groups per lane (more gathers in flight)
 constexpr int CSR_RCHUNK = 128 * CSR_VEC;      // replicas per warp task
+constexpr int CSR_MIN_BLOCKS = 8;              // 64 warps per SM: latency hiding for the gathers
 
 // L2 eviction priorities: the x/y/p stream is touched once per step (evict_first);
 // the gathered operand (q or signs, re-read ~degree times per step) should stay.
@@ -77,7 +81,7 @@ __device__ __forceinline__ void st_u32(void* a, uint32_t v, uint64_t pol) {
 }  // namespace l2
 
 template <bool SIGN>
-__global__ void __launch_bounds__(CSR_THREADS)
+__global__ void __launch_bounds__(CSR_THREADS, CSR_MIN_BLOCKS)
     csr_step_sm_kernel(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                        const int8_t* __restrict__ val, const void* __restrict__ g_cur, void* __restrict__ g_next,
                        float* __restrict__ xs, float* __restrict__ ys, float* __restrict__ ps, int64_t rp,
