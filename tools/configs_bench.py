@@ -16,9 +16,16 @@ import oracle  # noqa: E402  (instance generators only; the timed path is the GP
 from paper_2508_17655_b200 import InitMode, Solver, SolverConfig, Variant  # noqa: E402
 
 HBM = 6553.0
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def run(s, variant, n, R, steps, c, bytes_per_su_extra=0.0, ops_per_su=None):
+def peak(name, key):
+    """Measured tensor peaks (profiles/int8_peak.json, profiles/fp4_peak.json), TOP/s."""
+    with open(os.path.join(ROOT, "profiles", name)) as f:
+        return float(json.load(f)[key])
+
+
+def run(s, variant, n, R, steps, c, bytes_per_su_extra=0.0, ops_per_su=None, tensor_peak=None):
     cfg = SolverConfig(variant=variant, steps=1000 + steps, dt=1.25, c=c, a=0.2)
     s.init_state(R, InitMode.small_uniform, 1, 7)
     s.advance(cfg, 0, 3)
@@ -33,6 +40,12 @@ def run(s, variant, n, R, steps, c, bytes_per_su_extra=0.0, ops_per_su=None):
     out["hbm_frac"] = out["gbs"] / HBM
     if ops_per_su:
         out["tops"] = ops_per_su * n * R / (us * 1e-6) / 1e12
+        if tensor_peak:
+            out["tensor_frac"] = out["tops"] / tensor_peak[0]
+            out["tensor_peak"] = tensor_peak[1]
+    # the sign variants multiply with kind::mxf4 when J has an e2m1 copy; bSB/GbSB use int8 planes
+    sign = variant in (Variant.dsb, Variant.gdsb)
+    out["mma"] = "kind::mxf4 (e2m1)" if sign and s.operand_format == "e2m1" else "kind::i8"
     return out
 
 
@@ -43,6 +56,8 @@ def main():
     args = ap.parse_args()
     orc = oracle.orc()
     res = {}
+    i8 = (peak("int8_peak.json", "int8_tops_burst"), "int8 (cuBLASLt 8192^3 burst)")
+    f4 = (peak("fp4_peak.json", "fp4_tops_burst"), "fp4 (cuBLASLt NVFP4 8192^3 burst)")
     with Solver(0) as s:
         only = args.only.split(",")
         if "C1" in only or "C2" in only:
@@ -50,10 +65,10 @@ def main():
             c = 1 / (2 * math.sqrt(2000))
             if "C1" in only:
                 res["C1_gbsb_n2000_R1000"] = run(s, Variant.gbsb, 2000, 1000, args.steps, c, 2000 / 1000,
-                                                 ops_per_su=4 * 2 * 2048)
+                                                 ops_per_su=4 * 2 * 2000, tensor_peak=i8)
             if "C2" in only:
                 res["C2_gdsb_n2000_R8192"] = run(s, Variant.gdsb, 2000, 8192, args.steps, c, 2000 / 8192,
-                                                 ops_per_su=2 * 2048)
+                                                 ops_per_su=2 * 2000, tensor_peak=f4)
         if "C3" in only:
             n, m = 20000, 100000
             _, (rowptr, col, val) = orc.gen_er_csr(n, m, 1)
@@ -67,7 +82,7 @@ def main():
             J = orc.gen_sk_f32(n, 1)
             s.set_instance(J)
             res["C4_gbsb_sk_n4096_R2048"] = run(s, Variant.gbsb, n, 2048, args.steps, 0.5, 3 * n / 2048,
-                                                ops_per_su=12 * 2 * n)
+                                                ops_per_su=12 * 2 * n, tensor_peak=i8)
     print(json.dumps(res, indent=1))
 
 
