@@ -12,6 +12,9 @@
 // replicas 4l..4l+3 (+ 128 u for CSR_VEC > 1; int4 / char4 / float4 accesses, one 512 B
 // gather per warp per nonzero and group). CSR_VEC = 1 at 32 registers (8 blocks of 256
 // threads per SM) measured 77.9 us/step at C3 vs 80.2 for CSR_VEC = 2 at 48 registers;
+// with the gather address one IMAD.WIDE.U32 and no per-replica predicate, the nonzero loop
+// not unrolled (no spills at 32 registers) gives 71.2 (unroll 2: 74.7, 4: 78.9; 48 warps
+// with unroll 4: 91.7; an L2 prefetch of x, y, p at task start: 72.5);
 // a variant that prefetches x, y, p and batches 4-8 gathers before use was slower
 // (85-167 us: the extra registers cost more occupancy than the batching gains).
 // The row's (col, val) pairs are loaded once, one per lane, and broadcast with
@@ -31,7 +34,15 @@ namespace sbg {
 constexpr int CSR_THREADS = 256;
 constexpr int CSR_VEC = 1;                     // 4-replica groups per lane (more gathers in flight)
 constexpr int CSR_RCHUNK = 128 * CSR_VEC;      // replicas per warp task
-constexpr int CSR_MIN_BLOCKS = 8;              // 64 warps per SM: latency hiding for the gathers
+#ifndef CSR_MINB
+#define CSR_MINB 8
+#endif
+#ifndef CSR_UNROLL
+#define CSR_UNROLL 1
+#endif
+
+constexpr int CSR_UNR = CSR_UNROLL;             // nonzeros per unrolled gather round
+constexpr int CSR_MIN_BLOCKS = CSR_MINB;       // 64 warps per SM: latency hiding for the gathers
 
 // L2 eviction priorities: the x/y/p stream is touched once per step (evict_first);
 // the gathered operand (q or signs, re-read ~degree times per step) should stay.
@@ -92,10 +103,17 @@ __global__ void __launch_bounds__(CSR_THREADS, CSR_MIN_BLOCKS)
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const uint64_t stream = l2::evict_first(), keep = l2::evict_last();
+  // row stride of the gathered operand in bytes: row j of a lane's group is one IMAD.WIDE.U32 away
+  const uint32_t rsb = static_cast<uint32_t>(rp) * (SIGN ? 1u : 4u);
   for (int64_t t = wid; t < tasks; t += nw) {
     const int i = static_cast<int>(t / chunks);
     const int rc = static_cast<int>(t % chunks) * CSR_RCHUNK + 4 * lane;  // group u covers rc + 128 u .. +3
     const int kb = rowptr[i], ke = rowptr[i + 1];
+    // every lane gathers, padding replicas (rc >= R, inside rp) included: no predicate in the loop
+    const char* gb[CSR_VEC];
+#pragma unroll
+    for (int u = 0; u < CSR_VEC; ++u)
+      gb[u] = static_cast<const char*>(g_cur) + static_cast<size_t>(rc + 128 * u) * (SIGN ? 1 : 4);
     long long acc[CSR_VEC][4];
 #pragma unroll
     for (int u = 0; u < CSR_VEC; ++u) acc[u][0] = acc[u][1] = acc[u][2] = acc[u][3] = 0;
@@ -106,28 +124,26 @@ __global__ void __launch_bounds__(CSR_THREADS, CSR_MIN_BLOCKS)
         jl = col[k0 + lane];
         vl = val[k0 + lane];
       }
-#pragma unroll 2
+#pragma unroll CSR_UNR
       for (int kk = 0; kk < cnt; ++kk) {
         const int j = __shfl_sync(0xffffffffu, jl, kk);
         const long long v = __shfl_sync(0xffffffffu, vl, kk);
 #pragma unroll
         for (int u = 0; u < CSR_VEC; ++u) {
-          const int r = rc + 128 * u;
-          if (r < R) {
-            if (SIGN) {
-              const uint32_t w = l2::ld_u32(static_cast<const int8_t*>(g_cur) + static_cast<size_t>(j) * rp + r, keep);
-              const char4 s = *reinterpret_cast<const char4*>(&w);
-              acc[u][0] += v * s.x;
-              acc[u][1] += v * s.y;
-              acc[u][2] += v * s.z;
-              acc[u][3] += v * s.w;
-            } else {
-              const int4 q = l2::ld_i4(static_cast<const int32_t*>(g_cur) + static_cast<size_t>(j) * rp + r, keep);
-              acc[u][0] += v * q.x;
-              acc[u][1] += v * q.y;
-              acc[u][2] += v * q.z;
-              acc[u][3] += v * q.w;
-            }
+          const char* src = gb[u] + static_cast<uint64_t>(static_cast<uint32_t>(j)) * rsb;
+          if (SIGN) {
+            const uint32_t w = l2::ld_u32(src, keep);
+            const char4 s = *reinterpret_cast<const char4*>(&w);
+            acc[u][0] += v * s.x;
+            acc[u][1] += v * s.y;
+            acc[u][2] += v * s.z;
+            acc[u][3] += v * s.w;
+          } else {
+            const int4 q = l2::ld_i4(reinterpret_cast<const int32_t*>(src), keep);
+            acc[u][0] += v * q.x;
+            acc[u][1] += v * q.y;
+            acc[u][2] += v * q.z;
+            acc[u][3] += v * q.w;
           }
         }
       }

@@ -77,6 +77,7 @@ def main():
             csr_bytes = (4 * (n + 1) + 5 * 2 * m) / (n * 512)  # CSR once per step
             res["C3_gbsb_er_n20000_R512"] = run(s, Variant.gbsb, n, 512, args.steps, c, csr_bytes)
             res["C3_gbsb_er_n20000_R512"]["c"] = c
+            res["C3_gbsb_er_n20000_R512"]["mma"] = "CSR SIMT (exact int64)"
         if "C4" in only:
             n = 4096
             J = orc.gen_sk_f32(n, 1)
