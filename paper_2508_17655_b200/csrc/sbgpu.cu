@@ -46,7 +46,9 @@ constexpr int NPAIR_PLANE = 64;   // replicas per pair tile, fixed-point variant
 enum Kind { KIND_NONE = 0, KIND_DENSE_I8 = 1, KIND_CSR_I8 = 2, KIND_DENSE_FX = 3 };
 constexpr int FX_NA = 3;          // real J: 24-bit fixed point as 3 byte planes (u8, u8, s8)
 constexpr int BN_FX_SIGN = 64;    // replica tile, real J x sign plane (3 accumulators)
-constexpr int BN_FX_PLANE = 32;   // replica tile, real J x 4 x-planes (6 accumulators)
+constexpr int BN_FX_PLANE = 32;   // replica tile, real J x 4 x-planes (6 accumulators, double-buffered)
+constexpr int BN_FX_PLANE_W = 64; // the same with one accumulator buffer (default; == BN_PLANE)
+static_assert(BN_FX_PLANE_W == BN_PLANE, "the 64-wide real-J launch uses the maps_planes G boxes");
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
@@ -1327,7 +1329,10 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
     }
     if (resident) ctx->g_mode = 1;
     const bool fx = ctx->kind == KIND_DENSE_FX;
-    const int bn = fx ? (sign ? BN_FX_SIGN : BN_FX_PLANE) : (sign ? BN_SIGN : BN_PLANE);
+    // real J x 4 x-planes: 64-replica tiles with one accumulator buffer (6 x 64 TMEM columns)
+    // halve the MMA instruction count of 32-replica tiles; SBG_FX_BN=32 selects the latter
+    const bool fx64 = fx && !sign && dev_knob("SBG_FX_BN") != 32;
+    const int bn = fx64 ? BN_FX_PLANE_W : fx ? (sign ? BN_FX_SIGN : BN_FX_PLANE) : (sign ? BN_SIGN : BN_PLANE);
     const int64_t T = (ctx->npad / 128) * (ctx->rpad / bn);
     const int64_t max_steps = std::max<int64_t>(1, (int64_t(1) << 30) / T);
     const bool per_step = dev_knob("SBG_PER_STEP_LAUNCH") != 0;
@@ -1368,8 +1373,9 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
       // 20.4 us on pairs. SBG_STEP_CFG selects sweep alternatives (dev only).
       if (fx) {
         // real-valued J: 3 J planes x (sign | 4 x-planes), single-CTA
-        rc = sign ? launch_multistep<1, BN_FX_SIGN, 2, 4, FX_NA>(ctx, ctx->fxmaps_sign[cur], a)
-                  : launch_multistep<NPL, BN_FX_PLANE, 2, 3, FX_NA>(ctx, ctx->fxmaps_planes[cur], a);
+        rc = sign   ? launch_multistep<1, BN_FX_SIGN, 2, 4, FX_NA>(ctx, ctx->fxmaps_sign[cur], a)
+             : fx64 ? launch_multistep<NPL, BN_FX_PLANE_W, 2, 2, FX_NA>(ctx, ctx->maps_planes[cur], a)
+                    : launch_multistep<NPL, BN_FX_PLANE, 2, 3, FX_NA>(ctx, ctx->fxmaps_planes[cur], a);
       } else if (resident) {
         // default for sign variants: state resident in TMEM (step_resident.cuh); SBG_RESIDENT=0
         // selects the streaming kernels (dev comparison)

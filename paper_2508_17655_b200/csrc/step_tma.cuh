@@ -62,13 +62,16 @@ struct TmaStepCfg {
   static constexpr int BUF_RAW = 3 * ST_ARR + NPLANES * ST_G;
   static constexpr int BUF_BYTES = (BUF_RAW + 1023) / 1024 * 1024;
   static constexpr int ACC_COLS = NW * BN;              // one accumulator per plane weight
-  static constexpr int TMEM_COLS = 2 * ACC_COLS <= 256 ? 256 : 512;
+  // accumulator buffers: 2 when they fit TMEM, else 1 (the epilogue then drains all of a
+  // tile's accumulator columns first and releases them before its state chunks)
+  static constexpr int ABUF = 2 * ACC_COLS <= 512 ? 2 : 1;
+  static constexpr int TMEM_COLS = ABUF * ACC_COLS <= 256 ? 256 : 512;
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static constexpr int NUM_BARS = 2 * STAGES + 4 + 3 * NBUF;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + NBUF * BUF_BYTES + 1024 + 8 * NUM_BARS + 64;
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static_assert(BN % CW == 0, "chunking");
-  static_assert(2 * ACC_COLS <= 512, "TMEM allocation");
+  static_assert(ABUF * ACC_COLS <= 512, "TMEM allocation");
 };
 
 struct TmaMaps {
@@ -250,8 +253,8 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
       uint32_t ph = 0;
       int lt = 0;
       for (int g = blockIdx.x; g < total; g += gridDim.x, ++lt) {
-        const int buf = lt & 1;
-        ptx::mbar_wait(tempty_bar(buf), ((lt >> 1) & 1) ^ 1u);
+        const int buf = lt % Cfg::ABUF;
+        ptx::mbar_wait(tempty_bar(buf), ((lt / Cfg::ABUF) & 1) ^ 1u);
         ptx::tc_fence_after();
         const uint32_t d_base = tmem_base + buf * Cfg::ACC_COLS;
         for (int kb = 0; kb < KB; ++kb) {
@@ -397,15 +400,14 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
       const int s = g / T;
       const int rbase = ((g % T) / args.num_m) * BN;  // first replica of this tile
       k.inv = __frcp_rn(static_cast<float>(args.M - (args.t_begin + static_cast<uint64_t>(s))));
-      const int buf = lt & 1;
-      if (args.dbg < 2) ptx::mbar_wait(tfull_bar(buf), (lt >> 1) & 1);
+      const int buf = lt % Cfg::ABUF;
+      if (args.dbg < 2) ptx::mbar_wait(tfull_bar(buf), (lt / Cfg::ABUF) & 1);
       __syncwarp();
       ptx::tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * Cfg::ACC_COLS;
-      for (int c = 0; c < CHUNKS; ++c, ++ck) {
-        const int b = ck % NBUF;
+      // the field of chunk c (this thread's CWQ replicas) from the accumulator columns
+      auto load_F = [&](int c, float* F) {
         const int col0 = c * CW + h * CWQ;
-        float F[CWQ];
         if (NA > 1) {
           // fixed-point real J: F = fl32(sum_w fl64(acc_w * 2^(8w + fx_exp))), fixed order
           double f[CWQ];
@@ -444,6 +446,26 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
 #pragma unroll
           for (int j = 0; j < CWQ; ++j) F[j] = __fmul_rn(__ll2float_rn(tot[j]), 0x1p-30f);
         }
+      };
+      float Fall[Cfg::ABUF == 1 ? CHUNKS : 1][CWQ];
+      if constexpr (Cfg::ABUF == 1) {  // single accumulator buffer: drain it, release it, then update
+#pragma unroll
+        for (int c = 0; c < CHUNKS; ++c) load_F(c, Fall[c]);
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(tempty_bar(buf));
+      }
+#pragma unroll
+      for (int c = 0; c < CHUNKS; ++c, ++ck) {
+        const int b = ck % NBUF;
+        const int col0 = c * CW + h * CWQ;
+        float F[CWQ];
+        if constexpr (Cfg::ABUF == 1) {
+#pragma unroll
+          for (int j = 0; j < CWQ; ++j) F[j] = Fall[c][j];
+        } else {
+          load_F(c, F);
+        }
         if (args.dbg != 1) {
           ptx::mbar_wait(sfull_bar(b), (ck / NBUF) & 1);
           float* xs = reinterpret_cast<float*>(s_gen + b * Cfg::BUF_BYTES);
@@ -480,9 +502,11 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(sdone_bar(b));
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(tempty_bar(buf));
+      if constexpr (Cfg::ABUF == 2) {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(tempty_bar(buf));
+      }
     }
   }
 
