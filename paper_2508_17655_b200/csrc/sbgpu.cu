@@ -1414,6 +1414,8 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
           case 2: rc = launch_multistep_pair<NPL, NPAIR_PLANE, 3, 3>(ctx, ctx->pmaps_planes[cur], a); break;
           case 3: rc = launch_multistep_pair<NPL, NPAIR_PLANE, 4, 2>(ctx, ctx->pmaps_planes[cur], a); break;
           case 6: rc = launch_multistep_pair<NPL, NPAIR_PLANE, 5, 2>(ctx, ctx->pmaps_planes[cur], a); break;
+          // 128-replica pair tiles, one accumulator buffer (B halves of 64 rows: the maps_planes boxes)
+          case 9: rc = launch_multistep_pair<NPL, 2 * BN_PLANE, 3, 2>(ctx, ctx->maps_planes[cur], a); break;
           case 7: rc = launch_multistep<NPL, BN_PLANE, PLANE_STAGES, PLANE_NBUF>(ctx, ctx->maps_planes[cur], a); break;
           case 4: {  // smaller replica tiles: more tiles per step for small R
             MultiStepArgs a32 = a;
@@ -1427,7 +1429,16 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
             rc = launch_multistep<NPL, 32, 3, 4>(ctx, ctx->fxmaps_planes[cur], a32);
             break;
           }
-          default: rc = launch_multistep_pair<NPL, NPAIR_PLANE, 4, 2>(ctx, ctx->pmaps_planes[cur], a);
+          default: {
+            // 128-replica tiles halve the MMA instructions per output but only pay with enough
+            // tiles per step to fill the pairs (>= 2.5 waves; measured at n = 2000, GbSB:
+            // R = 3072 46.7 -> 43.9 us/step, R = 8192 132.1 -> 127.5; R = 1000 15.1 -> 23.5)
+            const int64_t wide_tiles = (ctx->npad / 256) * (ctx->rpad / (2 * BN_PLANE));
+            if (2 * wide_tiles >= 5 * int64_t(ctx->sms / 2))
+              rc = launch_multistep_pair<NPL, 2 * BN_PLANE, 3, 2>(ctx, ctx->maps_planes[cur], a);
+            else
+              rc = launch_multistep_pair<NPL, NPAIR_PLANE, 4, 2>(ctx, ctx->pmaps_planes[cur], a);
+          }
         }
       }
       if (rc) return rc;

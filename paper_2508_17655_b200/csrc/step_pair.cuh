@@ -55,8 +55,11 @@ struct PairStepCfg {
   static constexpr int BUF_RAW = 3 * ST_ARR + NPLANES * ST_G;
   static constexpr int BUF_BYTES = (BUF_RAW + 1023) / 1024 * 1024;
   static constexpr int ACC_COLS = NPLANES * N_PAIR;     // per CTA per accumulator buffer
-  static constexpr int NACC = Q4 ? 1 : 2;               // accumulator buffers
-  static constexpr int TMEM_COLS = Q4 ? 512 : 2 * ACC_COLS;
+  // accumulator buffers: 2 when they fit TMEM; 1 for e2m1 (scale factors) or wide tiles, whose
+  // epilogue (non-e2m1) then drains all accumulator columns before the state update
+  static constexpr int NACC = (Q4 || 2 * ACC_COLS > 512) ? 1 : 2;
+  static constexpr bool EARLY_DRAIN = !Q4 && NACC == 1;
+  static constexpr int TMEM_COLS = Q4 ? 512 : NACC * ACC_COLS;
   static constexpr uint32_t COL_SF = 512 - 16;          // Q4: unit E8M0 scale factors
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static constexpr int NUM_BARS = 2 * STAGES + 4 + 3 * NBUF;
@@ -309,10 +312,9 @@ __global__ void __cluster_dims__(2, 1, 1)
       __syncwarp();
       ptx::tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * Cfg::ACC_COLS;
-      for (int c = 0; c < CHUNKS; ++c, ++ck) {
-        const int b = ck % NBUF;
+      // the field of chunk c (this thread's CWQ replicas) from the accumulator columns
+      auto load_F = [&](int c, float* F) {
         const int col0 = c * CW + h * CWQ;
-        float F[CWQ];
         if (NPLANES == 1) {
           uint32_t v[CWQ];
           ptx::tmem_ld<CWQ>(t_row + col0, v);
@@ -334,6 +336,26 @@ __global__ void __cluster_dims__(2, 1, 1)
           }
 #pragma unroll
           for (int j = 0; j < CWQ; ++j) F[j] = __fmul_rn(__ll2float_rn(tot[j]), 0x1p-30f);
+        }
+      };
+      float Fall[Cfg::EARLY_DRAIN ? CHUNKS : 1][CWQ];
+      if constexpr (Cfg::EARLY_DRAIN) {  // one accumulator buffer: drain, release, then update
+#pragma unroll
+        for (int c = 0; c < CHUNKS; ++c) load_F(c, Fall[c]);
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader0);
+      }
+#pragma unroll
+      for (int c = 0; c < CHUNKS; ++c, ++ck) {
+        const int b = ck % NBUF;
+        const int col0 = c * CW + h * CWQ;
+        float F[CWQ];
+        if constexpr (Cfg::EARLY_DRAIN) {
+#pragma unroll
+          for (int j = 0; j < CWQ; ++j) F[j] = Fall[c][j];
+        } else {
+          load_F(c, F);
         }
         ptx::mbar_wait(sfull_bar(b), (ck / NBUF) & 1);
         float* xs = reinterpret_cast<float*>(s_gen + b * Cfg::BUF_BYTES);
@@ -368,9 +390,11 @@ __global__ void __cluster_dims__(2, 1, 1)
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(sdone_bar(b));
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(buf ? tempty_leader1 : tempty_leader0);
+      if constexpr (!Cfg::EARLY_DRAIN) {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(buf ? tempty_leader1 : tempty_leader0);
+      }
     }
   }
 

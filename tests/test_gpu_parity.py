@@ -458,3 +458,26 @@ def test_run_pipelined_copies_equal_serial(solver, orc, n, R, monkeypatch):
     assert (out[0].x_final.view(np.uint32) == out[1].x_final.view(np.uint32)).all()
     assert (out[0].energies == out[1].energies).all() and out[0].best_index == out[1].best_index
     assert (out[0].spins == out[1].spins).all()
+
+
+@pytest.mark.parametrize("variant", [BSB, GBSB])
+def test_wide_plane_tiles_bitwise(solver, orc, variant, monkeypatch):
+    """Fixed-point variants on 128-replica pair tiles with one accumulator buffer (chosen
+    automatically for large replica counts; forced here with SBG_STEP_CFG=9) equal the
+    64-replica double-buffered tiles and the fp32 mirror bitwise."""
+    n, R, M = 600, 300, 100
+    J = _sym(n, np.array([1, -1], np.int8), 31)
+    solver.set_instance(J)
+    x0, y0, p0 = orc.init_small_uniform(n, R, master=31)
+    c, dt, a = np.float32(1 / (2 * np.sqrt(n))), np.float32(1.25), np.float32(0.2)
+    cfg = cfg_for(variant, M, float(dt), float(c), float(a))
+    out = []
+    for knob in ("9", "3"):
+        monkeypatch.setenv("SBG_STEP_CFG", knob)
+        solver.set_state(x0, y0, p0)
+        solver.advance(cfg, 0, 15)
+        out.append(solver.get_state())
+    x, _, _ = orc.step_f32(variant, J, x0, y0, p0, 0, M, dt, c, a, 15)
+    for u, v in zip(out[0], out[1]):
+        assert (u.view(np.uint32) == v.view(np.uint32)).all()
+    assert (out[0][0].view(np.uint32) == x.view(np.uint32)).all()

@@ -83,3 +83,28 @@ def test_sk_energy_vs_reference_ising_energy(solver, orc):
     s = np.where(x >= 0, 1.0, -1.0)
     e_ref = -0.5 * np.einsum("ri,ij,rj->r", s, J64, s)
     assert np.abs(energy - e_ref).max() <= 1e-6 * np.abs(e_ref).max()
+
+
+@pytest.mark.parametrize("variant", [0, 2])
+def test_sk_tile_widths_bitwise(solver, orc, variant, monkeypatch):
+    """The real-J step on 64-replica tiles (one accumulator buffer, drained before the state
+    update; the default) and on 32-replica tiles (double-buffered; SBG_FX_BN=32) agree
+    bitwise with each other and with the fp32 mirror, replica count not a tile multiple."""
+    n, R, M = 384, 200, 100
+    J = orc.gen_sk_f32(n, 21)
+    planes, shift = orc.fx_quantize(J)
+    solver.set_instance(J)
+    x0, y0, p0 = orc.init_small_uniform(n, R, master=21)
+    c, dt, a = np.float32(0.5), np.float32(1.25), np.float32(0.2)
+    cfg = cfg_for(variant, M, float(dt), float(c), float(a))
+    out = []
+    for bn in ("64", "32"):
+        monkeypatch.setenv("SBG_FX_BN", bn)
+        solver.set_state(x0, y0, p0)
+        solver.advance(cfg, 0, 12)
+        out.append(solver.get_state())
+    x, y, p = orc.step_f32_fx(variant, planes, shift, x0, y0, p0, 0, M, dt, c, a, 12)
+    for g in out:
+        assert (g[0].view(np.uint32) == x.view(np.uint32)).all()
+        assert (g[1].view(np.uint32) == y.view(np.uint32)).all()
+        assert (g[2].view(np.uint32) == p.view(np.uint32)).all()
