@@ -141,7 +141,7 @@ __global__ void prep_planes_kernel(const float* __restrict__ x, uint8_t* __restr
     if (nplanes == 1) {
       G[gi] = ok ? static_cast<uint8_t>(sgn8(v)) : 0;
     } else {
-      const uint32_t q = static_cast<uint32_t>(quant30(v));
+      const uint32_t q = qdigits(quant30(v));
       for (int pl = 0; pl < nplanes; ++pl) G[pl * plane_stride + gi] = static_cast<uint8_t>(q >> (8 * pl));
     }
   }

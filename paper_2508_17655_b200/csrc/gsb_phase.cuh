@@ -111,6 +111,16 @@ __device__ __forceinline__ void gsb_phase2(float F0, float F1, float& x0, float&
 // as four byte planes (u8, u8, u8, s8). |x| <= 1 so |q| <= 2^30.
 __device__ __forceinline__ int32_t quant30(float x) { return __float2int_rn(__fmul_rn(x, 0x1p30f)); }
 
+// q as four SIGNED base-256 digits d_p in [-128, 127], q = sum_p d_p 2^(8p), packed one
+// per byte (plane p = byte p). Adding 128 to each of the three low bytes (with carries)
+// and flipping their top bits back gives the balanced digits: d_p = u_p - 128 for p < 3
+// and d_3 = u >> 24 (|q| <= 2^30 keeps it in [-64, 64]). Every plane is then s8, so one
+// MMA instruction can take all planes of the B operand; the field sum_p 2^(8p) (J . d_p)
+// is the same integer J . q as with unsigned low planes.
+__device__ __forceinline__ uint32_t qdigits(int32_t q) {
+  return static_cast<uint32_t>(q + 0x00808080) ^ 0x00808080u;
+}
+
 // sgn with sgn(0) = +1 (model.cpp:161-165, engine.cpp:73-77).
 __device__ __forceinline__ int8_t sgn8(float x) { return x >= 0.0f ? int8_t(1) : int8_t(-1); }
 

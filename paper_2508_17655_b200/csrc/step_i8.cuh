@@ -175,7 +175,6 @@ __global__ void __launch_bounds__(384, 1)
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t idesc_s = ptx::idesc_i8(128, BN, !args.a_unsigned, true);
-      const uint32_t idesc_u = ptx::idesc_i8(128, BN, !args.a_unsigned, false);
       int stage = 0;
       uint32_t ph = 0;
       int lt = 0;
@@ -193,7 +192,7 @@ __global__ void __launch_bounds__(384, 1)
           for (int pl = 0; pl < NPLANES; ++pl) {
             const uint64_t bdesc =
                 ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES);
-            const uint32_t idesc = (NPLANES == 1 || pl == NPLANES - 1) ? idesc_s : idesc_u;
+            const uint32_t idesc = idesc_s;  // sign plane or signed digit planes (qdigits)
 #pragma unroll
             for (int k = 0; k < Cfg::BK / 32; ++k) {
               // +32 bytes along K inside the 128-byte swizzle atom = +2 in the
@@ -288,7 +287,7 @@ __global__ void __launch_bounds__(384, 1)
                 if (NPLANES == 1) {
                   args.planes_next[goff] = static_cast<uint8_t>(sgn8(xs[j]));
                 } else {
-                  const uint32_t qv = static_cast<uint32_t>(quant30(xs[j]));
+                  const uint32_t qv = qdigits(quant30(xs[j]));
 #pragma unroll
                   for (int pl = 0; pl < NPLANES; ++pl)
                     args.planes_next[pl * plane_stride + goff] = static_cast<uint8_t>(qv >> (8 * pl));

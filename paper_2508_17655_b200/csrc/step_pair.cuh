@@ -59,6 +59,10 @@ struct PairStepCfg {
   // epilogue (non-e2m1) then drains all accumulator columns before the state update
   static constexpr int NACC = (Q4 || 2 * ACC_COLS > 512) ? 1 : 2;
   static constexpr bool EARLY_DRAIN = !Q4 && NACC == 1;
+  // all digit planes in one MMA (N = NPLANES * N_PAIR <= 256). The pair's output columns are
+  // then [CTA 0's B rows][CTA 1's B rows], each [plane][B_HALF replicas]: plane p of replica
+  // r (of the tile) sits at column (r / B_HALF) * NPLANES * B_HALF + p * B_HALF + r % B_HALF
+  static constexpr bool MERGED = !Q4 && NPLANES > 1 && NPLANES * N_PAIR <= 256;
   static constexpr int TMEM_COLS = Q4 ? 512 : NACC * ACC_COLS;
   static constexpr uint32_t COL_SF = 512 - 16;          // Q4: unit E8M0 scale factors
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
@@ -197,7 +201,9 @@ __global__ void __cluster_dims__(2, 1, 1)
     if (leader && args.dbg < 2) {  // --------------------------------- MMA issuer (leader CTA only)
       // whole warp walks the schedule; one elected lane issues (uniform descriptors)
       constexpr uint32_t idesc_s = Cfg::Q4 ? ptx::idesc_mxf4(256, N_PAIR) : ptx::idesc_i8(256, N_PAIR, true, true);
-      constexpr uint32_t idesc_u = ptx::idesc_i8(256, N_PAIR, true, false);
+      // MERGED: the NPLANES signed digit planes of B are consecutive smem tiles, i.e. one
+      // B operand of NPLANES * N_PAIR rows: one MMA per K-chunk reads A once for all planes
+      constexpr uint32_t idesc_m = ptx::idesc_i8(256, Cfg::MERGED ? NPLANES * N_PAIR : N_PAIR, true, true);
       const uint32_t sf = tmem_base + Cfg::COL_SF;
       int stage = 0;
       uint32_t ph = 0;
@@ -212,16 +218,22 @@ __global__ void __cluster_dims__(2, 1, 1)
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
             const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + stage * Cfg::A_BYTES);
+            if constexpr (Cfg::MERGED) {
+              const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + stage * NPLANES * Cfg::B_PLANE_BYTES);
 #pragma unroll
-            for (int pl = 0; pl < NPLANES; ++pl) {
-              const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES);
-              const uint32_t idesc = (NPLANES == 1 || pl == NPLANES - 1) ? idesc_s : idesc_u;
+              for (int k = 0; k < Cfg::BK / 32; ++k)
+                ptx::mma_i8_pair(d_base, adesc + 2 * k, bdesc + 2 * k, idesc_m, (kb | k) != 0);
+            } else {
 #pragma unroll
-              for (int k = 0; k < Cfg::BK / 32; ++k) {  // 32 bytes per MMA (K = 32 int8 / 64 e2m1)
-                if constexpr (Cfg::Q4)
-                  ptx::mma_mxf4_pair(d_base, adesc + 2 * k, bdesc + 2 * k, idesc, sf, (kb | k) != 0);
-                else
-                  ptx::mma_i8_pair(d_base + pl * N_PAIR, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+              for (int pl = 0; pl < NPLANES; ++pl) {
+                const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES);
+#pragma unroll
+                for (int k = 0; k < Cfg::BK / 32; ++k) {  // 32 bytes per MMA (K = 32 int8 / 64 e2m1)
+                  if constexpr (Cfg::Q4)
+                    ptx::mma_mxf4_pair(d_base, adesc + 2 * k, bdesc + 2 * k, idesc_s, sf, (kb | k) != 0);
+                  else
+                    ptx::mma_i8_pair(d_base + pl * N_PAIR, adesc + 2 * k, bdesc + 2 * k, idesc_s, (kb | k) != 0);
+                }
               }
             }
             ptx::mma_commit_pair_mc(empty_bar(stage), 0x3);
@@ -329,7 +341,10 @@ __global__ void __cluster_dims__(2, 1, 1)
 #pragma unroll
           for (int pl = 0; pl < NPLANES; ++pl) {
             uint32_t v[CWQ];
-            ptx::tmem_ld<CWQ>(t_row + pl * N_PAIR + col0, v);
+            const int col = Cfg::MERGED ? (col0 / Cfg::B_HALF) * NPLANES * Cfg::B_HALF + pl * Cfg::B_HALF +
+                                              col0 % Cfg::B_HALF
+                                        : pl * N_PAIR + col0;
+            ptx::tmem_ld<CWQ>(t_row + col, v);
             ptx::tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < CWQ; ++j) tot[j] += static_cast<long long>(static_cast<int32_t>(v[j])) << (8 * pl);
@@ -381,7 +396,7 @@ __global__ void __cluster_dims__(2, 1, 1)
           } else if (NPLANES == 1) {
             gs[idx] = static_cast<uint8_t>(sgn8(xv));
           } else {
-            const uint32_t qv = static_cast<uint32_t>(quant30(xv));
+            const uint32_t qv = qdigits(quant30(xv));
 #pragma unroll
             for (int pl = 0; pl < NPLANES; ++pl) gs[pl * Cfg::ST_G + idx] = static_cast<uint8_t>(qv >> (8 * pl));
           }

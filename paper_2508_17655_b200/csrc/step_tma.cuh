@@ -65,6 +65,8 @@ struct TmaStepCfg {
   // accumulator buffers: 2 when they fit TMEM, else 1 (the epilogue then drains all of a
   // tile's accumulator columns first and releases them before its state chunks)
   static constexpr int ABUF = 2 * ACC_COLS <= 512 ? 2 : 1;
+  // one MMA per J plane over all (signed digit) planes of B (N = NPLANES * BN <= 256)
+  static constexpr bool MERGED = NPLANES > 1 && NPLANES * BN <= 256;
   static constexpr int TMEM_COLS = ABUF * ACC_COLS <= 256 ? 256 : 512;
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static constexpr int NUM_BARS = 2 * STAGES + 4 + 3 * NBUF;
@@ -260,16 +262,41 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
         for (int kb = 0; kb < KB; ++kb) {
           ptx::mbar_wait(full_bar(stage), ph);
           ptx::tc_fence_after();
-          if (ptx::elect_one()) {
+          const bool issuer = ptx::elect_one();
+          if (Cfg::MERGED && issuer) {
+            // all NPLANES signed digit planes of B in one MMA per J plane ap: the product
+            // J_ap x d_p lands in accumulator ap + p (columns (ap + p) BN ..), as below. In a
+            // tile's first K-chunk, plane NPLANES-1 of ap >= 1 opens accumulator ap + NPLANES-1
+            // (a separate N = BN MMA without accumulate); everything else accumulates.
+            constexpr uint32_t NB = BN;
+#pragma unroll
+            for (int k = 0; k < Cfg::BK / 32; ++k) {
+#pragma unroll
+              for (int ap = 0; ap < NA; ++ap) {
+                const bool a_signed = NA == 1 || ap == NA - 1;
+                const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + (stage * NA + ap) * Cfg::A_BYTES) + 2 * k;
+                const uint64_t bd0 = ptx::smem_desc_k_sw128(b_base + stage * NPLANES * Cfg::B_PLANE_BYTES) + 2 * k;
+                const uint32_t d = d_base + ap * NB;
+                if (kb == 0 && k == 0 && ap > 0) {
+                  const uint64_t bdl =
+                      ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + NPLANES - 1) * Cfg::B_PLANE_BYTES);
+                  ptx::mma_i8(d, adesc, bd0, ptx::idesc_i8(128, (NPLANES - 1) * NB, a_signed, true), true);
+                  ptx::mma_i8(d + (NPLANES - 1) * NB, adesc, bdl, ptx::idesc_i8(128, NB, a_signed, true), false);
+                } else {
+                  ptx::mma_i8(d, adesc, bd0, ptx::idesc_i8(128, NPLANES * NB, a_signed, true), (kb | k | ap) != 0);
+                }
+              }
+            }
+            ptx::mma_commit(empty_bar(stage));
+          } else if (!Cfg::MERGED && issuer) {
 #pragma unroll
             for (int ap = 0; ap < NA; ++ap) {
               const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + (stage * NA + ap) * Cfg::A_BYTES);
 #pragma unroll
               for (int pl = 0; pl < NPLANES; ++pl) {
                 const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES);
-                // plane signedness: only the top plane of a multi-plane operand is signed
-                const uint32_t idesc =
-                    ptx::idesc_i8(128, BN, NA == 1 || ap == NA - 1, NPLANES == 1 || pl == NPLANES - 1);
+                // J planes: only the top plane is signed; B: sign plane or signed digit planes
+                const uint32_t idesc = ptx::idesc_i8(128, BN, NA == 1 || ap == NA - 1, true);
                 // products of equal weight 2^(8(ap+pl)) share one accumulator; the first
                 // pair of each weight (in this loop order) starts it at kb == 0
                 const int w = ap + pl;
@@ -486,7 +513,7 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
               if (NPLANES == 1) {
                 gs[idx] = static_cast<uint8_t>(sgn8(xv));
               } else {
-                const uint32_t qv = static_cast<uint32_t>(quant30(xv));
+                const uint32_t qv = qdigits(quant30(xv));
 #pragma unroll
                 for (int pl = 0; pl < NPLANES; ++pl) gs[pl * Cfg::ST_G + idx] = static_cast<uint8_t>(qv >> (8 * pl));
               }
