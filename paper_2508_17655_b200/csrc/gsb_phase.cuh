@@ -108,7 +108,7 @@ __device__ __forceinline__ void gsb_phase2(float F0, float F1, float& x0, float&
 }
 
 // q = rint(x * 2^30): the fixed-point image of x fed to the int8 tensor cores
-// as four byte planes (u8, u8, u8, s8). |x| <= 1 so |q| <= 2^30.
+// as four byte planes (signed base-256 digits, qdigits). |x| <= 1 so |q| <= 2^30.
 __device__ __forceinline__ int32_t quant30(float x) { return __float2int_rn(__fmul_rn(x, 0x1p30f)); }
 
 // q as four SIGNED base-256 digits d_p in [-128, 127], q = sum_p d_p 2^(8p), packed one

@@ -9,7 +9,7 @@
 //
 // G is the MMA B operand, K-major: G[r][j] int8, one plane (dsb/gdsb: the
 // sign matrix, exact +-1) or four byte planes of q = rint(x * 2^30)
-// (bsb/gbsb: u8,u8,u8,s8; the field sum is then exact in integers and scaled
+// (bsb/gbsb: signed base-256 digits, qdigits; the field sum is then exact in integers and scaled
 // once). J is the A operand, row-major int8 [npad][npad]. Both arrive by TMA
 // (128-byte swizzle) into a STAGES-deep mbarrier ring; one elected lane of
 // warp 1 issues the MMAs into one of two TMEM accumulator buffers, so the
