@@ -129,7 +129,10 @@ int sbg_set_couplings_entries_f64(sbg_ctx* ctx, int64_t n, int64_t m, const int6
 int64_t sbg_n(const sbg_ctx* ctx);
 
 /* Replica states. Replace SolverState (engine.hpp:40-47) x R.
- * sbg_set_state: host x, y, p (p may be NULL -> 1), each R x n, step index m = 0. */
+ * sbg_set_state: host x, y, p (p may be NULL -> 1), each R x n, step index m = 0.
+ * Domain: |x| <= 1, as every reference init produces (engine.cpp:25-39) and the walls keep
+ * (engine.cpp:93-99); the continuous variants' fixed-point field q = rint(x 2^30) as four
+ * signed base-256 digits is exact for |x| < 1.99 and undefined beyond. */
 int sbg_set_state(sbg_ctx* ctx, int64_t R, const float* x, const float* y, const float* p);
 /* Device-side init_state (see SBG_INIT_*), replicas offset .. offset+R-1. */
 int sbg_init_state(sbg_ctx* ctx, int64_t R, int32_t mode, uint64_t master, uint64_t tag,
