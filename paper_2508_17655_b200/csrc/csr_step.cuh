@@ -188,6 +188,158 @@ __global__ void __launch_bounds__(CSR_THREADS, CSR_MIN_BLOCKS)
   }
 }
 
+// Same step with the gathers staged through shared memory by cp.async (register-free loads):
+// a warp issues up to NB gathers of its row (and its x, y, p) before waiting once, so each
+// warp keeps NB loads in flight where the register-path kernel keeps one (its accumulate
+// consumes each gather before the next is issued, at 32 registers). Per warp: NB slots of
+// 32 * EB bytes (EB = 16 for q, 4 for sign bytes) + 1.5 KB of x, y, p. Bitwise the same
+// field and update as csr_step_sm_kernel (identical integer sums, same gsb_phase).
+constexpr int CSRA_THREADS = 128;
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, uint64_t pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+template <bool SIGN, int NB>
+__host__ __device__ constexpr size_t csra_warp_smem() {
+  return size_t(NB) * 32 * (SIGN ? 4 : 16) + 3 * 512;
+}
+
+template <bool SIGN, int NB>
+__global__ void __launch_bounds__(CSRA_THREADS)
+    csr_step_async_kernel(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                          const int8_t* __restrict__ val, const void* __restrict__ g_cur, void* __restrict__ g_next,
+                          float* __restrict__ xs, float* __restrict__ ys, float* __restrict__ ps, int64_t rp,
+                          int32_t R, PhaseConsts k, const float* __restrict__ a_rep = nullptr) {
+  constexpr int EB = SIGN ? 4 : 16;
+  extern __shared__ __align__(16) unsigned char csra_sm[];
+  const int lane = threadIdx.x & 31;
+  unsigned char* wsm = csra_sm + (threadIdx.x >> 5) * csra_warp_smem<SIGN, NB>();
+  const uint32_t slot0 = static_cast<uint32_t>(__cvta_generic_to_shared(wsm)) + lane * EB;
+  const float* xyp = reinterpret_cast<const float*>(wsm + NB * 32 * EB);
+  const uint32_t xyp0 = static_cast<uint32_t>(__cvta_generic_to_shared(xyp)) + lane * 16;
+  const int chunks = static_cast<int>((R + CSR_RCHUNK - 1) / CSR_RCHUNK);
+  const int64_t tasks = static_cast<int64_t>(n) * chunks;
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t stream = l2::evict_first(), keep = l2::evict_last();
+  const uint32_t rsb = static_cast<uint32_t>(rp) * (SIGN ? 1u : 4u);
+  for (int64_t t = wid; t < tasks; t += nw) {
+    const int i = static_cast<int>(t / chunks);
+    const int r = static_cast<int>(t % chunks) * CSR_RCHUNK + 4 * lane;
+    const size_t off = static_cast<size_t>(i) * rp + r;
+    // this task's x, y, p ride along with the first gather batch
+    cp_async16(xyp0, xs + off, stream);
+    cp_async16(xyp0 + 512, ys + off, stream);
+    cp_async16(xyp0 + 1024, ps + off, stream);
+    const int kb = rowptr[i], ke = rowptr[i + 1];
+    const char* gb = static_cast<const char*>(g_cur) + static_cast<size_t>(r) * (SIGN ? 1 : 4);
+    long long acc[4] = {0, 0, 0, 0};
+    for (int k0 = kb; k0 < ke; k0 += 32) {
+      const int cnt = min(32, ke - k0);
+      int jl = 0, vl = 0;
+      if (lane < cnt) {
+        jl = col[k0 + lane];
+        vl = val[k0 + lane];
+      }
+      for (int b0 = 0; b0 < cnt; b0 += NB) {
+        const int nb = min(NB, cnt - b0);
+#pragma unroll
+        for (int s = 0; s < NB; ++s) {
+          const int j = __shfl_sync(0xffffffffu, jl, b0 + s);
+          if (s < nb) {
+            const char* src = gb + static_cast<uint64_t>(static_cast<uint32_t>(j)) * rsb;
+            if (SIGN)
+              cp_async4(slot0 + s * 32 * EB, src, keep);
+            else
+              cp_async16(slot0 + s * 32 * EB, src, keep);
+          }
+        }
+        cp_async_commit_wait_all();
+#pragma unroll
+        for (int s = 0; s < NB; ++s) {
+          const long long v = __shfl_sync(0xffffffffu, vl, b0 + s);
+          if (s < nb) {
+            if (SIGN) {
+              const char4 g = *reinterpret_cast<const char4*>(wsm + s * 32 * EB + lane * EB);
+              acc[0] += v * g.x;
+              acc[1] += v * g.y;
+              acc[2] += v * g.z;
+              acc[3] += v * g.w;
+            } else {
+              const int4 q = *reinterpret_cast<const int4*>(wsm + s * 32 * EB + lane * EB);
+              acc[0] += v * q.x;
+              acc[1] += v * q.y;
+              acc[2] += v * q.z;
+              acc[3] += v * q.w;
+            }
+          }
+        }
+      }
+    }
+    cp_async_commit_wait_all();  // rows without nonzeros: x, y, p still in flight
+    float4 x4 = *reinterpret_cast<const float4*>(xyp + 4 * lane);
+    float4 y4 = *reinterpret_cast<const float4*>(xyp + 128 + 4 * lane);
+    float4 p4 = *reinterpret_cast<const float4*>(xyp + 256 + 4 * lane);
+    __syncwarp();  // the next task's cp.async reuses this warp's slots
+    if (r >= R) continue;
+    float F[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      F[e] = SIGN ? static_cast<float>(acc[e]) : __fmul_rn(__ll2float_rn(acc[e]), 0x1p-30f);
+    PhaseConsts kk[4] = {k, k, k, k};
+    if (a_rep) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) kk[e].a = a_rep[min(r + e, R - 1)];
+    }
+    gsb_phase(F[0], x4.x, y4.x, p4.x, kk[0]);
+    gsb_phase(F[1], x4.y, y4.y, p4.y, kk[1]);
+    gsb_phase(F[2], x4.z, y4.z, p4.z, kk[2]);
+    gsb_phase(F[3], x4.w, y4.w, p4.w, kk[3]);
+    l2::st_f4(xs + off, x4, stream);
+    l2::st_f4(ys + off, y4, stream);
+    l2::st_f4(ps + off, p4, stream);
+    if (SIGN) {
+      char4 s;
+      s.x = sgn8(x4.x);
+      s.y = sgn8(x4.y);
+      s.z = sgn8(x4.z);
+      s.w = sgn8(x4.w);
+      l2::st_u32(static_cast<int8_t*>(g_next) + off, *reinterpret_cast<uint32_t*>(&s), keep);
+    } else {
+      l2::st_i4(static_cast<int32_t*>(g_next) + off,
+                make_int4(quant30(x4.x), quant30(x4.y), quant30(x4.z), quant30(x4.w)), keep);
+    }
+  }
+}
+
+template <bool SIGN, int NB>
+inline cudaError_t launch_csr_async(cudaStream_t st, int sms, int32_t n, const int32_t* rowptr, const int32_t* col,
+                                    const int8_t* val, const void* g_cur, void* g_next, float* xs, float* ys,
+                                    float* ps, int64_t rp, int32_t R, PhaseConsts k, const float* a_rep) {
+  constexpr size_t smem = (CSRA_THREADS / 32) * csra_warp_smem<SIGN, NB>();
+  static int per_sm = 0;  // resident blocks per SM (shared memory bound), once per instantiation
+  if (per_sm == 0) {
+    cudaFuncSetAttribute(csr_step_async_kernel<SIGN, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_step_async_kernel<SIGN, NB>, CSRA_THREADS, smem);
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  }
+  const int64_t tasks = int64_t(n) * ((R + CSR_RCHUNK - 1) / CSR_RCHUNK);
+  const int wpb = CSRA_THREADS / 32;
+  const int blocks = int(std::min<int64_t>((tasks + wpb - 1) / wpb, int64_t(sms) * per_sm));
+  csr_step_async_kernel<SIGN, NB><<<blocks, CSRA_THREADS, smem, st>>>(n, rowptr, col, val, g_cur, g_next, xs, ys,
+                                                                      ps, rp, R, k, a_rep);
+  return cudaGetLastError();
+}
+
 // B operand of the current (spin-major) state: sign bytes or q = rint(x 2^30).
 template <bool SIGN>
 __global__ void csr_prep_kernel(const float* __restrict__ xs, void* __restrict__ g, size_t count) {

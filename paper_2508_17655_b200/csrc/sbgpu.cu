@@ -1282,24 +1282,63 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
       csr_prep_kernel<false><<<grid_for(ctx, cnt, 256), 256, 0, ctx->stream>>>(ctx->dXs, ctx->dQ[0], cnt);
     CK(cudaGetLastError());
     ++ctx->launches;
-    const int64_t tasks = ctx->n * ((ctx->R + CSR_RCHUNK - 1) / CSR_RCHUNK);
-    const int blocks = int(std::min<int64_t>((tasks + CSR_THREADS / 32 - 1) / (CSR_THREADS / 32), int64_t(ctx->sms) * 8));
-    int cur = 0;
     const float* arep = (honours_a && ctx->d_arep && ctx->arep_n == ctx->R) ? ctx->d_arep : nullptr;
-    for (uint64_t m = m_begin; m < m_end; ++m) {
-      PhaseConsts km = k;
-      km.inv = 1.0f / static_cast<float>(prm->steps - m);  // == __frcp_rn(M - m)
-      if (sign)
-        csr_step_sm_kernel<true><<<blocks, CSR_THREADS, 0, ctx->stream>>>(
-            n32, ctx->d_rowptr, ctx->d_col, ctx->d_val, ctx->dQ[cur], ctx->dQ[cur ^ 1], ctx->dXs, ctx->dYs, ctx->dPs,
-            ctx->rp, R32, km, arep);
-      else
-        csr_step_sm_kernel<false><<<blocks, CSR_THREADS, 0, ctx->stream>>>(
-            n32, ctx->d_rowptr, ctx->d_col, ctx->d_val, ctx->dQ[cur], ctx->dQ[cur ^ 1], ctx->dXs, ctx->dYs, ctx->dPs,
-            ctx->rp, R32, km, arep);
-      CK(cudaGetLastError());
-      ++ctx->launches;
-      cur ^= 1;
+    // Replica slabs (SBG_CSR_SLAB = width, a multiple of 128): replicas are independent, so the M
+    // steps may run slab by slab, each slab's x, y, p and operand buffers (n * W * 20 B) staying in
+    // L2 across its steps. Bitwise identical for every width. Measured at C3 (N=20000, R=512):
+    // 71.3 us/step in one pass, 69.5 with 256-wide slabs, 78.9 with 128 -- the step is bound by
+    // gather latency, not by the state stream, so the default is one pass over all replicas.
+    int64_t slab = dev_knob("SBG_CSR_SLAB");
+    if (slab <= 0) slab = ctx->R;
+    slab = std::max<int64_t>(CSR_RCHUNK, (slab + CSR_RCHUNK - 1) / CSR_RCHUNK * CSR_RCHUNK);
+    // SBG_CSR_ASYNC = NB in {4, 8, 12, 16}: gathers staged through shared memory by cp.async,
+    // NB per warp in flight (csr_step_async_kernel); 0 = the register-path kernel.
+    const int csra = dev_knob("SBG_CSR_ASYNC");
+    if (csra && csra != 4 && csra != 8 && csra != 12 && csra != 16)
+      return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "SBG_CSR_ASYNC must be 0, 4, 8, 12 or 16");
+    for (int64_t r0 = 0; r0 < ctx->R; r0 += slab) {
+      const int32_t Rs = int32_t(std::min<int64_t>(slab, ctx->R - r0));
+      const int64_t tasks = ctx->n * ((Rs + CSR_RCHUNK - 1) / CSR_RCHUNK);
+      const int blocks =
+          int(std::min<int64_t>((tasks + CSR_THREADS / 32 - 1) / (CSR_THREADS / 32), int64_t(ctx->sms) * 8));
+      const size_t gsz = sign ? 1 : 4;
+      const void* q0 = reinterpret_cast<const char*>(ctx->dQ[0]) + size_t(r0) * gsz;
+      void* q1 = reinterpret_cast<char*>(ctx->dQ[1]) + size_t(r0) * gsz;
+      const void* gq[2] = {q0, q1};
+      float *xs = ctx->dXs + r0, *ys = ctx->dYs + r0, *ps = ctx->dPs + r0;
+      const float* ar = arep ? arep + r0 : nullptr;
+      int cur = 0;
+      for (uint64_t m = m_begin; m < m_end; ++m) {
+        PhaseConsts km = k;
+        km.inv = 1.0f / static_cast<float>(prm->steps - m);  // == __frcp_rn(M - m)
+        void* gn = const_cast<void*>(gq[cur ^ 1]);
+        if (csra) {
+          cudaError_t e = cudaErrorInvalidValue;
+#define CSRA_CASE(NB)                                                                                        \
+  case NB:                                                                                                   \
+    e = sign ? launch_csr_async<true, NB>(ctx->stream, ctx->sms, n32, ctx->d_rowptr, ctx->d_col, ctx->d_val, \
+                                          gq[cur], gn, xs, ys, ps, ctx->rp, Rs, km, ar)                      \
+             : launch_csr_async<false, NB>(ctx->stream, ctx->sms, n32, ctx->d_rowptr, ctx->d_col,           \
+                                           ctx->d_val, gq[cur], gn, xs, ys, ps, ctx->rp, Rs, km, ar);       \
+    break;
+          switch (csra) {
+            CSRA_CASE(4)
+            CSRA_CASE(8)
+            CSRA_CASE(12)
+            CSRA_CASE(16)
+          }
+#undef CSRA_CASE
+          CK(e);
+        } else if (sign)
+          csr_step_sm_kernel<true><<<blocks, CSR_THREADS, 0, ctx->stream>>>(
+              n32, ctx->d_rowptr, ctx->d_col, ctx->d_val, gq[cur], gn, xs, ys, ps, ctx->rp, Rs, km, ar);
+        else
+          csr_step_sm_kernel<false><<<blocks, CSR_THREADS, 0, ctx->stream>>>(
+              n32, ctx->d_rowptr, ctx->d_col, ctx->d_val, gq[cur], gn, xs, ys, ps, ctx->rp, Rs, km, ar);
+        CK(cudaGetLastError());
+        ++ctx->launches;
+        cur ^= 1;
+      }
     }
     const dim3 tg_out(unsigned((ctx->R + 31) / 32), unsigned((ctx->n + 31) / 32));
     for (int a = 0; a < 3; ++a) {

@@ -208,6 +208,53 @@ def test_csr_equals_dense_and_mirror(solver, orc):
         assert (ce == -0.5 * orc.energy2_csr(n, csr, mx)).all()
 
 
+@pytest.mark.parametrize("knobs", [{"SBG_CSR_SLAB": "128"}, {"SBG_CSR_SLAB": "256"}, {"SBG_CSR_ASYNC": "4"},
+                                   {"SBG_CSR_ASYNC": "8"}, {"SBG_CSR_ASYNC": "12"}, {"SBG_CSR_ASYNC": "16"},
+                                   {"SBG_CSR_ASYNC": "8", "SBG_CSR_SLAB": "128"}])
+def test_csr_kernel_variants_bitwise(solver, orc, monkeypatch, knobs):
+    """CSR step variants equal the default kernel bitwise, per-replica A included: replica slabs
+    stepped from L2 (SBG_CSR_SLAB; ragged last slab, 300 = 128+128+44) and the cp.async-staged
+    gather kernel (SBG_CSR_ASYNC = gathers in flight per warp; rows of degree 0 and > 32)."""
+    n, m, R, steps = 3000, 15000, 300, 24
+    (ei, ej, w), (rowptr, col, val) = orc.gen_er_csr(n, m, 5)
+    # one isolated spin and one hub of degree 40: the zero-degree and multi-chunk rows
+    keep = ~((ei == 7) | (ej == 7))
+    ei, ej, w = ei[keep], ej[keep], w[keep]
+    hub = np.arange(100, 140)
+    ei = np.concatenate([ei, np.full(40, 11)])
+    ej = np.concatenate([ej, hub])
+    w = np.concatenate([w, np.where(hub % 3 == 0, 1, -1)]).astype(w.dtype)
+    pairs = {}
+    for a, b, v in zip(ei.tolist(), ej.tolist(), w.tolist()):
+        if a != b:
+            pairs[(min(a, b), max(a, b))] = v
+    rows = [[] for _ in range(n)]
+    for (a, b), v in pairs.items():
+        rows[a].append((b, -v))
+        rows[b].append((a, -v))
+    rowptr = np.zeros(n + 1, np.int32)
+    rowptr[1:] = np.cumsum([len(r) for r in rows])
+    col = np.array([c for r in rows for c, _ in sorted(r)], np.int32)
+    val = np.array([v for r in rows for _, v in sorted(r)], np.int8)
+    assert rowptr[8] == rowptr[7] and rowptr[12] - rowptr[11] > 32
+    x0, y0, p0 = orc.init_small_uniform(n, R, master=4)
+    a_rep = np.linspace(0.0, 0.6, R).astype(np.float32)
+    for variant in (GBSB, GDSB):
+        cfg = cfg_for(variant, 100, 1.25, 0.158, 0.2)
+        out = []
+        for env in ({}, knobs):
+            for key in ("SBG_CSR_SLAB", "SBG_CSR_ASYNC"):
+                monkeypatch.setenv(key, env.get(key, "0"))
+            solver.set_instance_csr(n, rowptr, col, val)
+            solver.set_state(x0, y0, p0)
+            solver.set_replica_a(a_rep)
+            solver.advance(cfg, 0, steps)
+            out.append(solver.get_state())
+        solver.set_replica_a(None)
+        for a, b in zip(*out):
+            assert (a.view(np.uint32) == b.view(np.uint32)).all(), (variant, knobs)
+
+
 def test_c2_shape_subset_bitwise(solver, orc):
     """C2 geometry (N=2000, R=8192, GdSB): GPU replicas r0..r0+7 equal the mirror after 5 steps."""
     from paper_2508_17655_b200 import InitMode
