@@ -176,7 +176,7 @@ int sbg_run_seeded(sbg_ctx* ctx, const sbg_params* params, int64_t R, int32_t in
 
 /* ---- Row sharding (C5: N too large for one GPU) ----------------------------
  * Rank `rank` of `world` owns spins [row0, row0 + rows) with rows = kpad/world,
- * kpad = n_global rounded up to 128*world; Jrows is its rows of J (valid x n_global,
+ * kpad = n_global rounded up to 256*world; Jrows is its rows of J (valid x n_global,
  * row-major). Its x, y, p cover its spins for every replica; the B operand G (signs
  * of ALL spins) is replicated: each step's epilogue writes this rank's slab into
  * its own G and, over NVLink, into every peer's G, then releases per-replica-block

@@ -150,7 +150,7 @@ __global__ void prep_planes_kernel(const float* __restrict__ x, uint8_t* __restr
 // The e2m1 sign plane ([rpad][npad / 2] bytes): byte b of row r packs spins 2b (low
 // nibble) and 2b + 1 as e2m1 codes (+1 = 0x2, -1 = 0xA; padding 0x0).
 __global__ void prep_sign4_kernel(const float* __restrict__ x, uint8_t* __restrict__ G, int32_t n, int32_t npad,
-                                  int32_t R, int32_t rpad) {
+                                  int32_t R, int32_t rpad, int64_t g_ld = -1, int64_t col0 = 0) {
   const int32_t hb = npad / 2;
   const size_t total = static_cast<size_t>(rpad) * hb;
   for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
@@ -161,7 +161,20 @@ __global__ void prep_sign4_kernel(const float* __restrict__ x, uint8_t* __restri
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       if (r < R && i + e < n) v |= (x[static_cast<size_t>(r) * npad + i + e] >= 0.0f ? 0x2u : 0xAu) << (4 * e);
-    G[idx] = static_cast<uint8_t>(v);
+    // row shards: this shard's slab of the global [rpad][kpad / 2] operand (col0 even)
+    G[g_ld < 0 ? idx : static_cast<size_t>(r) * g_ld + col0 / 2 + idx % hb] = static_cast<uint8_t>(v);
+  }
+}
+
+// Packed e2m1 sign codes [rpad][width / 2] -> int8 signs [rpad][width] (0x2 -> +1, 0xA -> -1,
+// padding 0 -> 0): the byte-per-spin plane the readout kernels take.
+__global__ void unpack_sign4_kernel(const uint8_t* __restrict__ G4, int8_t* __restrict__ S, int64_t width,
+                                    int32_t rpad) {
+  const size_t total = static_cast<size_t>(rpad) * width;
+  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const uint32_t c = (G4[idx / 2] >> (4 * (idx & 1))) & 0xFu;
+    S[idx] = c == 0 ? 0 : (c & 0x8u) ? -1 : 1;
   }
 }
 

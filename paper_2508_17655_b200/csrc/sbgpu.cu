@@ -277,10 +277,17 @@ int launch_multistep_pair(sbg_ctx* ctx, const TmaMaps& maps, MultiStepArgs a) {
   a.num_n = int32_t(ctx->rpad / NPAIR);
   const int64_t pair_tiles = int64_t(a.num_m / 2) * a.num_n * a.nsteps;
   const int grid = 2 * int(std::min<int64_t>(pair_tiles, ctx->sms / 2));
-  CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * a.num_n, ctx->stream));
+  if (!ctx->sharded) CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * a.num_n, ctx->stream));
   CK(launch_persistent(kern, grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream, maps, a));
   ++ctx->launches;
+  if (ctx->sharded) ctx->done_base += uint32_t(a.nsteps * a.num_m_total);
   return SBG_OK;
+}
+
+// Sign variants streaming J on e2m1 operands (CTA pairs, kind::mxf4): the large-N regime
+// (C5), row shards included; G is then the packed [rpad][kpad / 2] plane (g_mode 2).
+bool q4_stream(const sbg_ctx* ctx) {
+  return ctx->dJ4 && ctx->kind == KIND_DENSE_I8 && ctx->npad % 256 == 0 && dev_knob("SBG_STEP_CFG") == 0;
 }
 
 // Resident-state pair kernel (step_resident.cuh): sign variants, dense int8 J.
@@ -542,8 +549,8 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
                             gdim(ctx), 128, RES_NR, CU_TENSOR_MAP_SWIZZLE_NONE);
         }
         if (rcr) return rcr;
-        if (ctx->dJ4 && !ctx->sharded) {  // e2m1 operands: G as [rpad][npad / 2], two spins per byte
-          const uint64_t gb = uint64_t(ctx->npad / 2), gv4 = (gvalid + 1) / 2;
+        if (ctx->dJ4) {  // e2m1 operands: G as [rpad][kpad / 2], two spins per byte
+          const uint64_t gb = uint64_t(gdim(ctx) / 2), gv4 = (gvalid + 1) / 2;
           const int nrs[2] = {128, RES_NR};
           for (int w = 0; w < 2 && !rcr; ++w) {
             TmaMaps& qm = w ? ctx->qmaps160_sign[cur] : ctx->qmaps_sign[cur];
@@ -680,7 +687,7 @@ int gen_rows_common(sbg_ctx* ctx, int64_t n_global, int32_t world, int32_t rank,
   ctx->dJ4 = nullptr;
   ctx->dJ = nullptr;
   const bool shard = world > 1;
-  const int64_t kpad = shard ? round_up(n_global, int64_t(128) * world) : round_up(n_global, PAD_N);
+  const int64_t kpad = shard ? round_up(n_global, int64_t(256) * world) : round_up(n_global, PAD_N);
   const int64_t rows = shard ? kpad / world : kpad;
   const int64_t row0 = shard ? int64_t(rank) * rows : 0;
   const int64_t valid = std::max<int64_t>(0, std::min<int64_t>(rows, n_global - row0));
@@ -1349,15 +1356,16 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
   } else {
     const bool resident = use_resident(ctx, prm->variant);
     const int knob = dev_knob("SBG_STEP_CFG");
-    const bool pair_ok = (ctx->npad % 256) == 0 && !ctx->sharded;
+    const bool pair_ok = (ctx->npad % 256) == 0;
     // streaming sign launches on e2m1 operands (the J-streaming regime, e.g. C5: half the bytes)
-    const bool q4s = sign && !resident && ctx->dJ4 && pair_ok && knob == 0 && ctx->kind == KIND_DENSE_I8;
+    const bool q4s = sign && !resident && q4_stream(ctx);
     const int need = q4s ? 2 : sign ? 1 : NPL;
     if (ctx->g_mode != need && !resident) {  // the resident kernel publishes its own G_0
       if (q4s) {
         const size_t tot = size_t(ctx->rpad) * (ctx->npad / 2);
         prep_sign4_kernel<<<grid_for(ctx, tot, 256), 256, 0, ctx->stream>>>(
-            ctx->dX, ctx->dG[ctx->g_cur], int32_t(ctx->n), int32_t(ctx->npad), int32_t(ctx->R), int32_t(ctx->rpad));
+            ctx->dX, ctx->dG[ctx->g_cur], int32_t(ctx->n), int32_t(ctx->npad), int32_t(ctx->R), int32_t(ctx->rpad),
+            gdim(ctx) / 2, ctx->sharded ? ctx->row0 : 0);
         CK(cudaGetLastError());
         ++ctx->launches;
       } else {
@@ -1397,7 +1405,7 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
       a.num_m_total = int32_t(ctx->sharded ? ctx->num_m_total : ctx->npad / 128);
       a.col0 = int32_t(ctx->sharded ? ctx->row0 : 0);
       a.done_base = ctx->sharded ? ctx->done_base : 0;
-      a.g_ld = ctx->sharded ? ctx->kpad : ctx->npad;
+      a.g_ld = (ctx->sharded ? ctx->kpad : ctx->npad) / (q4s ? 2 : 1);  // bytes per G row
       a.npeers = ctx->sharded ? int32_t(ctx->peer_done.size()) : 0;
       for (int pr = 0; pr < a.npeers; ++pr) {
         // step parity 0 writes buffer cur^1, parity 1 buffer cur (as the local Gout maps)
@@ -1900,7 +1908,7 @@ int sbg_set_couplings_rows_i8(sbg_ctx* ctx, int64_t n_global, int32_t world, int
   CHECK_CTX(ctx);
   if (n_global < 1 || world < 1 || world > 8 || rank < 0 || rank >= world || !Jrows)
     return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "bad row-shard arguments");
-  const int64_t kpad = round_up(n_global, int64_t(128) * world);
+  const int64_t kpad = round_up(n_global, int64_t(256) * world);  // 256-row slabs: whole CTA pairs
   const int64_t rows = kpad / world;  // multiple of 128
   const int64_t row0 = int64_t(rank) * rows;
   const int64_t valid = std::max<int64_t>(0, std::min<int64_t>(rows, n_global - row0));
@@ -1936,7 +1944,8 @@ int sbg_set_couplings_rows_i8(sbg_ctx* ctx, int64_t n_global, int32_t world, int
   ctx->peer_g1.clear();
   ctx->peer_done.clear();
   if (valid == 0) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "rank owns no spins (too many ranks for n)");
-  return encode_2d_u8(ctx, &ctx->tmJ, ctx->dJ, kpad, rows, 128, 128);
+  const int rc = encode_2d_u8(ctx, &ctx->tmJ, ctx->dJ, kpad, rows, 128, 128);
+  return rc ? rc : build_q4(ctx, rows, kpad);
 }
 
 int sbg_shard_info(const sbg_ctx* ctx, int64_t* row0, int64_t* rows_valid, int64_t* rows_padded, int64_t* kpad) {
@@ -1982,9 +1991,19 @@ int sbg_shard_prepare(sbg_ctx* ctx, int32_t variant) {
   if (!ctx->sharded || !ctx->dX) return ctx->fail(SBG_ERR_STATE, "row shard with state required");
   if (!is_sign_variant(variant)) return ctx->fail(SBG_ERR_UNSUPPORTED, "row sharding supports dsb/gdsb");
   CK(cudaSetDevice(ctx->device));
-  int rc = prep_planes(ctx, ctx->dX, ctx->dG[ctx->g_cur], 1, ctx->R, ctx->rpad, /*into_global=*/true);
-  if (rc) return rc;
-  ctx->g_mode = 1;
+  if (q4_stream(ctx)) {
+    const size_t tot = size_t(ctx->rpad) * (ctx->npad / 2);
+    prep_sign4_kernel<<<grid_for(ctx, tot, 256), 256, 0, ctx->stream>>>(
+        ctx->dX, ctx->dG[ctx->g_cur], int32_t(ctx->n), int32_t(ctx->npad), int32_t(ctx->R), int32_t(ctx->rpad),
+        ctx->kpad / 2, ctx->row0);
+    CK(cudaGetLastError());
+    ++ctx->launches;
+    ctx->g_mode = 2;
+  } else {
+    int rc = prep_planes(ctx, ctx->dX, ctx->dG[ctx->g_cur], 1, ctx->R, ctx->rpad, /*into_global=*/true);
+    if (rc) return rc;
+    ctx->g_mode = 1;
+  }
   CK(cudaStreamSynchronize(ctx->stream));
   return SBG_OK;
 }
@@ -1995,9 +2014,11 @@ int sbg_shard_push_slab(sbg_ctx* ctx) {
   if (!ctx->sharded) return ctx->fail(SBG_ERR_STATE, "not a row shard");
   CK(cudaSetDevice(ctx->device));
   for (size_t i = 0; i < ctx->peer_g0.size(); ++i) {
-    uint8_t* dst = (ctx->g_cur == 0 ? ctx->peer_g0[i] : ctx->peer_g1[i]) + ctx->row0;
-    const uint8_t* src = ctx->dG[ctx->g_cur] + ctx->row0;
-    CK(cudaMemcpy2DAsync(dst, ctx->kpad, src, ctx->kpad, ctx->npad, ctx->R, cudaMemcpyDefault, ctx->stream));
+    const int64_t kb = ctx->g_mode == 2 ? 2 : 1;  // spins per byte (packed e2m1 plane)
+    uint8_t* dst = (ctx->g_cur == 0 ? ctx->peer_g0[i] : ctx->peer_g1[i]) + ctx->row0 / kb;
+    const uint8_t* src = ctx->dG[ctx->g_cur] + ctx->row0 / kb;
+    CK(cudaMemcpy2DAsync(dst, ctx->kpad / kb, src, ctx->kpad / kb, ctx->npad / kb, ctx->R, cudaMemcpyDefault,
+                         ctx->stream));
   }
   CK(cudaStreamSynchronize(ctx->stream));
   return SBG_OK;
@@ -2034,14 +2055,26 @@ int sbg_shard_ipc_open(sbg_ctx* ctx, const void* in192, void** g0, void** g1, vo
 // plane G[cur] (all spins, sign variants after a step or sbg_shard_prepare + push).
 int sbg_readout_partial(sbg_ctx* ctx, int64_t* e2) {
   CHECK_CTX(ctx);
-  if (!ctx->sharded || !ctx->dX || ctx->g_mode != 1) return ctx->fail(SBG_ERR_STATE, "sign-variant row shard required");
+  if (!ctx->sharded || !ctx->dX || (ctx->g_mode != 1 && ctx->g_mode != 2))
+    return ctx->fail(SBG_ERR_STATE, "sign-variant row shard required");
   CK(cudaSetDevice(ctx->device));
+  int gb = ctx->g_cur;
+  if (ctx->g_mode == 2) {
+    // packed e2m1 signs of all spins -> a byte-per-spin plane in the other G buffer (the next
+    // step's output buffer, rewritten in full by every rank's next step)
+    gb ^= 1;
+    const size_t tot = size_t(ctx->rpad) * ctx->kpad;
+    unpack_sign4_kernel<<<grid_for(ctx, tot, 256), 256, 0, ctx->stream>>>(
+        ctx->dG[ctx->g_cur], reinterpret_cast<int8_t*>(ctx->dG[gb]), ctx->kpad, int32_t(ctx->rpad));
+    CK(cudaGetLastError());
+    ++ctx->launches;
+  }
   CK(cudaMemsetAsync(ctx->dE2, 0, sizeof(unsigned long long) * ctx->rpad, ctx->stream));
   StepArgs a = base_args(ctx, BN_SIGN, ctx->R, ctx->rpad);
-  a.sign_in = reinterpret_cast<const int8_t*>(ctx->dG[ctx->g_cur]) + ctx->row0;
+  a.sign_in = reinterpret_cast<const int8_t*>(ctx->dG[gb]) + ctx->row0;
   a.sign_ld = ctx->kpad;
   a.e2 = ctx->dE2;
-  int rc = launch_step<1, BN_SIGN, EpiMode::Readout>(ctx, ctx->tmG_sign[ctx->g_cur], a);
+  int rc = launch_step<1, BN_SIGN, EpiMode::Readout>(ctx, ctx->tmG_sign[gb], a);
   if (rc) return rc;
   CK(cudaMemcpyAsync(e2, ctx->dE2, sizeof(long long) * ctx->R, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));

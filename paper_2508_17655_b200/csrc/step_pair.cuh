@@ -160,6 +160,16 @@ __global__ void __cluster_dims__(2, 1, 1)
   const int pair = blockIdx.x >> 1;
   const int npairs = gridDim.x >> 1;
   const int KB = args.kpad / (Cfg::BK * Cfg::KPB);
+  // Row shards (npeers > 0, K7): counters also count the peers' m-blocks (num_m_total per
+  // step) and are released by other GPUs over NVLink, so waits are system-scope.
+  const bool sharded = args.npeers > 0;
+  auto wait_dep = [&](int n_blk, int s) {
+    const uint32_t need = static_cast<uint32_t>(s * args.num_m_total);
+    if (sharded)
+      dep::wait_block_sys(args.done, n_blk, args.done_base, need);
+    else
+      dep::wait_block(args.done, n_blk, args.done_base, need);
+  };
 
   if (warp == 0) {
     if (args.dbg < 2) {  // ------------------------------------------- operand producer (both CTAs)
@@ -176,7 +186,7 @@ __global__ void __cluster_dims__(2, 1, 1)
         const int s = g / T2, w = g % T2;
         const int n_blk = w / num_mp, mp = w % num_mp;
         const int m_blk = 2 * mp + static_cast<int>(cr);
-        dep::wait_block(args.done, n_blk, args.done_base, static_cast<uint32_t>(s * args.num_m));
+        wait_dep(n_blk, s);
         const CUtensorMap* gin = &maps.Gin[s & 1];
         for (int kb = 0; kb < KB; ++kb) {
           ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
@@ -258,7 +268,7 @@ __global__ void __cluster_dims__(2, 1, 1)
       for (int g = pair; g < total; g += npairs) {
         const int s = g / T2, w = g % T2;
         const int n_blk = w / num_mp, mp = w % num_mp;
-        dep::wait_block(args.done, n_blk, args.done_base, static_cast<uint32_t>(s * args.num_m));
+        wait_dep(n_blk, s);
         const int i0 = (2 * mp + static_cast<int>(cr)) * Cfg::BM, rb = n_blk * N_PAIR;
         for (int c = 0; c < CHUNKS; ++c, ++ck) {
           const int b = ck % NBUF;
@@ -272,38 +282,74 @@ __global__ void __cluster_dims__(2, 1, 1)
       }
     }
   } else if (warp == 3) {
-    if (lane == 0) {  // ------------------------------------------------ state storer
+    // ---------------------------------------------------------------- state storer
+    // lane 0 drives the TMA stores; in sharded runs the whole warp also pushes the
+    // chunk's slab of G_{t+1} into every peer's buffer (16-byte NVLink stores).
+    if (lane == 0) {
       ptx::prefetch_tmap(&maps.Gout[0]);
       ptx::prefetch_tmap(&maps.Gout[1]);
-      int ck = 0;
-      const uint64_t stream = ptx::policy_evict_first();
-      const uint64_t keep = ptx::policy_evict_last();
-      for (int g = pair; g < total; g += npairs) {
-        const int s = g / T2, w = g % T2;
-        const int n_blk = w / num_mp, mp = w % num_mp;
-        const int i0 = (2 * mp + static_cast<int>(cr)) * Cfg::BM, rb = n_blk * N_PAIR;
-        const CUtensorMap* gout = &maps.Gout[s & 1];
-        for (int c = 0; c < CHUNKS; ++c, ++ck) {
-          const int b = ck % NBUF;
-          ptx::mbar_wait(sdone_bar(b), (ck / NBUF) & 1);
-          const uint32_t sb = s_base + b * Cfg::BUF_BYTES;
-          const int r0 = rb + c * CW;
+    }
+    int ck = 0;
+    const uint64_t stream = ptx::policy_evict_first();
+    const uint64_t keep = ptx::policy_evict_last();
+    constexpr int GROW = Cfg::BM / Cfg::KPB;  // bytes of one replica row of a G chunk
+    for (int g = pair; g < total; g += npairs) {
+      const int s = g / T2, w = g % T2;
+      const int n_blk = w / num_mp, mp = w % num_mp;
+      const int i0 = (2 * mp + static_cast<int>(cr)) * Cfg::BM, rb = n_blk * N_PAIR;
+      const CUtensorMap* gout = &maps.Gout[s & 1];
+      for (int c = 0; c < CHUNKS; ++c, ++ck) {
+        const int b = ck % NBUF;
+        ptx::mbar_wait(sdone_bar(b), (ck / NBUF) & 1);
+        const uint32_t sb = s_base + b * Cfg::BUF_BYTES;
+        const int r0 = rb + c * CW;
+        if (lane == 0) {
           ptx::tma_store_2d_hint(&maps.X, sb, i0, r0, stream);
           ptx::tma_store_2d_hint(&maps.Y, sb + Cfg::ST_ARR, i0, r0, stream);
           ptx::tma_store_2d_hint(&maps.P, sb + 2 * Cfg::ST_ARR, i0, r0, stream);
 #pragma unroll
           for (int pl = 0; pl < NPLANES; ++pl)
-            ptx::tma_store_2d_hint(gout, sb + 3 * Cfg::ST_ARR + pl * Cfg::ST_G, i0 / Cfg::KPB,
+            ptx::tma_store_2d_hint(gout, sb + 3 * Cfg::ST_ARR + pl * Cfg::ST_G, (args.col0 + i0) / Cfg::KPB,
                                    (NPLANES == 1 ? 0 : pl * args.rpad) + r0, keep);
           ptx::bulk_commit();
+        }
+        if (sharded) {
+          const uint8_t* gs = s_gen + b * Cfg::BUF_BYTES + 3 * Cfg::ST_ARR;
+          for (int pr = 0; pr < args.npeers; ++pr) {
+            uint8_t* dst0 = args.peer_g[s & 1][pr];
+#pragma unroll
+            for (int pl = 0; pl < NPLANES; ++pl) {
+              for (int e = lane; e < CW * GROW / 16; e += 32) {
+                const int row = e / (GROW / 16), piece = e % (GROW / 16);
+                const int rr = r0 + row;
+                if (rr >= args.R) continue;
+                const uint4 v = *reinterpret_cast<const uint4*>(gs + pl * Cfg::ST_G + row * GROW + piece * 16);
+                *reinterpret_cast<uint4*>(dst0 + (static_cast<size_t>(NPLANES == 1 ? 0 : pl * args.rpad) + rr) *
+                                                     args.g_ld + (args.col0 + i0) / Cfg::KPB + piece * 16) = v;
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
           ptx::bulk_wait_read0();
           ptx::mbar_arrive(sempty_bar(b));
         }
+        __syncwarp();
+      }
+      if (lane == 0) {
         ptx::bulk_wait0();
         dep::fence_proxy_async_global();
-        __threadfence();
-        dep::release_add(args.done + n_blk, 1u);
+        if (sharded) {
+          __threadfence_system();
+          dep::release_add_sys(args.done + n_blk, 1u);
+          for (int pr = 0; pr < args.npeers; ++pr) dep::release_add_sys(args.peer_done[pr] + n_blk, 1u);
+        } else {
+          __threadfence();
+          dep::release_add(args.done + n_blk, 1u);
+        }
       }
+      __syncwarp();
     }
   } else {
     // --------------------------------------------------------------------- epilogue

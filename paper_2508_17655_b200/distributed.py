@@ -96,8 +96,8 @@ def distributed_batch_best_of(solver, cfg, tuning, n_batch: int, master_seed: in
 
 def row_shard(n_global: int, world: int, rank: int) -> tuple[int, int, int]:
     """(row0, rows_valid, rows_padded): the split sbg_set_couplings_rows_i8 applies
-    (kpad = n rounded up to 128*world, equal 128-multiple slabs)."""
-    kpad = -(-n_global // (128 * world)) * 128 * world
+    (kpad = n rounded up to 256*world, equal 256-multiple slabs: whole CTA pairs)."""
+    kpad = -(-n_global // (256 * world)) * 256 * world
     rows = kpad // world
     row0 = rank * rows
     return row0, max(0, min(rows, n_global - row0)), rows

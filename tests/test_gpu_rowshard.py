@@ -7,12 +7,26 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
+# default: CTA-pair kernel on packed e2m1 J/G; SBG_Q4=0: CTA-pair kernel on int8 operands;
+# + SBG_STEP_CFG=-1: the single-CTA int8 kernel
+SHARD_KERNELS = [{}, {"SBG_Q4": "0"}, {"SBG_Q4": "0", "SBG_STEP_CFG": "-1"}]
 
-def test_two_shards_lockstep_equal_unsharded(orc):
+
+@pytest.fixture(params=SHARD_KERNELS, ids=["e2m1_pair", "int8_pair", "int8_single"])
+def shard_kernel(request, monkeypatch):
+    for k in ("SBG_Q4", "SBG_STEP_CFG"):
+        monkeypatch.delenv(k, raising=False)
+    for k, v in request.param.items():
+        monkeypatch.setenv(k, v)
+    return request.param
+
+
+@pytest.mark.parametrize("n,R,steps,world", [(700, 100, 25, 2), (3000, 300, 8, 4)])
+def test_two_shards_lockstep_equal_unsharded(orc, shard_kernel, n, R, steps, world):
     from paper_2508_17655_b200 import InitMode, Solver, SolverConfig, Variant
     from paper_2508_17655_b200.distributed import connect_row_shards_local, row_shard, row_sharded_energies
 
-    n, R, M, steps, world = 700, 100, 200, 25, 2
+    M = 200
     J = orc.gen_dense_i8(n, 31)
     cfg = SolverConfig(variant=Variant.gdsb, steps=M, dt=1.25, c=1 / (2 * np.sqrt(n)), a=0.2)
     with Solver(0) as full:
@@ -26,6 +40,7 @@ def test_two_shards_lockstep_equal_unsharded(orc):
         for k, s in enumerate(shards):
             row0, valid, _ = row_shard(n, world, k)
             s.set_instance_rows(J[row0:row0 + valid], n, world, k)
+            assert s.operand_format == ("int8" if shard_kernel else "e2m1")
             s.init_state(R, InitMode.small_uniform, 3, 7)
             x0, _, _ = s.get_state()
             ex, _, _ = orc.init_small_uniform(n, R, master=3, tag=7)
@@ -54,7 +69,7 @@ def test_two_shards_lockstep_equal_unsharded(orc):
             s.close()
 
 
-def test_hash_couplings_match_oracle_and_shards(orc):
+def test_hash_couplings_match_oracle_and_shards(orc, shard_kernel):
     """Device +-1 generator (large-N instances) == its oracle restatement; row shards of it
     reproduce the unsharded GdSB run bitwise (lockstep emulation)."""
     from paper_2508_17655_b200 import InitMode, Solver, SolverConfig, Variant
