@@ -132,6 +132,10 @@ struct sbg_ctx {
   uint32_t done_base = 0;  // done[] counters run on across launches (peers increment them)
   std::vector<uint8_t*> peer_g0, peer_g1;
   std::vector<uint32_t*> peer_done;
+  float* d_fpart = nullptr;  // K-split partial fields (pair kernel), fpart_cap floats
+  size_t fpart_cap = 0;
+  uint32_t* d_kdone = nullptr;
+  size_t kdone_cap = 0;
   float* d_arep = nullptr;  // optional per-replica A (sbg_set_replica_a), honoured by gbsb/gdsb
   int64_t arep_n = 0;
   uint32_t* d_done = nullptr;            // per replica-block tile counters of the multi-step kernel
@@ -275,13 +279,48 @@ int launch_multistep_pair(sbg_ctx* ctx, const TmaMaps& maps, MultiStepArgs a) {
   auto kern = gsb_multistep_pair_kernel<NP, NPAIR, ST, NB, CW, Q4>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
   a.num_n = int32_t(ctx->rpad / NPAIR);
-  const int64_t pair_tiles = int64_t(a.num_m / 2) * a.num_n * a.nsteps;
+  if (NP != 1) a.ksplit = 1;
+  if (a.ksplit > 1) {
+    const size_t need = size_t(a.ksplit - 1) * size_t(ctx->rpad) * size_t(ctx->npad);
+    if (ctx->fpart_cap < need) {
+      cudaFree(ctx->d_fpart);
+      ctx->d_fpart = nullptr;
+      ctx->fpart_cap = 0;
+      CK(cudaMalloc(&ctx->d_fpart, sizeof(float) * need));
+      ctx->fpart_cap = need;
+    }
+    const size_t nk = size_t(a.num_n) * size_t(a.num_m);
+    if (ctx->kdone_cap < nk) {
+      cudaFree(ctx->d_kdone);
+      ctx->d_kdone = nullptr;
+      ctx->kdone_cap = 0;
+      CK(cudaMalloc(&ctx->d_kdone, sizeof(uint32_t) * nk));
+      ctx->kdone_cap = nk;
+    }
+    CK(cudaMemsetAsync(ctx->d_kdone, 0, sizeof(uint32_t) * nk, ctx->stream));
+    a.fpart = ctx->d_fpart;
+    a.kdone = ctx->d_kdone;
+  }
+  const int64_t pair_tiles = int64_t(a.num_m / 2) * a.num_n * a.nsteps * std::max(1, a.ksplit);
   const int grid = 2 * int(std::min<int64_t>(pair_tiles, ctx->sms / 2));
   if (!ctx->sharded) CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * a.num_n, ctx->stream));
   CK(launch_persistent(kern, grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream, maps, a));
   ++ctx->launches;
   if (ctx->sharded) ctx->done_base += uint32_t(a.nsteps * a.num_m_total);
   return SBG_OK;
+}
+
+// K parts per pair tile (SBG_KSPLIT = n forces n parts; default 1). Splitting a tile's K range
+// over several CTA pairs would fill the pairs a whole-tile schedule leaves idle in its last wave
+// (C5: 49 tiles per rank at G = 8 on 74 pairs), and it is bitwise exact, but measured slower:
+// G = 8 per-rank step 202 -> 257 us with 3 parts, single-GPU C5 1033 -> 1678 us (ncu: tensor
+// pipe 61 -> 44 % of active cycles; the single accumulator buffer idles the MMAs while each
+// part's partial field drains through global memory, and the last part waits on the others).
+int ksplit_for(const sbg_ctx* ctx, int64_t tiles) {
+  (void)ctx;
+  (void)tiles;
+  const int knob = dev_knob("SBG_KSPLIT");
+  return knob > 1 ? std::min(knob, 8) : 1;
 }
 
 // Sign variants streaming J on e2m1 operands (CTA pairs, kind::mxf4): the large-N regime
@@ -899,6 +938,8 @@ void sbg_destroy(sbg_ctx* ctx) {
   free_state(ctx);
   cudaFree(ctx->d_arep);
   cudaFree(ctx->d_ready);
+  cudaFree(ctx->d_fpart);
+  cudaFree(ctx->d_kdone);
   cudaFree(ctx->dJ);
   cudaFree(ctx->dJ4);
   ctx->dJ4 = nullptr;
@@ -1453,6 +1494,7 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
           // non-resident sign launches are the large-N J-streaming regime (C5: 2.06 ms/step,
           // 0.79 of HBM with 5 operand stages vs 2.29 ms with 3); e2m1 operands halve J
           default:
+            a.ksplit = q4s ? ksplit_for(ctx, (ctx->npad / 256) * (ctx->rpad / NPAIR_SIGN)) : 1;
             rc = q4s ? launch_multistep_pair<1, NPAIR_SIGN, 5, 2, 16, true>(ctx, ctx->pqmaps_sign[cur], a)
                      : launch_multistep_pair<1, NPAIR_SIGN, 5, 2>(ctx, ctx->maps_sign[cur], a);
         }

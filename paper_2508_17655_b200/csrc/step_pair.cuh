@@ -156,7 +156,9 @@ __global__ void __cluster_dims__(2, 1, 1)
 
   const int num_mp = args.num_m / 2;
   const int T2 = num_mp * args.num_n;  // pair tiles per step
-  const int total = T2 * args.nsteps;
+  const int KS = args.ksplit > 1 ? args.ksplit : 1;
+  const int T2K = T2 * KS;             // work units per step: (pair tile, K part), parts adjacent
+  const int total = T2K * args.nsteps;
   const int pair = blockIdx.x >> 1;
   const int npairs = gridDim.x >> 1;
   const int KB = args.kpad / (Cfg::BK * Cfg::KPB);
@@ -183,12 +185,12 @@ __global__ void __cluster_dims__(2, 1, 1)
       uint32_t ph = 0;
       const uint64_t keep = ptx::policy_evict_last();  // J and G are re-read every step: keep them in L2
       for (int g = pair; g < total; g += npairs) {
-        const int s = g / T2, w = g % T2;
+        const int s = g / T2K, w = (g % T2K) / KS, kp = (g % T2K) % KS;
         const int n_blk = w / num_mp, mp = w % num_mp;
         const int m_blk = 2 * mp + static_cast<int>(cr);
         wait_dep(n_blk, s);
         const CUtensorMap* gin = &maps.Gin[s & 1];
-        for (int kb = 0; kb < KB; ++kb) {
+        for (int kb = kp * KB / KS; kb < (kp + 1) * KB / KS; ++kb) {
           ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
           if (ptx::elect_one()) {
             const uint32_t fb = ptx::mapa(full_bar(stage), 0);  // the leader's full barrier
@@ -220,10 +222,11 @@ __global__ void __cluster_dims__(2, 1, 1)
       int lt = 0;
       for (int g = pair; g < total; g += npairs, ++lt) {
         const int buf = lt % NACC;
+        const int kp = (g % T2K) % KS, kb0 = kp * KB / KS;
         ptx::mbar_wait(tempty_bar(buf), ((lt / NACC) & 1) ^ 1u);
         ptx::tc_fence_after();
         const uint32_t d_base = tmem_base + buf * Cfg::ACC_COLS;
-        for (int kb = 0; kb < KB; ++kb) {
+        for (int kb = kb0; kb < (kp + 1) * KB / KS; ++kb) {
           ptx::mbar_wait(full_bar(stage), ph);
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
@@ -232,7 +235,7 @@ __global__ void __cluster_dims__(2, 1, 1)
               const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + stage * NPLANES * Cfg::B_PLANE_BYTES);
 #pragma unroll
               for (int k = 0; k < Cfg::BK / 32; ++k)
-                ptx::mma_i8_pair(d_base, adesc + 2 * k, bdesc + 2 * k, idesc_m, (kb | k) != 0);
+                ptx::mma_i8_pair(d_base, adesc + 2 * k, bdesc + 2 * k, idesc_m, (kb != kb0 || k != 0));
             } else {
 #pragma unroll
               for (int pl = 0; pl < NPLANES; ++pl) {
@@ -240,9 +243,9 @@ __global__ void __cluster_dims__(2, 1, 1)
 #pragma unroll
                 for (int k = 0; k < Cfg::BK / 32; ++k) {  // 32 bytes per MMA (K = 32 int8 / 64 e2m1)
                   if constexpr (Cfg::Q4)
-                    ptx::mma_mxf4_pair(d_base, adesc + 2 * k, bdesc + 2 * k, idesc_s, sf, (kb | k) != 0);
+                    ptx::mma_mxf4_pair(d_base, adesc + 2 * k, bdesc + 2 * k, idesc_s, sf, (kb != kb0 || k != 0));
                   else
-                    ptx::mma_i8_pair(d_base + pl * N_PAIR, adesc + 2 * k, bdesc + 2 * k, idesc_s, (kb | k) != 0);
+                    ptx::mma_i8_pair(d_base + pl * N_PAIR, adesc + 2 * k, bdesc + 2 * k, idesc_s, (kb != kb0 || k != 0));
                 }
               }
             }
@@ -266,7 +269,8 @@ __global__ void __cluster_dims__(2, 1, 1)
       int ck = 0;
       const uint64_t stream = ptx::policy_evict_first();  // x, y, p are touched once per step
       for (int g = pair; g < total; g += npairs) {
-        const int s = g / T2, w = g % T2;
+        const int s = g / T2K, w = (g % T2K) / KS;
+        if ((g % T2K) % KS != KS - 1) continue;  // only the last K part updates the state
         const int n_blk = w / num_mp, mp = w % num_mp;
         wait_dep(n_blk, s);
         const int i0 = (2 * mp + static_cast<int>(cr)) * Cfg::BM, rb = n_blk * N_PAIR;
@@ -294,7 +298,8 @@ __global__ void __cluster_dims__(2, 1, 1)
     const uint64_t keep = ptx::policy_evict_last();
     constexpr int GROW = Cfg::BM / Cfg::KPB;  // bytes of one replica row of a G chunk
     for (int g = pair; g < total; g += npairs) {
-      const int s = g / T2, w = g % T2;
+      const int s = g / T2K, w = (g % T2K) / KS;
+      if ((g % T2K) % KS != KS - 1) continue;
       const int n_blk = w / num_mp, mp = w % num_mp;
       const int i0 = (2 * mp + static_cast<int>(cr)) * Cfg::BM, rb = n_blk * N_PAIR;
       const CUtensorMap* gout = &maps.Gout[s & 1];
@@ -362,14 +367,20 @@ __global__ void __cluster_dims__(2, 1, 1)
     int ck = 0;
     int lt = 0;
     for (int g = pair; g < total; g += npairs, ++lt) {
-      const int s = g / T2;
-      const int rbase = ((g % T2) / num_mp) * N_PAIR;  // first replica of this pair tile
+      const int s = g / T2K, w = (g % T2K) / KS, kp = (g % T2K) % KS;
+      const int rbase = (w / num_mp) * N_PAIR;  // first replica of this pair tile
+      const int m_blk = 2 * (w % num_mp) + static_cast<int>(cr);
       k.inv = __frcp_rn(static_cast<float>(args.M - (args.t_begin + static_cast<uint64_t>(s))));
       const int buf = lt % NACC;
       if (args.dbg < 2) ptx::mbar_wait(tfull_bar(buf), (lt / NACC) & 1);
       __syncwarp();
       ptx::tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * Cfg::ACC_COLS;
+      // K split: partial fields of parts 0..KS-2, replica-major so a warp's 32 rows are contiguous
+      const size_t frow = static_cast<size_t>(m_blk) * Cfg::BM + srow;
+      auto fpart_at = [&](int part, int col) {
+        return args.fpart + (static_cast<size_t>(part) * args.rpad + rbase + col) * args.npad + frow;
+      };
       // the field of chunk c (this thread's CWQ replicas) from the accumulator columns
       auto load_F = [&](int c, float* F) {
         const int col0 = c * CW + h * CWQ;
@@ -399,6 +410,34 @@ __global__ void __cluster_dims__(2, 1, 1)
           for (int j = 0; j < CWQ; ++j) F[j] = __fmul_rn(__ll2float_rn(tot[j]), 0x1p-30f);
         }
       };
+      if (NPLANES == 1 && KS > 1 && kp != KS - 1) {
+        // a leading K part: publish the partial field, free the accumulator, count the part
+#pragma unroll
+        for (int c = 0; c < CHUNKS; ++c) {
+          float F[CWQ];
+          load_F(c, F);
+#pragma unroll
+          for (int j = 0; j < CWQ; ++j) __stcg(fpart_at(kp, c * CW + h * CWQ + j), F[j]);
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(buf ? tempty_leader1 : tempty_leader0);
+        ptx::named_bar_sync(1, Cfg::EPI_WARPS * 32);
+        if (threadIdx.x == 4 * 32) {
+          __threadfence();
+          dep::release_add(args.kdone + static_cast<size_t>(w / num_mp) * args.num_m + m_blk, 1u);
+        }
+        continue;
+      }
+      if (NPLANES == 1 && KS > 1) {  // the last K part: wait for the other parts of this tile
+        if (threadIdx.x == 4 * 32) {
+          const uint32_t need = static_cast<uint32_t>((KS - 1) * (s + 1));
+          const uint32_t* kd = args.kdone + static_cast<size_t>(w / num_mp) * args.num_m + m_blk;
+          while (dep::ld_acquire(kd) < need) __nanosleep(32);
+          __threadfence();
+        }
+        ptx::named_bar_sync(1, Cfg::EPI_WARPS * 32);
+      }
       float Fall[Cfg::EARLY_DRAIN ? CHUNKS : 1][CWQ];
       if constexpr (Cfg::EARLY_DRAIN) {  // one accumulator buffer: drain, release, then update
 #pragma unroll
@@ -417,6 +456,12 @@ __global__ void __cluster_dims__(2, 1, 1)
           for (int j = 0; j < CWQ; ++j) F[j] = Fall[c][j];
         } else {
           load_F(c, F);
+        }
+        if (NPLANES == 1 && KS > 1) {
+          // exact integers below 2^24 (|F| <= kpad): fp32 sums in any order are exact
+          for (int part = 0; part < KS - 1; ++part)
+#pragma unroll
+            for (int j = 0; j < CWQ; ++j) F[j] += __ldcg(fpart_at(part, col0 + j));
         }
         ptx::mbar_wait(sfull_bar(b), (ck / NBUF) & 1);
         float* xs = reinterpret_cast<float*>(s_gen + b * Cfg::BUF_BYTES);

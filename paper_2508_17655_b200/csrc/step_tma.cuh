@@ -104,6 +104,13 @@ struct MultiStepArgs {
   uint8_t* peer_g[2][7]; // peers' G buffers for step parity 0/1 (NVLink peer / IPC pointers)
   uint32_t* peer_done[7];
   const float* a_rep;    // optional per-replica control strength A (sweeps over A in one launch)
+  // --- K split (CTA-pair kernel, sign plane): each pair tile's K range runs as ksplit units on
+  // different pairs; units 0..ksplit-2 store their partial fields (exact integers) into
+  // fpart[kp][rpad][npad] and count kdone[n_blk * num_m + m_blk]; unit ksplit-1 adds them to
+  // its own and runs the state update. ksplit <= 1: no split.
+  int32_t ksplit;
+  float* fpart;
+  uint32_t* kdone;
 };
 constexpr int MAX_PEERS = 7;
 

@@ -528,3 +528,32 @@ def test_wide_plane_tiles_bitwise(solver, orc, variant, monkeypatch):
     for u, v in zip(out[0], out[1]):
         assert (u.view(np.uint32) == v.view(np.uint32)).all()
     assert (out[0][0].view(np.uint32) == x.view(np.uint32)).all()
+
+
+@pytest.mark.parametrize("ks", [2, 3, 4])
+def test_e2m1_stream_k_split_bitwise(solver, orc, monkeypatch, ks):
+    """Streaming e2m1 pair kernel with each pair tile's K range split over ks CTA pairs
+    (SBG_KSPLIT; partial fields exchanged through global memory) == no split == the
+    resident kernel, bitwise, with per-replica A; K blocks not divisible by ks included."""
+    n, R, steps = 2000, 300, 12
+    J = orc.gen_dense_i8(n, 9)
+    x0, y0, p0 = orc.init_small_uniform(n, R, master=6)
+    a_rep = np.linspace(0.0, 0.5, R).astype(np.float32)
+    cfg = cfg_for(GDSB, 100, 1.25, float(1 / (2 * np.sqrt(n))), 0.2)
+    out = []
+    for env in ({}, {"SBG_RESIDENT": "0", "SBG_KSPLIT": "1"}, {"SBG_RESIDENT": "0", "SBG_KSPLIT": str(ks)}):
+        for key in ("SBG_RESIDENT", "SBG_KSPLIT"):
+            monkeypatch.delenv(key, raising=False)
+        for key, v in env.items():
+            monkeypatch.setenv(key, v)
+        solver.set_instance(J)
+        assert solver.operand_format == "e2m1"
+        solver.set_state(x0, y0, p0)
+        solver.set_replica_a(a_rep)
+        solver.advance(cfg, 0, 5)
+        solver.advance(cfg, 5, steps)
+        out.append(solver.get_state())
+        solver.set_replica_a(None)
+    for st in out[1:]:
+        for a, b in zip(out[0], st):
+            assert (a.view(np.uint32) == b.view(np.uint32)).all()
