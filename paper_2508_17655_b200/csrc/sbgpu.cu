@@ -120,6 +120,7 @@ struct sbg_ctx {
   TmaMaps rmaps160_sign[2];                  // resident-state pair kernel, NR 160 (B halves of 80 rows)
   TmaMaps qmaps_sign[2], qmaps160_sign[2];   // the same on e2m1 operands (J4; G as [rpad][npad / 2])
   TmaMaps pqmaps_sign[2];                    // streaming sign pair kernel on e2m1 operands
+  TmaMaps pq128maps_sign[2];                 // the same with 128-replica pair tiles
   unsigned long long* dE2p = nullptr;    // real-J readout: per-J-plane partial E2 [FX_NA][rpad]
   // CSR: spin-major working copies [npad][rp] and the ping-pong gathered operand (q int32 / sign int8)
   float *dXs = nullptr, *dYs = nullptr, *dPs = nullptr;
@@ -321,6 +322,16 @@ int ksplit_for(const sbg_ctx* ctx, int64_t tiles) {
   (void)tiles;
   const int knob = dev_knob("SBG_KSPLIT");
   return knob > 1 ? std::min(knob, 8) : 1;
+}
+
+// 128-replica pair tiles, replica blocks fastest (SBG_Q4_NPAIR=128; default 256): meant to fill
+// the pairs 256-replica tiles leave idle in the last wave while the replica blocks of one
+// pair-block share its J reads in L2. Bitwise equal, measured slower (C5 single GPU 1045 ->
+// 1277 us, G = 4 per rank 349 -> 364, G = 8 202 -> 264): half-width MMAs (N = 128) and twice the
+// per-tile fixed costs outweigh the better wave fill.
+bool q4_narrow(const sbg_ctx* ctx) {
+  (void)ctx;
+  return dev_knob("SBG_Q4_NPAIR") == 128;
 }
 
 // Sign variants streaming J on e2m1 operands (CTA pairs, kind::mxf4): the large-N regime
@@ -602,14 +613,16 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
                                 gb, 64, nrs[w], CU_TENSOR_MAP_SWIZZLE_NONE);
             }
           }
-          TmaMaps& pq = ctx->pqmaps_sign[cur];
-          pq = ctx->maps_sign[cur];
-          pq.J = ctx->tmJ4;
-          for (int par = 0; par < 2 && !rcr; ++par) {
-            rcr = encode_2d_u8(ctx, &pq.Gin[par], ctx->dG[cur ^ par], gb, rpad, 128, NPAIR_SIGN / 2);
-            if (!rcr)
-              rcr = encode_2d(ctx, &pq.Gout[par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ par ^ 1], gv4, R, gb,
-                              64, 16, CU_TENSOR_MAP_SWIZZLE_NONE);
+          for (int wv = 0; wv < 2 && !rcr; ++wv) {
+            TmaMaps& pq = wv ? ctx->pq128maps_sign[cur] : ctx->pqmaps_sign[cur];
+            pq = ctx->maps_sign[cur];
+            pq.J = ctx->tmJ4;
+            for (int par = 0; par < 2 && !rcr; ++par) {
+              rcr = encode_2d_u8(ctx, &pq.Gin[par], ctx->dG[cur ^ par], gb, rpad, 128, (wv ? 128 : NPAIR_SIGN) / 2);
+              if (!rcr)
+                rcr = encode_2d(ctx, &pq.Gout[par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ctx->dG[cur ^ par ^ 1], gv4, R,
+                                gb, 64, 16, CU_TENSOR_MAP_SWIZZLE_NONE);
+            }
           }
           if (rcr) return rcr;
         }
@@ -1495,8 +1508,13 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
           // 0.79 of HBM with 5 operand stages vs 2.29 ms with 3); e2m1 operands halve J
           default:
             a.ksplit = q4s ? ksplit_for(ctx, (ctx->npad / 256) * (ctx->rpad / NPAIR_SIGN)) : 1;
-            rc = q4s ? launch_multistep_pair<1, NPAIR_SIGN, 5, 2, 16, true>(ctx, ctx->pqmaps_sign[cur], a)
-                     : launch_multistep_pair<1, NPAIR_SIGN, 5, 2>(ctx, ctx->maps_sign[cur], a);
+            if (q4s && q4_narrow(ctx)) {
+              a.n_fast = 1;
+              rc = launch_multistep_pair<1, 128, 5, 2, 16, true>(ctx, ctx->pq128maps_sign[cur], a);
+            } else {
+              rc = q4s ? launch_multistep_pair<1, NPAIR_SIGN, 5, 2, 16, true>(ctx, ctx->pqmaps_sign[cur], a)
+                       : launch_multistep_pair<1, NPAIR_SIGN, 5, 2>(ctx, ctx->maps_sign[cur], a);
+            }
         }
       } else {
         switch (pair_ok ? knob : -1) {

@@ -158,6 +158,8 @@ __global__ void __cluster_dims__(2, 1, 1)
   const int T2 = num_mp * args.num_n;  // pair tiles per step
   const int KS = args.ksplit > 1 ? args.ksplit : 1;
   const int T2K = T2 * KS;             // work units per step: (pair tile, K part), parts adjacent
+  auto n_of = [&](int w) { return args.n_fast ? w % args.num_n : w / num_mp; };
+  auto mp_of = [&](int w) { return args.n_fast ? w / args.num_n : w % num_mp; };
   const int total = T2K * args.nsteps;
   const int pair = blockIdx.x >> 1;
   const int npairs = gridDim.x >> 1;
@@ -186,7 +188,7 @@ __global__ void __cluster_dims__(2, 1, 1)
       const uint64_t keep = ptx::policy_evict_last();  // J and G are re-read every step: keep them in L2
       for (int g = pair; g < total; g += npairs) {
         const int s = g / T2K, w = (g % T2K) / KS, kp = (g % T2K) % KS;
-        const int n_blk = w / num_mp, mp = w % num_mp;
+        const int n_blk = n_of(w), mp = mp_of(w);
         const int m_blk = 2 * mp + static_cast<int>(cr);
         wait_dep(n_blk, s);
         const CUtensorMap* gin = &maps.Gin[s & 1];
@@ -271,7 +273,7 @@ __global__ void __cluster_dims__(2, 1, 1)
       for (int g = pair; g < total; g += npairs) {
         const int s = g / T2K, w = (g % T2K) / KS;
         if ((g % T2K) % KS != KS - 1) continue;  // only the last K part updates the state
-        const int n_blk = w / num_mp, mp = w % num_mp;
+        const int n_blk = n_of(w), mp = mp_of(w);
         wait_dep(n_blk, s);
         const int i0 = (2 * mp + static_cast<int>(cr)) * Cfg::BM, rb = n_blk * N_PAIR;
         for (int c = 0; c < CHUNKS; ++c, ++ck) {
@@ -300,7 +302,7 @@ __global__ void __cluster_dims__(2, 1, 1)
     for (int g = pair; g < total; g += npairs) {
       const int s = g / T2K, w = (g % T2K) / KS;
       if ((g % T2K) % KS != KS - 1) continue;
-      const int n_blk = w / num_mp, mp = w % num_mp;
+      const int n_blk = n_of(w), mp = mp_of(w);
       const int i0 = (2 * mp + static_cast<int>(cr)) * Cfg::BM, rb = n_blk * N_PAIR;
       const CUtensorMap* gout = &maps.Gout[s & 1];
       for (int c = 0; c < CHUNKS; ++c, ++ck) {
@@ -368,8 +370,8 @@ __global__ void __cluster_dims__(2, 1, 1)
     int lt = 0;
     for (int g = pair; g < total; g += npairs, ++lt) {
       const int s = g / T2K, w = (g % T2K) / KS, kp = (g % T2K) % KS;
-      const int rbase = (w / num_mp) * N_PAIR;  // first replica of this pair tile
-      const int m_blk = 2 * (w % num_mp) + static_cast<int>(cr);
+      const int rbase = n_of(w) * N_PAIR;  // first replica of this pair tile
+      const int m_blk = 2 * mp_of(w) + static_cast<int>(cr);
       k.inv = __frcp_rn(static_cast<float>(args.M - (args.t_begin + static_cast<uint64_t>(s))));
       const int buf = lt % NACC;
       if (args.dbg < 2) ptx::mbar_wait(tfull_bar(buf), (lt / NACC) & 1);
@@ -425,14 +427,14 @@ __global__ void __cluster_dims__(2, 1, 1)
         ptx::named_bar_sync(1, Cfg::EPI_WARPS * 32);
         if (threadIdx.x == 4 * 32) {
           __threadfence();
-          dep::release_add(args.kdone + static_cast<size_t>(w / num_mp) * args.num_m + m_blk, 1u);
+          dep::release_add(args.kdone + static_cast<size_t>(n_of(w)) * args.num_m + m_blk, 1u);
         }
         continue;
       }
       if (NPLANES == 1 && KS > 1) {  // the last K part: wait for the other parts of this tile
         if (threadIdx.x == 4 * 32) {
           const uint32_t need = static_cast<uint32_t>((KS - 1) * (s + 1));
-          const uint32_t* kd = args.kdone + static_cast<size_t>(w / num_mp) * args.num_m + m_blk;
+          const uint32_t* kd = args.kdone + static_cast<size_t>(n_of(w)) * args.num_m + m_blk;
           while (dep::ld_acquire(kd) < need) __nanosleep(32);
           __threadfence();
         }

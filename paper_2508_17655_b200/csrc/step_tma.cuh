@@ -111,6 +111,9 @@ struct MultiStepArgs {
   int32_t ksplit;
   float* fpart;
   uint32_t* kdone;
+  // CTA-pair kernel tile order within a step: 0 = spin pair-blocks fastest, 1 = replica blocks
+  // fastest (the replica blocks of one pair-block run side by side and share its J reads in L2)
+  int32_t n_fast;
 };
 constexpr int MAX_PEERS = 7;
 

@@ -534,15 +534,17 @@ def test_wide_plane_tiles_bitwise(solver, orc, variant, monkeypatch):
 def test_e2m1_stream_k_split_bitwise(solver, orc, monkeypatch, ks):
     """Streaming e2m1 pair kernel with each pair tile's K range split over ks CTA pairs
     (SBG_KSPLIT; partial fields exchanged through global memory) == no split == the
-    resident kernel, bitwise, with per-replica A; K blocks not divisible by ks included."""
+    resident kernel == 128-replica pair tiles in replica-fast order (SBG_Q4_NPAIR), bitwise,
+    with per-replica A; K blocks not divisible by ks included."""
     n, R, steps = 2000, 300, 12
     J = orc.gen_dense_i8(n, 9)
     x0, y0, p0 = orc.init_small_uniform(n, R, master=6)
     a_rep = np.linspace(0.0, 0.5, R).astype(np.float32)
     cfg = cfg_for(GDSB, 100, 1.25, float(1 / (2 * np.sqrt(n))), 0.2)
     out = []
-    for env in ({}, {"SBG_RESIDENT": "0", "SBG_KSPLIT": "1"}, {"SBG_RESIDENT": "0", "SBG_KSPLIT": str(ks)}):
-        for key in ("SBG_RESIDENT", "SBG_KSPLIT"):
+    for env in ({}, {"SBG_RESIDENT": "0", "SBG_KSPLIT": "1"}, {"SBG_RESIDENT": "0", "SBG_KSPLIT": str(ks)},
+                {"SBG_RESIDENT": "0", "SBG_Q4_NPAIR": "128", "SBG_KSPLIT": str(ks - 1)}):
+        for key in ("SBG_RESIDENT", "SBG_KSPLIT", "SBG_Q4_NPAIR"):
             monkeypatch.delenv(key, raising=False)
         for key, v in env.items():
             monkeypatch.setenv(key, v)

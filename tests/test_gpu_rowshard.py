@@ -9,12 +9,12 @@ pytestmark = pytest.mark.gpu
 
 # default: CTA-pair kernel on packed e2m1 J/G; SBG_Q4=0: CTA-pair kernel on int8 operands;
 # + SBG_STEP_CFG=-1: the single-CTA int8 kernel
-SHARD_KERNELS = [{}, {"SBG_Q4": "0"}, {"SBG_Q4": "0", "SBG_STEP_CFG": "-1"}]
+SHARD_KERNELS = [{}, {"SBG_Q4_NPAIR": "128"}, {"SBG_Q4": "0"}, {"SBG_Q4": "0", "SBG_STEP_CFG": "-1"}]
 
 
-@pytest.fixture(params=SHARD_KERNELS, ids=["e2m1_pair", "int8_pair", "int8_single"])
+@pytest.fixture(params=SHARD_KERNELS, ids=["e2m1_pair", "e2m1_pair128", "int8_pair", "int8_single"])
 def shard_kernel(request, monkeypatch):
-    for k in ("SBG_Q4", "SBG_STEP_CFG"):
+    for k in ("SBG_Q4", "SBG_STEP_CFG", "SBG_Q4_NPAIR"):
         monkeypatch.delenv(k, raising=False)
     for k, v in request.param.items():
         monkeypatch.setenv(k, v)
@@ -40,7 +40,7 @@ def test_two_shards_lockstep_equal_unsharded(orc, shard_kernel, n, R, steps, wor
         for k, s in enumerate(shards):
             row0, valid, _ = row_shard(n, world, k)
             s.set_instance_rows(J[row0:row0 + valid], n, world, k)
-            assert s.operand_format == ("int8" if shard_kernel else "e2m1")
+            assert s.operand_format == ("int8" if "SBG_Q4" in shard_kernel else "e2m1")
             s.init_state(R, InitMode.small_uniform, 3, 7)
             x0, _, _ = s.get_state()
             ex, _, _ = orc.init_small_uniform(n, R, master=3, tag=7)
