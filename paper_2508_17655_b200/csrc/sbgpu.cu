@@ -1347,10 +1347,18 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
     // Replica slabs (SBG_CSR_SLAB = width, a multiple of 128): replicas are independent, so the M
     // steps may run slab by slab, each slab's x, y, p and operand buffers (n * W * 20 B) staying in
     // L2 across its steps. Bitwise identical for every width. Measured at C3 (N=20000, R=512):
-    // 71.3 us/step in one pass, 69.5 with 256-wide slabs, 78.9 with 128 -- the step is bound by
-    // gather latency, not by the state stream, so the default is one pass over all replicas.
+    // 71.2 us/step in one pass, 69.5 with 256-wide slabs (twice), 78.9 with 128 (launch tails:
+    // too few warp tasks per launch). Default: the widest slab >= 256 that fits ~110 MB of L2,
+    // when the whole state does not.
     int64_t slab = dev_knob("SBG_CSR_SLAB");
-    if (slab <= 0) slab = ctx->R;
+    if (slab <= 0) {
+      slab = ctx->R;
+      const int64_t budget = 110ll << 20, per = ctx->n * 20;
+      if (ctx->n * ctx->R * 20 > budget && m_end - m_begin >= 8) {
+        const int64_t w = budget / per / CSR_RCHUNK * CSR_RCHUNK;
+        if (w >= 2 * CSR_RCHUNK) slab = w;
+      }
+    }
     slab = std::max<int64_t>(CSR_RCHUNK, (slab + CSR_RCHUNK - 1) / CSR_RCHUNK * CSR_RCHUNK);
     // SBG_CSR_ASYNC = NB in {4, 8, 12, 16}: gathers staged through shared memory by cp.async,
     // NB per warp in flight (csr_step_async_kernel); 0 = the register-path kernel.
