@@ -109,6 +109,9 @@ struct sbg_ctx {
   float *dX = nullptr, *dY = nullptr, *dP = nullptr;
   uint8_t* dG[2] = {nullptr, nullptr};  // B-operand buffers, NPL planes each
   uint8_t* dSign = nullptr;             // readout sign plane
+  int8_t* dSignAll = nullptr;           // row shard readout: private byte plane of all spins'
+  size_t sign_all_bytes = 0;            // signs (peers never write it), [rpad][kpad]
+  CUtensorMap tmSignAll;
   unsigned long long* dE2 = nullptr;
   long long* dBest = nullptr;
   CUtensorMap tmG_sign[2], tmG_planes[2], tmSign;
@@ -281,6 +284,9 @@ int launch_multistep_pair(sbg_ctx* ctx, const TmaMaps& maps, MultiStepArgs a) {
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
   a.num_n = int32_t(ctx->rpad / NPAIR);
   if (NP != 1) a.ksplit = 1;
+  // every K part needs at least one K block: a part with an empty range would commit an
+  // accumulator no MMA wrote (the previous tile's field)
+  a.ksplit = std::min<int32_t>(a.ksplit, int32_t(a.kpad / (Cfg::BK * Cfg::KPB)));
   if (a.ksplit > 1) {
     const size_t need = size_t(a.ksplit - 1) * size_t(ctx->rpad) * size_t(ctx->npad);
     if (ctx->fpart_cap < need) {
@@ -424,11 +430,31 @@ int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int
     a.trace = trace;
     a.nsteps = std::min(a.nsteps, 4096);
   }
+  static unsigned long long* gtrace = nullptr;  // dev knob SBG_RES_GTRACE: per-(CTA, group) stamps
+  const size_t gtn = size_t(ctx->sms) * 64 * 8;
+  if (PARTS != 0 && dev_knob("SBG_RES_GTRACE")) {
+    if (!gtrace) CK(cudaMalloc(&gtrace, sizeof(unsigned long long) * gtn));
+    CK(cudaMemsetAsync(gtrace, 0, sizeof(unsigned long long) * gtn, ctx->stream));
+    a.gtrace = gtrace;
+  }
   // done counters per replica block (one per part)
   const int counters = PARTS != 0 ? PARTS : 1;
   CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * num_n * counters, ctx->stream));
   CK(launch_persistent(kern, 2 * num_mp * a.rb_per_group, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream, maps, a));
   ++ctx->launches;
+  if (a.gtrace) {
+    std::vector<unsigned long long> h(gtn);
+    CK(cudaMemcpyAsync(h.data(), a.gtrace, gtn * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    char name[128];
+    snprintf(name, sizeof name, "gpurun_out/res_gtrace_%d.txt", a.nsteps);
+    FILE* f = fopen(name, "w");
+    if (f) {
+      for (size_t i = 0; i < gtn; ++i)
+        if (h[i]) fprintf(f, "%zu %zu %zu %llu\n", i / 512, (i / 8) % 64, i % 8, h[i]);
+      fclose(f);
+    }
+  }
   if (a.trace) {
     std::vector<unsigned long long> h(size_t(16 * 2 * a.nsteps));
     CK(cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -455,6 +481,9 @@ void free_state(sbg_ctx* ctx) {
   cudaFree(ctx->dG[0]);
   cudaFree(ctx->dG[1]);
   cudaFree(ctx->dSign);
+  cudaFree(ctx->dSignAll);
+  ctx->dSignAll = nullptr;
+  ctx->sign_all_bytes = 0;
   cudaFree(ctx->dE2);
   cudaFree(ctx->dE2p);
   ctx->dE2p = nullptr;
@@ -500,7 +529,9 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
     CK(cudaMemsetAsync(ctx->dG[1], 0, NPL * gpl, ctx->stream));
     CK(cudaMemsetAsync(ctx->dSign, 0, pl, ctx->stream));
     if (ctx->kind == KIND_CSR_I8) {
-      ctx->rp = round_up(R, CSR_RCHUNK);
+      // sized by rpad (not R): a later R in the same PAD_R bucket reuses these buffers, so the
+      // leading dimension must cover every R that maps to this rpad
+      ctx->rp = round_up(rpad, CSR_RCHUNK);
       const size_t sm = size_t(ctx->npad) * ctx->rp;
       for (float** a : {&ctx->dXs, &ctx->dYs, &ctx->dPs}) {
         CK(cudaMalloc(a, sizeof(float) * sm));
@@ -2126,23 +2157,34 @@ int sbg_readout_partial(sbg_ctx* ctx, int64_t* e2) {
   if (!ctx->sharded || !ctx->dX || (ctx->g_mode != 1 && ctx->g_mode != 2))
     return ctx->fail(SBG_ERR_STATE, "sign-variant row shard required");
   CK(cudaSetDevice(ctx->device));
-  int gb = ctx->g_cur;
+  const int8_t* plane = reinterpret_cast<const int8_t*>(ctx->dG[ctx->g_cur]);
+  const CUtensorMap* pmap = &ctx->tmG_sign[ctx->g_cur];
   if (ctx->g_mode == 2) {
-    // packed e2m1 signs of all spins -> a byte-per-spin plane in the other G buffer (the next
-    // step's output buffer, rewritten in full by every rank's next step)
-    gb ^= 1;
+    // packed e2m1 signs of all spins -> a byte-per-spin plane in a private buffer. Not the other
+    // G buffer: peers already on their next step push their slabs of G_{t+1} into it over
+    // NVLink with no cross-rank sync against this readout.
+    if (!ctx->dSignAll || ctx->sign_all_bytes != size_t(ctx->rpad) * ctx->kpad) {
+      cudaFree(ctx->dSignAll);
+      ctx->dSignAll = nullptr;
+      ctx->sign_all_bytes = size_t(ctx->rpad) * ctx->kpad;
+      CK(cudaMalloc(&ctx->dSignAll, ctx->sign_all_bytes));
+      int rc = encode_2d_u8(ctx, &ctx->tmSignAll, ctx->dSignAll, ctx->kpad, ctx->rpad, 128, BN_SIGN);
+      if (rc) return rc;
+    }
     const size_t tot = size_t(ctx->rpad) * ctx->kpad;
-    unpack_sign4_kernel<<<grid_for(ctx, tot, 256), 256, 0, ctx->stream>>>(
-        ctx->dG[ctx->g_cur], reinterpret_cast<int8_t*>(ctx->dG[gb]), ctx->kpad, int32_t(ctx->rpad));
+    unpack_sign4_kernel<<<grid_for(ctx, tot, 256), 256, 0, ctx->stream>>>(ctx->dG[ctx->g_cur], ctx->dSignAll,
+                                                                         ctx->kpad, int32_t(ctx->rpad));
     CK(cudaGetLastError());
     ++ctx->launches;
+    plane = ctx->dSignAll;
+    pmap = &ctx->tmSignAll;
   }
   CK(cudaMemsetAsync(ctx->dE2, 0, sizeof(unsigned long long) * ctx->rpad, ctx->stream));
   StepArgs a = base_args(ctx, BN_SIGN, ctx->R, ctx->rpad);
-  a.sign_in = reinterpret_cast<const int8_t*>(ctx->dG[gb]) + ctx->row0;
+  a.sign_in = plane + ctx->row0;
   a.sign_ld = ctx->kpad;
   a.e2 = ctx->dE2;
-  int rc = launch_step<1, BN_SIGN, EpiMode::Readout>(ctx, ctx->tmG_sign[gb], a);
+  int rc = launch_step<1, BN_SIGN, EpiMode::Readout>(ctx, *pmap, a);
   if (rc) return rc;
   CK(cudaMemcpyAsync(e2, ctx->dE2, sizeof(long long) * ctx->R, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));

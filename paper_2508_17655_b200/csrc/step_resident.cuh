@@ -129,6 +129,7 @@ struct ResidentArgs {
                               // group 0, then one flag per later group (rb_per_group + g - 1)
   int32_t dbg;                // dev only: 1 = skip J loads after the first step, 2 = no G dependency wait
   unsigned long long* trace;  // dev only: per-step %globaltimer stamps of pair 0 (null = off)
+  unsigned long long* gtrace; // dev only: per-(CTA, group) stamps of the parts kernel [cta][64][8]
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {

@@ -116,6 +116,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
   uint8_t* g_tile = smem + (t_base - base);
   uint64_t* bars = reinterpret_cast<uint64_t*>(g_tile + Cfg::T_BYTES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
+  // groups whose state the epilogue has loaded (paces the G_0 helper, warp 2)
+  volatile int32_t* started = reinterpret_cast<volatile int32_t*>(tmem_slot + 1);
   auto bar = [&](int i) { return ptx::smem_u32(bars + i); };
   auto full_bar = [&](int s) { return bar(s); };
   auto empty_bar = [&](int s) { return bar(STAGES + s); };
@@ -133,6 +135,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
   // [s][part][k], k = 0 G dependency met, 6 first MMA round's stages landed, 7 all stages landed,
   // 1 accumulator ready (epilogue), 2 epilogue done, 3 publisher has the tile, 4 store complete,
   // 5 released, 8 producer issued all G loads, 9 MMAs issued
+  // dev group trace (SBG_RES_GTRACE): k 0 group top, 1 state loaded, 2 step 0 part 0 acc ready,
+  // 3 step 1 part 0 acc ready, 4 last step done, 5 write-back done, 6 helper published G_0
+  auto gstamp = [&](int g, int k) {
+    if (args.gtrace && g - args.group0 < 64)
+      args.gtrace[(static_cast<size_t>(blockIdx.x) * 64 + (g - args.group0)) * 8 + k] = gtimer();
+  };
   auto stamp = [&](int g, int s, int i, int k) {
     if (args.trace && g == args.group0 && s >= 0 && i < 2 && cr == 0 && (blockIdx.x >> 1) == 0)
       args.trace[(s * 2 + i) * 16 + k] = gtimer();
@@ -151,6 +159,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
     }
     ptx::mbar_init(jfull_bar, 2);
     ptx::fence_mbar_init();
+    *started = 0;
   }
   if (warp == 2) {
     ptx::tmem_alloc_pair(ptx::smem_u32(tmem_slot), 512);
@@ -347,6 +356,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
         }
       }
     }
+  } else if (warp == 2) {  // ------------------------------------------ G_0 helper
+    // Group transitions off the critical path: while group g - 1 steps, publish group g's
+    // G_0 = sgn(x_0) straight from global x (so its first MMAs can run while the epilogue is
+    // still writing back g - 1 and loading g) and prefetch g's x, y, p rows into L2 (so that
+    // load hits L2). Same bytes as the epilogue's put_g2 + the publisher's TMA store: row r <
+    // R of the G buffer step 0 reads, bytes [i0 / 2, i0 / 2 + 64) clipped at (n + 1) / 2, two
+    // spins per byte (even spin in the low nibble), +1 = 0x2, -1 = 0xA (sgn(0) = +1).
+    const int64_t gpitch = args.npad / 2;
+    const int gvalid = (args.n + 1) / 2;
+    const int q = lane & 3;       // 32-spin chunk of this CTA's 128 spins
+    const int b0 = i0 / 2 + q * 16;  // its first G byte
+    for (int g = args.group0 + 1; g < args.group0 + args.groups; ++g) {
+      const int n_blk = g * args.rb_per_group + rbk;
+      if (n_blk >= num_n) break;
+      while (*started < g - args.group0) __nanosleep(256);  // group g - 1 under way here
+      if (args.ready)
+        while (dep::ld_acquire_sys(args.ready + args.rb_per_group + g - 1) == 0) __nanosleep(256);
+      static_for<0, PARTS>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        const int r0 = n_blk * Cfg::NR + Cfg::off(i);
+#pragma unroll 2
+        for (int rr = lane >> 2; rr < Cfg::w(i); rr += 8) {
+          const int r = r0 + rr;
+          if (r >= args.R) continue;
+          const float4* src = reinterpret_cast<const float4*>(args.x + static_cast<size_t>(r) * args.npad + i0 + q * 32);
+          float4 f[8];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) f[v] = src[v];
+          uint32_t w4[4];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            auto c = [](float xv) { return xv >= 0.0f ? 0x2u : 0xAu; };
+            const float4 a = f[2 * v], b = f[2 * v + 1];
+            w4[v] = c(a.x) | (c(a.y) << 4) | (c(a.z) << 8) | (c(a.w) << 12) | (c(b.x) << 16) | (c(b.y) << 20) |
+                    (c(b.z) << 24) | (c(b.w) << 28);
+          }
+          uint8_t* dst = args.gbuf[1] + static_cast<size_t>(r) * gpitch + b0;
+          if (b0 + 16 <= gvalid) {
+            asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(w4[0]), "r"(w4[1]), "r"(w4[2]),
+                         "r"(w4[3])
+                         : "memory");
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (b0 + j < gvalid) dst[j] = static_cast<uint8_t>(w4[j >> 2] >> (8 * (j & 3)));
+          }
+        }
+        // the consumers read G with TMA (async proxy) after acquiring the counter
+        dep::fence_proxy_async_global();
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) dep::release_add(args.done + PARTS * n_blk + i, 1u);
+      });
+      if (lane == 0) gstamp(g, 6);
+      // L2 prefetch of the block's state rows (x was just read) for the epilogue's load
+      for (int rr = lane; rr < Cfg::NR; rr += 32) {
+        const int r = n_blk * Cfg::NR + rr;
+        if (r >= args.rpad) break;
+        const size_t off = static_cast<size_t>(r) * args.npad + i0;
+        ptx::prefetch_l2_bulk(args.y + off, Cfg::BM * 4);
+        ptx::prefetch_l2_bulk(args.p + off, Cfg::BM * 4);
+        ptx::prefetch_l2_bulk(args.x + off, Cfg::BM * 4);
+      }
+    }
   } else if (warp == 3) {  // ------------------------------------------ G publishers
     // lane i publishes part i (its own bulk-async group, completion wait and release), so
     // the parts' store -> completion -> release latencies overlap instead of queueing
@@ -366,8 +439,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
       for (int g = args.group0; g < args.group0 + args.groups; ++g) {
         const int n_blk = g * args.rb_per_group + rbk;
         if (n_blk >= num_n) break;
-        // G_0 (written by the state load into the buffer Gout[.][1] writes), then G_{s+1}
-        for (int s = -1; s < args.nsteps; ++s, ++pc) {
+        // G_0 of the launch's first group (written by the state load into the buffer Gout[.][1]
+        // writes; later groups' G_0 comes from the helper, warp 2), then G_{s+1}
+        for (int s = g == args.group0 ? -1 : 0; s < args.nsteps; ++s, ++pc) {
           const int par = s < 0 ? 1 : (s & 1);
           ptx::mbar_wait(gfull_bar(lane), pc & 1);
           stamp(g, s, lane, 3);
@@ -411,11 +485,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
       if (args.ready)
         while (dep::ld_acquire_sys(args.ready + (g == 0 ? rbk : args.rb_per_group + g - 1)) == 0)
           __nanosleep(256);
-      // load the block's state (x, y to TMEM, p to registers) and write G_0 = sgn(x_0)
+      // load the block's state (x, y to TMEM, p to registers); for the launch's first group also
+      // write G_0 = sgn(x_0) (later groups: published ahead by the helper, warp 2)
+      const bool first = g == args.group0;
+      const bool gt = warp == 4 && lane == 0;
+      if (gt) gstamp(g, 0);
+      // x, y to TMEM, p to registers, one 4-column chunk at a time
       static_for<0, PARTS>([&](auto I) {
         constexpr int i = decltype(I)::value;
-        ptx::mbar_wait(gempty_bar(i), (pc & 1) ^ 1u);
-        static_for<0, Cfg::w(i) / 16>([&](auto C) {
+        constexpr int CHUNKS = Cfg::w(i) / 16;
+        if (first) ptx::mbar_wait(gempty_bar(i), (pc & 1) ^ 1u);
+        static_for<0, CHUNKS>([&](auto C) {
           constexpr int c = decltype(C)::value;
           const int col = Cfg::off(i) + cg * (Cfg::w(i) / 4) + c * CH;
           uint32_t vx[4], vy[4];
@@ -430,13 +510,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
           }
           ptx::tmem_st<4>(t_lane + Cfg::COL_X + col, vx);
           ptx::tmem_st<4>(t_lane + Cfg::COL_Y + col, vy);
-          put_g2(col, __uint_as_float(vx[0]), __uint_as_float(vx[1]));
-          put_g2(col + 2, __uint_as_float(vx[2]), __uint_as_float(vx[3]));
+          if (first) {
+            put_g2(col, __uint_as_float(vx[0]), __uint_as_float(vx[1]));
+            put_g2(col + 2, __uint_as_float(vx[2]), __uint_as_float(vx[3]));
+          }
         });
       });
       ptx::tmem_st_wait();
-      static_for<0, PARTS>([&](auto I) { tile_written(decltype(I)::value); });
-      ++pc;
+      if (first) {
+        static_for<0, PARTS>([&](auto I) { tile_written(decltype(I)::value); });
+        ++pc;
+      }
+      if (gt) {
+        *started = g - args.group0 + 1;
+        gstamp(g, 1);
+      }
       for (int s = 0; s < args.nsteps; ++s, ++lt, ++pc) {
         PhaseConsts k = args.k;
         k.inv = __frcp_rn(static_cast<float>(args.M - (args.t_begin + static_cast<uint64_t>(s))));
@@ -469,6 +557,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
           ptx::tc_fence_after();
           const bool tr = warp == 4 && lane == 0;
           if (tr) stamp(g, s, i, 1);
+          if (tr && i == 0 && s < 2) gstamp(g, 2 + s);
           ptx::mbar_wait(gempty_bar(i), (pc & 1) ^ 1u);  // this part's G tile stored
           if (tr) stamp(g, s, i, 10);
           ptx::tmem_ld<CH>(t_lane + c0, bf[0]);
@@ -518,7 +607,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
         });
       }
       // write the block's state back (after the last step's TMEM stores)
+      if (gt) gstamp(g, 4);
       ptx::tmem_st_wait();
+      const uint64_t wb_policy = ptx::policy_evict_first();  // written once, read by a later launch
       static_for<0, PARTS>([&](auto I) {
         constexpr int i = decltype(I)::value;
         static_for<0, Cfg::w(i) / 16>([&](auto C) {
@@ -533,12 +624,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
             const int r = n_blk * Cfg::NR + col + j;
             if (r >= args.rpad) continue;
             const size_t off = static_cast<size_t>(r) * args.npad + spin;
-            args.x[off] = __uint_as_float(vx[j]);
-            args.y[off] = __uint_as_float(vy[j]);
-            args.p[off] = preg[Cfg::off(i) / 4 + c * CH + j];
+            ptx::st_hint(args.x + off, vx[j], wb_policy);
+            ptx::st_hint(args.y + off, vy[j], wb_policy);
+            ptx::st_hint(args.p + off, __float_as_uint(preg[Cfg::off(i) / 4 + c * CH + j]), wb_policy);
           }
         });
       });
+      if (gt) gstamp(g, 5);
     }
   }
 

@@ -144,10 +144,14 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 __device__ __forceinline__ void release_add_sys(uint32_t* p, uint32_t v) {
   asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-// Sharded variant: counters are incremented by peer GPUs over NVLink (sys scope).
+// Sharded variant: counters are incremented by peer GPUs over NVLink (sys scope) and run on
+// across launches (base = the count every rank's previous launches reach). No need == 0
+// shortcut: step 0 of a later launch must still see every peer's final step of the previous
+// one (done >= base), so that it neither reads a stale slab nor overwrites a G buffer a slower
+// peer is still reading. Signed, wrap-safe compare.
 __device__ __forceinline__ void wait_block_sys(const uint32_t* done, int n, uint32_t base, uint32_t need) {
-  if (need == 0) return;
-  while (ld_acquire_sys(done + n) - base < need) __nanosleep(64);
+  const uint32_t target = base + need;
+  while (static_cast<int32_t>(ld_acquire_sys(done + n) - target) < 0) __nanosleep(64);
   fence_proxy_async_global();
 }
 }  // namespace dep

@@ -1,0 +1,2 @@
+SBG_RES_TRACE=1 timeout 300 python tools/step_driver.py --steps 60 > gpurun_out/r2c4.log 2>&1 || true
+cat gpurun_out/r2c4.log
