@@ -136,6 +136,7 @@ struct sbg_ctx {
   uint32_t done_base = 0;  // done[] counters run on across launches (peers increment them)
   std::vector<uint8_t*> peer_g0, peer_g1;
   std::vector<uint32_t*> peer_done;
+  uint32_t* d_err = nullptr;  // row shards: peer-wait timeout flag (MultiStepArgs::err)
   float* d_fpart = nullptr;  // K-split partial fields (pair kernel), fpart_cap floats
   size_t fpart_cap = 0;
   uint32_t* d_kdone = nullptr;
@@ -176,6 +177,17 @@ int64_t gdim(const sbg_ctx* ctx) { return ctx->sharded ? ctx->kpad : ctx->npad; 
 
 #define CHECK_CTX(ctx) \
   if (!(ctx)) return SBG_ERR_INVALID_ARGUMENT
+
+// Row shards: a peer wait that timed out on the device (MultiStepArgs::err) is an error.
+static int shard_wait_check(sbg_ctx* ctx) {
+  if (!ctx->sharded || !ctx->d_err) return SBG_OK;
+  uint32_t e = 0;
+  CK(cudaMemcpy(&e, ctx->d_err, sizeof e, cudaMemcpyDeviceToHost));
+  if (e) return ctx->fail(SBG_ERR_CUDA, "row shard: a peer rank did not release its slab within 4 s "
+                                        "(peer died, not launched, or not wired); results are invalid");
+  return SBG_OK;
+}
+
 
 namespace {
 
@@ -984,6 +996,7 @@ void sbg_destroy(sbg_ctx* ctx) {
   cudaFree(ctx->d_ready);
   cudaFree(ctx->d_fpart);
   cudaFree(ctx->d_kdone);
+  cudaFree(ctx->d_err);
   cudaFree(ctx->dJ);
   cudaFree(ctx->dJ4);
   ctx->dJ4 = nullptr;
@@ -1500,6 +1513,7 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
       a.done_base = ctx->sharded ? ctx->done_base : 0;
       a.g_ld = (ctx->sharded ? ctx->kpad : ctx->npad) / (q4s ? 2 : 1);  // bytes per G row
       a.npeers = ctx->sharded ? int32_t(ctx->peer_done.size()) : 0;
+      a.err = ctx->d_err;
       for (int pr = 0; pr < a.npeers; ++pr) {
         // step parity 0 writes buffer cur^1, parity 1 buffer cur (as the local Gout maps)
         a.peer_g[0][pr] = cur == 0 ? ctx->peer_g1[size_t(pr)] : ctx->peer_g0[size_t(pr)];
@@ -2078,6 +2092,8 @@ int sbg_shard_set_peers(sbg_ctx* ctx, int32_t npeers, void* const* g0, void* con
     ctx->peer_done[size_t(i)] = static_cast<uint32_t*>(done[i]);
   }
   CK(cudaSetDevice(ctx->device));
+  if (!ctx->d_err) CK(cudaMalloc(&ctx->d_err, sizeof(uint32_t)));
+  CK(cudaMemsetAsync(ctx->d_err, 0, sizeof(uint32_t), ctx->stream));
   CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * (ctx->rpad / 16 + 1), ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->done_base = 0;
@@ -2188,7 +2204,7 @@ int sbg_readout_partial(sbg_ctx* ctx, int64_t* e2) {
   if (rc) return rc;
   CK(cudaMemcpyAsync(e2, ctx->dE2, sizeof(long long) * ctx->R, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  return SBG_OK;
+  return shard_wait_check(ctx);
 }
 
 // Per-replica control strength A (a_rep[r] for replica r of the current state,
@@ -2216,7 +2232,7 @@ int sbg_synchronize(sbg_ctx* ctx) {
   CHECK_CTX(ctx);
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->stream));
-  return SBG_OK;
+  return shard_wait_check(ctx);
 }
 
 int sbg_state_device(sbg_ctx* ctx, float** x, float** y, float** p, int64_t* ld, int64_t* rpad) {

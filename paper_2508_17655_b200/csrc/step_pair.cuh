@@ -170,7 +170,7 @@ __global__ void __cluster_dims__(2, 1, 1)
   auto wait_dep = [&](int n_blk, int s) {
     const uint32_t need = static_cast<uint32_t>(s * args.num_m_total);
     if (sharded)
-      dep::wait_block_sys(args.done, n_blk, args.done_base, need);
+      dep::wait_block_sys(args.done, n_blk, args.done_base, need, args.err);
     else
       dep::wait_block(args.done, n_blk, args.done_base, need);
   };

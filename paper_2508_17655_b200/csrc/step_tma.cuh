@@ -100,6 +100,8 @@ struct MultiStepArgs {
   int32_t col0;          // this rank's first spin (column offset of its slab of G)
   uint32_t done_base;    // done[] value at launch (counters run on across launches)
   int32_t npeers;        // other ranks that receive this rank's G slab
+  uint32_t* err;         // row shards: set to 1 when a peer wait times out (the launch then
+                         // finishes with garbage instead of hanging; the host reports it)
   int64_t g_ld;          // row pitch (bytes) of the G buffers
   uint8_t* peer_g[2][7]; // peers' G buffers for step parity 0/1 (NVLink peer / IPC pointers)
   uint32_t* peer_done[7];
@@ -149,9 +151,27 @@ __device__ __forceinline__ void release_add_sys(uint32_t* p, uint32_t v) {
 // shortcut: step 0 of a later launch must still see every peer's final step of the previous
 // one (done >= base), so that it neither reads a stale slab nor overwrites a G buffer a slower
 // peer is still reading. Signed, wrap-safe compare.
-__device__ __forceinline__ void wait_block_sys(const uint32_t* done, int n, uint32_t base, uint32_t need) {
+// A wait longer than SHARD_WAIT_NS (a peer rank died or was never launched) sets *err and
+// gives up; every other waiter then gives up at once.
+constexpr uint64_t SHARD_WAIT_NS = 4000000000ull;
+__device__ __forceinline__ uint64_t now_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void wait_block_sys(const uint32_t* done, int n, uint32_t base, uint32_t need,
+                                               uint32_t* err) {
   const uint32_t target = base + need;
-  while (static_cast<int32_t>(ld_acquire_sys(done + n) - target) < 0) __nanosleep(64);
+  if (static_cast<int32_t>(ld_acquire_sys(done + n) - target) < 0) {
+    const uint64_t t0 = now_ns();
+    while (static_cast<int32_t>(ld_acquire_sys(done + n) - target) < 0) {
+      __nanosleep(64);
+      if (err && (*reinterpret_cast<volatile uint32_t*>(err) != 0 || now_ns() - t0 > SHARD_WAIT_NS)) {
+        atomicExch(err, 1u);
+        break;
+      }
+    }
+  }
   fence_proxy_async_global();
 }
 }  // namespace dep
@@ -221,7 +241,7 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
   auto wait_dep = [&](int n_blk, int s) {
     const uint32_t need = static_cast<uint32_t>(s * args.num_m_total);
     if (sharded)
-      dep::wait_block_sys(args.done, n_blk, args.done_base, need);
+      dep::wait_block_sys(args.done, n_blk, args.done_base, need, args.err);
     else
       dep::wait_block(args.done, n_blk, args.done_base, need);
   };

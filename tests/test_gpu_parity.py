@@ -326,6 +326,54 @@ def test_sweep_grid_matches_mirror_per_cell(solver, orc):
         assert cl.best_energy == cl.energies.min()
 
 
+def test_dt_sweep_grid_matches_mirror_per_cell(solver, orc):
+    """dt_sweep (bench.cpp:206-269) on the GPU: cell (di, ti) runs at dt = tune_dt(lambda_min,
+    lambda_max, D_t) (spectral.cpp:277-286) and M = llround(t_M / dt), replicas seeded
+    derive_seed(seed, {dt_sweep, di, ti, r}) with the reference init; every cell's energies
+    bitwise vs the fp32 mirror run with the same dt, M and seeds."""
+    from paper_2508_17655_b200 import SolverConfig, TuningResult, Variant
+    from paper_2508_17655_b200.solver import SEED_STREAM_DT_SWEEP, _derive_seed, dt_sweep, tune_dt
+
+    n, reps = 64, 5
+    J = orc.gen_dense_i8(n, 19)
+    solver.set_instance(J)
+    lmin, lmax = -14.2, 15.1
+    t = TuningResult(c=1 / (2 * np.sqrt(n)), dt=1.0, lambda_min=lmin, lambda_max=lmax)
+    base = SolverConfig(variant=Variant.gbsb, seed=77)
+    d_ts, t_fs = [0.8, 1.25], [40.0, 101.5]
+    cells = dt_sweep(solver, d_ts, t_fs, 0.2, reps, base, t, target=-1e9)
+    assert [(cl.di, cl.ti) for cl in cells] == [(di, ti) for di in range(2) for ti in range(2)]
+    for cl in cells:
+        dt = tune_dt(lmin, lmax, d_ts[cl.di])
+        assert cl.dt == dt
+        q = t_fs[cl.ti] / dt
+        assert cl.m_steps == int(np.floor(q + 0.5))
+        seeds = [_derive_seed(77, [SEED_STREAM_DT_SWEEP, cl.di, cl.ti, r]) for r in range(reps)]
+        x, y, p = orc.init_reference_seeds(n, seeds)
+        x, y, p = orc.step_f32(2, J, x, y, p, 0, cl.m_steps, np.float32(dt), np.float32(t.c), np.float32(0.2),
+                               cl.m_steps)
+        assert (cl.energies == -0.5 * orc.energy2_i8(J, x)).all(), (cl.di, cl.ti)
+
+
+def test_csr_solver_reused_across_replica_counts(solver, orc):
+    """One CSR context run with R = 1, then R = 200 (same 256-replica padding bucket), then
+    R = 300: every run bitwise equal to the fp32 mirror (the spin-major working buffers
+    are sized for the bucket, not for the first R)."""
+    n, m = 1500, 6000
+    _, csr = orc.gen_er_csr(n, m, 5)
+    c, dt = np.float32(0.2), np.float32(1.25)
+    solver.set_instance_csr(n, *csr)
+    for R in (1, 200, 300, 17):
+        x0, y0, p0 = orc.init_small_uniform(n, R, master=R)
+        solver.set_state(x0, y0, p0)
+        solver.advance(cfg_for(GBSB, 50, float(dt), float(c), 0.2), 0, 9)
+        x, y, p = solver.get_state()
+        mx, my, mp = orc.step_f32_csr(GBSB, n, csr, x0, y0, p0, 0, 50, dt, c, np.float32(0.2), 9)
+        assert (x == mx).all() and (y == my).all() and (p == mp).all(), R
+        _, e, _, _ = solver.readout()
+        assert (e == -0.5 * orc.energy2_csr(n, csr, mx)).all(), R
+
+
 def test_trajectory_sampling_records_start_strides_final(solver, orc):
     """test_engine.cpp:232-249 analogue: stride 50 over M=120 -> m = 0, 50, 100, 120, bitwise states."""
     from paper_2508_17655_b200 import SolverConfig, TuningResult, Variant

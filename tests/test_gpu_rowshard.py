@@ -32,7 +32,10 @@ def test_two_shards_lockstep_equal_unsharded(orc, shard_kernel, n, R, steps, wor
     with Solver(0) as full:
         full.set_instance(J)
         full.init_state(R, InitMode.small_uniform, 3, 7)
-        full.advance(cfg, 0, steps)
+        mid = steps // 2
+        full.advance(cfg, 0, mid)
+        _, fe_mid, _, _ = full.readout()
+        full.advance(cfg, mid, steps)
         fx, fy, fp = full.get_state()
         _, fe, _, _ = full.readout()
     shards = [Solver(0) for _ in range(world)]
@@ -55,6 +58,8 @@ def test_two_shards_lockstep_equal_unsharded(orc, shard_kernel, n, R, steps, wor
                 s.advance(cfg, m, m + 1)
             for s in shards:
                 s.synchronize()
+            if m + 1 == mid:  # mid-run readout between two steps (private unpack buffer)
+                assert (row_sharded_energies([s.readout_partial() for s in shards]) == fe_mid).all()
         parts = []
         for k, s in enumerate(shards):
             row0, valid, _ = row_shard(n, world, k)
