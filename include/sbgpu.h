@@ -169,6 +169,12 @@ int sbg_fields_fixed(sbg_ctx* ctx, int64_t R, const float* x, float* F);
  * H2D, M steps, readout, D2H, all inside the call. Outputs may be NULL. */
 int sbg_run(sbg_ctx* ctx, const sbg_params* params, int64_t R, const float* x0, const float* y0,
             float* x_final, int8_t* spins, double* energy, int64_t* best_index, sbg_timing* timing);
+/* batch_best_of's result (bench.cpp:70-92) from host initial states: sbg_run, then only the
+ * winner crosses to the host -- its n spins (best_spins), energy and index (ties to the
+ * lowest replica) -- plus, if non-NULL, the R energies. */
+int sbg_run_best(sbg_ctx* ctx, const sbg_params* params, int64_t R, const float* x0, const float* y0,
+                 int8_t* best_spins, double* best_energy, int64_t* best_index, double* energies,
+                 sbg_timing* timing);
 /* Same with device-generated initial states (sbg_init_state). */
 int sbg_run_seeded(sbg_ctx* ctx, const sbg_params* params, int64_t R, int32_t init_mode,
                    uint64_t master, uint64_t tag, int64_t replica_offset, int8_t* spins,

@@ -25,7 +25,7 @@ EXPORTS = [
     "sbg_set_couplings_dense_i8", "sbg_set_couplings_dense_f64", "sbg_set_couplings_dense_f32",
     "sbg_coupling_scale_exp", "sbg_gen_couplings_dense_pm1",
     "sbg_set_couplings_csr_i8", "sbg_n", "sbg_set_state", "sbg_init_state", "sbg_get_state", "sbg_advance",
-    "sbg_readout", "sbg_readout_best", "sbg_fields_sign", "sbg_fields_fixed", "sbg_run", "sbg_run_seeded", "sbg_synchronize",
+    "sbg_readout", "sbg_readout_best", "sbg_fields_sign", "sbg_fields_fixed", "sbg_run", "sbg_run_best", "sbg_run_seeded", "sbg_synchronize",
     "sbg_kernel_launches", "sbg_state_device", "sbg_last_advance_ms", "sbg_success_tts", "sbg_tune_wigner_f64",
     "sbg_set_couplings_rows_i8", "sbg_shard_info", "sbg_shard_buffers", "sbg_shard_set_peers", "sbg_shard_prepare",
     "sbg_shard_push_slab", "sbg_shard_ipc_export", "sbg_shard_ipc_open", "sbg_readout_partial",
@@ -103,6 +103,7 @@ def lib() -> C.CDLL:
     L.sbg_fields_sign.argtypes = [P, i64, P, P]
     L.sbg_fields_fixed.argtypes = [P, i64, P, P]
     L.sbg_run.argtypes = [P, C.POINTER(Params), i64, P, P, P, P, P, P, C.POINTER(Timing)]
+    L.sbg_run_best.argtypes = [P, C.POINTER(Params), i64, P, P, P, P, P, P, C.POINTER(Timing)]
     L.sbg_run_seeded.argtypes = [P, C.POINTER(Params), i64, i32, u64, u64, i64, P, P, P, C.POINTER(Timing)]
     L.sbg_synchronize.argtypes = [P]
     L.sbg_kernel_launches.restype = i64

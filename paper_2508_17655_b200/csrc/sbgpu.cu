@@ -152,6 +152,8 @@ struct sbg_ctx {
   cudaStream_t cstream = nullptr;  // host->device copies overlapped with the resident kernel (sbg_run)
   cudaEvent_t evc[3];
   float last_advance_ms = 0.f;
+  int8_t* tail_best_spins = nullptr;  // sbg_run_best: winner-only readout in run_tail
+  double* tail_best_energy = nullptr;
 
   int fail(int code, const char* fmt, ...) {
     char buf[512];
@@ -1789,7 +1791,7 @@ static int run_tail(sbg_ctx* ctx, const sbg_params* prm, float* x_final, int8_t*
   }
   CK(cudaEventRecord(ctx->ev[4], ctx->stream));
   rc = spins ? sbg_readout(ctx, spins, energy, best_index, nullptr)
-             : sbg_readout_best(ctx, nullptr, nullptr, best_index, energy);
+             : sbg_readout_best(ctx, ctx->tail_best_spins, ctx->tail_best_energy, best_index, energy);
   if (rc) return rc;
   CK(cudaEventRecord(ctx->ev[5], ctx->stream));
   if (x_final) {
@@ -1975,6 +1977,20 @@ int sbg_run(sbg_ctx* ctx, const sbg_params* prm, int64_t R, const float* x0, con
   if (rc) return rc;
   CK(cudaEventRecord(ctx->ev[7], ctx->stream));
   return run_tail(ctx, prm, x_final, spins, energy, best_index, timing);
+}
+
+int sbg_run_best(sbg_ctx* ctx, const sbg_params* prm, int64_t R, const float* x0, const float* y0,
+                 int8_t* best_spins, double* best_energy, int64_t* best_index, double* energies,
+                 sbg_timing* timing) {
+  CHECK_CTX(ctx);
+  if (!best_spins || !best_energy || !best_index)
+    return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "sbg_run_best needs best_spins, best_energy and best_index");
+  ctx->tail_best_spins = best_spins;
+  ctx->tail_best_energy = best_energy;
+  const int rc = sbg_run(ctx, prm, R, x0, y0, nullptr, nullptr, energies, best_index, timing);
+  ctx->tail_best_spins = nullptr;
+  ctx->tail_best_energy = nullptr;
+  return rc;
 }
 
 int sbg_run_seeded(sbg_ctx* ctx, const sbg_params* prm, int64_t R, int32_t init_mode, uint64_t master,

@@ -490,6 +490,27 @@ class Solver:
             cuts = ((self.total_weight - energy) / 2).astype(np.int64)
         return BatchResult(spins, energy, cuts, int(best.value), timing.as_dict(), x_final, rcfg, tuning)
 
+    def run_best(self, cfg: SolverConfig, tuning: TuningResult, x0: np.ndarray, y0: Optional[np.ndarray] = None,
+                 want_energies: bool = True):
+        """batch_best_of's result (bench.cpp:70-92) for R = len(x0) replicas from host initial
+        states in one call (sbg_run_best): H2D, M steps, readout, and D2H of only the winner's
+        spins, energy and index (+ the R energies if want_energies).
+        Returns (best_spins, best_energy, best_index, energies | None, timing dict)."""
+        rcfg = resolve_config(cfg, tuning)
+        prm = self.params(rcfg)
+        x0 = np.ascontiguousarray(x0, np.float32)
+        y0 = np.ascontiguousarray(y0 if y0 is not None else np.zeros_like(x0), np.float32)
+        R = x0.shape[0]
+        spins = np.empty(self.n, np.int8)
+        be = C.c_double()
+        bi = C.c_int64()
+        energies = np.empty(R, np.float64) if want_energies else None
+        timing = _lib.Timing()
+        self._check(self._L.sbg_run_best(self._h, C.byref(prm), R, ptr(x0), ptr(y0), ptr(spins), C.byref(be),
+                                         C.byref(bi), ptr(energies), C.byref(timing)))
+        self.R = R
+        return spins, float(be.value), int(bi.value), energies, timing.as_dict()
+
     def _run_batch_sampled(self, rcfg, tuning, R, x0, y0, master_seed, tag, replica_offset, want_spins):
         """run() with sample_stride (engine.cpp:117-133): x recorded at m = 0, every
         stride steps and at the final step; trajectory[k] = (m, x of all replicas)."""
