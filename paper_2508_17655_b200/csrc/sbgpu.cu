@@ -30,6 +30,7 @@
 #include "step_pair.cuh"
 #include "step_resident.cuh"
 #include "step_resident_parts.cuh"
+#include "step_resident_ts.cuh"
 
 using namespace sbg;
 
@@ -402,10 +403,14 @@ int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int
                     const uint32_t* ready = nullptr) {
   // PARTS > 0: step_resident_parts.cuh (e2m1, 160-replica blocks as PARTS interleaved column
   // parts; JRES = J resident in shared memory); else step_resident.cuh
-  using Cfg = std::conditional_t<PARTS != 0, PartsCfg<ST, JRES, (PARTS > 0 ? PARTS : 2)>,
-                                 ResCfg<ST, EPI, CH, NR, false, Q4>>;
+  // PARTS < 0: step_resident_ts.cuh with -PARTS parts (J in TMEM, x, y in shared memory)
+  using Cfg = std::conditional_t<
+      (PARTS < 0), TsCfg<ST, (PARTS < 0 ? -PARTS : 2)>,
+      std::conditional_t<(PARTS > 0), PartsCfg<ST, JRES, (PARTS > 0 ? PARTS : 2)>, ResCfg<ST, EPI, CH, NR, false, Q4>>>;
   auto kern = [] {
-    if constexpr (PARTS != 0)
+    if constexpr (PARTS < 0)
+      return gsb_resident_ts_kernel<ST, -PARTS>;
+    else if constexpr (PARTS > 0)
       return gsb_resident_parts_kernel<ST, JRES, PARTS>;
     else
       return gsb_resident_pair_kernel<ST, EPI, CH, NR, Q4>;
@@ -437,6 +442,8 @@ int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int
   a.gbuf[0] = ctx->dG[ctx->g_cur ^ 1];  // step parity 0 writes the other buffer (as Gout[0])
   a.gbuf[1] = ctx->dG[ctx->g_cur];
   a.dbg = dev_knob("SBG_STEP_DBG");
+  a.j4 = ctx->dJ4;
+  a.j4_pitch = ctx->npad / 2;
   static unsigned long long* trace = nullptr;  // dev knob SBG_RES_TRACE: stamps of pair 0, group 0
   if (dev_knob("SBG_RES_TRACE")) {
     if (!trace) CK(cudaMalloc(&trace, sizeof(unsigned long long) * 16 * 2 * 4096));
@@ -446,13 +453,13 @@ int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int
   }
   static unsigned long long* gtrace = nullptr;  // dev knob SBG_RES_GTRACE: per-(CTA, group) stamps
   const size_t gtn = size_t(ctx->sms) * 64 * 8;
-  if (PARTS != 0 && dev_knob("SBG_RES_GTRACE")) {
+  if (PARTS != 0 && dev_knob("SBG_RES_GTRACE")) {  // parts and TS kernels
     if (!gtrace) CK(cudaMalloc(&gtrace, sizeof(unsigned long long) * gtn));
     CK(cudaMemsetAsync(gtrace, 0, sizeof(unsigned long long) * gtn, ctx->stream));
     a.gtrace = gtrace;
   }
   // done counters per replica block (one per part)
-  const int counters = PARTS != 0 ? PARTS : 1;
+  const int counters = PARTS != 0 ? (PARTS > 0 ? PARTS : -PARTS) : 1;
   CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * num_n * counters, ctx->stream));
   CK(launch_persistent(kern, 2 * num_mp * a.rb_per_group, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream, maps, a));
   ++ctx->launches;
@@ -1846,6 +1853,23 @@ static int encode_part_maps(sbg_ctx* ctx, PartMaps* pm, int cur, int w0, int w1)
 }
 
 extern "C++" {
+// The TS kernel (J in TMEM, x, y in shared memory): the parts kernel's G maps plus 2D boxes
+// {128 spins, 160 replicas} of the replica-major x and y (rows >= rpad read as zero).
+template <int PARTS, int ST>
+int launch_ts(sbg_ctx* ctx, int cur, const MultiStepArgs& a, int groups, const uint32_t* ready) {
+  using T = PartTable<PARTS>;
+  TsMaps tm;
+  int rc = encode_part_maps(ctx, &tm.g, cur, T::W[0], T::W[PARTS - 1]);
+  if (rc) return rc;
+  rc = encode_2d(ctx, &tm.X, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ctx->dX, uint64_t(ctx->npad), uint64_t(ctx->rpad),
+                 sizeof(float) * ctx->npad, 128, RES_NR, CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (!rc)
+    rc = encode_2d(ctx, &tm.Y, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ctx->dY, uint64_t(ctx->npad), uint64_t(ctx->rpad),
+                   sizeof(float) * ctx->npad, 128, RES_NR, CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (rc) return rc;
+  return launch_resident<16, 4, ST, RES_NR, true, -PARTS, true>(ctx, tm, a, 0, groups, ready);
+}
+
 template <int PARTS, int ST, bool JRES>
 int launch_parts(sbg_ctx* ctx, int cur, const MultiStepArgs& a, int groups, const uint32_t* ready) {
   using T = PartTable<PARTS>;
@@ -1868,6 +1892,13 @@ static int launch_resident_default(sbg_ctx* ctx, int cur, const MultiStepArgs& a
     // each part-step's G in one 3D TMA load; larger npad: 2 parts, J streamed.
     if (q4 && !getenv_is0("SBG_RES_SPLIT")) {
       if (ctx->npad > 2048) return launch_parts<2, 10, false>(ctx, cur, a, groups, ready);
+      // default: J in TMEM (TS MMAs at the N/2 floor), x, y in shared memory; SBG_RES_TS=0: the
+      // parts kernel (J in shared memory)
+      if (!getenv_is0("SBG_RES_TS")) {
+        // (wider parts' G super-stages do not fit beside x and y in shared memory)
+        if (dev_knob("SBG_RES_PARTS") == 5) return launch_ts<5, 3>(ctx, cur, a, groups, ready);
+        return launch_ts<4, 2>(ctx, cur, a, groups, ready);
+      }
       switch (dev_knob("SBG_RES_PARTS")) {
         case 2: return launch_parts<2, 2, true>(ctx, cur, a, groups, ready);
         case 3: return launch_parts<3, 2, true>(ctx, cur, a, groups, ready);

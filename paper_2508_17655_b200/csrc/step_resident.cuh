@@ -130,6 +130,8 @@ struct ResidentArgs {
   int32_t dbg;                // dev only: 1 = skip J loads after the first step, 2 = no G dependency wait
   unsigned long long* trace;  // dev only: per-step %globaltimer stamps of pair 0 (null = off)
   unsigned long long* gtrace; // dev only: per-(CTA, group) stamps of the parts kernel [cta][64][8]
+  const uint8_t* j4;          // TS kernel: packed e2m1 J [npad][npad / 2] (rows loaded into TMEM)
+  int64_t j4_pitch;           // its row pitch in bytes
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {

@@ -48,6 +48,10 @@ template <>
 struct PartTable<4> {
   static constexpr int W[4] = {48, 48, 32, 32};
 };
+template <>
+struct PartTable<5> {
+  static constexpr int W[5] = {32, 32, 32, 32, 32};
+};
 
 // Tensor maps of the parts kernel: G boxes depend on the part width (two width classes:
 // class 0 = W[0], class 1 = the narrower parts).
@@ -300,7 +304,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
               ptx::tc_fence_after();
               if (ptx::elect_one()) {
                 const uint32_t bb = b_base + stage * Cfg::STAGE_BYTES;
-                for (int kb = 0; kb < KB; ++kb) {
+                const int kb_end = args.dbg == 3 ? 2 : KB;  // dev timing probe: MMA cost off the chain
+                for (int kb = 0; kb < kb_end; ++kb) {
                   const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + kb * Cfg::A_BYTES);
                   const uint64_t bdesc = ptx::smem_desc_k_sw128(bb + kb * (Cfg::w(i) / 2) * Cfg::BK);
 #pragma unroll

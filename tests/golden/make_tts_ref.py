@@ -6,6 +6,7 @@ exists and `make -C oracle` has built oracle/_ref:
     python tests/golden/make_tts_ref.py gbsb      # ~2.5 h on 8 cores
     python tests/golden/make_tts_ref.py gdsb      # ~5 min  (M=1000)
     python tests/golden/make_tts_ref.py gdsb_long # ~2.5 h  (M=21500)
+    python tests/golden/make_tts_ref.py sk        # C4: SK N=4096 energy law, 256 trials
 
 Instance: gen_random_dense(2000, 1) (model.cpp:144-159), the seeded stand-in
 for K2000 (the G-set file is not in this container).
@@ -51,7 +52,28 @@ C = 1.0 / (2.0 * math.sqrt(N))
 JOBS = {"gbsb": (2, 21500), "gdsb": (3, 1000), "gdsb_long": (3, 21500)}
 
 
+def sk_job() -> None:
+    """C4 (BASELINE configs[3]) energy law: SK N=4096 (orc_gen_sk_f32(4096, 1), J ~ N(0, 1/N)
+    fp32 widened to fp64), GbSB, A=0.2, dt=1.25, c=0.5 (Wigner for sigma = 1/sqrt N), M=1000,
+    256 trials from the BASELINE init x0, y0 ~ U(-0.1, 0.1) of replicas r < 256
+    (derive_seed(1, {7, r}), the states the GPU test injects); every trial is the UNMODIFIED
+    reference step() (replica fan-out, ref_replica_fanout) and ising_energy (model.cpp:112-123)."""
+    R = oracle.ref("timing")
+    orc = oracle.orc()
+    n, trials, M = 4096, 256, 1000
+    J = orc.gen_sk_f32(n, 1).astype(np.float64)
+    x0, y0, _ = orc.init_small_uniform(n, trials, master=1, tag=7)
+    t0 = time.time()
+    e, wall = R.replica_fanout(2, J, x0, y0, M, DT, 0.5, A, 0)
+    print(f"sk: {trials} trials in {time.time() - t0:.0f} s", flush=True)
+    np.savez_compressed(os.path.join(HERE, "tts_ref_sk_n4096.npz"), energies=e, variant=np.int64(2), steps=np.int64(M),
+                        a=np.float64(A), dt=np.float64(DT), c=np.float64(0.5), n=np.int64(n), master=np.int64(1),
+                        tag=np.int64(7), source=np.array("oracle/_ref step() fan-out (ref_replica_fanout)"))
+
+
 def main(tag: str) -> None:
+    if tag == "sk":
+        return sk_job()
     variant, M = JOBS[tag]
     R = oracle.ref("timing")
     Rp = oracle.ref("parity")

@@ -495,6 +495,25 @@ def test_e2m1_resident_equals_int8(solver, n, R, variant, values, monkeypatch):
     _same(a, c)
 
 
+@pytest.mark.parametrize("n,R,variant,parts", [(2000, 8192, GDSB, "4"), (2000, 3000, DSB, "4"), (1500, 2000, GDSB, "5"),
+                                               (513, 6000, GDSB, "4"), (777, 400, DSB, "5")])
+def test_ts_kernel_equals_parts_kernel(solver, n, R, variant, parts, monkeypatch):
+    """The TS resident kernel (J in TMEM as the A operand of tcgen05.mma [a_tmem], x, y in
+    shared memory, state moved by TMA at group boundaries; the default) against the parts
+    kernel (J in shared memory, x, y in TMEM; SBG_RES_TS=0): states, energies and winner
+    bitwise equal, over several replica groups, odd n (half-filled last packed byte),
+    per-replica A, e2m1 J values beyond +-1."""
+    J = _sym(n, np.array([1, -1], np.int8) if n % 2 == 0 else E2M1_INTS, n)
+    arep = np.random.default_rng(n).random(R).astype(np.float32)
+    monkeypatch.setenv("SBG_RES_PARTS", parts)
+    f_ts, a = _run_resident(solver, J, R, variant, 23, monkeypatch, True, arep=arep)
+    monkeypatch.setenv("SBG_RES_TS", "0")
+    monkeypatch.setenv("SBG_RES_PARTS", "4")
+    f_pa, b = _run_resident(solver, J, R, variant, 23, monkeypatch, True, arep=arep)
+    assert f_ts == f_pa == "e2m1"
+    _same(a, b)
+
+
 def test_e2m1_streaming_large_n(solver, monkeypatch):
     """Past the resident kernel's size limit the streaming pair kernel runs on e2m1 operands
     (single-buffered accumulator, nibble-packed G written by the epilogue): bitwise equal to

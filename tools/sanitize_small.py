@@ -32,4 +32,37 @@ with Solver(0) as s:
     for v in (Variant.gdsb, Variant.gbsb):
         s.run_batch(SolverConfig(variant=v, steps=10, dt=1.25, c=0.5, a=0.2), TuningResult(c=0.5, dt=1.25), 40,
                     master_seed=2)
+    # resident parts kernel over several replica groups (helper-warp G_0 of later groups),
+    # sbg_run_best with pipelined host copies
+    s.gen_random_dense(300, 4)
+    cfg = SolverConfig(variant=Variant.gdsb, steps=6, dt=1.25, c=1 / (2 * math.sqrt(300)), a=0.2)
+    s.init_state(6200, InitMode.small_uniform, 1, 7)
+    s.advance(cfg, 0, 3)
+    s.readout_best()
+    x0, y0, _ = orc.init_small_uniform(300, 6200, master=3)
+    s.run_best(cfg, TuningResult(c=cfg.c, dt=1.25), x0, y0)
+# row shards in lockstep (2 shards on this GPU, one step per launch)
+from paper_2508_17655_b200.distributed import connect_row_shards_local  # noqa: E402
+
+shards = [Solver(0) for _ in range(2)]
+try:
+    for k, sh in enumerate(shards):
+        sh.gen_random_dense(700, 5, 2, k)
+        sh.init_state(40, InitMode.small_uniform, 1, 7)
+    connect_row_shards_local(shards)
+    for sh in shards:
+        sh.shard_prepare(Variant.gdsb)
+    for sh in shards:
+        sh.shard_push_slab()
+    cfg = SolverConfig(variant=Variant.gdsb, steps=10, dt=1.25, c=0.02, a=0.2)
+    for m in range(3):
+        for sh in shards:
+            sh.advance(cfg, m, m + 1)
+        for sh in shards:
+            sh.synchronize()
+    for sh in shards:
+        sh.readout_partial()
+finally:
+    for sh in shards:
+        sh.close()
 print("sanitize run ok")
