@@ -1,0 +1,7 @@
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "ts_kernel or resident or e2m1 or c2_shape or pipelined or p2" > gpurun_out/r2c15_tests.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/r2c15_tests.log
+timeout 300 python bench.py --steps 20 --warmup 5 --no-tts --no-cpu-baseline --no-configs > gpurun_out/r2c15_b20.log 2>&1
+timeout 300 python bench.py --steps 200 --warmup 5 --no-tts --no-cpu-baseline --no-configs > gpurun_out/r2c15_b200.log 2>&1
+grep -o '"ms_per_step": [0-9.e-]*' gpurun_out/r2c15_b*.log
+grep -o '"e2e": {"value": [0-9.e+]*' gpurun_out/r2c15_b*.log
+SBG_RES_TRACE=1 timeout 300 python tools/step_driver.py --steps 60 > gpurun_out/r2c15_t.log 2>&1
+SBG_RES_GTRACE=1 timeout 300 python tools/step_driver.py --steps 20 > gpurun_out/r2c15_g.log 2>&1
