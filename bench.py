@@ -93,9 +93,10 @@ def peaks():
 
 DTYPES = {"e2m1": "e2m1 operands (tcgen05 kind::mxf4, unit E8M0 scales, f32 acc: exact integer field) / f32 state",
           "int8": "i8 operands (tcgen05 kind::i8, s32 acc) / f32 state"}
-KERNELS = {"e2m1": "gsb_resident_parts_kernel<3,true,4> (four interleaved column-part chains per 160-replica block, "
-                   "J resident in shared memory, one 3D TMA load of G per part-step, p in registers, later groups' "
-                   "G_0 published ahead by a helper warp)",
+KERNELS = {"e2m1": "gsb_resident_ts_kernel<2,4> (four interleaved column-part chains per 160-replica block; J in TMEM "
+                   "as the A operand of TS-form kind::mxf4 MMAs; x, y in shared memory, moved by TMA at group "
+                   "boundaries; p in registers; one 3D TMA load of G per part-step; later groups' G_0 published "
+                   "ahead by a helper warp)",
            "int8": "gsb_resident_pair_kernel<5,16,4,160,false>"}
 
 
@@ -387,7 +388,7 @@ def run_ours(args):
                      "traffic_source": (tr["source"] + " (bytes per launch of the timed K steps)") if tr else None,
                      "peak_source": t_src,
                      "op_type": f"{fmt} tensor ops (2 per MAC), 2*N*N*R per step",
-                     "kernel": KERNELS[fmt] + "; all timed steps in one launch, x, y in TMEM",
+                     "kernel": KERNELS[fmt] + "; all timed steps in one launch",
                      "streaming_equivalent": {"bytes_per_step": stream_bytes,
                                               "gbs": stream_bytes / (ms_per_step / 1e3) / 1e9,
                                               "hbm_peak_gbs": hbm_peak, "hbm_peak_source": hbm_src,

@@ -452,7 +452,7 @@ int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int
     a.nsteps = std::min(a.nsteps, 4096);
   }
   static unsigned long long* gtrace = nullptr;  // dev knob SBG_RES_GTRACE: per-(CTA, group) stamps
-  const size_t gtn = size_t(ctx->sms) * 64 * 8;
+  const size_t gtn = size_t(ctx->sms) * 64 * 8 + size_t(ctx->sms) * 32;  // + the TS kernel's skew trace
   if (PARTS != 0 && dev_knob("SBG_RES_GTRACE")) {  // parts and TS kernels
     if (!gtrace) CK(cudaMalloc(&gtrace, sizeof(unsigned long long) * gtn));
     CK(cudaMemsetAsync(gtrace, 0, sizeof(unsigned long long) * gtn, ctx->stream));
@@ -471,9 +471,17 @@ int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int
     snprintf(name, sizeof name, "gpurun_out/res_gtrace_%d.txt", a.nsteps);
     FILE* f = fopen(name, "w");
     if (f) {
-      for (size_t i = 0; i < gtn; ++i)
+      const size_t grid = size_t(2 * (ctx->npad / 256) * a.rb_per_group);
+      for (size_t i = 0; i < size_t(ctx->sms) * 512; ++i)
         if (h[i]) fprintf(f, "%zu %zu %zu %llu\n", i / 512, (i / 8) % 64, i % 8, h[i]);
       fclose(f);
+      snprintf(name, sizeof name, "gpurun_out/res_skew_%d.txt", a.nsteps);
+      f = fopen(name, "w");
+      if (f) {
+        for (size_t i = 0; i < grid * 32; ++i)
+          if (h[grid * 512 + i]) fprintf(f, "%zu %zu %llu\n", i / 32, i % 32, h[grid * 512 + i]);
+        fclose(f);
+      }
     }
   }
   if (a.trace) {

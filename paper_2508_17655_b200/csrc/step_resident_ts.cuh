@@ -360,6 +360,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
             dep::fence_proxy_async_global();
             dep::release_add(args.done + PARTS * n_blk + k, 1u);
             stamp(g, s, k, 5);
+            // dev skew trace (SBG_RES_GTRACE): every CTA's release time of part 0, steps 8..39 of group 0
+            if (k == 0 && args.gtrace && g == args.group0 && s >= 8 && s < 40)
+              args.gtrace[size_t(gridDim.x) * 512 + size_t(blockIdx.x) * 32 + (s - 8)] = gtimer();
           });
         }
       }
