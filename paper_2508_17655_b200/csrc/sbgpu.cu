@@ -472,7 +472,7 @@ int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int
     FILE* f = fopen(name, "w");
     if (f) {
       const size_t grid = size_t(2 * (ctx->npad / 256) * a.rb_per_group);
-      for (size_t i = 0; i < size_t(ctx->sms) * 512; ++i)
+      for (size_t i = 0; i < grid * 512; ++i)
         if (h[i]) fprintf(f, "%zu %zu %zu %llu\n", i / 512, (i / 8) % 64, i % 8, h[i]);
       fclose(f);
       snprintf(name, sizeof name, "gpurun_out/res_skew_%d.txt", a.nsteps);
@@ -1869,12 +1869,16 @@ int launch_ts(sbg_ctx* ctx, int cur, const MultiStepArgs& a, int groups, const u
   TsMaps tm;
   int rc = encode_part_maps(ctx, &tm.g, cur, T::W[0], T::W[PARTS - 1]);
   if (rc) return rc;
-  rc = encode_2d(ctx, &tm.X, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ctx->dX, uint64_t(ctx->npad), uint64_t(ctx->rpad),
-                 sizeof(float) * ctx->npad, 128, RES_NR, CU_TENSOR_MAP_SWIZZLE_NONE);
-  if (!rc)
-    rc = encode_2d(ctx, &tm.Y, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ctx->dY, uint64_t(ctx->npad), uint64_t(ctx->rpad),
-                   sizeof(float) * ctx->npad, 128, RES_NR, CU_TENSOR_MAP_SWIZZLE_NONE);
+  const int ws[2] = {T::W[0], T::W[PARTS - 1]};
+  for (int c = 0; c < 2 && !rc; ++c) {
+    rc = encode_2d(ctx, &tm.X[c], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ctx->dX, uint64_t(ctx->npad),
+                   uint64_t(ctx->rpad), sizeof(float) * ctx->npad, 128, uint32_t(ws[c]), CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (!rc)
+      rc = encode_2d(ctx, &tm.Y[c], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ctx->dY, uint64_t(ctx->npad),
+                     uint64_t(ctx->rpad), sizeof(float) * ctx->npad, 128, uint32_t(ws[c]), CU_TENSOR_MAP_SWIZZLE_NONE);
+  }
   if (rc) return rc;
+  if (a.nsteps < 1) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "resident launch without steps");
   return launch_resident<16, 4, ST, RES_NR, true, -PARTS, true>(ctx, tm, a, 0, groups, ready);
 }
 

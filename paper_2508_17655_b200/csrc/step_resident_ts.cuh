@@ -57,7 +57,7 @@ __device__ __forceinline__ void sts_f32(uint32_t a, float v) {
 // Tensor maps of the TS kernel: the parts kernel's G maps plus the state boxes.
 struct TsMaps {
   PartMaps g;
-  CUtensorMap X, Y;  // f32 [rpad][npad], box {128 spins, 160 replicas}
+  CUtensorMap X[2], Y[2];  // f32 [rpad][npad], box {128 spins, part width} per width class
 };
 
 template <int STAGES_, int PARTS_>
@@ -79,7 +79,7 @@ struct TsCfg {
   static constexpr int XY_BYTES = NR * BM * 4;     // 80 KB each
   static constexpr int T_BYTES = NR * BM / 2;      // G tiles of all parts: [160][64] bytes
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
-  static constexpr int NUM_BARS = 2 * STAGES + 4 * PARTS + 1;
+  static constexpr int NUM_BARS = 2 * STAGES + 5 * PARTS;
   static constexpr int SMEM_BYTES = 2 * XY_BYTES + STAGES * STAGE_BYTES + T_BYTES + 1024 + 8 * NUM_BARS + 64;
   static constexpr uint32_t COL_J = NR, COL_SF = 512 - 16;
   static_assert(off(PARTS - 1) + w(PARTS - 1) == NR, "parts cover the block");
@@ -114,7 +114,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
   auto tempty_bar = [&](int i) { return bar(2 * STAGES + PARTS + i); };
   auto gfull_bar = [&](int i) { return bar(2 * STAGES + 2 * PARTS + i); };
   auto gempty_bar = [&](int i) { return bar(2 * STAGES + 3 * PARTS + i); };
-  const uint32_t sfull_bar = bar(2 * STAGES + 4 * PARTS);  // x, y of a group landed (TMA)
+  auto sfull_bar = [&](int i) { return bar(2 * STAGES + 4 * PARTS + i); };  // part i's x, y landed (TMA)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -141,7 +141,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
       ptx::mbar_init(gfull_bar(i), Cfg::EPI_WARPS);
       ptx::mbar_init(gempty_bar(i), 1);
     }
-    ptx::mbar_init(sfull_bar, 1);
+    for (int i = 0; i < PARTS; ++i) ptx::mbar_init(sfull_bar(i), 1);
     ptx::fence_mbar_init();
     *started = 0;
   }
@@ -338,10 +338,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
       ptx::prefetch_tmap(&maps.g.Gout[0][1]);
       ptx::prefetch_tmap(&maps.g.Gout[1][0]);
       ptx::prefetch_tmap(&maps.g.Gout[1][1]);
+      for (int c = 0; c < 2; ++c) {
+        ptx::prefetch_tmap(&maps.X[c]);
+        ptx::prefetch_tmap(&maps.Y[c]);
+      }
+      // x, y of a group's part k: one 2D TMA box each into shared memory (rows >= rpad
+      // zero-filled), completing on sfull(k); the epilogue waits for it before the part's step 0
+      auto load_state = [&](int g, int k_off, int k_cls, int k_w, int k) {
+        const int n_blk = g * args.rb_per_group + rbk;
+        if (args.ready)
+          while (dep::ld_acquire_sys(args.ready + (g == 0 ? rbk : args.rb_per_group + g - 1)) == 0)
+            __nanosleep(256);
+        const uint32_t so = static_cast<uint32_t>(k_off * Cfg::BM * 4);
+        ptx::mbar_arrive_expect_tx(sfull_bar(k), 2u * k_w * Cfg::BM * 4u);
+        ptx::tma_load_2d(x_base + so, &maps.X[k_cls], sfull_bar(k), i0, n_blk * Cfg::NR + k_off);
+        ptx::tma_load_2d(y_base + so, &maps.Y[k_cls], sfull_bar(k), i0, n_blk * Cfg::NR + k_off);
+      };
+      if (args.group0 * args.rb_per_group + rbk < num_n)
+        static_for<0, PARTS>([&](auto I) {
+          constexpr int k = decltype(I)::value;
+          load_state(args.group0, Cfg::off(k), Cfg::cls(k), Cfg::w(k), k);
+        });
       int pc = 0;
       for (int g = args.group0; g < args.group0 + args.groups; ++g) {
         const int n_blk = g * args.rb_per_group + rbk;
         if (n_blk >= num_n) break;
+        const bool next = g + 1 < args.group0 + args.groups && (g + 1) * args.rb_per_group + rbk < num_n;
         // G_0 of the launch's first group (the epilogue writes it at group start), then G_{s+1}
         for (int s = g == args.group0 ? -1 : 0; s < args.nsteps; ++s, ++pc) {
           const int par = s < 0 ? 1 : (s & 1);
@@ -351,8 +373,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
             stamp(g, s, k, 3);
             ptx::tma_store_2d(&maps.g.Gout[Cfg::cls(k)][par], t_base + Cfg::off(k) * (Cfg::BM / 2), i0 / 2,
                               n_blk * Cfg::NR + Cfg::off(k));
+            if (s == args.nsteps - 1) {
+              // the group's last step: part k's x, y go back to global memory now (the
+              // epilogue's smem writes were proxy-fenced before its gfull arrival), overlapping
+              // the other parts' last step; gempty(k) below then also frees them for the next
+              // group's loads
+              const uint32_t so = static_cast<uint32_t>(Cfg::off(k) * Cfg::BM * 4);
+              ptx::tma_store_2d(&maps.X[Cfg::cls(k)], x_base + so, i0, n_blk * Cfg::NR + Cfg::off(k));
+              ptx::tma_store_2d(&maps.Y[Cfg::cls(k)], y_base + so, i0, n_blk * Cfg::NR + Cfg::off(k));
+            }
             ptx::bulk_commit();
             ptx::bulk_wait_read0();
+            // the group's last step: part k's buffers are free, the next group's part k loads now
+            if (s == args.nsteps - 1 && next) load_state(g + 1, Cfg::off(k), Cfg::cls(k), Cfg::w(k), k);
             ptx::mbar_arrive(gempty_bar(k));  // tile reusable
             ptx::bulk_wait0();
             stamp(g, s, k, 4);
@@ -361,8 +394,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
             dep::release_add(args.done + PARTS * n_blk + k, 1u);
             stamp(g, s, k, 5);
             // dev skew trace (SBG_RES_GTRACE): every CTA's release time of part 0, steps 8..39 of group 0
-            if (k == 0 && args.gtrace && g == args.group0 && s >= 8 && s < 40)
-              args.gtrace[size_t(gridDim.x) * 512 + size_t(blockIdx.x) * 32 + (s - 8)] = gtimer();
+            if (k == 0 && args.gtrace && g == args.group0 && s >= 8 && s < 40) {
+              uint32_t smid;
+              asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+              args.gtrace[size_t(gridDim.x) * 512 + size_t(blockIdx.x) * 32 + (s - 8)] =
+                  (gtimer() & 0xFFFFFFFFFFFFull) | (uint64_t(smid) << 48);
+            }
           });
         }
       }
@@ -374,7 +411,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
     const int spin = i0 + sl;
     const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
     const uint32_t g_sel = (lane & 1) ? 0x15u : 0x40u;
-    const bool io = warp == 4 && lane == 0;  // issues the state TMA loads / stores
+    const bool io = warp == 4 && lane == 0;  // dev trace stamps, the helper pacing signal
     auto xa = [&](int col) { return x_base + static_cast<uint32_t>(col * Cfg::BM + sl) * 4u; };
     auto ya = [&](int col) { return y_base + static_cast<uint32_t>(col * Cfg::BM + sl) * 4u; };
     float preg[Cfg::NR / 4];
@@ -389,26 +426,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(gfull_bar(i));
     };
-    if (io) {
-      ptx::prefetch_tmap(&maps.X);
-      ptx::prefetch_tmap(&maps.Y);
-    }
     int lt = 0, pc = 0, gl = 0;
     for (int g = args.group0; g < args.group0 + args.groups; ++g, ++gl) {
       const int n_blk = g * args.rb_per_group + rbk;
       if (n_blk >= num_n) break;
       const bool first = g == args.group0;
       if (io) gstamp(g, 0);
-      // ---- group start: x, y of the block by TMA (rows >= rpad are zero-filled), p to registers
-      if (io) {
-        if (args.ready)
-          while (dep::ld_acquire_sys(args.ready + (g == 0 ? rbk : args.rb_per_group + g - 1)) == 0)
-            __nanosleep(256);
-        ptx::bulk_wait_read0();  // the previous group's state stores have read the buffers
-        ptx::mbar_arrive_expect_tx(sfull_bar, 2 * Cfg::XY_BYTES);
-        ptx::tma_load_2d(x_base, &maps.X, sfull_bar, i0, n_blk * Cfg::NR);
-        ptx::tma_load_2d(y_base, &maps.Y, sfull_bar, i0, n_blk * Cfg::NR);
-      }
+      // ---- group start: x, y arrive by TMA (issued by the publisher, sfull), p to registers
       static_for<0, PARTS>([&](auto I) {
         constexpr int i = decltype(I)::value;
         static_for<0, Cfg::w(i) / 16>([&](auto C) {
@@ -421,11 +445,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
           }
         });
       });
-      ptx::mbar_wait(sfull_bar, gl & 1);
       if (first) {  // G_0 = sgn(x_0) of the launch's first group (later groups: the helper)
         static_for<0, PARTS>([&](auto I) {
           constexpr int i = decltype(I)::value;
           ptx::mbar_wait(gempty_bar(i), (pc & 1) ^ 1u);
+          ptx::mbar_wait(sfull_bar(i), gl & 1);
           static_for<0, Cfg::w(i) / 16>([&](auto C) {
             constexpr int c = decltype(C)::value;
             const int col = Cfg::off(i) + cg * (Cfg::w(i) / 4) + c * CH;
@@ -458,6 +482,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
               by[b][j] = ptx::lds_f32(ya(c0 + c * CH + j));
             }
           };
+          if (s == 0) ptx::mbar_wait(sfull_bar(i), gl & 1);  // this part's state has landed
           ld_xy(0, 0);  // the state does not depend on the MMA: read before its completion
           ptx::mbar_wait(tfull_bar(i), lt & 1);
           __syncwarp();
@@ -515,15 +540,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
           if (io) stamp(g, s, i, 2);
         });
       }
-      // ---- group end: x, y back by TMA (after every epilogue thread's last smem writes), p by stores
+      // ---- group end: x, y went back with the last step's G tiles (the publisher); p by stores
       if (io) gstamp(g, 4);
-      ptx::fence_proxy_async_smem();
-      ptx::named_bar(1, 32 * Cfg::EPI_WARPS);
-      if (io) {
-        ptx::tma_store_2d(&maps.X, x_base, i0, n_blk * Cfg::NR);
-        ptx::tma_store_2d(&maps.Y, y_base, i0, n_blk * Cfg::NR);
-        ptx::bulk_commit();
-      }
       const uint64_t wb_policy = ptx::policy_evict_first();
       static_for<0, PARTS>([&](auto I) {
         constexpr int i = decltype(I)::value;
@@ -541,7 +559,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
       });
       if (io) gstamp(g, 5);
     }
-    if (io) ptx::bulk_wait0();  // the last group's state stores are complete before exit
   }
 
   ptx::tc_fence_before();
