@@ -344,7 +344,7 @@ def run_ours(args):
         if not args.no_tts:
             extra.update(measure_tts(s))
     else:
-        extra["c5_row_shards"] = c5_row_shard_leg(args, rank, world, local)
+        extra["c5_row_shards"] = c5_leg_in_children(args, rank, world)
     s.close()
 
     if world == 1 and not args.no_configs:
@@ -631,6 +631,50 @@ def measure_configs(args, device: int):
 
 # ------------------------------------------------------------------ C5 row shards (N > 1)
 
+def c5_leg_in_children(args, rank: int, world: int):
+    """Run the C5 row-shard leg in one child process per rank (own process group on a fresh
+    port, own CUDA context) under a timeout, so a failure there -- a CUDA fault, a hung peer --
+    cannot take the headline measurement of this process down with it."""
+    import tempfile
+
+    import torch
+    import torch.distributed as dist
+
+    port = torch.tensor([free_port() if rank == 0 else 0], device="cuda", dtype=torch.int64)
+    dist.broadcast(port, src=0)
+    env = dict(os.environ, MASTER_PORT=str(int(port.item())), MASTER_ADDR="127.0.0.1")
+    out = os.path.join(tempfile.gettempdir(), f"sbg_c5leg_{os.getpid()}_{rank}.json")
+    cmd = [sys.executable, os.path.abspath(__file__), "--c5-child", out, "--gpus", str(world), "--steps",
+           str(args.steps), "--warmup", str(args.warmup)]
+    res = {"error": "child did not report"}
+    try:
+        rc = subprocess.run(cmd, env=env, timeout=900).returncode
+        if os.path.exists(out):
+            with open(out) as f:
+                res = json.load(f)
+        elif rc != 0:
+            res = {"error": f"child exited with {rc}"}
+    except subprocess.TimeoutExpired:
+        res = {"error": "child timed out (900 s)"}
+    finally:
+        if os.path.exists(out):
+            os.remove(out)
+    return res
+
+
+def c5_child_main(args):
+    rank, world, local = dist_env()
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    res = c5_row_shard_leg(args, rank, world, local)
+    with open(args.c5_child, "w") as f:
+        json.dump(res, f)
+    dist.destroy_process_group()
+
+
 def c5_row_shard_leg(args, rank: int, world: int, local: int):
     """BASELINE configs[4]: N=100000 dense +-1 (gen_random_dense(100000, 1), each rank
     generating its own rows on the device), GdSB, R=256, row-sharded over the ranks. The
@@ -657,7 +701,7 @@ def c5_row_shard_leg(args, rank: int, world: int, local: int):
     s = None
     try:
         s = Solver(local)
-        s.gen_random_dense(n, 1, world, rank)
+        s.gen_random_dense(n, 1, world, rank, shard=True)
         s.init_state(R, InitMode.small_uniform, 1, 7)
         ok = True
     except Exception as e:  # noqa: BLE001
@@ -688,9 +732,32 @@ def c5_row_shard_leg(args, rank: int, world: int, local: int):
         ok, err, ms = False, f"steps: {e}", float("nan")
     info = s.shard_info() if ok else {}
     fmt = s.operand_format
+    part = None
+    if ok:
+        try:
+            part = s.readout_partial()  # this rank's E2 share after all 2 + K steps
+        except Exception as e:  # noqa: BLE001
+            ok, err = False, f"readout: {e}"
     s.close()
     if not all_ok(ok):
         return {"error": err or "a rank failed (peer wait timeout or CUDA error)"}
+    # correctness of the cross-GPU run: the ranks' E2 shares must sum to the energies of the same
+    # 2 + K steps run unsharded on rank 0 (the whole J fits one B200), bitwise
+    from paper_2508_17655_b200.distributed import row_sharded_energies
+
+    t = torch.as_tensor(part, device="cuda")
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t)
+    check = None
+    if rank == 0:
+        e_sh = row_sharded_energies([q.cpu().numpy() for q in parts])
+        with Solver(local) as u:
+            u.gen_random_dense(n, 1)
+            u.init_state(R, InitMode.small_uniform, 1, 7)
+            u.advance(cfg, 0, 2)
+            u.advance(cfg, 2, 2 + args.steps)
+            _, e_un, _, _ = u.readout()
+        check = bool((e_sh == e_un).all())
     t = torch.tensor([ms], device="cuda", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
@@ -701,6 +768,7 @@ def c5_row_shard_leg(args, rank: int, world: int, local: int):
     return {"workload": "C5 (BASELINE configs[4]): N=100000 dense +-1, GdSB, R=256, row-sharded", "ranks": world,
             "us_per_step_per_rank": us, "su_per_s_boxwide": n * R / (us * 1e-6), "steps": args.steps,
             "operands": fmt, "rows_per_rank": info["rows_padded"],
+            "energies_bitwise_equal_unsharded": check,
             "hbm_gbs_per_rank": byts / (us * 1e-6) / 1e9, "hbm_frac": byts / (us * 1e-6) / 1e9 / hbm,
             "hbm_peak_source": src,
             "timed": "one persistent launch of K steps per rank, CUDA events, max over ranks"}
@@ -732,7 +800,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tts", action="store_true")
     ap.add_argument("--no-configs", action="store_true")
+    ap.add_argument("--c5-child", default=None, help=argparse.SUPPRESS)  # internal: the N>1 C5 leg
     args = ap.parse_args()
+    if args.c5_child:
+        return c5_child_main(args)
     if args.warmup < 3:
         args.warmup = 3
     _, world, _ = dist_env()

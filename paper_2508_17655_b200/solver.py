@@ -352,10 +352,10 @@ class Solver:
         self._check(self._L.sbg_readout_partial(self._h, ptr(e2)))
         return e2
 
-    def gen_random_dense(self, n: int, seed: int, world: int = 1, rank: int = 0) -> None:
+    def gen_random_dense(self, n: int, seed: int, world: int = 1, rank: int = 0, shard: bool = False) -> None:
         """gen_random_dense (model.cpp:144-159) generated on the device in the reference's
-        exact draw order; world > 1 keeps only this rank's rows (row sharding)."""
-        if world == 1:
+        exact draw order; world > 1 (or shard=True) keeps only this rank's rows (row sharding)."""
+        if world == 1 and not shard:
             self._check(self._L.sbg_gen_couplings_dense_pm1(self._h, n, seed))
             self.n = n
         else:
