@@ -2,6 +2,10 @@
 exercise the hot path, run on the GPU through the C ABI:
   1  A = 0 GbSB == bSB bitwise over 100 random configurations      (acceptance.cpp:49-81)
   2  >= 48/50 N=10 ground states with best-of-20, M = 2000, A = 0.2 (acceptance.cpp:85-109)
+  5  chaos-indicator limits at N=800: mean delta(t_M) < 0.05 at A = 0 and within 0.05
+     of 1/sqrt(2) at A = 1.0 (15 A values x 100 pairs, M = 1000)     (acceptance.cpp:148-199)
+  6  edge-of-chaos co-location: the A of maximal P_S (13 A values x 200 GbSB runs, target =
+     best of all runs and 200 dSB baselines) has mean delta in (0.1, 0.6) (acceptance.cpp:201-215)
   7  GbSB (best A) beats bSB in P_S on >= 8/10 N=700 instances     (acceptance.cpp:219-255)
 plus P4 at the C1 scale (N=2000, M=1000): GPU final-energy law vs the reference's
 own fp64 runs from the same initial states."""
@@ -109,3 +113,41 @@ def test_p4_c1_scale_energy_law_vs_reference(solver, orc):
         p1, p2 = (b.energies <= tgt).mean(), (e_ref <= tgt).mean()
         sigma = math.sqrt(p1 * (1 - p1) / R_gpu + p2 * (1 - p2) / R_ref) + 1e-3
         assert abs(p1 - p2) <= 4 * sigma, (pct, p1, p2)
+
+
+@pytest.fixture(scope="module")
+def chaos_experiment():
+    """run_chaos_experiment (acceptance.cpp:148-190) on the GPU: gen_random_dense(800, 11),
+    Wigner tuning, chaos scan over {0, 0.05, ..., 0.6} + {0.8, 1.0} (100 pairs, M = 1000,
+    seed 501), the GbSB success sweep over {0, ..., 0.6} (200 runs, M = 1000, seed 601) and
+    the dSB baseline (200 runs, seed 701); target = best of everything, P_S restated."""
+    from paper_2508_17655_b200 import Solver, SolverConfig, Variant, auto_tune_wigner
+    from paper_2508_17655_b200.solver import chaos_scan, success_probability, sweep
+
+    with Solver(0) as s:
+        s.gen_random_dense(800, 11)
+        J = s.get_couplings()
+        t = auto_tune_wigner(J.astype(np.float64))
+        a_grid = [0.05 * k for k in range(13)]
+        scan = chaos_scan(s, a_grid + [0.8, 1.0], 100, SolverConfig(variant=Variant.gbsb, steps=1000, seed=501), t)
+        cells = sweep(s, [1000], a_grid, 200, SolverConfig(variant=Variant.gbsb, seed=601), t, target=-math.inf)
+        dsb = sweep(s, [1000], [0.0], 200, SolverConfig(variant=Variant.dsb, seed=701), t, target=-math.inf)
+    target = min([float(dsb[0].energies.min())] + [cl.best_energy for cl in cells])
+    ps = [success_probability(cl.energies, target) for cl in cells]
+    return {"a_grid": a_grid, "scan": scan, "ps": ps, "target": target}
+
+
+def test_criterion_5_chaos_indicator_limits(chaos_experiment):
+    scan = chaos_experiment["scan"]
+    at_zero, at_largest = scan[0].mean_final_delta, scan[-1].mean_final_delta
+    assert scan[-1].a == 1.0
+    assert at_zero < 0.05, at_zero
+    assert abs(at_largest - 1 / math.sqrt(2)) <= 0.05, at_largest
+
+
+def test_criterion_6_edge_of_chaos_colocation(chaos_experiment):
+    ps, scan = chaos_experiment["ps"], chaos_experiment["scan"]
+    best = max(range(len(ps)), key=lambda k: (ps[k].p_s, -k))  # first maximum, as the reference's loop
+    delta = scan[best].mean_final_delta  # same grid order
+    assert ps[best].hit_count > 0, chaos_experiment["target"]
+    assert 0.1 < delta < 0.6, (chaos_experiment["a_grid"][best], ps[best].p_s, delta)
