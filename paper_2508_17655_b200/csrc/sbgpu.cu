@@ -154,6 +154,8 @@ struct sbg_ctx {
   cudaEvent_t evc[3];
   float last_advance_ms = 0.f;
   int8_t* tail_best_spins = nullptr;  // sbg_run_best: winner-only readout in run_tail
+  bool csr_sm_current = false;  // CSR: the spin-major working copies hold the state (dX/dY/dP stale)
+  int csr_q = -1;               // ... and dQ[csr_q] holds its gathered operand (sign: +2), -1 none
   double* tail_best_energy = nullptr;
 
   int fail(int code, const char* fmt, ...) {
@@ -527,6 +529,7 @@ void free_state(sbg_ctx* ctx) {
   cudaFree(ctx->d_done);
   ctx->d_done = nullptr;
   ctx->dX = ctx->dY = ctx->dP = nullptr;
+  ctx->csr_sm_current = false;
   ctx->dG[0] = ctx->dG[1] = ctx->dSign = nullptr;
   ctx->dE2 = nullptr;
   ctx->dBest = nullptr;
@@ -536,6 +539,7 @@ void free_state(sbg_ctx* ctx) {
 // (Re)allocate the replica state for R replicas of the current instance.
 int ensure_state(sbg_ctx* ctx, int64_t R) {
   if (ctx->kind == KIND_NONE) return ctx->fail(SBG_ERR_STATE, "couplings not set");
+  ctx->csr_sm_current = false;  // every caller rewrites the replica-major state next
   if (R < 1) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "replica count must be >= 1");
   const int64_t rpad = round_up(R, PAD_R);
   if (rpad > (int64_t(1) << 30) / 4) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "too many replicas");
@@ -1299,6 +1303,25 @@ int sbg_set_couplings_entries_f64(sbg_ctx* ctx, int64_t n, int64_t m, const int6
   return sbg_set_couplings_dense_f64(ctx, n, J.data());
 }
 
+// CSR: sbg_advance leaves the state in the spin-major working copies (the next advance
+// continues from them with no transposes); anything that reads the replica-major x, y, p
+// first brings them up to date (three transposes, once).
+static int csr_sync(sbg_ctx* ctx) {
+  if (ctx->kind != KIND_CSR_I8 || !ctx->csr_sm_current) return SBG_OK;
+  const dim3 tb(32, 8);
+  const dim3 tg_out(unsigned((ctx->R + 31) / 32), unsigned((ctx->n + 31) / 32));
+  float* rm[3] = {ctx->dX, ctx->dY, ctx->dP};
+  float* sm[3] = {ctx->dXs, ctx->dYs, ctx->dPs};
+  for (int a = 0; a < 3; ++a) {
+    transpose_f32_kernel<<<tg_out, tb, 0, ctx->stream>>>(sm[a], rm[a], int32_t(ctx->n), int32_t(ctx->R), ctx->rp,
+                                                         ctx->npad);
+    CK(cudaGetLastError());
+    ++ctx->launches;
+  }
+  ctx->csr_sm_current = false;
+  return SBG_OK;
+}
+
 int sbg_set_state(sbg_ctx* ctx, int64_t R, const float* x, const float* y, const float* p) {
   CHECK_CTX(ctx);
   if (!x || !y) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "x and y are required");
@@ -1358,6 +1381,7 @@ int sbg_get_state(sbg_ctx* ctx, float* x, float* y, float* p) {
   CHECK_CTX(ctx);
   if (!ctx->dX) return ctx->fail(SBG_ERR_STATE, "no state");
   CK(cudaSetDevice(ctx->device));
+  if (int rc = csr_sync(ctx)) return rc;
   const size_t pitch = sizeof(float) * ctx->npad, w = sizeof(float) * ctx->n;
   if (x) CK(cudaMemcpy2DAsync(x, w, ctx->dX, pitch, w, ctx->R, cudaMemcpyDeviceToHost, ctx->stream));
   if (y) CK(cudaMemcpy2DAsync(y, w, ctx->dY, pitch, w, ctx->R, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1386,24 +1410,32 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
   k.inv = 0.0f;
   CK(cudaEventRecord(ctx->ev[0], ctx->stream));
   if (ctx->kind == KIND_CSR_I8) {
-    // replica-major -> spin-major, B operand, M steps (ping-pong), spin-major -> replica-major
+    // replica-major -> spin-major (unless the last advance left the state there), B operand, M
+    // steps (ping-pong); the state stays spin-major until something reads it (csr_sync)
     const int32_t n32 = int32_t(ctx->n), R32 = int32_t(ctx->R);
     const dim3 tb(32, 8);
     const dim3 tg_in(unsigned((ctx->n + 31) / 32), unsigned((ctx->R + 31) / 32));
     float* rm[3] = {ctx->dX, ctx->dY, ctx->dP};
     float* sm[3] = {ctx->dXs, ctx->dYs, ctx->dPs};
-    for (int a = 0; a < 3; ++a) {
+    for (int a = 0; !ctx->csr_sm_current && a < 3; ++a) {
       transpose_f32_kernel<<<tg_in, tb, 0, ctx->stream>>>(rm[a], sm[a], R32, n32, ctx->npad, ctx->rp);
       CK(cudaGetLastError());
       ++ctx->launches;
     }
     const size_t cnt = size_t(ctx->npad) * ctx->rp;
-    if (sign)
-      csr_prep_kernel<true><<<grid_for(ctx, cnt, 256), 256, 0, ctx->stream>>>(ctx->dXs, ctx->dQ[0], cnt);
-    else
-      csr_prep_kernel<false><<<grid_for(ctx, cnt, 256), 256, 0, ctx->stream>>>(ctx->dXs, ctx->dQ[0], cnt);
-    CK(cudaGetLastError());
-    ++ctx->launches;
+    // the operand of the current state: left in dQ[q0] by the previous advance (same kind), or
+    // built here into dQ[0]
+    int q0 = 0;
+    if (ctx->csr_sm_current && ctx->csr_q >= 0 && (ctx->csr_q >= 2) == sign) {
+      q0 = ctx->csr_q & 1;
+    } else {
+      if (sign)
+        csr_prep_kernel<true><<<grid_for(ctx, cnt, 256), 256, 0, ctx->stream>>>(ctx->dXs, ctx->dQ[0], cnt);
+      else
+        csr_prep_kernel<false><<<grid_for(ctx, cnt, 256), 256, 0, ctx->stream>>>(ctx->dXs, ctx->dQ[0], cnt);
+      CK(cudaGetLastError());
+      ++ctx->launches;
+    }
     const float* arep = (honours_a && ctx->d_arep && ctx->arep_n == ctx->R) ? ctx->d_arep : nullptr;
     // Replica slabs (SBG_CSR_SLAB = width, a multiple of 128): replicas are independent, so the M
     // steps may run slab by slab, each slab's x, y, p and operand buffers (n * W * 20 B) staying in
@@ -1432,9 +1464,9 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
       const int blocks =
           int(std::min<int64_t>((tasks + CSR_THREADS / 32 - 1) / (CSR_THREADS / 32), int64_t(ctx->sms) * 8));
       const size_t gsz = sign ? 1 : 4;
-      const void* q0 = reinterpret_cast<const char*>(ctx->dQ[0]) + size_t(r0) * gsz;
-      void* q1 = reinterpret_cast<char*>(ctx->dQ[1]) + size_t(r0) * gsz;
-      const void* gq[2] = {q0, q1};
+      const void* qa = reinterpret_cast<const char*>(ctx->dQ[q0]) + size_t(r0) * gsz;
+      void* qb = reinterpret_cast<char*>(ctx->dQ[q0 ^ 1]) + size_t(r0) * gsz;
+      const void* gq[2] = {qa, qb};
       float *xs = ctx->dXs + r0, *ys = ctx->dYs + r0, *ps = ctx->dPs + r0;
       const float* ar = arep ? arep + r0 : nullptr;
       int cur = 0;
@@ -1470,12 +1502,8 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
         cur ^= 1;
       }
     }
-    const dim3 tg_out(unsigned((ctx->R + 31) / 32), unsigned((ctx->n + 31) / 32));
-    for (int a = 0; a < 3; ++a) {
-      transpose_f32_kernel<<<tg_out, tb, 0, ctx->stream>>>(sm[a], rm[a], n32, R32, ctx->rp, ctx->npad);
-      CK(cudaGetLastError());
-      ++ctx->launches;
-    }
+    ctx->csr_sm_current = true;
+    ctx->csr_q = (q0 ^ int((m_end - m_begin) & 1)) + (sign ? 2 : 0);
   } else {
     const bool resident = use_resident(ctx, prm->variant);
     const int knob = dev_knob("SBG_STEP_CFG");
@@ -1640,7 +1668,8 @@ namespace {
 // Energies of every replica (device) + argmin; leaves dE2/dBest/dSign populated.
 int readout_device(sbg_ctx* ctx) {
   CK(cudaSetDevice(ctx->device));
-  int rc;
+  int rc = csr_sync(ctx);
+  if (rc) return rc;
   CK(cudaMemsetAsync(ctx->dE2, 0, sizeof(unsigned long long) * ctx->rpad, ctx->stream));
   if (ctx->kind == KIND_CSR_I8) {
     rc = launch_csr_readout(ctx->stream, ctx->sms, int32_t(ctx->n), ctx->d_rowptr, ctx->d_col, ctx->d_val,
@@ -1811,6 +1840,7 @@ static int run_tail(sbg_ctx* ctx, const sbg_params* prm, float* x_final, int8_t*
   CK(cudaEventRecord(ctx->ev[5], ctx->stream));
   if (x_final) {
     const size_t pitch = sizeof(float) * ctx->npad, w = sizeof(float) * ctx->n;
+    if (int rc2 = csr_sync(ctx)) return rc2;
     CK(cudaMemcpy2DAsync(x_final, w, ctx->dX, pitch, w, ctx->R, cudaMemcpyDeviceToHost, ctx->stream));
   }
   CK(cudaEventRecord(ctx->ev[6], ctx->stream));
@@ -2297,6 +2327,7 @@ int sbg_synchronize(sbg_ctx* ctx) {
 int sbg_state_device(sbg_ctx* ctx, float** x, float** y, float** p, int64_t* ld, int64_t* rpad) {
   CHECK_CTX(ctx);
   if (!ctx->dX) return ctx->fail(SBG_ERR_STATE, "no state");
+  if (int rc = csr_sync(ctx)) return rc;
   if (x) *x = ctx->dX;
   if (y) *y = ctx->dY;
   if (p) *p = ctx->dP;

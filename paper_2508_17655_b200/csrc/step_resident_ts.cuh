@@ -489,9 +489,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
           ptx::tc_fence_after();
           if (io && i == 0 && s < 2) gstamp(g, 2 + s);
           if (io) stamp(g, s, i, 1);
-          ptx::mbar_wait(gempty_bar(i), (pc & 1) ^ 1u);  // this part's G tile stored
-          if (io) stamp(g, s, i, 10);
           ptx::tmem_ld<CH>(t_lane + c0, bf[0]);
+          ptx::mbar_wait(gempty_bar(i), (pc & 1) ^ 1u);  // this part's G tile stored (under the load)
+          if (io) stamp(g, s, i, 10);
           ptx::tmem_ld_wait();
           if (io) stamp(g, s, i, 11);
           auto chunks = [&](auto has_arep) {

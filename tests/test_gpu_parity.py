@@ -355,6 +355,33 @@ def test_dt_sweep_grid_matches_mirror_per_cell(solver, orc):
         assert (cl.energies == -0.5 * orc.energy2_i8(J, x)).all(), (cl.di, cl.ti)
 
 
+def test_csr_chunked_advances_keep_state_spin_major(solver, orc):
+    """CSR advances leave the state in the spin-major working copies and the next advance
+    continues from there; readers (get_state, readout) bring the replica-major copy up to date.
+    Chunked advances with and without reads in between == one advance == the mirror."""
+    n, m, R = 2500, 9000, 300
+    _, csr = orc.gen_er_csr(n, m, 8)
+    c, dt = np.float32(0.21), np.float32(1.25)
+    x0, y0, p0 = orc.init_small_uniform(n, R, master=4)
+    cfg = cfg_for(GBSB, 60, float(dt), float(c), 0.2)
+    solver.set_instance_csr(n, *csr)
+    outs = []
+    for plan in ([(0, 17)], [(0, 5), (5, 11), (11, 17)], [(0, 9), "read", (9, 17)]):
+        solver.set_state(x0, y0, p0)
+        for step in plan:
+            if step == "read":
+                solver.get_state()
+                solver.readout()
+            else:
+                solver.advance(cfg, *step)
+        outs.append(solver.get_state())
+    mx, my, mp = orc.step_f32_csr(GBSB, n, csr, x0, y0, p0, 0, 60, dt, c, np.float32(0.2), 17)
+    for x, y, p in outs:
+        assert (x == mx).all() and (y == my).all() and (p == mp).all()
+    _, e, _, _ = solver.readout()
+    assert (e == -0.5 * orc.energy2_csr(n, csr, mx)).all()
+
+
 def test_csr_solver_reused_across_replica_counts(solver, orc):
     """One CSR context run with R = 1, then R = 200 (same 256-replica padding bucket), then
     R = 300: every run bitwise equal to the fp32 mirror (the spin-major working buffers
