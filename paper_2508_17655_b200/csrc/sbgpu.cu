@@ -400,18 +400,18 @@ int resident_nr(const sbg_ctx* ctx) {
 }
 
 template <int EPI, int CH, int ST = RES_STAGES, int NR = 128, bool Q4 = false, int PARTS = 0, bool JRES = false,
-          class Maps = TmaMaps>
+          class Maps = TmaMaps, bool PKB = false>
 int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int group0 = 0, int ngroups = -1,
                     const uint32_t* ready = nullptr) {
   // PARTS > 0: step_resident_parts.cuh (e2m1, 160-replica blocks as PARTS interleaved column
   // parts; JRES = J resident in shared memory); else step_resident.cuh
   // PARTS < 0: step_resident_ts.cuh with -PARTS parts (J in TMEM, x, y in shared memory)
   using Cfg = std::conditional_t<
-      (PARTS < 0), TsCfg<ST, (PARTS < 0 ? -PARTS : 2)>,
+      (PARTS < 0), TsCfg<ST, (PARTS < 0 ? -PARTS : 2), PKB>,
       std::conditional_t<(PARTS > 0), PartsCfg<ST, JRES, (PARTS > 0 ? PARTS : 2)>, ResCfg<ST, EPI, CH, NR, false, Q4>>>;
   auto kern = [] {
     if constexpr (PARTS < 0)
-      return gsb_resident_ts_kernel<ST, -PARTS>;
+      return gsb_resident_ts_kernel<ST, -PARTS, PKB>;
     else if constexpr (PARTS > 0)
       return gsb_resident_parts_kernel<ST, JRES, PARTS>;
     else
@@ -461,7 +461,7 @@ int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int
     a.gtrace = gtrace;
   }
   // done counters per replica block (one per part)
-  const int counters = PARTS != 0 ? (PARTS > 0 ? PARTS : -PARTS) : 1;
+  const int counters = PARTS != 0 ? (PARTS > 0 ? PARTS : -PARTS * (PKB ? num_mp : 1)) : 1;
   CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * num_n * counters, ctx->stream));
   CK(launch_persistent(kern, 2 * num_mp * a.rb_per_group, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream, maps, a));
   ++ctx->launches;
@@ -557,7 +557,8 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
     CK(cudaMalloc(&ctx->dE2, sizeof(unsigned long long) * rpad));
     CK(cudaMalloc(&ctx->dE2p, sizeof(unsigned long long) * rpad * FX_NA));
     CK(cudaMalloc(&ctx->dBest, 2 * sizeof(long long)));
-    CK(cudaMalloc(&ctx->d_done, sizeof(uint32_t) * (rpad / 16 + 1)));
+    // per replica block / part / CTA pair (TS kernel: <= 5 parts x 8 pairs per 160 replicas)
+    CK(cudaMalloc(&ctx->d_done, sizeof(uint32_t) * (rpad / 2 + 64)));
     CK(cudaMemsetAsync(ctx->dG[0], 0, NPL * gpl, ctx->stream));
     CK(cudaMemsetAsync(ctx->dG[1], 0, NPL * gpl, ctx->stream));
     CK(cudaMemsetAsync(ctx->dSign, 0, pl, ctx->stream));
@@ -1893,7 +1894,7 @@ static int encode_part_maps(sbg_ctx* ctx, PartMaps* pm, int cur, int w0, int w1)
 extern "C++" {
 // The TS kernel (J in TMEM, x, y in shared memory): the parts kernel's G maps plus 2D boxes
 // {128 spins, 160 replicas} of the replica-major x and y (rows >= rpad read as zero).
-template <int PARTS, int ST>
+template <int PARTS, int ST, bool PKB>
 int launch_ts(sbg_ctx* ctx, int cur, const MultiStepArgs& a, int groups, const uint32_t* ready) {
   using T = PartTable<PARTS>;
   TsMaps tm;
@@ -1909,7 +1910,7 @@ int launch_ts(sbg_ctx* ctx, int cur, const MultiStepArgs& a, int groups, const u
   }
   if (rc) return rc;
   if (a.nsteps < 1) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "resident launch without steps");
-  return launch_resident<16, 4, ST, RES_NR, true, -PARTS, true>(ctx, tm, a, 0, groups, ready);
+  return launch_resident<16, 4, ST, RES_NR, true, -PARTS, true, TsMaps, PKB>(ctx, tm, a, 0, groups, ready);
 }
 
 template <int PARTS, int ST, bool JRES>
@@ -1938,8 +1939,14 @@ static int launch_resident_default(sbg_ctx* ctx, int cur, const MultiStepArgs& a
       // parts kernel (J in shared memory)
       if (!getenv_is0("SBG_RES_TS")) {
         // (wider parts' G super-stages do not fit beside x and y in shared memory)
-        if (dev_knob("SBG_RES_PARTS") == 5) return launch_ts<5, 3>(ctx, cur, a, groups, ready);
-        return launch_ts<4, 2>(ctx, cur, a, groups, ready);
+        // SBG_RES_PKB=1 (dev): per-K-block dependencies and MMA issue in landing order. Bitwise
+        // equal, measured slower (26.7 -> 34.7 us/step): the producer's eight diverged polling
+        // lanes (each acquire invalidates L1) and the MMA warp's per-part poll over all eight
+        // K blocks serialise more than the wait for the slowest producer they were to hide.
+        const bool pkb = dev_knob("SBG_RES_PKB") == 1;
+        if (dev_knob("SBG_RES_PARTS") == 5)
+          return pkb ? launch_ts<5, 3, true>(ctx, cur, a, groups, ready) : launch_ts<5, 3, false>(ctx, cur, a, groups, ready);
+        return pkb ? launch_ts<4, 2, true>(ctx, cur, a, groups, ready) : launch_ts<4, 2, false>(ctx, cur, a, groups, ready);
       }
       switch (dev_knob("SBG_RES_PARTS")) {
         case 2: return launch_parts<2, 2, true>(ctx, cur, a, groups, ready);

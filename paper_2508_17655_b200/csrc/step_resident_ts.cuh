@@ -60,8 +60,14 @@ struct TsMaps {
   CUtensorMap X[2], Y[2];  // f32 [rpad][npad], box {128 spins, part width} per width class
 };
 
-template <int STAGES_, int PARTS_>
+// PKB_: per-K-block dependencies. Each K block of a part's G operand (256 spins = one CTA
+// pair's slab) has its own done counter, TMA load and mbarrier, and the MMA warp issues the
+// K blocks' MMAs in the order they land (exact integer sums: any order gives the same field),
+// so a part's MMAs overlap the wait for the slowest of the 16 producer CTAs instead of
+// starting after it.
+template <int STAGES_, int PARTS_, bool PKB_ = false>
 struct TsCfg {
+  static constexpr bool PKB = PKB_;
   static constexpr int PARTS = PARTS_;
   using T = PartTable<PARTS>;
   __host__ __device__ static constexpr int w(int i) { return T::W[i]; }
@@ -79,7 +85,7 @@ struct TsCfg {
   static constexpr int XY_BYTES = NR * BM * 4;     // 80 KB each
   static constexpr int T_BYTES = NR * BM / 2;      // G tiles of all parts: [160][64] bytes
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
-  static constexpr int NUM_BARS = 2 * STAGES + 5 * PARTS;
+  static constexpr int NUM_BARS = 2 * STAGES + 5 * PARTS + (PKB ? STAGES * KB_MAX : 0);
   static constexpr int SMEM_BYTES = 2 * XY_BYTES + STAGES * STAGE_BYTES + T_BYTES + 1024 + 8 * NUM_BARS + 64;
   static constexpr uint32_t COL_J = NR, COL_SF = 512 - 16;
   static_assert(off(PARTS - 1) + w(PARTS - 1) == NR, "parts cover the block");
@@ -88,10 +94,10 @@ struct TsCfg {
   static_assert(STAGE_BYTES % 1024 == 0 && XY_BYTES % 1024 == 0, "alignment");
 };
 
-template <int STAGES_, int PARTS_>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS_>::THREADS, 1)
+template <int STAGES_, int PARTS_, bool PKB_>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS_, PKB_>::THREADS, 1)
     gsb_resident_ts_kernel(const __grid_constant__ TsMaps maps, const ResidentArgs args) {
-  using Cfg = TsCfg<STAGES_, PARTS_>;
+  using Cfg = TsCfg<STAGES_, PARTS_, PKB_>;
   constexpr int CH = Cfg::CH;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int PARTS = Cfg::PARTS;
@@ -115,6 +121,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
   auto gfull_bar = [&](int i) { return bar(2 * STAGES + 2 * PARTS + i); };
   auto gempty_bar = [&](int i) { return bar(2 * STAGES + 3 * PARTS + i); };
   auto sfull_bar = [&](int i) { return bar(2 * STAGES + 4 * PARTS + i); };  // part i's x, y landed (TMA)
+  auto fullk_bar = [&](int st, int kb) { return bar(2 * STAGES + 5 * PARTS + st * Cfg::KB_MAX + kb); };  // PKB
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -142,6 +149,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
       ptx::mbar_init(gempty_bar(i), 1);
     }
     for (int i = 0; i < PARTS; ++i) ptx::mbar_init(sfull_bar(i), 1);
+    if constexpr (Cfg::PKB)
+      for (int st = 0; st < STAGES; ++st)
+        for (int kb = 0; kb < Cfg::KB_MAX; ++kb) ptx::mbar_init(fullk_bar(st, kb), 2);
     ptx::fence_mbar_init();
     *started = 0;
   }
@@ -161,6 +171,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
   const int i0 = m_blk * Cfg::BM;
   const int KB = args.npad / (2 * Cfg::BK);
   const int num_n = (args.rpad + Cfg::NR - 1) / Cfg::NR;
+  // done counter a CTA releases for (block, part): per (block, part) counting all num_m CTAs,
+  // or with PKB per (block, part, CTA pair) counting the pair's 2 CTAs
+  auto done_idx = [&](int n_blk, int i) { return Cfg::PKB ? (n_blk * PARTS + i) * num_mp + mp : PARTS * n_blk + i; };
 
   if (warp >= 4) {
     // unit E8M0 scale factors, and this CTA's 128 rows of J into TMEM: lane = row, K block kb at
@@ -197,7 +210,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
   if (warp == 0) {  // ------------------------------------------------ G producer
     if (ptx::elect_one())
       for (int c = 0; c < 2; ++c)
-        for (int p = 0; p < 2; ++p) ptx::prefetch_tmap(&maps.g.Gin3[c][p]);
+        for (int p = 0; p < 2; ++p) {
+          ptx::prefetch_tmap(&maps.g.Gin3[c][p]);
+          ptx::prefetch_tmap(&maps.g.Gin[c][p]);
+        }
     int stage = 0;
     uint32_t ph = 0;
     const uint64_t keep = ptx::policy_evict_last();
@@ -209,17 +225,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
           constexpr int i = decltype(I)::value;
           constexpr uint32_t b_bytes = (Cfg::w(i) / 2) * Cfg::BK;
           const int b_row0 = n_blk * Cfg::NR + Cfg::off(i) + static_cast<int>(cr) * (Cfg::w(i) / 2);
-          dep::wait_block(args.done, PARTS * n_blk + i, 0u, static_cast<uint32_t>((s + 1) * args.num_m));
-          if (lane == 0) stamp(g, s, i, 0);
-          ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
-          if (lane == 0) stamp(g, s, i, 8);
-          if (ptx::elect_one()) {
-            const uint32_t fb = ptx::mapa(full_bar(stage), 0);
-            ptx::mbar_arrive_expect_tx_cluster(fb, KB * b_bytes);
-            ptx::tma_load_3d_pair_hint(b_base + stage * Cfg::STAGE_BYTES, &maps.g.Gin3[Cfg::cls(i)][s & 1], fb, 0,
-                                       b_row0, 0, keep);
+          if constexpr (Cfg::PKB) {
+            // lane kb: wait for producer pair kb's slab of G_s, then load it (its own barrier)
+            ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
+            if (lane < KB) {
+              const uint32_t* cnt = args.done + (n_blk * PARTS + i) * num_mp + lane;
+              const uint32_t need = static_cast<uint32_t>(2 * (s + 1));
+              while (dep::ld_acquire(cnt) < need) __nanosleep(32);
+              dep::fence_proxy_async_global();
+              if (lane == 0) stamp(g, s, i, 0);
+              const uint32_t fb = ptx::mapa(fullk_bar(stage, lane), 0);
+              ptx::mbar_arrive_expect_tx_cluster(fb, b_bytes);
+              ptx::tma_load_2d_pair_hint(b_base + stage * Cfg::STAGE_BYTES + lane * b_bytes,
+                                         &maps.g.Gin[Cfg::cls(i)][s & 1], fb, lane * Cfg::BK, b_row0, keep);
+            }
+            __syncwarp();
+          } else {
+            dep::wait_block(args.done, PARTS * n_blk + i, 0u, static_cast<uint32_t>((s + 1) * args.num_m));
+            if (lane == 0) stamp(g, s, i, 0);
+            ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
+            if (lane == 0) stamp(g, s, i, 8);
+            if (ptx::elect_one()) {
+              const uint32_t fb = ptx::mapa(full_bar(stage), 0);
+              ptx::mbar_arrive_expect_tx_cluster(fb, KB * b_bytes);
+              ptx::tma_load_3d_pair_hint(b_base + stage * Cfg::STAGE_BYTES, &maps.g.Gin3[Cfg::cls(i)][s & 1], fb, 0,
+                                         b_row0, 0, keep);
+            }
+            __syncwarp();
           }
-          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             ph ^= 1u;
@@ -241,7 +274,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
             constexpr int i = decltype(I)::value;
             constexpr uint32_t idesc = ptx::idesc_mxf4(256, Cfg::w(i));
             ptx::mbar_wait(tempty_bar(i), (lt & 1) ^ 1u);
-            ptx::mbar_wait(full_bar(stage), ph);
+            if constexpr (!Cfg::PKB) ptx::mbar_wait(full_bar(stage), ph);
             if (lane == 0) {
               stamp(g, s, i, 6);
               stamp(g, s, i, 7);
@@ -250,12 +283,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
             if (ptx::elect_one()) {
               const uint32_t d = tmem_base + Cfg::off(i);
               const uint32_t bb = b_base + stage * Cfg::STAGE_BYTES;
-              for (int kb = 0; kb < KB; ++kb) {
+              auto kblock = [&](int kb, bool first) {
                 const uint64_t bdesc = ptx::smem_desc_k_sw128(bb + kb * (Cfg::w(i) / 2) * Cfg::BK);
                 const uint32_t a = tmem_base + Cfg::COL_J + kb * 32;
 #pragma unroll
                 for (int k = 0; k < Cfg::BK / 32; ++k)
-                  ptx::mma_mxf4_pair_ts(d, a + 8 * k, bdesc + 2 * k, idesc, sf, (kb | k) != 0);
+                  ptx::mma_mxf4_pair_ts(d, a + 8 * k, bdesc + 2 * k, idesc, sf, !(first && k == 0));
+              };
+              if constexpr (Cfg::PKB) {
+                // K blocks in the order their slabs land; the first one issued zero-initialises
+                uint32_t left = (1u << KB) - 1u;
+                bool first = true;
+                while (left) {
+                  for (int kb = 0; kb < KB; ++kb)
+                    if (((left >> kb) & 1u) && ptx::mbar_test_wait(fullk_bar(stage, kb), ph)) {
+                      ptx::tc_fence_after();
+                      kblock(kb, first);
+                      first = false;
+                      left &= ~(1u << kb);
+                    }
+                }
+              } else {
+                for (int kb = 0; kb < KB; ++kb) kblock(kb, kb == 0);
               }
               ptx::mma_commit_pair_mc(empty_bar(stage), 0x3);
               ptx::mma_commit_pair_mc(tfull_bar(i), 0x3);
@@ -316,7 +365,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
         dep::fence_proxy_async_global();
         __threadfence();
         __syncwarp();
-        if (lane == 0) dep::release_add(args.done + PARTS * n_blk + i, 1u);
+        if (lane == 0) dep::release_add(args.done + done_idx(n_blk, i), 1u);
       });
       if (lane == 0) gstamp(g, 6);
       for (int rr = lane; rr < Cfg::NR; rr += 32) {
@@ -391,7 +440,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
             stamp(g, s, k, 4);
             // red.release orders the completed (proxy-fenced) tile writes before the count
             dep::fence_proxy_async_global();
-            dep::release_add(args.done + PARTS * n_blk + k, 1u);
+            dep::release_add(args.done + done_idx(n_blk, k), 1u);
             stamp(g, s, k, 5);
             // dev skew trace (SBG_RES_GTRACE): every CTA's release time of part 0, steps 8..39 of group 0
             if (k == 0 && args.gtrace && g == args.group0 && s >= 8 && s < 40) {

@@ -522,9 +522,11 @@ def test_e2m1_resident_equals_int8(solver, n, R, variant, values, monkeypatch):
     _same(a, c)
 
 
-@pytest.mark.parametrize("n,R,variant,parts", [(2000, 8192, GDSB, "4"), (2000, 3000, DSB, "4"), (1500, 2000, GDSB, "5"),
-                                               (513, 6000, GDSB, "4"), (777, 400, DSB, "5")])
-def test_ts_kernel_equals_parts_kernel(solver, n, R, variant, parts, monkeypatch):
+@pytest.mark.parametrize("n,R,variant,parts,pkb", [(2000, 8192, GDSB, "4", "0"), (2000, 3000, DSB, "4", "0"),
+                                                   (1500, 2000, GDSB, "5", "0"), (513, 6000, GDSB, "4", "0"),
+                                                   (777, 400, DSB, "5", "0"), (2000, 8192, GDSB, "4", "1"),
+                                                   (777, 400, DSB, "5", "1")])
+def test_ts_kernel_equals_parts_kernel(solver, n, R, variant, parts, pkb, monkeypatch):
     """The TS resident kernel (J in TMEM as the A operand of tcgen05.mma [a_tmem], x, y in
     shared memory, state moved by TMA at group boundaries; the default) against the parts
     kernel (J in shared memory, x, y in TMEM; SBG_RES_TS=0): states, energies and winner
@@ -533,7 +535,9 @@ def test_ts_kernel_equals_parts_kernel(solver, n, R, variant, parts, monkeypatch
     J = _sym(n, np.array([1, -1], np.int8) if n % 2 == 0 else E2M1_INTS, n)
     arep = np.random.default_rng(n).random(R).astype(np.float32)
     monkeypatch.setenv("SBG_RES_PARTS", parts)
+    monkeypatch.setenv("SBG_RES_PKB", pkb)  # 1: per-K-block dependencies (dev variant)
     f_ts, a = _run_resident(solver, J, R, variant, 23, monkeypatch, True, arep=arep)
+    monkeypatch.delenv("SBG_RES_PKB")
     monkeypatch.setenv("SBG_RES_TS", "0")
     monkeypatch.setenv("SBG_RES_PARTS", "4")
     f_pa, b = _run_resident(solver, J, R, variant, 23, monkeypatch, True, arep=arep)
