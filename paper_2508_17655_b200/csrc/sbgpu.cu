@@ -1410,6 +1410,10 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
   k.dt = float(prm->dt);
   k.inv = 0.0f;
   CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+  if (m_end == m_begin) {  // nothing to step (engine.cpp:55-110 is never called)
+    CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+    return SBG_OK;
+  }
   if (ctx->kind == KIND_CSR_I8) {
     // replica-major -> spin-major (unless the last advance left the state there), B operand, M
     // steps (ping-pong); the state stays spin-major until something reads it (csr_sync)

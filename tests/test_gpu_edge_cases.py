@@ -123,3 +123,28 @@ def test_odd_sizes_bitwise(solver, orc, n, R):
         x, y, p = solver.get_state()
         ex, ey, ep = orc.step_f32(variant, J, x0, y0, p0, 0, 7, np.float32(1.25), np.float32(c), np.float32(0.2), 7)
         assert (x == ex).all() and (y == ey).all() and (p == ep).all(), (variant, n, R)
+
+
+@pytest.mark.parametrize("kind", ["dense_pm1", "sk", "csr"])
+def test_empty_advance_is_a_no_op(solver, orc, kind):
+    """advance(m, m) steps nothing (engine.cpp:55-110 is never called) on every kernel family,
+    including the resident kernels and the CSR path's spin-major working copies."""
+    n, R = 400, 50
+    if kind == "dense_pm1":
+        solver.set_instance(orc.gen_dense_i8(n, 3))
+    elif kind == "sk":
+        solver.set_instance(orc.gen_sk_f32(n, 3))
+    else:
+        _, csr = orc.gen_er_csr(n, 1500, 3)
+        solver.set_instance_csr(n, *csr)
+    x0, y0, p0 = orc.init_small_uniform(n, R, master=5)
+    solver.set_state(x0, y0, p0)
+    for v in (GDSB, GBSB):
+        solver.advance(cfg(v, 20, 1.25, 0.05, 0.2), 7, 7)
+    x, y, p = solver.get_state()
+    assert (x == x0).all() and (y == y0).all() and (p == p0).all()
+    solver.advance(cfg(GDSB, 20, 1.25, 0.05, 0.2), 0, 3)
+    x3, _, _ = solver.get_state()
+    solver.advance(cfg(GDSB, 20, 1.25, 0.05, 0.2), 3, 3)
+    x3b, _, _ = solver.get_state()
+    assert (x3 == x3b).all()
