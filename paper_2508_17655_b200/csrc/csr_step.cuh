@@ -26,12 +26,17 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #include "gsb_phase.cuh"
 
 namespace sbg {
 
 constexpr int CSR_THREADS = 256;
+// the gathers of the ping-pong operand: random 512 B rows with no reuse inside an SM
+#ifndef CSR_GATHER_LD
+#define CSR_GATHER_LD "ld.global.L2::cache_hint"  // L1::no_allocate measured the same (68.5 us)
+#endif
 constexpr int CSR_VEC = 1;                     // 4-replica groups per lane (more gathers in flight)
 constexpr int CSR_RCHUNK = 128 * CSR_VEC;      // replicas per warp task
 #ifndef CSR_MINB
@@ -71,7 +76,7 @@ __device__ __forceinline__ void st_f4(float* a, float4 v, uint64_t pol) {
 }
 __device__ __forceinline__ int4 ld_i4(const int32_t* a, uint64_t pol) {
   int4 v;
-  asm volatile("ld.global.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+  asm volatile(CSR_GATHER_LD ".v4.s32 {%0,%1,%2,%3}, [%4], %5;"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(a), "l"(pol));
   return v;
@@ -83,7 +88,7 @@ __device__ __forceinline__ void st_i4(int32_t* a, int4 v, uint64_t pol) {
 }
 __device__ __forceinline__ uint32_t ld_u32(const void* a, uint64_t pol) {
   uint32_t v;
-  asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  asm volatile(CSR_GATHER_LD ".u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
   return v;
 }
 __device__ __forceinline__ void st_u32(void* a, uint32_t v, uint64_t pol) {
@@ -184,6 +189,103 @@ __global__ void __launch_bounds__(CSR_THREADS, CSR_MIN_BLOCKS)
         l2::st_i4(static_cast<int32_t*>(g_next) + off,
                   make_int4(quant30(x4.x), quant30(x4.y), quant30(x4.z), quant30(x4.w)), keep);
       }
+    }
+  }
+}
+
+// The register-path step with the gather loop software-pipelined by one: the load of nonzero
+// k + 1 is issued before the accumulate of nonzero k, so every warp keeps two gathers in
+// flight (the plain loop issues the next load only after the previous one's accumulate has
+// waited for it). Four more registers per thread; MINB blocks of 256 threads per SM. Dev
+// variant (SBG_CSR_PF=6/7), bitwise equal, measured slower at C3: 84.3 (6 blocks, 40 regs) /
+// 91.7 (7 blocks, 32 regs + spills) vs 68.1 us/step -- like every other way of putting more
+// gathers in flight (unroll, cp.async batches).
+template <bool SIGN, int MINB>
+__global__ void __launch_bounds__(CSR_THREADS, MINB)
+    csr_step_pf_kernel(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                       const int8_t* __restrict__ val, const void* __restrict__ g_cur, void* __restrict__ g_next,
+                       float* __restrict__ xs, float* __restrict__ ys, float* __restrict__ ps, int64_t rp,
+                       int32_t R, PhaseConsts k, const float* __restrict__ a_rep = nullptr) {
+  const int lane = threadIdx.x & 31;
+  const int chunks = static_cast<int>((R + CSR_RCHUNK - 1) / CSR_RCHUNK);
+  const int64_t tasks = static_cast<int64_t>(n) * chunks;
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t stream = l2::evict_first(), keep = l2::evict_last();
+  const uint32_t rsb = static_cast<uint32_t>(rp) * (SIGN ? 1u : 4u);
+  using G = std::conditional_t<SIGN, uint32_t, int4>;
+  auto gather = [&](const char* src) -> G {
+    if constexpr (SIGN)
+      return l2::ld_u32(src, keep);
+    else
+      return l2::ld_i4(reinterpret_cast<const int32_t*>(src), keep);
+  };
+  for (int64_t t = wid; t < tasks; t += nw) {
+    const int i = static_cast<int>(t / chunks);
+    const int rc = static_cast<int>(t % chunks) * CSR_RCHUNK + 4 * lane;
+    const int kb = rowptr[i], ke = rowptr[i + 1];
+    const char* gb = static_cast<const char*>(g_cur) + static_cast<size_t>(rc) * (SIGN ? 1 : 4);
+    long long acc[4] = {0, 0, 0, 0};
+    for (int k0 = kb; k0 < ke; k0 += 32) {
+      const int cnt = min(32, ke - k0);
+      int jl = 0, vl = 0;
+      if (lane < cnt) {
+        jl = col[k0 + lane];
+        vl = val[k0 + lane];
+      }
+      G nxt = gather(gb + static_cast<uint64_t>(static_cast<uint32_t>(__shfl_sync(0xffffffffu, jl, 0))) * rsb);
+#pragma unroll 1
+      for (int kk = 0; kk < cnt; ++kk) {
+        const G cur = nxt;
+        const int jn = __shfl_sync(0xffffffffu, jl, kk + 1 < cnt ? kk + 1 : kk);
+        if (kk + 1 < cnt) nxt = gather(gb + static_cast<uint64_t>(static_cast<uint32_t>(jn)) * rsb);
+        const long long v = __shfl_sync(0xffffffffu, vl, kk);
+        if constexpr (SIGN) {
+          const char4 sg = *reinterpret_cast<const char4*>(&cur);
+          acc[0] += v * sg.x;
+          acc[1] += v * sg.y;
+          acc[2] += v * sg.z;
+          acc[3] += v * sg.w;
+        } else {
+          acc[0] += v * cur.x;
+          acc[1] += v * cur.y;
+          acc[2] += v * cur.z;
+          acc[3] += v * cur.w;
+        }
+      }
+    }
+    const int r = rc;
+    if (r >= R) continue;
+    const size_t off = static_cast<size_t>(i) * rp + r;
+    float4 x4 = l2::ld_f4(xs + off, stream);
+    float4 y4 = l2::ld_f4(ys + off, stream);
+    float4 p4 = l2::ld_f4(ps + off, stream);
+    float F[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      F[e] = SIGN ? static_cast<float>(acc[e]) : __fmul_rn(__ll2float_rn(acc[e]), 0x1p-30f);
+    PhaseConsts kk4[4] = {k, k, k, k};
+    if (a_rep) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) kk4[e].a = a_rep[min(r + e, R - 1)];
+    }
+    gsb_phase(F[0], x4.x, y4.x, p4.x, kk4[0]);
+    gsb_phase(F[1], x4.y, y4.y, p4.y, kk4[1]);
+    gsb_phase(F[2], x4.z, y4.z, p4.z, kk4[2]);
+    gsb_phase(F[3], x4.w, y4.w, p4.w, kk4[3]);
+    l2::st_f4(xs + off, x4, stream);
+    l2::st_f4(ys + off, y4, stream);
+    l2::st_f4(ps + off, p4, stream);
+    if (SIGN) {
+      char4 sg;
+      sg.x = sgn8(x4.x);
+      sg.y = sgn8(x4.y);
+      sg.z = sgn8(x4.z);
+      sg.w = sgn8(x4.w);
+      l2::st_u32(static_cast<int8_t*>(g_next) + off, *reinterpret_cast<uint32_t*>(&sg), keep);
+    } else {
+      l2::st_i4(static_cast<int32_t*>(g_next) + off,
+                make_int4(quant30(x4.x), quant30(x4.y), quant30(x4.z), quant30(x4.w)), keep);
     }
   }
 }

@@ -1496,6 +1496,19 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
           }
 #undef CSRA_CASE
           CK(e);
+        } else if (const int pf = dev_knob("SBG_CSR_PF"); pf == 6 || pf == 7) {
+          // dev: gather loop pipelined by one (two gathers in flight per warp), pf blocks per SM
+          const int pblocks = int(std::min<int64_t>((tasks + CSR_THREADS / 32 - 1) / (CSR_THREADS / 32),
+                                                    int64_t(ctx->sms) * pf));
+#define CSR_PF(S, B) \
+  csr_step_pf_kernel<S, B><<<pblocks, CSR_THREADS, 0, ctx->stream>>>(n32, ctx->d_rowptr, ctx->d_col, ctx->d_val, \
+                                                                   gq[cur], gn, xs, ys, ps, ctx->rp, Rs, km, ar)
+          if (sign) {
+            if (pf == 6) CSR_PF(true, 6); else CSR_PF(true, 7);
+          } else {
+            if (pf == 6) CSR_PF(false, 6); else CSR_PF(false, 7);
+          }
+#undef CSR_PF
         } else if (sign)
           csr_step_sm_kernel<true><<<blocks, CSR_THREADS, 0, ctx->stream>>>(
               n32, ctx->d_rowptr, ctx->d_col, ctx->d_val, gq[cur], gn, xs, ys, ps, ctx->rp, Rs, km, ar);

@@ -210,7 +210,8 @@ def test_csr_equals_dense_and_mirror(solver, orc):
 
 @pytest.mark.parametrize("knobs", [{"SBG_CSR_SLAB": "128"}, {"SBG_CSR_SLAB": "256"}, {"SBG_CSR_ASYNC": "4"},
                                    {"SBG_CSR_ASYNC": "8"}, {"SBG_CSR_ASYNC": "12"}, {"SBG_CSR_ASYNC": "16"},
-                                   {"SBG_CSR_ASYNC": "8", "SBG_CSR_SLAB": "128"}])
+                                   {"SBG_CSR_ASYNC": "8", "SBG_CSR_SLAB": "128"}, {"SBG_CSR_PF": "6"},
+                                   {"SBG_CSR_PF": "7"}])
 def test_csr_kernel_variants_bitwise(solver, orc, monkeypatch, knobs):
     """CSR step variants equal the default kernel bitwise, per-replica A included: replica slabs
     stepped from L2 (SBG_CSR_SLAB; ragged last slab, 300 = 128+128+44) and the cp.async-staged
