@@ -230,6 +230,8 @@ def run_reference(args):
     oracle.build()
     total = args.steps + args.warmup
     budget = max(0.5, min(5.0, 150.0 / max(total, 1)))
+    if os.environ.get("SBG_BENCH_REF_BUDGET"):  # tests: a shorter sample per timed step
+        budget = float(os.environ["SBG_BENCH_REF_BUDGET"])
     vals = []
     threads, sample = 0, ""
     for it in range(total):
