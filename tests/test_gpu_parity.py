@@ -356,6 +356,30 @@ def test_dt_sweep_grid_matches_mirror_per_cell(solver, orc):
         assert (cl.energies == -0.5 * orc.energy2_i8(J, x)).all(), (cl.di, cl.ti)
 
 
+@pytest.mark.parametrize("n,R,variant", [(2000, 3000, GDSB), (600, 700, GBSB), (300, 1, DSB)])
+def test_run_best_returns_the_batch_best_of_winner(solver, orc, n, R, variant):
+    """sbg_run_best (batch_best_of's result, bench.cpp:70-92): the winner's spins, energy and
+    index (ties -> lowest replica) and the R energies equal a full run_batch readout of the
+    same host initial states, and the winner's spins are sgn of its final x (sgn(0) = +1)."""
+    from paper_2508_17655_b200 import SolverConfig, TuningResult, Variant
+
+    J = orc.gen_dense_i8(n, 12)
+    solver.set_instance(J)
+    x0, y0, _ = orc.init_small_uniform(n, R, master=6)
+    c = 1 / (2 * np.sqrt(n))
+    cfg = SolverConfig(variant=Variant(variant), steps=40, dt=1.25, c=c, a=0.2)
+    t = TuningResult(c=c, dt=1.25)
+    spins, be, bi, energies, timing = solver.run_best(cfg, t, x0, y0)
+    b = solver.run_batch(cfg, t, R, x0=x0, y0=y0, want_x=True)
+    assert (energies == b.energies).all()
+    assert bi == b.best_index == int(np.flatnonzero(b.energies == b.energies.min())[0])
+    assert be == b.energies[bi]
+    assert (spins == b.spins[bi]).all()
+    assert (spins == np.where(b.x_final[bi] >= 0, 1, -1)).all()
+    _, e_only, bi2, none, _ = solver.run_best(cfg, t, x0, y0, want_energies=False)
+    assert none is None and bi2 == bi and e_only == be
+
+
 def test_csr_chunked_advances_keep_state_spin_major(solver, orc):
     """CSR advances leave the state in the spin-major working copies and the next advance
     continues from there; readers (get_state, readout) bring the replica-major copy up to date.
