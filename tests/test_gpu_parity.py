@@ -570,6 +570,20 @@ def test_ts_kernel_equals_parts_kernel(solver, n, R, variant, parts, pkb, monkey
     _same(a, b)
 
 
+@pytest.mark.parametrize("n,R", [(2000, 1440), (2000, 1441), (2048, 160), (2048, 159), (256, 1), (256, 11840),
+                                 (255, 300), (1793, 2881)])
+def test_ts_kernel_edge_geometries_equal_streaming(solver, n, R, monkeypatch):
+    """The TS resident kernel at group / block / padding boundaries (exactly one group of 9
+    blocks, one replica past it, one block, npad = 256 with one CTA pair per block and 74
+    blocks per group, odd n) against the streaming kernel (SBG_RESIDENT=0): bitwise."""
+    J = _sym(n, np.array([1, -1], np.int8), n + R)
+    arep = np.random.default_rng(R).random(R).astype(np.float32)
+    f_ts, a = _run_resident(solver, J, R, GDSB, 9, monkeypatch, True, arep=arep)
+    _, b = _run_resident(solver, J, R, GDSB, 9, monkeypatch, True, resident="0", arep=arep)
+    assert f_ts == "e2m1"
+    _same(a, b)
+
+
 def test_e2m1_streaming_large_n(solver, monkeypatch):
     """Past the resident kernel's size limit the streaming pair kernel runs on e2m1 operands
     (single-buffered accumulator, nibble-packed G written by the epilogue): bitwise equal to
