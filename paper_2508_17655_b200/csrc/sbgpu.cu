@@ -400,18 +400,18 @@ int resident_nr(const sbg_ctx* ctx) {
 }
 
 template <int EPI, int CH, int ST = RES_STAGES, int NR = 128, bool Q4 = false, int PARTS = 0, bool JRES = false,
-          class Maps = TmaMaps, bool PKB = false>
+          class Maps = TmaMaps, bool PKB = false, bool KH2 = false>
 int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int group0 = 0, int ngroups = -1,
                     const uint32_t* ready = nullptr) {
   // PARTS > 0: step_resident_parts.cuh (e2m1, 160-replica blocks as PARTS interleaved column
   // parts; JRES = J resident in shared memory); else step_resident.cuh
   // PARTS < 0: step_resident_ts.cuh with -PARTS parts (J in TMEM, x, y in shared memory)
   using Cfg = std::conditional_t<
-      (PARTS < 0), TsCfg<ST, (PARTS < 0 ? -PARTS : 2), PKB>,
+      (PARTS < 0), TsCfg<ST, (PARTS < 0 ? -PARTS : 2), PKB, KH2>,
       std::conditional_t<(PARTS > 0), PartsCfg<ST, JRES, (PARTS > 0 ? PARTS : 2)>, ResCfg<ST, EPI, CH, NR, false, Q4>>>;
   auto kern = [] {
     if constexpr (PARTS < 0)
-      return gsb_resident_ts_kernel<ST, -PARTS, PKB>;
+      return gsb_resident_ts_kernel<ST, -PARTS, PKB, KH2>;
     else if constexpr (PARTS > 0)
       return gsb_resident_parts_kernel<ST, JRES, PARTS>;
     else
@@ -1911,12 +1911,28 @@ static int encode_part_maps(sbg_ctx* ctx, PartMaps* pm, int cur, int w0, int w1)
 extern "C++" {
 // The TS kernel (J in TMEM, x, y in shared memory): the parts kernel's G maps plus 2D boxes
 // {128 spins, 160 replicas} of the replica-major x and y (rows >= rpad read as zero).
-template <int PARTS, int ST, bool PKB>
+template <int PARTS, int ST, bool PKB, bool KH2 = false>
 int launch_ts(sbg_ctx* ctx, int cur, const MultiStepArgs& a, int groups, const uint32_t* ready) {
   using T = PartTable<PARTS>;
   TsMaps tm;
   int rc = encode_part_maps(ctx, &tm.g, cur, T::W[0], T::W[PARTS - 1]);
   if (rc) return rc;
+  if (KH2) {  // the 3D G view with box depth KB / 2
+    auto enc = get_encode();
+    const uint64_t gb = uint64_t(ctx->npad / 2);
+    const uint32_t kh = uint32_t(ctx->npad / 512);
+    const int ws2[2] = {T::W[0], T::W[PARTS - 1]};
+    for (int c = 0; c < 2; ++c)
+      for (int par = 0; par < 2; ++par) {
+        cuuint64_t dims[3] = {128, cuuint64_t(ctx->rpad), cuuint64_t(gb / 128)};
+        cuuint64_t strides[2] = {cuuint64_t(gb), 128};
+        cuuint32_t box[3] = {128, uint32_t(ws2[c] / 2), kh}, es[3] = {1, 1, 1};
+        if (enc(&tm.Gin3h[c][par], CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, ctx->dG[cur ^ par], dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+          return ctx->fail(SBG_ERR_CUDA, "cuTensorMapEncodeTiled (3D G halves) failed");
+      }
+  }
   const int ws[2] = {T::W[0], T::W[PARTS - 1]};
   for (int c = 0; c < 2 && !rc; ++c) {
     rc = encode_2d(ctx, &tm.X[c], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ctx->dX, uint64_t(ctx->npad),
@@ -1927,7 +1943,7 @@ int launch_ts(sbg_ctx* ctx, int cur, const MultiStepArgs& a, int groups, const u
   }
   if (rc) return rc;
   if (a.nsteps < 1) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "resident launch without steps");
-  return launch_resident<16, 4, ST, RES_NR, true, -PARTS, true, TsMaps, PKB>(ctx, tm, a, 0, groups, ready);
+  return launch_resident<16, 4, ST, RES_NR, true, -PARTS, true, TsMaps, PKB, KH2>(ctx, tm, a, 0, groups, ready);
 }
 
 template <int PARTS, int ST, bool JRES>
@@ -1963,6 +1979,9 @@ static int launch_resident_default(sbg_ctx* ctx, int cur, const MultiStepArgs& a
         const bool pkb = dev_knob("SBG_RES_PKB") == 1;
         if (dev_knob("SBG_RES_PARTS") == 5)
           return pkb ? launch_ts<5, 3, true>(ctx, cur, a, groups, ready) : launch_ts<5, 3, false>(ctx, cur, a, groups, ready);
+        // SBG_RES_KH2=1: each part-step's G in two halves (MMAs on the first while the second lands)
+        if (!pkb && dev_knob("SBG_RES_KH2") == 1 && (ctx->npad / 256) % 2 == 0)
+          return launch_ts<4, 2, false, true>(ctx, cur, a, groups, ready);
         return pkb ? launch_ts<4, 2, true>(ctx, cur, a, groups, ready) : launch_ts<4, 2, false>(ctx, cur, a, groups, ready);
       }
       switch (dev_knob("SBG_RES_PARTS")) {

@@ -57,6 +57,7 @@ __device__ __forceinline__ void sts_f32(uint32_t a, float v) {
 // Tensor maps of the TS kernel: the parts kernel's G maps plus the state boxes.
 struct TsMaps {
   PartMaps g;
+  CUtensorMap Gin3h[2][2];  // KH2: the 3D G view with box depth KB / 2 (a part-step's G in two halves)
   CUtensorMap X[2], Y[2];  // f32 [rpad][npad], box {128 spins, part width} per width class
 };
 
@@ -65,9 +66,12 @@ struct TsMaps {
 // K blocks' MMAs in the order they land (exact integer sums: any order gives the same field),
 // so a part's MMAs overlap the wait for the slowest of the 16 producer CTAs instead of
 // starting after it.
-template <int STAGES_, int PARTS_, bool PKB_ = false>
+// KH2_: a part-step's G operand in two 3D loads (K blocks [0, KB/2) and [KB/2, KB)) on two
+// barriers, so the first half's MMAs run while the second half is in flight.
+template <int STAGES_, int PARTS_, bool PKB_ = false, bool KH2_ = false>
 struct TsCfg {
   static constexpr bool PKB = PKB_;
+  static constexpr bool KH2 = KH2_;
   static constexpr int PARTS = PARTS_;
   using T = PartTable<PARTS>;
   __host__ __device__ static constexpr int w(int i) { return T::W[i]; }
@@ -85,19 +89,20 @@ struct TsCfg {
   static constexpr int XY_BYTES = NR * BM * 4;     // 80 KB each
   static constexpr int T_BYTES = NR * BM / 2;      // G tiles of all parts: [160][64] bytes
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
-  static constexpr int NUM_BARS = 2 * STAGES + 5 * PARTS + (PKB ? STAGES * KB_MAX : 0);
+  static constexpr int NUM_BARS = 2 * STAGES + 5 * PARTS + (PKB ? STAGES * KB_MAX : 0) + (KH2 ? STAGES : 0);
   static constexpr int SMEM_BYTES = 2 * XY_BYTES + STAGES * STAGE_BYTES + T_BYTES + 1024 + 8 * NUM_BARS + 64;
   static constexpr uint32_t COL_J = NR, COL_SF = 512 - 16;
   static_assert(off(PARTS - 1) + w(PARTS - 1) == NR, "parts cover the block");
   static_assert(COL_J + 32 * KB_MAX <= COL_SF, "TMEM columns");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static_assert(STAGE_BYTES % 1024 == 0 && XY_BYTES % 1024 == 0, "alignment");
+  static_assert(!(PKB && KH2), "one G load scheme");
 };
 
-template <int STAGES_, int PARTS_, bool PKB_>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS_, PKB_>::THREADS, 1)
+template <int STAGES_, int PARTS_, bool PKB_, bool KH2_>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS_, PKB_, KH2_>::THREADS, 1)
     gsb_resident_ts_kernel(const __grid_constant__ TsMaps maps, const ResidentArgs args) {
-  using Cfg = TsCfg<STAGES_, PARTS_, PKB_>;
+  using Cfg = TsCfg<STAGES_, PARTS_, PKB_, KH2_>;
   constexpr int CH = Cfg::CH;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int PARTS = Cfg::PARTS;
@@ -122,6 +127,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
   auto gempty_bar = [&](int i) { return bar(2 * STAGES + 3 * PARTS + i); };
   auto sfull_bar = [&](int i) { return bar(2 * STAGES + 4 * PARTS + i); };  // part i's x, y landed (TMA)
   auto fullk_bar = [&](int st, int kb) { return bar(2 * STAGES + 5 * PARTS + st * Cfg::KB_MAX + kb); };  // PKB
+  auto full2_bar = [&](int st) { return bar(2 * STAGES + 5 * PARTS + st); };  // KH2: second half (first: full_bar)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -152,6 +158,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
     if constexpr (Cfg::PKB)
       for (int st = 0; st < STAGES; ++st)
         for (int kb = 0; kb < Cfg::KB_MAX; ++kb) ptx::mbar_init(fullk_bar(st, kb), 2);
+    if constexpr (Cfg::KH2)
+      for (int st = 0; st < STAGES; ++st) ptx::mbar_init(full2_bar(st), 2);
     ptx::fence_mbar_init();
     *started = 0;
   }
@@ -247,9 +255,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
             if (lane == 0) stamp(g, s, i, 8);
             if (ptx::elect_one()) {
               const uint32_t fb = ptx::mapa(full_bar(stage), 0);
-              ptx::mbar_arrive_expect_tx_cluster(fb, KB * b_bytes);
-              ptx::tma_load_3d_pair_hint(b_base + stage * Cfg::STAGE_BYTES, &maps.g.Gin3[Cfg::cls(i)][s & 1], fb, 0,
-                                         b_row0, 0, keep);
+              if constexpr (Cfg::KH2) {
+                const int kh = KB / 2;
+                const uint32_t fb2 = ptx::mapa(full2_bar(stage), 0);
+                ptx::mbar_arrive_expect_tx_cluster(fb, kh * b_bytes);
+                ptx::tma_load_3d_pair_hint(b_base + stage * Cfg::STAGE_BYTES, &maps.Gin3h[Cfg::cls(i)][s & 1], fb, 0,
+                                           b_row0, 0, keep);
+                ptx::mbar_arrive_expect_tx_cluster(fb2, kh * b_bytes);
+                ptx::tma_load_3d_pair_hint(b_base + stage * Cfg::STAGE_BYTES + kh * b_bytes,
+                                           &maps.Gin3h[Cfg::cls(i)][s & 1], fb2, 0, b_row0, kh, keep);
+              } else {
+                ptx::mbar_arrive_expect_tx_cluster(fb, KB * b_bytes);
+                ptx::tma_load_3d_pair_hint(b_base + stage * Cfg::STAGE_BYTES, &maps.g.Gin3[Cfg::cls(i)][s & 1], fb,
+                                           0, b_row0, 0, keep);
+              }
             }
             __syncwarp();
           }
@@ -303,6 +322,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
                       left &= ~(1u << kb);
                     }
                 }
+              } else if constexpr (Cfg::KH2) {
+                for (int kb = 0; kb < KB / 2; ++kb) kblock(kb, kb == 0);
+                ptx::mbar_wait(full2_bar(stage), ph);  // the second half of the part-step's G
+                ptx::tc_fence_after();
+                for (int kb = KB / 2; kb < KB; ++kb) kblock(kb, false);
               } else {
                 for (int kb = 0; kb < KB; ++kb) kblock(kb, kb == 0);
               }
