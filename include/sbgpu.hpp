@@ -282,6 +282,30 @@ class Solver {
     return std::move(all[last_best_]);
   }
 
+  // batch_best_of from host initial states (x0, y0: R x n, replica-major) in one device pass
+  // (sbg_run_best): only the winner -- its spins, energy and index (ties to the lowest
+  // replica, bench.cpp:84-87) -- crosses back to the host. best_index receives the index.
+  RunResult batch_best_of_states(const SolverConfig& cfg, const TuningResult& tuning, std::size_t R,
+                                 const std::vector<float>& x0, const std::vector<float>& y0,
+                                 std::size_t* best_index = nullptr) {
+    if (R < 1) throw std::invalid_argument("batch size must be >= 1");
+    if (x0.size() != R * n_ || y0.size() != R * n_) throw std::invalid_argument("initial state size mismatch");
+    const SolverConfig rc = resolve_config(cfg, tuning);
+    const sbg_params prm = params(rc);
+    RunResult res;
+    res.final_spins.resize(n_);
+    std::int64_t best = 0;
+    sbg_timing timing{};
+    check(sbg_run_best(ctx_, &prm, static_cast<std::int64_t>(R), x0.data(), y0.data(), res.final_spins.data(),
+                       &res.energy, &best, nullptr, &timing));
+    if (total_weight_) res.cut = (*total_weight_ - static_cast<long long>(res.energy)) / 2;
+    res.wall_time_s = timing.total_ms / 1e3;
+    res.config_echo = rc;
+    res.tuning_echo = tuning;
+    if (best_index) *best_index = static_cast<std::size_t>(best);
+    return res;
+  }
+
   std::size_t n() const noexcept { return n_; }
   sbg_ctx* handle() noexcept { return ctx_; }
 

@@ -8,6 +8,10 @@
 
 #include "sbgpu.hpp"
 
+static void check_rc(int rc) {
+  if (rc != 0) throw std::runtime_error("sbgpu call failed");
+}
+
 int main(int argc, char** argv) {
   const std::size_t n = 64, R = 8;
   std::vector<double> J(n * n, 0.0);
@@ -43,6 +47,17 @@ int main(int argc, char** argv) {
   cfg.init_mode = sbgpu::InitMode::small_uniform;
   auto batch = s.run_batch(cfg, tuning, R, 7, sbgpu::seed_stream::gpu_init);
   auto best = s.batch_best_of(cfg, tuning, R, 7);
+  // the same batch from host initial states: (x0, y0) = the device init read back
+  std::vector<float> x0(R * n), y0(R * n);
+  {
+    sbgpu::Solver t(0);
+    t.set_instance(n, J);
+    check_rc(sbg_init_state(t.handle(), static_cast<std::int64_t>(R), SBG_INIT_SMALL_UNIFORM, 7,
+                            sbgpu::seed_stream::gpu_init, 0));
+    check_rc(sbg_get_state(t.handle(), x0.data(), y0.data(), nullptr));
+  }
+  std::size_t best_idx = 0;
+  auto best_states = s.batch_best_of_states(cfg, tuning, R, x0, y0, &best_idx);
   std::vector<double> energies;
   for (auto& r : batch) energies.push_back(r.energy);
   const auto st = sbgpu::success_probability(energies, best.energy);
@@ -63,9 +78,11 @@ int main(int argc, char** argv) {
   for (std::size_t r = 0; r < R; ++r) std::printf("%s%lld", r ? ", " : "", *batch[r].cut);
   std::printf("], \"best_energy\": %.1f, \"best_seed\": %llu, \"p_s\": %.17g, \"tts_mid\": %.17g, \"invalid_caught\": %d,"
               " \"convergence_caught\": %d, \"lambda_max\": %.17g, \"lambda_min\": %.17g, \"iterations\": %zu,"
-              " \"wigner_c\": %.17g}\n",
+              " \"wigner_c\": %.17g, \"states_best_energy\": %.1f, \"states_best_index\": %zu,"
+              " \"states_best_spins_match\": %d}\n",
               best.energy, static_cast<unsigned long long>(best.config_echo.seed), st.p_s, tts.tts_s, invalid_caught,
-              convergence_caught, est.lambda_max, est.lambda_min, est.iterations, tw.c);
+              convergence_caught, est.lambda_max, est.lambda_min, est.iterations, tw.c, best_states.energy, best_idx,
+              best_states.final_spins == batch[best_idx].final_spins ? 1 : 0);
   (void)argc;
   (void)argv;
   return 0;

@@ -53,6 +53,10 @@ def test_cpp_api_matches_oracle(tmp_path, orc):
     assert out["cuts"] == [int((W - v) // 2) for v in e]
     assert abs(out["tts_mid"] - 6.6439) < 1e-3
     assert out["wigner_c"] == out["c"]
+    # batch_best_of from host initial states (sbg_run_best): the same winner, spins included
+    bi = int(np.flatnonzero(e == e.min())[0])
+    assert out["states_best_index"] == bi and out["states_best_energy"] == e[bi]
+    assert out["states_best_spins_match"] == 1
     if oracle.ref_available():  # device power iteration == the reference's, bitwise
         rc, want, _, _ = oracle.ref().extreme_eigenvalues(J.astype(np.float64), 1e-6, 100000)
         assert rc == 0 and (out["lambda_max"], out["lambda_min"], out["iterations"]) == (
