@@ -489,27 +489,30 @@ void orc_step_f32_fx(int variant, int64_t n, const uint8_t* planes, int shift, i
     if (is_sign_variant(variant)) {
       for (int64_t j = 0; j < n; ++j) qb[j] = xr[j] >= 0.0f ? 1 : -1;
     } else {
+      /* q = rint(x 2^30) as four SIGNED base-256 digits, the GPU's qdigits (gsb_phase.cuh) */
       for (int64_t j = 0; j < n; ++j) {
-        const uint32_t q = (uint32_t)quant30(xr[j]);
-        for (int b = 0; b < 4; ++b) {
-          const uint8_t byte = (uint8_t)(q >> (8 * b));
-          qb[b * n + j] = b == 3 ? (int64_t)(int8_t)byte : (int64_t)byte;
-        }
+        const uint32_t u = (uint32_t)(quant30(xr[j]) + 0x00808080) ^ 0x00808080u;
+        for (int b = 0; b < 4; ++b) qb[b * n + j] = (int64_t)(int8_t)(uint8_t)(u >> (8 * b));
       }
     }
     const int nb = is_sign_variant(variant) ? 1 : 4;
     const int nw = 3 + nb - 1;
+    /* continuous variants: the plane products of weight 2^(8w), w = a + b < 2 (J's two low
+     * bytes times q's two low digits, < 2^-27 of the field) are not formed (step_tma.cuh,
+     * FX_W0): 9 of the 12 products */
+    const int w0 = is_sign_variant(variant) ? 0 : 2;
     const int e0 = is_sign_variant(variant) ? -shift : -(shift + 30);
     for (int64_t i = 0; i < n; ++i) {
       int64_t acc[6] = {0, 0, 0, 0, 0, 0};
       for (int pa = 0; pa < 3; ++pa)
         for (int b = 0; b < nb; ++b) {
+          if (pa + b < w0) continue;
           int64_t t = 0;
           for (int64_t j = 0; j < n; ++j) t += jplane(planes, n, pa, i, j) * qb[b * n + j];
           acc[pa + b] += t;
         }
       double f = 0.0;
-      for (int w = 0; w < nw; ++w) f = f + (double)acc[w] * ldexp(1.0, 8 * w + e0);
+      for (int w = w0; w < nw; ++w) f = f + (double)acc[w] * ldexp(1.0, 8 * w + e0);
       F[i] = (float)f;
     }
     for (int64_t i = 0; i < n; ++i) orc_phase_f32(F[i], xr + i, y + r * ld + i, p + r * ld + i, a, c, dt, inv);

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsbgpu.so")
+LIB_PATH = os.environ.get("SBG_LIB_OVERRIDE") or os.path.join(HERE, "libsbgpu.so")  # dev A/B builds
 
 SBG_OK, SBG_ERR_INVALID_ARGUMENT, SBG_ERR_OUT_OF_MEMORY, SBG_ERR_CUDA, SBG_ERR_NCCL, SBG_ERR_STATE, \
     SBG_ERR_UNSUPPORTED, SBG_ERR_CONVERGENCE = range(8)

@@ -31,6 +31,10 @@
 #include "step_resident_parts.cuh"
 #include "step_tma.cuh"
 
+#ifndef SBG_TS_LD1
+#define SBG_TS_LD1 0  // 1: one TMEM load + wait per part-step (measured the same, 26.6 us; spills 36 B)
+#endif
+
 namespace sbg {
 
 namespace ptx {
@@ -546,7 +550,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
           constexpr int i = decltype(I)::value;
           constexpr int CHUNKS = Cfg::w(i) / 16;
           const int c0 = Cfg::off(i) + cg * (Cfg::w(i) / 4);
-          uint32_t bf[2][CH];
           float bx[2][CH], by[2][CH];
           auto ld_xy = [&](int c, int b) {
 #pragma unroll
@@ -562,17 +565,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
           ptx::tc_fence_after();
           if (io && i == 0 && s < 2) gstamp(g, 2 + s);
           if (io) stamp(g, s, i, 1);
+#if SBG_TS_LD1
+          // this warp's whole slice of the part's field (W/4 columns) in one or two tcgen05.ld
+          // and ONE wait: the per-chunk load-wait round trips (~0.2 us each under the MMAs'
+          // TMEM traffic) were most of the epilogue's time
+          constexpr int NC = Cfg::w(i) / 4;
+          uint32_t fv[NC];
+          if constexpr (NC == 12) {
+            ptx::tmem_ld<8>(t_lane + c0, *reinterpret_cast<uint32_t(*)[8]>(&fv[0]));
+            ptx::tmem_ld<4>(t_lane + c0 + 8, *reinterpret_cast<uint32_t(*)[4]>(&fv[8]));
+          } else if constexpr (NC == 8) {
+            ptx::tmem_ld<8>(t_lane + c0, *reinterpret_cast<uint32_t(*)[8]>(&fv[0]));
+          } else {
+            static_assert(NC == 8 || NC == 12, "part widths 48 / 32");
+          }
+          ptx::mbar_wait(gempty_bar(i), (pc & 1) ^ 1u);  // this part's G tile stored (under the load)
+          if (io) stamp(g, s, i, 10);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < NC; ++j) asm volatile("" : "+r"(fv[j]));
+          if (io) stamp(g, s, i, 11);
+          auto fld = [&](int c, int j) { return __uint_as_float(fv[c * CH + j]); };
+#else
+          uint32_t bf[2][CH];
           ptx::tmem_ld<CH>(t_lane + c0, bf[0]);
           ptx::mbar_wait(gempty_bar(i), (pc & 1) ^ 1u);  // this part's G tile stored (under the load)
           if (io) stamp(g, s, i, 10);
           ptx::tmem_ld_wait();
           if (io) stamp(g, s, i, 11);
+          auto fld = [&](int c, int j) { return __uint_as_float(bf[c & 1][j]); };
+#endif
           auto chunks = [&](auto has_arep) {
             static_for<0, CHUNKS>([&](auto C) {
               constexpr int c = decltype(C)::value;
               constexpr int b = c & 1;
               if constexpr (c + 1 < CHUNKS) {
+#if !SBG_TS_LD1
                 ptx::tmem_ld<CH>(t_lane + c0 + (c + 1) * CH, bf[b ^ 1]);
+#endif
                 ld_xy(c + 1, b ^ 1);
               }
               const int col = c0 + c * CH;
@@ -587,18 +617,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
                   const int r = n_blk * Cfg::NR + col + j;
                   a2 = f2::pk(arep[min(r, args.R - 1)], arep[min(r + 1, args.R - 1)]);
                 }
-                gsb_phase2(__uint_as_float(bf[b][j]), __uint_as_float(bf[b][j + 1]), x0, x1, y0, y1, p0, p1, k2, a2);
+                gsb_phase2(fld(c, j), fld(c, j + 1), x0, x1, y0, y1, p0, p1, k2, a2);
                 ptx::sts_f32(xa(col + j), x0);
                 ptx::sts_f32(xa(col + j + 1), x1);
                 ptx::sts_f32(ya(col + j), y0);
                 ptx::sts_f32(ya(col + j + 1), y1);
                 put_g2(col + j, x0, x1);
               }
+#if !SBG_TS_LD1
               if constexpr (c + 1 < CHUNKS) {
                 ptx::tmem_ld_wait();
 #pragma unroll
                 for (int j = 0; j < CH; ++j) asm volatile("" : "+r"(bf[b ^ 1][j]));
               }
+#endif
             });
           };
           if (arep)

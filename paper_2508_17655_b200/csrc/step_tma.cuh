@@ -49,6 +49,10 @@ struct TmaStepCfg {
   static constexpr int BK = 128;
   static constexpr int NA = NA_;                        // J byte planes (1: int8 J; 3: fixed-point real J)
   static constexpr int NW = NA + NPLANES - 1;           // distinct plane weights 2^(8(a+b))
+  // fixed-point real J with continuous x: the products of weight w = a + b < W0 (J's two low
+  // bytes times q's two low digits: < 2^-27 of the field, below its fp32 rounding) are not
+  // formed: 9 of the 12 plane products; accumulator k holds weight W0 + k
+  static constexpr int W0 = (NA > 1 && NPLANES == 4) ? 2 : 0;
   static constexpr int A_BYTES = BM * BK;               // one J plane tile
   static constexpr int B_PLANE_BYTES = BN * BK;
   static constexpr int STAGE_BYTES = NA * A_BYTES + NPLANES * B_PLANE_BYTES;
@@ -61,7 +65,7 @@ struct TmaStepCfg {
   static constexpr int ST_G = CW * BM;                  // one byte plane chunk: 2 KB
   static constexpr int BUF_RAW = 3 * ST_ARR + NPLANES * ST_G;
   static constexpr int BUF_BYTES = (BUF_RAW + 1023) / 1024 * 1024;
-  static constexpr int ACC_COLS = NW * BN;              // one accumulator per plane weight
+  static constexpr int ACC_COLS = (NW - W0) * BN;       // one accumulator per formed plane weight
   // accumulator buffers: 2 when they fit TMEM, else 1 (the epilogue then drains all of a
   // tile's accumulator columns first and releases them before its state chunks)
   static constexpr int ABUF = 2 * ACC_COLS <= 512 ? 2 : 1;
@@ -133,9 +137,26 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 }
 // Block until `need` tiles of replica block n are complete, then order the
 // caller's subsequent async-proxy (TMA) reads after that observation.
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+#ifndef SBG_POLL
+#define SBG_POLL 0  // 0: ld.acquire + 32 ns sleep per poll; 1: relaxed spin, then one acquire; 2: acquire spin
+#endif
 __device__ __forceinline__ void wait_block(const uint32_t* done, int n, uint32_t base, uint32_t need) {
   if (need == 0) return;
+#if SBG_POLL == 1
+  while (ld_relaxed(done + n) - base < need) {
+  }
+  (void)ld_acquire(done + n);
+#elif SBG_POLL == 2
+  while (ld_acquire(done + n) - base < need) {
+  }
+#else
   while (ld_acquire(done + n) - base < need) __nanosleep(32);
+#endif
   fence_proxy_async_global();
 }
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
@@ -302,22 +323,29 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
             // J_ap x d_p lands in accumulator ap + p (columns (ap + p) BN ..), as below. In a
             // tile's first K-chunk, plane NPLANES-1 of ap >= 1 opens accumulator ap + NPLANES-1
             // (a separate N = BN MMA without accumulate); everything else accumulates.
+            // With W0 > 0, J plane ap multiplies digit planes pl0 = max(0, W0 - ap) .. NPLANES-1
+            // only (a contiguous run of B rows: N = (NPLANES - pl0) BN) into accumulators
+            // ap + pl0 - W0 ..; ap = 0 opens accumulators 0 .. NPLANES-1-W0.
             constexpr uint32_t NB = BN;
 #pragma unroll
             for (int k = 0; k < Cfg::BK / 32; ++k) {
 #pragma unroll
               for (int ap = 0; ap < NA; ++ap) {
+                const int pl0 = Cfg::W0 - ap > 0 ? Cfg::W0 - ap : 0;
+                const uint32_t np = static_cast<uint32_t>(NPLANES - pl0);
                 const bool a_signed = NA == 1 || ap == NA - 1;
                 const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + (stage * NA + ap) * Cfg::A_BYTES) + 2 * k;
-                const uint64_t bd0 = ptx::smem_desc_k_sw128(b_base + stage * NPLANES * Cfg::B_PLANE_BYTES) + 2 * k;
-                const uint32_t d = d_base + ap * NB;
+                const uint64_t bd0 =
+                    ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + pl0) * Cfg::B_PLANE_BYTES) + 2 * k;
+                const uint32_t d = d_base + (ap + pl0 - Cfg::W0) * NB;
                 if (kb == 0 && k == 0 && ap > 0) {
                   const uint64_t bdl =
                       ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + NPLANES - 1) * Cfg::B_PLANE_BYTES);
-                  ptx::mma_i8(d, adesc, bd0, ptx::idesc_i8(128, (NPLANES - 1) * NB, a_signed, true), true);
-                  ptx::mma_i8(d + (NPLANES - 1) * NB, adesc, bdl, ptx::idesc_i8(128, NB, a_signed, true), false);
+                  if (np > 1)
+                    ptx::mma_i8(d, adesc, bd0, ptx::idesc_i8(128, (np - 1) * NB, a_signed, true), true);
+                  ptx::mma_i8(d + (np - 1) * NB, adesc, bdl, ptx::idesc_i8(128, NB, a_signed, true), false);
                 } else {
-                  ptx::mma_i8(d, adesc, bd0, ptx::idesc_i8(128, NPLANES * NB, a_signed, true), (kb | k | ap) != 0);
+                  ptx::mma_i8(d, adesc, bd0, ptx::idesc_i8(128, np * NB, a_signed, true), (kb | k | ap) != 0);
                 }
               }
             }
@@ -334,10 +362,12 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
                 // products of equal weight 2^(8(ap+pl)) share one accumulator; the first
                 // pair of each weight (in this loop order) starts it at kb == 0
                 const int w = ap + pl;
+                if (w < Cfg::W0) continue;  // product not formed (see W0)
                 const bool first_pair = ap == (w - (NPLANES - 1) > 0 ? w - (NPLANES - 1) : 0);
 #pragma unroll
                 for (int k = 0; k < Cfg::BK / 32; ++k)
-                  ptx::mma_i8(d_base + w * BN, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0 || !first_pair);
+                  ptx::mma_i8(d_base + (w - Cfg::W0) * BN, adesc + 2 * k, bdesc + 2 * k, idesc,
+                              (kb | k) != 0 || !first_pair);
               }
             }
             ptx::mma_commit(empty_bar(stage));
@@ -475,9 +505,9 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
 #pragma unroll
           for (int j = 0; j < CWQ; ++j) f[j] = 0.0;
 #pragma unroll
-          for (int w = 0; w < Cfg::NW; ++w) {
+          for (int w = Cfg::W0; w < Cfg::NW; ++w) {
             uint32_t v[CWQ];
-            ptx::tmem_ld<CWQ>(t_row + w * BN + col0, v);
+            ptx::tmem_ld<CWQ>(t_row + (w - Cfg::W0) * BN + col0, v);
             ptx::tmem_ld_wait();
             const double sc = ldexp(1.0, 8 * w + args.fx_exp);
 #pragma unroll

@@ -107,7 +107,7 @@ def main(tag: str) -> None:
                                                         "orc_step_f64 GdSB from reference init_state"))
 
     t0, done = time.time(), 0
-    with ThreadPoolExecutor(os.cpu_count() or 1) as ex:
+    with ThreadPoolExecutor(int(os.environ.get("SBG_JOBS", os.cpu_count() or 1))) as ex:
         for r, e in ex.map(one, todo):
             energies[r] = e
             done += 1

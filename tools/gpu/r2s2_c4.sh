@@ -1,0 +1,4 @@
+# C4 (real J) after the 9-product contraction: SK tests, P3 at N=4096, timing
+timeout 900 python -m pytest tests/test_gpu_sk.py tests/test_gpu_p3_scale.py -q -x > gpurun_out/c4_tests.log 2>&1; echo "tests rc=$?"; tail -3 gpurun_out/c4_tests.log
+for r in 1 2; do timeout 300 python tools/configs_bench.py --only C4 --steps 20 2>&1 | grep -o '"us_per_step": [0-9.]*'; done
+timeout 900 python -m pytest tests/test_gpu_statistics.py -q -x -k "sk or c4 or 4096" > gpurun_out/c4_stat.log 2>&1; echo "stat rc=$?"; tail -3 gpurun_out/c4_stat.log
