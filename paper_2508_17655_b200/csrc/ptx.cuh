@@ -162,6 +162,22 @@ __device__ __forceinline__ uint64_t smem_desc_k_sw128(uint32_t smem_addr) {
   return d;
 }
 
+// The same with a 64-byte swizzle: rows of 64 B, 8-row core groups 512 B apart.
+__device__ __forceinline__ uint64_t smem_desc_k_sw64(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr & 0x3FFFF) >> 4);  // start address [0,14)
+  d |= static_cast<uint64_t>(1) << 16;                      // LBO (16 B units) [16,30)
+  d |= static_cast<uint64_t>(512 >> 4) << 32;               // SBO [32,46)
+  d |= static_cast<uint64_t>(1) << 46;                      // version = 1 (sm_100)
+  d |= static_cast<uint64_t>(4) << 61;                      // SWIZZLE_64B
+  return d;
+}
+template <int BK>
+__device__ __forceinline__ uint64_t smem_desc_k(uint32_t smem_addr) {
+  static_assert(BK == 128 || BK == 64, "K-major rows of 128 or 64 bytes");
+  return BK == 128 ? smem_desc_k_sw128(smem_addr) : smem_desc_k_sw64(smem_addr);
+}
+
 // Instruction descriptor for kind::i8, s32 accumulate, both operands K-major.
 __host__ __device__ constexpr uint32_t idesc_i8(uint32_t M, uint32_t N, bool a_signed, bool b_signed) {
   return (2u << 4)                              // c_format = S32

@@ -119,6 +119,10 @@ struct sbg_ctx {
   TmaMaps maps_sign[2], maps_planes[2];  // multi-step kernel maps, indexed by the current B buffer
   TmaMaps pmaps_planes[2];               // pair kernel, fixed-point planes (B half = 32 rows)
   TmaMaps fxmaps_sign[2], fxmaps_planes[2];  // real-J kernels (B tiles of 64 / 32 rows)
+  // real J x 4 digit planes: 64-byte K stages (TmaStepCfg::BK = 64, 64-byte swizzle), B tiles
+  // of 64 / 32 replica rows; J (tmJfx64) is set at launch
+  TmaMaps fxq_planes64[2], fxq_planes32[2];
+  CUtensorMap tmJfx64;
   TmaMaps maps_sign_cw8[2];                  // sign pair kernel with 8-replica state chunks
   TmaMaps rmaps_sign[2];                     // resident-state pair kernel, NR 128 (B halves of 64 rows)
   TmaMaps rmaps160_sign[2];                  // resident-state pair kernel, NR 160 (B halves of 80 rows)
@@ -197,7 +201,7 @@ static int shard_wait_check(sbg_ctx* ctx) {
 namespace {
 
 int encode_2d_u8(sbg_ctx* ctx, CUtensorMap* tm, const void* base, uint64_t inner, uint64_t rows,
-                 uint32_t box_inner, uint32_t box_rows) {
+                 uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto enc = get_encode();
   if (!enc) return ctx->fail(SBG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
   cuuint64_t dims[2] = {inner, rows};
@@ -205,7 +209,7 @@ int encode_2d_u8(sbg_ctx* ctx, CUtensorMap* tm, const void* base, uint64_t inner
   cuuint32_t box[2] = {box_inner, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return ctx->fail(SBG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
   return SBG_OK;
@@ -701,6 +705,16 @@ int ensure_state(sbg_ctx* ctx, int64_t R) {
         rc = encode_2d_u8(ctx, &ctx->fxmaps_planes[cur].Gin[par], ctx->dG[cur ^ par], ctx->npad, NPL * rpad, 128,
                           BN_FX_PLANE);
         if (rc) return rc;
+        ctx->fxq_planes64[cur] = ctx->maps_planes[cur];
+        ctx->fxq_planes32[cur] = ctx->fxmaps_planes[cur];
+      }
+      for (int par = 0; par < 2; ++par) {
+        int rc = encode_2d_u8(ctx, &ctx->fxq_planes64[cur].Gin[par], ctx->dG[cur ^ par], ctx->npad, NPL * rpad, 64,
+                              BN_FX_PLANE_W, CU_TENSOR_MAP_SWIZZLE_64B);
+        if (rc) return rc;
+        rc = encode_2d_u8(ctx, &ctx->fxq_planes32[cur].Gin[par], ctx->dG[cur ^ par], ctx->npad, NPL * rpad, 64,
+                          BN_FX_PLANE, CU_TENSOR_MAP_SWIZZLE_64B);
+        if (rc) return rc;
       }
     }
   }
@@ -1137,6 +1151,7 @@ int sbg_set_couplings_dense_f32(sbg_ctx* ctx, int64_t n, const float* J) {
   ctx->fx_shift = shift;
   ctx->energy_scale = std::ldexp(1.0, -shift);
   int rc = encode_2d_u8(ctx, &ctx->tmJ, ctx->dJ, npad, FX_NA * npad, 128, 128);
+  if (rc == SBG_OK) rc = encode_2d_u8(ctx, &ctx->tmJfx64, ctx->dJ, npad, FX_NA * npad, 64, 128, CU_TENSOR_MAP_SWIZZLE_64B);
   for (int a = 0; a < FX_NA && rc == SBG_OK; ++a)
     rc = encode_2d_u8(ctx, &ctx->tmJplane[a], ctx->dJ + size_t(a) * npad * npad, npad, npad, 128, 128);
   return rc;
@@ -1590,9 +1605,18 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
       // 20.4 us on pairs. SBG_STEP_CFG selects sweep alternatives (dev only).
       if (fx) {
         // real-valued J: 3 J planes x (sign | 4 x-planes), single-CTA
+#if SBG_FX_BK == 64
+        // dev: 64-byte K stages, 4 deep (bitwise equal, measured slower: DESIGN K4)
+        TmaMaps mq = fx64 ? ctx->fxq_planes64[cur] : ctx->fxq_planes32[cur];
+        mq.J = ctx->tmJfx64;
+        rc = sign   ? launch_multistep<1, BN_FX_SIGN, 2, 4, FX_NA>(ctx, ctx->fxmaps_sign[cur], a)
+             : fx64 ? launch_multistep<NPL, BN_FX_PLANE_W, 4, 2, FX_NA>(ctx, mq, a)
+                    : launch_multistep<NPL, BN_FX_PLANE, 4, 3, FX_NA>(ctx, mq, a);
+#else
         rc = sign   ? launch_multistep<1, BN_FX_SIGN, 2, 4, FX_NA>(ctx, ctx->fxmaps_sign[cur], a)
              : fx64 ? launch_multistep<NPL, BN_FX_PLANE_W, 2, 2, FX_NA>(ctx, ctx->maps_planes[cur], a)
                     : launch_multistep<NPL, BN_FX_PLANE, 2, 3, FX_NA>(ctx, ctx->fxmaps_planes[cur], a);
+#endif
       } else if (resident) {
         // default for sign variants: state resident in TMEM (step_resident.cuh); SBG_RESIDENT=0
         // selects the streaming kernels (dev comparison)

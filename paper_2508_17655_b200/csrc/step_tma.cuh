@@ -41,13 +41,20 @@
 #include "gsb_phase.cuh"
 #include "ptx.cuh"
 
+#ifndef SBG_FX_BK
+#define SBG_FX_BK 128
+#endif
+
 namespace sbg {
 
 template <int NPLANES, int BN, int STAGES_, int NBUF_, int NA_ = 1>
 struct TmaStepCfg {
   static constexpr int BM = 128;
-  static constexpr int BK = 128;
   static constexpr int NA = NA_;                        // J byte planes (1: int8 J; 3: fixed-point real J)
+  // K bytes per operand stage: 128 (128-byte swizzle). SBG_FX_BK=64 (dev): real J x 4 digit
+  // planes in 64-byte stages (64-byte swizzle), twice as many at half the size -- bitwise
+  // equal, measured slower at C4 (257 vs 244 us/step)
+  static constexpr int BK = (NA_ > 1 && NPLANES == 4) ? SBG_FX_BK : 128;
   static constexpr int NW = NA + NPLANES - 1;           // distinct plane weights 2^(8(a+b))
   // fixed-point real J with continuous x: the products of weight w = a + b < W0 (J's two low
   // bytes times q's two low digits: < 2^-27 of the field, below its fp32 rounding) are not
@@ -334,13 +341,13 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
                 const int pl0 = Cfg::W0 - ap > 0 ? Cfg::W0 - ap : 0;
                 const uint32_t np = static_cast<uint32_t>(NPLANES - pl0);
                 const bool a_signed = NA == 1 || ap == NA - 1;
-                const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + (stage * NA + ap) * Cfg::A_BYTES) + 2 * k;
+                const uint64_t adesc = ptx::smem_desc_k<Cfg::BK>(a_base + (stage * NA + ap) * Cfg::A_BYTES) + 2 * k;
                 const uint64_t bd0 =
-                    ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + pl0) * Cfg::B_PLANE_BYTES) + 2 * k;
+                    ptx::smem_desc_k<Cfg::BK>(b_base + (stage * NPLANES + pl0) * Cfg::B_PLANE_BYTES) + 2 * k;
                 const uint32_t d = d_base + (ap + pl0 - Cfg::W0) * NB;
                 if (kb == 0 && k == 0 && ap > 0) {
                   const uint64_t bdl =
-                      ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + NPLANES - 1) * Cfg::B_PLANE_BYTES);
+                      ptx::smem_desc_k<Cfg::BK>(b_base + (stage * NPLANES + NPLANES - 1) * Cfg::B_PLANE_BYTES);
                   if (np > 1)
                     ptx::mma_i8(d, adesc, bd0, ptx::idesc_i8(128, (np - 1) * NB, a_signed, true), true);
                   ptx::mma_i8(d + (np - 1) * NB, adesc, bdl, ptx::idesc_i8(128, NB, a_signed, true), false);
@@ -353,10 +360,10 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
           } else if (!Cfg::MERGED && issuer) {
 #pragma unroll
             for (int ap = 0; ap < NA; ++ap) {
-              const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + (stage * NA + ap) * Cfg::A_BYTES);
+              const uint64_t adesc = ptx::smem_desc_k<Cfg::BK>(a_base + (stage * NA + ap) * Cfg::A_BYTES);
 #pragma unroll
               for (int pl = 0; pl < NPLANES; ++pl) {
-                const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES);
+                const uint64_t bdesc = ptx::smem_desc_k<Cfg::BK>(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES);
                 // J planes: only the top plane is signed; B: sign plane or signed digit planes
                 const uint32_t idesc = ptx::idesc_i8(128, BN, NA == 1 || ap == NA - 1, true);
                 // products of equal weight 2^(8(ap+pl)) share one accumulator; the first
