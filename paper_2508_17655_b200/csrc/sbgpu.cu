@@ -298,10 +298,10 @@ int launch_multistep(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& a) 
   return SBG_OK;
 }
 
-template <int NP, int NPAIR, int ST, int NB, int CW = 16, bool Q4 = false>
+template <int NP, int NPAIR, int ST, int NB, int CW = 16, bool Q4 = false, int NA = 1>
 int launch_multistep_pair(sbg_ctx* ctx, const TmaMaps& maps, MultiStepArgs a) {
-  using Cfg = PairStepCfg<NP, NPAIR, ST, NB, CW, Q4>;
-  auto kern = gsb_multistep_pair_kernel<NP, NPAIR, ST, NB, CW, Q4>;
+  using Cfg = PairStepCfg<NP, NPAIR, ST, NB, CW, Q4, NA>;
+  auto kern = gsb_multistep_pair_kernel<NP, NPAIR, ST, NB, CW, Q4, NA>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
   a.num_n = int32_t(ctx->rpad / NPAIR);
   if (NP != 1) a.ksplit = 1;
@@ -1613,9 +1613,14 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
              : fx64 ? launch_multistep<NPL, BN_FX_PLANE_W, 4, 2, FX_NA>(ctx, mq, a)
                     : launch_multistep<NPL, BN_FX_PLANE, 4, 3, FX_NA>(ctx, mq, a);
 #else
-        rc = sign   ? launch_multistep<1, BN_FX_SIGN, 2, 4, FX_NA>(ctx, ctx->fxmaps_sign[cur], a)
-             : fx64 ? launch_multistep<NPL, BN_FX_PLANE_W, 2, 2, FX_NA>(ctx, ctx->maps_planes[cur], a)
-                    : launch_multistep<NPL, BN_FX_PLANE, 2, 3, FX_NA>(ctx, ctx->fxmaps_planes[cur], a);
+        // continuous variants on CTA pairs (128-replica pair tiles, nine products, one
+        // accumulator buffer); SBG_FX_PAIR=0 selects the single-CTA kernel (dev comparison)
+        if (!sign && fx64 && dev_knob("SBG_FX_PAIR") != 0 && ctx->rpad % 128 == 0 && (ctx->npad / 128) % 2 == 0)
+          rc = launch_multistep_pair<NPL, 128, 2, 2, 16, false, FX_NA>(ctx, ctx->maps_planes[cur], a);
+        else
+          rc = sign   ? launch_multistep<1, BN_FX_SIGN, 2, 4, FX_NA>(ctx, ctx->fxmaps_sign[cur], a)
+               : fx64 ? launch_multistep<NPL, BN_FX_PLANE_W, 2, 2, FX_NA>(ctx, ctx->maps_planes[cur], a)
+                      : launch_multistep<NPL, BN_FX_PLANE, 2, 3, FX_NA>(ctx, ctx->fxmaps_planes[cur], a);
 #endif
       } else if (resident) {
         // default for sign variants: state resident in TMEM (step_resident.cuh); SBG_RESIDENT=0

@@ -35,14 +35,23 @@ namespace sbg {
 // -- half the J bytes per step (the bound of the J-streaming regime, C5) at twice the MMA
 // rate. Its unit scale factors take 16 TMEM columns, so the accumulator is single-buffered
 // (N_PAIR = 256 leaves no room for two).
-template <int NPLANES, int N_PAIR, int STAGES_, int NBUF_, int CW_ = 16, bool Q4_ = false>
+// NA_ = 3 (real J, continuous variants): J as the three fixed-point byte planes of step_tma.cuh
+// (u8, u8, s8) times the four signed digit planes of q, the nine products of weight
+// 2^(8w), w = a + b >= W0 = 2, one MMA each (N = N_PAIR), into four accumulators; the pair
+// halves the shared-memory operand traffic per MMA of the single-CTA real-J kernel, which is
+// what bounds that one (C4).
+template <int NPLANES, int N_PAIR, int STAGES_, int NBUF_, int CW_ = 16, bool Q4_ = false, int NA_ = 1>
 struct PairStepCfg {
   static constexpr bool Q4 = Q4_;
+  static constexpr int NA = NA_;                        // J byte planes
+  static constexpr int NW = NA + NPLANES - 1;           // distinct plane weights
+  static constexpr int W0 = NA > 1 ? 2 : 0;             // products of weight < W0 not formed
   static constexpr int KPB = Q4 ? 2 : 1;                // K elements per operand byte
   static constexpr int BM = 128;                        // spins per CTA
   static constexpr int BK = 128;                        // K bytes per stage
   static constexpr int B_HALF = N_PAIR / 2;             // B rows staged per CTA (per plane)
-  static constexpr int A_BYTES = BM * BK;
+  static constexpr int A_PLANE_BYTES = BM * BK;         // one J plane tile
+  static constexpr int A_BYTES = NA * A_PLANE_BYTES;
   static constexpr int B_PLANE_BYTES = B_HALF * BK;
   static constexpr int STAGE_BYTES = A_BYTES + NPLANES * B_PLANE_BYTES;
   static constexpr int STAGES = STAGES_;
@@ -54,7 +63,7 @@ struct PairStepCfg {
   static constexpr int ST_G = CW * BM / KPB;
   static constexpr int BUF_RAW = 3 * ST_ARR + NPLANES * ST_G;
   static constexpr int BUF_BYTES = (BUF_RAW + 1023) / 1024 * 1024;
-  static constexpr int ACC_COLS = NPLANES * N_PAIR;     // per CTA per accumulator buffer
+  static constexpr int ACC_COLS = (NA > 1 ? NW - W0 : NPLANES) * N_PAIR;  // per CTA per accumulator buffer
   // accumulator buffers: 2 when they fit TMEM; 1 for e2m1 (scale factors) or wide tiles, whose
   // epilogue (non-e2m1) then drains all accumulator columns before the state update
   static constexpr int NACC = (Q4 || 2 * ACC_COLS > 512) ? 1 : 2;
@@ -62,7 +71,7 @@ struct PairStepCfg {
   // all digit planes in one MMA (N = NPLANES * N_PAIR <= 256). The pair's output columns are
   // then [CTA 0's B rows][CTA 1's B rows], each [plane][B_HALF replicas]: plane p of replica
   // r (of the tile) sits at column (r / B_HALF) * NPLANES * B_HALF + p * B_HALF + r % B_HALF
-  static constexpr bool MERGED = !Q4 && NPLANES > 1 && NPLANES * N_PAIR <= 256;
+  static constexpr bool MERGED = NA == 1 && !Q4 && NPLANES > 1 && NPLANES * N_PAIR <= 256;
   static constexpr int TMEM_COLS = Q4 ? 512 : NACC * ACC_COLS;
   static constexpr uint32_t COL_SF = 512 - 16;          // Q4: unit E8M0 scale factors
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
@@ -73,13 +82,15 @@ struct PairStepCfg {
   static_assert(N_PAIR % CW == 0, "chunking");
   static_assert(TMEM_COLS == 256 || TMEM_COLS == 512, "TMEM allocation");
   static_assert(!Q4 || (NPLANES == 1 && ACC_COLS <= 496), "e2m1: sign plane, room for the scale factors");
+  static_assert(NA == 1 || (NA == 3 && NPLANES == 4 && !Q4), "real J: continuous variants, int8 planes");
 };
 
-template <int NPLANES, int N_PAIR, int STAGES_, int NBUF_, int CW_ = 16, bool Q4_ = false>
+template <int NPLANES, int N_PAIR, int STAGES_, int NBUF_, int CW_ = 16, bool Q4_ = false, int NA_ = 1>
 __global__ void __cluster_dims__(2, 1, 1)
-    __launch_bounds__(PairStepCfg<NPLANES, N_PAIR, STAGES_, NBUF_, CW_, Q4_>::THREADS, 1)
+    __launch_bounds__(PairStepCfg<NPLANES, N_PAIR, STAGES_, NBUF_, CW_, Q4_, NA_>::THREADS, 1)
         gsb_multistep_pair_kernel(const __grid_constant__ TmaMaps maps, const MultiStepArgs args) {
-  using Cfg = PairStepCfg<NPLANES, N_PAIR, STAGES_, NBUF_, CW_, Q4_>;
+  using Cfg = PairStepCfg<NPLANES, N_PAIR, STAGES_, NBUF_, CW_, Q4_, NA_>;
+  constexpr int NA = Cfg::NA;
   constexpr int NACC = Cfg::NACC;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int NBUF = Cfg::NBUF;
@@ -197,7 +208,10 @@ __global__ void __cluster_dims__(2, 1, 1)
           if (ptx::elect_one()) {
             const uint32_t fb = ptx::mapa(full_bar(stage), 0);  // the leader's full barrier
             ptx::mbar_arrive_expect_tx_cluster(fb, Cfg::STAGE_BYTES);
-            ptx::tma_load_2d_pair_hint(a_base + stage * Cfg::A_BYTES, &maps.J, fb, kb * Cfg::BK, m_blk * Cfg::BM, keep);
+#pragma unroll
+            for (int ap = 0; ap < NA; ++ap)  // J planes stacked [NA][npad] rows in one map
+              ptx::tma_load_2d_pair_hint(a_base + stage * Cfg::A_BYTES + ap * Cfg::A_PLANE_BYTES, &maps.J, fb,
+                                         kb * Cfg::BK, ap * args.num_m * Cfg::BM + m_blk * Cfg::BM, keep);
 #pragma unroll
             for (int pl = 0; pl < NPLANES; ++pl)
               ptx::tma_load_2d_pair_hint(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES, gin, fb, kb * Cfg::BK,
@@ -233,7 +247,26 @@ __global__ void __cluster_dims__(2, 1, 1)
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
             const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + stage * Cfg::A_BYTES);
-            if constexpr (Cfg::MERGED) {
+            if constexpr (NA > 1) {
+              // real J: product (J plane ap, digit plane pl) of weight w = ap + pl >= W0 into
+              // accumulator w - W0; the first product of each weight in this loop order opens it
+#pragma unroll
+              for (int ap = 0; ap < NA; ++ap) {
+                const uint64_t ad = ptx::smem_desc_k_sw128(a_base + stage * Cfg::A_BYTES + ap * Cfg::A_PLANE_BYTES);
+                const uint32_t idesc = ptx::idesc_i8(256, N_PAIR, ap == NA - 1, true);
+#pragma unroll
+                for (int pl = 0; pl < NPLANES; ++pl) {
+                  const int w = ap + pl;
+                  if (w < Cfg::W0) continue;
+                  const bool first_pair = ap == (w - (NPLANES - 1) > 0 ? w - (NPLANES - 1) : 0);
+                  const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + (stage * NPLANES + pl) * Cfg::B_PLANE_BYTES);
+#pragma unroll
+                  for (int k = 0; k < Cfg::BK / 32; ++k)
+                    ptx::mma_i8_pair(d_base + (w - Cfg::W0) * N_PAIR, ad + 2 * k, bdesc + 2 * k, idesc,
+                                     (kb != kb0 || k != 0) || !first_pair);
+                }
+              }
+            } else if constexpr (Cfg::MERGED) {
               const uint64_t bdesc = ptx::smem_desc_k_sw128(b_base + stage * NPLANES * Cfg::B_PLANE_BYTES);
 #pragma unroll
               for (int k = 0; k < Cfg::BK / 32; ++k)
@@ -386,7 +419,24 @@ __global__ void __cluster_dims__(2, 1, 1)
       // the field of chunk c (this thread's CWQ replicas) from the accumulator columns
       auto load_F = [&](int c, float* F) {
         const int col0 = c * CW + h * CWQ;
-        if (NPLANES == 1) {
+        if constexpr (NA > 1) {
+          // fixed-point real J: F = fl32(sum_w fl64(acc_w * 2^(8w + fx_exp))), fixed order (as step_tma.cuh)
+          double f[CWQ];
+#pragma unroll
+          for (int j = 0; j < CWQ; ++j) f[j] = 0.0;
+#pragma unroll
+          for (int w = Cfg::W0; w < Cfg::NW; ++w) {
+            uint32_t v[CWQ];
+            ptx::tmem_ld<CWQ>(t_row + (w - Cfg::W0) * N_PAIR + col0, v);
+            ptx::tmem_ld_wait();
+            const double sc = ldexp(1.0, 8 * w + args.fx_exp);
+#pragma unroll
+            for (int j = 0; j < CWQ; ++j)
+              f[j] = __dadd_rn(f[j], __dmul_rn(static_cast<double>(static_cast<int32_t>(v[j])), sc));
+          }
+#pragma unroll
+          for (int j = 0; j < CWQ; ++j) F[j] = __double2float_rn(f[j]);
+        } else if (NPLANES == 1) {
           uint32_t v[CWQ];
           ptx::tmem_ld<CWQ>(t_row + col0, v);
           ptx::tmem_ld_wait();
