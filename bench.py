@@ -577,7 +577,8 @@ def measure_configs(args, device: int):
             d["cpu_baseline"] = cb
         out["C3"] = d
 
-    # C4: SK N=4096, J ~ N(0, 1/N) fp32, GbSB, R=2048 (24-bit fixed-point J: 3 planes x 4 digit planes)
+    # C4: SK N=4096, J ~ N(0, 1/N) fp32, GbSB, R=2048 (24-bit fixed-point J: 3 planes x 4 digit planes,
+    # nine products formed)
     with Solver(device) as s:
         n, R = 4096, 2048
         J = orc.gen_sk_f32(n, 1)
@@ -586,9 +587,9 @@ def measure_configs(args, device: int):
         us = timed(s, Variant.gbsb, n, R, c)
         d = {"workload": "C4 (BASELINE configs[3]): SK N=4096 fp32 J, GbSB, R=2048", "us_per_step": us,
              "su_per_s": n * R / (us * 1e-6), "steps": K,
-             "roofline": _tensor_roofline("3 J byte planes x 4 x digit planes, exact int products", "int8",
-                                          2.0 * n * n * R, 12 * 2.0 * n * n * R, us, 12),
-             "kernel": "gsb_multistep_kernel<4,64,2,2,3> (fixed-point real J)"}
+             "roofline": _tensor_roofline("3 J byte planes x 4 x digit planes, the 9 of weight >= 2^16, exact int "
+                                          "products", "int8", 2.0 * n * n * R, 9 * 2.0 * n * n * R, us, 9),
+             "kernel": "gsb_multistep_pair_kernel<4,128,2,2,16,false,3> (fixed-point real J on CTA pairs)"}
         d["roofline"]["traffic"] = traffic_for("c4_sk", K)
         if not args.no_cpu_baseline:
             d["cpu_baseline"] = cpu_leg(2, J.astype(np.float64), 32, c, 6.0, "gbsb (fp64 J)")

@@ -1615,7 +1615,7 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
 #else
         // continuous variants on CTA pairs (128-replica pair tiles, nine products, one
         // accumulator buffer); SBG_FX_PAIR=0 selects the single-CTA kernel (dev comparison)
-        if (!sign && fx64 && dev_knob("SBG_FX_PAIR") != 0 && ctx->rpad % 128 == 0 && (ctx->npad / 128) % 2 == 0)
+        if (!sign && fx64 && !getenv_is0("SBG_FX_PAIR") && ctx->rpad % 128 == 0 && (ctx->npad / 128) % 2 == 0)
           rc = launch_multistep_pair<NPL, 128, 2, 2, 16, false, FX_NA>(ctx, ctx->maps_planes[cur], a);
         else
           rc = sign   ? launch_multistep<1, BN_FX_SIGN, 2, 4, FX_NA>(ctx, ctx->fxmaps_sign[cur], a)

@@ -83,7 +83,7 @@ def main():
             J = orc.gen_sk_f32(n, 1)
             s.set_instance(J)
             res["C4_gbsb_sk_n4096_R2048"] = run(s, Variant.gbsb, n, 2048, args.steps, 0.5, 3 * n / 2048,
-                                                ops_per_su=12 * 2 * n, tensor_peak=i8)
+                                                ops_per_su=9 * 2 * n, tensor_peak=i8)
     print(json.dumps(res, indent=1))
 
 

@@ -18,7 +18,7 @@ import sys
 SPEC = {  # key: (kernel-name prefix, which occurrence is the timed launch)
     "c2_resident_e2m1": ("void gsb_resident_ts_kernel<2, 4>", 1),
     "c1_planes": ("void gsb_multistep_pair_kernel<4, 64, 4, 2, 16, 0>", 1),
-    "c4_sk": ("void gsb_multistep_kernel<4, 64, 2, 2, 3>", 1),
+    "c4_sk": ("void gsb_multistep_pair_kernel<4, 128, 2, 2, 16, 0, 3>", 1),
     "c5_single": ("void gsb_multistep_pair_kernel<1, 256, 5, 2, 16, 1>", 1),
 }
 
