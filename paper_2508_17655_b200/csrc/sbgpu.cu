@@ -256,7 +256,11 @@ template <int NP, int BN, EpiMode MODE>
 int launch_step(sbg_ctx* ctx, const CUtensorMap& tmG, const StepArgs& a, const CUtensorMap* tmA = nullptr) {
   using Cfg = StepCfg<NP, BN>;
   auto kern = gsb_step_i8_kernel<NP, BN, MODE>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  static int attr_device = -1;  // once per instantiation and device
+  if (attr_device != ctx->device) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    attr_device = ctx->device;
+  }
   const int tiles = a.num_m * a.num_n;
   const int grid = std::min(tiles, ctx->sms);
   kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream>>>(tmA ? *tmA : ctx->tmJ, tmG, a);
@@ -303,7 +307,11 @@ template <int NP, int BN, int ST, int NB, int NA = 1>
 int launch_multistep(sbg_ctx* ctx, const TmaMaps& maps, const MultiStepArgs& a) {
   using Cfg = TmaStepCfg<NP, BN, ST, NB, NA>;
   auto kern = gsb_multistep_kernel<NP, BN, ST, NB, NA>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  static int attr_device = -1;  // once per instantiation and device
+  if (attr_device != ctx->device) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    attr_device = ctx->device;
+  }
   const int64_t tiles = int64_t(a.num_m) * a.num_n * a.nsteps;
   // persistent: one CTA per SM (all must be co-resident for the dependency walk)
   const int grid = int(std::min<int64_t>(tiles, ctx->sms));
@@ -318,7 +326,11 @@ template <int NP, int NPAIR, int ST, int NB, int CW = 16, bool Q4 = false, int N
 int launch_multistep_pair(sbg_ctx* ctx, const TmaMaps& maps, MultiStepArgs a) {
   using Cfg = PairStepCfg<NP, NPAIR, ST, NB, CW, Q4, NA>;
   auto kern = gsb_multistep_pair_kernel<NP, NPAIR, ST, NB, CW, Q4, NA>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  static int attr_device = -1;  // once per instantiation and device
+  if (attr_device != ctx->device) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    attr_device = ctx->device;
+  }
   a.num_n = int32_t(ctx->rpad / NPAIR);
   if (NP != 1) a.ksplit = 1;
   // every K part needs at least one K block: a part with an empty range would commit an
