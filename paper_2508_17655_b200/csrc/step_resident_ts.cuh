@@ -31,6 +31,9 @@
 #include "step_resident_parts.cuh"
 #include "step_tma.cuh"
 
+#ifndef SBG_TS_PPART
+#define SBG_TS_PPART 0  // 1: p written back / loaded part by part in a group's last step
+#endif
 #ifndef SBG_TS_LD1
 #define SBG_TS_LD1 0  // 1: one TMEM load + wait per part-step (measured the same, 26.6 us; spills 36 B)
 #endif
@@ -492,6 +495,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
     auto xa = [&](int col) { return x_base + static_cast<uint32_t>(col * Cfg::BM + sl) * 4u; };
     auto ya = [&](int col) { return y_base + static_cast<uint32_t>(col * Cfg::BM + sl) * 4u; };
     float preg[Cfg::NR / 4];
+    // p of part I of replica block nb: this thread's spin, its column quarter of the part
+    auto load_p = [&](auto I, int nb) {
+      constexpr int i = decltype(I)::value;
+      static_for<0, Cfg::w(i) / 16>([&](auto C) {
+        constexpr int c = decltype(C)::value;
+        const int col = Cfg::off(i) + cg * (Cfg::w(i) / 4) + c * CH;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = nb * Cfg::NR + col + j;
+          preg[Cfg::off(i) / 4 + c * CH + j] = r < args.rpad ? args.p[static_cast<size_t>(r) * args.npad + spin] : 0.0f;
+        }
+      });
+    };
+    auto store_p = [&](auto I, int nb) {
+      constexpr int i = decltype(I)::value;
+      const uint64_t wb_policy = ptx::policy_evict_first();
+      static_for<0, Cfg::w(i) / 16>([&](auto C) {
+        constexpr int c = decltype(C)::value;
+        const int col = Cfg::off(i) + cg * (Cfg::w(i) / 4) + c * CH;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = nb * Cfg::NR + col + j;
+          if (r < args.rpad)
+            ptx::st_hint(args.p + static_cast<size_t>(r) * args.npad + spin,
+                         __float_as_uint(preg[Cfg::off(i) / 4 + c * CH + j]), wb_policy);
+        }
+      });
+    };
     auto put_g2 = [&](int row, float xa_, float xb_) {
       const uint32_t mine = (xa_ >= 0.0f ? 0x2u : 0xAu) | ((xb_ >= 0.0f ? 0x2u : 0xAu) << 8);
       const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, mine, 1);
@@ -510,18 +541,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
       const bool first = g == args.group0;
       if (io) gstamp(g, 0);
       // ---- group start: x, y arrive by TMA (issued by the publisher, sfull), p to registers
-      static_for<0, PARTS>([&](auto I) {
-        constexpr int i = decltype(I)::value;
-        static_for<0, Cfg::w(i) / 16>([&](auto C) {
-          constexpr int c = decltype(C)::value;
-          const int col = Cfg::off(i) + cg * (Cfg::w(i) / 4) + c * CH;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int r = n_blk * Cfg::NR + col + j;
-            preg[Cfg::off(i) / 4 + c * CH + j] = r < args.rpad ? args.p[static_cast<size_t>(r) * args.npad + spin] : 0.0f;
-          }
-        });
-      });
+      // (SBG_TS_PPART: later groups' p was loaded part by part during the previous group's last step)
+      if (first || !SBG_TS_PPART)
+        static_for<0, PARTS>([&](auto I) { load_p(I, n_blk); });
       if (first) {  // G_0 = sgn(x_0) of the launch's first group (later groups: the helper)
         static_for<0, PARTS>([&](auto I) {
           constexpr int i = decltype(I)::value;
@@ -643,25 +665,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(tempty_bar(i), 0));
           if (io) stamp(g, s, i, 2);
+          if constexpr (SBG_TS_PPART) {
+            // the group's last step: this part's p goes back now and the next group's p of this
+            // part is loaded into the same registers (consumed at its step 0), overlapping the
+            // other parts' last-step epilogues
+            if (s == args.nsteps - 1) {
+              store_p(I, n_blk);
+              const int nb = (g + 1) * args.rb_per_group + rbk;
+              if (g + 1 < args.group0 + args.groups && nb < num_n) load_p(I, nb);
+            }
+          }
         });
       }
       // ---- group end: x, y went back with the last step's G tiles (the publisher); p by stores
       if (io) gstamp(g, 4);
-      const uint64_t wb_policy = ptx::policy_evict_first();
-      static_for<0, PARTS>([&](auto I) {
-        constexpr int i = decltype(I)::value;
-        static_for<0, Cfg::w(i) / 16>([&](auto C) {
-          constexpr int c = decltype(C)::value;
-          const int col = Cfg::off(i) + cg * (Cfg::w(i) / 4) + c * CH;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int r = n_blk * Cfg::NR + col + j;
-            if (r < args.rpad)
-              ptx::st_hint(args.p + static_cast<size_t>(r) * args.npad + spin,
-                           __float_as_uint(preg[Cfg::off(i) / 4 + c * CH + j]), wb_policy);
-          }
-        });
-      });
+      if (!SBG_TS_PPART) static_for<0, PARTS>([&](auto I) { store_p(I, n_blk); });
       if (io) gstamp(g, 5);
     }
   }
