@@ -289,6 +289,7 @@ class _Orc:
         L.orc_step_f32_fx.argtypes = [C.c_int, _i64, _P, C.c_int, _i64, _i64, _P, _P, _P, _u64, _u64, _f32, _f32,
                                       _f32]
         L.orc_energy2_fx.argtypes = [_i64, _P, _i64, _i64, _P, _P]
+        L.orc_fields_fx.argtypes = [C.c_int, _i64, _P, C.c_int, _i64, _i64, _P, _P]
         L.orc_init_reference_seeds.argtypes = [_i64, _i64, _i64, _P, C.c_int, _P, _P, _P]
         L.orc_phase_batch_f32.argtypes = [_i64, _P, _P, _P, _P, _f32, _f32, _f32, _u64, _u64]
 
@@ -444,6 +445,14 @@ class _Orc:
             self.lib.orc_step_f32_fx(variant, n, _ptr(planes), shift, x.shape[0], x.shape[1], _ptr(x), _ptr(y),
                                      _ptr(p), m + k, M, dt, c, a)
         return x, y, p
+
+    def fields_fx(self, variant, planes, shift, x):
+        """The GPU's fixed-point field of real J (9 plane products for the continuous variants)."""
+        planes = np.ascontiguousarray(planes, np.uint8)
+        x = np.ascontiguousarray(x, np.float32)
+        F = np.empty_like(x)
+        self.lib.orc_fields_fx(variant, planes.shape[1], _ptr(planes), shift, x.shape[0], x.shape[1], _ptr(x), _ptr(F))
+        return F
 
     def energy_fx(self, planes, shift, x):
         planes = np.ascontiguousarray(planes, np.uint8)

@@ -478,14 +478,14 @@ static inline int64_t jplane(const uint8_t* planes, int64_t n, int a, int64_t i,
   return a == 2 ? (int64_t)(int8_t)b : (int64_t)b;
 }
 
-void orc_step_f32_fx(int variant, int64_t n, const uint8_t* planes, int shift, int64_t R, int64_t ld, float* x,
-                     float* y, float* p, uint64_t m, uint64_t M, float dt, float c, float a_cfg) {
-  const float a = honours_a(variant) ? a_cfg : 0.0f;
-  const float inv = 1.0f / (float)(M - m);
-  float* F = (float*)malloc(sizeof(float) * (size_t)n);
+void orc_fields_fx(int variant, int64_t n, const uint8_t* planes, int shift, int64_t R, int64_t ld, const float* x,
+                   float* F) {
+  /* The GPU's fixed-point field of real J (step_tma.cuh / step_pair.cuh, NA = 3) for R
+   * replicas: F[r][i] = fl32(sum_w fl64(acc_w 2^(8w + e0))), acc_w = exact sum of the plane
+   * products of weight w. */
   int64_t* qb = (int64_t*)malloc(sizeof(int64_t) * (size_t)n * 4);
   for (int64_t r = 0; r < R; ++r) {
-    float* xr = x + r * ld;
+    const float* xr = x + r * ld;
     if (is_sign_variant(variant)) {
       for (int64_t j = 0; j < n; ++j) qb[j] = xr[j] >= 0.0f ? 1 : -1;
     } else {
@@ -513,12 +513,22 @@ void orc_step_f32_fx(int variant, int64_t n, const uint8_t* planes, int shift, i
         }
       double f = 0.0;
       for (int w = w0; w < nw; ++w) f = f + (double)acc[w] * ldexp(1.0, 8 * w + e0);
-      F[i] = (float)f;
+      F[r * ld + i] = (float)f;
     }
-    for (int64_t i = 0; i < n; ++i) orc_phase_f32(F[i], xr + i, y + r * ld + i, p + r * ld + i, a, c, dt, inv);
   }
-  free(F);
   free(qb);
+}
+
+void orc_step_f32_fx(int variant, int64_t n, const uint8_t* planes, int shift, int64_t R, int64_t ld, float* x,
+                     float* y, float* p, uint64_t m, uint64_t M, float dt, float c, float a_cfg) {
+  const float a = honours_a(variant) ? a_cfg : 0.0f;
+  const float inv = 1.0f / (float)(M - m);
+  float* F = (float*)malloc(sizeof(float) * (size_t)(R * ld));
+  orc_fields_fx(variant, n, planes, shift, R, ld, x, F);
+  for (int64_t r = 0; r < R; ++r)
+    for (int64_t i = 0; i < n; ++i)
+      orc_phase_f32(F[r * ld + i], x + r * ld + i, y + r * ld + i, p + r * ld + i, a, c, dt, inv);
+  free(F);
 }
 
 void orc_energy2_fx(int64_t n, const uint8_t* planes, int64_t R, int64_t ld, const float* x, int64_t* E2) {

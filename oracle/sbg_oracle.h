@@ -102,6 +102,9 @@ int64_t orc_argmin_i64(int64_t R, const int64_t* v);
 /* ---- real-valued J (fixed-point image, GPU op order) ------------------- */
 /* Quantise J like sbg_set_couplings_dense_f32; returns the scale exponent s. */
 int orc_fx_quantize(int64_t n, const float* J, uint8_t* planes /* [3][n][n] */);
+/* The fixed-point field alone (continuous variants: the 9 plane products of weight >= 2^16). */
+void orc_fields_fx(int variant, int64_t n, const uint8_t* planes, int shift, int64_t R, int64_t ld, const float* x,
+                   float* F);
 void orc_step_f32_fx(int variant, int64_t n, const uint8_t* planes, int shift, int64_t R, int64_t ld, float* x,
                      float* y, float* p, uint64_t m, uint64_t M, float dt, float c, float a);
 void orc_energy2_fx(int64_t n, const uint8_t* planes, int64_t R, int64_t ld, const float* x, int64_t* E2);
