@@ -196,6 +196,13 @@ int sbg_shard_buffers(sbg_ctx* ctx, void** g0, void** g1, void** done);
 int sbg_shard_set_peers(sbg_ctx* ctx, int32_t npeers, void* const* g0, void* const* g1, void* const* done);
 int sbg_shard_prepare(sbg_ctx* ctx, int32_t variant);
 int sbg_shard_push_slab(sbg_ctx* ctx);
+/* Test-only: nranks (2..8) row shards living on ONE GPU, wired to each other with
+ * sbg_shard_set_peers and prepared (sbg_shard_prepare + sbg_shard_push_slab), advanced from
+ * m_begin to m_end in ONE cooperative launch of the e2m1 CTA-pair kernel, each rank on its own
+ * group of CTAs: the multi-step cross-rank waits of K7 run as over NVLink, without separate
+ * launches that wait on one another on one GPU. Timing: sbg_last_advance_ms(ctxs[0]). */
+int sbg_shard_advance_fused(sbg_ctx* const* ctxs, int32_t nranks, const sbg_params* prm, uint64_t m_begin,
+                            uint64_t m_end);
 /* Device-generated +-1 couplings for large-N throughput runs: J_ij = J_ji = sign from
  * splitmix64(seed ^ (min(i,j) * n + max(i,j))), zero diagonal (i.i.d. uniform +-1 like
  * gen_random_dense, NOT its draw order; parity tests use the exact order at small n).

@@ -28,7 +28,8 @@ EXPORTS = [
     "sbg_readout", "sbg_readout_best", "sbg_fields_sign", "sbg_fields_fixed", "sbg_run", "sbg_run_best", "sbg_run_seeded", "sbg_synchronize",
     "sbg_kernel_launches", "sbg_state_device", "sbg_last_advance_ms", "sbg_success_tts", "sbg_tune_wigner_f64",
     "sbg_set_couplings_rows_i8", "sbg_shard_info", "sbg_shard_buffers", "sbg_shard_set_peers", "sbg_shard_prepare",
-    "sbg_shard_push_slab", "sbg_shard_ipc_export", "sbg_shard_ipc_open", "sbg_readout_partial",
+    "sbg_shard_push_slab", "sbg_shard_advance_fused", "sbg_shard_ipc_export", "sbg_shard_ipc_open",
+    "sbg_readout_partial",
     "sbg_gen_couplings_hash_pm1", "sbg_set_replica_a", "sbg_init_state_seeds",
     "sbg_gen_couplings_dense_pm1_rows", "sbg_get_couplings_i8", "sbg_extreme_eigenvalues", "sbg_auto_tune",
     "sbg_set_couplings_graph", "sbg_set_couplings_entries_f64",
@@ -119,6 +120,7 @@ def lib() -> C.CDLL:
     L.sbg_shard_set_peers.argtypes = [P, i32, P, P, P]
     L.sbg_shard_prepare.argtypes = [P, i32]
     L.sbg_shard_push_slab.argtypes = [P]
+    L.sbg_shard_advance_fused.argtypes = [P, i32, P, u64, u64]
     L.sbg_shard_ipc_export.argtypes = [P, P]
     L.sbg_shard_ipc_open.argtypes = [P, P, P, P, P]
     L.sbg_readout_partial.argtypes = [P, P]

@@ -98,6 +98,8 @@ struct TsMapKey {
 struct sbg_ctx {
   int device = 0;
   TsMaps ts_cache[2];
+  void* d_fused = nullptr;  // sbg_shard_advance_fused: rank tables (maps, args)
+  size_t fused_cap = 0;
   TsMapKey ts_key[2];
   bool ts_ok[2] = {false, false};
   int sms = 148;
@@ -1066,6 +1068,7 @@ void sbg_destroy(sbg_ctx* ctx) {
   cudaFree(ctx->d_fpart);
   cudaFree(ctx->d_kdone);
   cudaFree(ctx->d_err);
+  cudaFree(ctx->d_fused);
   cudaFree(ctx->dJ);
   cudaFree(ctx->dJ4);
   ctx->dJ4 = nullptr;
@@ -2353,6 +2356,116 @@ int sbg_shard_push_slab(sbg_ctx* ctx) {
                          ctx->stream));
   }
   CK(cudaStreamSynchronize(ctx->stream));
+  return SBG_OK;
+}
+
+// Test-only emulation of `nranks` row shards of ONE GPU as ONE cooperative launch of the e2m1
+// CTA-pair kernel (FUSED): every rank keeps its own J rows, state, G buffers and done counter,
+// wired to the others exactly as for separate GPUs (sbg_shard_set_peers), and runs m_begin ..
+// m_end in one multi-step schedule on its own group of 2 * floor(sms / (2 nranks)) CTAs, so the
+// cross-rank multi-step waits (system-scope acquire/release, slab pushes from the epilogue)
+// execute as they would over NVLink. (Ranks that wait on one another must never be separate
+// launches on one GPU: nothing guarantees they are co-resident.)
+int sbg_shard_advance_fused(sbg_ctx* const* ctxs, int32_t nranks, const sbg_params* prm, uint64_t m_begin,
+                            uint64_t m_end) {
+  if (!ctxs || nranks < 2 || nranks > MAX_PEERS + 1) return SBG_ERR_INVALID_ARGUMENT;
+  sbg_ctx* ctx = ctxs[0];
+  CHECK_CTX(ctx);
+  for (int r = 0; r < nranks; ++r) {
+    sbg_ctx* c = ctxs[r];
+    CHECK_CTX(c);
+    int rc = validate_params(c, prm);
+    if (rc) return rc;
+    if (!c->sharded || !c->dX || c->R < 1) return ctx->fail(SBG_ERR_STATE, "rank %d: row shard with state required", r);
+    if (c->device != ctx->device) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "fused ranks must share one device");
+    if (!is_sign_variant(prm->variant) || !q4_stream(c) || c->g_mode != 2)
+      return ctx->fail(SBG_ERR_UNSUPPORTED, "rank %d: fused emulation needs e2m1 shards after sbg_shard_prepare", r);
+    if (int(c->peer_done.size()) != nranks - 1 || c->R != ctx->R || c->rpad != ctx->rpad || c->kpad != ctx->kpad ||
+        c->npad != ctx->npad || c->g_cur != ctx->g_cur)
+      return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "rank %d: shards must be wired to each other and alike", r);
+  }
+  if (m_end > prm->steps || m_begin > m_end)
+    return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "state already at the final step");
+  CK(cudaSetDevice(ctx->device));
+  for (int r = 1; r < nranks; ++r) CK(cudaStreamSynchronize(ctxs[r]->stream));  // their prep is done
+  CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+  if (m_end == m_begin) {
+    CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+    return SBG_OK;
+  }
+  const bool honours_a = prm->variant == SBG_GDSB;
+  PhaseConsts k;
+  k.a = honours_a ? float(prm->a) : 0.0f;
+  k.c = float(prm->c);
+  k.dt = float(prm->dt);
+  k.inv = 0.0f;
+  const int cur = ctx->g_cur;
+  const int32_t ns = int32_t(m_end - m_begin);
+  std::vector<MultiStepArgs> args(static_cast<size_t>(nranks));
+  std::vector<TmaMaps> maps(static_cast<size_t>(nranks));
+  for (int r = 0; r < nranks; ++r) {
+    sbg_ctx* c = ctxs[r];
+    MultiStepArgs& a = args[size_t(r)];
+    std::memset(&a, 0, sizeof a);
+    a.n = int32_t(c->n);
+    a.npad = int32_t(c->npad);
+    a.R = int32_t(c->R);
+    a.rpad = int32_t(c->rpad);
+    a.num_m = int32_t(c->npad / 128);
+    a.num_n = int32_t(c->rpad / NPAIR_SIGN);
+    a.k = k;
+    a.M = prm->steps;
+    a.t_begin = m_begin;
+    a.nsteps = ns;
+    a.done = c->d_done;
+    a.kpad = int32_t(c->kpad);
+    a.num_m_total = int32_t(c->num_m_total);
+    a.col0 = int32_t(c->row0);
+    a.done_base = c->done_base;
+    a.g_ld = c->kpad / 2;
+    a.npeers = int32_t(c->peer_done.size());
+    a.err = c->d_err;
+    for (int pr = 0; pr < a.npeers; ++pr) {
+      a.peer_g[0][pr] = cur == 0 ? c->peer_g1[size_t(pr)] : c->peer_g0[size_t(pr)];
+      a.peer_g[1][pr] = cur == 0 ? c->peer_g0[size_t(pr)] : c->peer_g1[size_t(pr)];
+      a.peer_done[pr] = c->peer_done[size_t(pr)];
+    }
+    a.ksplit = 1;
+    maps[size_t(r)] = c->pqmaps_sign[cur];
+  }
+  // rank tables in device memory (CUtensorMap needs 64-byte alignment: cudaMalloc gives 256)
+  const size_t abytes = sizeof(MultiStepArgs) * size_t(nranks), mbytes = sizeof(TmaMaps) * size_t(nranks);
+  const size_t moff = (mbytes + 255) / 256 * 256;
+  if (ctx->fused_cap < moff + abytes) {
+    cudaFree(ctx->d_fused);
+    ctx->d_fused = nullptr;
+    ctx->fused_cap = 0;
+    CK(cudaMalloc(&ctx->d_fused, moff + abytes));
+    ctx->fused_cap = moff + abytes;
+  }
+  uint8_t* dmaps = static_cast<uint8_t*>(ctx->d_fused);
+  uint8_t* dargs = dmaps + moff;
+  CK(cudaMemcpyAsync(dmaps, maps.data(), mbytes, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(dargs, args.data(), abytes, cudaMemcpyHostToDevice, ctx->stream));
+  MultiStepArgs a0 = args[0];
+  a0.ranks = nranks;
+  a0.rank_args = reinterpret_cast<const MultiStepArgs*>(dargs);
+  a0.rank_maps = reinterpret_cast<const TmaMaps*>(dmaps);
+  using Cfg = PairStepCfg<1, NPAIR_SIGN, 5, 2, 16, true>;
+  auto kern = gsb_multistep_pair_kernel<1, NPAIR_SIGN, 5, 2, 16, true, 1, true>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  const int cpr = 2 * ((ctx->sms / 2) / nranks);
+  CK(launch_persistent(kern, cpr * nranks, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream, maps[0], a0));
+  CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));  // the other ranks' streams see the results
+  for (int r = 0; r < nranks; ++r) {
+    sbg_ctx* c = ctxs[r];
+    ++c->launches;
+    c->done_base += uint32_t(ns) * uint32_t(c->num_m_total);
+    c->g_cur = cur ^ int(ns & 1);
+    const int rc = shard_wait_check(c);
+    if (rc) return ctx->fail(SBG_ERR_CUDA, "rank %d: %s", r, c->err.c_str());
+  }
   return SBG_OK;
 }
 

@@ -85,11 +85,19 @@ struct PairStepCfg {
   static_assert(NA == 1 || (NA == 3 && NPLANES == 4 && !Q4), "real J: continuous variants, int8 planes");
 };
 
-template <int NPLANES, int N_PAIR, int STAGES_, int NBUF_, int CW_ = 16, bool Q4_ = false, int NA_ = 1>
+template <int NPLANES, int N_PAIR, int STAGES_, int NBUF_, int CW_ = 16, bool Q4_ = false, int NA_ = 1,
+          bool FUSED = false>
 __global__ void __cluster_dims__(2, 1, 1)
     __launch_bounds__(PairStepCfg<NPLANES, N_PAIR, STAGES_, NBUF_, CW_, Q4_, NA_>::THREADS, 1)
-        gsb_multistep_pair_kernel(const __grid_constant__ TmaMaps maps, const MultiStepArgs args) {
+        gsb_multistep_pair_kernel(const __grid_constant__ TmaMaps maps_p, const __grid_constant__ MultiStepArgs args_p) {
   using Cfg = PairStepCfg<NPLANES, N_PAIR, STAGES_, NBUF_, CW_, Q4_, NA_>;
+  // FUSED: this CTA's rank of a fused row-shard emulation (MultiStepArgs::ranks); rank groups
+  // hold an even number of CTAs, so a cluster never straddles two ranks
+  const int cpr = FUSED ? static_cast<int>(gridDim.x) / args_p.ranks : static_cast<int>(gridDim.x);
+  const int rank = FUSED ? static_cast<int>(blockIdx.x) / cpr : 0;
+  const MultiStepArgs& args = FUSED ? args_p.rank_args[rank] : args_p;
+  const TmaMaps& maps = FUSED ? args_p.rank_maps[rank] : maps_p;
+  const int bid = FUSED ? static_cast<int>(blockIdx.x) % cpr : static_cast<int>(blockIdx.x);
   constexpr int NA = Cfg::NA;
   constexpr int NACC = Cfg::NACC;
   constexpr int STAGES = Cfg::STAGES;
@@ -172,8 +180,8 @@ __global__ void __cluster_dims__(2, 1, 1)
   auto n_of = [&](int w) { return args.n_fast ? w % args.num_n : w / num_mp; };
   auto mp_of = [&](int w) { return args.n_fast ? w / args.num_n : w % num_mp; };
   const int total = T2K * args.nsteps;
-  const int pair = blockIdx.x >> 1;
-  const int npairs = gridDim.x >> 1;
+  const int pair = bid >> 1;
+  const int npairs = cpr >> 1;
   const int KB = args.kpad / (Cfg::BK * Cfg::KPB);
   // Row shards (npeers > 0, K7): counters also count the peers' m-blocks (num_m_total per
   // step) and are released by other GPUs over NVLink, so waits are system-scope.

@@ -127,6 +127,14 @@ struct MultiStepArgs {
   // CTA-pair kernel tile order within a step: 0 = spin pair-blocks fastest, 1 = replica blocks
   // fastest (the replica blocks of one pair-block run side by side and share its J reads in L2)
   int32_t n_fast;
+  // Fused rank emulation (CTA-pair kernel instantiated with FUSED, test-only): `ranks` row
+  // shards of ONE GPU in one cooperative launch, CTAs [r * grid / ranks, (r + 1) * grid / ranks)
+  // running rank r with rank_args[r] / rank_maps[r] (device memory), so the multi-step
+  // cross-rank waits execute inside one launch (kernels that wait on one another must never be
+  // separate launches on one GPU).
+  int32_t ranks;
+  const MultiStepArgs* rank_args;
+  const TmaMaps* rank_maps;
 };
 constexpr int MAX_PEERS = 7;
 

@@ -112,6 +112,21 @@ def connect_row_shards_local(solvers) -> None:
         s.shard_set_peers([b for j, b in enumerate(bufs) if j != k])
 
 
+def advance_row_shards_fused(solvers, cfg, m_begin: int, m_end: int) -> float:
+    """Test-only: advance row shards that ALL live on one GPU (wired with
+    connect_row_shards_local, prepared with shard_prepare / shard_push_slab) from m_begin to
+    m_end in ONE cooperative launch, each rank on its own group of CTA pairs, so the multi-step
+    cross-rank waits run as they would over NVLink (sbg_shard_advance_fused). Returns the
+    device milliseconds of the launch."""
+    import ctypes as C
+
+    lib = solvers[0]._L
+    hs = (C.c_void_p * len(solvers))(*[s._h for s in solvers])
+    prm = solvers[0].params(cfg)
+    solvers[0]._check(lib.sbg_shard_advance_fused(hs, len(solvers), C.byref(prm), m_begin, m_end))
+    return solvers[0].last_advance_ms()
+
+
 def connect_row_shards_ipc(solver, group=None) -> None:
     """Peer wiring across processes (one rank per GPU): CUDA IPC handles of every rank's
     (G0, G1, done) are all-gathered over torch.distributed and opened locally."""

@@ -114,3 +114,57 @@ def test_hash_couplings_match_oracle_and_shards(orc, shard_kernel):
     finally:
         for s in shards:
             s.close()
+
+
+@pytest.mark.parametrize("n,R,world,chunks", [(3000, 300, 2, (0, 5, 13)), (6000, 256, 4, (0, 1, 9, 12)),
+                                              (8000, 100, 8, (0, 7))])
+def test_fused_multistep_row_shards_equal_unsharded(orc, n, R, world, chunks):
+    """The K7 protocol MULTI-STEP: `world` e2m1 row shards on this GPU advanced in one
+    cooperative launch per chunk (sbg_shard_advance_fused: each rank on its own CTA pairs, the
+    same system-scope waits on peer counters and epilogue slab pushes as across GPUs), chunks
+    of several steps back to back with no host barrier between the ranks' steps, a mid-run
+    readout_partial between two chunks -- bitwise equal to the unsharded run."""
+    from paper_2508_17655_b200 import InitMode, Solver, SolverConfig, Variant
+    from paper_2508_17655_b200.distributed import (advance_row_shards_fused, connect_row_shards_local, row_shard,
+                                                   row_sharded_energies)
+
+    M = 200
+    J = orc.gen_dense_i8(n, 29)
+    cfg = SolverConfig(variant=Variant.gdsb, steps=M, dt=1.25, c=1 / (2 * np.sqrt(n)), a=0.2)
+    mid = chunks[len(chunks) // 2]
+    with Solver(0) as full:
+        full.set_instance(J)
+        full.init_state(R, InitMode.small_uniform, 5, 7)
+        full.advance(cfg, 0, mid)
+        _, fe_mid, _, _ = full.readout()
+        full.advance(cfg, mid, chunks[-1])
+        fx, fy, fp = full.get_state()
+        _, fe, _, _ = full.readout()
+    shards = [Solver(0) for _ in range(world)]
+    try:
+        for k, s in enumerate(shards):
+            row0, valid, _ = row_shard(n, world, k)
+            s.set_instance_rows(J[row0:row0 + valid], n, world, k)
+            assert s.operand_format == "e2m1"
+            s.init_state(R, InitMode.small_uniform, 5, 7)
+        connect_row_shards_local(shards)
+        for s in shards:
+            s.shard_prepare(Variant.gdsb)
+        for s in shards:
+            s.shard_push_slab()
+        for m0, m1 in zip(chunks[:-1], chunks[1:]):
+            assert advance_row_shards_fused(shards, cfg, m0, m1) > 0
+            if m1 == mid:
+                assert (row_sharded_energies([s.readout_partial() for s in shards]) == fe_mid).all()
+        parts = []
+        for k, s in enumerate(shards):
+            row0, valid, _ = row_shard(n, world, k)
+            x, y, p = s.get_state()
+            assert (x == fx[:, row0:row0 + valid]).all(), k
+            assert (y == fy[:, row0:row0 + valid]).all(), k
+            assert (p == fp[:, row0:row0 + valid]).all(), k
+            parts.append(s.readout_partial())
+        assert (row_sharded_energies(parts) == fe).all()
+    finally:
+        for s in shards:
+            s.close()
