@@ -120,7 +120,8 @@ def lib() -> C.CDLL:
     L.sbg_shard_set_peers.argtypes = [P, i32, P, P, P]
     L.sbg_shard_prepare.argtypes = [P, i32]
     L.sbg_shard_push_slab.argtypes = [P]
-    L.sbg_shard_advance_fused.argtypes = [P, i32, P, u64, u64]
+    if hasattr(L, "sbg_shard_advance_fused"):  # (dev A/B against builds that predate it)
+        L.sbg_shard_advance_fused.argtypes = [P, i32, P, u64, u64]
     L.sbg_shard_ipc_export.argtypes = [P, P]
     L.sbg_shard_ipc_open.argtypes = [P, P, P, P, P]
     L.sbg_readout_partial.argtypes = [P, P]

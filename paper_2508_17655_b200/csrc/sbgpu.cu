@@ -2029,6 +2029,13 @@ int launch_ts(sbg_ctx* ctx, int cur, const MultiStepArgs& a, int groups, const u
     ctx->ts_cache[cur] = tm;
     ctx->ts_key[cur] = key;
     ctx->ts_ok[cur] = true;
+    // the other G-buffer parity too (an odd-length advance flips it): the next launch hits
+    TsMaps other = tm;
+    rc = encode_part_maps(ctx, &other.g, cur ^ 1, T::W[0], T::W[PARTS - 1]);
+    if (rc) return rc;
+    ctx->ts_cache[cur ^ 1] = other;
+    ctx->ts_key[cur ^ 1] = key;
+    ctx->ts_ok[cur ^ 1] = true;
   }
   if (a.nsteps < 1) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "resident launch without steps");
   return launch_resident<16, 4, ST, RES_NR, true, -PARTS, true, TsMaps, PKB, KH2>(ctx, tm, a, 0, groups, ready);
