@@ -359,12 +359,35 @@ int launch_multistep_pair(sbg_ctx* ctx, const TmaMaps& maps, MultiStepArgs a) {
     a.fpart = ctx->d_fpart;
     a.kdone = ctx->d_kdone;
   }
-  const int64_t pair_tiles = int64_t(a.num_m / 2) * a.num_n * a.nsteps * std::max(1, a.ksplit);
+  const int64_t t2 = int64_t(a.num_m / 2) * a.num_n;
+  const int64_t tt = a.ksplit > 1 ? (a.ktail > 0 ? std::min<int64_t>(a.ktail, t2) : t2) : 0;
+  const int64_t pair_tiles = (t2 - tt + tt * std::max(1, a.ksplit)) * a.nsteps;  // work units
   const int grid = 2 * int(std::min<int64_t>(pair_tiles, ctx->sms / 2));
   if (!ctx->sharded) CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * a.num_n, ctx->stream));
+  static unsigned long long* utrace = nullptr;  // dev knob SBG_PAIR_TRACE: per (CTA, unit) stamps
+  const size_t utn = size_t(grid) * 64 * 8;
+  if (dev_knob("SBG_PAIR_TRACE")) {
+    cudaFree(utrace);
+    CK(cudaMalloc(&utrace, utn * 8));
+    CK(cudaMemsetAsync(utrace, 0, utn * 8, ctx->stream));
+    a.utrace = utrace;
+  }
   CK(launch_persistent(kern, grid, Cfg::THREADS, Cfg::SMEM_BYTES, ctx->stream, maps, a));
   ++ctx->launches;
   if (ctx->sharded) ctx->done_base += uint32_t(a.nsteps * a.num_m_total);
+  if (a.utrace) {
+    std::vector<unsigned long long> h(utn);
+    CK(cudaMemcpyAsync(h.data(), a.utrace, utn * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    FILE* f = fopen("gpurun_out/pair_utrace.txt", "w");
+    if (f) {
+      for (size_t i = 0; i < utn / 8; ++i)
+        if (h[i * 8 + 6] || h[i * 8])
+          fprintf(f, "%zu %zu %llu %llu %llu %llu %llu %llu %llu\n", i / 64, i % 64, h[i * 8], h[i * 8 + 1],
+                  h[i * 8 + 2], h[i * 8 + 3], h[i * 8 + 4], h[i * 8 + 5], h[i * 8 + 6]);
+      fclose(f);
+    }
+  }
   return SBG_OK;
 }
 
@@ -379,6 +402,23 @@ int ksplit_for(const sbg_ctx* ctx, int64_t tiles) {
   (void)tiles;
   const int knob = dev_knob("SBG_KSPLIT");
   return knob > 1 ? std::min(knob, 8) : 1;
+}
+
+// Tail-only K split (default for the e2m1 streaming pair kernel; SBG_KTAIL=0 disables): with
+// T2 pair tiles per step on P pairs and T2 >= P, the T2 mod P tiles of the last, partial round
+// run as KS = min(4, P / (T2 mod P)) K parts each, so that round takes ~1/KS of a tile instead
+// of a whole tile while every other pair idles (C5: 391 tiles on 74 pairs = 5 whole rounds + 21
+// tiles). Sets a.ksplit / a.ktail; the explicit uniform split (SBG_KSPLIT) wins when set.
+void tail_split(const sbg_ctx* ctx, int64_t tiles, MultiStepArgs& a) {
+  a.ktail = 0;
+  a.ksplit = ksplit_for(ctx, tiles);
+  if (a.ksplit > 1 || getenv_is0("SBG_KTAIL")) return;
+  const int64_t P = ctx->sms / 2, tail = tiles % P;
+  if (tiles < P || tail == 0) return;
+  const int64_t ks = std::min<int64_t>(4, P / tail);
+  if (ks < 2) return;
+  a.ksplit = int32_t(ks);
+  a.ktail = int32_t(tail);
 }
 
 // 128-replica pair tiles, replica blocks fastest (SBG_Q4_NPAIR=128; default 256): meant to fill
@@ -1688,13 +1728,22 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
           // non-resident sign launches are the large-N J-streaming regime (C5: 2.06 ms/step,
           // 0.79 of HBM with 5 operand stages vs 2.29 ms with 3); e2m1 operands halve J
           default:
-            a.ksplit = q4s ? ksplit_for(ctx, (ctx->npad / 256) * (ctx->rpad / NPAIR_SIGN)) : 1;
+            if (q4s)
+              tail_split(ctx, (ctx->npad / 256) * (ctx->rpad / NPAIR_SIGN), a);
+            else
+              a.ksplit = 1;
             if (q4s && q4_narrow(ctx)) {
               a.n_fast = 1;
               rc = launch_multistep_pair<1, 128, 5, 2, 16, true>(ctx, ctx->pq128maps_sign[cur], a);
             } else {
-              rc = q4s ? launch_multistep_pair<1, NPAIR_SIGN, 5, 2, 16, true>(ctx, ctx->pqmaps_sign[cur], a)
-                       : launch_multistep_pair<1, NPAIR_SIGN, 5, 2>(ctx, ctx->maps_sign[cur], a);
+              const int c5 = dev_knob("SBG_C5_CFG");  // dev: (operand stages, state buffers) alternatives
+              if (q4s && c5 == 43)
+                rc = launch_multistep_pair<1, NPAIR_SIGN, 4, 3, 16, true>(ctx, ctx->pqmaps_sign[cur], a);
+              else if (q4s && c5 == 34)
+                rc = launch_multistep_pair<1, NPAIR_SIGN, 3, 4, 16, true>(ctx, ctx->pqmaps_sign[cur], a);
+              else
+                rc = q4s ? launch_multistep_pair<1, NPAIR_SIGN, 5, 2, 16, true>(ctx, ctx->pqmaps_sign[cur], a)
+                         : launch_multistep_pair<1, NPAIR_SIGN, 5, 2>(ctx, ctx->maps_sign[cur], a);
             }
         }
       } else {

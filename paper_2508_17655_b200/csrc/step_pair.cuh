@@ -29,7 +29,20 @@
 #include "ptx.cuh"
 #include "step_tma.cuh"
 
+#ifndef SBG_Q4_EARLY
+#define SBG_Q4_EARLY 1  // e2m1 pair kernel drains its single accumulator early (C5 1013 -> 973 us; 0: off)
+#endif
+#ifndef SBG_PAIR_STATE_PF
+#define SBG_PAIR_STATE_PF 0  // 1: L2 prefetch of a tile's state at its start (measured slower at C5: 1043 vs 1014 us)
+#endif
+
 namespace sbg {
+
+__device__ __forceinline__ unsigned long long gtimer_pair() {  // dev traces (%globaltimer, ns)
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Q4_ (sign plane only): packed e2m1 J and G with kind::mxf4 MMAs, as in step_resident.cuh
 // -- half the J bytes per step (the bound of the J-streaming regime, C5) at twice the MMA
@@ -67,7 +80,10 @@ struct PairStepCfg {
   // accumulator buffers: 2 when they fit TMEM; 1 for e2m1 (scale factors) or wide tiles, whose
   // epilogue (non-e2m1) then drains all accumulator columns before the state update
   static constexpr int NACC = (Q4 || 2 * ACC_COLS > 512) ? 1 : 2;
-  static constexpr bool EARLY_DRAIN = !Q4 && NACC == 1;
+  // e2m1 too with SBG_Q4_EARLY: the single accumulator (the scale factors leave no room for a
+  // second) is drained to registers and released before the state update, so the next tile's
+  // MMAs overlap the update instead of waiting for it
+  static constexpr bool EARLY_DRAIN = (!Q4 || SBG_Q4_EARLY) && NACC == 1;
   // all digit planes in one MMA (N = NPLANES * N_PAIR <= 256). The pair's output columns are
   // then [CTA 0's B rows][CTA 1's B rows], each [plane][B_HALF replicas]: plane p of replica
   // r (of the tile) sits at column (r / B_HALF) * NPLANES * B_HALF + p * B_HALF + r % B_HALF
@@ -176,7 +192,22 @@ __global__ void __cluster_dims__(2, 1, 1)
   const int num_mp = args.num_m / 2;
   const int T2 = num_mp * args.num_n;  // pair tiles per step
   const int KS = args.ksplit > 1 ? args.ksplit : 1;
-  const int T2K = T2 * KS;             // work units per step: (pair tile, K part), parts adjacent
+  // K split: the last TT pair tiles of each step run as KS K-part units (parts adjacent; all
+  // tiles when ktail <= 0), the first T2 - TT as whole units -- with ktail = T2 mod npairs the
+  // split fills the last, partial round of tiles instead of leaving pairs idle
+  const int TT = KS > 1 ? (args.ktail > 0 ? min(args.ktail, T2) : T2) : 0;
+  const int TW = T2 - TT;
+  const int T2K = TW + TT * KS;        // work units per step
+  // unit g -> step s, pair tile w, K part kp of ks
+  auto unit = [&](int g, int& s, int& w, int& kp, int& ks) {
+    s = g / T2K;
+    const int u = g % T2K;
+    if (u < TW) {
+      w = u, kp = 0, ks = 1;
+    } else {
+      w = TW + (u - TW) / KS, kp = (u - TW) % KS, ks = KS;
+    }
+  };
   auto n_of = [&](int w) { return args.n_fast ? w % args.num_n : w / num_mp; };
   auto mp_of = [&](int w) { return args.n_fast ? w / args.num_n : w % num_mp; };
   const int total = T2K * args.nsteps;
@@ -206,12 +237,13 @@ __global__ void __cluster_dims__(2, 1, 1)
       uint32_t ph = 0;
       const uint64_t keep = ptx::policy_evict_last();  // J and G are re-read every step: keep them in L2
       for (int g = pair; g < total; g += npairs) {
-        const int s = g / T2K, w = (g % T2K) / KS, kp = (g % T2K) % KS;
+        int s, w, kp, ks;
+        unit(g, s, w, kp, ks);
         const int n_blk = n_of(w), mp = mp_of(w);
         const int m_blk = 2 * mp + static_cast<int>(cr);
         wait_dep(n_blk, s);
         const CUtensorMap* gin = &maps.Gin[s & 1];
-        for (int kb = kp * KB / KS; kb < (kp + 1) * KB / KS; ++kb) {
+        for (int kb = kp * KB / ks; kb < (kp + 1) * KB / ks; ++kb) {
           ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
           if (ptx::elect_one()) {
             const uint32_t fb = ptx::mapa(full_bar(stage), 0);  // the leader's full barrier
@@ -246,11 +278,19 @@ __global__ void __cluster_dims__(2, 1, 1)
       int lt = 0;
       for (int g = pair; g < total; g += npairs, ++lt) {
         const int buf = lt % NACC;
-        const int kp = (g % T2K) % KS, kb0 = kp * KB / KS;
+        int s_, w_, kp, ks;
+        unit(g, s_, w_, kp, ks);
+        const int kb0 = kp * KB / ks;
+        auto ust = [&](int k) {
+          if (args.utrace && lt < 64 && lane == 0)
+            args.utrace[(static_cast<size_t>(blockIdx.x) * 64 + lt) * 8 + k] = gtimer_pair();
+        };
+        ust(5);
         ptx::mbar_wait(tempty_bar(buf), ((lt / NACC) & 1) ^ 1u);
+        ust(0);
         ptx::tc_fence_after();
         const uint32_t d_base = tmem_base + buf * Cfg::ACC_COLS;
-        for (int kb = kb0; kb < (kp + 1) * KB / KS; ++kb) {
+        for (int kb = kb0; kb < (kp + 1) * KB / ks; ++kb) {
           ptx::mbar_wait(full_bar(stage), ph);
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
@@ -302,6 +342,7 @@ __global__ void __cluster_dims__(2, 1, 1)
         }
         if (ptx::elect_one()) ptx::mma_commit_pair_mc(tfull_bar(buf), 0x3);
         __syncwarp();
+        ust(1);
       }
     }
   } else if (warp == 2) {
@@ -312,11 +353,21 @@ __global__ void __cluster_dims__(2, 1, 1)
       int ck = 0;
       const uint64_t stream = ptx::policy_evict_first();  // x, y, p are touched once per step
       for (int g = pair; g < total; g += npairs) {
-        const int s = g / T2K, w = (g % T2K) / KS;
-        if ((g % T2K) % KS != KS - 1) continue;  // only the last K part updates the state
+        int s, w, kp, ks;
+        unit(g, s, w, kp, ks);
+        if (kp != ks - 1) continue;  // only the last K part updates the state
         const int n_blk = n_of(w), mp = mp_of(w);
         wait_dep(n_blk, s);
         const int i0 = (2 * mp + static_cast<int>(cr)) * Cfg::BM, rb = n_blk * N_PAIR;
+#if SBG_PAIR_STATE_PF
+        // the whole tile's x, y, p into L2 now, while its MMAs run: the 2-deep ring below then
+        // refills from L2 during the epilogue instead of paying an HBM round trip per chunk
+        for (int c = NBUF; c < CHUNKS; ++c) {
+          ptx::tma_prefetch_2d(&maps.X, i0, rb + c * CW);
+          ptx::tma_prefetch_2d(&maps.Y, i0, rb + c * CW);
+          ptx::tma_prefetch_2d(&maps.P, i0, rb + c * CW);
+        }
+#endif
         for (int c = 0; c < CHUNKS; ++c, ++ck) {
           const int b = ck % NBUF;
           ptx::mbar_wait(sempty_bar(b), ((ck / NBUF) & 1) ^ 1u);
@@ -341,8 +392,9 @@ __global__ void __cluster_dims__(2, 1, 1)
     const uint64_t keep = ptx::policy_evict_last();
     constexpr int GROW = Cfg::BM / Cfg::KPB;  // bytes of one replica row of a G chunk
     for (int g = pair; g < total; g += npairs) {
-      const int s = g / T2K, w = (g % T2K) / KS;
-      if ((g % T2K) % KS != KS - 1) continue;
+      int s, w, kp, ks;
+      unit(g, s, w, kp, ks);
+      if (kp != ks - 1) continue;
       const int n_blk = n_of(w), mp = mp_of(w);
       const int i0 = (2 * mp + static_cast<int>(cr)) * Cfg::BM, rb = n_blk * N_PAIR;
       const CUtensorMap* gout = &maps.Gout[s & 1];
@@ -410,7 +462,8 @@ __global__ void __cluster_dims__(2, 1, 1)
     int ck = 0;
     int lt = 0;
     for (int g = pair; g < total; g += npairs, ++lt) {
-      const int s = g / T2K, w = (g % T2K) / KS, kp = (g % T2K) % KS;
+      int s, w, kp, ks;
+      unit(g, s, w, kp, ks);
       const int rbase = n_of(w) * N_PAIR;  // first replica of this pair tile
       const int m_blk = 2 * mp_of(w) + static_cast<int>(cr);
       k.inv = __frcp_rn(static_cast<float>(args.M - (args.t_begin + static_cast<uint64_t>(s))));
@@ -418,6 +471,12 @@ __global__ void __cluster_dims__(2, 1, 1)
       if (args.dbg < 2) ptx::mbar_wait(tfull_bar(buf), (lt / NACC) & 1);
       __syncwarp();
       ptx::tc_fence_after();
+      const bool utr = args.utrace && lt < 64 && threadIdx.x == 4 * 32;
+      auto ust = [&](int k) {
+        if (utr) args.utrace[(static_cast<size_t>(blockIdx.x) * 64 + lt) * 8 + k] = gtimer_pair();
+      };
+      ust(2);
+      if (utr) args.utrace[(static_cast<size_t>(blockIdx.x) * 64 + lt) * 8 + 6] = (uint64_t(s) << 40) | (uint64_t(w) << 8) | (uint64_t(kp) << 4) | uint64_t(ks);
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * Cfg::ACC_COLS;
       // K split: partial fields of parts 0..KS-2, replica-major so a warp's 32 rows are contiguous
       const size_t frow = static_cast<size_t>(m_blk) * Cfg::BM + srow;
@@ -470,7 +529,7 @@ __global__ void __cluster_dims__(2, 1, 1)
           for (int j = 0; j < CWQ; ++j) F[j] = __fmul_rn(__ll2float_rn(tot[j]), 0x1p-30f);
         }
       };
-      if (NPLANES == 1 && KS > 1 && kp != KS - 1) {
+      if (NPLANES == 1 && ks > 1 && kp != ks - 1) {
         // a leading K part: publish the partial field, free the accumulator, count the part
 #pragma unroll
         for (int c = 0; c < CHUNKS; ++c) {
@@ -487,9 +546,10 @@ __global__ void __cluster_dims__(2, 1, 1)
           __threadfence();
           dep::release_add(args.kdone + static_cast<size_t>(n_of(w)) * args.num_m + m_blk, 1u);
         }
+        ust(4);
         continue;
       }
-      if (NPLANES == 1 && KS > 1) {  // the last K part: wait for the other parts of this tile
+      if (NPLANES == 1 && ks > 1) {  // the last K part: wait for the other parts of this tile
         if (threadIdx.x == 4 * 32) {
           const uint32_t need = static_cast<uint32_t>((KS - 1) * (s + 1));
           const uint32_t* kd = args.kdone + static_cast<size_t>(n_of(w)) * args.num_m + m_blk;
@@ -497,6 +557,7 @@ __global__ void __cluster_dims__(2, 1, 1)
           __threadfence();
         }
         ptx::named_bar_sync(1, Cfg::EPI_WARPS * 32);
+        ust(3);
       }
       float Fall[Cfg::EARLY_DRAIN ? CHUNKS : 1][CWQ];
       if constexpr (Cfg::EARLY_DRAIN) {  // one accumulator buffer: drain, release, then update
@@ -517,9 +578,9 @@ __global__ void __cluster_dims__(2, 1, 1)
         } else {
           load_F(c, F);
         }
-        if (NPLANES == 1 && KS > 1) {
+        if (NPLANES == 1 && ks > 1) {
           // exact integers below 2^24 (|F| <= kpad): fp32 sums in any order are exact
-          for (int part = 0; part < KS - 1; ++part)
+          for (int part = 0; part < ks - 1; ++part)
 #pragma unroll
             for (int j = 0; j < CWQ; ++j) F[j] += __ldcg(fpart_at(part, col0 + j));
         }
@@ -556,6 +617,7 @@ __global__ void __cluster_dims__(2, 1, 1)
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(sdone_bar(b));
       }
+      ust(4);
       if constexpr (!Cfg::EARLY_DRAIN) {
         ptx::tc_fence_before();
         __syncwarp();

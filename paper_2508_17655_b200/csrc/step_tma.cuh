@@ -122,6 +122,8 @@ struct MultiStepArgs {
   // fpart[kp][rpad][npad] and count kdone[n_blk * num_m + m_blk]; unit ksplit-1 adds them to
   // its own and runs the state update. ksplit <= 1: no split.
   int32_t ksplit;
+  int32_t ktail;  // > 0: only the last ktail pair tiles of a step are split (the rest run whole)
+  unsigned long long* utrace;  // dev (SBG_PAIR_TRACE): per (CTA, unit slot) %globaltimer stamps, 8 each
   float* fpart;
   uint32_t* kdone;
   // CTA-pair kernel tile order within a step: 0 = spin pair-blocks fastest, 1 = replica blocks

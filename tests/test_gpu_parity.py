@@ -700,3 +700,31 @@ def test_e2m1_stream_k_split_bitwise(solver, orc, monkeypatch, ks):
     for st in out[1:]:
         for a, b in zip(out[0], st):
             assert (a.view(np.uint32) == b.view(np.uint32)).all()
+
+
+@pytest.mark.parametrize("n,R", [(19200, 256), (25600, 300), (19200, 37)])
+def test_e2m1_stream_tail_split_bitwise(solver, monkeypatch, n, R):
+    """The default tail-only K split of the streaming e2m1 pair kernel (the T2 mod P tiles of a
+    step's last, partial round of pair tiles run as K parts: 75 tiles on 74 pairs -> 1 tile in
+    4 parts; 100 -> 26 tiles in 2 parts; two replica blocks -> 150 tiles) == no split
+    (SBG_KTAIL=0), bitwise, with per-replica A, over two launches."""
+    from paper_2508_17655_b200 import InitMode
+
+    cfg = cfg_for(GDSB, 100, 1.25, float(1 / (2 * np.sqrt(n))), 0.2)
+    a_rep = np.linspace(0.0, 0.5, R).astype(np.float32)
+    out = []
+    for env in ({}, {"SBG_KTAIL": "0"}):
+        for key in ("SBG_RESIDENT", "SBG_KSPLIT", "SBG_KTAIL", "SBG_Q4_NPAIR"):
+            monkeypatch.delenv(key, raising=False)
+        for key, v in env.items():
+            monkeypatch.setenv(key, v)
+        solver.gen_random_dense(n, 3)
+        assert solver.operand_format == "e2m1"
+        solver.init_state(R, InitMode.small_uniform, 2, 7)
+        solver.set_replica_a(a_rep)
+        solver.advance(cfg, 0, 5)
+        solver.advance(cfg, 5, 12)
+        out.append(solver.get_state())
+        solver.set_replica_a(None)
+    for a, b in zip(out[0], out[1]):
+        assert (a.view(np.uint32) == b.view(np.uint32)).all()
