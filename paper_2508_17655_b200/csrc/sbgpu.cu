@@ -1660,6 +1660,9 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
       a.nsteps = int32_t(ns);
       a.done = ctx->d_done;
       a.a_rep = (honours_a && ctx->d_arep && ctx->arep_n == ctx->R) ? ctx->d_arep : nullptr;
+      a.sx = ctx->dX;
+      a.sy = ctx->dY;
+      a.sp = ctx->dP;
       const int cur = ctx->g_cur;
       a.kpad = int32_t(ctx->sharded ? ctx->kpad : ctx->npad);
       a.num_m_total = int32_t(ctx->sharded ? ctx->num_m_total : ctx->npad / 128);

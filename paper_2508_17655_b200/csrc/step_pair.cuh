@@ -29,6 +29,9 @@
 #include "ptx.cuh"
 #include "step_tma.cuh"
 
+#ifndef SBG_PAIR_DIRECT
+#define SBG_PAIR_DIRECT 0  // 1: direct-state epilogue (bitwise equal; measured slower: C1 15.8 -> 16.2, C4 199 -> 202 us)
+#endif
 #ifndef SBG_Q4_EARLY
 #define SBG_Q4_EARLY 1  // e2m1 pair kernel drains its single accumulator early (C5 1013 -> 973 us; 0: off)
 #endif
@@ -84,6 +87,11 @@ struct PairStepCfg {
   // second) is drained to registers and released before the state update, so the next tile's
   // MMAs overlap the update instead of waiting for it
   static constexpr bool EARLY_DRAIN = (!Q4 || SBG_Q4_EARLY) && NACC == 1;
+  // continuous variants (digit planes): x, y, p go between HBM and the epilogue threads' registers
+  // directly (coalesced 128 B per warp and replica) instead of through the shared-memory ring and
+  // TMA -- the ring then only stages the G planes. Shared memory is what paces these kernels
+  // (TMA writes + MMA operand reads + the state passes); this removes four state passes.
+  static constexpr bool DIRECT = SBG_PAIR_DIRECT && NPLANES > 1 && !Q4;
   // all digit planes in one MMA (N = NPLANES * N_PAIR <= 256). The pair's output columns are
   // then [CTA 0's B rows][CTA 1's B rows], each [plane][B_HALF replicas]: plane p of replica
   // r (of the tile) sits at column (r / B_HALF) * NPLANES * B_HALF + p * B_HALF + r % B_HALF
@@ -371,6 +379,10 @@ __global__ void __cluster_dims__(2, 1, 1)
         for (int c = 0; c < CHUNKS; ++c, ++ck) {
           const int b = ck % NBUF;
           ptx::mbar_wait(sempty_bar(b), ((ck / NBUF) & 1) ^ 1u);
+          if constexpr (Cfg::DIRECT) {  // only the G staging slot: free -> hand it to the epilogue
+            ptx::mbar_arrive(sfull_bar(b));
+            continue;
+          }
           ptx::mbar_arrive_expect_tx(sfull_bar(b), 3 * Cfg::ST_ARR);
           const uint32_t sb = s_base + b * Cfg::BUF_BYTES;
           ptx::tma_load_2d_hint(sb, &maps.X, sfull_bar(b), i0, rb + c * CW, stream);
@@ -404,9 +416,11 @@ __global__ void __cluster_dims__(2, 1, 1)
         const uint32_t sb = s_base + b * Cfg::BUF_BYTES;
         const int r0 = rb + c * CW;
         if (lane == 0) {
-          ptx::tma_store_2d_hint(&maps.X, sb, i0, r0, stream);
-          ptx::tma_store_2d_hint(&maps.Y, sb + Cfg::ST_ARR, i0, r0, stream);
-          ptx::tma_store_2d_hint(&maps.P, sb + 2 * Cfg::ST_ARR, i0, r0, stream);
+          if constexpr (!Cfg::DIRECT) {
+            ptx::tma_store_2d_hint(&maps.X, sb, i0, r0, stream);
+            ptx::tma_store_2d_hint(&maps.Y, sb + Cfg::ST_ARR, i0, r0, stream);
+            ptx::tma_store_2d_hint(&maps.P, sb + 2 * Cfg::ST_ARR, i0, r0, stream);
+          }
 #pragma unroll
           for (int pl = 0; pl < NPLANES; ++pl)
             ptx::tma_store_2d_hint(gout, sb + 3 * Cfg::ST_ARR + pl * Cfg::ST_G, (args.col0 + i0) / Cfg::KPB,
@@ -468,6 +482,25 @@ __global__ void __cluster_dims__(2, 1, 1)
       const int m_blk = 2 * mp_of(w) + static_cast<int>(cr);
       k.inv = __frcp_rn(static_cast<float>(args.M - (args.t_begin + static_cast<uint64_t>(s))));
       const int buf = lt % NACC;
+      // DIRECT: this tile's x, y, p rows (replica r, spins i0 .. i0+127: lane = spin) straight
+      // from global memory, chunk c + 1 in flight while chunk c updates. The tile's dependency
+      // (step s - 1 of its replica block complete, met before its MMAs could start) is acquired
+      // here by every thread, so the loads are ordered after the writes they depend on.
+      float dx[2][CWQ], dy[2][CWQ], dp[2][CWQ];
+      const size_t dbase = static_cast<size_t>(rbase + h * CWQ) * args.npad + m_blk * Cfg::BM + srow;
+      auto d_ld = [&](int c, int bb) {
+#pragma unroll
+        for (int j = 0; j < CWQ; ++j) {
+          const size_t o = dbase + static_cast<size_t>(c * CW + j) * args.npad;
+          dx[bb][j] = __ldcs(args.sx + o);
+          dy[bb][j] = __ldcs(args.sy + o);
+          dp[bb][j] = __ldcs(args.sp + o);
+        }
+      };
+      if constexpr (Cfg::DIRECT) {
+        if ((kp == ks - 1) && s > 0) dep::wait_block(args.done, n_of(w), args.done_base, s * args.num_m_total);
+        if (kp == ks - 1) d_ld(0, 0);
+      }
       if (args.dbg < 2) ptx::mbar_wait(tfull_bar(buf), (lt / NACC) & 1);
       __syncwarp();
       ptx::tc_fence_after();
@@ -584,6 +617,9 @@ __global__ void __cluster_dims__(2, 1, 1)
 #pragma unroll
             for (int j = 0; j < CWQ; ++j) F[j] += __ldcg(fpart_at(part, col0 + j));
         }
+        if constexpr (Cfg::DIRECT) {
+          if (c + 1 < CHUNKS) d_ld(c + 1, (c + 1) & 1);
+        }
         ptx::mbar_wait(sfull_bar(b), (ck / NBUF) & 1);
         float* xs = reinterpret_cast<float*>(s_gen + b * Cfg::BUF_BYTES);
         float* ys = xs + CW * Cfg::BM;
@@ -592,13 +628,25 @@ __global__ void __cluster_dims__(2, 1, 1)
 #pragma unroll
         for (int j = 0; j < CWQ; ++j) {
           const int idx = (h * CWQ + j) * Cfg::BM + srow;
-          float xv = xs[idx], yv = ys[idx], pv = ps[idx];
+          float xv, yv, pv;
+          if constexpr (Cfg::DIRECT) {
+            xv = dx[c & 1][j], yv = dy[c & 1][j], pv = dp[c & 1][j];
+          } else {
+            xv = xs[idx], yv = ys[idx], pv = ps[idx];
+          }
           PhaseConsts kj = k;
           if (args.a_rep) kj.a = args.a_rep[min(rbase + col0 + j, args.R - 1)];
           gsb_phase(F[j], xv, yv, pv, kj);
-          xs[idx] = xv;
-          ys[idx] = yv;
-          ps[idx] = pv;
+          if constexpr (Cfg::DIRECT) {
+            const size_t o = dbase + static_cast<size_t>(c * CW + j) * args.npad;
+            __stcs(args.sx + o, xv);
+            __stcs(args.sy + o, yv);
+            __stcs(args.sp + o, pv);
+          } else {
+            xs[idx] = xv;
+            ys[idx] = yv;
+            ps[idx] = pv;
+          }
           if constexpr (Cfg::Q4) {
             // e2m1 codes (+1 = 0x2, -1 = 0xA) two spins per byte: lanes 2i, 2i+1 hold spins
             // 2i, 2i+1 of column j; the even lane writes the byte (warp-uniform shuffle)

@@ -124,6 +124,7 @@ struct MultiStepArgs {
   int32_t ksplit;
   int32_t ktail;  // > 0: only the last ktail pair tiles of a step are split (the rest run whole)
   unsigned long long* utrace;  // dev (SBG_PAIR_TRACE): per (CTA, unit slot) %globaltimer stamps, 8 each
+  float *sx, *sy, *sp;         // replica-major state [rpad][npad] (pair kernel with direct state access)
   float* fpart;
   uint32_t* kdone;
   // CTA-pair kernel tile order within a step: 0 = spin pair-blocks fastest, 1 = replica blocks
