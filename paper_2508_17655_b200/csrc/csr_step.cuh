@@ -57,10 +57,30 @@ __device__ __forceinline__ uint64_t evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint64_t evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
+}
+// the x, y, p stream: evict_first (one pass) by default; with replica slabs (state + operands
+// sized to stay in L2 across the slab's steps) CSR_STATE_POLICY = 1 / 2 keeps it normal / last --
+// measured slower at C3: 71.8 / 75.5 vs 69.6 us/step (and with 128-replica slabs 75.3 / 76.3 vs 80.7)
+#ifndef CSR_STATE_POLICY
+#define CSR_STATE_POLICY 0
+#endif
+__device__ __forceinline__ uint64_t state_policy() {
+#if CSR_STATE_POLICY == 1
+  return evict_normal();
+#elif CSR_STATE_POLICY == 2
+  return evict_last();
+#else
+  return evict_first();
+#endif
 }
 __device__ __forceinline__ float4 ld_f4(const float* a, uint64_t pol) {
   float4 v;
@@ -107,7 +127,7 @@ __global__ void __launch_bounds__(CSR_THREADS, CSR_MIN_BLOCKS)
   const int64_t tasks = static_cast<int64_t>(n) * chunks;
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const uint64_t stream = l2::evict_first(), keep = l2::evict_last();
+  const uint64_t stream = l2::state_policy(), keep = l2::evict_last();
   // row stride of the gathered operand in bytes: row j of a lane's group is one IMAD.WIDE.U32 away
   const uint32_t rsb = static_cast<uint32_t>(rp) * (SIGN ? 1u : 4u);
   for (int64_t t = wid; t < tasks; t += nw) {
@@ -211,7 +231,7 @@ __global__ void __launch_bounds__(CSR_THREADS, MINB)
   const int64_t tasks = static_cast<int64_t>(n) * chunks;
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const uint64_t stream = l2::evict_first(), keep = l2::evict_last();
+  const uint64_t stream = l2::state_policy(), keep = l2::evict_last();
   const uint32_t rsb = static_cast<uint32_t>(rp) * (SIGN ? 1u : 4u);
   using G = std::conditional_t<SIGN, uint32_t, int4>;
   auto gather = [&](const char* src) -> G {
@@ -332,7 +352,7 @@ __global__ void __launch_bounds__(CSRA_THREADS)
   const int64_t tasks = static_cast<int64_t>(n) * chunks;
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const uint64_t stream = l2::evict_first(), keep = l2::evict_last();
+  const uint64_t stream = l2::state_policy(), keep = l2::evict_last();
   const uint32_t rsb = static_cast<uint32_t>(rp) * (SIGN ? 1u : 4u);
   for (int64_t t = wid; t < tasks; t += nw) {
     const int i = static_cast<int>(t / chunks);
