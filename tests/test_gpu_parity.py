@@ -728,3 +728,29 @@ def test_e2m1_stream_tail_split_bitwise(solver, monkeypatch, n, R):
         solver.set_replica_a(None)
     for a, b in zip(out[0], out[1]):
         assert (a.view(np.uint32) == b.view(np.uint32)).all()
+
+
+def test_ts_map_cache_follows_state_and_couplings(solver, orc):
+    """The TS kernel's tensor maps are cached per G-buffer parity (sbgpu.cu TsMapKey): one
+    Solver re-used across replica counts (new state buffers), odd and even advance lengths
+    (both parities) and a new J must step exactly like fresh solvers."""
+    from paper_2508_17655_b200 import InitMode, Solver
+
+    n = 2000
+    cfg = cfg_for(GDSB, 100, 1.25, float(1 / (2 * np.sqrt(n))), 0.2)
+    runs = [(300, 1, (0, 3, 10)), (700, 1, (0, 5, 6, 9)), (300, 2, (0, 7, 12))]
+    got = []
+    for R, seed, chunks in runs:
+        solver.gen_random_dense(n, seed)
+        solver.init_state(R, InitMode.small_uniform, 4, 7)
+        for m0, m1 in zip(chunks[:-1], chunks[1:]):
+            solver.advance(cfg, m0, m1)
+        got.append(solver.get_state())
+    for (R, seed, chunks), st in zip(runs, got):
+        with Solver(0) as fresh:
+            fresh.gen_random_dense(n, seed)
+            fresh.init_state(R, InitMode.small_uniform, 4, 7)
+            fresh.advance(cfg, 0, chunks[-1])
+            ref = fresh.get_state()
+        for a, b in zip(st, ref):
+            assert (a.view(np.uint32) == b.view(np.uint32)).all(), (R, seed)
