@@ -46,6 +46,9 @@ constexpr int CSR_RCHUNK = 128 * CSR_VEC;      // replicas per warp task
 #define CSR_UNROLL 1
 #endif
 
+#ifndef CSR_LEAN_DEFAULT
+#define CSR_LEAN_DEFAULT 2  // gathers per round of csr_step_lean_kernel (SBG_CSR_LEAN overrides)
+#endif
 constexpr int CSR_UNR = CSR_UNROLL;             // nonzeros per unrolled gather round
 constexpr int CSR_MIN_BLOCKS = CSR_MINB;       // 64 warps per SM: latency hiding for the gathers
 
@@ -209,6 +212,137 @@ __global__ void __launch_bounds__(CSR_THREADS, CSR_MIN_BLOCKS)
         l2::st_i4(static_cast<int32_t*>(g_next) + off,
                   make_int4(quant30(x4.x), quant30(x4.y), quant30(x4.z), quant30(x4.w)), keep);
       }
+    }
+  }
+}
+
+// The same step with fewer issued instructions per task (the step above runs at ~0.6 warp
+// instructions per scheduler-cycle with 64 warps per SM: issue slots, not bytes, pace it).
+//   * (row, chunk) advance incrementally per warp: no 64-bit division per task;
+//   * the row's nonzeros are staged once per task in shared memory as (column, value) and read
+//     back UNR at a time with one broadcast LDS.128 (the loop above spends two shuffles, their
+//     convergence check, a constant reload and a 64-bit add per nonzero);
+//   * the gather address is a 32-bit element index (column x rp + replica) and one scaled add;
+//   * UNR nonzeros per round with their gathers issued back to back; a ragged tail gathers row 0
+//     with value 0 (lanes >= cnt stage zeros), so the loop has no remainder code;
+//   * the phase update runs two replicas at a time on the packed FP32 pipe (gsb_phase2, bitwise
+//     gsb_phase), and all state addresses are 32-bit element offsets (host-checked: n * rp * 4 B
+//     < 4 GB, else the kernel above runs).
+// Same integer field, same update: bitwise equal (test_csr_kernel_variants_bitwise).
+template <bool SIGN, int UNR>
+__global__ void __launch_bounds__(CSR_THREADS, CSR_MIN_BLOCKS)
+    csr_step_lean_kernel(uint32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                         const int8_t* __restrict__ val, const void* __restrict__ g_cur, void* __restrict__ g_next,
+                         float* __restrict__ xs, float* __restrict__ ys, float* __restrict__ ps, uint32_t rp,
+                         uint32_t R, PhaseConsts k, PhaseIdent id, const float* __restrict__ a_rep = nullptr) {
+  static_assert(UNR == 1 || UNR == 2 || UNR == 4, "gathers per round");
+  __shared__ __align__(16) uint2 stage[CSR_THREADS / 32][32];  // (column, value) of the row's nonzeros
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t chunks = (R + CSR_RCHUNK - 1) / CSR_RCHUNK;
+  const uint32_t nw = gridDim.x * (CSR_THREADS / 32);
+  const uint32_t di = nw / chunks, dc = nw - di * chunks;
+  const uint32_t wid = blockIdx.x * (CSR_THREADS / 32) + wib;
+  uint32_t i = wid / chunks, c = wid - i * chunks;
+  const uint64_t stream = l2::state_policy(), keep = l2::evict_last();
+  const uint32_t sp = static_cast<uint32_t>(__cvta_generic_to_shared(stage[wib]));  // this warp's 256 B
+  const PhaseConsts2 k2(k, id);
+  using Acc = std::conditional_t<SIGN, int32_t, long long>;
+  while (i < n) {
+    const uint32_t r = c * CSR_RCHUNK + 4 * lane;
+    const int kb = rowptr[i], ke = rowptr[i + 1];
+    Acc acc[4] = {0, 0, 0, 0};
+    for (int k0 = kb; k0 < ke; k0 += 32) {
+      const int cnt = min(32, ke - k0);
+      uint32_t ej = 0, ev = 0;  // lanes >= cnt stage (row 0, value 0): the ragged tail of a round
+      if (static_cast<int>(lane) < cnt) {
+        ej = static_cast<uint32_t>(col[k0 + lane]);
+        ev = static_cast<uint32_t>(static_cast<int32_t>(val[k0 + lane]));
+      }
+      __syncwarp();  // the previous round's reads are done
+      asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(sp + lane * 8), "r"(ej), "r"(ev) : "memory");
+      __syncwarp();
+#pragma unroll 1
+      for (uint32_t a = sp, ae = sp + static_cast<uint32_t>(cnt) * 8; a < ae; a += 8 * UNR) {
+        uint32_t ew[2 * UNR];  // {col, val} x UNR, one broadcast load
+        if constexpr (UNR == 1) {
+          asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(ew[0]), "=r"(ew[1]) : "r"(a));
+        } else {
+#pragma unroll
+          for (int h = 0; h < UNR / 2; ++h)
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(ew[4 * h]), "=r"(ew[4 * h + 1]), "=r"(ew[4 * h + 2]), "=r"(ew[4 * h + 3])
+                         : "r"(a + 16 * h));
+        }
+        // element index of the lane's group in row col (32-bit: host-checked), then one scaled add
+        uint32_t src[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) src[u] = ew[2 * u] * rp + r;
+        if constexpr (SIGN) {
+          uint32_t w[UNR];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) w[u] = l2::ld_u32(static_cast<const int8_t*>(g_cur) + src[u], keep);
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) {
+            const int32_t v = static_cast<int32_t>(ew[2 * u + 1]);
+            const char4 s = *reinterpret_cast<const char4*>(&w[u]);
+            acc[0] += v * s.x;
+            acc[1] += v * s.y;
+            acc[2] += v * s.z;
+            acc[3] += v * s.w;
+          }
+        } else {
+          int4 q[UNR];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) q[u] = l2::ld_i4(static_cast<const int32_t*>(g_cur) + src[u], keep);
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) {
+            const long long v = static_cast<int32_t>(ew[2 * u + 1]);
+            acc[0] += v * q[u].x;
+            acc[1] += v * q[u].y;
+            acc[2] += v * q[u].z;
+            acc[3] += v * q[u].w;
+          }
+        }
+      }
+    }
+    if (r < R) {
+      const uint32_t off = i * rp + r;
+      float4 x4 = l2::ld_f4(xs + off, stream);
+      float4 y4 = l2::ld_f4(ys + off, stream);
+      float4 p4 = l2::ld_f4(ps + off, stream);
+      float F[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        F[e] = SIGN ? static_cast<float>(acc[e]) : __fmul_rn(__ll2float_rn(acc[e]), 0x1p-30f);
+      uint64_t a01 = k2.a, a23 = k2.a;
+      if (a_rep) {
+        const uint32_t last = R - 1;
+        a01 = f2::pk(a_rep[min(r, last)], a_rep[min(r + 1, last)]);
+        a23 = f2::pk(a_rep[min(r + 2, last)], a_rep[min(r + 3, last)]);
+      }
+      gsb_phase2(F[0], F[1], x4.x, x4.y, y4.x, y4.y, p4.x, p4.y, k2, a01);
+      gsb_phase2(F[2], F[3], x4.z, x4.w, y4.z, y4.w, p4.z, p4.w, k2, a23);
+      // replicas >= R inside the last group are padding: their slots exist (rp) and stay inert
+      l2::st_f4(xs + off, x4, stream);
+      l2::st_f4(ys + off, y4, stream);
+      l2::st_f4(ps + off, p4, stream);
+      if (SIGN) {
+        char4 s;
+        s.x = sgn8(x4.x);
+        s.y = sgn8(x4.y);
+        s.z = sgn8(x4.z);
+        s.w = sgn8(x4.w);
+        l2::st_u32(static_cast<int8_t*>(g_next) + off, *reinterpret_cast<uint32_t*>(&s), keep);
+      } else {
+        l2::st_i4(static_cast<int32_t*>(g_next) + off,
+                  make_int4(quant30(x4.x), quant30(x4.y), quant30(x4.z), quant30(x4.w)), keep);
+      }
+    }
+    i += di;
+    c += dc;
+    if (c >= chunks) {
+      c -= chunks;
+      ++i;
     }
   }
 }

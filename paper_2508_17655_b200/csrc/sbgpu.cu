@@ -1552,6 +1552,13 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
     // SBG_CSR_ASYNC = NB in {4, 8, 12, 16}: gathers staged through shared memory by cp.async,
     // NB per warp in flight (csr_step_async_kernel); 0 = the register-path kernel.
     const int csra = dev_knob("SBG_CSR_ASYNC");
+    // SBG_CSR_LEAN: -1 = the round-1 register-path kernel, 1 / 2 / 4 = csr_step_lean_kernel with that
+    // many gathers per round, unset = the default (needs 32-bit byte offsets into the operand)
+    int lean = dev_knob("SBG_CSR_LEAN");
+    if (lean == 0) lean = CSR_LEAN_DEFAULT;
+    if (lean != -1 && lean != 1 && lean != 2 && lean != 4)
+      return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "SBG_CSR_LEAN must be -1, 1, 2 or 4");
+    if (lean < 0 || uint64_t(ctx->npad) * uint64_t(ctx->rp) * 4 >= (1ull << 32)) lean = 0;
     if (csra && csra != 4 && csra != 8 && csra != 12 && csra != 16)
       return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "SBG_CSR_ASYNC must be 0, 4, 8, 12 or 16");
     for (int64_t r0 = 0; r0 < ctx->R; r0 += slab) {
@@ -1600,6 +1607,19 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
             if (pf == 6) CSR_PF(false, 6); else CSR_PF(false, 7);
           }
 #undef CSR_PF
+        } else if (lean) {
+          // fewer instructions per task (csr_step_lean_kernel), `lean` nonzeros per gather round
+          const PhaseIdent ident{-0.0f, 1.0f, -1.0f};
+#define CSR_LEAN(S, U)                                                                                          \
+  csr_step_lean_kernel<S, U><<<blocks, CSR_THREADS, 0, ctx->stream>>>(                                           \
+      uint32_t(n32), ctx->d_rowptr, ctx->d_col, ctx->d_val, gq[cur], gn, xs, ys, ps, uint32_t(ctx->rp), uint32_t(Rs),  \
+      km, ident, ar)
+          if (sign) {
+            if (lean == 1) CSR_LEAN(true, 1); else if (lean == 2) CSR_LEAN(true, 2); else CSR_LEAN(true, 4);
+          } else {
+            if (lean == 1) CSR_LEAN(false, 1); else if (lean == 2) CSR_LEAN(false, 2); else CSR_LEAN(false, 4);
+          }
+#undef CSR_LEAN
         } else if (sign)
           csr_step_sm_kernel<true><<<blocks, CSR_THREADS, 0, ctx->stream>>>(
               n32, ctx->d_rowptr, ctx->d_col, ctx->d_val, gq[cur], gn, xs, ys, ps, ctx->rp, Rs, km, ar);
