@@ -1567,8 +1567,10 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
     for (int64_t r0 = 0; r0 < ctx->R; r0 += slab) {
       const int32_t Rs = int32_t(std::min<int64_t>(slab, ctx->R - r0));
       const int64_t tasks = ctx->n * ((Rs + CSR_RCHUNK - 1) / CSR_RCHUNK);
-      const int blocks =
+      int blocks =
           int(std::min<int64_t>((tasks + CSR_THREADS / 32 - 1) / (CSR_THREADS / 32), int64_t(ctx->sms) * 8));
+      // dev: SBG_CSR_BLOCKS = grid size of a step launch (tasks per warp = tasks / (8 * blocks))
+      if (const int kb = dev_knob("SBG_CSR_BLOCKS"); kb > 0) blocks = std::min(blocks, kb);
       const size_t gsz = sign ? 1 : 4;
       const void* qa = reinterpret_cast<const char*>(ctx->dQ[q0]) + size_t(r0) * gsz;
       void* qb = reinterpret_cast<char*>(ctx->dQ[q0 ^ 1]) + size_t(r0) * gsz;
