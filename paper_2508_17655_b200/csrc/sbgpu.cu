@@ -470,6 +470,13 @@ int resident_nr(const sbg_ctx* ctx) {
   int rb = 0, g128 = 0, g160 = 0;
   resident_geometry(ctx, ctx->npad, ctx->rpad, &rb, &g128, 128);
   resident_geometry(ctx, ctx->npad, ctx->rpad, &rb, &g160, RES_NR);
+  // The TS kernel (e2m1 J in TMEM, npad <= 2048, four interleaved part chains) steps a 160-replica
+  // block in ~4.6 us against ~6.2 us for a 128-replica block of the single-chain kernel: take it
+  // whenever it does not ADD groups (R = 1000: 7 blocks of 160 instead of 8 of 128, one group either
+  // way). SBG_RES_NR_TS=0 restores the group-count rule (dev A/B).
+  const bool ts = ctx->dJ4 && !ctx->sharded && ctx->npad <= 2048 && !getenv_is0("SBG_RES_SPLIT") &&
+                  !getenv_is0("SBG_RES_TS") && !getenv_is0("SBG_RES_NR_TS");
+  if (ts && g160 <= g128) return RES_NR;
   return g160 < g128 ? RES_NR : 128;
 }
 
