@@ -481,18 +481,18 @@ int resident_nr(const sbg_ctx* ctx) {
 }
 
 template <int EPI, int CH, int ST = RES_STAGES, int NR = 128, bool Q4 = false, int PARTS = 0, bool JRES = false,
-          class Maps = TmaMaps, bool PKB = false, bool KH2 = false, bool MPUB = false>
+          class Maps = TmaMaps, bool PKB = false, bool KH2 = false>
 int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int group0 = 0, int ngroups = -1,
                     const uint32_t* ready = nullptr) {
   // PARTS > 0: step_resident_parts.cuh (e2m1, 160-replica blocks as PARTS interleaved column
   // parts; JRES = J resident in shared memory); else step_resident.cuh
   // PARTS < 0: step_resident_ts.cuh with -PARTS parts (J in TMEM, x, y in shared memory)
   using Cfg = std::conditional_t<
-      (PARTS < 0), TsCfg<ST, (PARTS < 0 ? -PARTS : 2), PKB, KH2, MPUB>,
+      (PARTS < 0), TsCfg<ST, (PARTS < 0 ? -PARTS : 2), PKB, KH2>,
       std::conditional_t<(PARTS > 0), PartsCfg<ST, JRES, (PARTS > 0 ? PARTS : 2)>, ResCfg<ST, EPI, CH, NR, false, Q4>>>;
   auto kern = [] {
     if constexpr (PARTS < 0)
-      return gsb_resident_ts_kernel<ST, -PARTS, PKB, KH2, MPUB>;
+      return gsb_resident_ts_kernel<ST, -PARTS, PKB, KH2>;
     else if constexpr (PARTS > 0)
       return gsb_resident_parts_kernel<ST, JRES, PARTS>;
     else
@@ -531,7 +531,6 @@ int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int
   a.dbg = dev_knob("SBG_STEP_DBG");
   a.j4 = ctx->dJ4;
   a.j4_pitch = ctx->npad / 2;
-  a.bpoll = dev_knob("SBG_TS_BPOLL") == 1;  // dev: measured equal to one wait per part (27.5 vs 27.35 us), off
   static unsigned long long* trace = nullptr;  // dev knob SBG_RES_TRACE: stamps of pair 0, group 0
   if (dev_knob("SBG_RES_TRACE")) {
     if (!trace) CK(cudaMalloc(&trace, sizeof(unsigned long long) * 16 * 4 * 4096));
@@ -579,7 +578,7 @@ int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int
     FILE* f = fopen("gpurun_out/res_trace.txt", "w");
     if (f) {
       // parts 0, 1 of each step; the TS kernel also stamps parts 2, 3 (second region)
-      const int nparts = PARTS < 0 ? 4 : 2;
+      const int nparts = (PARTS < 0 && SBG_TS_TRACE4) ? 4 : 2;
       for (int s = 0; s < a.nsteps; ++s)
         for (int c = 0; c < nparts; ++c) {
           const unsigned long long* r = &h[size_t(((c >> 1) * 2 * 4096 + s * 2 + (c & 1)) * 16)];
@@ -2060,7 +2059,7 @@ static int encode_part_maps(sbg_ctx* ctx, PartMaps* pm, int cur, int w0, int w1)
 extern "C++" {
 // The TS kernel (J in TMEM, x, y in shared memory): the parts kernel's G maps plus 2D boxes
 // {128 spins, 160 replicas} of the replica-major x and y (rows >= rpad read as zero).
-template <int PARTS, int ST, bool PKB, bool KH2 = false, bool MPUB = false>
+template <int PARTS, int ST, bool PKB, bool KH2 = false>
 int launch_ts(sbg_ctx* ctx, int cur, const MultiStepArgs& a, int groups, const uint32_t* ready) {
   using T = PartTable<PARTS>;
   TsMapKey key;
@@ -2077,7 +2076,7 @@ int launch_ts(sbg_ctx* ctx, int cur, const MultiStepArgs& a, int groups, const u
   key.w1 = T::W[PARTS - 1];
   if (!KH2 && ctx->ts_ok[cur] && ctx->ts_key[cur] == key) {
     if (a.nsteps < 1) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "resident launch without steps");
-    return launch_resident<16, 4, ST, RES_NR, true, -PARTS, true, TsMaps, PKB, KH2, MPUB>(ctx, ctx->ts_cache[cur], a, 0,
+    return launch_resident<16, 4, ST, RES_NR, true, -PARTS, true, TsMaps, PKB, KH2>(ctx, ctx->ts_cache[cur], a, 0,
                                                                                      groups, ready);
   }
   ctx->ts_ok[cur] = false;
@@ -2122,7 +2121,7 @@ int launch_ts(sbg_ctx* ctx, int cur, const MultiStepArgs& a, int groups, const u
     ctx->ts_ok[cur ^ 1] = true;
   }
   if (a.nsteps < 1) return ctx->fail(SBG_ERR_INVALID_ARGUMENT, "resident launch without steps");
-  return launch_resident<16, 4, ST, RES_NR, true, -PARTS, true, TsMaps, PKB, KH2, MPUB>(ctx, tm, a, 0, groups, ready);
+  return launch_resident<16, 4, ST, RES_NR, true, -PARTS, true, TsMaps, PKB, KH2>(ctx, tm, a, 0, groups, ready);
 }
 
 template <int PARTS, int ST, bool JRES>
@@ -2156,10 +2155,6 @@ static int launch_resident_default(sbg_ctx* ctx, int cur, const MultiStepArgs& a
         // lanes (each acquire invalidates L1) and the MMA warp's per-part poll over all eight
         // K blocks serialise more than the wait for the slowest producer they were to hide.
         const bool pkb = dev_knob("SBG_RES_PKB") == 1;
-        // SBG_TS_MPUB=1 (dev): one publisher warp per part (768 threads, setmaxnreg)
-        if (!pkb && dev_knob("SBG_TS_MPUB") == 1)
-          return dev_knob("SBG_RES_PARTS") == 5 ? launch_ts<5, 3, false, false, true>(ctx, cur, a, groups, ready)
-                                                : launch_ts<4, 2, false, false, true>(ctx, cur, a, groups, ready);
         if (dev_knob("SBG_RES_PARTS") == 5)
           return pkb ? launch_ts<5, 3, true>(ctx, cur, a, groups, ready) : launch_ts<5, 3, false>(ctx, cur, a, groups, ready);
         // SBG_RES_KH2=1: each part-step's G in two halves (MMAs on the first while the second lands)

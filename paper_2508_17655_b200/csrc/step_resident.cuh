@@ -132,7 +132,6 @@ struct ResidentArgs {
   unsigned long long* gtrace; // dev only: per-(CTA, group) stamps of the parts kernel [cta][64][8]
   const uint8_t* j4;          // TS kernel: packed e2m1 J [npad][npad / 2] (rows loaded into TMEM)
   int64_t j4_pitch;           // its row pitch in bytes
-  int32_t bpoll;              // TS kernel: 1 = the producer observes all parts' done counters in one round trip
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {

@@ -34,6 +34,9 @@
 #ifndef SBG_TS_PPART
 #define SBG_TS_PPART 0  // 1: p written back / loaded part by part in a group's last step
 #endif
+#ifndef SBG_TS_TRACE4
+#define SBG_TS_TRACE4 0  // 1: SBG_RES_TRACE stamps all four parts (tools/dev/trace_parts4.py), dev builds only
+#endif
 #ifndef SBG_TS_LD1
 #define SBG_TS_LD1 0  // 1: one TMEM load + wait per part-step (measured the same, 26.6 us; spills 36 B)
 #endif
@@ -75,16 +78,10 @@ struct TsMaps {
 // starting after it.
 // KH2_: a part-step's G operand in two 3D loads (K blocks [0, KB/2) and [KB/2, KB)) on two
 // barriers, so the first half's MMAs run while the second half is in flight.
-// MPUB_: one publisher WARP per part (warp 3 for part 0, four extra warps 20..23 for parts 1..4)
-// instead of one thread for all parts: a part's TMA store completion + red.release (~0.85 us,
-// the thread stalls in the release fence) then overlaps the other parts' instead of queueing
-// behind them. The extra warpgroup costs registers: setmaxnreg moves them from the non-epilogue
-// warpgroups to the epilogue ones (768 threads would otherwise cap the epilogue at 80).
-template <int STAGES_, int PARTS_, bool PKB_ = false, bool KH2_ = false, bool MPUB_ = false>
+template <int STAGES_, int PARTS_, bool PKB_ = false, bool KH2_ = false>
 struct TsCfg {
   static constexpr bool PKB = PKB_;
   static constexpr bool KH2 = KH2_;
-  static constexpr bool MPUB = MPUB_;
   static constexpr int PARTS = PARTS_;
   using T = PartTable<PARTS>;
   __host__ __device__ static constexpr int w(int i) { return T::W[i]; }
@@ -101,8 +98,7 @@ struct TsCfg {
   static constexpr int CH = 4;                     // columns per chunk
   static constexpr int XY_BYTES = NR * BM * 4;     // 80 KB each
   static constexpr int T_BYTES = NR * BM / 2;      // G tiles of all parts: [160][64] bytes
-  static constexpr int THREADS = 128 + 32 * EPI_WARPS + (MPUB ? 128 : 0);
-  static constexpr int EPI_REGS = 96;              // MPUB: the epilogue warpgroups' setmaxnreg.inc
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static constexpr int NUM_BARS = 2 * STAGES + 5 * PARTS + (PKB ? STAGES * KB_MAX : 0) + (KH2 ? STAGES : 0);
   static constexpr int SMEM_BYTES = 2 * XY_BYTES + STAGES * STAGE_BYTES + T_BYTES + 1024 + 8 * NUM_BARS + 64;
   static constexpr uint32_t COL_J = NR, COL_SF = 512 - 16;
@@ -113,10 +109,10 @@ struct TsCfg {
   static_assert(!(PKB && KH2), "one G load scheme");
 };
 
-template <int STAGES_, int PARTS_, bool PKB_, bool KH2_, bool MPUB_ = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS_, PKB_, KH2_, MPUB_>::THREADS, 1)
+template <int STAGES_, int PARTS_, bool PKB_, bool KH2_>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS_, PKB_, KH2_>::THREADS, 1)
     gsb_resident_ts_kernel(const __grid_constant__ TsMaps maps, const ResidentArgs args) {
-  using Cfg = TsCfg<STAGES_, PARTS_, PKB_, KH2_, MPUB_>;
+  using Cfg = TsCfg<STAGES_, PARTS_, PKB_, KH2_>;
   constexpr int CH = Cfg::CH;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int PARTS = Cfg::PARTS;
@@ -149,8 +145,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
   const bool leader = cr == 0;
   // dev trace (SBG_RES_TRACE): the parts kernel's per-step stamps (pair 0 leader, group 0, parts 0, 1)
   auto stamp = [&](int g, int s, int i, int k) {
-    // parts 0, 1 in the parts kernel's layout, parts 2, 3 in a second region of the same shape
-    if (args.trace && g == args.group0 && s >= 0 && i < 4 && cr == 0 && (blockIdx.x >> 1) == 0)
+    // parts 0, 1 in the parts kernel's layout; SBG_TS_TRACE4 builds also stamp parts 2, 3 into a
+    // second region of the same shape (compile-time: stamps in all four parts' loops change the
+    // register allocation of this kernel and cost 4 % even with the trace off)
+    if (args.trace && g == args.group0 && s >= 0 && i < (SBG_TS_TRACE4 ? 4 : 2) && cr == 0 && (blockIdx.x >> 1) == 0)
       args.trace[((i >> 1) * 2 * 4096 + s * 2 + (i & 1)) * 16 + k] = gtimer();
   };
   auto gstamp = [&](int g, int k) {
@@ -198,7 +196,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
   // or with PKB per (block, part, CTA pair) counting the pair's 2 CTAs
   auto done_idx = [&](int n_blk, int i) { return Cfg::PKB ? (n_blk * PARTS + i) * num_mp + mp : PARTS * n_blk + i; };
 
-  if (warp >= 4 && warp < 4 + Cfg::EPI_WARPS) {
+  if (warp >= 4) {
     // unit E8M0 scale factors, and this CTA's 128 rows of J into TMEM: lane = row, K block kb at
     // columns COL_J + 32 kb, the packed row's bytes as little-endian 32-bit words (8 e2m1 each,
     // even element in the low nibble: the layout the TS MMA reads, mxf4_ts_probe.cu)
@@ -230,14 +228,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
   ptx::cluster_sync_all();
   ptx::tc_fence_after();
 
-  const bool epi_warp = warp >= 4 && warp < 4 + Cfg::EPI_WARPS;
-  // publisher of part k: warp 3 (all parts), or with MPUB warp 3 for part 0 and warp 19 + k for k >= 1
-  const int my_part = !Cfg::MPUB ? -1 : (warp == 3 ? 0 : warp - (3 + Cfg::EPI_WARPS));
-  // MPUB: register reallocation between warpgroups (launch: 80 per thread for 768 threads; an inc
-  // can only take what the decs of the same CTA released: 256 x 32 = 512 x 16), the
-  // setmaxnreg at the head of each role's branch so that ptxas allocates the branch with it
-  if (!epi_warp) {
-  if constexpr (Cfg::MPUB) ptx::setmaxnreg_dec<48>();
   if (warp == 0) {  // ------------------------------------------------ G producer
     if (ptx::elect_one())
       for (int c = 0; c < 2; ++c)
@@ -251,7 +241,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
     for (int g = args.group0; g < args.group0 + args.groups; ++g) {
       const int n_blk = g * args.rb_per_group + rbk;
       if (n_blk >= num_n) break;
-      uint32_t seen = 0;  // bpoll: lane i's last observation of part i's counter of this block
       for (int s = 0; s < args.nsteps; ++s) {
         static_for<0, PARTS>([&](auto I) {
           constexpr int i = decltype(I)::value;
@@ -273,23 +262,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
             }
             __syncwarp();
           } else {
-            const uint32_t need = static_cast<uint32_t>((s + 1) * args.num_m);
-            if (args.bpoll) {
-              // One ld.acquire round trip observes every part's counter (lane k: part k), so a
-              // part whose dependency is already met costs the producer no round trip of its own
-              // (one serial round trip per part-step made the producer the pacing unit: ~1 us
-              // each). Lane i, which made the observation, issues part i's load below.
-              while (__shfl_sync(0xFFFFFFFFu, seen, i) < need) {
-                if (lane < PARTS) seen = dep::ld_acquire(args.done + PARTS * n_blk + lane);
-              }
-              if (lane == i) dep::fence_proxy_async_global();
-            } else {
-              dep::wait_block(args.done, PARTS * n_blk + i, 0u, need);
-            }
+            dep::wait_block(args.done, PARTS * n_blk + i, 0u, static_cast<uint32_t>((s + 1) * args.num_m));
             if (lane == 0) stamp(g, s, i, 0);
             ptx::mbar_wait(empty_bar(stage), ph ^ 1u);
             if (lane == 0) stamp(g, s, i, 8);
-            if (args.bpoll ? lane == i : ptx::elect_one()) {
+            if (ptx::elect_one()) {
               const uint32_t fb = ptx::mapa(full_bar(stage), 0);
               if constexpr (Cfg::KH2) {
                 const int kh = KB / 2;
@@ -437,7 +414,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
         ptx::prefetch_l2_bulk(args.x + off, Cfg::BM * 4);
       }
     }
-  } else if (warp == 3 || !epi_warp) {  // ------------------------------ G publisher(s)
+  } else if (warp == 3) {  // ------------------------------------------ G publisher
     // One thread publishes every part in turn (parts complete in order): TMA store of the part's
     // G tile, completion, proxy fence and red.release of its counter. (One lane per part, as in
     // the parts kernel, measured 28.6 vs 26.5 us/step: the four diverged lanes' waits serialise
@@ -466,7 +443,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
       if (args.group0 * args.rb_per_group + rbk < num_n)
         static_for<0, PARTS>([&](auto I) {
           constexpr int k = decltype(I)::value;
-          if (my_part < 0 || my_part == k) load_state(args.group0, Cfg::off(k), Cfg::cls(k), Cfg::w(k), k);
+          load_state(args.group0, Cfg::off(k), Cfg::cls(k), Cfg::w(k), k);
         });
       int pc = 0;
       for (int g = args.group0; g < args.group0 + args.groups; ++g) {
@@ -478,7 +455,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
           const int par = s < 0 ? 1 : (s & 1);
           static_for<0, PARTS>([&](auto I) {
             constexpr int k = decltype(I)::value;
-            if (my_part >= 0 && my_part != k) return;
             ptx::mbar_wait(gfull_bar(k), pc & 1);
             stamp(g, s, k, 3);
             ptx::tma_store_2d(&maps.g.Gout[Cfg::cls(k)][par], t_base + Cfg::off(k) * (Cfg::BM / 2), i0 / 2,
@@ -514,9 +490,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
         }
       }
     }
-  }
   } else {  // ------------------------------------------------------------- epilogue
-    if constexpr (Cfg::MPUB) ptx::setmaxnreg_inc<Cfg::EPI_REGS>();
     const int q = warp & 3;
     const int cg = (warp - 4) >> 2;
     const int sl = q * 32 + lane;  // this thread's spin within the CTA

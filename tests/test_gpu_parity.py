@@ -555,9 +555,7 @@ def test_e2m1_resident_equals_int8(solver, n, R, variant, values, monkeypatch):
                                                    (1500, 2000, GDSB, "5", "0"), (513, 6000, GDSB, "4", "0"),
                                                    (777, 400, DSB, "5", "0"), (2000, 8192, GDSB, "4", "1"),
                                                    (777, 400, DSB, "5", "1"), (2000, 8192, GDSB, "4", "kh2"),
-                                                   (1500, 2000, DSB, "4", "kh2"), (2000, 8192, GDSB, "4", "mpub"),
-                                                   (777, 400, DSB, "5", "mpub"), (513, 6000, GDSB, "4", "mpub"),
-                                                   (2000, 8192, GDSB, "4", "bpoll"), (777, 400, DSB, "5", "bpoll")])
+                                                   (1500, 2000, DSB, "4", "kh2")])
 def test_ts_kernel_equals_parts_kernel(solver, n, R, variant, parts, pkb, monkeypatch):
     """The TS resident kernel (J in TMEM as the A operand of tcgen05.mma [a_tmem], x, y in
     shared memory, state moved by TMA at group boundaries; the default) against the parts
@@ -570,13 +568,9 @@ def test_ts_kernel_equals_parts_kernel(solver, n, R, variant, parts, pkb, monkey
     # 1: per-K-block dependencies; kh2: each part-step's G in two halves (dev variants)
     monkeypatch.setenv("SBG_RES_PKB", "1" if pkb == "1" else "0")
     monkeypatch.setenv("SBG_RES_KH2", "1" if pkb == "kh2" else "0")
-    monkeypatch.setenv("SBG_TS_MPUB", "1" if pkb == "mpub" else "0")  # one publisher warp per part
-    monkeypatch.setenv("SBG_TS_BPOLL", "1" if pkb == "bpoll" else "0")  # all parts' counters in one round trip
     f_ts, a = _run_resident(solver, J, R, variant, 23, monkeypatch, True, arep=arep)
     monkeypatch.delenv("SBG_RES_PKB")
     monkeypatch.delenv("SBG_RES_KH2")
-    monkeypatch.delenv("SBG_TS_MPUB")
-    monkeypatch.delenv("SBG_TS_BPOLL")
     monkeypatch.setenv("SBG_RES_TS", "0")
     monkeypatch.setenv("SBG_RES_PARTS", "4")
     f_pa, b = _run_resident(solver, J, R, variant, 23, monkeypatch, True, arep=arep)
