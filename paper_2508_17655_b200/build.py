@@ -35,6 +35,18 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in DEPS if os.path.exists(d))
 
 
+def build_devhooks() -> str:
+    """libsbgpu_dev.so: the same library with the dev hooks (trace stamps, SBG_STEP_DBG probes)
+    compiled in; tools/dev/* load it through SBG_LIB_OVERRIDE. Never the measured library."""
+    out = os.path.join(HERE, "libsbgpu_dev.so")
+    cmd = [nvcc(), *NVCC_FLAGS, "-DSBG_DEVHOOKS=1", "-DSBG_TS_TRACE4=1", "-o", out, *SOURCES]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stderr[-4000:])
+        raise RuntimeError("nvcc failed (dev hooks build)")
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
@@ -53,4 +65,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    if "--devhooks" in sys.argv:
+        print(build_devhooks())
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

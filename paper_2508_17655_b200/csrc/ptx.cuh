@@ -7,6 +7,16 @@
 #include <cstdint>
 #include <cuda.h>
 
+// Dev hooks (trace stamps, SBG_STEP_DBG probes) are compiled OUT of the shipped library: the
+// resident kernels sit at their register cap and even switched-off runtime hooks in their loops
+// cost 4-5 % (same-box A/B at C2: 26.6 -> 25.3 us/step). `build.py --devhooks` builds
+// libsbgpu_dev.so with them (tools/dev/* load it through SBG_LIB_OVERRIDE).
+#ifndef SBG_DEVHOOKS
+#define SBG_DEVHOOKS 0
+#endif
+#define SBG_DBG(a) (SBG_DEVHOOKS ? (a).dbg : 0)
+#define SBG_HOOK_PTR(p) (SBG_DEVHOOKS ? (p) : nullptr)
+
 namespace sbg {
 namespace ptx {
 

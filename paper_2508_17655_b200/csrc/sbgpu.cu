@@ -281,6 +281,20 @@ int dev_knob(const char* name) {
   const char* e = getenv(name);
   return e ? atoi(e) : 0;
 }
+// Knobs that need the dev hooks compiled into the kernels (SBG_DEVHOOKS, `build.py --devhooks`):
+// in the shipped library they are refused loudly instead of silently tracing nothing.
+int hook_knob(const char* name) {
+  const int v = dev_knob(name);
+  if (v && !SBG_DEVHOOKS) {
+    static bool warned = false;
+    if (!warned)
+      fprintf(stderr, "sbgpu: %s ignored: this library was built without dev hooks "
+                      "(python paper_2508_17655_b200/build.py --devhooks builds libsbgpu_dev.so)\n", name);
+    warned = true;
+    return 0;
+  }
+  return v;
+}
 bool getenv_is0(const char* name) {
   const char* e = getenv(name);
   return e && atoi(e) == 0;
@@ -366,7 +380,7 @@ int launch_multistep_pair(sbg_ctx* ctx, const TmaMaps& maps, MultiStepArgs a) {
   if (!ctx->sharded) CK(cudaMemsetAsync(ctx->d_done, 0, sizeof(uint32_t) * a.num_n, ctx->stream));
   static unsigned long long* utrace = nullptr;  // dev knob SBG_PAIR_TRACE: per (CTA, unit) stamps
   const size_t utn = size_t(grid) * 64 * 8;
-  if (dev_knob("SBG_PAIR_TRACE")) {
+  if (hook_knob("SBG_PAIR_TRACE")) {
     cudaFree(utrace);
     CK(cudaMalloc(&utrace, utn * 8));
     CK(cudaMemsetAsync(utrace, 0, utn * 8, ctx->stream));
@@ -528,11 +542,11 @@ int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int
   a.ready = ready;
   a.gbuf[0] = ctx->dG[ctx->g_cur ^ 1];  // step parity 0 writes the other buffer (as Gout[0])
   a.gbuf[1] = ctx->dG[ctx->g_cur];
-  a.dbg = dev_knob("SBG_STEP_DBG");
+  a.dbg = hook_knob("SBG_STEP_DBG");
   a.j4 = ctx->dJ4;
   a.j4_pitch = ctx->npad / 2;
   static unsigned long long* trace = nullptr;  // dev knob SBG_RES_TRACE: stamps of pair 0, group 0
-  if (dev_knob("SBG_RES_TRACE")) {
+  if (hook_knob("SBG_RES_TRACE")) {
     if (!trace) CK(cudaMalloc(&trace, sizeof(unsigned long long) * 16 * 4 * 4096));
     CK(cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 16 * 4 * 4096, ctx->stream));
     a.trace = trace;
@@ -540,7 +554,7 @@ int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int
   }
   static unsigned long long* gtrace = nullptr;  // dev knob SBG_RES_GTRACE: per-(CTA, group) stamps
   const size_t gtn = size_t(ctx->sms) * 64 * 8 + size_t(ctx->sms) * 32;  // + the TS kernel's skew trace
-  if (PARTS != 0 && dev_knob("SBG_RES_GTRACE")) {  // parts and TS kernels
+  if (PARTS != 0 && hook_knob("SBG_RES_GTRACE")) {  // parts and TS kernels
     if (!gtrace) CK(cudaMalloc(&gtrace, sizeof(unsigned long long) * gtn));
     CK(cudaMemsetAsync(gtrace, 0, sizeof(unsigned long long) * gtn, ctx->stream));
     a.gtrace = gtrace;
@@ -1708,7 +1722,7 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
         a.peer_g[1][pr] = cur == 0 ? ctx->peer_g0[size_t(pr)] : ctx->peer_g1[size_t(pr)];
         a.peer_done[pr] = ctx->peer_done[size_t(pr)];
       }
-      a.dbg = dev_knob("SBG_STEP_DBG");
+      a.dbg = hook_knob("SBG_STEP_DBG");
       // Defaults (measured on B200, tools/step_driver.py): sign variants on CTA pairs
       // (3 operand stages, 4 state buffers): 73 us/step at N=2000, R=8192, vs 83 us
       // single-CTA; fixed-point planes single-CTA (3, 2): 18.5 us/step at R=1024 vs

@@ -234,7 +234,7 @@ __global__ void __cluster_dims__(2, 1, 1)
   };
 
   if (warp == 0) {
-    if (args.dbg < 2) {  // ------------------------------------------- operand producer (both CTAs)
+    if (SBG_DBG(args) < 2) {  // ------------------------------------------- operand producer (both CTAs)
       // whole warp walks the schedule (uniform values), one elected lane issues TMA
       if (ptx::elect_one()) {
         ptx::prefetch_tmap(&maps.J);
@@ -274,7 +274,7 @@ __global__ void __cluster_dims__(2, 1, 1)
       }
     }
   } else if (warp == 1) {
-    if (leader && args.dbg < 2) {  // --------------------------------- MMA issuer (leader CTA only)
+    if (leader && SBG_DBG(args) < 2) {  // --------------------------------- MMA issuer (leader CTA only)
       // whole warp walks the schedule; one elected lane issues (uniform descriptors)
       constexpr uint32_t idesc_s = Cfg::Q4 ? ptx::idesc_mxf4(256, N_PAIR) : ptx::idesc_i8(256, N_PAIR, true, true);
       // MERGED: the NPLANES signed digit planes of B are consecutive smem tiles, i.e. one
@@ -290,8 +290,8 @@ __global__ void __cluster_dims__(2, 1, 1)
         unit(g, s_, w_, kp, ks);
         const int kb0 = kp * KB / ks;
         auto ust = [&](int k) {
-          if (args.utrace && lt < 64 && lane == 0)
-            args.utrace[(static_cast<size_t>(blockIdx.x) * 64 + lt) * 8 + k] = gtimer_pair();
+          if (SBG_HOOK_PTR(args.utrace) && lt < 64 && lane == 0)
+            SBG_HOOK_PTR(args.utrace)[(static_cast<size_t>(blockIdx.x) * 64 + lt) * 8 + k] = gtimer_pair();
         };
         ust(5);
         ptx::mbar_wait(tempty_bar(buf), ((lt / NACC) & 1) ^ 1u);
@@ -501,15 +501,15 @@ __global__ void __cluster_dims__(2, 1, 1)
         if ((kp == ks - 1) && s > 0) dep::wait_block(args.done, n_of(w), args.done_base, s * args.num_m_total);
         if (kp == ks - 1) d_ld(0, 0);
       }
-      if (args.dbg < 2) ptx::mbar_wait(tfull_bar(buf), (lt / NACC) & 1);
+      if (SBG_DBG(args) < 2) ptx::mbar_wait(tfull_bar(buf), (lt / NACC) & 1);
       __syncwarp();
       ptx::tc_fence_after();
-      const bool utr = args.utrace && lt < 64 && threadIdx.x == 4 * 32;
+      const bool utr = SBG_HOOK_PTR(args.utrace) && lt < 64 && threadIdx.x == 4 * 32;
       auto ust = [&](int k) {
-        if (utr) args.utrace[(static_cast<size_t>(blockIdx.x) * 64 + lt) * 8 + k] = gtimer_pair();
+        if (utr) SBG_HOOK_PTR(args.utrace)[(static_cast<size_t>(blockIdx.x) * 64 + lt) * 8 + k] = gtimer_pair();
       };
       ust(2);
-      if (utr) args.utrace[(static_cast<size_t>(blockIdx.x) * 64 + lt) * 8 + 6] = (uint64_t(s) << 40) | (uint64_t(w) << 8) | (uint64_t(kp) << 4) | uint64_t(ks);
+      if (utr) SBG_HOOK_PTR(args.utrace)[(static_cast<size_t>(blockIdx.x) * 64 + lt) * 8 + 6] = (uint64_t(s) << 40) | (uint64_t(w) << 8) | (uint64_t(kp) << 4) | uint64_t(ks);
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * Cfg::ACC_COLS;
       // K split: partial fields of parts 0..KS-2, replica-major so a warp's 32 rows are contiguous
       const size_t frow = static_cast<size_t>(m_blk) * Cfg::BM + srow;

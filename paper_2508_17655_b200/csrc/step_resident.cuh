@@ -227,7 +227,7 @@ __global__ void __cluster_dims__(2, 1, 1)
         constexpr int PRE = STAGES < 16 ? STAGES : 16;
         int st0 = stage;
         uint32_t ph0 = ph;
-        const bool skipJ = args.dbg == 1 && (s > 0 || g > 0);
+        const bool skipJ = SBG_DBG(args) == 1 && (s > 0 || g > 0);
         for (int kb = 0; kb < PRE && kb < KB; ++kb) {
           ptx::mbar_wait(empty_bar(st0), ph0 ^ 1u);
           if (ptx::elect_one() && !skipJ) {
@@ -243,8 +243,8 @@ __global__ void __cluster_dims__(2, 1, 1)
         }
         // G_t of block n is complete when all num_m CTAs released it (the launch's
         // initial G_0 is published by the kernel itself at group start: one release each)
-        if (args.dbg != 2) dep::wait_block(args.done, n_blk, 0u, static_cast<uint32_t>((s + 1) * args.num_m));
-        if (args.trace && pair == 0 && g == 0 && lane == 0) args.trace[(s * 2 + cr) * 16 + 0] = gtimer();
+        if (SBG_DBG(args) != 2) dep::wait_block(args.done, n_blk, 0u, static_cast<uint32_t>((s + 1) * args.num_m));
+        if (SBG_HOOK_PTR(args.trace) && pair == 0 && g == 0 && lane == 0) SBG_HOOK_PTR(args.trace)[(s * 2 + cr) * 16 + 0] = gtimer();
         const CUtensorMap* gin = &maps.Gin[s & 1];
         for (int kb = 0; kb < KB; ++kb) {
           const bool pre = kb < PRE;
@@ -429,7 +429,7 @@ __global__ void __cluster_dims__(2, 1, 1)
         ptx::mbar_wait(tfull, lt & 1);
         __syncwarp();
         ptx::tc_fence_after();
-        if (args.trace && pair == 0 && g == 0 && epi_tid == 0) args.trace[(s * 2 + cr) * 16 + 1] = gtimer();
+        if (SBG_HOOK_PTR(args.trace) && pair == 0 && g == 0 && epi_tid == 0) SBG_HOOK_PTR(args.trace)[(s * 2 + cr) * 16 + 1] = gtimer();
         // chunks of CH replica columns; TMEM loads of chunk c+1 overlap the math of chunk c
         uint32_t bf[2][CH], bx[2][CH], by[2][CH], bp[2][CH];
         auto ld_chunk = [&](int c, int b) {
@@ -452,8 +452,8 @@ __global__ void __cluster_dims__(2, 1, 1)
         };
         ld_chunk(0, 0);
         wait_chunk(0);
-        const bool tr = args.trace && pair == 0 && g == 0 && epi_tid == 0;
-        if (tr) args.trace[(s * 2 + cr) * 16 + 4] = gtimer();
+        const bool tr = SBG_HOOK_PTR(args.trace) && pair == 0 && g == 0 && epi_tid == 0;
+        if (tr) SBG_HOOK_PTR(args.trace)[(s * 2 + cr) * 16 + 4] = gtimer();
         auto chunks = [&](auto has_arep) {
 #pragma unroll
           for (int c = 0; c < Cfg::CHUNKS; ++c) {
@@ -497,17 +497,17 @@ __global__ void __cluster_dims__(2, 1, 1)
           chunks(std::true_type{});
         else
           chunks(std::false_type{});
-        if (tr) args.trace[(s * 2 + cr) * 16 + 5] = gtimer();
+        if (tr) SBG_HOOK_PTR(args.trace)[(s * 2 + cr) * 16 + 5] = gtimer();
         ptx::tmem_st_wait();
-        if (tr) args.trace[(s * 2 + cr) * 16 + 6] = gtimer();
+        if (tr) SBG_HOOK_PTR(args.trace)[(s * 2 + cr) * 16 + 6] = gtimer();
         // F consumed: the leader may overwrite the accumulator
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader);
         // publish G_{t+1} for this CTA's 128 spins x NR replicas
-        if (tr) args.trace[(s * 2 + cr) * 16 + 2] = gtimer();
+        if (tr) SBG_HOOK_PTR(args.trace)[(s * 2 + cr) * 16 + 2] = gtimer();
         publish(n_blk, s & 1);
-        if (tr) args.trace[(s * 2 + cr) * 16 + 3] = gtimer();
+        if (tr) SBG_HOOK_PTR(args.trace)[(s * 2 + cr) * 16 + 3] = gtimer();
       }
       // write the block's state back
 #pragma unroll 1

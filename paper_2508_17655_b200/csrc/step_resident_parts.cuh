@@ -142,12 +142,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
   // dev group trace (SBG_RES_GTRACE): k 0 group top, 1 state loaded, 2 step 0 part 0 acc ready,
   // 3 step 1 part 0 acc ready, 4 last step done, 5 write-back done, 6 helper published G_0
   auto gstamp = [&](int g, int k) {
-    if (args.gtrace && g - args.group0 < 64)
-      args.gtrace[(static_cast<size_t>(blockIdx.x) * 64 + (g - args.group0)) * 8 + k] = gtimer();
+    if (SBG_HOOK_PTR(args.gtrace) && g - args.group0 < 64)
+      SBG_HOOK_PTR(args.gtrace)[(static_cast<size_t>(blockIdx.x) * 64 + (g - args.group0)) * 8 + k] = gtimer();
   };
   auto stamp = [&](int g, int s, int i, int k) {
-    if (args.trace && g == args.group0 && s >= 0 && i < 2 && cr == 0 && (blockIdx.x >> 1) == 0)
-      args.trace[(s * 2 + i) * 16 + k] = gtimer();
+    if (SBG_HOOK_PTR(args.trace) && g == args.group0 && s >= 0 && i < 2 && cr == 0 && (blockIdx.x >> 1) == 0)
+      SBG_HOOK_PTR(args.trace)[(s * 2 + i) * 16 + k] = gtimer();
   };
 
   if (warp == 0 && lane == 0) {
@@ -304,7 +304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PartsCfg<STAGES_, JR
               ptx::tc_fence_after();
               if (ptx::elect_one()) {
                 const uint32_t bb = b_base + stage * Cfg::STAGE_BYTES;
-                const int kb_end = args.dbg == 3 ? 2 : KB;  // dev timing probe: MMA cost off the chain
+                const int kb_end = SBG_DBG(args) == 3 ? 2 : KB;  // dev timing probe: MMA cost off the chain
                 for (int kb = 0; kb < kb_end; ++kb) {
                   const uint64_t adesc = ptx::smem_desc_k_sw128(a_base + kb * Cfg::A_BYTES);
                   const uint64_t bdesc = ptx::smem_desc_k_sw128(bb + kb * (Cfg::w(i) / 2) * Cfg::BK);

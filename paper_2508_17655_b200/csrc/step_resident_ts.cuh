@@ -145,15 +145,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
   const bool leader = cr == 0;
   // dev trace (SBG_RES_TRACE): the parts kernel's per-step stamps (pair 0 leader, group 0, parts 0, 1)
   auto stamp = [&](int g, int s, int i, int k) {
+    if constexpr (!SBG_DEVHOOKS) return;
     // parts 0, 1 in the parts kernel's layout; SBG_TS_TRACE4 builds also stamp parts 2, 3 into a
     // second region of the same shape (compile-time: stamps in all four parts' loops change the
     // register allocation of this kernel and cost 4 % even with the trace off)
-    if (args.trace && g == args.group0 && s >= 0 && i < (SBG_TS_TRACE4 ? 4 : 2) && cr == 0 && (blockIdx.x >> 1) == 0)
-      args.trace[((i >> 1) * 2 * 4096 + s * 2 + (i & 1)) * 16 + k] = gtimer();
+    if (SBG_HOOK_PTR(args.trace) && g == args.group0 && s >= 0 && i < (SBG_TS_TRACE4 ? 4 : 2) && cr == 0 && (blockIdx.x >> 1) == 0)
+      SBG_HOOK_PTR(args.trace)[((i >> 1) * 2 * 4096 + s * 2 + (i & 1)) * 16 + k] = gtimer();
   };
   auto gstamp = [&](int g, int k) {
-    if (args.gtrace && g - args.group0 < 64)
-      args.gtrace[(static_cast<size_t>(blockIdx.x) * 64 + (g - args.group0)) * 8 + k] = gtimer();
+    if constexpr (!SBG_DEVHOOKS) return;
+    if (SBG_HOOK_PTR(args.gtrace) && g - args.group0 < 64)
+      SBG_HOOK_PTR(args.gtrace)[(static_cast<size_t>(blockIdx.x) * 64 + (g - args.group0)) * 8 + k] = gtimer();
   };
 
   if (warp == 0 && lane == 0) {
@@ -480,10 +482,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
             dep::release_add(args.done + done_idx(n_blk, k), 1u);
             stamp(g, s, k, 5);
             // dev skew trace (SBG_RES_GTRACE): every CTA's release time of part 0, steps 8..39 of group 0
-            if (k == 0 && args.gtrace && g == args.group0 && s >= 8 && s < 40) {
+            if (SBG_DEVHOOKS && k == 0 && SBG_HOOK_PTR(args.gtrace) && g == args.group0 && s >= 8 && s < 40) {
               uint32_t smid;
               asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-              args.gtrace[size_t(gridDim.x) * 512 + size_t(blockIdx.x) * 32 + (s - 8)] =
+              SBG_HOOK_PTR(args.gtrace)[size_t(gridDim.x) * 512 + size_t(blockIdx.x) * 32 + (s - 8)] =
                   (gtimer() & 0xFFFFFFFFFFFFull) | (uint64_t(smid) << 48);
             }
           });

@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
   };
 
   if (warp == 0) {
-    if (args.dbg < 2) {  // ------------------------------------------ operand producer
+    if (SBG_DBG(args) < 2) {  // ------------------------------------------ operand producer
       // whole warp walks the schedule (uniform values), one elected lane issues TMA
       if (ptx::elect_one()) {
         ptx::prefetch_tmap(&maps.J);
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
       }
     }
   } else if (warp == 1) {
-    if (args.dbg < 2) {  // ------------------------------------------------ MMA issuer
+    if (SBG_DBG(args) < 2) {  // ------------------------------------------------ MMA issuer
       // the whole warp walks the (warp-uniform) schedule; one elected lane issues
       int stage = 0;
       uint32_t ph = 0;
@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
       }
     }
   } else if (warp == 2) {
-    if (lane == 0 && args.dbg != 1) {  // ------------------------------- state loader
+    if (lane == 0 && SBG_DBG(args) != 1) {  // ------------------------------- state loader
       ptx::prefetch_tmap(&maps.X);
       ptx::prefetch_tmap(&maps.Y);
       ptx::prefetch_tmap(&maps.P);
@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
         const uint32_t sb = s_base + b * Cfg::BUF_BYTES;
         const int r0 = rb + c * CW;
         if (lane == 0) {
-          if (args.dbg != 1) {
+          if (SBG_DBG(args) != 1) {
             ptx::tma_store_2d(&maps.X, sb, i0, r0);
             ptx::tma_store_2d(&maps.Y, sb + Cfg::ST_ARR, i0, r0);
             ptx::tma_store_2d(&maps.P, sb + 2 * Cfg::ST_ARR, i0, r0);
@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
       const int rbase = ((g % T) / args.num_m) * BN;  // first replica of this tile
       k.inv = __frcp_rn(static_cast<float>(args.M - (args.t_begin + static_cast<uint64_t>(s))));
       const int buf = lt % Cfg::ABUF;
-      if (args.dbg < 2) ptx::mbar_wait(tfull_bar(buf), (lt / Cfg::ABUF) & 1);
+      if (SBG_DBG(args) < 2) ptx::mbar_wait(tfull_bar(buf), (lt / Cfg::ABUF) & 1);
       __syncwarp();
       ptx::tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * Cfg::ACC_COLS;
@@ -575,13 +575,13 @@ __global__ void __launch_bounds__(TmaStepCfg<NPLANES, BN, STAGES_, NBUF_, NA_>::
         } else {
           load_F(c, F);
         }
-        if (args.dbg != 1) {
+        if (SBG_DBG(args) != 1) {
           ptx::mbar_wait(sfull_bar(b), (ck / NBUF) & 1);
           float* xs = reinterpret_cast<float*>(s_gen + b * Cfg::BUF_BYTES);
           float* ys = xs + CW * Cfg::BM;
           float* ps = ys + CW * Cfg::BM;
           uint8_t* gs = reinterpret_cast<uint8_t*>(ps + CW * Cfg::BM);
-          if (args.dbg != 3) {
+          if (SBG_DBG(args) != 3) {
 #pragma unroll
             for (int j = 0; j < CWQ; ++j) {
               const int idx = (h * CWQ + j) * Cfg::BM + srow;

@@ -1,4 +1,6 @@
-"""Per-group timeline of the TS kernel (SBG_RES_GTRACE=1): for each replica group the median over CTAs
+"""[needs the dev-hooks library: python paper_2508_17655_b200/build.py --devhooks, then
+SBG_LIB_OVERRIDE=paper_2508_17655_b200/libsbgpu_dev.so]
+Per-group timeline of the TS kernel (SBG_RES_GTRACE=1): for each replica group the median over CTAs
 of group start (0), p loaded + G_0 handed over (1), first / second accumulator ready (2, 3), last step
 done (4), p stored (5), helper done with the group's G_0 (6), all relative to the earliest stamp."""
 import sys

@@ -1,4 +1,6 @@
-"""Timeline of the parts kernel (SBG_RES_TRACE=1): pair 0's leader CTA, group 0, parts 0/1.
+"""[needs the dev-hooks library: python paper_2508_17655_b200/build.py --devhooks, then
+SBG_LIB_OVERRIDE=paper_2508_17655_b200/libsbgpu_dev.so]
+Timeline of the parts kernel (SBG_RES_TRACE=1): pair 0's leader CTA, group 0, parts 0/1.
 Prints, per part, the mean time of each event relative to part 0's G-dependency-met stamp of
 the same step (us), and the step period."""
 import sys

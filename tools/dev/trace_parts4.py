@@ -1,4 +1,6 @@
-"""Timeline of the TS kernel (SBG_RES_TRACE=1) over all four parts of pair 0's leader CTA, group 0:
+"""[needs the dev-hooks library: python paper_2508_17655_b200/build.py --devhooks, then
+SBG_LIB_OVERRIDE=paper_2508_17655_b200/libsbgpu_dev.so]
+Timeline of the TS kernel (SBG_RES_TRACE=1) over all four parts of pair 0's leader CTA, group 0:
 for each part the mean time of every event relative to part 0's dependency-met stamp of the same
 step, the epilogue's busy time per part, and how long the epilogue waited for each accumulator."""
 import sys

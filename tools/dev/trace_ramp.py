@@ -1,4 +1,6 @@
-"""Step periods of part 0 at the start of group 0 (SBG_RES_TRACE=1): how fast the four staggered
+"""[needs the dev-hooks library: python paper_2508_17655_b200/build.py --devhooks, then
+SBG_LIB_OVERRIDE=paper_2508_17655_b200/libsbgpu_dev.so]
+Step periods of part 0 at the start of group 0 (SBG_RES_TRACE=1): how fast the four staggered
 part chains of the TS kernel settle into the steady state."""
 import sys
 import numpy as np
