@@ -438,7 +438,9 @@ def measure_tts(s):
     tun = TuningResult(c=c, dt=DT)
     for v in ("gbsb", "gdsb"):
         cfg = SolverConfig(variant=Variant[v], steps=TTS_M, dt=DT, c=c, a=A_CTRL, init_mode=InitMode.uniform_random)
-        s.run_batch(cfg, tun, 64, master_seed=7, want_spins=False)  # warm
+        # warm-up at the batch's own replica count: the first run at a new R pays one-off costs (state
+        # reallocation, first use of the kernels that geometry selects) that are not T_com
+        s.run_batch(cfg, tun, n_trials, master_seed=7, want_spins=False)
         t0 = time.perf_counter()
         b = s.run_batch(cfg, tun, n_trials, master_seed=1, want_spins=False)  # derive_seed(1, {3, r})
         t_batch = time.perf_counter() - t0

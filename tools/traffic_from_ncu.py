@@ -42,7 +42,7 @@ def dram(d):
 
 def main(files):
     res = {k: {"kernel": v[0], "launch_bytes": {}, "launch_ns": {}} for k, v in SPEC.items()}
-    res["c3_csr"] = {"kernel": "csr_step_sm_kernel<0> (one launch per replica slab and step, summed over the "
+    res["c3_csr"] = {"kernel": "csr_step_lean_kernel<0, 2> (one launch per replica slab and step, summed over the "
                                "timed advance)", "launch_bytes": {}, "launch_ns": {}, "transposes_bytes": {}}
     for f in files:
         K = int(f.rsplit("_", 1)[1].split(".")[0])
