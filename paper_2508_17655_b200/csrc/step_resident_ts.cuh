@@ -34,6 +34,9 @@
 #ifndef SBG_TS_PPART
 #define SBG_TS_PPART 0  // 1: p written back / loaded part by part in a group's last step
 #endif
+#ifndef SBG_TS_REGS
+#define SBG_TS_REGS 0  // dev: 1 = setmaxnreg moves registers from warps 0..3 (48) to the epilogue warps (104)
+#endif
 #ifndef SBG_TS_TRACE4
 #define SBG_TS_TRACE4 0  // 1: SBG_RES_TRACE stamps all four parts (tools/dev/trace_parts4.py), dev builds only
 #endif
@@ -230,6 +233,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
   ptx::cluster_sync_all();
   ptx::tc_fence_after();
 
+#if SBG_TS_REGS
+  if (warp < 4) {
+    ptx::setmaxnreg_dec<48>();
+#endif
   if (warp == 0) {  // ------------------------------------------------ G producer
     if (ptx::elect_one())
       for (int c = 0; c < 2; ++c)
@@ -492,7 +499,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
         }
       }
     }
+#if SBG_TS_REGS
+  }
+  } else {
+    ptx::setmaxnreg_inc<104>();
+#else
   } else {  // ------------------------------------------------------------- epilogue
+#endif
     const int q = warp & 3;
     const int cg = (warp - 4) >> 2;
     const int sl = q * 32 + lane;  // this thread's spin within the CTA
