@@ -229,7 +229,11 @@ __global__ void __launch_bounds__(CSR_THREADS, CSR_MIN_BLOCKS)
 //     gsb_phase), and all state addresses are 32-bit element offsets (host-checked: n * rp * 4 B
 //     < 4 GB, else the kernel above runs).
 // Same integer field, same update: bitwise equal (test_csr_kernel_variants_bitwise).
-template <bool SIGN, int UNR>
+// PFS: the task's x, y, p (3 x 512 B per warp) are fetched into shared memory by cp.async at task
+// start and read back after the gather loop, so their DRAM latency runs under the gathers instead
+// of after them (ncu: 17 % of the stall samples sat on the first FFMA2 of the phase update) --
+// without holding 12 registers across the loop.
+template <bool SIGN, int UNR, bool PFS = false>
 __global__ void __launch_bounds__(CSR_THREADS, CSR_MIN_BLOCKS)
     csr_step_lean_kernel(uint32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                          const int8_t* __restrict__ val, const void* __restrict__ g_cur, void* __restrict__ g_next,
@@ -237,6 +241,7 @@ __global__ void __launch_bounds__(CSR_THREADS, CSR_MIN_BLOCKS)
                          uint32_t R, PhaseConsts k, PhaseIdent id, const float* __restrict__ a_rep = nullptr) {
   static_assert(UNR == 1 || UNR == 2 || UNR == 4, "gathers per round");
   __shared__ __align__(16) uint2 stage[CSR_THREADS / 32][32];  // (column, value) of the row's nonzeros
+  __shared__ __align__(16) float4 sstate[PFS ? CSR_THREADS / 32 : 1][3][PFS ? 32 : 1];  // PFS: x, y, p of the task
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t chunks = (R + CSR_RCHUNK - 1) / CSR_RCHUNK;
   const uint32_t nw = gridDim.x * (CSR_THREADS / 32);
@@ -251,6 +256,22 @@ __global__ void __launch_bounds__(CSR_THREADS, CSR_MIN_BLOCKS)
     const uint32_t r = c * CSR_RCHUNK + 4 * lane;
     const int kb = rowptr[i], ke = rowptr[i + 1];
     Acc acc[4] = {0, 0, 0, 0};
+    uint32_t ss = 0;
+    if constexpr (PFS) {
+      ss = static_cast<uint32_t>(__cvta_generic_to_shared(&sstate[wib][0][lane]));
+      if (r < R) {
+        const uint32_t off = i * rp + r;
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(ss), "l"(xs + off), "l"(stream)
+                     : "memory");
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(ss + 512), "l"(ys + off),
+                     "l"(stream)
+                     : "memory");
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(ss + 1024), "l"(ps + off),
+                     "l"(stream)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     for (int k0 = kb; k0 < ke; k0 += 32) {
       const int cnt = min(32, ke - k0);
       uint32_t ej = 0, ev = 0;  // lanes >= cnt stage (row 0, value 0): the ragged tail of a round
@@ -305,11 +326,24 @@ __global__ void __launch_bounds__(CSR_THREADS, CSR_MIN_BLOCKS)
         }
       }
     }
+    if constexpr (PFS) asm volatile("cp.async.wait_group 0;" ::: "memory");
     if (r < R) {
       const uint32_t off = i * rp + r;
-      float4 x4 = l2::ld_f4(xs + off, stream);
-      float4 y4 = l2::ld_f4(ys + off, stream);
-      float4 p4 = l2::ld_f4(ps + off, stream);
+      float4 x4, y4, p4;
+      if constexpr (PFS) {
+        auto lds4 = [](uint32_t a) {
+          float4 v;
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+          return v;
+        };
+        x4 = lds4(ss);
+        y4 = lds4(ss + 512);
+        p4 = lds4(ss + 1024);
+      } else {
+        x4 = l2::ld_f4(xs + off, stream);
+        y4 = l2::ld_f4(ys + off, stream);
+        p4 = l2::ld_f4(ps + off, stream);
+      }
       float F[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e)

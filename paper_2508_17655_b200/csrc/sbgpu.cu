@@ -1635,8 +1635,9 @@ int sbg_advance(sbg_ctx* ctx, const sbg_params* prm, uint64_t m_begin, uint64_t 
         } else if (lean) {
           // fewer instructions per task (csr_step_lean_kernel), `lean` nonzeros per gather round
           const PhaseIdent ident{-0.0f, 1.0f, -1.0f};
+          const bool pfs = dev_knob("SBG_CSR_PFS") == 1;  // x, y, p prefetched into shared memory by cp.async
 #define CSR_LEAN(S, U)                                                                                          \
-  csr_step_lean_kernel<S, U><<<blocks, CSR_THREADS, 0, ctx->stream>>>(                                           \
+  (pfs ? csr_step_lean_kernel<S, U, true> : csr_step_lean_kernel<S, U, false>)<<<blocks, CSR_THREADS, 0, ctx->stream>>>( \
       uint32_t(n32), ctx->d_rowptr, ctx->d_col, ctx->d_val, gq[cur], gn, xs, ys, ps, uint32_t(ctx->rp), uint32_t(Rs),  \
       km, ident, ar)
           if (sign) {

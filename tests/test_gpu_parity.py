@@ -213,13 +213,16 @@ def test_csr_equals_dense_and_mirror(solver, orc):
                                    {"SBG_CSR_ASYNC": "8", "SBG_CSR_SLAB": "128"}, {"SBG_CSR_PF": "6"},
                                    {"SBG_CSR_PF": "7"}, {"SBG_CSR_LEAN": "1"}, {"SBG_CSR_LEAN": "2"},
                                    {"SBG_CSR_LEAN": "4"}, {"SBG_CSR_LEAN": "0"},
-                                   {"SBG_CSR_LEAN": "2", "SBG_CSR_SLAB": "128"}])
+                                   {"SBG_CSR_LEAN": "2", "SBG_CSR_SLAB": "128"},
+                                   {"SBG_CSR_LEAN": "2", "SBG_CSR_PFS": "1"}, {"SBG_CSR_LEAN": "2", "SBG_CSR_PFS": "0"},
+                                   {"SBG_CSR_LEAN": "4", "SBG_CSR_PFS": "1", "SBG_CSR_SLAB": "128"}])
 def test_csr_kernel_variants_bitwise(solver, orc, monkeypatch, knobs):
     """CSR step variants equal the round-1 register-path kernel (SBG_CSR_LEAN=-1) bitwise,
     per-replica A included: replica slabs stepped from L2 (SBG_CSR_SLAB; ragged last slab,
     300 = 128+128+44), the cp.async-staged gather kernel (SBG_CSR_ASYNC = gathers in flight per
     warp), the pipelined gather (SBG_CSR_PF) and the lean kernel (SBG_CSR_LEAN = gathers per
-    round; 0 = the default); rows of degree 0 and > 32."""
+    round; 0 = the default; SBG_CSR_PFS = x, y, p prefetched into shared memory by cp.async);
+    rows of degree 0 and > 32."""
     n, m, R, steps = 3000, 15000, 300, 24
     (ei, ej, w), (rowptr, col, val) = orc.gen_er_csr(n, m, 5)
     # one isolated spin and one hub of degree 40: the zero-degree and multi-chunk rows
@@ -248,7 +251,7 @@ def test_csr_kernel_variants_bitwise(solver, orc, monkeypatch, knobs):
         cfg = cfg_for(variant, 100, 1.25, 0.158, 0.2)
         out = []
         for env in ({"SBG_CSR_LEAN": "-1"}, {"SBG_CSR_LEAN": "-1", **knobs}):
-            for key in ("SBG_CSR_SLAB", "SBG_CSR_ASYNC", "SBG_CSR_PF", "SBG_CSR_LEAN"):
+            for key in ("SBG_CSR_SLAB", "SBG_CSR_ASYNC", "SBG_CSR_PF", "SBG_CSR_LEAN", "SBG_CSR_PFS"):
                 monkeypatch.setenv(key, env.get(key, "0"))
             solver.set_instance_csr(n, rowptr, col, val)
             solver.set_state(x0, y0, p0)
