@@ -550,6 +550,7 @@ int launch_resident(sbg_ctx* ctx, const Maps& maps, const MultiStepArgs& ms, int
     if (!trace) CK(cudaMalloc(&trace, sizeof(unsigned long long) * 16 * 4 * 4096));
     CK(cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 16 * 4 * 4096, ctx->stream));
     a.trace = trace;
+    a.trace_group = hook_knob("SBG_RES_TRACE") - 1;  // 1 = the launch's first group, 2 = the second, ...
     a.nsteps = std::min(a.nsteps, 4096);
   }
   static unsigned long long* gtrace = nullptr;  // dev knob SBG_RES_GTRACE: per-(CTA, group) stamps

@@ -132,6 +132,7 @@ struct ResidentArgs {
   unsigned long long* gtrace; // dev only: per-(CTA, group) stamps of the parts kernel [cta][64][8]
   const uint8_t* j4;          // TS kernel: packed e2m1 J [npad][npad / 2] (rows loaded into TMEM)
   int64_t j4_pitch;           // its row pitch in bytes
+  int32_t trace_group;        // dev only: the launch-relative group SBG_RES_TRACE stamps (SBG_RES_TRACE - 1)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {

@@ -152,7 +152,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TsCfg<STAGES_, PARTS
     // parts 0, 1 in the parts kernel's layout; SBG_TS_TRACE4 builds also stamp parts 2, 3 into a
     // second region of the same shape (compile-time: stamps in all four parts' loops change the
     // register allocation of this kernel and cost 4 % even with the trace off)
-    if (SBG_HOOK_PTR(args.trace) && g == args.group0 && s >= 0 && i < (SBG_TS_TRACE4 ? 4 : 2) && cr == 0 && (blockIdx.x >> 1) == 0)
+    if (SBG_HOOK_PTR(args.trace) && g == args.group0 + args.trace_group && s >= 0 && i < (SBG_TS_TRACE4 ? 4 : 2) && cr == 0 &&
+        (blockIdx.x >> 1) == 0)
       SBG_HOOK_PTR(args.trace)[((i >> 1) * 2 * 4096 + s * 2 + (i & 1)) * 16 + k] = gtimer();
   };
   auto gstamp = [&](int g, int k) {
