@@ -634,7 +634,7 @@ def test_non_e2m1_couplings_stay_int8(solver, monkeypatch):
     assert solver.operand_format == "e2m1"
 
 
-@pytest.mark.parametrize("n,R", [(2000, 8192), (500, 2500)])
+@pytest.mark.parametrize("n,R", [(2000, 8192), (500, 2500), (2000, 2304)])  # 2304: two groups of the TS kernel by the tie rule
 def test_run_pipelined_copies_equal_serial(solver, orc, n, R, monkeypatch):
     """sbg_run on the resident kernel overlaps each replica group's host->device copy with
     the earlier groups' steps (stream-ordered ready flags): results bitwise equal to the
